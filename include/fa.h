@@ -1,0 +1,144 @@
+/*
+ * fa.h -- C ABI of libfa: B200-native parallel non-divergent (D8) flow
+ * accumulation, after Barnes, "Parallel Non-divergent Flow Accumulation for
+ * Trillion Cell Digital Elevation Models" (arXiv 1608.04431).
+ *
+ * Citations: "P:Lnn" is /root/reference/PAPER.md line nn; "Dn" is reading n
+ * in DESIGN.md ("Readings of the paper").
+ *
+ * Conventions (all entry points)
+ *  - Rasters are row-major, contiguous (pitch == cols).  Pointers may be
+ *    CUDA device pointers on the context's device, or host pointers (pinned
+ *    or pageable); the library detects which (cudaPointerGetAttributes) and
+ *    stages host buffers through device memory inside the call.  The caller
+ *    owns every buffer it passes; the library never frees them.
+ *  - Every call enqueues on the context's stream and returns only after the
+ *    work completed, so data-dependent errors (cycle, bad code, overflow)
+ *    are reported.  Outputs are undefined unless FA_OK is returned.
+ *  - No call aborts, throws or prints.  fa_last_error() gives a message.
+ *  - Scratch memory is owned by the context: allocated lazily, grown on
+ *    demand, freed by fa_destroy().  A context is bound to one device and is
+ *    not thread-safe.
+ *  - Direction codes (D1): 0 NoFlow, 1 N(0,-1), 2 NE(+1,-1), 3 E(+1,0),
+ *    4 SE(+1,+1), 5 S(0,+1), 6 SW(-1,+1), 7 W(-1,0), 8 NW(-1,-1) as (dx,dy)
+ *    with y = row index growing downward; 255 NoData.
+ *  - NoData elevation: z == nodata or z non-finite.  NoData output marker:
+ *    0xFFFFFFFF (u32), all-ones (u64), quiet NaN (f64) (D9).
+ */
+#ifndef FA_H
+#define FA_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FA_API __attribute__((visibility("default")))
+#else
+#define FA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fa_ctx fa_ctx;
+
+typedef enum {
+  FA_OK = 0,
+  FA_E_ARG = 1,      /* NULL/negative sizes, dem and dirs both or neither, bad wtype/atype, bad weight (D21) */
+  FA_E_DIRCODE = 2,  /* a direction byte not in {0..8, 255} (D1) */
+  FA_E_CYCLE = 3,    /* some data cell never retires: the direction graph has a cycle */
+  FA_E_OVERFLOW = 4, /* integer accumulation could exceed the output type (D10) */
+  FA_E_NOMEM = 5,
+  FA_E_CUDA = 6,
+  FA_E_NCCL = 7,
+  FA_E_STATE = 8     /* wrong device, ranks disagree, communicator missing */
+} fa_status;
+
+typedef enum { FA_W_NONE = 0, FA_W_U32 = 1, FA_W_F32 = 2 } fa_wtype; /* NONE => w = 1 */
+typedef enum { FA_A_U32 = 0, FA_A_U64 = 1, FA_A_F64 = 2 } fa_atype;
+/* valid (wtype, atype): (NONE|U32, U32|U64), (F32, F64), (NONE, F64) */
+
+/* Create a context on `device`, enqueuing on `cuda_stream` (a cudaStream_t;
+ * NULL = the legacy default stream).  tile_rows x tile_cols is the paper's
+ * tile ("subdivided into rectangular tiles of equal dimension"); the
+ * last tile row/column is ragged (D20).  <= 0 means the whole raster is one
+ * tile.  The tiling never changes results; it sets the
+ * granularity of the perimeter records (fa_perimeter_records) and of the
+ * multi-GPU exchange. */
+FA_API fa_status fa_create(fa_ctx** out, int device, void* cuda_stream, int64_t tile_rows,
+                    int64_t tile_cols);
+FA_API fa_status fa_destroy(fa_ctx* ctx);
+FA_API const char* fa_last_error(const fa_ctx* ctx);
+
+/* H1: D8 flow directions of a DEM ("D8 ... a single one of its
+ * neighbours"; BASELINE north_star: steepest strictly-downhill neighbour,
+ * diagonal drop divided by sqrt2 (exact compare, D4), ties to the lowest
+ * code (D2), outlet fallback to the lowest off-grid/NoData code (D3),
+ * NoFlow (0) if none (D6), NoData -> 255).
+ *   dem  : rows x cols float32, in.       dirs : rows x cols uint8, out. */
+FA_API fa_status fa_flowdirs(fa_ctx* ctx, const float* dem, int64_t rows, int64_t cols, float nodata,
+                      uint8_t* dirs);
+
+/* H1-H6: flow accumulation A(p) = w(p) + sum_{n: target(n)=p} A(n)
+ * (Eq. 1, alpha in {0,1}).  Exactly one of `dem` (then D8 is
+ * computed, H1) or `dirs` is non-NULL.  `w` may be NULL (w = 1).  Flow into
+ * NoData or off the grid is dropped (D8); NoFlow cells keep inflow plus
+ * their own w (D7).  Integer results are exact; f64 results are within
+ * 1e-9 relative of the exact sum (D13).  f32 weights must be finite and
+ * >= 0 (D21); weights of NoData cells are ignored.
+ *   acc : rows x cols of u32 / u64 / f64 according to atype, out. */
+FA_API fa_status fa_accumulate(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem, float nodata,
+                        const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc,
+                        fa_atype atype);
+
+/* H4/H5 intermediates for tests and tools: number of tile perimeter slots
+ * for a rows x cols raster under the context's tiling (tiles row-major,
+ * slots per tile in clockwise perimeter order from the tile's top-left,
+ * P = 2h+2w-4, or h*w for a 1-wide tile). */
+FA_API int64_t fa_perimeter_slots(const fa_ctx* ctx, int64_t rows, int64_t cols);
+
+/* Run the tiled method and return, per tile perimeter slot ("(a) its
+ * flow direction F, (b) its flow accumulation A, and (c) its link L"):
+ *   links   (u32): Alg. 2 FollowPath: the perimeter index of
+ *                  the exit cell where the slot's in-tile path leaves the
+ *                  tile, 0xFFFFFFFE FlowExternal, 0xFFFFFFFF FlowTerminates;
+ *   tile_acc(atype): A_T, the tile-local accumulation (Alg. 1 on the tile);
+ *   offsets (atype): x, the external inbound flow the global solve returns
+ *                  to the slot (P:L220 A', read as a_in, D11).
+ * Any of the three may be NULL.  Same inputs as fa_accumulate; `acc` (may be
+ * NULL) receives the final accumulation. */
+FA_API fa_status fa_perimeter_records(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem,
+                               float nodata, const uint8_t* dirs, const void* w, fa_wtype wtype,
+                               fa_atype atype, uint32_t* links, void* tile_acc, void* offsets,
+                               void* acc);
+
+/* Multi-GPU (H7): rank 0 calls fa_nccl_unique_id and broadcasts the 128
+ * bytes (e.g. with torch.distributed); every rank then calls
+ * fa_accumulate_dist collectively with identical global_rows, cols, nranks,
+ * wtype, atype and tiling.  Rank r owns rows [row_begin, row_begin +
+ * local_rows) (strips contiguous, ordered by rank, each a multiple of the
+ * tile height except the last).  dem/dirs/w/acc are the rank's strip.
+ * Collectives: one halo row of z to/from each neighbour strip (DEM input),
+ * an all-gather of the strips' perimeter records, a status
+ * all-reduce.  The perimeter graph is then solved redundantly on every rank
+ * (no second exchange). */
+FA_API fa_status fa_nccl_unique_id(void* out128);
+FA_API fa_status fa_accumulate_dist(fa_ctx* ctx, const void* nccl_id128, int rank, int nranks,
+                             int64_t global_rows, int64_t cols, int64_t row_begin,
+                             int64_t local_rows, const float* dem, float nodata,
+                             const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc,
+                             fa_atype atype);
+
+/* Per-phase statistics of the last call (device-timed with CUDA events). */
+typedef struct {
+  double ms_total, ms_pass1, ms_graph, ms_pass2, ms_exchange;
+  int64_t cells, blocks, graph_nodes, tile_nodes;
+  int64_t peel_rounds, contract_levels, jump_rounds;
+  int64_t bytes_exchanged;
+} fa_stats;
+FA_API fa_status fa_get_stats(const fa_ctx* ctx, fa_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FA_H */

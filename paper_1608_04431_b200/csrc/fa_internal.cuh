@@ -1,0 +1,221 @@
+// fa_internal.cuh -- shared device/host definitions of libfa (the CUDA path).
+// Independent of oracle/: nothing here is shared with the CPU oracle.
+//
+// Citations: "P:Lnn" = /root/reference/PAPER.md line nn; "Dn" = DESIGN.md reading n.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+
+namespace fa {
+
+// ---------------------------------------------------------------- constants
+constexpr uint8_t kNoData = 255;  // D1
+constexpr uint8_t kNoFlow = 0;
+constexpr uint32_t kNone = 0xFFFFFFFFu;            // no node / no parent
+constexpr uint32_t kFlowExternal = 0xFFFFFFFEu;    // Alg. 2 sentinel
+constexpr uint32_t kFlowTerminates = 0xFFFFFFFFu;  // Alg. 2 sentinel
+
+// Block = the CTA-resident sub-tile: the paper's Alg. 1 + Alg. 2
+// run on it entirely in shared memory.
+constexpr int BR = 64;                 // block rows
+constexpr int BC = 64;                 // block cols
+constexpr int BN = BR * BC;            // cells per block
+constexpr int PB = 2 * (BR + BC) - 4;  // perimeter slots per block (252)
+constexpr int kThreads = 512;          // threads per block kernel
+
+// status bits (device flag word)
+constexpr uint32_t ST_BADCODE = 1u;
+constexpr uint32_t ST_BADWEIGHT = 2u;
+constexpr uint32_t ST_CYCLE = 4u;
+
+// node flags (per block-exit node)
+constexpr uint8_t NF_OUT_TILE = 1;  // target outside the node's tile (FlowExternal at tile level, D22)
+constexpr uint8_t NF_DEAD = 2;      // target off-grid or NoData: flow dropped (D8)
+
+// direction code k -> (dx, dy), S:L33 / D1.  Index 0 unused.
+__host__ __device__ constexpr int dir_dx(int k) {
+  return (k == 2 || k == 3 || k == 4) ? 1 : (k == 6 || k == 7 || k == 8) ? -1 : 0;
+}
+__host__ __device__ constexpr int dir_dy(int k) {
+  return (k == 1 || k == 2 || k == 8) ? -1 : (k == 4 || k == 5 || k == 6) ? 1 : 0;
+}
+// code pointing back: opp(k) = ((k + 3) & 7) + 1
+__host__ __device__ constexpr int dir_opp(int k) { return ((k + 3) & 7) + 1; }
+
+// ---------------------------------------------------------------- geometry
+// Raster H x W, cut into tiles TH x TW (ragged last row/col, D20), each tile
+// cut into blocks BR x BC (ragged at the tile's far edges).  Global block grid
+// NBR x NBC = (TR * nbt_r) x (TC * nbt_c); blocks past a ragged tile edge are
+// empty (h or w <= 0) and skipped.
+struct Geom {
+  int64_t H, W;      // raster (or strip) size
+  int64_t TH, TW;    // tile size
+  int64_t TR, TC;    // tiles
+  int64_t nbt_r, nbt_c;  // blocks per tile (rows / cols)
+  int64_t NBR, NBC;  // global block grid
+  int64_t nblocks;
+  int64_t row0;      // global row of this raster's first row (strips)
+  int64_t GH;        // global raster rows (== H single GPU)
+
+  __host__ __device__ int64_t tile_of_block(int64_t b) const {
+    int64_t gr = b / NBC, gc = b % NBC;
+    return (gr / nbt_r) * TC + gc / nbt_c;
+  }
+  // block extent
+  __host__ __device__ void block_box(int64_t b, int64_t& y0, int64_t& x0, int& h, int& w) const {
+    int64_t gr = b / NBC, gc = b % NBC;
+    int64_t ty = gr / nbt_r, tx = gc / nbt_c;
+    y0 = ty * TH + (gr % nbt_r) * BR;
+    x0 = tx * TW + (gc % nbt_c) * BC;
+    int64_t ty1 = (ty + 1) * TH < H ? (ty + 1) * TH : H;
+    int64_t tx1 = (tx + 1) * TW < W ? (tx + 1) * TW : W;
+    int64_t hh = ty1 - y0, ww = tx1 - x0;
+    h = hh <= 0 ? 0 : (hh > BR ? BR : (int)hh);
+    w = ww <= 0 ? 0 : (ww > BC ? BC : (int)ww);
+  }
+  __host__ __device__ int64_t block_of(int64_t y, int64_t x, int& ly, int& lx) const {
+    int64_t ty = y / TH, tx = x / TW;
+    int64_t ry = y - ty * TH, rx = x - tx * TW;
+    int64_t gr = ty * nbt_r + ry / BR, gc = tx * nbt_c + rx / BC;
+    ly = (int)(ry % BR);
+    lx = (int)(rx % BC);
+    return gr * NBC + gc;
+  }
+  __host__ __device__ void tile_box(int64_t t, int64_t& y0, int64_t& x0, int64_t& h,
+                                    int64_t& w) const {
+    int64_t ty = t / TC, tx = t % TC;
+    y0 = ty * TH;
+    x0 = tx * TW;
+    h = (y0 + TH <= H) ? TH : H - y0;
+    w = (x0 + TW <= W) ? TW : W - x0;
+  }
+};
+
+Geom make_geom(int64_t H, int64_t W, int64_t th, int64_t tw);
+
+// ---------------------------------------------------------------- perimeter order
+// Clockwise from the top-left: top row L->R, right column, bottom row R->L,
+// left column bottom->top; 1-wide boxes are row-major (S:L60-67 convention).
+__host__ __device__ inline int64_t perim_count(int64_t h, int64_t w) {
+  if (h <= 0 || w <= 0) return 0;
+  if (h == 1 || w == 1) return h * w;
+  return 2 * (h + w) - 4;
+}
+__host__ __device__ inline void perim_xy(int64_t p, int64_t h, int64_t w, int64_t& x, int64_t& y) {
+  if (h == 1 || w == 1) {
+    y = p / w;
+    x = p % w;
+    return;
+  }
+  if (p < w) { x = p; y = 0; return; }
+  p -= w;
+  if (p < h - 1) { x = w - 1; y = p + 1; return; }
+  p -= h - 1;
+  if (p < w - 1) { x = w - 2 - p; y = h - 1; return; }
+  p -= w - 1;
+  x = 0;
+  y = h - 2 - p;
+}
+__host__ __device__ inline int64_t perim_index(int64_t x, int64_t y, int64_t h, int64_t w) {
+  if (h == 1 || w == 1) return y * w + x;
+  if (y == 0) return x;
+  if (x == w - 1) return w + y - 1;
+  if (y == h - 1) return w + (h - 1) + (w - 2 - x);
+  if (x == 0) return w + (h - 1) + (w - 1) + (h - 2 - y);
+  return -1;
+}
+
+// ---------------------------------------------------------------- D8 (H1)
+// Steepest strictly-downhill data neighbour; drops fl32(zc - zn) (D5);
+// cardinal vs diagonal by the exact compare 2a^2 > b^2 in fp64 (D4);
+// ties to the lowest code (D2); no downhill data neighbour -> lowest
+// off-grid/NoData code (outlet, D3), else NoFlow (D6).  `zs` holds staged
+// elevations where NoData and off-grid are NaN.
+template <int STRIDE>
+__device__ __forceinline__ uint8_t d8_code(const float* zs, int i) {
+  const float zc = zs[i];
+  if (isnan(zc)) return kNoData;
+  int first_out = 0, kc = 0, kd = 0;
+  float a = 0.0f, b = 0.0f;
+#pragma unroll
+  for (int k = 1; k <= 8; ++k) {
+    const float zn = zs[i + dir_dy(k) * STRIDE + dir_dx(k)];
+    if (isnan(zn)) {
+      if (!first_out) first_out = k;
+      continue;
+    }
+    const float d = __fsub_rn(zc, zn);
+    if (!(d > 0.0f)) continue;
+    if (k & 1) {
+      if (kc == 0 || d > a) { a = d; kc = k; }
+    } else {
+      if (kd == 0 || d > b) { b = d; kd = k; }
+    }
+  }
+  if (kc && kd) {
+    const double da = (double)a, db = (double)b;
+    return (uint8_t)(__dmul_rn(__dmul_rn(2.0, da), da) > __dmul_rn(db, db) ? kc : kd);
+  }
+  if (kc) return (uint8_t)kc;
+  if (kd) return (uint8_t)kd;
+  return (uint8_t)(first_out ? first_out : kNoFlow);
+}
+
+__device__ __forceinline__ float stage_z(float v, float nodata) {
+  return (isfinite(v) && v != nodata) ? v : __int_as_float(0x7fc00000);
+}
+
+// ---------------------------------------------------------------- accumulator traits
+template <class T> struct AccT;
+template <> struct AccT<uint32_t> {
+  __host__ __device__ static uint32_t marker() { return 0xFFFFFFFFu; }
+};
+template <> struct AccT<unsigned long long> {
+  __host__ __device__ static unsigned long long marker() { return ~0ull; }
+};
+template <> struct AccT<double> {
+  __device__ static double marker() { return __longlong_as_double(0x7ff8000000000000ll); }
+};
+
+__device__ __forceinline__ void atomic_add(uint32_t* p, uint32_t v) { atomicAdd(p, v); }
+__device__ __forceinline__ void atomic_add(unsigned long long* p, unsigned long long v) { atomicAdd(p, v); }
+__device__ __forceinline__ void atomic_add(double* p, double v) { atomicAdd(p, v); }
+
+// arguments of the block kernels (pass 1 / pass 2, block.cu)
+template <class T, int WK>
+struct PassArgs {
+  Geom g;
+  const float* dem;       // pass 1 from DEM
+  float nodata;
+  const uint8_t* dirs_in; // pass 1 from dirs, and pass 2
+  uint8_t* dirs_out;      // pass 1 from DEM: D8 output (may be null)
+  const void* w;          // weights (WK: 0 none, 1 u32, 2 f32)
+  // pass 1 outputs
+  uint32_t* node_count;
+  T* node_val;
+  uint32_t* node_slot;
+  uint32_t* node_tgt;
+  uint8_t* node_flags;
+  uint32_t* slot_root;
+  unsigned long long* wsum;
+  // pass 2 inputs / outputs
+  const T* x_slot;
+  T* acc;
+  uint32_t* status;
+};
+
+// warp-aggregated append of `v` (if pred) to list[*count]
+__device__ __forceinline__ void warp_append(bool pred, uint32_t v, uint32_t* list, uint32_t* count) {
+  const unsigned mask = __ballot_sync(0xFFFFFFFFu, pred);
+  if (!mask) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(mask) - 1;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(mask));
+  base = __shfl_sync(0xFFFFFFFFu, base, leader);
+  if (pred) list[base + __popc(mask & ((1u << lane) - 1))] = v;
+}
+
+}  // namespace fa

@@ -1,0 +1,350 @@
+// forest.cu -- accumulation on an explicit forest (the perimeter / block-exit
+// graphs), S(v) = val(v) + sum_{children c} S(c).
+//
+// The paper solves its global flow graph "using the same strategy described
+// in Algorithm 1": dependency counts and a queue of ready nodes.  A
+// level-synchronous version of that (one kernel per round, warp-aggregated
+// atomics) is efficient while the ready frontier is wide.  Deep graphs
+// (rivers crossing hundreds of blocks, the serpentine of config 2) make the
+// frontier "long and thin", so once it falls below remaining/8 the residual
+// forest is contracted instead:
+//   * every residual node with exactly one pending child is a chain node; a
+//     node with 0 or >= 2 pending children starts a segment;
+//   * pointer jumping along the unique-pending-child links gives every node
+//     its segment start st(v) and the prefix pre(v) of values from st(v)
+//     (exclusive) down to v (inclusive): S(v) = S(st(v)) + pre(v);
+//   * the segment starts form a smaller forest (every internal node has >= 2
+//     children), solved recursively; then S is expanded back.
+// This is rake (peel) + compress (chain jumping) tree contraction, O(log)
+// phases; each phase is a handful of grid-stride kernels.
+#include "forest.cuh"
+
+namespace fa {
+
+namespace {
+
+__global__ void k_count_children(uint32_t n, const uint32_t* __restrict__ parent, uint32_t* cnt) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t p = parent[v];
+    if (p != kNone) atomicAdd(&cnt[p], 1u);
+  }
+}
+
+// frontier = {v : cnt[v] == 0}; done[v] = 0.  All lanes iterate uniformly.
+__global__ void k_init_frontier(uint32_t n, const uint32_t* __restrict__ cnt, uint8_t* done,
+                                uint32_t* front, uint32_t* fcount) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
+    const uint32_t v = base + threadIdx.x;
+    const bool ok = v < n && cnt[v] == 0;
+    if (v < n) done[v] = 0;
+    warp_append(ok, v, front, fcount);
+  }
+}
+
+template <class T>
+__global__ void k_peel(const uint32_t* __restrict__ front, uint32_t nf,
+                       const uint32_t* __restrict__ parent, T* val, uint32_t* cnt, uint8_t* done,
+                       uint32_t* next, uint32_t* ncount) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < nf; base += stride) {
+    const uint32_t i = base + threadIdx.x;
+    bool push = false;
+    uint32_t p = kNone;
+    if (i < nf) {
+      const uint32_t v = front[i];
+      done[v] = 1;
+      p = parent[v];
+      if (p != kNone) {
+        atomic_add(&val[p], val[v]);
+        push = atomicSub(&cnt[p], 1u) == 1u;
+      }
+    }
+    warp_append(push, p, next, ncount);
+  }
+}
+
+__global__ void k_compact_residual(uint32_t n, const uint8_t* __restrict__ done, uint32_t* R,
+                                   uint32_t* mcount, uint32_t* rid) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
+    const uint32_t v = base + threadIdx.x;
+    const bool keep = v < n && !done[v];
+    // rid assigned after the append: recompute position via a second pass is
+    // avoided by writing rid inside warp_append's ordering below
+    const unsigned mask = __ballot_sync(0xFFFFFFFFu, keep);
+    if (!mask) continue;
+    const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+    uint32_t b0 = 0;
+    if (lane == leader) b0 = atomicAdd(mcount, (uint32_t)__popc(mask));
+    b0 = __shfl_sync(0xFFFFFFFFu, b0, leader);
+    if (keep) {
+      const uint32_t r = b0 + __popc(mask & ((1u << lane) - 1));
+      R[r] = v;
+      rid[v] = r;
+    }
+  }
+}
+
+template <class T>
+__global__ void k_build_local(uint32_t m, const uint32_t* __restrict__ R,
+                              const uint32_t* __restrict__ parent, const T* __restrict__ val,
+                              const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ rid,
+                              uint32_t* lpar, T* lval, uint32_t* lpc, uint32_t* up) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
+    const uint32_t v = R[r];
+    const uint32_t p = parent[v];
+    lpar[r] = p == kNone ? kNone : rid[p];
+    lval[r] = val[v];
+    lpc[r] = cnt[v];
+    up[r] = kNone;
+  }
+}
+
+__global__ void k_set_up(uint32_t m, const uint32_t* __restrict__ lpar, const uint32_t* __restrict__ lpc,
+                         uint32_t* up) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
+    const uint32_t q = lpar[r];
+    if (q != kNone && lpc[q] == 1u) up[q] = r;
+  }
+}
+
+template <class T>
+__global__ void k_jump_init(uint32_t m, const uint32_t* __restrict__ lpc, const uint32_t* __restrict__ up,
+                            const T* __restrict__ lval, uint32_t* nxt, T* acc) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
+    const bool start = lpc[r] != 1u;
+    nxt[r] = start ? r : up[r];
+    acc[r] = start ? (T)0 : lval[r];
+  }
+}
+
+template <class T>
+__global__ void k_jump(uint32_t m, const uint32_t* __restrict__ lpc, const uint32_t* __restrict__ nxt_in,
+                       const T* __restrict__ acc_in, uint32_t* nxt_out, T* acc_out, uint32_t* changed) {
+  bool ch = false;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
+    const uint32_t n1 = nxt_in[r];
+    if (lpc[n1] != 1u) {  // reached a segment start
+      nxt_out[r] = n1;
+      acc_out[r] = acc_in[r];
+    } else {
+      nxt_out[r] = nxt_in[n1];
+      acc_out[r] = acc_in[r] + acc_in[n1];
+      ch = true;
+    }
+  }
+  if (__syncthreads_or(ch) && threadIdx.x == 0) atomicOr(changed, 1u);
+}
+
+// starts -> dense segment ids; sval = own value, spar = kNone
+template <class T>
+__global__ void k_seg_ids(uint32_t m, const uint32_t* __restrict__ lpc, const T* __restrict__ lval,
+                          uint32_t* sid, uint32_t* scount, T* sval, uint32_t* spar) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < m; base += stride) {
+    const uint32_t r = base + threadIdx.x;
+    const bool start = r < m && lpc[r] != 1u;
+    const unsigned mask = __ballot_sync(0xFFFFFFFFu, start);
+    if (!mask) continue;
+    const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+    uint32_t b0 = 0;
+    if (lane == leader) b0 = atomicAdd(scount, (uint32_t)__popc(mask));
+    b0 = __shfl_sync(0xFFFFFFFFu, b0, leader);
+    if (start) {
+      const uint32_t s = b0 + __popc(mask & ((1u << lane) - 1));
+      sid[r] = s;
+      sval[s] = lval[r];
+      spar[s] = kNone;
+    }
+  }
+}
+
+// every segment end r (parent is a junction or none) links its segment start
+// to the junction and hands the junction its chain prefix pre(r)
+template <class T>
+__global__ void k_seg_build(uint32_t m, const uint32_t* __restrict__ lpar, const uint32_t* __restrict__ lpc,
+                            const uint32_t* __restrict__ nxt, const T* __restrict__ acc,
+                            const uint32_t* __restrict__ sid, uint32_t* spar, T* sval) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
+    const uint32_t q = lpar[r];
+    if (q != kNone && lpc[q] == 1u) continue;  // not an end
+    const uint32_t s = sid[nxt[r]];
+    if (q == kNone) {
+      spar[s] = kNone;
+    } else {
+      spar[s] = sid[q];
+      atomic_add(&sval[sid[q]], acc[r]);
+    }
+  }
+}
+
+template <class T>
+__global__ void k_expand(uint32_t m, const uint32_t* __restrict__ R, const uint32_t* __restrict__ nxt,
+                         const T* __restrict__ acc, const uint32_t* __restrict__ sid,
+                         const T* __restrict__ sval, T* val) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x)
+    val[R[r]] = sval[sid[nxt[r]]] + acc[r];
+}
+
+__global__ void k_set_flag(uint32_t* st, uint32_t f) { atomicOr(st, f); }
+
+constexpr int kMaxLevels = 64;
+constexpr int kMaxJump = 40;
+
+template <class T>
+cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, int level) {
+  if (n == 0) return cudaSuccess;
+  if (level > kMaxLevels) {
+    k_set_flag<<<1, 1, 0, rt.st>>>(rt.d_status, ST_CYCLE);
+    return cudaGetLastError();
+  }
+  cudaStream_t st = rt.st;
+  uint32_t* cnt = rt.alloc<uint32_t>(n);
+  uint8_t* done = rt.alloc<uint8_t>(n);
+  uint32_t* fa_ = rt.alloc<uint32_t>(n);
+  uint32_t* fb = rt.alloc<uint32_t>(n);
+  uint32_t* ctr = rt.alloc<uint32_t>(4);
+  if (rt.err) return rt.err;
+  cudaMemsetAsync(cnt, 0, n * sizeof(uint32_t), st);
+  cudaMemsetAsync(ctr, 0, 4 * sizeof(uint32_t), st);
+  k_count_children<<<grid_for(n), 256, 0, st>>>(n, parent, cnt);
+  k_init_frontier<<<grid_for(n), 256, 0, st>>>(n, cnt, done, fa_, ctr);
+  rt.read(ctr, 1);
+  uint32_t nf = rt.h_cnt[0];
+  uint64_t remaining = n;
+  bool contracted = false;
+  while (nf > 0 && !rt.err) {
+    if ((uint64_t)nf * 8 < remaining) {
+      // ---------------- contract the residual forest
+      contracted = true;
+      ++rt.contract_levels;
+      uint32_t* R = rt.alloc<uint32_t>(remaining);
+      uint32_t* rid = rt.alloc<uint32_t>(n);
+      cudaMemsetAsync(ctr + 1, 0, sizeof(uint32_t), st);
+      k_compact_residual<<<grid_for(n), 256, 0, st>>>(n, done, R, ctr + 1, rid);
+      const uint32_t m = (uint32_t)remaining;
+      uint32_t* lpar = rt.alloc<uint32_t>(m);
+      uint32_t* lpc = rt.alloc<uint32_t>(m);
+      uint32_t* up = rt.alloc<uint32_t>(m);
+      uint32_t* nxa = rt.alloc<uint32_t>(m);
+      uint32_t* nxb = rt.alloc<uint32_t>(m);
+      uint32_t* sid = rt.alloc<uint32_t>(m);
+      T* lval = rt.alloc<T>(m);
+      T* aca = rt.alloc<T>(m);
+      T* acb = rt.alloc<T>(m);
+      if (rt.err) return rt.err;
+      k_build_local<T><<<grid_for(m), 256, 0, st>>>(m, R, parent, val, cnt, rid, lpar, lval, lpc, up);
+      k_set_up<<<grid_for(m), 256, 0, st>>>(m, lpar, lpc, up);
+      k_jump_init<T><<<grid_for(m), 256, 0, st>>>(m, lpc, up, lval, nxa, aca);
+      int rounds = 0;
+      for (;;) {
+        cudaMemsetAsync(ctr + 2, 0, sizeof(uint32_t), st);
+        k_jump<T><<<grid_for(m), 256, 0, st>>>(m, lpc, nxa, aca, nxb, acb, ctr + 2);
+        std::swap(nxa, nxb);
+        std::swap(aca, acb);
+        ++rounds;
+        ++rt.jump_rounds;
+        rt.read(ctr + 2, 1);
+        if (!rt.h_cnt[0] || rt.err) break;
+        if (rounds > kMaxJump) {
+          k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);
+          break;
+        }
+      }
+      // segment forest over the starts
+      cudaMemsetAsync(ctr + 3, 0, sizeof(uint32_t), st);
+      T* sval = rt.alloc<T>(m);
+      uint32_t* spar = rt.alloc<uint32_t>(m);
+      if (rt.err) return rt.err;
+      k_seg_ids<T><<<grid_for(m), 256, 0, st>>>(m, lpc, lval, sid, ctr + 3, sval, spar);
+      k_seg_build<T><<<grid_for(m), 256, 0, st>>>(m, lpar, lpc, nxa, aca, sid, spar, sval);
+      rt.read(ctr + 3, 1);
+      const uint32_t ms = rt.h_cnt[0];
+      if (rounds <= kMaxJump && ms < m) {
+        solve_level<T>(rt, ms, spar, sval, level + 1);
+      } else if (ms >= m) {
+        // no chain node: cannot happen with a thin frontier unless cyclic
+        k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);
+      }
+      k_expand<T><<<grid_for(m), 256, 0, st>>>(m, R, nxa, aca, sid, sval, val);
+      for (void* p : {(void*)R, (void*)rid, (void*)lpar, (void*)lpc, (void*)up, (void*)nxa,
+                      (void*)nxb, (void*)sid, (void*)lval, (void*)aca, (void*)acb, (void*)sval,
+                      (void*)spar})
+        rt.free(p);
+      remaining = 0;
+      break;
+    }
+    // ---------------- one peel round (Alg. 1 queue loop, level-synchronous)
+    cudaMemsetAsync(ctr + 1, 0, sizeof(uint32_t), st);
+    k_peel<T><<<grid_for(nf), 256, 0, st>>>(fa_, nf, parent, val, cnt, done, fb, ctr + 1);
+    ++rt.peel_rounds;
+    remaining -= nf;
+    std::swap(fa_, fb);
+    rt.read(ctr + 1, 1);
+    nf = rt.h_cnt[0];
+  }
+  if (!contracted && remaining != 0) k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);
+  rt.free(cnt);
+  rt.free(done);
+  rt.free(fa_);
+  rt.free(fb);
+  rt.free(ctr);
+  return rt.err ? rt.err : cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- roots
+__global__ void k_root_init(uint32_t n, const uint32_t* __restrict__ parent, uint32_t* r) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    r[v] = parent[v] == kNone ? v : parent[v];
+}
+__global__ void k_root_jump(uint32_t n, const uint32_t* __restrict__ in, uint32_t* out, uint32_t* changed) {
+  bool ch = false;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t a = in[v], b = in[a];
+    out[v] = b;
+    ch |= a != b;
+  }
+  if (__syncthreads_or(ch) && threadIdx.x == 0) atomicOr(changed, 1u);
+}
+
+}  // namespace
+
+template <class T>
+cudaError_t forest_solve(Runtime& rt, uint32_t n, const uint32_t* parent, T* val) {
+  return solve_level<T>(rt, n, parent, val, 0);
+}
+template cudaError_t forest_solve<uint32_t>(Runtime&, uint32_t, const uint32_t*, uint32_t*);
+template cudaError_t forest_solve<unsigned long long>(Runtime&, uint32_t, const uint32_t*,
+                                                      unsigned long long*);
+template cudaError_t forest_solve<double>(Runtime&, uint32_t, const uint32_t*, double*);
+
+cudaError_t forest_roots(Runtime& rt, uint32_t n, const uint32_t* parent, uint32_t* root) {
+  if (n == 0) return cudaSuccess;
+  cudaStream_t st = rt.st;
+  uint32_t* tmp = rt.alloc<uint32_t>(n);
+  uint32_t* ctr = rt.alloc<uint32_t>(1);
+  if (rt.err) return rt.err;
+  k_root_init<<<grid_for(n), 256, 0, st>>>(n, parent, root);
+  uint32_t* a = root;
+  uint32_t* b = tmp;
+  int rounds = 0;
+  for (;;) {
+    cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st);
+    k_root_jump<<<grid_for(n), 256, 0, st>>>(n, a, b, ctr);
+    std::swap(a, b);
+    ++rounds;
+    rt.read(ctr, 1);
+    if (!rt.h_cnt[0] || rt.err) break;
+    if (rounds > kMaxJump) {
+      k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);
+      break;
+    }
+  }
+  if (a != root) cudaMemcpyAsync(root, a, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
+  rt.free(tmp);
+  rt.free(ctr);
+  return rt.err ? rt.err : cudaGetLastError();
+}
+
+}  // namespace fa

@@ -1,0 +1,188 @@
+"""Thin ctypes binding over libfa.so (include/fa.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C ABI; torch is
+used for device memory, streams and process groups.  There is no CPU
+fallback: importing this module on a box without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfa.so")
+
+FA_OK, FA_E_ARG, FA_E_DIRCODE, FA_E_CYCLE, FA_E_OVERFLOW, FA_E_NOMEM, FA_E_CUDA, FA_E_NCCL, FA_E_STATE = range(9)
+STATUS_NAMES = {0: "FA_OK", 1: "FA_E_ARG", 2: "FA_E_DIRCODE", 3: "FA_E_CYCLE", 4: "FA_E_OVERFLOW",
+                5: "FA_E_NOMEM", 6: "FA_E_CUDA", 7: "FA_E_NCCL", 8: "FA_E_STATE"}
+W_NONE, W_U32, W_F32 = 0, 1, 2
+A_U32, A_U64, A_F64 = 0, 1, 2
+ATYPES = {"u32": A_U32, "u64": A_U64, "f64": A_F64}
+TORCH_ACC = {A_U32: torch.uint32, A_U64: torch.uint64, A_F64: torch.float64}
+FLOW_EXTERNAL = 0xFFFFFFFE
+FLOW_TERMINATES = 0xFFFFFFFF
+
+EXPORTS = ["fa_create", "fa_destroy", "fa_last_error", "fa_flowdirs", "fa_accumulate",
+           "fa_perimeter_slots", "fa_perimeter_records", "fa_nccl_unique_id", "fa_accumulate_dist",
+           "fa_get_stats"]
+
+
+class FaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("ms_total", ctypes.c_double), ("ms_pass1", ctypes.c_double), ("ms_graph", ctypes.c_double),
+                ("ms_pass2", ctypes.c_double), ("ms_exchange", ctypes.c_double),
+                ("cells", ctypes.c_int64), ("blocks", ctypes.c_int64), ("graph_nodes", ctypes.c_int64),
+                ("tile_nodes", ctypes.c_int64), ("peel_rounds", ctypes.c_int64),
+                ("contract_levels", ctypes.c_int64), ("jump_rounds", ctypes.c_int64),
+                ("bytes_exchanged", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libfa.so (must have been built: __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libfa.so not built at {LIB_PATH}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I, F = ctypes.c_void_p, ctypes.c_int64, ctypes.c_float
+    lib.fa_create.argtypes = [ctypes.POINTER(P), ctypes.c_int, P, I, I]
+    lib.fa_destroy.argtypes = [P]
+    lib.fa_last_error.argtypes = [P]
+    lib.fa_last_error.restype = ctypes.c_char_p
+    lib.fa_flowdirs.argtypes = [P, P, I, I, F, P]
+    lib.fa_accumulate.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int]
+    lib.fa_perimeter_slots.argtypes = [P, I, I]
+    lib.fa_perimeter_slots.restype = I
+    lib.fa_perimeter_records.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, ctypes.c_int, P, P, P, P]
+    lib.fa_nccl_unique_id.argtypes = [P]
+    lib.fa_accumulate_dist.argtypes = [P, P, ctypes.c_int, ctypes.c_int, I, I, I, I, P, F, P, P,
+                                       ctypes.c_int, P, ctypes.c_int]
+    lib.fa_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
+    for fn in EXPORTS:
+        if fn not in ("fa_last_error", "fa_perimeter_slots"):
+            getattr(lib, fn).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        assert t.is_contiguous(), "tensors must be contiguous"
+        return ctypes.c_void_p(t.data_ptr())
+    import numpy as np
+
+    if isinstance(t, np.ndarray):
+        assert t.flags["C_CONTIGUOUS"]
+        return t.ctypes.data_as(ctypes.c_void_p)
+    raise TypeError(type(t))
+
+
+def _wtype(w):
+    if w is None:
+        return W_NONE
+    dt = w.dtype
+    if dt in (torch.uint32, torch.int32) or str(dt) in ("uint32", "int32"):
+        return W_U32
+    if dt == torch.float32 or str(dt) == "float32":
+        return W_F32
+    raise TypeError(f"weights must be uint32 or float32, got {dt}")
+
+
+class Context:
+    """One fa_ctx: bound to a device and a CUDA stream, with a tile size."""
+
+    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None,
+                 tile: tuple[int, int] = (0, 0)):
+        self.lib = load()
+        self.device = device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        self.tile = tuple(tile)
+        h = ctypes.c_void_p()
+        st = self.lib.fa_create(ctypes.byref(h), device, ctypes.c_void_p(self.stream.cuda_stream),
+                                int(tile[0]), int(tile[1]))
+        if st != FA_OK:
+            raise FaError(st, "fa_create failed")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.fa_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _check(self, st):
+        if st != FA_OK:
+            raise FaError(st, self.lib.fa_last_error(self.h).decode())
+
+    def stats(self) -> dict:
+        s = Stats()
+        self._check(self.lib.fa_get_stats(self.h, ctypes.byref(s)))
+        return s.as_dict()
+
+    # ---------------------------------------------------------------- H1
+    def flowdirs(self, dem, nodata: float = -9999.0, out=None):
+        rows, cols = dem.shape
+        if out is None:
+            out = torch.empty((rows, cols), dtype=torch.uint8, device=dem.device) if isinstance(
+                dem, torch.Tensor) else __import__("numpy").empty((rows, cols), "uint8")
+        self._check(self.lib.fa_flowdirs(self.h, _ptr(dem), rows, cols, float(nodata), _ptr(out)))
+        return out
+
+    # ---------------------------------------------------------------- H1-H6
+    def accumulate(self, dem=None, dirs=None, w=None, atype: str = "u32", nodata: float = -9999.0,
+                   out=None):
+        src = dem if dem is not None else dirs
+        rows, cols = src.shape
+        a = ATYPES[atype]
+        if out is None:
+            if isinstance(src, torch.Tensor):
+                out = torch.empty((rows, cols), dtype=TORCH_ACC[a], device=src.device)
+            else:
+                import numpy as np
+
+                out = np.empty((rows, cols), {A_U32: np.uint32, A_U64: np.uint64, A_F64: np.float64}[a])
+        self._check(self.lib.fa_accumulate(self.h, rows, cols, _ptr(dem), float(nodata), _ptr(dirs),
+                                           _ptr(w), _wtype(w), _ptr(out), a))
+        return out
+
+    def perimeter_slots(self, rows: int, cols: int) -> int:
+        return int(self.lib.fa_perimeter_slots(self.h, rows, cols))
+
+    def perimeter_records(self, dem=None, dirs=None, w=None, atype: str = "u32", nodata: float = -9999.0):
+        """(links u32, A_T, x, A) per tile perimeter slot (H4/H5), as device tensors."""
+        src = dem if dem is not None else dirs
+        rows, cols = src.shape
+        a = ATYPES[atype]
+        ns = self.perimeter_slots(rows, cols)
+        dev = src.device
+        links = torch.empty(ns, dtype=torch.uint32, device=dev)
+        at = torch.empty(ns, dtype=TORCH_ACC[a], device=dev)
+        xo = torch.empty(ns, dtype=TORCH_ACC[a], device=dev)
+        acc = torch.empty((rows, cols), dtype=TORCH_ACC[a], device=dev)
+        self._check(self.lib.fa_perimeter_records(self.h, rows, cols, _ptr(dem), float(nodata), _ptr(dirs),
+                                                  _ptr(w), _wtype(w), a, _ptr(links), _ptr(at), _ptr(xo),
+                                                  _ptr(acc)))
+        return links, at, xo, acc
