@@ -135,6 +135,7 @@ typedef struct {
   int64_t cells, blocks, graph_nodes, tile_nodes;
   int64_t peel_rounds, contract_levels, jump_rounds;
   int64_t bytes_exchanged;
+  int64_t launches; /* kernels launched by the call */
 } fa_stats;
 FA_API fa_status fa_get_stats(const fa_ctx* ctx, fa_stats* out);
 

@@ -153,7 +153,7 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
   Runtime& rt = ctx->rt;
   rt.st = st;
   rt.err = cudaSuccess;
-  rt.peel_rounds = rt.contract_levels = rt.jump_rounds = 0;
+  rt.peel_rounds = rt.contract_levels = rt.jump_rounds = rt.launches = 0;
   Geom g = make_geom(H, W, ctx->tile_r, ctx->tile_c);
   const int64_t slots = g.nblocks * PB;
   if (slots >= (int64_t)0xFFFFFFF0ll)
@@ -192,6 +192,7 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
   a.acc = acc;
   rt.d_status = ctx->d_small + 1;
   CK(launch_pass1<T, WK>(a, dem != nullptr, st));
+  ++rt.launches;
   CK(cudaEventRecord(ctx->ev[1], st));
   CK(rt.read(ctx->d_small, 4));
   const uint32_t nn = rt.h_cnt[0];
@@ -219,9 +220,11 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
   const bool multi = (g.TR * g.TC > 1) || rec.want;
   if (!multi) {
     CK(launch_g1_parent(st, nn, node_tgt, node_flags, slot_root, false, parent));
+    ++rt.launches;
     CK(cudaMemcpyAsync(S, node_val, nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
     CK(forest_solve<T>(rt, nn, parent, S));
     CK(launch_scatter_x<T>(st, nn, node_tgt, S, x_slot));
+    ++rt.launches;
   } else {
     uint32_t* troot = rt.alloc<uint32_t>(nn);
     uint32_t* parent2 = rt.alloc<uint32_t>(nn);
@@ -232,17 +235,21 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
     if (xT) CK(cudaMemsetAsync(xT, 0, slots * sizeof(T), st));
     // per-tile problem: G1 with tile-leaving edges cut -> A_T at block exits
     CK(launch_g1_parent(st, nn, node_tgt, node_flags, slot_root, true, parent));
+    ++rt.launches;
     CK(cudaMemcpyAsync(S1, node_val, nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
     CK(forest_solve<T>(rt, nn, parent, S1));
     CK(forest_roots(rt, nn, parent, troot));
     // global perimeter graph -> S2 = A at tile exits
     CK(launch_g2<T>(st, nn, node_tgt, node_flags, slot_root, troot, S1, parent2, S2));
+    ++rt.launches;
     CK(forest_solve<T>(rt, nn, parent2, S2));
     // offsets x_T injected at tile entries -> true A at every block exit
     CK(cudaMemcpyAsync(S, node_val, nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
     CK(launch_inject<T>(st, nn, node_tgt, node_flags, slot_root, S2, S, xT));
+    ++rt.launches;
     CK(forest_solve<T>(rt, nn, parent, S));
     CK(launch_scatter_x<T>(st, nn, node_tgt, S, x_slot));
+    ++rt.launches;
     if (rec.want) {
       const int64_t nt = g.TR * g.TC;
       int64_t* hb = new int64_t[nt + 1];
@@ -253,6 +260,7 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
       delete[] hb;
       CK(launch_tile_records<T>(st, g, ns, db, a.dirs_in, slot_root, troot, node_flags, node_slot,
                                 S1, xT, rec.links, (T*)rec.tile_acc, (T*)rec.offsets));
+      ++rt.launches;
       rt.free(db);
     }
     for (void* p : {(void*)troot, (void*)parent2, (void*)S1, (void*)S2, (void*)xT}) rt.free(p);
@@ -260,7 +268,7 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
   if (rt.err) return set_err(ctx, FA_E_CUDA, std::string("graph solve: ") + cudaGetErrorString(rt.err));
   CK(cudaEventRecord(ctx->ev[2], st));
   // ---------------- pass 2 (H6)
-  if (acc) CK(launch_pass2<T, WK>(a, st));
+  if (acc) { CK(launch_pass2<T, WK>(a, st)); ++rt.launches; }
   CK(cudaEventRecord(ctx->ev[3], st));
   for (void* p : {(void*)dirs_buf, (void*)slot_root, (void*)node_val, (void*)node_slot,
                   (void*)node_tgt, (void*)node_flags, (void*)x_slot, (void*)parent, (void*)S})
@@ -282,6 +290,7 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
   ctx->stats.peel_rounds = rt.peel_rounds;
   ctx->stats.contract_levels = rt.contract_levels;
   ctx->stats.jump_rounds = rt.jump_rounds;
+  ctx->stats.launches = rt.launches;
   return FA_OK;
 }
 

@@ -197,6 +197,7 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
   if (n == 0) return cudaSuccess;
   if (level > kMaxLevels) {
     k_set_flag<<<1, 1, 0, rt.st>>>(rt.d_status, ST_CYCLE);
+    ++rt.launches;
     return cudaGetLastError();
   }
   cudaStream_t st = rt.st;
@@ -209,7 +210,9 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
   cudaMemsetAsync(cnt, 0, n * sizeof(uint32_t), st);
   cudaMemsetAsync(ctr, 0, 4 * sizeof(uint32_t), st);
   k_count_children<<<grid_for(n), 256, 0, st>>>(n, parent, cnt);
+  ++rt.launches;
   k_init_frontier<<<grid_for(n), 256, 0, st>>>(n, cnt, done, fa_, ctr);
+  ++rt.launches;
   rt.read(ctr, 1);
   uint32_t nf = rt.h_cnt[0];
   uint64_t remaining = n;
@@ -223,6 +226,7 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
       uint32_t* rid = rt.alloc<uint32_t>(n);
       cudaMemsetAsync(ctr + 1, 0, sizeof(uint32_t), st);
       k_compact_residual<<<grid_for(n), 256, 0, st>>>(n, done, R, ctr + 1, rid);
+      ++rt.launches;
       const uint32_t m = (uint32_t)remaining;
       uint32_t* lpar = rt.alloc<uint32_t>(m);
       uint32_t* lpc = rt.alloc<uint32_t>(m);
@@ -235,12 +239,16 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
       T* acb = rt.alloc<T>(m);
       if (rt.err) return rt.err;
       k_build_local<T><<<grid_for(m), 256, 0, st>>>(m, R, parent, val, cnt, rid, lpar, lval, lpc, up);
+      ++rt.launches;
       k_set_up<<<grid_for(m), 256, 0, st>>>(m, lpar, lpc, up);
+      ++rt.launches;
       k_jump_init<T><<<grid_for(m), 256, 0, st>>>(m, lpc, up, lval, nxa, aca);
+      ++rt.launches;
       int rounds = 0;
       for (;;) {
         cudaMemsetAsync(ctr + 2, 0, sizeof(uint32_t), st);
         k_jump<T><<<grid_for(m), 256, 0, st>>>(m, lpc, nxa, aca, nxb, acb, ctr + 2);
+        ++rt.launches;
         std::swap(nxa, nxb);
         std::swap(aca, acb);
         ++rounds;
@@ -249,6 +257,7 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
         if (!rt.h_cnt[0] || rt.err) break;
         if (rounds > kMaxJump) {
           k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);
+          ++rt.launches;
           break;
         }
       }
@@ -258,7 +267,9 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
       uint32_t* spar = rt.alloc<uint32_t>(m);
       if (rt.err) return rt.err;
       k_seg_ids<T><<<grid_for(m), 256, 0, st>>>(m, lpc, lval, sid, ctr + 3, sval, spar);
+      ++rt.launches;
       k_seg_build<T><<<grid_for(m), 256, 0, st>>>(m, lpar, lpc, nxa, aca, sid, spar, sval);
+      ++rt.launches;
       rt.read(ctr + 3, 1);
       const uint32_t ms = rt.h_cnt[0];
       if (rounds <= kMaxJump && ms < m) {
@@ -266,8 +277,10 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
       } else if (ms >= m) {
         // no chain node: cannot happen with a thin frontier unless cyclic
         k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);
+        ++rt.launches;
       }
       k_expand<T><<<grid_for(m), 256, 0, st>>>(m, R, nxa, aca, sid, sval, val);
+      ++rt.launches;
       for (void* p : {(void*)R, (void*)rid, (void*)lpar, (void*)lpc, (void*)up, (void*)nxa,
                       (void*)nxb, (void*)sid, (void*)lval, (void*)aca, (void*)acb, (void*)sval,
                       (void*)spar})
@@ -278,6 +291,7 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
     // ---------------- one peel round (Alg. 1 queue loop, level-synchronous)
     cudaMemsetAsync(ctr + 1, 0, sizeof(uint32_t), st);
     k_peel<T><<<grid_for(nf), 256, 0, st>>>(fa_, nf, parent, val, cnt, done, fb, ctr + 1);
+    ++rt.launches;
     ++rt.peel_rounds;
     remaining -= nf;
     std::swap(fa_, fb);
@@ -326,18 +340,21 @@ cudaError_t forest_roots(Runtime& rt, uint32_t n, const uint32_t* parent, uint32
   uint32_t* ctr = rt.alloc<uint32_t>(1);
   if (rt.err) return rt.err;
   k_root_init<<<grid_for(n), 256, 0, st>>>(n, parent, root);
+  ++rt.launches;
   uint32_t* a = root;
   uint32_t* b = tmp;
   int rounds = 0;
   for (;;) {
     cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st);
     k_root_jump<<<grid_for(n), 256, 0, st>>>(n, a, b, ctr);
+    ++rt.launches;
     std::swap(a, b);
     ++rounds;
     rt.read(ctr, 1);
     if (!rt.h_cnt[0] || rt.err) break;
     if (rounds > kMaxJump) {
       k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);
+      ++rt.launches;
       break;
     }
   }

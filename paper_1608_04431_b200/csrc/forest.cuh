@@ -13,7 +13,7 @@ struct Runtime {
   uint32_t* h_cnt = nullptr;     // pinned host mirror [16]
   uint32_t* d_status = nullptr;  // status word (ST_*)
   // statistics
-  int64_t peel_rounds = 0, contract_levels = 0, jump_rounds = 0;
+  int64_t peel_rounds = 0, contract_levels = 0, jump_rounds = 0, launches = 0;
   cudaError_t err = cudaSuccess;
 
   template <class U>
