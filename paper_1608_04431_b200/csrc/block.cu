@@ -70,47 +70,68 @@ __device__ __forceinline__ T from_w(double wd, unsigned long long wu) {
 // In-block accumulation by chain following (shared by both passes).  On
 // entry: dirh, msk, pend and A (= w [+ x]) are set and synced.  Returns the
 // number of cells this thread retired.
+//
+// One flat loop per lane: when a lane's walk ends it immediately starts its
+// next source, so lanes of a warp never wait for each other between walks
+// (a per-source loop would make every warp pay the sum over its sources of
+// the longest walk among its 32 lanes).  Each step issues its three shared
+// loads (direction, donor mask, value of the next cell) together.
 template <class T>
 __device__ __forceinline__ uint32_t chain_follow(SmemCommon& s, T* A, int h, int w) {
   uint32_t retired = 0;
-  for (int i = threadIdx.x; i < BN; i += kThreads) {
-    const int ly0 = i / BC, lx0 = i % BC;
-    if (ly0 >= h || lx0 >= w) continue;
-    if (s.dirh[(ly0 + 1) * HS + lx0 + 1] == kNoData || s.msk[i] != 0) continue;
-    int ly = ly0, lx = lx0, c = i;
-    T a = A[c];
-    ++retired;
-    for (;;) {
-      const int d = s.dirh[(ly + 1) * HS + lx + 1];
-      if (d == kNoFlow || d > 8) break;
-      const int ty = ly + dir_dy(d), tx = lx + dir_dx(d);
-      if ((unsigned)ty >= (unsigned)h || (unsigned)tx >= (unsigned)w) break;  // leaves the block
-      if (s.dirh[(ty + 1) * HS + tx + 1] == kNoData) break;                   // dropped (D8)
-      const int t = ty * BC + tx;
-      const uint32_t m = s.msk[t];
-      if ((m & (m - 1)) == 0) {
-        // sole in-block donor: no other walk ever touches A[t]
-        a = A[t] + a;
-        A[t] = a;
-      } else {
-        const uint32_t bit = 1u << (dir_opp(d) - 1);
-        const int sh = (t & 3) * 8;
-        __threadfence_block();  // release our A[c]
-        const uint32_t old = atomicAnd(&s.pend[t >> 2], ~(bit << sh));
-        if (((old >> sh) & 0xFFu) != bit) break;  // other donors still pending
-        __threadfence_block();  // acquire the other donors' values
-        T acc = A[t];
-#pragma unroll
-        for (int k = 1; k <= 8; ++k)
-          if (m & (1u << (k - 1))) acc = acc + A[(ty + dir_dy(k)) * BC + tx + dir_dx(k)];
-        a = acc;
-        A[t] = a;
+  int next = threadIdx.x;  // next candidate source of this lane
+  int ly = 0, lx = 0, d = kNoFlow;
+  bool live = false;
+  T a = (T)0;
+  for (;;) {
+    if (!live) {
+      // fetch this lane's next source (data cell without in-block donors)
+      while (next < BN) {
+        const int i = next;
+        next += kThreads;
+        const int y = i / BC, x = i % BC;
+        if (y >= h || x >= w) continue;
+        const int dd = s.dirh[(y + 1) * HS + x + 1];
+        if (dd == kNoData || s.msk[i] != 0) continue;
+        ly = y;
+        lx = x;
+        d = dd;
+        a = A[i];
+        live = true;
+        ++retired;
+        break;
       }
-      ly = ty;
-      lx = tx;
-      c = t;
-      ++retired;
+      if (!live) break;
     }
+    // one step of the walk from (ly, lx) with direction d and value a
+    if (d == kNoFlow || d > 8) { live = false; continue; }
+    const int ty = ly + dir_dy(d), tx = lx + dir_dx(d);
+    if ((unsigned)ty >= (unsigned)h || (unsigned)tx >= (unsigned)w) { live = false; continue; }
+    const int t = ty * BC + tx;
+    const int dt = s.dirh[(ty + 1) * HS + tx + 1];
+    const uint32_t m = s.msk[t];
+    const T at = A[t];  // w(t) [+ x(t)]: only the walk that finishes t writes A[t]
+    if (dt == kNoData) { live = false; continue; }  // dropped into NoData (D8)
+    if ((m & (m - 1)) == 0) {
+      a = at + a;  // sole in-block donor: no atomic needed
+    } else {
+      const uint32_t bit = 1u << (dir_opp(d) - 1);
+      const int sh = (t & 3) * 8;
+      __threadfence_block();  // release our A[c]
+      const uint32_t old = atomicAnd(&s.pend[t >> 2], ~(bit << sh));
+      if (((old >> sh) & 0xFFu) != bit) { live = false; continue; }  // others pending
+      __threadfence_block();  // acquire the other donors' values
+      T acc = at;
+#pragma unroll
+      for (int k = 1; k <= 8; ++k)
+        if (m & (1u << (k - 1))) acc = acc + A[(ty + dir_dy(k)) * BC + tx + dir_dx(k)];
+      a = acc;
+    }
+    A[t] = a;
+    ly = ty;
+    lx = tx;
+    d = dt;
+    ++retired;
   }
   return retired;
 }
