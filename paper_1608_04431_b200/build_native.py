@@ -37,16 +37,22 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
+    """variant "prof": -DFA_PHASE_CLOCKS per-phase cycle counters -> libfa_prof.so
+    (a tuning tool; never the product library)."""
+    lib = LIB if not variant else os.path.join(HERE, f"libfa_{variant}.so")
+    if not force and not variant and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), *sources(), "-o", LIB + ".tmp", "-ldl"]
+    extra = ["-DFA_PHASE_CLOCKS"] if variant == "prof" else []
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), *sources(), "-o", lib + ".tmp", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libfa.so")
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(lib + ".tmp", lib)
+    if variant:
+        return lib
     with open(os.path.join(HERE, "ptxas.log"), "w") as f:
         f.write(res.stdout + res.stderr)
     if verbose:

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -43,8 +44,21 @@ Geom make_geom(int64_t H, int64_t W, int64_t th, int64_t tw) {
   g.TW = (tw > 0 && tw < W) ? tw : W;
   g.TR = (H + g.TH - 1) / g.TH;
   g.TC = (W + g.TW - 1) / g.TW;
-  g.nbt_r = (g.TH + BR - 1) / BR;
-  g.nbt_c = (g.TW + BC - 1) / BC;
+  g.br = kBR;
+  g.bc = kBC;
+  g.nw = kNW;
+  // tuning override: FA_BLOCK = 32x32 | 32x64 | 64x64 (block.cu instantiates these)
+  if (const char* e = getenv("FA_BLOCK")) {
+    if (!strcmp(e, "32x32x1")) { g.nw = 1; }
+    else if (!strcmp(e, "32x32x4")) { g.nw = 4; }
+    else if (!strcmp(e, "32x64")) { g.br = 32; g.bc = 64; }
+    else if (!strcmp(e, "64x64")) { g.br = 64; g.bc = 64; g.nw = 4; }
+    else if (!strcmp(e, "64x64x1")) { g.br = 64; g.bc = 64; g.nw = 1; }
+    else if (!strcmp(e, "64x64x2")) { g.br = 64; g.bc = 64; g.nw = 2; }
+  }
+  g.pb = 2 * (g.br + g.bc) - 4;
+  g.nbt_r = (g.TH + g.br - 1) / g.br;
+  g.nbt_c = (g.TW + g.bc - 1) / g.bc;
   g.NBR = g.TR * g.nbt_r;
   g.NBC = g.TC * g.nbt_c;
   g.nblocks = g.NBR * g.NBC;
@@ -155,7 +169,7 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
   rt.err = cudaSuccess;
   rt.peel_rounds = rt.contract_levels = rt.jump_rounds = rt.launches = 0;
   Geom g = make_geom(H, W, ctx->tile_r, ctx->tile_c);
-  const int64_t slots = g.nblocks * PB;
+  const int64_t slots = g.nblocks * g.pb;
   if (slots >= (int64_t)0xFFFFFFF0ll)
     return set_err(ctx, FA_E_ARG, "raster too large for one device (block slots exceed 2^32)");
   CK(cudaEventRecord(ctx->ev[0], st));
@@ -217,7 +231,12 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
   uint32_t* parent = rt.alloc<uint32_t>(nn);
   T* S = rt.alloc<T>(nn);
   if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
-  const bool multi = (g.TR * g.TC > 1) || rec.want;
+  // On one device every tile is resident, so the per-tile problems and the
+  // global perimeter graph are solved jointly as one uncut block-exit graph
+  // (identical results: accumulation is linear).  The explicit
+  // tile level (cut graph, tile roots, G2, injection) runs when the tile
+  // records are requested -- and is the unit of the multi-GPU exchange.
+  const bool multi = rec.want;
   if (!multi) {
     CK(launch_g1_parent(st, nn, node_tgt, node_flags, slot_root, false, parent));
     ++rt.launches;

@@ -10,161 +10,380 @@
 //   pass 2 (k_pass2): [H6 offset propagation, EVICT P:L255-262]: rerun H2-H3 with
 //     w + x at the block perimeter cells (x = external inbound flow, D11/D12).
 //
-// H3 scheduling (differs from the paper's FIFO): chain
-// following.  Every source (no in-block donor) starts a walk; a walk adds its
-// value into the next cell and continues while it is that cell's only pending
-// donor.  Cells with exactly one donor need no atomic at all; at a junction the
-// arriving walk clears its bit in the target's pending-donor mask with one
-// shared-memory atomicAnd, and the last arrival gathers the donors' finished
-// values (fixed donor order) and continues.  Work is O(1) per cell; the
-// critical path is the longest in-block flow path.
+// H3 scheduling (differs from the paper's FIFO): walks.  The
+// block's sources (data cells without in-block donors) are compacted into a
+// shared queue.  A lane takes a source and walks downstream, adding its value
+// into the next cell and continuing while it is that cell's only pending
+// donor -- cells with exactly one donor need no atomic.  At a junction the
+// walk clears its bit in the target's pending-donor mask (one shared
+// atomicAnd on a packed word); only the last arrival gathers the donors'
+// values (fixed donor order) and continues.  A lane whose walk ends takes the
+// next source at once, so lanes stay busy while a few long rivers are walked.
+//
+// Why small blocks (default 32 x 32, one warp): a block's walks finish no
+// sooner than its longest in-block flow path, so throughput = cells in flight
+// per SM / block latency.  Shared memory bounds the cells in flight (~14 KB
+// per 32x32 f64 block -> 16 blocks per SM); smaller blocks shorten the
+// critical path (ncu on 64x64 blocks: 25 % occupancy, issue 35 %, stalls on
+// global loads and on the end-of-walk barrier).
+//
+// Shared-memory layout: directions are stored with a 1-cell halo ring, row
+// stride HS = BC + 8 with the block interior at column 4 (4-byte aligned rows
+// for SWAR); ring cells hold 254 (outside the block) or 255 (NoData /
+// off-grid), so walks need no bounds tests.  Masks and values use stride BC.
 #include "fa_internal.cuh"
 
 namespace fa {
 
-constexpr int HS = BC + 2;             // halo'd row stride
-constexpr int HN = (BR + 2) * (BC + 2);  // halo'd cells
+constexpr uint8_t kOut = 254;  // ring cell: outside the block, data
 
+// Optional per-phase cycle accounting (profiling build only, -DFA_PHASE_CLOCKS):
+// thread 0 of every CTA adds the cycles each phase took to g_phase[i].
+#ifdef FA_PHASE_CLOCKS
+__device__ unsigned long long g_phase[16];
+#define PH_T0 long long _ph_t = clock64()
+#define PH_MARK(i)                                                          \
+  do {                                                                      \
+    if (threadIdx.x == 0) {                                                 \
+      const long long _n = clock64();                                       \
+      atomicAdd(&g_phase[i], (unsigned long long)(_n - _ph_t));             \
+      _ph_t = _n;                                                           \
+    }                                                                       \
+  } while (0)
+}  // namespace fa
+extern "C" __attribute__((visibility("default"))) int fa_debug_phase_clocks(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, fa::g_phase, sizeof(fa::g_phase)) != cudaSuccess) return 1;
+  if (reset) {
+    static const unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(fa::g_phase, z, sizeof(z));
+  }
+  return 0;
+}
+namespace fa {
+#else
+#define PH_T0 (void)0
+#define PH_MARK(i) (void)0
+#endif
 
-struct __align__(16) SmemCommon {
-  uint8_t dirh[HN];   // directions with a 1-cell halo ring (ring: 255 = NoData/off-grid)
-  uint8_t msk[BN];    // in-block donor mask: bit k-1 set if neighbour in direction k drains here
-  uint32_t pend[BN / 4];  // pending-donor masks, 4 cells per word (atomicAnd)
-  uint32_t slot_nid[PB];
-  uint32_t cnt_exit, base, processed, ndata;
+// packed signed 8-bit offsets of direction codes 1..8 for a row stride S
+__host__ __device__ constexpr uint64_t pack_offsets(int S) {
+  uint64_t t = 0;
+  for (int k = 1; k <= 8; ++k)
+    t |= (uint64_t)(uint8_t)(int8_t)(dir_dy(k) * S + dir_dx(k)) << (8 * (k - 1));
+  return t;
+}
+
+template <int BR_, int BC_, int NW_>
+struct Cfg {
+  static constexpr int BR = BR_, BC = BC_, NW = NW_;
+  static constexpr int NT = 32 * NW;
+  static constexpr int BN = BR * BC;
+  static constexpr int PB = 2 * (BR + BC) - 4;
+  static constexpr int HS = BC + 8;               // halo'd row stride (interior at col 4)
+  static constexpr int HN = (BR + 2) * HS;
+  static constexpr int ZS = BC + 2;               // staged elevations stride
+  static constexpr int ZN = (BR + 2) * ZS;
+  static constexpr uint64_t OFFH = pack_offsets(HS);
+  static constexpr uint64_t OFFA = pack_offsets(BC);
+  static_assert(BC % 4 == 0 && BN % (4 * NT) == 0, "block shape");
+  static_assert(HS <= 120, "int8 offsets");
+  __device__ static __forceinline__ int offH(int d) { return (int)(int8_t)(OFFH >> (8 * (d - 1))); }
+  __device__ static __forceinline__ int offA(int d) { return (int)(int8_t)(OFFA >> (8 * (d - 1))); }
+  __device__ static __forceinline__ int hidx(int ly, int lx) { return (ly + 1) * HS + lx + 4; }
+  __device__ static __forceinline__ int a2h(int i) { return hidx(i / BC, i % BC); }
+  // packed successor of a cell: target index | donor-bit position << IB |
+  // target-is-junction << (IB+3); two stop codes: leaves the block (an exit,
+  // Alg. 2 "outside the tile") / ends inside (NoFlow or in-block NoData)
+  static constexpr int IB = BN <= 1024 ? 10 : 12;
+  using Nxt = typename std::conditional<BN <= 1024, uint16_t, uint32_t>::type;
+  static constexpr uint32_t JBIT = 1u << (IB + 3);
+  static constexpr uint32_t STOP_OUT = BN <= 1024 ? 0xFFFEu : 0xFFFFFFFEu;
+  static constexpr uint32_t STOP_END = BN <= 1024 ? 0xFFFFu : 0xFFFFFFFFu;
+  static_assert(BN <= (1 << IB), "index bits");
 };
 
-template <class T>
+template <class C>
+struct __align__(16) Smem {
+  uint8_t dirh[C::HN];
+  uint32_t msk4[C::BN / 4];  // donor masks, one byte per cell
+  uint32_t pend[C::BN / 4];  // pending-donor masks (atomicAnd)
+  uint16_t src[C::BN];       // source queue (A index)
+  typename C::Nxt nxt[C::BN];  // packed successors
+  uint32_t slot_nid[C::PB];
+  uint32_t nsrc, qhead, cnt_exit, base, processed, ndata;
+  __device__ __forceinline__ uint8_t msk(int i) const { return reinterpret_cast<const uint8_t*>(msk4)[i]; }
+};
+
+template <class C, class T>
 struct SmemSize {
-  static constexpr size_t a_bytes = sizeof(T) * BN;
-  static constexpr size_t z_bytes = sizeof(float) * HN;
+  static constexpr size_t a_bytes = sizeof(T) * C::BN;
+  static constexpr size_t z_bytes = sizeof(float) * C::ZN;
   static constexpr size_t region = ((a_bytes > z_bytes ? a_bytes : z_bytes) + 15) / 16 * 16;
-  static constexpr size_t total = region + sizeof(SmemCommon);
+  static constexpr size_t total = region + sizeof(Smem<C>);
 };
 
 template <int WK>
-__device__ __forceinline__ bool load_weight(const void* w, int64_t gi, double& wd, unsigned long long& wu) {
-  if (WK == 0) {
-    wd = 1.0;
-    wu = 1;
-    return true;
-  } else if (WK == 1) {
-    uint32_t v = static_cast<const uint32_t*>(w)[gi];
-    wd = (double)v;
-    wu = v;
-    return true;
-  } else {
-    float v = static_cast<const float*>(w)[gi];
-    wd = (double)v;
-    wu = 0;
-    return isfinite(v) && v >= 0.0f;  // D21
+__device__ __forceinline__ bool weight_ok(float v) {
+  return WK != 2 || (isfinite(v) && v >= 0.0f);  // D21
+}
+
+template <class T, int WK>
+__device__ __forceinline__ T wval(const void* w, int64_t gi) {
+  if constexpr (WK == 0) return (T)1;
+  else if constexpr (WK == 1) return (T) static_cast<const uint32_t*>(w)[gi];
+  else return (T) static_cast<const float*>(w)[gi];
+}
+
+// ---------------------------------------------------------------- H2
+// Donor masks by an 8-neighbour gather, 4 cells per 32-bit SWAR word (no
+// atomics; Alg. 1 first loop P:L131-148), and the compacted source queue.
+// Ring codes (254/255) never equal a direction, so no bounds tests.
+template <class C>
+__device__ __forceinline__ void build_masks(Smem<C>& s, int h, int w) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t* D = reinterpret_cast<const uint32_t*>(s.dirh);
+  for (int q = threadIdx.x; q < C::BN / 4; q += C::NT) {
+    const int ly = (4 * q) / C::BC, lx = (4 * q) % C::BC;
+    const int hw = C::hidx(ly, lx) >> 2;  // word index of the 4 cells
+    constexpr int RW = C::HS / 4;
+    const uint32_t u0 = D[hw - RW - 1], u1 = D[hw - RW], u2 = D[hw - RW + 1];
+    const uint32_t c0 = D[hw - 1], c1 = D[hw], c2 = D[hw + 1];
+    const uint32_t d0 = D[hw + RW - 1], d1 = D[hw + RW], d2 = D[hw + RW + 1];
+    // neighbour bytes for the 4 cells in each direction (byte j <-> cell j)
+    const uint32_t nN = u1, nS = d1;
+    const uint32_t nE = __funnelshift_r(c1, c2, 8), nW = __funnelshift_r(c0, c1, 24);
+    const uint32_t nNE = __funnelshift_r(u1, u2, 8), nNW = __funnelshift_r(u0, u1, 24);
+    const uint32_t nSE = __funnelshift_r(d1, d2, 8), nSW = __funnelshift_r(d0, d1, 24);
+    uint32_t m = 0;
+    // a neighbour in direction k is a donor iff its code points back: opp(k)
+    m |= (__vcmpeq4(nN, 0x05050505u) & 0x01010101u) << 0;   // k=1 N  -> S(5)
+    m |= (__vcmpeq4(nNE, 0x06060606u) & 0x01010101u) << 1;  // k=2 NE -> SW(6)
+    m |= (__vcmpeq4(nE, 0x07070707u) & 0x01010101u) << 2;   // k=3 E  -> W(7)
+    m |= (__vcmpeq4(nSE, 0x08080808u) & 0x01010101u) << 3;  // k=4 SE -> NW(8)
+    m |= (__vcmpeq4(nS, 0x01010101u) & 0x01010101u) << 4;   // k=5 S  -> N(1)
+    m |= (__vcmpeq4(nSW, 0x02020202u) & 0x01010101u) << 5;  // k=6 SW -> NE(2)
+    m |= (__vcmpeq4(nW, 0x03030303u) & 0x01010101u) << 6;   // k=7 W  -> E(3)
+    m |= (__vcmpeq4(nNW, 0x04040404u) & 0x01010101u) << 7;  // k=8 NW -> SE(4)
+    // NoData (255) and ring cells (254, inside the word when the block is
+    // ragged) are not cells of the block: no donors, never sources
+    const uint32_t nd = __vcmpgeu4(c1, 0xFEFEFEFEu);
+    m &= ~nd;
+    s.msk4[q] = m;
+    s.pend[q] = m;
+    // sources: data cells without in-block donors
+    const uint32_t zero = __vcmpeq4(m, 0u) & ~nd;  // 0xFF per source byte
+    const uint32_t sb = zero & 0x80808080u;
+    const int cnt = __popc(sb);
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    uint32_t base = 0;
+    if (lane == 31 && total) base = atomicAdd(&s.nsrc, (uint32_t)total);
+    base = __shfl_sync(0xFFFFFFFFu, base, 31) + (uint32_t)(incl - cnt);
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (sb & (0x80u << (8 * j))) s.src[base++] = (uint16_t)(4 * q + j);
+  }
+  __syncthreads();
+  // packed successors (needs every mask: the junction flag is the target's)
+  for (int i = threadIdx.x; i < C::BN; i += C::NT) {
+    const int ly = i / C::BC, lx = i % C::BC;
+    const int d = s.dirh[C::hidx(ly, lx)];
+    uint32_t v = C::STOP_END;  // NoFlow, NoData, ring, or drops into in-block NoData
+    if (d >= 1 && d <= 8 && ly < h && lx < w) {
+      const int ty = ly + dir_dy(d), tx = lx + dir_dx(d);
+      const int dt = s.dirh[C::hidx(ty, tx)];
+      if ((unsigned)ty >= (unsigned)h || (unsigned)tx >= (unsigned)w) {
+        v = C::STOP_OUT;  // leaves the block (possibly into NoData / off-grid): a block exit
+      } else if (dt < kOut) {
+        const int t = i + C::offA(d);
+        const uint32_t m = s.msk(t);
+        v = (uint32_t)t | ((uint32_t)((d + 3) & 7) << C::IB) | ((m & (m - 1)) ? C::JBIT : 0u);
+      }
+    }
+    s.nxt[i] = (typename C::Nxt)v;
   }
 }
 
-template <class T>
-__device__ __forceinline__ T from_w(double wd, unsigned long long wu) {
-  if constexpr (std::is_same<T, double>::value) return wd;
-  else return (T)wu;
-}
-
-// In-block accumulation by chain following (shared by both passes).  On
-// entry: dirh, msk, pend and A (= w [+ x]) are set and synced.  Returns the
-// number of cells this thread retired.
-//
-// One flat loop per lane: when a lane's walk ends it immediately starts its
-// next source, so lanes of a warp never wait for each other between walks
-// (a per-source loop would make every warp pay the sum over its sources of
-// the longest walk among its 32 lanes).  Each step issues its three shared
-// loads (direction, donor mask, value of the next cell) together.
-template <class T>
-__device__ __forceinline__ uint32_t chain_follow(SmemCommon& s, T* A, int h, int w) {
+// ---------------------------------------------------------------- H3
+// Walks from the shared source queue (both passes).  On entry dirh, masks,
+// pend, src/nsrc and A (= w [+ x]) are set and synced.  Returns the number of
+// cells this thread retired.
+template <class C, class T>
+__device__ __forceinline__ uint32_t chain_follow(Smem<C>& s, T* A) {
+  const uint32_t nsrc = s.nsrc;
   uint32_t retired = 0;
-  int next = threadIdx.x;  // next candidate source of this lane
-  int ly = 0, lx = 0, d = kNoFlow;
-  bool live = false;
+  uint32_t nx = C::STOP_END;  // successor word of the walk's current cell
   T a = (T)0;
   for (;;) {
-    if (!live) {
-      // fetch this lane's next source (data cell without in-block donors)
-      while (next < BN) {
-        const int i = next;
-        next += kThreads;
-        const int y = i / BC, x = i % BC;
-        if (y >= h || x >= w) continue;
-        const int dd = s.dirh[(y + 1) * HS + x + 1];
-        if (dd == kNoData || s.msk[i] != 0) continue;
-        ly = y;
-        lx = x;
-        d = dd;
-        a = A[i];
-        live = true;
-        ++retired;
-        break;
-      }
-      if (!live) break;
+    if (nx >= C::STOP_OUT) {
+      // walk ended: take the next source (per-lane shared atomic; no warp
+      // votes, so a lane never waits for the others of its warp)
+      const uint32_t q = atomicAdd(&s.qhead, 1u);
+      if (q >= nsrc) break;
+      const int c = s.src[q];
+      a = A[c];
+      nx = s.nxt[c];
+      ++retired;
+      continue;
     }
-    // one step of the walk from (ly, lx) with direction d and value a
-    if (d == kNoFlow || d > 8) { live = false; continue; }
-    const int ty = ly + dir_dy(d), tx = lx + dir_dx(d);
-    if ((unsigned)ty >= (unsigned)h || (unsigned)tx >= (unsigned)w) { live = false; continue; }
-    const int t = ty * BC + tx;
-    const int dt = s.dirh[(ty + 1) * HS + tx + 1];
-    const uint32_t m = s.msk[t];
+    // one step downstream: target t is an in-block data cell
+    const int t = nx & ((1u << C::IB) - 1);
     const T at = A[t];  // w(t) [+ x(t)]: only the walk that finishes t writes A[t]
-    if (dt == kNoData) { live = false; continue; }  // dropped into NoData (D8)
-    if ((m & (m - 1)) == 0) {
-      a = at + a;  // sole in-block donor: no atomic needed
-    } else {
-      const uint32_t bit = 1u << (dir_opp(d) - 1);
+    const uint32_t nt = s.nxt[t];
+    if (nx & C::JBIT) {
+      // junction: clear our bit; the last arrival gathers the donors
+      const uint32_t bit = 1u << ((nx >> C::IB) & 7);
       const int sh = (t & 3) * 8;
-      __threadfence_block();  // release our A[c]
+      __threadfence_block();  // release our value
       const uint32_t old = atomicAnd(&s.pend[t >> 2], ~(bit << sh));
-      if (((old >> sh) & 0xFFu) != bit) { live = false; continue; }  // others pending
+      if (((old >> sh) & 0xFFu) != bit) { nx = C::STOP_END; continue; }  // others pending
       __threadfence_block();  // acquire the other donors' values
+      uint32_t m = s.msk(t);
       T acc = at;
-#pragma unroll
-      for (int k = 1; k <= 8; ++k)
-        if (m & (1u << (k - 1))) acc = acc + A[(ty + dir_dy(k)) * BC + tx + dir_dx(k)];
+      do {  // donors in code order (fixed summation order)
+        const int k = __ffs(m);
+        m &= m - 1;
+        acc = acc + A[t + C::offA(k)];
+      } while (m);
       a = acc;
+    } else {
+      a = at + a;  // sole in-block donor: no atomic
     }
     A[t] = a;
-    ly = ty;
-    lx = tx;
-    d = dt;
+    nx = nt;
     ++retired;
   }
   return retired;
 }
 
-// donor masks by gather (H2, Alg. 1 first loop P:L131-148, no atomics)
-__device__ __forceinline__ void build_masks(SmemCommon& s, int h, int w) {
-  for (int i = threadIdx.x; i < BN; i += kThreads) {
-    const int ly = i / BC, lx = i % BC;
-    uint32_t m = 0;
-    if (ly < h && lx < w && s.dirh[(ly + 1) * HS + lx + 1] != kNoData) {
-#pragma unroll
-      for (int k = 1; k <= 8; ++k) {
-        const int ny = ly + dir_dy(k), nx = lx + dir_dx(k);
-        if ((unsigned)ny < (unsigned)h && (unsigned)nx < (unsigned)w &&
-            s.dirh[(ny + 1) * HS + nx + 1] == dir_opp(k))
-          m |= 1u << (k - 1);
-      }
-    }
-    s.msk[i] = (uint8_t)m;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < BN / 4; i += kThreads) {
-    const uint32_t* m4 = reinterpret_cast<const uint32_t*>(s.msk);
-    s.pend[i] = m4[i];
-  }
+// ---------------------------------------------------------------- shared stages
+template <class C>
+__device__ __forceinline__ void init_dirh(Smem<C>& s) {
+  uint32_t* D = reinterpret_cast<uint32_t*>(s.dirh);
+  for (int i = threadIdx.x; i < C::HN / 4; i += C::NT) D[i] = 0xFFFFFFFFu;
 }
 
-template <class T, int WK, bool FROM_DEM>
-__global__ void __launch_bounds__(kThreads) k_pass1(PassArgs<T, WK> P) {
+// interior directions from global (pass 2 and pass 1 from dirs); bad codes
+// -> NoData, flagged when `check`
+template <class C>
+__device__ __forceinline__ void load_dirs(Smem<C>& s, const uint8_t* dirs, const Geom& g, int64_t y0,
+                                          int64_t x0, int h, int w, bool check, uint32_t* status) {
+  const bool vec = w == C::BC && ((x0 & 3) == 0) && ((g.W & 3) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(dirs) & 3) == 0);
+  bool bad = false;
+  if (vec) {
+    for (int q = threadIdx.x; q < h * (C::BC / 4); q += C::NT) {
+      const int ly = q / (C::BC / 4), lx = (q % (C::BC / 4)) * 4;
+      uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(dirs + (y0 + ly) * g.W + x0 + lx));
+      // bytes > 8 and != 255 are illegal (D1)
+      const uint32_t hi = __vcmpgtu4(v, 0x08080808u) & ~__vcmpeq4(v, 0xFFFFFFFFu);
+      if (hi) { bad = true; v |= hi; }
+      *reinterpret_cast<uint32_t*>(&s.dirh[C::hidx(ly, lx)]) = v;
+    }
+  } else {
+    for (int i = threadIdx.x; i < h * C::BC; i += C::NT) {
+      const int ly = i / C::BC, lx = i % C::BC;
+      if (lx >= w) continue;
+      uint8_t d = dirs[(y0 + ly) * g.W + x0 + lx];
+      if (d > 8 && d != kNoData) { bad = true; d = kNoData; }
+      s.dirh[C::hidx(ly, lx)] = d;
+    }
+  }
+  if (check && bad) atomicOr(status, ST_BADCODE);
+}
+
+// Weights prefetched into registers at kernel entry (full, aligned blocks),
+// so their HBM latency overlaps the staging / D8 / mask phases.
+template <class C, int WK>
+struct WPre {
+  static constexpr int R = C::BN / (4 * C::NT);  // 16-byte groups per thread
+  uint4 r[WK == 0 ? 1 : R];
+  bool vec = false;
+  __device__ __forceinline__ void load(const void* wp, const Geom& g, int64_t y0, int64_t x0, int h, int w) {
+    if (WK == 0) return;
+    vec = h == C::BR && w == C::BC && ((x0 & 3) == 0) && ((g.W & 3) == 0) &&
+          ((reinterpret_cast<uintptr_t>(wp) & 15) == 0);
+    if (!vec) return;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const int q = threadIdx.x + k * C::NT;
+      const int ly = q / (C::BC / 4), lx = (q % (C::BC / 4)) * 4;
+      r[k] = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(wp) + (y0 + ly) * g.W + x0 + lx));
+    }
+  }
+};
+
+// A = w (Eq. 1; Alg. 1 "A(c) <- A(c) + 1") for data cells
+template <class C, class T, int WK>
+__device__ __forceinline__ void init_values(Smem<C>& s, T* A, const void* wp, const WPre<C, WK>& pre,
+                                            const Geom& g, int64_t y0, int64_t x0, int h, int w,
+                                            uint32_t* status, unsigned long long* wsum_out) {
+  unsigned long long wsum = 0;
+  uint32_t nd = 0;
+  bool bad = false;
+  // store one group of 4 cells (raw weight bits in u[]) into A
+  auto put = [&](int q, const uint32_t u[4], bool have) {
+    const int ly = q / (C::BC / 4), lx = (q % (C::BC / 4)) * 4;
+    const uint32_t dw = *reinterpret_cast<const uint32_t*>(&s.dirh[C::hidx(ly, lx)]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const bool data = ((dw >> (8 * j)) & 0xFF) < kOut;  // excludes NoData and the ring
+      if (!data) continue;
+      T v;
+      if constexpr (WK == 0) {
+        v = (T)1;
+      } else if constexpr (WK == 1) {
+        v = (T)u[j];
+      } else {
+        const float f = __uint_as_float(u[j]);
+        if (!weight_ok<WK>(f)) bad = true;
+        v = (T)f;
+      }
+      (void)have;
+      A[ly * C::BC + lx + j] = v;
+      ++nd;
+      if constexpr (!std::is_same<T, double>::value) wsum += (unsigned long long)v;
+    }
+  };
+  if (WK != 0 && pre.vec) {
+#pragma unroll
+    for (int k = 0; k < WPre<C, WK>::R; ++k) {
+      const uint32_t u[4] = {pre.r[k].x, pre.r[k].y, pre.r[k].z, pre.r[k].w};
+      put(threadIdx.x + k * C::NT, u, true);
+    }
+  } else {
+    for (int q = threadIdx.x; q < h * (C::BC / 4); q += C::NT) {
+      const int ly = q / (C::BC / 4), lx = (q % (C::BC / 4)) * 4;
+      const int64_t gi = (y0 + ly) * g.W + x0 + lx;
+      uint32_t u[4] = {0, 0, 0, 0};
+      if (WK != 0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (lx + j < w) u[j] = static_cast<const uint32_t*>(wp)[gi + j];
+      }
+      put(q, u, true);
+    }
+  }
+  if (bad) atomicOr(status, ST_BADWEIGHT);
+  if (!std::is_same<T, double>::value && wsum_out) {
+    for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xFFFFFFFFu, wsum, o);
+    if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(wsum_out, wsum);
+  }
+  atomicAdd(&s.ndata, nd);
+}
+
+// ---------------------------------------------------------------- pass 1
+template <class C, class T, int WK, bool FROM_DEM>
+__global__ void __launch_bounds__(C::NT) k_pass1(PassArgs<T, WK> P) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* A = reinterpret_cast<T*>(smem);
   float* zs = reinterpret_cast<float*>(smem);
-  SmemCommon& s = *reinterpret_cast<SmemCommon*>(smem + SmemSize<T>::region);
+  Smem<C>& s = *reinterpret_cast<Smem<C>*>(smem + SmemSize<C, T>::region);
   const Geom& g = P.g;
   const int64_t b = blockIdx.x;
   int64_t y0, x0;
@@ -172,149 +391,137 @@ __global__ void __launch_bounds__(kThreads) k_pass1(PassArgs<T, WK> P) {
   g.block_box(b, y0, x0, h, w);
   const int tid = threadIdx.x;
   if (h <= 0 || w <= 0) {
-    for (int p = tid; p < PB; p += kThreads) P.slot_root[b * PB + p] = kNone;
+    for (int p = tid; p < C::PB; p += C::NT) P.slot_root[b * C::PB + p] = kNone;
     return;
   }
-  if (tid == 0) { s.cnt_exit = 0; s.processed = 0; s.ndata = 0; }
-  // ---- stage the block + halo ring
-  for (int i = tid; i < HN; i += kThreads) {
-    s.dirh[i] = kNoData;
-    if (FROM_DEM) zs[i] = __int_as_float(0x7fc00000);
-  }
-  __syncthreads();
-  const int rw = w + 2, rn = (h + 2) * (w + 2);
-  for (int i = tid; i < rn; i += kThreads) {
-    const int ly = i / rw - 1, lx = i % rw - 1;
-    const int64_t gy = y0 + ly, gx = x0 + lx;
-    const bool in = gy >= 0 && gx >= 0 && gy < g.H && gx < g.W;
-    const int hi = (ly + 1) * HS + lx + 1;
-    if (FROM_DEM) {
-      if (in) zs[hi] = stage_z(P.dem[gy * g.W + gx], P.nodata);
-    } else if (in) {
-      uint8_t d = P.dirs_in[gy * g.W + gx];
-      const bool inner = ly >= 0 && lx >= 0 && ly < h && lx < w;
-      if (d > 8 && d != kNoData) {
-        if (inner) atomicOr(P.status, ST_BADCODE);
-        d = kNoData;
-      }
-      s.dirh[hi] = d;
-    }
-  }
-  __syncthreads();
+  WPre<C, WK> pre;
+  pre.load(P.w, g, y0, x0, h, w);  // in flight during staging, D8 and masks
+  if (tid == 0) s.cnt_exit = s.processed = s.ndata = s.nsrc = s.qhead = 0;
+  init_dirh(s);
   if (FROM_DEM) {
-    // H1: D8 for the block's cells; the halo ring only records NoData-ness
-    for (int i = tid; i < rn; i += kThreads) {
+    // ---- stage z with its halo (NoData and off-grid -> NaN), then D8 (H1)
+    const int rw = w + 2, rn = (h + 2) * (w + 2);
+    for (int i = tid; i < rn; i += C::NT) {
       const int ly = i / rw - 1, lx = i % rw - 1;
-      const int hi = (ly + 1) * HS + lx + 1;
+      const int64_t gy = y0 + ly, gx = x0 + lx;
+      float v = __int_as_float(0x7fc00000);
+      if (gy >= 0 && gx >= 0 && gy < g.H && gx < g.W) v = stage_z(P.dem[gy * g.W + gx], P.nodata);
+      zs[(ly + 1) * C::ZS + lx + 1] = v;
+    }
+    __syncthreads();
+    for (int i = tid; i < rn; i += C::NT) {
+      const int ly = i / rw - 1, lx = i % rw - 1;
+      const int zi = (ly + 1) * C::ZS + lx + 1;
       const bool inner = ly >= 0 && lx >= 0 && ly < h && lx < w;
+      uint8_t code;
       if (inner) {
-        const uint8_t code = d8_code<HS>(zs, hi);
-        s.dirh[hi] = code;
+        code = d8_code<C::ZS>(zs, zi);
         if (P.dirs_out) P.dirs_out[(y0 + ly) * g.W + x0 + lx] = code;
       } else {
-        s.dirh[hi] = isnan(zs[hi]) ? kNoData : (uint8_t)kNoFlow;
+        code = isnan(zs[zi]) ? kNoData : kOut;
       }
+      s.dirh[C::hidx(ly, lx)] = code;
     }
     __syncthreads();  // zs dead from here on; A aliases it
+  } else {
+    __syncthreads();
+    load_dirs<C>(s, P.dirs_in, g, y0, x0, h, w, true, P.status);
+    // halo ring: 254 for data outside the block, 255 for NoData / off-grid
+    const int rn = 2 * (w + 2) + 2 * h;
+    for (int i = tid; i < rn; i += C::NT) {
+      int ly, lx;
+      if (i < w + 2) { ly = -1; lx = i - 1; }
+      else if (i < 2 * (w + 2)) { ly = h; lx = i - (w + 2) - 1; }
+      else { const int j = i - 2 * (w + 2); ly = j >> 1; lx = (j & 1) ? w : -1; }
+      const int64_t gy = y0 + ly, gx = x0 + lx;
+      uint8_t code = kNoData;
+      if (gy >= 0 && gx >= 0 && gy < g.H && gx < g.W && P.dirs_in[gy * g.W + gx] != kNoData) code = kOut;
+      s.dirh[C::hidx(ly, lx)] = code;
+    }
+    __syncthreads();
   }
-  build_masks(s, h, w);
-  // ---- A = w (Eq. 1; Alg. 1 "A(c) <- A(c) + 1")
-  unsigned long long wsum = 0;
-  uint32_t nd = 0;
-  for (int i = tid; i < BN; i += kThreads) {
-    const int ly = i / BC, lx = i % BC;
-    if (ly >= h || lx >= w) continue;
-    if (s.dirh[(ly + 1) * HS + lx + 1] == kNoData) continue;
-    double wd;
-    unsigned long long wu;
-    if (!load_weight<WK>(P.w, (y0 + ly) * g.W + x0 + lx, wd, wu)) atomicOr(P.status, ST_BADWEIGHT);
-    A[i] = from_w<T>(wd, wu);
-    wsum += wu;
-    ++nd;
-  }
-  if (!std::is_same<T, double>::value && P.wsum) {
-    for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xFFFFFFFFu, wsum, o);
-    if ((tid & 31) == 0 && wsum) atomicAdd(P.wsum, wsum);
-  }
-  atomicAdd(&s.ndata, nd);
+  build_masks<C>(s, h, w);
+  init_values<C, T, WK>(s, A, P.w, pre, g, y0, x0, h, w, P.status, P.wsum);
   __syncthreads();
-  // ---- H3
-  const uint32_t ret = chain_follow<T>(s, A, h, w);
+  const uint32_t ret = chain_follow<C, T>(s, A);
   atomicAdd(&s.processed, ret);
   __syncthreads();
   if (tid == 0 && s.processed != s.ndata) atomicOr(P.status, ST_CYCLE);
   // ---- H4: block exits -> graph nodes (compacted), perimeter links
   const int np = (int)perim_count(h, w);
-  int64_t px = 0, py = 0;
-  bool is_exit = false;
-  int rank = 0, d = 0;
-  if (tid < np) {
-    perim_xy(tid, h, w, px, py);
-    d = s.dirh[(py + 1) * HS + px + 1];
-    if (d >= 1 && d <= 8) {
-      const int ty = (int)py + dir_dy(d), tx = (int)px + dir_dx(d);
-      is_exit = (unsigned)ty >= (unsigned)h || (unsigned)tx >= (unsigned)w;
+  for (int p = tid; p < C::PB; p += C::NT) {
+    uint32_t r = kNone;
+    if (p < np) {
+      int64_t px, py;
+      perim_xy(p, h, w, px, py);
+      const int d = s.dirh[C::hidx((int)py, (int)px)];
+      if (d >= 1 && d <= 8) {
+        const int ty = (int)py + dir_dy(d), tx = (int)px + dir_dx(d);
+        if ((unsigned)ty >= (unsigned)h || (unsigned)tx >= (unsigned)w) r = atomicAdd(&s.cnt_exit, 1u);
+      }
     }
-    if (is_exit) rank = atomicAdd(&s.cnt_exit, 1u);
+    s.slot_nid[p] = r;  // rank among the block's exits, for now
   }
   __syncthreads();
   if (tid == 0) s.base = s.cnt_exit ? atomicAdd(P.node_count, s.cnt_exit) : 0;
   __syncthreads();
-  if (tid < np) {
-    uint32_t nid = kNone;
-    if (is_exit) {
-      nid = s.base + rank;
-      const int ty = (int)py + dir_dy(d), tx = (int)px + dir_dx(d);
-      const bool dead = s.dirh[(ty + 1) * HS + tx + 1] == kNoData;
-      const int64_t gy = y0 + ty, gx = x0 + tx;
-      uint8_t fl = dead ? NF_DEAD : 0;
-      int64_t t0y, t0x, th, tw;
-      g.tile_box(g.tile_of_block(b), t0y, t0x, th, tw);
-      if (gy < t0y || gx < t0x || gy >= t0y + th || gx >= t0x + tw) fl |= NF_OUT_TILE;
-      uint32_t tgt = kNone;
-      if (!dead) {
-        int tly, tlx;
-        const int64_t tb = g.block_of(gy, gx, tly, tlx);
-        int64_t by0, bx0;
-        int bh, bw;
-        g.block_box(tb, by0, bx0, bh, bw);
-        tgt = (uint32_t)(tb * PB + perim_index(tlx, tly, bh, bw));
-      }
-      P.node_val[nid] = A[py * BC + px];
-      P.node_slot[nid] = (uint32_t)(b * PB + tid);
-      P.node_tgt[nid] = tgt;
-      P.node_flags[nid] = fl;
+  int64_t t0y, t0x, th, tw;
+  g.tile_box(g.tile_of_block(b), t0y, t0x, th, tw);
+  for (int p = tid; p < np; p += C::NT) {
+    const uint32_t rank = s.slot_nid[p];
+    if (rank == kNone) continue;
+    const uint32_t nid = s.base + rank;
+    int64_t px, py;
+    perim_xy(p, h, w, px, py);
+    const int d = s.dirh[C::hidx((int)py, (int)px)];
+    const int ty = (int)py + dir_dy(d), tx = (int)px + dir_dx(d);
+    const bool dead = s.dirh[C::hidx(ty, tx)] == kNoData;
+    const int64_t gy = y0 + ty, gx = x0 + tx;
+    uint8_t fl = dead ? NF_DEAD : 0;
+    if (gy < t0y || gx < t0x || gy >= t0y + th || gx >= t0x + tw) fl |= NF_OUT_TILE;
+    uint32_t tgt = kNone;
+    if (!dead) {
+      int tly, tlx;
+      const int64_t tb = g.block_of(gy, gx, tly, tlx);
+      int64_t by0, bx0;
+      int bh, bw;
+      g.block_box(tb, by0, bx0, bh, bw);
+      tgt = (uint32_t)(tb * C::PB + perim_index(tlx, tly, bh, bw));
     }
-    s.slot_nid[tid] = nid;
+    P.node_val[nid] = A[py * C::BC + px];
+    P.node_slot[nid] = (uint32_t)(b * C::PB + p);
+    P.node_tgt[nid] = tgt;
+    P.node_flags[nid] = fl;
+    s.slot_nid[p] = nid;
   }
   __syncthreads();
-  for (int p = tid; p < PB; p += kThreads) {
+  // Alg. 2 FollowPath for every block perimeter cell (root exit node or none)
+  for (int p = tid; p < C::PB; p += C::NT) {
     uint32_t root = kNone;
     if (p < np) {
       int64_t cx, cy;
       perim_xy(p, h, w, cx, cy);
+      int c = (int)cy * C::BC + (int)cx;
       for (int steps = 0; steps <= h * w; ++steps) {
-        const int dd = s.dirh[(cy + 1) * HS + cx + 1];
-        if (dd == kNoFlow || dd > 8) break;  // FlowTerminates
-        const int ny = (int)cy + dir_dy(dd), nx = (int)cx + dir_dx(dd);
-        if ((unsigned)ny >= (unsigned)h || (unsigned)nx >= (unsigned)w) {
-          root = s.slot_nid[perim_index(cx, cy, h, w)];
+        const uint32_t nx = s.nxt[c];
+        if (nx == C::STOP_OUT) {  // c is a block exit
+          root = s.slot_nid[perim_index(c % C::BC, c / C::BC, h, w)];
           break;
         }
-        if (s.dirh[(ny + 1) * HS + nx + 1] == kNoData) break;  // terminates in NoData
-        cx = nx;
-        cy = ny;
+        if (nx == C::STOP_END) break;  // FlowTerminates (NoFlow / in-block NoData)
+        c = nx & ((1u << C::IB) - 1);
       }
     }
-    P.slot_root[b * PB + p] = root;
+    P.slot_root[b * C::PB + p] = root;
   }
 }
 
-template <class T, int WK>
-__global__ void __launch_bounds__(kThreads) k_pass2(PassArgs<T, WK> P) {
+// ---------------------------------------------------------------- pass 2
+template <class C, class T, int WK>
+__global__ void __launch_bounds__(C::NT) k_pass2(PassArgs<T, WK> P) {
   extern __shared__ __align__(16) unsigned char smem[];
   T* A = reinterpret_cast<T*>(smem);
-  SmemCommon& s = *reinterpret_cast<SmemCommon*>(smem + SmemSize<T>::region);
+  Smem<C>& s = *reinterpret_cast<Smem<C>*>(smem + SmemSize<C, T>::region);
   const Geom& g = P.g;
   const int64_t b = blockIdx.x;
   int64_t y0, x0;
@@ -322,76 +529,117 @@ __global__ void __launch_bounds__(kThreads) k_pass2(PassArgs<T, WK> P) {
   g.block_box(b, y0, x0, h, w);
   if (h <= 0 || w <= 0) return;
   const int tid = threadIdx.x;
-  if (tid == 0) { s.processed = 0; s.ndata = 0; }
-  for (int i = tid; i < HN; i += kThreads) s.dirh[i] = kNoData;
+  PH_T0;
+  WPre<C, WK> pre;
+  pre.load(P.w, g, y0, x0, h, w);  // in flight during staging and masks
+  if (tid == 0) s.processed = s.ndata = s.nsrc = s.qhead = 0;
+  init_dirh(s);  // ring = 255: never a donor, stops walks
   __syncthreads();
-  for (int i = tid; i < BN; i += kThreads) {
-    const int ly = i / BC, lx = i % BC;
-    if (ly >= h || lx >= w) continue;
-    uint8_t d = P.dirs_in[(y0 + ly) * g.W + x0 + lx];
-    if (d > 8) d = kNoData;  // codes were validated in pass 1
-    s.dirh[(ly + 1) * HS + lx + 1] = d;
-  }
+  load_dirs<C>(s, P.dirs_in, g, y0, x0, h, w, false, P.status);
   __syncthreads();
-  build_masks(s, h, w);
-  uint32_t nd = 0;
-  for (int i = tid; i < BN; i += kThreads) {
-    const int ly = i / BC, lx = i % BC;
-    if (ly >= h || lx >= w) continue;
-    if (s.dirh[(ly + 1) * HS + lx + 1] == kNoData) continue;
-    double wd;
-    unsigned long long wu;
-    load_weight<WK>(P.w, (y0 + ly) * g.W + x0 + lx, wd, wu);
-    A[i] = from_w<T>(wd, wu);
-    ++nd;
-  }
-  atomicAdd(&s.ndata, nd);
+  PH_MARK(0);
+  build_masks<C>(s, h, w);
   __syncthreads();
+  PH_MARK(1);
+  init_values<C, T, WK>(s, A, P.w, pre, g, y0, x0, h, w, P.status, nullptr);
+  __syncthreads();
+  PH_MARK(2);
   // inject x at the block perimeter (offset propagation; D12)
   const int np = (int)perim_count(h, w);
-  for (int p = tid; p < np; p += kThreads) {
+  for (int p = tid; p < np; p += C::NT) {
     int64_t px, py;
     perim_xy(p, h, w, px, py);
-    if (s.dirh[(py + 1) * HS + px + 1] == kNoData) continue;
-    const T x = P.x_slot[b * PB + p];
-    A[py * BC + px] = A[py * BC + px] + x;
+    if (s.dirh[C::hidx((int)py, (int)px)] == kNoData) continue;
+    const T x = P.x_slot[b * C::PB + p];
+    A[py * C::BC + px] = A[py * C::BC + px] + x;
   }
   __syncthreads();
-  const uint32_t ret = chain_follow<T>(s, A, h, w);
+  PH_MARK(3);
+  const uint32_t ret = chain_follow<C, T>(s, A);
   atomicAdd(&s.processed, ret);
   __syncthreads();
+  PH_MARK(4);
   if (tid == 0 && s.processed != s.ndata) atomicOr(P.status, ST_CYCLE);
-  for (int i = tid; i < BN; i += kThreads) {
-    const int ly = i / BC, lx = i % BC;
-    if (ly >= h || lx >= w) continue;
-    const bool nodata = s.dirh[(ly + 1) * HS + lx + 1] == kNoData;
-    P.acc[(y0 + ly) * g.W + x0 + lx] = nodata ? AccT<T>::marker() : A[i];
+  // ---- write A (NoData marker D9), vectorised when aligned
+  T* out = P.acc;
+  constexpr int V = 16 / sizeof(T);  // cells per 16-byte store
+  const bool vec = w == C::BC && ((x0 % V) == 0) && ((g.W % V) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  if (vec) {
+    for (int q = tid; q < h * (C::BC / V); q += C::NT) {
+      const int ly = q / (C::BC / V), lx = (q % (C::BC / V)) * V;
+      alignas(16) T v[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j)
+        v[j] = s.dirh[C::hidx(ly, lx + j)] == kNoData ? AccT<T>::marker() : A[ly * C::BC + lx + j];
+      *reinterpret_cast<uint4*>(out + (y0 + ly) * g.W + x0 + lx) = *reinterpret_cast<const uint4*>(v);
+    }
+  } else {
+    for (int i = tid; i < h * C::BC; i += C::NT) {
+      const int ly = i / C::BC, lx = i % C::BC;
+      if (lx >= w) continue;
+      const bool nodata = s.dirh[C::hidx(ly, lx)] == kNoData;
+      out[(y0 + ly) * g.W + x0 + lx] = nodata ? AccT<T>::marker() : A[i];
+    }
   }
+  PH_MARK(5);
 }
 
 // ---------------------------------------------------------------- launchers
-template <class T, int WK>
-cudaError_t launch_pass1(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t st) {
-  const size_t sm = SmemSize<T>::total;
+template <class C, class T, int WK>
+cudaError_t launch_pass1_c(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t st) {
+  const size_t sm = SmemSize<C, T>::total;
   if (from_dem) {
-    auto k = k_pass1<T, WK, true>;
+    auto k = k_pass1<C, T, WK, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<(unsigned)a.g.nblocks, kThreads, sm, st>>>(a);
+    k<<<(unsigned)a.g.nblocks, C::NT, sm, st>>>(a);
   } else {
-    auto k = k_pass1<T, WK, false>;
+    auto k = k_pass1<C, T, WK, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<(unsigned)a.g.nblocks, kThreads, sm, st>>>(a);
+    k<<<(unsigned)a.g.nblocks, C::NT, sm, st>>>(a);
   }
   return cudaGetLastError();
+}
+
+template <class C, class T, int WK>
+cudaError_t launch_pass2_c(const PassArgs<T, WK>& a, cudaStream_t st) {
+  const size_t sm = SmemSize<C, T>::total;
+  auto k = k_pass2<C, T, WK>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k<<<(unsigned)a.g.nblocks, C::NT, sm, st>>>(a);
+  return cudaGetLastError();
+}
+
+using Cfg32 = Cfg<32, 32, 2>;
+using Cfg32w1 = Cfg<32, 32, 1>;
+using Cfg32w4 = Cfg<32, 32, 4>;
+using Cfg3264 = Cfg<32, 64, 2>;
+using Cfg64 = Cfg<64, 64, 4>;
+using Cfg64w1 = Cfg<64, 64, 1>;
+using Cfg64w2 = Cfg<64, 64, 2>;
+
+template <class T, int WK>
+cudaError_t launch_pass1(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t st) {
+  if (a.g.br == 32 && a.g.bc == 32 && a.g.nw == 1) return launch_pass1_c<Cfg32w1, T, WK>(a, from_dem, st);
+  if (a.g.br == 32 && a.g.bc == 32 && a.g.nw == 4) return launch_pass1_c<Cfg32w4, T, WK>(a, from_dem, st);
+  if (a.g.br == 32 && a.g.bc == 32) return launch_pass1_c<Cfg32, T, WK>(a, from_dem, st);
+  if (a.g.br == 32 && a.g.bc == 64) return launch_pass1_c<Cfg3264, T, WK>(a, from_dem, st);
+  if (a.g.br == 64 && a.g.bc == 64 && a.g.nw == 1) return launch_pass1_c<Cfg64w1, T, WK>(a, from_dem, st);
+  if (a.g.br == 64 && a.g.bc == 64 && a.g.nw == 2) return launch_pass1_c<Cfg64w2, T, WK>(a, from_dem, st);
+  if (a.g.br == 64 && a.g.bc == 64) return launch_pass1_c<Cfg64, T, WK>(a, from_dem, st);
+  return cudaErrorInvalidValue;
 }
 
 template <class T, int WK>
 cudaError_t launch_pass2(const PassArgs<T, WK>& a, cudaStream_t st) {
-  const size_t sm = SmemSize<T>::total;
-  auto k = k_pass2<T, WK>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k<<<(unsigned)a.g.nblocks, kThreads, sm, st>>>(a);
-  return cudaGetLastError();
+  if (a.g.br == 32 && a.g.bc == 32 && a.g.nw == 1) return launch_pass2_c<Cfg32w1, T, WK>(a, st);
+  if (a.g.br == 32 && a.g.bc == 32 && a.g.nw == 4) return launch_pass2_c<Cfg32w4, T, WK>(a, st);
+  if (a.g.br == 32 && a.g.bc == 32) return launch_pass2_c<Cfg32, T, WK>(a, st);
+  if (a.g.br == 32 && a.g.bc == 64) return launch_pass2_c<Cfg3264, T, WK>(a, st);
+  if (a.g.br == 64 && a.g.bc == 64 && a.g.nw == 1) return launch_pass2_c<Cfg64w1, T, WK>(a, st);
+  if (a.g.br == 64 && a.g.bc == 64 && a.g.nw == 2) return launch_pass2_c<Cfg64w2, T, WK>(a, st);
+  if (a.g.br == 64 && a.g.bc == 64) return launch_pass2_c<Cfg64, T, WK>(a, st);
+  return cudaErrorInvalidValue;
 }
 
 #define FA_INST(T, WK)                                                              \

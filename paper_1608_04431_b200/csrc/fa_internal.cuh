@@ -18,12 +18,11 @@ constexpr uint32_t kFlowExternal = 0xFFFFFFFEu;    // Alg. 2 sentinel
 constexpr uint32_t kFlowTerminates = 0xFFFFFFFFu;  // Alg. 2 sentinel
 
 // Block = the CTA-resident sub-tile: the paper's Alg. 1 + Alg. 2
-// run on it entirely in shared memory.
-constexpr int BR = 64;                 // block rows
-constexpr int BC = 64;                 // block cols
-constexpr int BN = BR * BC;            // cells per block
-constexpr int PB = 2 * (BR + BC) - 4;  // perimeter slots per block (252)
-constexpr int kThreads = 512;          // threads per block kernel
+// run on it entirely in shared memory.  Its shape is a compile-time
+// parameter of the block kernels (block.cu) and a run-time field of Geom.
+constexpr int kBR = 32;  // default block rows
+constexpr int kBC = 32;  // default block cols
+constexpr int kNW = 2;   // default warps per block
 
 // status bits (device flag word)
 constexpr uint32_t ST_BADCODE = 1u;
@@ -34,13 +33,19 @@ constexpr uint32_t ST_CYCLE = 4u;
 constexpr uint8_t NF_OUT_TILE = 1;  // target outside the node's tile (FlowExternal at tile level, D22)
 constexpr uint8_t NF_DEAD = 2;      // target off-grid or NoData: flow dropped (D8)
 
-// direction code k -> (dx, dy), S:L33 / D1.  Index 0 unused.
-__host__ __device__ constexpr int dir_dx(int k) {
-  return (k == 2 || k == 3 || k == 4) ? 1 : (k == 6 || k == 7 || k == 8) ? -1 : 0;
-}
-__host__ __device__ constexpr int dir_dy(int k) {
-  return (k == 1 || k == 2 || k == 8) ? -1 : (k == 4 || k == 5 || k == 6) ? 1 : 0;
-}
+// direction code k -> (dx, dy), S:L33 / D1.  Index 0 unused.  Packed 2-bit
+// tables (value + 1) so a run-time code costs a shift and a mask.
+constexpr uint32_t kDxTab = (1u << 2) | (2u << 4) | (2u << 6) | (2u << 8) | (1u << 10) | (0u << 12) |
+                            (0u << 14) | (0u << 16);
+constexpr uint32_t kDyTab = (0u << 2) | (0u << 4) | (1u << 6) | (2u << 8) | (2u << 10) | (2u << 12) |
+                            (1u << 14) | (0u << 16);
+__host__ __device__ constexpr int dir_dx(int k) { return (int)((kDxTab >> (2 * k)) & 3u) - 1; }
+__host__ __device__ constexpr int dir_dy(int k) { return (int)((kDyTab >> (2 * k)) & 3u) - 1; }
+static_assert(dir_dx(1) == 0 && dir_dy(1) == -1 && dir_dx(2) == 1 && dir_dy(2) == -1 && dir_dx(3) == 1 &&
+                  dir_dy(3) == 0 && dir_dx(4) == 1 && dir_dy(4) == 1 && dir_dx(5) == 0 && dir_dy(5) == 1 &&
+                  dir_dx(6) == -1 && dir_dy(6) == 1 && dir_dx(7) == -1 && dir_dy(7) == 0 &&
+                  dir_dx(8) == -1 && dir_dy(8) == -1,
+              "direction table (S:L33)");
 // code pointing back: opp(k) = ((k + 3) & 7) + 1
 __host__ __device__ constexpr int dir_opp(int k) { return ((k + 3) & 7) + 1; }
 
@@ -58,6 +63,8 @@ struct Geom {
   int64_t nblocks;
   int64_t row0;      // global row of this raster's first row (strips)
   int64_t GH;        // global raster rows (== H single GPU)
+  int br, bc, pb;    // block shape and perimeter slots per block (2(br+bc)-4)
+  int nw;            // warps per block kernel CTA
 
   __host__ __device__ int64_t tile_of_block(int64_t b) const {
     int64_t gr = b / NBC, gc = b % NBC;
@@ -67,20 +74,20 @@ struct Geom {
   __host__ __device__ void block_box(int64_t b, int64_t& y0, int64_t& x0, int& h, int& w) const {
     int64_t gr = b / NBC, gc = b % NBC;
     int64_t ty = gr / nbt_r, tx = gc / nbt_c;
-    y0 = ty * TH + (gr % nbt_r) * BR;
-    x0 = tx * TW + (gc % nbt_c) * BC;
+    y0 = ty * TH + (gr % nbt_r) * br;
+    x0 = tx * TW + (gc % nbt_c) * bc;
     int64_t ty1 = (ty + 1) * TH < H ? (ty + 1) * TH : H;
     int64_t tx1 = (tx + 1) * TW < W ? (tx + 1) * TW : W;
     int64_t hh = ty1 - y0, ww = tx1 - x0;
-    h = hh <= 0 ? 0 : (hh > BR ? BR : (int)hh);
-    w = ww <= 0 ? 0 : (ww > BC ? BC : (int)ww);
+    h = hh <= 0 ? 0 : (hh > br ? br : (int)hh);
+    w = ww <= 0 ? 0 : (ww > bc ? bc : (int)ww);
   }
   __host__ __device__ int64_t block_of(int64_t y, int64_t x, int& ly, int& lx) const {
     int64_t ty = y / TH, tx = x / TW;
     int64_t ry = y - ty * TH, rx = x - tx * TW;
-    int64_t gr = ty * nbt_r + ry / BR, gc = tx * nbt_c + rx / BC;
-    ly = (int)(ry % BR);
-    lx = (int)(rx % BC);
+    int64_t gr = ty * nbt_r + ry / br, gc = tx * nbt_c + rx / bc;
+    ly = (int)(ry % br);
+    lx = (int)(rx % bc);
     return gr * NBC + gc;
   }
   __host__ __device__ void tile_box(int64_t t, int64_t& y0, int64_t& x0, int64_t& h,

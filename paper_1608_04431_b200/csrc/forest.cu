@@ -64,6 +64,48 @@ __global__ void k_peel(const uint32_t* __restrict__ front, uint32_t nf,
   }
 }
 
+// Walks on the global forest ("last arrival continues"): each ready node adds
+// its finished sum into its parent; the thread whose decrement retires the
+// parent's last pending child continues from the parent.  One launch replaces
+// the wide rounds of level-synchronous peeling; a walk stops after `cap`
+// steps and re-queues the ready node, leaving deep chains to contraction.
+template <class T>
+__global__ void k_walk(const uint32_t* __restrict__ front, uint32_t nf, const uint32_t* __restrict__ parent,
+                       T* val, uint32_t* cnt, uint8_t* done, uint32_t* next, uint32_t* ncount,
+                       uint32_t* nretired, int cap) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  uint32_t retired = 0;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < nf; base += stride) {
+    const uint32_t i = base + threadIdx.x;
+    bool push = false;
+    uint32_t pnode = kNone;
+    if (i < nf) {
+      uint32_t v = front[i];
+      T s = __ldcg(&val[v]);
+      for (int steps = 0;; ++steps) {
+        done[v] = 1;
+        ++retired;
+        const uint32_t p = parent[v];
+        if (p == kNone) break;
+        atomic_add(&val[p], s);
+        __threadfence();  // our contribution before our decrement
+        if (atomicSub(&cnt[p], 1u) != 1u) break;
+        __threadfence();  // every contribution to p is now visible
+        if (steps + 1 >= cap) {
+          push = true;
+          pnode = p;
+          break;
+        }
+        s = __ldcg(&val[p]);
+        v = p;
+      }
+    }
+    warp_append(push, pnode, next, ncount);
+  }
+  for (int o = 16; o; o >>= 1) retired += __shfl_xor_sync(0xFFFFFFFFu, retired, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(nretired, retired);
+}
+
 __global__ void k_compact_residual(uint32_t n, const uint8_t* __restrict__ done, uint32_t* R,
                                    uint32_t* mcount, uint32_t* rid) {
   const uint32_t stride = gridDim.x * blockDim.x;
@@ -191,6 +233,7 @@ __global__ void k_set_flag(uint32_t* st, uint32_t f) { atomicOr(st, f); }
 
 constexpr int kMaxLevels = 64;
 constexpr int kMaxJump = 40;
+constexpr int kWalkCap = 512;  // steps per walk before re-queueing (deep chains -> contraction)
 
 template <class T>
 cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, int level) {
@@ -217,6 +260,17 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
   uint32_t nf = rt.h_cnt[0];
   uint64_t remaining = n;
   bool contracted = false;
+  if (nf > 0) {
+    // bulk of the forest: one launch of capped walks from every leaf
+    cudaMemsetAsync(ctr + 1, 0, 2 * sizeof(uint32_t), st);
+    k_walk<T><<<grid_for(nf), 256, 0, st>>>(fa_, nf, parent, val, cnt, done, fb, ctr + 1, ctr + 2, kWalkCap);
+    ++rt.launches;
+    ++rt.peel_rounds;
+    std::swap(fa_, fb);
+    rt.read(ctr + 1, 2);
+    nf = rt.h_cnt[0];
+    remaining -= rt.h_cnt[1];
+  }
   while (nf > 0 && !rt.err) {
     if ((uint64_t)nf * 8 < remaining) {
       // ---------------- contract the residual forest

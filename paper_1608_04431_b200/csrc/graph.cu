@@ -104,7 +104,7 @@ __global__ void k_tile_records(Geom g, int64_t nslots, const int64_t* __restrict
     int64_t by0, bx0;
     int bh, bw;
     g.block_box(b, by0, bx0, bh, bw);
-    const int64_t bslot = b * PB + perim_index(lx, ly, bh, bw);
+    const int64_t bslot = b * g.pb + perim_index(lx, ly, bh, bw);
     uint32_t L = kFlowTerminates;
     T at = (T)0;
     if (d >= 1 && d <= 8) {
@@ -119,7 +119,7 @@ __global__ void k_tile_records(Geom g, int64_t nslots, const int64_t* __restrict
           const uint32_t r = troot[e];
           if (flags[r] & NF_OUT_TILE) {
             const uint32_t rs = node_slot[r];
-            const int64_t rb = rs / PB, rp = rs % PB;
+            const int64_t rb = rs / g.pb, rp = rs % g.pb;
             int64_t ry0, rx0;
             int rh, rw;
             g.block_box(rb, ry0, rx0, rh, rw);

@@ -12,7 +12,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfa.so")
+LIB_PATH = os.environ.get("FA_LIB") or os.path.join(_HERE, "libfa.so")  # FA_LIB: tuning builds only
 
 FA_OK, FA_E_ARG, FA_E_DIRCODE, FA_E_CYCLE, FA_E_OVERFLOW, FA_E_NOMEM, FA_E_CUDA, FA_E_NCCL, FA_E_STATE = range(9)
 STATUS_NAMES = {0: "FA_OK", 1: "FA_E_ARG", 2: "FA_E_DIRCODE", 3: "FA_E_CYCLE", 4: "FA_E_OVERFLOW",

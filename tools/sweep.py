@@ -1,0 +1,47 @@
+"""Tuning sweep (not the benchmark): time fa_accumulate on a config for several
+block shapes (FA_BLOCK) and print per-phase device times."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import inputs  # noqa: E402
+from paper_1608_04431_b200 import fa  # noqa: E402
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
+    rows = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] != "0" else None
+    shapes = sys.argv[3].split(",") if len(sys.argv) > 3 else ["32x32", "32x64", "64x64"]
+    tiles = sys.argv[4] if len(sys.argv) > 4 else None
+    t0 = time.time()
+    cfg = inputs.make_config(name, rows, rows)
+    print(f"{name} {cfg.rows}x{cfg.cols} gen {time.time() - t0:.1f}s", flush=True)
+    tile = cfg.tile if tiles is None else tuple(int(v) for v in tiles.split("x"))
+    st = torch.cuda.Stream()
+    src = torch.from_numpy(cfg.dem if cfg.dem is not None else cfg.dirs).cuda()
+    w = torch.from_numpy(cfg.w).cuda() if cfg.w is not None else None
+    out = torch.empty((cfg.rows, cfg.cols), dtype=fa.TORCH_ACC[fa.ATYPES[cfg.atype]], device="cuda")
+    kw = dict(dem=src) if cfg.dem is not None else dict(dirs=src)
+    for shape in shapes:
+        os.environ["FA_BLOCK"] = shape
+        with fa.Context(0, stream=st, tile=tile) as ctx:
+            for _ in range(2):
+                ctx.accumulate(w=w, atype=cfg.atype, out=out, **kw)
+            res = []
+            for _ in range(4):
+                ctx.accumulate(w=w, atype=cfg.atype, out=out, **kw)
+                res.append(ctx.stats())
+        p = {k: float(np.median([r[k] for r in res])) for k in ("ms_pass1", "ms_graph", "ms_pass2", "ms_total")}
+        r = res[-1]
+        print(f"{shape}: total {p['ms_total']:.2f} ms  pass1 {p['ms_pass1']:.2f}  graph {p['ms_graph']:.2f}  "
+              f"pass2 {p['ms_pass2']:.2f}  -> {cfg.cells / p['ms_total'] / 1e6:.1f} Gcells/s  "
+              f"nodes {r['graph_nodes']} launches {r['launches']} peel {r['peel_rounds']} "
+              f"contract {r['contract_levels']} jumps {r['jump_rounds']}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
