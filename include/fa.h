@@ -91,6 +91,16 @@ FA_API fa_status fa_accumulate(fa_ctx* ctx, int64_t rows, int64_t cols, const fl
                         const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc,
                         fa_atype atype);
 
+/* The row-strip pipeline of fa_accumulate_dist (H4-H7) on one device: the
+ * raster is cut into `nstrips` strips of whole tile rows, each strip runs
+ * phase A (pass 1 with halo rows, tile records), the records of all strips
+ * are exchanged by device copies instead of NCCL, and each strip runs phase
+ * B.  Same inputs, outputs and results as fa_accumulate; it exists so the
+ * multi-GPU data path can be verified on one GPU. */
+FA_API fa_status fa_accumulate_strips(fa_ctx* ctx, int nstrips, int64_t rows, int64_t cols,
+                                      const float* dem, float nodata, const uint8_t* dirs,
+                                      const void* w, fa_wtype wtype, void* acc, fa_atype atype);
+
 /* H4/H5 intermediates for tests and tools: number of tile perimeter slots
  * for a rows x cols raster under the context's tiling (tiles row-major,
  * slots per tile in clockwise perimeter order from the tile's top-left,

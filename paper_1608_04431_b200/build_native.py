@@ -25,6 +25,14 @@ NVCC_FLAGS = [
 ]
 
 
+def nccl_include() -> str:
+    """The torch-bundled NCCL headers (libnccl itself is dlopen'ed at run time,
+    so the process never holds two NCCL copies)."""
+    import nvidia.nccl
+
+    return os.path.join(list(nvidia.nccl.__path__)[0], "include")
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -45,7 +53,8 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     extra = ["-DFA_PHASE_CLOCKS"] if variant == "prof" else []
-    cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), *sources(), "-o", lib + ".tmp", "-ldl"]
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", nccl_include(), *sources(),
+           "-o", lib + ".tmp", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

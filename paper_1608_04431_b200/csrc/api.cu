@@ -1,15 +1,28 @@
 // api.cu -- the C ABI of libfa (include/fa.h) and the host orchestration of
-// the hot path: pass 1 (H1-H4 per block) -> graph solve (H5) -> pass 2 (H6).
+// the hot path:
+//   pass 1 (H1-H4 per block) -> graph solve (H5) -> pass 2 (H6),
+// plus the tiled / row-strip pipeline (H4-H7) used by fa_perimeter_records,
+// fa_accumulate_strips (several strips on one device) and fa_accumulate_dist
+// (one strip per rank, NCCL over NVLink):
+//   phase A (per strip): pass 1 with halo rows, tile-cut block-exit graph ->
+//     A_T, tile roots -> tile perimeter records (F, A, L)
+//   exchange: the records of every strip reach every rank
+//   phase B (per strip): the producer's global graph over all tile perimeter
+//     slots, solved redundantly -> offsets x_T (a_in, D11) ->
+//     injected into the strip's tile-cut graph -> pass 2 (EVICT).
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
 #include <type_traits>
+#include <vector>
 
 #include "fa.h"
 #include "forest.cuh"
+#include "nccl.h"
 
 namespace fa {
 
@@ -22,19 +35,23 @@ cudaError_t launch_d8(const float* dem, int64_t H, int64_t W, float nodata, uint
 cudaError_t launch_g1_parent(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
                              const uint32_t* slot_root, bool cut, uint32_t* parent);
 template <class T>
-cudaError_t launch_scatter_x(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const T* S, T* x_slot);
-template <class T>
-cudaError_t launch_g2(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
-                      const uint32_t* slot_root, const uint32_t* troot, const T* S1, uint32_t* parent2,
-                      T* val2);
-template <class T>
-cudaError_t launch_inject(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
-                          const uint32_t* slot_root, const T* S2, T* val1, T* xT_slot);
+cudaError_t launch_scatter_x(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
+                             const T* S, T* x_slot, bool intra_tile);
 template <class T>
 cudaError_t launch_tile_records(cudaStream_t st, const Geom& g, int64_t nslots, const int64_t* tbase,
                                 const uint8_t* dirs, const uint32_t* slot_root, const uint32_t* troot,
                                 const uint8_t* flags, const uint32_t* node_slot, const T* S1,
-                                const T* xT_slot, uint32_t* links, T* tile_acc, T* offs);
+                                uint32_t* links, uint8_t* fdir, T* tile_acc);
+template <class T>
+cudaError_t launch_g2_slots(cudaStream_t st, const Geom& gg, int64_t nslots, const int64_t* tbase,
+                            const uint32_t* links, const uint8_t* fdir, const T* tile_acc, uint32_t* parent,
+                            T* val);
+template <class T>
+cudaError_t launch_xT(cudaStream_t st, int64_t nslots, const uint32_t* parent, const uint32_t* links,
+                      const T* S2, T* xT);
+template <class T>
+cudaError_t launch_inject_slots(cudaStream_t st, const Geom& g, int64_t nslots, const int64_t* tbase,
+                                const T* xT, const uint32_t* slot_root, T* val1, T* x_slot);
 
 Geom make_geom(int64_t H, int64_t W, int64_t th, int64_t tw) {
   Geom g{};
@@ -47,7 +64,7 @@ Geom make_geom(int64_t H, int64_t W, int64_t th, int64_t tw) {
   g.br = kBR;
   g.bc = kBC;
   g.nw = kNW;
-  // tuning override: FA_BLOCK = 32x32 | 32x64 | 64x64 (block.cu instantiates these)
+  // tuning override: FA_BLOCK = 32x32 | 32x32x1 | 32x32x4 | 32x64 | 64x64[x1|x2]
   if (const char* e = getenv("FA_BLOCK")) {
     if (!strcmp(e, "32x32x1")) { g.nw = 1; }
     else if (!strcmp(e, "32x32x4")) { g.nw = 4; }
@@ -67,6 +84,43 @@ Geom make_geom(int64_t H, int64_t W, int64_t th, int64_t tw) {
   return g;
 }
 
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct Nccl {
+  void* h = nullptr;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclBroadcast) broadcast = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+  bool load() {
+    if (h) return true;
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+#define FA_SYM(f, n) f = reinterpret_cast<decltype(f)>(dlsym(h, n))
+    FA_SYM(getUniqueId, "ncclGetUniqueId");
+    FA_SYM(commInitRank, "ncclCommInitRank");
+    FA_SYM(commDestroy, "ncclCommDestroy");
+    FA_SYM(groupStart, "ncclGroupStart");
+    FA_SYM(groupEnd, "ncclGroupEnd");
+    FA_SYM(send, "ncclSend");
+    FA_SYM(recv, "ncclRecv");
+    FA_SYM(broadcast, "ncclBroadcast");
+    FA_SYM(allReduce, "ncclAllReduce");
+    FA_SYM(errorString, "ncclGetErrorString");
+#undef FA_SYM
+    return getUniqueId && commInitRank && commDestroy && groupStart && groupEnd && send && recv &&
+           broadcast && allReduce && errorString;
+  }
+};
+Nccl& nccl() {
+  static Nccl n;
+  return n;
+}
 
 }  // namespace fa
 
@@ -80,6 +134,10 @@ struct fa_ctx {
   cudaEvent_t ev[6]{};
   uint32_t* d_small = nullptr;  // [0]=node_count [1]=status [2..3]=wsum(u64) [4..15] scratch
   uint32_t* h_small = nullptr;
+  // multi-GPU
+  ncclComm_t comm = nullptr;
+  int rank = -1, nranks = 0;
+  unsigned char comm_id[128]{};
 };
 
 namespace {
@@ -96,6 +154,19 @@ fa_status set_err(fa_ctx* c, fa_status s, const std::string& m) {
     cudaError_t _e = (__VA_ARGS__);                                                     \
     if (_e != cudaSuccess)                                                              \
       return set_err(ctx, FA_E_CUDA, std::string(#__VA_ARGS__ " failed: ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define NK(...)                                                                         \
+  do {                                                                                  \
+    ncclResult_t _r = (__VA_ARGS__);                                                    \
+    if (_r != ncclSuccess)                                                              \
+      return set_err(ctx, FA_E_NCCL, std::string(#__VA_ARGS__ " failed: ") + fa::nccl().errorString(_r)); \
+  } while (0)
+
+#define FS(...)                        \
+  do {                                 \
+    fa_status _s = (__VA_ARGS__);      \
+    if (_s != FA_OK) return _s;        \
   } while (0)
 
 bool is_device_ptr(const void* p) {
@@ -134,198 +205,374 @@ cudaError_t stage_out_alloc(cudaStream_t st, void* p, size_t bytes, Staged& s) {
   return cudaMallocAsync(&s.dev, bytes, st);
 }
 
-template <class T>
-constexpr fa_atype atype_of() {
-  return std::is_same<T, uint32_t>::value ? FA_A_U32
-         : std::is_same<T, double>::value ? FA_A_F64 : FA_A_U64;
+int64_t tile_perim_total(const Geom& g, std::vector<int64_t>* base) {
+  int64_t tot = 0;
+  if (base) base->assign(g.TR * g.TC + 1, 0);
+  for (int64_t t = 0; t < g.TR * g.TC; ++t) {
+    int64_t y0, x0, h, w;
+    g.tile_box(t, y0, x0, h, w);
+    if (base) (*base)[t] = tot;
+    tot += fa::perim_count(h, w);
+  }
+  if (base) (*base)[g.TR * g.TC] = tot;
+  return tot;
 }
 
+// ---------------------------------------------------------------- strip state
+template <class T>
+struct Strip {
+  Geom g{};               // strip geometry (H = strip rows; tiling as configured)
+  int64_t row_begin = 0;  // global row of strip row 0
+  const float* dem = nullptr;
+  const float* dem_up = nullptr;
+  const float* dem_dn = nullptr;
+  const uint8_t* dirs = nullptr;
+  const uint8_t* dirs_up = nullptr;
+  const uint8_t* dirs_dn = nullptr;
+  const void* w = nullptr;
+  T* acc = nullptr;
+  float nodata = 0;
+  // device state
+  uint8_t* dirs_buf = nullptr;
+  uint32_t* slot_root = nullptr;
+  T* node_val = nullptr;
+  uint32_t* node_slot = nullptr;
+  uint32_t* node_tgt = nullptr;
+  uint8_t* node_flags = nullptr;
+  T* x_slot = nullptr;
+  uint32_t nn = 0;
+  uint32_t* parent = nullptr;
+  T* S = nullptr;
+  uint32_t* troot = nullptr;
+  int64_t slot0 = 0, nslots = 0;  // this strip's range of global tile perimeter slots
+  int64_t* dtbase = nullptr;      // local tile slot bases (device)
+  void release(fa::Runtime& rt) {
+    for (void* p : {(void*)dirs_buf, (void*)slot_root, (void*)node_val, (void*)node_slot, (void*)node_tgt,
+                    (void*)node_flags, (void*)x_slot, (void*)parent, (void*)S, (void*)troot, (void*)dtbase})
+      rt.free(p);
+    dirs_buf = nullptr;
+    slot_root = node_slot = node_tgt = parent = troot = nullptr;
+    node_val = x_slot = S = nullptr;
+    node_flags = nullptr;
+    dtbase = nullptr;
+  }
+  const uint8_t* dirs_in() const { return dem ? dirs_buf : dirs; }
+};
+
+template <class T, int WK>
+fa::PassArgs<T, WK> pass_args(fa_ctx* ctx, Strip<T>& s) {
+  fa::PassArgs<T, WK> a{};
+  a.g = s.g;
+  a.dem = s.dem;
+  a.nodata = s.nodata;
+  a.dirs_in = s.dirs_in();
+  a.dirs_out = s.dirs_buf;
+  a.w = s.w;
+  a.dem_up = s.dem_up;
+  a.dem_dn = s.dem_dn;
+  a.dirs_up = s.dirs_up;
+  a.dirs_dn = s.dirs_dn;
+  a.node_count = ctx->d_small + 0;
+  a.status = ctx->d_small + 1;
+  a.wsum = reinterpret_cast<unsigned long long*>(ctx->d_small + 2);
+  a.node_val = s.node_val;
+  a.node_slot = s.node_slot;
+  a.node_tgt = s.node_tgt;
+  a.node_flags = s.node_flags;
+  a.slot_root = s.slot_root;
+  a.x_slot = s.x_slot;
+  a.acc = s.acc;
+  return a;
+}
+
+// status word -> ABI status (data-dependent errors)
+fa_status check_status(fa_ctx* ctx, uint32_t stat, unsigned long long wsum, bool is_u32) {
+  using namespace fa;
+  if (stat & ST_BADCODE) return set_err(ctx, FA_E_DIRCODE, "direction raster holds a byte outside {0..8,255}");
+  if (stat & ST_BADWEIGHT) return set_err(ctx, FA_E_ARG, "f32 weights must be finite and >= 0");
+  if (is_u32 && wsum >= 0xFFFFFFFFull)
+    return set_err(ctx, FA_E_OVERFLOW, "sum of weights reaches the u32 range (NoData marker); use u64");
+  if (stat & ST_CYCLE) return set_err(ctx, FA_E_CYCLE, "direction graph has a cycle (some cells never retire)");
+  return FA_OK;
+}
+
+// pass 1 of a strip + block-exit graph parents (cut at tile edges when `cut`)
+template <class T, int WK>
+fa_status strip_pass1(fa_ctx* ctx, Strip<T>& s, bool cut) {
+  using namespace fa;
+  cudaStream_t st = ctx->st;
+  Runtime& rt = ctx->rt;
+  const Geom& g = s.g;
+  const int64_t slots = g.nblocks * g.pb;
+  if (slots >= (int64_t)0xFFFFFFF0ll)
+    return set_err(ctx, FA_E_ARG, "raster too large for one device (block slots exceed 2^32)");
+  if (s.dem) s.dirs_buf = rt.alloc<uint8_t>((size_t)(g.H * g.W));
+  s.slot_root = rt.alloc<uint32_t>(slots);
+  s.node_val = rt.alloc<T>(slots);
+  s.node_slot = rt.alloc<uint32_t>(slots);
+  s.node_tgt = rt.alloc<uint32_t>(slots);
+  s.node_flags = rt.alloc<uint8_t>(slots);
+  s.x_slot = rt.alloc<T>(slots);
+  if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+  CK(cudaMemsetAsync(ctx->d_small, 0, sizeof(uint32_t), st));  // node counter (status accumulates)
+  CK(cudaMemsetAsync(s.x_slot, 0, slots * sizeof(T), st));
+  CK(launch_pass1<T, WK>(pass_args<T, WK>(ctx, s), s.dem != nullptr, st));
+  ++rt.launches;
+  CK(rt.read(ctx->d_small, 4));
+  s.nn = rt.h_cnt[0];
+  s.parent = rt.alloc<uint32_t>(s.nn);
+  s.S = rt.alloc<T>(s.nn);
+  if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+  CK(launch_g1_parent(st, s.nn, s.node_tgt, s.node_flags, s.slot_root, cut, s.parent));
+  ++rt.launches;
+  return FA_OK;
+}
+
+// phase A tail: A_T at block exits, tile roots, tile perimeter records
+template <class T>
+fa_status strip_records(fa_ctx* ctx, Strip<T>& s, uint32_t* links, uint8_t* fdir, T* tile_acc) {
+  using namespace fa;
+  cudaStream_t st = ctx->st;
+  Runtime& rt = ctx->rt;
+  s.troot = rt.alloc<uint32_t>(s.nn);
+  std::vector<int64_t> hb;
+  s.nslots = tile_perim_total(s.g, &hb);
+  s.dtbase = rt.alloc<int64_t>(hb.size());
+  if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+  CK(cudaMemcpyAsync(s.dtbase, hb.data(), hb.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(s.S, s.node_val, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  CK(forest_solve<T>(rt, s.nn, s.parent, s.S));  // A_T at every block exit (Alg. 1 on each tile)
+  CK(forest_roots(rt, s.nn, s.parent, s.troot));
+  CK(launch_tile_records<T>(st, s.g, s.nslots, s.dtbase, s.dirs_in(), s.slot_root, s.troot, s.node_flags,
+                            s.node_slot, s.S, links + s.slot0, fdir + s.slot0, tile_acc + s.slot0));
+  ++rt.launches;
+  CK(cudaStreamSynchronize(st));  // hb must outlive the async copy
+  return FA_OK;
+}
+
+// the producer's global graph over all tile slots -> offsets x_T (all slots)
+template <class T>
+fa_status solve_g2(fa_ctx* ctx, const Geom& gg, int64_t nslots, const std::vector<int64_t>& hbase,
+                   const uint32_t* links, const uint8_t* fdir, const T* tile_acc, T* xT) {
+  using namespace fa;
+  cudaStream_t st = ctx->st;
+  Runtime& rt = ctx->rt;
+  if (nslots >= (int64_t)0xFFFFFFF0ll) return set_err(ctx, FA_E_ARG, "too many tile perimeter slots");
+  int64_t* db = rt.alloc<int64_t>(hbase.size());
+  uint32_t* par = rt.alloc<uint32_t>(nslots);
+  T* val = rt.alloc<T>(nslots);
+  if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+  CK(cudaMemcpyAsync(db, hbase.data(), hbase.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  CK(launch_g2_slots<T>(st, gg, nslots, db, links, fdir, tile_acc, par, val));
+  ++rt.launches;
+  CK(forest_solve<T>(rt, (uint32_t)nslots, par, val));
+  CK(cudaMemsetAsync(xT, 0, nslots * sizeof(T), st));
+  CK(launch_xT<T>(st, nslots, par, links, val, xT));
+  ++rt.launches;
+  CK(cudaStreamSynchronize(st));
+  rt.free(db);
+  rt.free(par);
+  rt.free(val);
+  return FA_OK;
+}
+
+// phase B tail: inject x_T, solve the tile-cut graph, scatter, pass 2
+template <class T, int WK>
+fa_status strip_finish(fa_ctx* ctx, Strip<T>& s, const T* xT_global) {
+  using namespace fa;
+  cudaStream_t st = ctx->st;
+  Runtime& rt = ctx->rt;
+  CK(cudaMemcpyAsync(s.S, s.node_val, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  CK(launch_inject_slots<T>(st, s.g, s.nslots, s.dtbase, xT_global + s.slot0, s.slot_root, s.S, s.x_slot));
+  ++rt.launches;
+  CK(forest_solve<T>(rt, s.nn, s.parent, s.S));  // true A at every block exit
+  CK(launch_scatter_x<T>(st, s.nn, s.node_tgt, s.node_flags, s.S, s.x_slot, true));
+  ++rt.launches;
+  if (s.acc) {
+    CK(launch_pass2<T, WK>(pass_args<T, WK>(ctx, s), st));
+    ++rt.launches;
+  }
+  return FA_OK;
+}
+
+void record_stats(fa_ctx* ctx, int64_t cells, int64_t blocks, int64_t nodes, int64_t tile_nodes) {
+  float t01 = 0, t12 = 0, t23 = 0;
+  cudaEventElapsedTime(&t01, ctx->ev[0], ctx->ev[1]);
+  cudaEventElapsedTime(&t12, ctx->ev[1], ctx->ev[2]);
+  cudaEventElapsedTime(&t23, ctx->ev[2], ctx->ev[3]);
+  fa_stats& S = ctx->stats;
+  const double ex = S.ms_exchange;
+  const int64_t bx = S.bytes_exchanged;
+  S = fa_stats{};
+  S.ms_pass1 = t01;
+  S.ms_graph = t12;
+  S.ms_pass2 = t23;
+  S.ms_total = t01 + t12 + t23;
+  S.ms_exchange = ex;
+  S.bytes_exchanged = bx;
+  S.cells = cells;
+  S.blocks = blocks;
+  S.graph_nodes = nodes;
+  S.tile_nodes = tile_nodes;
+  S.peel_rounds = ctx->rt.peel_rounds;
+  S.contract_levels = ctx->rt.contract_levels;
+  S.jump_rounds = ctx->rt.jump_rounds;
+  S.launches = ctx->rt.launches;
+}
+
+void reset_run(fa_ctx* ctx) {
+  fa::Runtime& rt = ctx->rt;
+  rt.st = ctx->st;
+  rt.err = cudaSuccess;
+  rt.peel_rounds = rt.contract_levels = rt.jump_rounds = rt.launches = 0;
+  rt.d_status = ctx->d_small + 1;
+  ctx->stats.ms_exchange = 0;
+  ctx->stats.bytes_exchanged = 0;
+}
+
+// ---------------------------------------------------------------- single device
 struct Records {
-  uint32_t* links = nullptr;  // device
+  uint32_t* links = nullptr;  // device outputs (fa_perimeter_records)
   void* tile_acc = nullptr;
   void* offsets = nullptr;
   bool want = false;
 };
 
-int64_t tile_perim_total(const Geom& g, int64_t* base /* TR*TC+1 or null */) {
-  int64_t tot = 0;
-  for (int64_t t = 0; t < g.TR * g.TC; ++t) {
-    int64_t y0, x0, h, w;
-    g.tile_box(t, y0, x0, h, w);
-    if (base) base[t] = tot;
-    tot += fa::perim_count(h, w);
-  }
-  if (base) base[g.TR * g.TC] = tot;
-  return tot;
-}
-
 template <class T, int WK>
-fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nodata,
-                  const uint8_t* dirs, const void* w, T* acc, Records& rec) {
+fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nodata, const uint8_t* dirs,
+                  const void* w, T* acc, Records& rec, int nstrips) {
   using namespace fa;
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
-  rt.st = st;
-  rt.err = cudaSuccess;
-  rt.peel_rounds = rt.contract_levels = rt.jump_rounds = rt.launches = 0;
-  Geom g = make_geom(H, W, ctx->tile_r, ctx->tile_c);
-  const int64_t slots = g.nblocks * g.pb;
-  if (slots >= (int64_t)0xFFFFFFF0ll)
-    return set_err(ctx, FA_E_ARG, "raster too large for one device (block slots exceed 2^32)");
-  CK(cudaEventRecord(ctx->ev[0], st));
-  uint8_t* dirs_buf = nullptr;
-  if (dem) {
-    CK(cudaMallocAsync(&dirs_buf, (size_t)(H * W), st));
-  }
-  uint32_t* slot_root = rt.alloc<uint32_t>(slots);
-  T* node_val = rt.alloc<T>(slots);
-  uint32_t* node_slot = rt.alloc<uint32_t>(slots);
-  uint32_t* node_tgt = rt.alloc<uint32_t>(slots);
-  uint8_t* node_flags = rt.alloc<uint8_t>(slots);
-  T* x_slot = rt.alloc<T>(slots);
-  if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+  reset_run(ctx);
   CK(cudaMemsetAsync(ctx->d_small, 0, 16 * sizeof(uint32_t), st));
-  CK(cudaMemsetAsync(x_slot, 0, slots * sizeof(T), st));
-
-  PassArgs<T, WK> a{};
-  a.g = g;
-  a.dem = dem;
-  a.nodata = nodata;
-  a.dirs_in = dem ? dirs_buf : dirs;
-  a.dirs_out = dirs_buf;
-  a.w = w;
-  a.node_count = ctx->d_small + 0;
-  a.status = ctx->d_small + 1;
-  a.wsum = reinterpret_cast<unsigned long long*>(ctx->d_small + 2);
-  a.node_val = node_val;
-  a.node_slot = node_slot;
-  a.node_tgt = node_tgt;
-  a.node_flags = node_flags;
-  a.slot_root = slot_root;
-  a.x_slot = x_slot;
-  a.acc = acc;
-  rt.d_status = ctx->d_small + 1;
-  CK(launch_pass1<T, WK>(a, dem != nullptr, st));
-  ++rt.launches;
-  CK(cudaEventRecord(ctx->ev[1], st));
-  CK(rt.read(ctx->d_small, 4));
-  const uint32_t nn = rt.h_cnt[0];
-  const uint32_t stat = rt.h_cnt[1];
-  unsigned long long wsum = 0;
-  memcpy(&wsum, &rt.h_cnt[2], 8);
-  fa_status bad = FA_OK;
-  std::string msg;
-  if (stat & ST_BADCODE) { bad = FA_E_DIRCODE; msg = "direction raster holds a byte outside {0..8,255}"; }
-  else if (stat & ST_BADWEIGHT) { bad = FA_E_ARG; msg = "f32 weights must be finite and >= 0"; }
-  else if (std::is_same<T, uint32_t>::value && wsum >= 0xFFFFFFFFull) {
-    bad = FA_E_OVERFLOW; msg = "sum of weights reaches the u32 range (NoData marker); use u64";
+  CK(cudaEventRecord(ctx->ev[0], st));
+  const Geom gg = make_geom(H, W, ctx->tile_r, ctx->tile_c);
+  if (!rec.want && nstrips <= 1) {
+    // On one device every tile is resident, so the per-tile problems and the
+    // global perimeter graph are solved jointly as one uncut block-exit graph
+    // (identical results: accumulation is linear).  The explicit
+    // tile level runs for the records and the strip / multi-GPU paths.
+    Strip<T> s;
+    s.g = gg;
+    s.dem = dem;
+    s.dirs = dirs;
+    s.w = w;
+    s.acc = acc;
+    s.nodata = nodata;
+    fa_status r = strip_pass1<T, WK>(ctx, s, false);
+    if (r != FA_OK) { s.release(rt); return r; }
+    CK(cudaEventRecord(ctx->ev[1], st));
+    const uint32_t stat = rt.h_cnt[1];
+    unsigned long long wsum = 0;
+    memcpy(&wsum, &rt.h_cnt[2], 8);
+    r = check_status(ctx, stat & ~ST_CYCLE, wsum, std::is_same<T, uint32_t>::value);
+    if (r != FA_OK) { s.release(rt); cudaStreamSynchronize(st); return r; }
+    CK(cudaMemcpyAsync(s.S, s.node_val, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    CK(forest_solve<T>(rt, s.nn, s.parent, s.S));
+    CK(launch_scatter_x<T>(st, s.nn, s.node_tgt, s.node_flags, s.S, s.x_slot, false));
+    ++rt.launches;
+    if (rt.err) { s.release(rt); return set_err(ctx, FA_E_CUDA, cudaGetErrorString(rt.err)); }
+    CK(cudaEventRecord(ctx->ev[2], st));
+    CK(launch_pass2<T, WK>(pass_args<T, WK>(ctx, s), st));
+    ++rt.launches;
+    CK(cudaEventRecord(ctx->ev[3], st));
+    s.release(rt);
+    CK(rt.read(ctx->d_small + 1, 1));
+    r = check_status(ctx, rt.h_cnt[0], 0, false);
+    if (r != FA_OK) return r;
+    record_stats(ctx, H * W, gg.nblocks, s.nn, 0);
+    return FA_OK;
   }
-  if (bad != FA_OK) {
-    for (void* p : {(void*)dirs_buf, (void*)slot_root, (void*)node_val, (void*)node_slot,
-                    (void*)node_tgt, (void*)node_flags, (void*)x_slot})
-      rt.free(p);
-    cudaStreamSynchronize(st);
-    return set_err(ctx, bad, msg);
-  }
-  // ---------------- graph (H5)
-  uint32_t* parent = rt.alloc<uint32_t>(nn);
-  T* S = rt.alloc<T>(nn);
+  // ---- tiled / strip pipeline on one device (strips = whole tile rows)
+  std::vector<int64_t> hbase;
+  const int64_t nslots = tile_perim_total(gg, &hbase);
+  uint32_t* links = rt.alloc<uint32_t>(nslots);
+  uint8_t* fdir = rt.alloc<uint8_t>(nslots);
+  T* tile_acc = rt.alloc<T>(nslots);
+  T* xT = rt.alloc<T>(nslots);
   if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
-  // On one device every tile is resident, so the per-tile problems and the
-  // global perimeter graph are solved jointly as one uncut block-exit graph
-  // (identical results: accumulation is linear).  The explicit
-  // tile level (cut graph, tile roots, G2, injection) runs when the tile
-  // records are requested -- and is the unit of the multi-GPU exchange.
-  const bool multi = rec.want;
-  if (!multi) {
-    CK(launch_g1_parent(st, nn, node_tgt, node_flags, slot_root, false, parent));
-    ++rt.launches;
-    CK(cudaMemcpyAsync(S, node_val, nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
-    CK(forest_solve<T>(rt, nn, parent, S));
-    CK(launch_scatter_x<T>(st, nn, node_tgt, S, x_slot));
-    ++rt.launches;
-  } else {
-    uint32_t* troot = rt.alloc<uint32_t>(nn);
-    uint32_t* parent2 = rt.alloc<uint32_t>(nn);
-    T* S1 = rt.alloc<T>(nn);
-    T* S2 = rt.alloc<T>(nn);
-    T* xT = rec.want ? rt.alloc<T>(slots) : nullptr;
-    if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
-    if (xT) CK(cudaMemsetAsync(xT, 0, slots * sizeof(T), st));
-    // per-tile problem: G1 with tile-leaving edges cut -> A_T at block exits
-    CK(launch_g1_parent(st, nn, node_tgt, node_flags, slot_root, true, parent));
-    ++rt.launches;
-    CK(cudaMemcpyAsync(S1, node_val, nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
-    CK(forest_solve<T>(rt, nn, parent, S1));
-    CK(forest_roots(rt, nn, parent, troot));
-    // global perimeter graph -> S2 = A at tile exits
-    CK(launch_g2<T>(st, nn, node_tgt, node_flags, slot_root, troot, S1, parent2, S2));
-    ++rt.launches;
-    CK(forest_solve<T>(rt, nn, parent2, S2));
-    // offsets x_T injected at tile entries -> true A at every block exit
-    CK(cudaMemcpyAsync(S, node_val, nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
-    CK(launch_inject<T>(st, nn, node_tgt, node_flags, slot_root, S2, S, xT));
-    ++rt.launches;
-    CK(forest_solve<T>(rt, nn, parent, S));
-    CK(launch_scatter_x<T>(st, nn, node_tgt, S, x_slot));
-    ++rt.launches;
-    if (rec.want) {
-      const int64_t nt = g.TR * g.TC;
-      int64_t* hb = new int64_t[nt + 1];
-      const int64_t ns = tile_perim_total(g, hb);
-      int64_t* db = rt.alloc<int64_t>(nt + 1);
-      CK(cudaMemcpyAsync(db, hb, (nt + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-      CK(cudaStreamSynchronize(st));
-      delete[] hb;
-      CK(launch_tile_records<T>(st, g, ns, db, a.dirs_in, slot_root, troot, node_flags, node_slot,
-                                S1, xT, rec.links, (T*)rec.tile_acc, (T*)rec.offsets));
-      ++rt.launches;
-      rt.free(db);
-    }
-    for (void* p : {(void*)troot, (void*)parent2, (void*)S1, (void*)S2, (void*)xT}) rt.free(p);
+  const int G = nstrips < 1 ? 1 : (int)(nstrips > gg.TR ? gg.TR : nstrips);
+  std::vector<Strip<T>> strips(G);
+  int64_t blocks = 0, nodes = 0;
+  auto cleanup = [&]() {
+    for (auto& s : strips) s.release(rt);
+    for (void* p : {(void*)links, (void*)fdir, (void*)tile_acc, (void*)xT}) rt.free(p);
+  };
+  for (int i = 0; i < G; ++i) {
+    // strip i: tile rows [i*TR/G, (i+1)*TR/G)
+    const int64_t tr0 = gg.TR * i / G, tr1 = gg.TR * (i + 1) / G;
+    const int64_t r0 = tr0 * gg.TH, r1 = tr1 * gg.TH < H ? tr1 * gg.TH : H;
+    Strip<T>& s = strips[i];
+    // same tiles as the whole raster: the strip is whole tile rows (a strip
+    // shorter than a tile row is the ragged last tile row itself)
+    s.g = make_geom(r1 - r0, W, gg.TH, gg.TW);
+    s.row_begin = r0;
+    s.nodata = nodata;
+    s.dem = dem ? dem + r0 * W : nullptr;
+    s.dem_up = dem && r0 > 0 ? dem + (r0 - 1) * W : nullptr;
+    s.dem_dn = dem && r1 < H ? dem + r1 * W : nullptr;
+    s.dirs = dirs ? dirs + r0 * W : nullptr;
+    s.dirs_up = dirs && r0 > 0 ? dirs + (r0 - 1) * W : nullptr;
+    s.dirs_dn = dirs && r1 < H ? dirs + r1 * W : nullptr;
+    s.w = w ? static_cast<const char*>(w) + r0 * W * (WK == 0 ? 0 : 4) : nullptr;
+    s.acc = acc ? acc + r0 * W : nullptr;
+    s.slot0 = hbase[tr0 * gg.TC];
+    fa_status r = strip_pass1<T, WK>(ctx, s, true);
+    if (r != FA_OK) { cleanup(); return r; }
+    r = strip_records<T>(ctx, s, links, fdir, tile_acc);
+    if (r != FA_OK) { cleanup(); return r; }
+    blocks += s.g.nblocks;
+    nodes += s.nn;
   }
-  if (rt.err) return set_err(ctx, FA_E_CUDA, std::string("graph solve: ") + cudaGetErrorString(rt.err));
+  CK(cudaEventRecord(ctx->ev[1], st));
+  CK(rt.read(ctx->d_small + 1, 3));
+  {
+    unsigned long long wsum = 0;
+    memcpy(&wsum, &rt.h_cnt[1], 8);
+    fa_status r = check_status(ctx, rt.h_cnt[0] & ~ST_CYCLE, wsum, std::is_same<T, uint32_t>::value);
+    if (r != FA_OK) { cleanup(); cudaStreamSynchronize(st); return r; }
+  }
+  fa_status r = solve_g2<T>(ctx, gg, nslots, hbase, links, fdir, tile_acc, xT);
+  if (r != FA_OK) { cleanup(); return r; }
   CK(cudaEventRecord(ctx->ev[2], st));
-  // ---------------- pass 2 (H6)
-  if (acc) { CK(launch_pass2<T, WK>(a, st)); ++rt.launches; }
+  for (auto& s : strips) {
+    r = strip_finish<T, WK>(ctx, s, xT);
+    if (r != FA_OK) { cleanup(); return r; }
+  }
   CK(cudaEventRecord(ctx->ev[3], st));
-  for (void* p : {(void*)dirs_buf, (void*)slot_root, (void*)node_val, (void*)node_slot,
-                  (void*)node_tgt, (void*)node_flags, (void*)x_slot, (void*)parent, (void*)S})
-    rt.free(p);
+  if (rec.want) {
+    if (rec.links) CK(cudaMemcpyAsync(rec.links, links, nslots * 4, cudaMemcpyDeviceToDevice, st));
+    if (rec.tile_acc) CK(cudaMemcpyAsync(rec.tile_acc, tile_acc, nslots * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    if (rec.offsets) CK(cudaMemcpyAsync(rec.offsets, xT, nslots * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  }
+  cleanup();
+  if (rt.err) return set_err(ctx, FA_E_CUDA, cudaGetErrorString(rt.err));
   CK(rt.read(ctx->d_small + 1, 1));
-  if (rt.h_cnt[0] & ST_CYCLE)
-    return set_err(ctx, FA_E_CYCLE, "direction graph has a cycle (some cells never retire)");
-  float t01 = 0, t12 = 0, t23 = 0;
-  cudaEventElapsedTime(&t01, ctx->ev[0], ctx->ev[1]);
-  cudaEventElapsedTime(&t12, ctx->ev[1], ctx->ev[2]);
-  cudaEventElapsedTime(&t23, ctx->ev[2], ctx->ev[3]);
-  ctx->stats.ms_pass1 = t01;
-  ctx->stats.ms_graph = t12;
-  ctx->stats.ms_pass2 = t23;
-  ctx->stats.ms_total = t01 + t12 + t23;
-  ctx->stats.cells = H * W;
-  ctx->stats.blocks = g.nblocks;
-  ctx->stats.graph_nodes = nn;
-  ctx->stats.peel_rounds = rt.peel_rounds;
-  ctx->stats.contract_levels = rt.contract_levels;
-  ctx->stats.jump_rounds = rt.jump_rounds;
-  ctx->stats.launches = rt.launches;
+  r = check_status(ctx, rt.h_cnt[0], 0, false);
+  if (r != FA_OK) return r;
+  record_stats(ctx, H * W, blocks, nodes, nslots);
+  return FA_OK;
+}
+
+fa_status check_types(fa_ctx* ctx, const float* dem, const uint8_t* dirs, const void* w, fa_wtype wtype,
+                      fa_atype atype) {
+  if ((dem == nullptr) == (dirs == nullptr))
+    return set_err(ctx, FA_E_ARG, "exactly one of dem or dirs must be given");
+  const bool ok_combo = ((wtype == FA_W_NONE || wtype == FA_W_U32) && (atype == FA_A_U32 || atype == FA_A_U64)) ||
+                        ((wtype == FA_W_F32 || wtype == FA_W_NONE) && atype == FA_A_F64);
+  if (!ok_combo) return set_err(ctx, FA_E_ARG, "unsupported (wtype, atype) combination");
+  if (wtype != FA_W_NONE && !w) return set_err(ctx, FA_E_ARG, "weights pointer is NULL");
   return FA_OK;
 }
 
 fa_status accumulate_impl(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem, float nodata,
-                          const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc,
-                          fa_atype atype, Records& rec) {
+                          const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc, fa_atype atype,
+                          Records& rec, int nstrips) {
   if (!ctx) return FA_E_ARG;
   ctx->err.clear();
   if (rows <= 0 || cols <= 0) return set_err(ctx, FA_E_ARG, "rows and cols must be > 0");
-  if ((dem == nullptr) == (dirs == nullptr))
-    return set_err(ctx, FA_E_ARG, "exactly one of dem or dirs must be given");
-  const bool ok_combo = ((wtype == FA_W_NONE || wtype == FA_W_U32) &&
-                         (atype == FA_A_U32 || atype == FA_A_U64)) ||
-                        ((wtype == FA_W_F32 || wtype == FA_W_NONE) && atype == FA_A_F64);
-  if (!ok_combo) return set_err(ctx, FA_E_ARG, "unsupported (wtype, atype) combination");
-  if (wtype != FA_W_NONE && !w) return set_err(ctx, FA_E_ARG, "weights pointer is NULL");
+  FS(check_types(ctx, dem, dirs, w, wtype, atype));
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->st;
   const size_t n = (size_t)rows * (size_t)cols;
@@ -350,15 +597,15 @@ fa_status accumulate_impl(fa_ctx* ctx, int64_t rows, int64_t cols, const float* 
   const uint8_t* d_dirs = (const uint8_t*)sdirs.dev;
   fa_status s;
   if (atype == FA_A_U32) {
-    s = wtype == FA_W_NONE ? run_acc<uint32_t, 0>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, (uint32_t*)sacc.dev, drec)
-                           : run_acc<uint32_t, 1>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, (uint32_t*)sacc.dev, drec);
+    s = wtype == FA_W_NONE ? run_acc<uint32_t, 0>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, (uint32_t*)sacc.dev, drec, nstrips)
+                           : run_acc<uint32_t, 1>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, (uint32_t*)sacc.dev, drec, nstrips);
   } else if (atype == FA_A_U64) {
     using U = unsigned long long;
-    s = wtype == FA_W_NONE ? run_acc<U, 0>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, (U*)sacc.dev, drec)
-                           : run_acc<U, 1>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, (U*)sacc.dev, drec);
+    s = wtype == FA_W_NONE ? run_acc<U, 0>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, (U*)sacc.dev, drec, nstrips)
+                           : run_acc<U, 1>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, (U*)sacc.dev, drec, nstrips);
   } else {
-    s = wtype == FA_W_NONE ? run_acc<double, 0>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, (double*)sacc.dev, drec)
-                           : run_acc<double, 2>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, (double*)sacc.dev, drec);
+    s = wtype == FA_W_NONE ? run_acc<double, 0>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, (double*)sacc.dev, drec, nstrips)
+                           : run_acc<double, 2>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, (double*)sacc.dev, drec, nstrips);
   }
   if (s == FA_OK) {
     if (sacc.owned) CK(cudaMemcpyAsync(acc, sacc.dev, n * asz, cudaMemcpyDeviceToHost, st));
@@ -369,9 +616,132 @@ fa_status accumulate_impl(fa_ctx* ctx, int64_t rows, int64_t cols, const float* 
   for (Staged* p : {&sdem, &sdirs, &sw, &sacc, &sl, &sa, &so})
     if (p->owned) cudaFreeAsync(p->dev, st);
   cudaError_t e = cudaStreamSynchronize(st);
-  if (s == FA_OK && e != cudaSuccess)
-    return set_err(ctx, FA_E_CUDA, std::string("stream: ") + cudaGetErrorString(e));
+  if (s == FA_OK && e != cudaSuccess) return set_err(ctx, FA_E_CUDA, std::string("stream: ") + cudaGetErrorString(e));
   return s;
+}
+
+// ---------------------------------------------------------------- multi-GPU (H7)
+template <class T>
+ncclDataType_t nccl_type() {
+  return std::is_same<T, uint32_t>::value ? ncclUint32 : std::is_same<T, double>::value ? ncclFloat64 : ncclUint64;
+}
+
+template <class T, int WK>
+fa_status run_dist(fa_ctx* ctx, int64_t GH, int64_t W, int64_t row_begin, int64_t H, const float* dem,
+                   float nodata, const uint8_t* dirs, const void* w, T* acc) {
+  using namespace fa;
+  cudaStream_t st = ctx->st;
+  Runtime& rt = ctx->rt;
+  Nccl& N = nccl();
+  const int rank = ctx->rank, nranks = ctx->nranks;
+  reset_run(ctx);
+  CK(cudaMemsetAsync(ctx->d_small, 0, 16 * sizeof(uint32_t), st));
+  CK(cudaEventRecord(ctx->ev[0], st));
+  const Geom gg = make_geom(GH, W, ctx->tile_r, ctx->tile_c);
+  if (row_begin % gg.TH != 0 || (row_begin + H != GH && H % gg.TH != 0))
+    return set_err(ctx, FA_E_ARG, "strips must consist of whole tile rows");
+  cudaEvent_t ex0, ex1;
+  cudaEventCreate(&ex0);
+  cudaEventCreate(&ex1);
+  // ---- C1: halo rows (one row each way, grouped send/recv)
+  const size_t esz = dem ? 4 : 1;
+  const void* src = dem ? (const void*)dem : (const void*)dirs;
+  void *up = nullptr, *dn = nullptr;
+  if (rank > 0) up = rt.alloc<uint8_t>(W * esz);
+  if (rank < nranks - 1) dn = rt.alloc<uint8_t>(W * esz);
+  if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+  CK(cudaEventRecord(ex0, st));
+  NK(N.groupStart());
+  const ncclDataType_t rt_row = dem ? ncclFloat32 : ncclUint8;
+  if (rank > 0) {
+    NK(N.send(src, W, rt_row, rank - 1, ctx->comm, st));
+    NK(N.recv(up, W, rt_row, rank - 1, ctx->comm, st));
+  }
+  if (rank < nranks - 1) {
+    NK(N.send(static_cast<const char*>(src) + (H - 1) * W * esz, W, rt_row, rank + 1, ctx->comm, st));
+    NK(N.recv(dn, W, rt_row, rank + 1, ctx->comm, st));
+  }
+  NK(N.groupEnd());
+  CK(cudaEventRecord(ex1, st));
+  // ---- phase A on this strip
+  std::vector<int64_t> hbase;
+  const int64_t nslots = tile_perim_total(gg, &hbase);
+  uint32_t* links = rt.alloc<uint32_t>(nslots);
+  uint8_t* fdir = rt.alloc<uint8_t>(nslots);
+  T* tile_acc = rt.alloc<T>(nslots);
+  T* xT = rt.alloc<T>(nslots);
+  if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+  Strip<T> s;
+  s.g = make_geom(H, W, gg.TH, gg.TW);
+  s.row_begin = row_begin;
+  s.nodata = nodata;
+  s.dem = dem;
+  s.dirs = dirs;
+  s.dem_up = dem ? (const float*)up : nullptr;
+  s.dem_dn = dem ? (const float*)dn : nullptr;
+  s.dirs_up = dem ? nullptr : (const uint8_t*)up;
+  s.dirs_dn = dem ? nullptr : (const uint8_t*)dn;
+  s.w = w;
+  s.acc = acc;
+  s.slot0 = hbase[(row_begin / gg.TH) * gg.TC];
+  auto cleanup = [&]() {
+    s.release(rt);
+    for (void* p : {(void*)links, (void*)fdir, (void*)tile_acc, (void*)xT, up, dn}) rt.free(p);
+  };
+  fa_status r = strip_pass1<T, WK>(ctx, s, true);
+  if (r == FA_OK) r = strip_records<T>(ctx, s, links, fdir, tile_acc);
+  if (r != FA_OK) { cleanup(); return r; }
+  CK(cudaEventRecord(ctx->ev[1], st));
+  // ---- C3 status all-reduce (max) + C2 exchange of the tile records
+  // (every rank's slots are a contiguous range: one broadcast per rank)
+  NK(N.allReduce(ctx->d_small + 1, ctx->d_small + 1, 1, ncclUint32, ncclMax, ctx->comm, st));
+  std::vector<int64_t> s0(nranks + 1), rows_of(nranks);
+  {
+    // ranks' first rows: gathered through the same all-reduce trick (one value each)
+    int64_t* d = rt.alloc<int64_t>(nranks);
+    CK(cudaMemsetAsync(d, 0, nranks * sizeof(int64_t), st));
+    CK(cudaMemcpyAsync(d + rank, &row_begin, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    NK(N.allReduce(d, d, nranks, ncclInt64, ncclSum, ctx->comm, st));
+    CK(cudaMemcpyAsync(rows_of.data(), d, nranks * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    rt.free(d);
+  }
+  for (int q = 0; q < nranks; ++q) s0[q] = hbase[(rows_of[q] / gg.TH) * gg.TC];
+  s0[nranks] = nslots;
+  CK(cudaEventRecord(ex0, st));
+  NK(N.groupStart());
+  for (int q = 0; q < nranks; ++q) {
+    const size_t cnt = (size_t)(s0[q + 1] - s0[q]);
+    NK(N.broadcast(links + s0[q], links + s0[q], cnt, ncclUint32, q, ctx->comm, st));
+    NK(N.broadcast(fdir + s0[q], fdir + s0[q], cnt, ncclUint8, q, ctx->comm, st));
+    NK(N.broadcast(tile_acc + s0[q], tile_acc + s0[q], cnt, nccl_type<T>(), q, ctx->comm, st));
+  }
+  NK(N.groupEnd());
+  CK(cudaEventRecord(ex1, st));
+  CK(rt.read(ctx->d_small + 1, 1));
+  r = check_status(ctx, rt.h_cnt[0] & ~ST_CYCLE, 0, false);
+  if (r != FA_OK) { cleanup(); return r; }
+  // ---- phase B: global graph redundantly on every rank, then this strip
+  r = solve_g2<T>(ctx, gg, nslots, hbase, links, fdir, tile_acc, xT);
+  if (r == FA_OK) {
+    CK(cudaEventRecord(ctx->ev[2], st));
+    r = strip_finish<T, WK>(ctx, s, xT);
+  }
+  if (r != FA_OK) { cleanup(); return r; }
+  NK(N.allReduce(ctx->d_small + 1, ctx->d_small + 1, 1, ncclUint32, ncclMax, ctx->comm, st));
+  CK(cudaEventRecord(ctx->ev[3], st));
+  cleanup();
+  CK(rt.read(ctx->d_small + 1, 1));
+  r = check_status(ctx, rt.h_cnt[0], 0, false);
+  float exm = 0;
+  cudaEventElapsedTime(&exm, ex0, ex1);
+  cudaEventDestroy(ex0);
+  cudaEventDestroy(ex1);
+  ctx->stats.ms_exchange = exm;
+  ctx->stats.bytes_exchanged = (int64_t)(nslots * (4 + 1 + sizeof(T)) + 2 * W * esz);
+  if (r != FA_OK) return r;
+  record_stats(ctx, H * W, s.g.nblocks, s.nn, nslots);
+  return FA_OK;
 }
 
 }  // namespace
@@ -417,6 +787,7 @@ fa_status fa_destroy(fa_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->st) cudaStreamSynchronize(ctx->st);
   else cudaDeviceSynchronize();
+  if (ctx->comm) fa::nccl().commDestroy(ctx->comm);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   cudaFree(ctx->d_small);
@@ -449,6 +820,7 @@ fa_status fa_flowdirs(fa_ctx* ctx, const float* dem, int64_t rows, int64_t cols,
   ctx->stats = fa_stats{};
   ctx->stats.ms_total = ctx->stats.ms_pass1 = ms;
   ctx->stats.cells = rows * cols;
+  ctx->stats.launches = 1;
   return FA_OK;
 }
 
@@ -456,7 +828,16 @@ fa_status fa_accumulate(fa_ctx* ctx, int64_t rows, int64_t cols, const float* de
                         const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc, fa_atype atype) {
   Records rec;
   if (!acc) return set_err(ctx, FA_E_ARG, "acc is NULL");
-  return accumulate_impl(ctx, rows, cols, dem, nodata, dirs, w, wtype, acc, atype, rec);
+  return accumulate_impl(ctx, rows, cols, dem, nodata, dirs, w, wtype, acc, atype, rec, 1);
+}
+
+fa_status fa_accumulate_strips(fa_ctx* ctx, int nstrips, int64_t rows, int64_t cols, const float* dem,
+                               float nodata, const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc,
+                               fa_atype atype) {
+  Records rec;
+  if (!acc) return set_err(ctx, FA_E_ARG, "acc is NULL");
+  if (nstrips < 1) return set_err(ctx, FA_E_ARG, "nstrips must be >= 1");
+  return accumulate_impl(ctx, rows, cols, dem, nodata, dirs, w, wtype, acc, atype, rec, nstrips);
 }
 
 int64_t fa_perimeter_slots(const fa_ctx* ctx, int64_t rows, int64_t cols) {
@@ -473,13 +854,65 @@ fa_status fa_perimeter_records(fa_ctx* ctx, int64_t rows, int64_t cols, const fl
   rec.links = links;
   rec.tile_acc = tile_acc;
   rec.offsets = offsets;
-  return accumulate_impl(ctx, rows, cols, dem, nodata, dirs, w, wtype, acc, atype, rec);
+  return accumulate_impl(ctx, rows, cols, dem, nodata, dirs, w, wtype, acc, atype, rec, 1);
 }
 
 fa_status fa_get_stats(const fa_ctx* ctx, fa_stats* out) {
   if (!ctx || !out) return FA_E_ARG;
   *out = ctx->stats;
   return FA_OK;
+}
+
+fa_status fa_nccl_unique_id(void* out128) {
+  if (!out128) return FA_E_ARG;
+  if (!fa::nccl().load()) return FA_E_NCCL;
+  ncclUniqueId id;
+  if (fa::nccl().getUniqueId(&id) != ncclSuccess) return FA_E_NCCL;
+  memcpy(out128, &id, sizeof(id));
+  return FA_OK;
+}
+
+fa_status fa_accumulate_dist(fa_ctx* ctx, const void* nccl_id128, int rank, int nranks, int64_t global_rows,
+                             int64_t cols, int64_t row_begin, int64_t local_rows, const float* dem, float nodata,
+                             const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc, fa_atype atype) {
+  if (!ctx) return FA_E_ARG;
+  ctx->err.clear();
+  if (!nccl_id128 || nranks < 1 || rank < 0 || rank >= nranks || global_rows <= 0 || cols <= 0 ||
+      local_rows <= 0 || row_begin < 0 || row_begin + local_rows > global_rows || !acc)
+    return set_err(ctx, FA_E_ARG, "bad arguments");
+  FS(check_types(ctx, dem, dirs, w, wtype, atype));
+  for (const void* p : {(const void*)dem, (const void*)dirs, (const void*)w, (const void*)acc})
+    if (p && !is_device_ptr(p)) return set_err(ctx, FA_E_ARG, "fa_accumulate_dist takes device buffers");
+  CK(cudaSetDevice(ctx->device));
+  fa::Nccl& N = fa::nccl();
+  if (!N.load()) return set_err(ctx, FA_E_NCCL, "cannot load libnccl.so.2");
+  if (ctx->comm && (ctx->rank != rank || ctx->nranks != nranks || memcmp(ctx->comm_id, nccl_id128, 128))) {
+    N.commDestroy(ctx->comm);
+    ctx->comm = nullptr;
+  }
+  if (!ctx->comm) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id128, sizeof(id));
+    NK(N.commInitRank(&ctx->comm, nranks, id, rank));
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+    memcpy(ctx->comm_id, nccl_id128, 128);
+  }
+  fa_status s;
+  if (atype == FA_A_U32) {
+    s = wtype == FA_W_NONE ? run_dist<uint32_t, 0>(ctx, global_rows, cols, row_begin, local_rows, dem, nodata, dirs, w, (uint32_t*)acc)
+                           : run_dist<uint32_t, 1>(ctx, global_rows, cols, row_begin, local_rows, dem, nodata, dirs, w, (uint32_t*)acc);
+  } else if (atype == FA_A_U64) {
+    using U = unsigned long long;
+    s = wtype == FA_W_NONE ? run_dist<U, 0>(ctx, global_rows, cols, row_begin, local_rows, dem, nodata, dirs, w, (U*)acc)
+                           : run_dist<U, 1>(ctx, global_rows, cols, row_begin, local_rows, dem, nodata, dirs, w, (U*)acc);
+  } else {
+    s = wtype == FA_W_NONE ? run_dist<double, 0>(ctx, global_rows, cols, row_begin, local_rows, dem, nodata, dirs, w, (double*)acc)
+                           : run_dist<double, 2>(ctx, global_rows, cols, row_begin, local_rows, dem, nodata, dirs, w, (double*)acc);
+  }
+  cudaError_t e = cudaStreamSynchronize(ctx->st);
+  if (s == FA_OK && e != cudaSuccess) return set_err(ctx, FA_E_CUDA, std::string("stream: ") + cudaGetErrorString(e));
+  return s;
 }
 
 }  // extern "C"

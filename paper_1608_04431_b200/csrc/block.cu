@@ -91,15 +91,6 @@ struct Cfg {
   __device__ static __forceinline__ int offA(int d) { return (int)(int8_t)(OFFA >> (8 * (d - 1))); }
   __device__ static __forceinline__ int hidx(int ly, int lx) { return (ly + 1) * HS + lx + 4; }
   __device__ static __forceinline__ int a2h(int i) { return hidx(i / BC, i % BC); }
-  // packed successor of a cell: target index | donor-bit position << IB |
-  // target-is-junction << (IB+3); two stop codes: leaves the block (an exit,
-  // Alg. 2 "outside the tile") / ends inside (NoFlow or in-block NoData)
-  static constexpr int IB = BN <= 1024 ? 10 : 12;
-  using Nxt = typename std::conditional<BN <= 1024, uint16_t, uint32_t>::type;
-  static constexpr uint32_t JBIT = 1u << (IB + 3);
-  static constexpr uint32_t STOP_OUT = BN <= 1024 ? 0xFFFEu : 0xFFFFFFFEu;
-  static constexpr uint32_t STOP_END = BN <= 1024 ? 0xFFFFu : 0xFFFFFFFFu;
-  static_assert(BN <= (1 << IB), "index bits");
 };
 
 template <class C>
@@ -108,7 +99,6 @@ struct __align__(16) Smem {
   uint32_t msk4[C::BN / 4];  // donor masks, one byte per cell
   uint32_t pend[C::BN / 4];  // pending-donor masks (atomicAnd)
   uint16_t src[C::BN];       // source queue (A index)
-  typename C::Nxt nxt[C::BN];  // packed successors
   uint32_t slot_nid[C::PB];
   uint32_t nsrc, qhead, cnt_exit, base, processed, ndata;
   __device__ __forceinline__ uint8_t msk(int i) const { return reinterpret_cast<const uint8_t*>(msk4)[i]; }
@@ -188,74 +178,88 @@ __device__ __forceinline__ void build_masks(Smem<C>& s, int h, int w) {
     for (int j = 0; j < 4; ++j)
       if (sb & (0x80u << (8 * j))) s.src[base++] = (uint16_t)(4 * q + j);
   }
-  __syncthreads();
-  // packed successors (needs every mask: the junction flag is the target's)
-  for (int i = threadIdx.x; i < C::BN; i += C::NT) {
-    const int ly = i / C::BC, lx = i % C::BC;
-    const int d = s.dirh[C::hidx(ly, lx)];
-    uint32_t v = C::STOP_END;  // NoFlow, NoData, ring, or drops into in-block NoData
-    if (d >= 1 && d <= 8 && ly < h && lx < w) {
-      const int ty = ly + dir_dy(d), tx = lx + dir_dx(d);
-      const int dt = s.dirh[C::hidx(ty, tx)];
-      if ((unsigned)ty >= (unsigned)h || (unsigned)tx >= (unsigned)w) {
-        v = C::STOP_OUT;  // leaves the block (possibly into NoData / off-grid): a block exit
-      } else if (dt < kOut) {
-        const int t = i + C::offA(d);
-        const uint32_t m = s.msk(t);
-        v = (uint32_t)t | ((uint32_t)((d + 3) & 7) << C::IB) | ((m & (m - 1)) ? C::JBIT : 0u);
-      }
-    }
-    s.nxt[i] = (typename C::Nxt)v;
-  }
+  (void)h;
+  (void)w;
 }
 
 // ---------------------------------------------------------------- H3
 // Walks from the shared source queue (both passes).  On entry dirh, masks,
 // pend, src/nsrc and A (= w [+ x]) are set and synced.  Returns the number of
 // cells this thread retired.
+__device__ __forceinline__ void fence_cta() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
+
 template <class C, class T>
 __device__ __forceinline__ uint32_t chain_follow(Smem<C>& s, T* A) {
   const uint32_t nsrc = s.nsrc;
   uint32_t retired = 0;
-  uint32_t nx = C::STOP_END;  // successor word of the walk's current cell
+  bool live = false;
+  int ch = 0, ca = 0, d = 0;
   T a = (T)0;
+#ifdef FA_PHASE_CLOCKS
+  uint32_t iters = 0;
+  struct Tally {
+    uint32_t& it;
+    const uint32_t& ret;
+    __device__ ~Tally() {
+      uint32_t mx = it, sm = ret;
+      for (int o = 16; o; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+        sm += __shfl_xor_sync(0xFFFFFFFFu, sm, o);
+      }
+      if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&g_phase[14], (unsigned long long)mx);
+        atomicAdd(&g_phase[15], (unsigned long long)sm);
+      }
+    }
+  } tally{iters, retired};
+#endif
   for (;;) {
-    if (nx >= C::STOP_OUT) {
-      // walk ended: take the next source (per-lane shared atomic; no warp
-      // votes, so a lane never waits for the others of its warp)
+#ifdef FA_PHASE_CLOCKS
+    ++iters;
+#endif
+    if (!live) {
+      // take the next source (per-lane shared atomic; no warp votes, so a
+      // lane never waits for the others of its warp)
       const uint32_t q = atomicAdd(&s.qhead, 1u);
       if (q >= nsrc) break;
-      const int c = s.src[q];
-      a = A[c];
-      nx = s.nxt[c];
+      ca = s.src[q];
+      ch = C::a2h(ca);
+      d = s.dirh[ch];
+      a = A[ca];
+      live = true;
       ++retired;
-      continue;
     }
-    // one step downstream: target t is an in-block data cell
-    const int t = nx & ((1u << C::IB) - 1);
-    const T at = A[t];  // w(t) [+ x(t)]: only the walk that finishes t writes A[t]
-    const uint32_t nt = s.nxt[t];
-    if (nx & C::JBIT) {
+    // one step downstream
+    if (d == kNoFlow || d > 8) { live = false; continue; }
+    const int th = ch + C::offH(d);
+    const int ta = (ca + C::offA(d)) & (C::BN - 1);  // clamped; unused when the walk stops
+    const int dt = s.dirh[th];
+    const uint32_t m = s.msk(ta);
+    const T at = A[ta];  // w(t) [+ x(t)]: only the walk that finishes t writes A[t]
+    if (dt >= kOut) { live = false; continue; }  // leaves the block, or drops into NoData (D8)
+    if ((m & (m - 1)) == 0) {
+      a = at + a;  // sole in-block donor: no atomic
+    } else {
       // junction: clear our bit; the last arrival gathers the donors
-      const uint32_t bit = 1u << ((nx >> C::IB) & 7);
-      const int sh = (t & 3) * 8;
-      __threadfence_block();  // release our value
-      const uint32_t old = atomicAnd(&s.pend[t >> 2], ~(bit << sh));
-      if (((old >> sh) & 0xFFu) != bit) { nx = C::STOP_END; continue; }  // others pending
-      __threadfence_block();  // acquire the other donors' values
-      uint32_t m = s.msk(t);
+      const uint32_t bit = 1u << ((d + 3) & 7);  // bit of the opposite direction
+      const int sh = (ta & 3) * 8;
+      fence_cta();  // release our value
+      const uint32_t old = atomicAnd(&s.pend[ta >> 2], ~(bit << sh));
+      if (((old >> sh) & 0xFFu) != bit) { live = false; continue; }  // others pending
+      fence_cta();  // acquire the other donors' values
+      uint32_t mm = m;
       T acc = at;
       do {  // donors in code order (fixed summation order)
-        const int k = __ffs(m);
-        m &= m - 1;
-        acc = acc + A[t + C::offA(k)];
-      } while (m);
+        const int k = __ffs(mm);
+        mm &= mm - 1;
+        acc = acc + A[ta + C::offA(k)];
+      } while (mm);
       a = acc;
-    } else {
-      a = at + a;  // sole in-block donor: no atomic
     }
-    A[t] = a;
-    nx = nt;
+    A[ta] = a;
+    ch = th;
+    ca = ta;
+    d = dt;
     ++retired;
   }
   return retired;
@@ -394,6 +398,7 @@ __global__ void __launch_bounds__(C::NT) k_pass1(PassArgs<T, WK> P) {
     for (int p = tid; p < C::PB; p += C::NT) P.slot_root[b * C::PB + p] = kNone;
     return;
   }
+  PH_T0;
   WPre<C, WK> pre;
   pre.load(P.w, g, y0, x0, h, w);  // in flight during staging, D8 and masks
   if (tid == 0) s.cnt_exit = s.processed = s.ndata = s.nsrc = s.qhead = 0;
@@ -405,10 +410,14 @@ __global__ void __launch_bounds__(C::NT) k_pass1(PassArgs<T, WK> P) {
       const int ly = i / rw - 1, lx = i % rw - 1;
       const int64_t gy = y0 + ly, gx = x0 + lx;
       float v = __int_as_float(0x7fc00000);
-      if (gy >= 0 && gx >= 0 && gy < g.H && gx < g.W) v = stage_z(P.dem[gy * g.W + gx], P.nodata);
+      if (gx >= 0 && gx < g.W) {
+        const float* row = gy < 0 ? P.dem_up : gy >= g.H ? P.dem_dn : P.dem + gy * g.W;
+        if (row && gy >= -1 && gy <= g.H) v = stage_z(row[gx], P.nodata);
+      }
       zs[(ly + 1) * C::ZS + lx + 1] = v;
     }
     __syncthreads();
+    PH_MARK(8);
     for (int i = tid; i < rn; i += C::NT) {
       const int ly = i / rw - 1, lx = i % rw - 1;
       const int zi = (ly + 1) * C::ZS + lx + 1;
@@ -423,6 +432,7 @@ __global__ void __launch_bounds__(C::NT) k_pass1(PassArgs<T, WK> P) {
       s.dirh[C::hidx(ly, lx)] = code;
     }
     __syncthreads();  // zs dead from here on; A aliases it
+    PH_MARK(9);
   } else {
     __syncthreads();
     load_dirs<C>(s, P.dirs_in, g, y0, x0, h, w, true, P.status);
@@ -435,7 +445,10 @@ __global__ void __launch_bounds__(C::NT) k_pass1(PassArgs<T, WK> P) {
       else { const int j = i - 2 * (w + 2); ly = j >> 1; lx = (j & 1) ? w : -1; }
       const int64_t gy = y0 + ly, gx = x0 + lx;
       uint8_t code = kNoData;
-      if (gy >= 0 && gx >= 0 && gy < g.H && gx < g.W && P.dirs_in[gy * g.W + gx] != kNoData) code = kOut;
+      if (gx >= 0 && gx < g.W) {
+        const uint8_t* row = gy < 0 ? P.dirs_up : gy >= g.H ? P.dirs_dn : P.dirs_in + gy * g.W;
+        if (row && gy >= -1 && gy <= g.H && row[gx] != kNoData) code = kOut;
+      }
       s.dirh[C::hidx(ly, lx)] = code;
     }
     __syncthreads();
@@ -443,9 +456,11 @@ __global__ void __launch_bounds__(C::NT) k_pass1(PassArgs<T, WK> P) {
   build_masks<C>(s, h, w);
   init_values<C, T, WK>(s, A, P.w, pre, g, y0, x0, h, w, P.status, P.wsum);
   __syncthreads();
+  PH_MARK(10);
   const uint32_t ret = chain_follow<C, T>(s, A);
   atomicAdd(&s.processed, ret);
   __syncthreads();
+  PH_MARK(11);
   if (tid == 0 && s.processed != s.ndata) atomicOr(P.status, ST_CYCLE);
   // ---- H4: block exits -> graph nodes (compacted), perimeter links
   const int np = (int)perim_count(h, w);
@@ -479,8 +494,8 @@ __global__ void __launch_bounds__(C::NT) k_pass1(PassArgs<T, WK> P) {
     const int64_t gy = y0 + ty, gx = x0 + tx;
     uint8_t fl = dead ? NF_DEAD : 0;
     if (gy < t0y || gx < t0x || gy >= t0y + th || gx >= t0x + tw) fl |= NF_OUT_TILE;
-    uint32_t tgt = kNone;
-    if (!dead) {
+    uint32_t tgt = kNone;  // none: dropped, or in another strip (carried by the tile records)
+    if (!dead && gy >= 0 && gy < g.H) {
       int tly, tlx;
       const int64_t tb = g.block_of(gy, gx, tly, tlx);
       int64_t by0, bx0;
@@ -495,25 +510,31 @@ __global__ void __launch_bounds__(C::NT) k_pass1(PassArgs<T, WK> P) {
     s.slot_nid[p] = nid;
   }
   __syncthreads();
+  PH_MARK(12);
   // Alg. 2 FollowPath for every block perimeter cell (root exit node or none)
   for (int p = tid; p < C::PB; p += C::NT) {
     uint32_t root = kNone;
     if (p < np) {
       int64_t cx, cy;
       perim_xy(p, h, w, cx, cy);
-      int c = (int)cy * C::BC + (int)cx;
+      int ly = (int)cy, lx = (int)cx;
       for (int steps = 0; steps <= h * w; ++steps) {
-        const uint32_t nx = s.nxt[c];
-        if (nx == C::STOP_OUT) {  // c is a block exit
-          root = s.slot_nid[perim_index(c % C::BC, c / C::BC, h, w)];
+        const int dd = s.dirh[C::hidx(ly, lx)];
+        if (dd == kNoFlow || dd > 8) break;  // FlowTerminates (NoFlow)
+        const int ny = ly + dir_dy(dd), nx = lx + dir_dx(dd);
+        if ((unsigned)ny >= (unsigned)h || (unsigned)nx >= (unsigned)w) {
+          root = s.slot_nid[perim_index(lx, ly, h, w)];  // (ly, lx) is a block exit
           break;
         }
-        if (nx == C::STOP_END) break;  // FlowTerminates (NoFlow / in-block NoData)
-        c = nx & ((1u << C::IB) - 1);
+        if (s.dirh[C::hidx(ny, nx)] == kNoData) break;  // terminates in in-block NoData
+        ly = ny;
+        lx = nx;
       }
     }
     P.slot_root[b * C::PB + p] = root;
   }
+  __syncthreads();
+  PH_MARK(13);
 }
 
 // ---------------------------------------------------------------- pass 2

@@ -199,6 +199,12 @@ struct PassArgs {
   const uint8_t* dirs_in; // pass 1 from dirs, and pass 2
   uint8_t* dirs_out;      // pass 1 from DEM: D8 output (may be null)
   const void* w;          // weights (WK: 0 none, 1 u32, 2 f32)
+  // halo rows of a row strip (H7): global rows row0-1 and row0+H, or null
+  // when the strip touches the raster edge (then those rows are off-grid)
+  const float* dem_up;
+  const float* dem_dn;
+  const uint8_t* dirs_up;
+  const uint8_t* dirs_dn;
   // pass 1 outputs
   uint32_t* node_count;
   T* node_val;

@@ -1,4 +1,5 @@
-// graph.cu -- block-exit graph G1, tile perimeter graph G2 and the offsets.
+// graph.cu -- block-exit graph G1, the tile perimeter records and the paper's
+// global perimeter graph G2.
 //
 // Nodes of G1 are the block exit cells written by pass 1 (one per block
 // perimeter cell whose direction leaves its block, Alg. 2 "FlowExternal" at
@@ -6,13 +7,25 @@
 // target cell's in-block path (slot_root), i.e. the paper's producer graph
 // ("adjoining edges (or corners)") with the entry->exit links of
 // Alg. 2 composed in.  Cutting the edges that leave a paper tile gives the
-// per-tile problem (Alg. 1 on the tile); the tile exits then form
-// G2, the paper's global flow graph.
+// per-tile problem (Alg. 1 on the tile): its solution A_T and the
+// tile roots give the tile perimeter records (F, A, L per perimeter cell,
+// P:L213).  G2 is then built from those records exactly as the paper's
+// producer does and solved with the same forest primitive; the
+// returned offsets are the external inbound flows a_in (D11).
 #include "forest.cuh"
 
 namespace fa {
 
 namespace {
+
+__device__ __forceinline__ int64_t tile_of_slot(const int64_t* __restrict__ tbase, int64_t ntiles, int64_t s) {
+  int64_t lo = 0, hi = ntiles - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) / 2;
+    if (tbase[mid] <= s) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
 
 __global__ void k_g1_parent(uint32_t nn, const uint32_t* __restrict__ tgt,
                             const uint8_t* __restrict__ flags, const uint32_t* __restrict__ slot_root,
@@ -25,75 +38,28 @@ __global__ void k_g1_parent(uint32_t nn, const uint32_t* __restrict__ tgt,
   }
 }
 
+// x at block entry cells from the finished block exits (intra_tile: only
+// edges inside a tile; cross-tile flow then arrives through x_T)
 template <class T>
-__global__ void k_scatter_x(uint32_t nn, const uint32_t* __restrict__ tgt, const T* __restrict__ S,
-                            T* x_slot) {
+__global__ void k_scatter_x(uint32_t nn, const uint32_t* __restrict__ tgt, const uint8_t* __restrict__ flags,
+                            const T* __restrict__ S, T* x_slot, bool intra_tile) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += gridDim.x * blockDim.x) {
     const uint32_t t = tgt[v];
-    if (t != kNone) atomic_add(&x_slot[t], S[v]);
+    if (t != kNone && !(intra_tile && (flags[v] & NF_OUT_TILE))) atomic_add(&x_slot[t], S[v]);
   }
 }
 
-// G2 over tile exits: parent = tile-level root of the entry's in-tile path
-// when it is a tile exit (Alg. 2 link), else none (FlowTerminates or dead).
-// Value = A_T at FlowExternal nodes, 0 otherwise ("set to A = 0").
-template <class T>
-__global__ void k_g2(uint32_t nn, const uint32_t* __restrict__ tgt, const uint8_t* __restrict__ flags,
-                     const uint32_t* __restrict__ slot_root, const uint32_t* __restrict__ troot,
-                     const T* __restrict__ S1, uint32_t* parent2, T* val2) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += gridDim.x * blockDim.x) {
-    const uint8_t f = flags[v];
-    uint32_t p = kNone;
-    T val = (T)0;
-    if (f & NF_OUT_TILE) {
-      val = S1[v];
-      const uint32_t t = tgt[v];
-      if (t != kNone) {
-        const uint32_t g = slot_root[t];
-        if (g != kNone) {
-          const uint32_t r = troot[g];
-          if (flags[r] & NF_OUT_TILE) p = r;
-        }
-      }
-    }
-    parent2[v] = p;
-    val2[v] = val;
-  }
-}
-
-// inject the tile offsets x_T into G1 at the entry's block exit, and record
-// x_T per block slot (the paper's A' returned to each tile, read as a_in).
-template <class T>
-__global__ void k_inject(uint32_t nn, const uint32_t* __restrict__ tgt, const uint8_t* __restrict__ flags,
-                         const uint32_t* __restrict__ slot_root, const T* __restrict__ S2, T* val1,
-                         T* xT_slot) {
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += gridDim.x * blockDim.x) {
-    if (!(flags[v] & NF_OUT_TILE)) continue;
-    const uint32_t t = tgt[v];
-    if (t == kNone) continue;
-    const T s = S2[v];
-    if (xT_slot) atomic_add(&xT_slot[t], s);
-    const uint32_t g = slot_root[t];
-    if (g != kNone) atomic_add(&val1[g], s);
-  }
-}
-
-// H4 tile perimeter records (links, A_T, x_T) for every tile perimeter slot
+// H4 tile perimeter records of one strip: F (direction), L (Alg. 2 link) and
+// A_T (tile-local accumulation, at FlowExternal slots) per tile perimeter slot
 template <class T>
 __global__ void k_tile_records(Geom g, int64_t nslots, const int64_t* __restrict__ tbase,
                                const uint8_t* __restrict__ dirs, const uint32_t* __restrict__ slot_root,
                                const uint32_t* __restrict__ troot, const uint8_t* __restrict__ flags,
                                const uint32_t* __restrict__ node_slot, const T* __restrict__ S1,
-                               const T* __restrict__ xT_slot, uint32_t* links, T* tile_acc, T* offs) {
+                               uint32_t* links, uint8_t* fdir, T* tile_acc) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots;
        s += (int64_t)gridDim.x * blockDim.x) {
-    // tile of slot s: binary search in tbase
-    int64_t lo = 0, hi = g.TR * g.TC - 1;
-    while (lo < hi) {
-      int64_t mid = (lo + hi + 1) / 2;
-      if (tbase[mid] <= s) lo = mid; else hi = mid - 1;
-    }
-    const int64_t t = lo, p = s - tbase[t];
+    const int64_t t = tile_of_slot(tbase, g.TR * g.TC, s), p = s - tbase[t];
     int64_t ty0, tx0, th, tw, px, py;
     g.tile_box(t, ty0, tx0, th, tw);
     perim_xy(p, th, tw, px, py);
@@ -105,34 +71,107 @@ __global__ void k_tile_records(Geom g, int64_t nslots, const int64_t* __restrict
     int bh, bw;
     g.block_box(b, by0, bx0, bh, bw);
     const int64_t bslot = b * g.pb + perim_index(lx, ly, bh, bw);
-    uint32_t L = kFlowTerminates;
+    uint32_t L = kFlowTerminates;  // Alg. 2: NoData / NoFlow / path ends inside
     T at = (T)0;
     if (d >= 1 && d <= 8) {
       const int64_t ny = py + dir_dy(d), nx = px + dir_dx(d);
+      const uint32_t e = slot_root[bslot];
       if (ny < 0 || nx < 0 || ny >= th || nx >= tw) {
-        L = kFlowExternal;
-        const uint32_t e = slot_root[bslot];  // the cell is its own block exit
-        if (e != kNone) at = S1[e];
-      } else {
-        const uint32_t e = slot_root[bslot];
-        if (e != kNone) {
-          const uint32_t r = troot[e];
-          if (flags[r] & NF_OUT_TILE) {
-            const uint32_t rs = node_slot[r];
-            const int64_t rb = rs / g.pb, rp = rs % g.pb;
-            int64_t ry0, rx0;
-            int rh, rw;
-            g.block_box(rb, ry0, rx0, rh, rw);
-            int64_t rx, ryy;
-            perim_xy(rp, rh, rw, rx, ryy);
-            L = (uint32_t)perim_index(rx0 + rx - tx0, ry0 + ryy - ty0, th, tw);
-          }
+        L = kFlowExternal;  // "c_n is outside the tile" and c = c0 (D22)
+        if (e != kNone) at = S1[e];  // the cell is its own block exit
+      } else if (e != kNone) {
+        const uint32_t r = troot[e];
+        if (flags[r] & NF_OUT_TILE) {  // the path leaves the tile at exit r
+          const uint32_t rs = node_slot[r];
+          const int64_t rb = rs / g.pb, rp = rs % g.pb;
+          int64_t ry0, rx0;
+          int rh, rw;
+          g.block_box(rb, ry0, rx0, rh, rw);
+          int64_t rx, ryy;
+          perim_xy(rp, rh, rw, rx, ryy);
+          L = (uint32_t)perim_index(rx0 + rx - tx0, ry0 + ryy - ty0, th, tw);
         }
       }
     }
-    if (links) links[s] = L;
-    if (tile_acc) tile_acc[s] = at;
-    if (offs) offs[s] = xT_slot ? xT_slot[bslot] : (T)0;
+    links[s] = L;
+    fdir[s] = d;
+    tile_acc[s] = at;
+  }
+}
+
+// G2, the producer's global flow graph over every tile perimeter slot of the
+// whole raster: a FlowExternal slot drains into the adjoining
+// tile's perimeter cell (edges or corners) unless that is NoData or off the
+// DEM; a linked slot drains into its exit; the value is A_T at FlowExternal
+// slots and 0 elsewhere ("set to A = 0").
+template <class T>
+__global__ void k_g2_slots(Geom gg, int64_t nslots, const int64_t* __restrict__ tbase,
+                           const uint32_t* __restrict__ links, const uint8_t* __restrict__ fdir,
+                           const T* __restrict__ tile_acc, uint32_t* parent, T* val) {
+  const int64_t ntiles = gg.TR * gg.TC;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t L = links[s];
+    uint32_t par = kNone;
+    T v = (T)0;
+    if (L == kFlowExternal) {
+      v = tile_acc[s];
+      const int64_t t = tile_of_slot(tbase, ntiles, s), p = s - tbase[t];
+      int64_t ty0, tx0, th, tw, px, py;
+      gg.tile_box(t, ty0, tx0, th, tw);
+      perim_xy(p, th, tw, px, py);
+      const int d = fdir[s];
+      const int64_t ny = ty0 + py + dir_dy(d), nx = tx0 + px + dir_dx(d);
+      if (ny >= 0 && nx >= 0 && ny < gg.H && nx < gg.W) {
+        const int64_t t2 = (ny / gg.TH) * gg.TC + nx / gg.TW;
+        int64_t y2, x2, h2, w2;
+        gg.tile_box(t2, y2, x2, h2, w2);
+        const int64_t s2 = tbase[t2] + perim_index(nx - x2, ny - y2, h2, w2);
+        if (fdir[s2] != kNoData) par = (uint32_t)s2;
+      }
+    } else if (L != kFlowTerminates) {
+      const int64_t t = tile_of_slot(tbase, ntiles, s);
+      par = (uint32_t)(tbase[t] + L);
+    }
+    parent[s] = par;
+    val[s] = v;
+  }
+}
+
+// offsets x_T(u) = sum of S over FlowExternal slots draining into u (a_in)
+template <class T>
+__global__ void k_xT(int64_t nslots, const uint32_t* __restrict__ parent, const uint32_t* __restrict__ links,
+                     const T* __restrict__ S2, T* xT) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = parent[s];
+    if (u != kNone && links[s] == kFlowExternal) atomic_add(&xT[u], S2[s]);
+  }
+}
+
+// inject the offsets of a strip's tile slots: into pass 2 at the entry cell,
+// and into the tile-cut block-exit graph at the exit its in-block path reaches
+template <class T>
+__global__ void k_inject_slots(Geom g, int64_t nslots, const int64_t* __restrict__ tbase,
+                               const T* __restrict__ xT, const uint32_t* __restrict__ slot_root, T* val1,
+                               T* x_slot) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const T x = xT[s];
+    if (x == (T)0) continue;
+    const int64_t t = tile_of_slot(tbase, g.TR * g.TC, s), p = s - tbase[t];
+    int64_t ty0, tx0, th, tw, px, py;
+    g.tile_box(t, ty0, tx0, th, tw);
+    perim_xy(p, th, tw, px, py);
+    int ly, lx;
+    const int64_t b = g.block_of(ty0 + py, tx0 + px, ly, lx);
+    int64_t by0, bx0;
+    int bh, bw;
+    g.block_box(b, by0, bx0, bh, bw);
+    const int64_t bslot = b * g.pb + perim_index(lx, ly, bh, bw);
+    atomic_add(&x_slot[bslot], x);
+    const uint32_t e = slot_root[bslot];
+    if (e != kNone) atomic_add(&val1[e], x);
   }
 }
 
@@ -145,23 +184,9 @@ cudaError_t launch_g1_parent(cudaStream_t st, uint32_t nn, const uint32_t* tgt, 
 }
 
 template <class T>
-cudaError_t launch_scatter_x(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const T* S, T* x_slot) {
-  k_scatter_x<T><<<grid_for(nn), 256, 0, st>>>(nn, tgt, S, x_slot);
-  return cudaGetLastError();
-}
-
-template <class T>
-cudaError_t launch_g2(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
-                      const uint32_t* slot_root, const uint32_t* troot, const T* S1, uint32_t* parent2,
-                      T* val2) {
-  k_g2<T><<<grid_for(nn), 256, 0, st>>>(nn, tgt, flags, slot_root, troot, S1, parent2, val2);
-  return cudaGetLastError();
-}
-
-template <class T>
-cudaError_t launch_inject(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
-                          const uint32_t* slot_root, const T* S2, T* val1, T* xT_slot) {
-  k_inject<T><<<grid_for(nn), 256, 0, st>>>(nn, tgt, flags, slot_root, S2, val1, xT_slot);
+cudaError_t launch_scatter_x(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
+                             const T* S, T* x_slot, bool intra_tile) {
+  k_scatter_x<T><<<grid_for(nn), 256, 0, st>>>(nn, tgt, flags, S, x_slot, intra_tile);
   return cudaGetLastError();
 }
 
@@ -169,22 +194,51 @@ template <class T>
 cudaError_t launch_tile_records(cudaStream_t st, const Geom& g, int64_t nslots, const int64_t* tbase,
                                 const uint8_t* dirs, const uint32_t* slot_root, const uint32_t* troot,
                                 const uint8_t* flags, const uint32_t* node_slot, const T* S1,
-                                const T* xT_slot, uint32_t* links, T* tile_acc, T* offs) {
+                                uint32_t* links, uint8_t* fdir, T* tile_acc) {
+  if (nslots <= 0) return cudaSuccess;
   k_tile_records<T><<<grid_for(nslots), 256, 0, st>>>(g, nslots, tbase, dirs, slot_root, troot, flags,
-                                                       node_slot, S1, xT_slot, links, tile_acc, offs);
+                                                       node_slot, S1, links, fdir, tile_acc);
   return cudaGetLastError();
 }
 
-#define FA_INST(T)                                                                                 \
-  template cudaError_t launch_scatter_x<T>(cudaStream_t, uint32_t, const uint32_t*, const T*, T*); \
-  template cudaError_t launch_g2<T>(cudaStream_t, uint32_t, const uint32_t*, const uint8_t*,       \
-                                    const uint32_t*, const uint32_t*, const T*, uint32_t*, T*);    \
-  template cudaError_t launch_inject<T>(cudaStream_t, uint32_t, const uint32_t*, const uint8_t*,   \
-                                        const uint32_t*, const T*, T*, T*);                        \
-  template cudaError_t launch_tile_records<T>(cudaStream_t, const Geom&, int64_t, const int64_t*,  \
-                                              const uint8_t*, const uint32_t*, const uint32_t*,    \
-                                              const uint8_t*, const uint32_t*, const T*, const T*, \
-                                              uint32_t*, T*, T*);
+template <class T>
+cudaError_t launch_g2_slots(cudaStream_t st, const Geom& gg, int64_t nslots, const int64_t* tbase,
+                            const uint32_t* links, const uint8_t* fdir, const T* tile_acc, uint32_t* parent,
+                            T* val) {
+  if (nslots <= 0) return cudaSuccess;
+  k_g2_slots<T><<<grid_for(nslots), 256, 0, st>>>(gg, nslots, tbase, links, fdir, tile_acc, parent, val);
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_xT(cudaStream_t st, int64_t nslots, const uint32_t* parent, const uint32_t* links,
+                      const T* S2, T* xT) {
+  if (nslots <= 0) return cudaSuccess;
+  k_xT<T><<<grid_for(nslots), 256, 0, st>>>(nslots, parent, links, S2, xT);
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_inject_slots(cudaStream_t st, const Geom& g, int64_t nslots, const int64_t* tbase,
+                                const T* xT, const uint32_t* slot_root, T* val1, T* x_slot) {
+  if (nslots <= 0) return cudaSuccess;
+  k_inject_slots<T><<<grid_for(nslots), 256, 0, st>>>(g, nslots, tbase, xT, slot_root, val1, x_slot);
+  return cudaGetLastError();
+}
+
+#define FA_INST(T)                                                                                  \
+  template cudaError_t launch_scatter_x<T>(cudaStream_t, uint32_t, const uint32_t*, const uint8_t*,  \
+                                           const T*, T*, bool);                                     \
+  template cudaError_t launch_tile_records<T>(cudaStream_t, const Geom&, int64_t, const int64_t*,   \
+                                              const uint8_t*, const uint32_t*, const uint32_t*,     \
+                                              const uint8_t*, const uint32_t*, const T*, uint32_t*, \
+                                              uint8_t*, T*);                                        \
+  template cudaError_t launch_g2_slots<T>(cudaStream_t, const Geom&, int64_t, const int64_t*,       \
+                                          const uint32_t*, const uint8_t*, const T*, uint32_t*, T*); \
+  template cudaError_t launch_xT<T>(cudaStream_t, int64_t, const uint32_t*, const uint32_t*, const T*, \
+                                    T*);                                                            \
+  template cudaError_t launch_inject_slots<T>(cudaStream_t, const Geom&, int64_t, const int64_t*,   \
+                                              const T*, const uint32_t*, T*, T*);
 FA_INST(uint32_t)
 FA_INST(unsigned long long)
 FA_INST(double)

@@ -25,8 +25,18 @@ FLOW_EXTERNAL = 0xFFFFFFFE
 FLOW_TERMINATES = 0xFFFFFFFF
 
 EXPORTS = ["fa_create", "fa_destroy", "fa_last_error", "fa_flowdirs", "fa_accumulate",
-           "fa_perimeter_slots", "fa_perimeter_records", "fa_nccl_unique_id", "fa_accumulate_dist",
-           "fa_get_stats"]
+           "fa_accumulate_strips", "fa_perimeter_slots", "fa_perimeter_records", "fa_nccl_unique_id",
+           "fa_accumulate_dist", "fa_get_stats"]
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL id for fa_accumulate_dist (rank 0 creates, all ranks receive)."""
+    lib = load()
+    buf = ctypes.create_string_buffer(128)
+    st = lib.fa_nccl_unique_id(buf)
+    if st != FA_OK:
+        raise FaError(st, "fa_nccl_unique_id failed")
+    return buf.raw
 
 
 class FaError(RuntimeError):
@@ -65,6 +75,7 @@ def load() -> ctypes.CDLL:
     lib.fa_last_error.restype = ctypes.c_char_p
     lib.fa_flowdirs.argtypes = [P, P, I, I, F, P]
     lib.fa_accumulate.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int]
+    lib.fa_accumulate_strips.argtypes = [P, ctypes.c_int, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int]
     lib.fa_perimeter_slots.argtypes = [P, I, I]
     lib.fa_perimeter_slots.restype = I
     lib.fa_perimeter_records.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, ctypes.c_int, P, P, P, P]
@@ -166,6 +177,32 @@ class Context:
                 out = np.empty((rows, cols), {A_U32: np.uint32, A_U64: np.uint64, A_F64: np.float64}[a])
         self._check(self.lib.fa_accumulate(self.h, rows, cols, _ptr(dem), float(nodata), _ptr(dirs),
                                            _ptr(w), _wtype(w), _ptr(out), a))
+        return out
+
+    def accumulate_strips(self, nstrips: int, dem=None, dirs=None, w=None, atype: str = "u32",
+                          nodata: float = -9999.0, out=None):
+        """The multi-GPU strip pipeline (H4-H7) run as `nstrips` strips on this device."""
+        src = dem if dem is not None else dirs
+        rows, cols = src.shape
+        a = ATYPES[atype]
+        if out is None:
+            out = torch.empty((rows, cols), dtype=TORCH_ACC[a], device=src.device)
+        self._check(self.lib.fa_accumulate_strips(self.h, int(nstrips), rows, cols, _ptr(dem), float(nodata),
+                                                  _ptr(dirs), _ptr(w), _wtype(w), _ptr(out), a))
+        return out
+
+    def accumulate_dist(self, nccl_id: bytes, rank: int, nranks: int, global_rows: int, row_begin: int,
+                        dem=None, dirs=None, w=None, atype: str = "u32", nodata: float = -9999.0, out=None):
+        """One rank's strip of the multi-GPU accumulation (collective over all ranks)."""
+        src = dem if dem is not None else dirs
+        rows, cols = src.shape
+        a = ATYPES[atype]
+        if out is None:
+            out = torch.empty((rows, cols), dtype=TORCH_ACC[a], device=src.device)
+        buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        self._check(self.lib.fa_accumulate_dist(self.h, buf, rank, nranks, global_rows, cols, row_begin, rows,
+                                                _ptr(dem), float(nodata), _ptr(dirs), _ptr(w), _wtype(w),
+                                                _ptr(out), a))
         return out
 
     def perimeter_slots(self, rows: int, cols: int) -> int:

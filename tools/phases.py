@@ -11,7 +11,8 @@ import torch  # noqa: E402
 import inputs  # noqa: E402
 from paper_1608_04431_b200 import fa  # noqa: E402
 
-NAMES = ["stage dirs", "masks+succ", "init w", "inject x", "walks", "write A"]
+NAMES = ["stage dirs", "masks", "init w", "inject x", "walks", "write A"]
+NAMES1 = ["stage z", "D8", "masks+init", "walks", "exit nodes", "perim walks"]
 
 
 def main():
@@ -34,11 +35,15 @@ def main():
             ctx.accumulate(w=w, atype=cfg.atype, **kw)
             st = ctx.stats()
             dbg(buf, 1)
-        tot = sum(buf[i] for i in range(6)) or 1
         nb = st["blocks"]
-        print(f"{shape}: pass2 {st['ms_pass2']:.2f} ms, {nb} blocks; mean cycles/block per phase:")
-        for i, n in enumerate(NAMES):
-            print(f"   {n:12s} {buf[i] / nb:10.0f}  ({buf[i] / tot * 100:4.1f}%)")
+        for title, idx, names, ms in (("pass1", range(8, 14), NAMES1, st["ms_pass1"]),
+                                      ("pass2", range(0, 6), NAMES, st["ms_pass2"])):
+            tot = sum(buf[i] for i in idx) or 1
+            print(f"{shape}: {title} {ms:.2f} ms, {nb} blocks; mean cycles/block per phase:")
+            for i, n in zip(idx, names):
+                print(f"   {n:12s} {buf[i] / nb:10.0f}  ({buf[i] / tot * 100:4.1f}%)")
+        print(f"   walk loop: sum over warps of max lane iterations {buf[14]}, lane-steps {buf[15]}"
+              f" -> lane efficiency {buf[15] / max(1, 32 * buf[14]) * 100:.1f}%")
 
 
 if __name__ == "__main__":
