@@ -30,6 +30,15 @@ template <class T, int WK>
 cudaError_t launch_pass1(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t st);
 template <class T, int WK>
 cudaError_t launch_pass2(const PassArgs<T, WK>& a, cudaStream_t st);
+template <class T>
+cudaError_t launch_retain(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st);
+// RETAIN (default): pass 1 stores the block-local accumulation in the output
+// and the finalize only walks the entry paths; FA_EVICT=1 selects EVICT
+// (pass 2 recomputes the block accumulation with w + x).  P:L79-81, L279-284.
+inline bool use_retain() {
+  const char* e = getenv("FA_EVICT");
+  return !(e && e[0] == '1');
+}
 cudaError_t launch_d8(const float* dem, int64_t H, int64_t W, float nodata, uint8_t* dirs,
                       cudaStream_t st);
 cudaError_t launch_g1_parent(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
@@ -282,6 +291,7 @@ fa::PassArgs<T, WK> pass_args(fa_ctx* ctx, Strip<T>& s) {
   a.slot_root = s.slot_root;
   a.x_slot = s.x_slot;
   a.acc = s.acc;
+  a.retain = s.acc != nullptr && fa::use_retain();
   return a;
 }
 
@@ -389,7 +399,8 @@ fa_status strip_finish(fa_ctx* ctx, Strip<T>& s, const T* xT_global) {
   CK(launch_scatter_x<T>(st, s.nn, s.node_tgt, s.node_flags, s.S, s.x_slot, true));
   ++rt.launches;
   if (s.acc) {
-    CK(launch_pass2<T, WK>(pass_args<T, WK>(ctx, s), st));
+    if (use_retain()) CK(launch_retain<T>(s.g, s.x_slot, s.dirs_in(), s.acc, st));
+    else CK(launch_pass2<T, WK>(pass_args<T, WK>(ctx, s), st));
     ++rt.launches;
   }
   return FA_OK;
@@ -474,7 +485,8 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
     ++rt.launches;
     if (rt.err) { s.release(rt); return set_err(ctx, FA_E_CUDA, cudaGetErrorString(rt.err)); }
     CK(cudaEventRecord(ctx->ev[2], st));
-    CK(launch_pass2<T, WK>(pass_args<T, WK>(ctx, s), st));
+    if (use_retain()) CK(launch_retain<T>(s.g, s.x_slot, s.dirs_in(), s.acc, st));
+    else CK(launch_pass2<T, WK>(pass_args<T, WK>(ctx, s), st));
     ++rt.launches;
     CK(cudaEventRecord(ctx->ev[3], st));
     s.release(rt);

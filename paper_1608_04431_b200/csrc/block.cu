@@ -381,6 +381,32 @@ __device__ __forceinline__ void init_values(Smem<C>& s, T* A, const void* wp, co
   atomicAdd(&s.ndata, nd);
 }
 
+// write the block's values A (NoData marker D9), 16-byte stores when aligned
+template <class C, class T>
+__device__ __forceinline__ void write_block(const Smem<C>& s, const T* A, T* out, const Geom& g, int64_t y0,
+                                            int64_t x0, int h, int w) {
+  constexpr int V = 16 / sizeof(T);  // cells per 16-byte store
+  const bool vec = w == C::BC && ((x0 % V) == 0) && ((g.W % V) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  if (vec) {
+    for (int q = threadIdx.x; q < h * (C::BC / V); q += C::NT) {
+      const int ly = q / (C::BC / V), lx = (q % (C::BC / V)) * V;
+      alignas(16) T v[V];
+#pragma unroll
+      for (int j = 0; j < V; ++j)
+        v[j] = s.dirh[C::hidx(ly, lx + j)] == kNoData ? AccT<T>::marker() : A[ly * C::BC + lx + j];
+      *reinterpret_cast<uint4*>(out + (y0 + ly) * g.W + x0 + lx) = *reinterpret_cast<const uint4*>(v);
+    }
+  } else {
+    for (int i = threadIdx.x; i < h * C::BC; i += C::NT) {
+      const int ly = i / C::BC, lx = i % C::BC;
+      if (lx >= w) continue;
+      const bool nodata = s.dirh[C::hidx(ly, lx)] == kNoData;
+      out[(y0 + ly) * g.W + x0 + lx] = nodata ? AccT<T>::marker() : A[i];
+    }
+  }
+}
+
 // ---------------------------------------------------------------- pass 1
 template <class C, class T, int WK, bool FROM_DEM>
 __global__ void __launch_bounds__(C::NT) k_pass1(PassArgs<T, WK> P) {
@@ -462,6 +488,9 @@ __global__ void __launch_bounds__(C::NT) k_pass1(PassArgs<T, WK> P) {
   __syncthreads();
   PH_MARK(11);
   if (tid == 0 && s.processed != s.ndata) atomicOr(P.status, ST_CYCLE);
+  // RETAIN: the block-local accumulation goes straight to the output;
+  // pass 2 then only adds the offsets along the entry paths (k_retain)
+  if (P.retain) write_block<C, T>(s, A, P.acc, g, y0, x0, h, w);
   // ---- H4: block exits -> graph nodes (compacted), perimeter links
   const int np = (int)perim_count(h, w);
   for (int p = tid; p < C::PB; p += C::NT) {
@@ -581,30 +610,63 @@ __global__ void __launch_bounds__(C::NT) k_pass2(PassArgs<T, WK> P) {
   __syncthreads();
   PH_MARK(4);
   if (tid == 0 && s.processed != s.ndata) atomicOr(P.status, ST_CYCLE);
-  // ---- write A (NoData marker D9), vectorised when aligned
-  T* out = P.acc;
-  constexpr int V = 16 / sizeof(T);  // cells per 16-byte store
-  const bool vec = w == C::BC && ((x0 % V) == 0) && ((g.W % V) == 0) &&
-                   ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-  if (vec) {
-    for (int q = tid; q < h * (C::BC / V); q += C::NT) {
-      const int ly = q / (C::BC / V), lx = (q % (C::BC / V)) * V;
-      alignas(16) T v[V];
-#pragma unroll
-      for (int j = 0; j < V; ++j)
-        v[j] = s.dirh[C::hidx(ly, lx + j)] == kNoData ? AccT<T>::marker() : A[ly * C::BC + lx + j];
-      *reinterpret_cast<uint4*>(out + (y0 + ly) * g.W + x0 + lx) = *reinterpret_cast<const uint4*>(v);
-    }
-  } else {
-    for (int i = tid; i < h * C::BC; i += C::NT) {
-      const int ly = i / C::BC, lx = i % C::BC;
-      if (lx >= w) continue;
-      const bool nodata = s.dirh[C::hidx(ly, lx)] == kNoData;
-      out[(y0 + ly) * g.W + x0 + lx] = nodata ? AccT<T>::marker() : A[i];
-    }
-  }
+  write_block<C, T>(s, A, P.acc, g, y0, x0, h, w);
   PH_MARK(5);
 }
+
+// ---------------------------------------------------------------- RETAIN finalize
+// "add A' to every cell in its downstream flow path" (Alg. 3): one
+// thread per block entry slot with a non-zero offset x walks the entry's
+// in-block path, adding x to every cell up to the block exit (or the NoFlow
+// terminal; flow into NoData is dropped).  acc already holds the block-local
+// accumulation written by pass 1, so A = A_blk + sum of the offsets whose path
+// passes the cell (linearity, D12).  Offsets on shared path segments sum.
+template <class T>
+__global__ void __launch_bounds__(256) k_retain(Geom g, const T* __restrict__ x_slot,
+                                                const uint8_t* __restrict__ dirs, T* acc) {
+  const int64_t nslots = g.nblocks * g.pb;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const T x = x_slot[s];
+    if (x == (T)0) continue;
+    const int64_t b = s / g.pb, p = s % g.pb;
+    int64_t y0, x0;
+    int h, w;
+    g.block_box(b, y0, x0, h, w);
+    if (p >= perim_count(h, w)) continue;
+    int64_t px, py;
+    perim_xy(p, h, w, px, py);
+    int ly = (int)py, lx = (int)px;
+    int64_t gi = (y0 + ly) * g.W + x0 + lx;
+    int d = __ldg(dirs + gi);
+    for (int steps = 0; steps <= h * w; ++steps) {
+      atomic_add(&acc[gi], x);
+      if (d == kNoFlow || d > 8) break;
+      const int ny = ly + dir_dy(d), nx = lx + dir_dx(d);
+      if ((unsigned)ny >= (unsigned)h || (unsigned)nx >= (unsigned)w) break;  // leaves the block
+      const int64_t ni = gi + dir_dy(d) * g.W + dir_dx(d);
+      const int nd = __ldg(dirs + ni);
+      if (nd == kNoData) break;  // dropped (D8)
+      ly = ny;
+      lx = nx;
+      gi = ni;
+      d = nd;
+    }
+  }
+}
+
+template <class T>
+cudaError_t launch_retain(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st) {
+  const int64_t n = g.nblocks * g.pb;
+  int64_t grid = (n + 255) / 256;
+  if (grid > 148 * 32) grid = 148 * 32;
+  k_retain<T><<<(unsigned)(grid < 1 ? 1 : grid), 256, 0, st>>>(g, x_slot, dirs, acc);
+  return cudaGetLastError();
+}
+template cudaError_t launch_retain<uint32_t>(const Geom&, const uint32_t*, const uint8_t*, uint32_t*, cudaStream_t);
+template cudaError_t launch_retain<unsigned long long>(const Geom&, const unsigned long long*, const uint8_t*,
+                                                       unsigned long long*, cudaStream_t);
+template cudaError_t launch_retain<double>(const Geom&, const double*, const uint8_t*, double*, cudaStream_t);
 
 // ---------------------------------------------------------------- launchers
 template <class C, class T, int WK>

@@ -217,6 +217,7 @@ struct PassArgs {
   const T* x_slot;
   T* acc;
   uint32_t* status;
+  bool retain;  // pass 1 writes the block-local accumulation into acc (RETAIN)
 };
 
 // warp-aggregated append of `v` (if pred) to list[*count]
