@@ -431,31 +431,86 @@ __global__ void __launch_bounds__(C::NT) k_pass1(PassArgs<T, WK> P) {
   init_dirh(s);
   if (FROM_DEM) {
     // ---- stage z with its halo (NoData and off-grid -> NaN), then D8 (H1)
-    const int rw = w + 2, rn = (h + 2) * (w + 2);
-    for (int i = tid; i < rn; i += C::NT) {
-      const int ly = i / rw - 1, lx = i % rw - 1;
-      const int64_t gy = y0 + ly, gx = x0 + lx;
-      float v = __int_as_float(0x7fc00000);
-      if (gx >= 0 && gx < g.W) {
-        const float* row = gy < 0 ? P.dem_up : gy >= g.H ? P.dem_dn : P.dem + gy * g.W;
-        if (row && gy >= -1 && gy <= g.H) v = stage_z(row[gx], P.nodata);
+    // full, aligned blocks: each window row = BC/4 float4 loads + 2 halo
+    // scalars; otherwise one scalar per cell (compile-time strides only)
+    const bool zvec = w == C::BC && ((x0 & 3) == 0) && ((g.W & 3) == 0) &&
+                      ((reinterpret_cast<uintptr_t>(P.dem) & 15) == 0) &&
+                      (!P.dem_up || (reinterpret_cast<uintptr_t>(P.dem_up) & 15) == 0) &&
+                      (!P.dem_dn || (reinterpret_cast<uintptr_t>(P.dem_dn) & 15) == 0);
+    if (zvec) {
+      constexpr int Q = C::BC / 4 + 2;  // per window row: BC/4 quads + 2 halo cells
+      for (int i = tid; i < (C::BR + 2) * Q; i += C::NT) {
+        const int r = i / Q, k = i % Q, ly = r - 1;
+        const int64_t gy = y0 + ly;
+        const float* row = (ly > h) ? nullptr
+                           : gy < 0 ? (gy == -1 ? P.dem_up : nullptr)
+                           : gy >= g.H ? (gy == g.H ? P.dem_dn : nullptr)
+                                       : P.dem + gy * g.W;
+        float* zrow = zs + r * C::ZS;
+        if (k < C::BC / 4) {
+          float4 v = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
+                                 __int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
+          if (row) {
+            v = __ldg(reinterpret_cast<const float4*>(row + x0) + k);
+            v.x = stage_z(v.x, P.nodata); v.y = stage_z(v.y, P.nodata);
+            v.z = stage_z(v.z, P.nodata); v.w = stage_z(v.w, P.nodata);
+          }
+          zrow[1 + 4 * k] = v.x; zrow[2 + 4 * k] = v.y; zrow[3 + 4 * k] = v.z; zrow[4 + 4 * k] = v.w;
+        } else {
+          const int lx = k == C::BC / 4 ? -1 : C::BC;
+          const int64_t gx = x0 + lx;
+          float v = __int_as_float(0x7fc00000);
+          if (row && gx >= 0 && gx < g.W) v = stage_z(row[gx], P.nodata);
+          zrow[lx + 1] = v;
+        }
       }
-      zs[(ly + 1) * C::ZS + lx + 1] = v;
+    } else {
+      for (int i = tid; i < C::ZN; i += C::NT) {
+        const int ly = i / C::ZS - 1, lx = i % C::ZS - 1;
+        float v = __int_as_float(0x7fc00000);
+        if (ly <= h && lx <= w) {
+          const int64_t gy = y0 + ly, gx = x0 + lx;
+          if (gx >= 0 && gx < g.W) {
+            const float* row = gy < 0 ? P.dem_up : gy >= g.H ? P.dem_dn : P.dem + gy * g.W;
+            if (row && gy >= -1 && gy <= g.H) v = stage_z(row[gx], P.nodata);
+          }
+        }
+        zs[i] = v;
+      }
     }
     __syncthreads();
     PH_MARK(8);
-    for (int i = tid; i < rn; i += C::NT) {
-      const int ly = i / rw - 1, lx = i % rw - 1;
-      const int zi = (ly + 1) * C::ZS + lx + 1;
-      const bool inner = ly >= 0 && lx >= 0 && ly < h && lx < w;
-      uint8_t code;
-      if (inner) {
-        code = d8_code<C::ZS>(zs, zi);
-        if (P.dirs_out) P.dirs_out[(y0 + ly) * g.W + x0 + lx] = code;
-      } else {
-        code = isnan(zs[zi]) ? kNoData : kOut;
+    // D8 for the block's cells, 4 per thread: one 32-bit shared store and one
+    // 32-bit global store of the packed codes
+    for (int q = tid; q < C::BN / 4; q += C::NT) {
+      const int ly = (4 * q) / C::BC, lx = (4 * q) % C::BC;
+      if (ly >= h) continue;
+      uint32_t packed = 0xFFFFFFFFu;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (lx + j < w) {
+          const uint32_t code = d8_code<C::ZS>(zs, (ly + 1) * C::ZS + lx + j + 1);
+          packed = (packed & ~(0xFFu << (8 * j))) | (code << (8 * j));
+        }
+      *reinterpret_cast<uint32_t*>(&s.dirh[C::hidx(ly, lx)]) = packed;
+      if (P.dirs_out) {
+        uint8_t* dst = P.dirs_out + (y0 + ly) * g.W + x0 + lx;
+        if (lx + 3 < w && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
+          *reinterpret_cast<uint32_t*>(dst) = packed;
+        } else {
+          for (int j = 0; j < 4 && lx + j < w; ++j) dst[j] = (uint8_t)(packed >> (8 * j));
+        }
       }
-      s.dirh[C::hidx(ly, lx)] = code;
+    }
+    __syncthreads();
+    // halo ring: NoData-ness only (after the packed stores, which may cover it)
+    const int rn = 2 * (w + 2) + 2 * h;
+    for (int i = tid; i < rn; i += C::NT) {
+      int ly, lx;
+      if (i < w + 2) { ly = -1; lx = i - 1; }
+      else if (i < 2 * (w + 2)) { ly = h; lx = i - (w + 2) - 1; }
+      else { const int j = i - 2 * (w + 2); ly = j >> 1; lx = (j & 1) ? w : -1; }
+      s.dirh[C::hidx(ly, lx)] = isnan(zs[(ly + 1) * C::ZS + lx + 1]) ? kNoData : kOut;
     }
     __syncthreads();  // zs dead from here on; A aliases it
     PH_MARK(9);
@@ -629,11 +684,11 @@ __global__ void __launch_bounds__(256) k_retain(Geom g, const T* __restrict__ x_
        s += (int64_t)gridDim.x * blockDim.x) {
     const T x = x_slot[s];
     if (x == (T)0) continue;
-    const int64_t b = s / g.pb, p = s % g.pb;
+    const uint32_t b = (uint32_t)s / (uint32_t)g.pb, p = (uint32_t)s - b * (uint32_t)g.pb;
     int64_t y0, x0;
     int h, w;
     g.block_box(b, y0, x0, h, w);
-    if (p >= perim_count(h, w)) continue;
+    if (p >= (uint32_t)perim_count(h, w)) continue;
     int64_t px, py;
     perim_xy(p, h, w, px, py);
     int ly = (int)py, lx = (int)px;

@@ -66,33 +66,35 @@ struct Geom {
   int br, bc, pb;    // block shape and perimeter slots per block (2(br+bc)-4)
   int nw;            // warps per block kernel CTA
 
+  // Block / tile arithmetic in 32 bits (rows, columns, block ids < 2^32 per
+  // device); 64-bit integer division is a long instruction sequence on GPUs.
   __host__ __device__ int64_t tile_of_block(int64_t b) const {
-    int64_t gr = b / NBC, gc = b % NBC;
-    return (gr / nbt_r) * TC + gc / nbt_c;
+    const uint32_t gr = (uint32_t)b / (uint32_t)NBC, gc = (uint32_t)b % (uint32_t)NBC;
+    return (int64_t)(gr / (uint32_t)nbt_r) * TC + gc / (uint32_t)nbt_c;
   }
   // block extent
   __host__ __device__ void block_box(int64_t b, int64_t& y0, int64_t& x0, int& h, int& w) const {
-    int64_t gr = b / NBC, gc = b % NBC;
-    int64_t ty = gr / nbt_r, tx = gc / nbt_c;
-    y0 = ty * TH + (gr % nbt_r) * br;
-    x0 = tx * TW + (gc % nbt_c) * bc;
-    int64_t ty1 = (ty + 1) * TH < H ? (ty + 1) * TH : H;
-    int64_t tx1 = (tx + 1) * TW < W ? (tx + 1) * TW : W;
-    int64_t hh = ty1 - y0, ww = tx1 - x0;
+    const uint32_t gr = (uint32_t)b / (uint32_t)NBC, gc = (uint32_t)b % (uint32_t)NBC;
+    const uint32_t ty = gr / (uint32_t)nbt_r, tx = gc / (uint32_t)nbt_c;
+    y0 = (int64_t)ty * TH + (int64_t)(gr - ty * (uint32_t)nbt_r) * br;
+    x0 = (int64_t)tx * TW + (int64_t)(gc - tx * (uint32_t)nbt_c) * bc;
+    const int64_t ty1 = ((int64_t)ty + 1) * TH < H ? ((int64_t)ty + 1) * TH : H;
+    const int64_t tx1 = ((int64_t)tx + 1) * TW < W ? ((int64_t)tx + 1) * TW : W;
+    const int64_t hh = ty1 - y0, ww = tx1 - x0;
     h = hh <= 0 ? 0 : (hh > br ? br : (int)hh);
     w = ww <= 0 ? 0 : (ww > bc ? bc : (int)ww);
   }
   __host__ __device__ int64_t block_of(int64_t y, int64_t x, int& ly, int& lx) const {
-    int64_t ty = y / TH, tx = x / TW;
-    int64_t ry = y - ty * TH, rx = x - tx * TW;
-    int64_t gr = ty * nbt_r + ry / br, gc = tx * nbt_c + rx / bc;
-    ly = (int)(ry % br);
-    lx = (int)(rx % bc);
-    return gr * NBC + gc;
+    const uint32_t ty = (uint32_t)y / (uint32_t)TH, tx = (uint32_t)x / (uint32_t)TW;
+    const uint32_t ry = (uint32_t)y - ty * (uint32_t)TH, rx = (uint32_t)x - tx * (uint32_t)TW;
+    const uint32_t qy = ry / (uint32_t)br, qx = rx / (uint32_t)bc;
+    ly = (int)(ry - qy * (uint32_t)br);
+    lx = (int)(rx - qx * (uint32_t)bc);
+    return (int64_t)(ty * (uint32_t)nbt_r + qy) * NBC + tx * (uint32_t)nbt_c + qx;
   }
   __host__ __device__ void tile_box(int64_t t, int64_t& y0, int64_t& x0, int64_t& h,
                                     int64_t& w) const {
-    int64_t ty = t / TC, tx = t % TC;
+    const int64_t ty = (uint32_t)t / (uint32_t)TC, tx = (uint32_t)t % (uint32_t)TC;
     y0 = ty * TH;
     x0 = tx * TW;
     h = (y0 + TH <= H) ? TH : H - y0;
@@ -144,30 +146,32 @@ template <int STRIDE>
 __device__ __forceinline__ uint8_t d8_code(const float* zs, int i) {
   const float zc = zs[i];
   if (isnan(zc)) return kNoData;
-  int first_out = 0, kc = 0, kd = 0;
-  float a = 0.0f, b = 0.0f;
+  // drops; a NaN neighbour (NoData / off-grid) gives a NaN drop, which no
+  // comparison below accepts, so the common path needs no NaN tests
+  float d[9];
 #pragma unroll
-  for (int k = 1; k <= 8; ++k) {
-    const float zn = zs[i + dir_dy(k) * STRIDE + dir_dx(k)];
-    if (isnan(zn)) {
-      if (!first_out) first_out = k;
-      continue;
-    }
-    const float d = __fsub_rn(zc, zn);
-    if (!(d > 0.0f)) continue;
-    if (k & 1) {
-      if (kc == 0 || d > a) { a = d; kc = k; }
-    } else {
-      if (kd == 0 || d > b) { b = d; kd = k; }
-    }
-  }
+  for (int k = 1; k <= 8; ++k) d[k] = __fsub_rn(zc, zs[i + dir_dy(k) * STRIDE + dir_dx(k)]);
+  // best cardinal / diagonal: strictly larger replaces, so the first
+  // (lowest) code wins ties (D2)
+  float a = 0.0f, b = 0.0f;
+  int kc = 0, kd = 0;
+#pragma unroll
+  for (int k = 1; k <= 7; k += 2)
+    if (d[k] > a) { a = d[k]; kc = k; }
+#pragma unroll
+  for (int k = 2; k <= 8; k += 2)
+    if (d[k] > b) { b = d[k]; kd = k; }
   if (kc && kd) {
     const double da = (double)a, db = (double)b;
     return (uint8_t)(__dmul_rn(__dmul_rn(2.0, da), da) > __dmul_rn(db, db) ? kc : kd);
   }
-  if (kc) return (uint8_t)kc;
-  if (kd) return (uint8_t)kd;
-  return (uint8_t)(first_out ? first_out : kNoFlow);
+  if (kc | kd) return (uint8_t)(kc | kd);
+  // no downhill data neighbour: outlet through the lowest off-grid / NoData
+  // code (D3), else NoFlow (D6)
+#pragma unroll
+  for (int k = 1; k <= 8; ++k)
+    if (isnan(zs[i + dir_dy(k) * STRIDE + dir_dx(k)])) return (uint8_t)k;
+  return kNoFlow;
 }
 
 __device__ __forceinline__ float stage_z(float v, float nodata) {
