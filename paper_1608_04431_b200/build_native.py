@@ -53,13 +53,36 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     extra = ["-DFA_PHASE_CLOCKS"] if variant == "prof" else []
-    cmd = [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", nccl_include(), *sources(),
-           "-o", lib + ".tmp", "-ldl"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", nccl_include()]
+    objdir = os.path.join(HERE, "build", variant or "release")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        r = subprocess.run([nvcc, *compile_flags, *extra, *inc, "-c", src, "-o", obj],
+                           capture_output=True, text=True)
+        return src, obj, r
+
+    # one nvcc per translation unit, in parallel (the units only call each
+    # other's host-side launchers, so no device link step is needed)
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, sources()))
+    log = "".join(r.stdout + r.stderr for _, _, r in results)
+    bad = [src for src, _, r in results if r.returncode != 0]
+    if bad:
+        sys.stderr.write(log)
+        raise RuntimeError("nvcc failed building libfa.so: " + ", ".join(bad))
+    res = subprocess.run([nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
+                          *[o for _, o, _ in results], "-o", lib + ".tmp", "-ldl"],
+                         capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError("nvcc failed building libfa.so")
+        raise RuntimeError("nvcc failed linking libfa.so")
     os.replace(lib + ".tmp", lib)
+    res.stdout, res.stderr = log, ""
     if variant:
         return lib
     with open(os.path.join(HERE, "ptxas.log"), "w") as f:

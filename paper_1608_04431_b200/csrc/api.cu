@@ -73,16 +73,18 @@ Geom make_geom(int64_t H, int64_t W, int64_t th, int64_t tw) {
   g.br = kBR;
   g.bc = kBC;
   g.nw = kNW;
-  // tuning override: FA_BLOCK = 32x32 | 32x32x1 | 32x32x4 | 32x64 | 64x64[x1|x2]
-  if (const char* e = getenv("FA_BLOCK")) {
-    if (!strcmp(e, "32x32x1")) { g.nw = 1; }
-    else if (!strcmp(e, "32x32x4")) { g.nw = 4; }
-    else if (!strcmp(e, "32x64")) { g.br = 32; g.bc = 64; }
-    else if (!strcmp(e, "64x64")) { g.br = 64; g.bc = 64; g.nw = 4; }
-    else if (!strcmp(e, "64x64x1")) { g.br = 64; g.bc = 64; g.nw = 1; }
-    else if (!strcmp(e, "64x64x2")) { g.br = 64; g.bc = 64; g.nw = 2; }
+  // tuning overrides: FA_WARPS = warps (one block each) per CTA, 1..4;
+  // FA_BR = block rows, 16 or 32 (blocks are BR x 32, one per warp)
+  if (const char* e = getenv("FA_WARPS")) {
+    const int v = atoi(e);
+    if (v >= 1 && v <= 4) g.nw = v;
+  }
+  if (const char* e = getenv("FA_BR")) {
+    const int v = atoi(e);
+    if (v == 16 || v == 32) g.br = v;
   }
   g.pb = 2 * (g.br + g.bc) - 4;
+  g.regular = (g.TH % g.br == 0 && g.TW % g.bc == 0) ? 1 : 0;
   g.nbt_r = (g.TH + g.br - 1) / g.br;
   g.nbt_c = (g.TW + g.bc - 1) / g.bc;
   g.NBR = g.TR * g.nbt_r;
@@ -326,7 +328,9 @@ fa_status strip_pass1(fa_ctx* ctx, Strip<T>& s, bool cut) {
   if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
   CK(cudaMemsetAsync(ctx->d_small, 0, sizeof(uint32_t), st));  // node counter (status accumulates)
   CK(cudaMemsetAsync(s.x_slot, 0, slots * sizeof(T), st));
-  CK(launch_pass1<T, WK>(pass_args<T, WK>(ctx, s), s.dem != nullptr, st));
+  fa::PassArgs<T, WK> pa = pass_args<T, WK>(ctx, s);
+  pa.cut = cut;
+  CK(launch_pass1<T, WK>(pa, s.dem != nullptr, st));
   ++rt.launches;
   CK(rt.read(ctx->d_small, 4));
   s.nn = rt.h_cnt[0];

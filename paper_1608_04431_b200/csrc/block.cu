@@ -1,69 +1,61 @@
-// block.cu -- CTA-resident block kernels (SURVEY N1 "SMEM-resident fused tile
-// kernel"): each CTA owns a BR x BC block and runs the paper's single-tile
-// algorithm on it entirely in shared memory.
+// block.cu -- warp-resident block kernels (SURVEY N1 "SMEM-resident fused tile
+// kernel"): each WARP owns one R x 32 block of the raster (R = 16 or 32) and
+// runs the paper's single-tile algorithm on it entirely in shared memory,
+// with no CTA-wide barrier (only __syncwarp), so blocks never wait on one
+// another.
 //
-//   pass 1 (k_pass1): [H1 D8 from the DEM + 1-cell halo] -> [H2 in-block donor
-//     masks by an 8-neighbour gather, no atomics] -> [H3 in-block accumulation,
-//     Alg. 1 P:L127-176] -> [H4 block perimeter records: one node per block exit
-//     cell with its block-local accumulation, and for every perimeter cell the
-//     exit its in-block path reaches, Alg. 2 P:L178-204].
-//   pass 2 (k_pass2): [H6 offset propagation, EVICT P:L255-262]: rerun H2-H3 with
-//     w + x at the block perimeter cells (x = external inbound flow, D11/D12).
+//   pass 1 (k_pass1): [H1 D8 from the DEM, 2-cell halo] -> [successor words,
+//     H2 in-block donor masks by an 8-neighbour SWAR gather (no atomics),
+//     source queue] -> [H3 in-block accumulation, Alg. 1 P:L127-176] ->
+//     [H4 block perimeter records: one node per block exit cell with its
+//     block-local accumulation, and for the perimeter cells other blocks can
+//     drain into, the exit their in-block path reaches (Alg. 2)].
+//     RETAIN writes the block-local accumulation to the output here.
+//   pass 2 (k_pass2): [H6 offset propagation, EVICT P:L255-262]: rerun H2-H3
+//     from the directions with w + x at the block perimeter cells (x =
+//     external inbound flow, D11/D12), write A.
 //
-// H3 scheduling (differs from the paper's FIFO): walks.  The
-// block's sources (data cells without in-block donors) are compacted into a
-// shared queue.  A lane takes a source and walks downstream, adding its value
-// into the next cell and continuing while it is that cell's only pending
-// donor -- cells with exactly one donor need no atomic.  At a junction the
-// walk clears its bit in the target's pending-donor mask (one shared
-// atomicAnd on a packed word); only the last arrival gathers the donors'
-// values (fixed donor order) and continues.  A lane whose walk ends takes the
-// next source at once, so lanes stay busy while a few long rivers are walked.
+// Lane layout.  Lane l owns column l of the block: the D8 stencil runs down
+// the column with a rolling 3x3 register window (3 shared loads per cell
+// instead of 9), writing the code and the cell's successor word.  The 2-cell
+// halo lets the warp also evaluate D8 on the ring of cells around the block,
+// which says which perimeter cells are entries (have a donor outside the
+// block): only those need an Alg. 2 walk for the block-exit graph.
 //
-// Why small blocks (default 32 x 32, one warp): a block's walks finish no
-// sooner than its longest in-block flow path, so throughput = cells in flight
-// per SM / block latency.  Shared memory bounds the cells in flight (~14 KB
-// per 32x32 f64 block -> 16 blocks per SM); smaller blocks shorten the
-// critical path (ncu on 64x64 blocks: 25 % occupancy, issue 35 %, stalls on
-// global loads and on the end-of-walk barrier).
+// Successor word (u16 per cell, block-local index i = 32*ly + lx):
+//   bit 15 STOP  -- no in-block successor (NoFlow, drops into in-block NoData,
+//                   or leaves the block);
+//   bit 14 EXIT  -- (with STOP) the target is outside the block: a block exit;
+//   bits 11-13   -- code - 1 (without STOP);
+//   bits 0-10    -- target index (without STOP).
 //
-// Shared-memory layout: directions are stored with a 1-cell halo ring, row
-// stride HS = BC + 8 with the block interior at column 4 (4-byte aligned rows
-// for SWAR); ring cells hold 254 (outside the block) or 255 (NoData /
-// off-grid), so walks need no bounds tests.  Masks and values use stride BC.
+// H3 scheduling (differs from the paper's FIFO): lockstep
+// walks.  Every lane walks from a source (a data cell with no in-block
+// donor) downstream, adding its value into the next cell and continuing
+// while it is that cell's only donor (plain load/store).  At a junction the
+// walk adds its value into the junction cell with a shared-memory atomic and
+// clears its bit in the cell's pending-donor mask (atomicAnd); the arrival
+// that clears the last bit continues from the junction, whose value is then
+// complete.  Idle lanes take the next sources from the warp's compacted
+// source queue (one ballot per iteration, no atomics).  Visibility: each
+// iteration starts with __syncwarp, and a walk continuing from a junction
+// reads the junction's value only after a second __syncwarp at the end of
+// the iteration in which it cleared the last bit (memory ordering among the
+// warp's lanes).  fp64 sums at junctions follow the arrival order, which the
+// single-warp schedule fixes; results are within the D13 tolerance of any
+// order.
 #include "fa_internal.cuh"
 
 namespace fa {
 
 constexpr uint8_t kOut = 254;  // ring cell: outside the block, data
 
-// Optional per-phase cycle accounting (profiling build only, -DFA_PHASE_CLOCKS):
-// thread 0 of every CTA adds the cycles each phase took to g_phase[i].
-#ifdef FA_PHASE_CLOCKS
-__device__ unsigned long long g_phase[16];
-#define PH_T0 long long _ph_t = clock64()
-#define PH_MARK(i)                                                          \
-  do {                                                                      \
-    if (threadIdx.x == 0) {                                                 \
-      const long long _n = clock64();                                       \
-      atomicAdd(&g_phase[i], (unsigned long long)(_n - _ph_t));             \
-      _ph_t = _n;                                                           \
-    }                                                                       \
-  } while (0)
-}  // namespace fa
-extern "C" __attribute__((visibility("default"))) int fa_debug_phase_clocks(unsigned long long* out, int reset) {
-  if (cudaMemcpyFromSymbol(out, fa::g_phase, sizeof(fa::g_phase)) != cudaSuccess) return 1;
-  if (reset) {
-    static const unsigned long long z[16] = {0};
-    cudaMemcpyToSymbol(fa::g_phase, z, sizeof(z));
-  }
-  return 0;
-}
-namespace fa {
-#else
-#define PH_T0 (void)0
-#define PH_MARK(i) (void)0
-#endif
+constexpr uint32_t SU_STOP = 0x8000u, SU_EXIT = 0x4000u, SU_T = 0x07FFu;
+// direction codes (bit k) leaving a cell through its N / S / W / E side
+constexpr uint32_t DM_N = (1u << 1) | (1u << 2) | (1u << 8);
+constexpr uint32_t DM_S = (1u << 4) | (1u << 5) | (1u << 6);
+constexpr uint32_t DM_W = (1u << 6) | (1u << 7) | (1u << 8);
+constexpr uint32_t DM_E = (1u << 2) | (1u << 3) | (1u << 4);
 
 // packed signed 8-bit offsets of direction codes 1..8 for a row stride S
 __host__ __device__ constexpr uint64_t pack_offsets(int S) {
@@ -73,600 +65,835 @@ __host__ __device__ constexpr uint64_t pack_offsets(int S) {
   return t;
 }
 
-template <int BR_, int BC_, int NW_>
-struct Cfg {
-  static constexpr int BR = BR_, BC = BC_, NW = NW_;
-  static constexpr int NT = 32 * NW;
-  static constexpr int BN = BR * BC;
+template <int R>
+struct WBT {
+  static constexpr int BR = R, BC = 32, BN = BR * BC;
   static constexpr int PB = 2 * (BR + BC) - 4;
-  static constexpr int HS = BC + 8;               // halo'd row stride (interior at col 4)
-  static constexpr int HN = (BR + 2) * HS;
-  static constexpr int ZS = BC + 2;               // staged elevations stride
-  static constexpr int ZN = (BR + 2) * ZS;
+  static constexpr int HS = 48, HOFF = 16;  // dirh: row stride, interior column (16-B aligned rows)
+  static constexpr int HN = (BR + 2) * HS + 16;
+  static constexpr int ZS = 40, ZOFF = 4;   // z window: row stride, interior column (16-B aligned)
+  static constexpr int ZR = BR + 4;         // window rows: 2-cell halo
+  static constexpr int ZN = ZR * ZS;
   static constexpr uint64_t OFFH = pack_offsets(HS);
   static constexpr uint64_t OFFA = pack_offsets(BC);
-  static_assert(BC % 4 == 0 && BN % (4 * NT) == 0, "block shape");
-  static_assert(HS <= 120, "int8 offsets");
   __device__ static __forceinline__ int offH(int d) { return (int)(int8_t)(OFFH >> (8 * (d - 1))); }
   __device__ static __forceinline__ int offA(int d) { return (int)(int8_t)(OFFA >> (8 * (d - 1))); }
-  __device__ static __forceinline__ int hidx(int ly, int lx) { return (ly + 1) * HS + lx + 4; }
-  __device__ static __forceinline__ int a2h(int i) { return hidx(i / BC, i % BC); }
+  __device__ static __forceinline__ int hidx(int ly, int lx) { return (ly + 1) * HS + HOFF + lx; }
+  __device__ static __forceinline__ int zidx(int ly, int lx) { return (ly + 2) * ZS + ZOFF + lx; }
+  static_assert(HS <= 120 && ZS <= 120, "int8 offsets");
+  static_assert(PB <= 128, "perimeter slots: at most 4 per lane");
+  static_assert(BN <= 2048, "11-bit successor index");
 };
 
-template <class C>
-struct __align__(16) Smem {
-  uint8_t dirh[C::HN];
-  uint32_t msk4[C::BN / 4];  // donor masks, one byte per cell
-  uint32_t pend[C::BN / 4];  // pending-donor masks (atomicAnd)
-  uint16_t src[C::BN];       // source queue (A index)
-  uint32_t slot_nid[C::PB];
-  uint32_t nsrc, qhead, cnt_exit, base, processed, ndata;
+template <class T, int R>
+struct __align__(16) WSmem {
+  using WB = WBT<R>;
+  static constexpr size_t kA = sizeof(T) * WB::BN, kZ = sizeof(float) * WB::ZN;
+  union __align__(16) {
+    T A[WB::BN];
+    float z[WB::ZN];
+    unsigned char raw[kA > kZ ? kA : kZ];
+  } u;
+  uint8_t dirh[WB::HN];
+  uint32_t msk4[WB::BN / 4];  // donor masks, one byte per cell
+  uint32_t pend[WB::BN / 4];  // pending-donor masks (atomicAnd); slot -> node id after the walks (PB <= BN/4)
+  alignas(8) uint16_t succ[WB::BN];
+  uint16_t src[WB::BN];       // source queue (cells with no in-block donor and an in-block successor)
+  uint8_t need[128];          // perimeter slot needs its exit (an entry, or a tile-edge slot)
   __device__ __forceinline__ uint8_t msk(int i) const { return reinterpret_cast<const uint8_t*>(msk4)[i]; }
+  __device__ __forceinline__ uint32_t* slot_nid() { return pend; }
 };
 
-template <class C, class T>
-struct SmemSize {
-  static constexpr size_t a_bytes = sizeof(T) * C::BN;
-  static constexpr size_t z_bytes = sizeof(float) * C::ZN;
-  static constexpr size_t region = ((a_bytes > z_bytes ? a_bytes : z_bytes) + 15) / 16 * 16;
-  static constexpr size_t total = region + sizeof(Smem<C>);
-};
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+constexpr unsigned kFull = 0xFFFFFFFFu;
 
 template <int WK>
 __device__ __forceinline__ bool weight_ok(float v) {
   return WK != 2 || (isfinite(v) && v >= 0.0f);  // D21
 }
 
-template <class T, int WK>
-__device__ __forceinline__ T wval(const void* w, int64_t gi) {
-  if constexpr (WK == 0) return (T)1;
-  else if constexpr (WK == 1) return (T) static_cast<const uint32_t*>(w)[gi];
-  else return (T) static_cast<const float*>(w)[gi];
+// in-block perimeter order (clockwise from the top-left), ints
+__device__ __forceinline__ void bperim_xy(int p, int h, int w, int& x, int& y) {
+  if (h == 1 || w == 1) { y = p / w; x = p - y * w; return; }
+  if (p < w) { x = p; y = 0; return; }
+  p -= w;
+  if (p < h - 1) { x = w - 1; y = p + 1; return; }
+  p -= h - 1;
+  if (p < w - 1) { x = w - 2 - p; y = h - 1; return; }
+  p -= w - 1;
+  x = 0;
+  y = h - 2 - p;
+}
+__device__ __forceinline__ int bperim_count(int h, int w) {
+  if (h <= 0 || w <= 0) return 0;
+  if (h == 1 || w == 1) return h * w;
+  return 2 * (h + w) - 4;
+}
+__device__ __forceinline__ int bperim_index(int x, int y, int h, int w) {
+  if (h == 1 || w == 1) return y * w + x;
+  if (y == 0) return x;
+  if (x == w - 1) return w + y - 1;
+  if (y == h - 1) return w + (h - 1) + (w - 2 - x);
+  return w + (h - 1) + (w - 1) + (h - 2 - y);
+}
+
+// shared-memory accumulate at a junction (u32: native atomic; 64-bit: CAS,
+// starting from the value just read)
+__device__ __forceinline__ void sh_add(uint32_t* p, uint32_t v, uint32_t) { atomicAdd(p, v); }
+__device__ __forceinline__ void sh_add(unsigned long long* p, unsigned long long v, unsigned long long cur) {
+  for (;;) {
+    const unsigned long long prev = atomicCAS(p, cur, cur + v);
+    if (prev == cur) return;
+    cur = prev;
+  }
+}
+__device__ __forceinline__ void sh_add(double* p, double v, double cur) {
+  unsigned long long* q = reinterpret_cast<unsigned long long*>(p);
+  unsigned long long c = __double_as_longlong(cur);
+  for (;;) {
+    const unsigned long long prev = atomicCAS(q, c, __double_as_longlong(__longlong_as_double(c) + v));
+    if (prev == c) return;
+    c = prev;
+  }
+}
+
+// ---------------------------------------------------------------- H1 core
+// D8 of one cell from its 3x3 window (NaN = NoData / off-grid): steepest
+// strictly-downhill data neighbour, drops fl32(zc - zn) (D5), cardinal vs
+// diagonal by the exact compare 2a^2 > b^2 in fp64 (D4), ties to the lowest
+// code (D2); none -> lowest NaN neighbour (outlet, D3; returned | 16 so the
+// caller knows the target is NoData), else NoFlow (D6).
+__device__ __forceinline__ int d8_window(float zc, float zN, float zNE, float zE, float zSE, float zS,
+                                         float zSW, float zW, float zNW) {
+  if (isnan(zc)) return kNoData;
+  const float d1 = __fsub_rn(zc, zN), d3 = __fsub_rn(zc, zE), d5 = __fsub_rn(zc, zS), d7 = __fsub_rn(zc, zW);
+  const float d2 = __fsub_rn(zc, zNE), d4 = __fsub_rn(zc, zSE), d6 = __fsub_rn(zc, zSW),
+              d8 = __fsub_rn(zc, zNW);
+  // NaN drops fail every comparison; strictly-larger replaces: lowest code wins ties
+  float a = 0.0f, b = 0.0f;
+  int kc = 0, kd = 0;
+  if (d1 > a) { a = d1; kc = 1; }
+  if (d3 > a) { a = d3; kc = 3; }
+  if (d5 > a) { a = d5; kc = 5; }
+  if (d7 > a) { a = d7; kc = 7; }
+  if (d2 > b) { b = d2; kd = 2; }
+  if (d4 > b) { b = d4; kd = 4; }
+  if (d6 > b) { b = d6; kd = 6; }
+  if (d8 > b) { b = d8; kd = 8; }
+  if (kc && kd) {
+    const double da = (double)a, db = (double)b;
+    return __dmul_rn(__dmul_rn(2.0, da), da) > __dmul_rn(db, db) ? kc : kd;
+  }
+  if (kc | kd) return kc | kd;
+  int k = kNoFlow;
+  if (isnan(zN)) k = 1;
+  else if (isnan(zNE)) k = 2;
+  else if (isnan(zE)) k = 3;
+  else if (isnan(zSE)) k = 4;
+  else if (isnan(zS)) k = 5;
+  else if (isnan(zSW)) k = 6;
+  else if (isnan(zW)) k = 7;
+  else if (isnan(zNW)) k = 8;
+  return k ? (k | 16) : kNoFlow;
+}
+
+// successor word of in-block cell i with code d (| 16: the target is NoData);
+// `forb` = direction codes that leave the block from this cell
+template <int R>
+__device__ __forceinline__ uint32_t succ_word(int i, int d, uint32_t forb) {
+  const int k = d & 15;
+  if (d == kNoData || k == 0) return SU_STOP;
+  if ((forb >> k) & 1u) return SU_STOP | SU_EXIT;
+  if (d & 16) return SU_STOP;  // drops into in-block NoData (D8)
+  return (uint32_t)(i + WBT<R>::offA(k)) | ((uint32_t)(k - 1) << 11);
+}
+
+__device__ __forceinline__ uint32_t forb_col(int lx, int w) {
+  return (lx == 0 ? DM_W : 0u) | (lx == w - 1 ? DM_E : 0u);
+}
+__device__ __forceinline__ uint32_t forb_row(int ly, int h) {
+  return (ly == 0 ? DM_N : 0u) | (ly == h - 1 ? DM_S : 0u);
+}
+
+// ---------------------------------------------------------------- staging
+template <class T, int R>
+__device__ __forceinline__ void init_smem(WSmem<T, R>& s) {
+  uint32_t* D = reinterpret_cast<uint32_t*>(s.dirh);
+  const int lane = lane_id();
+  for (int i = lane; i < WBT<R>::HN / 4; i += 32) D[i] = 0xFFFFFFFFu;
+  reinterpret_cast<uint32_t*>(s.need)[lane] = 0u;
+}
+
+__device__ __forceinline__ const float* dem_row(const float* dem, const float* up, const float* dn, int64_t H,
+                                                int64_t W, int64_t gy) {
+  if (gy < -1 || gy > H) return nullptr;
+  if (gy == -1) return up;
+  if (gy == H) return dn;
+  return dem + gy * W;
+}
+
+// z window (block + 2-cell halo; NoData / off-grid -> NaN).  Rows of a strip
+// halo come from dem_up / dem_dn (H7); rows beyond those read as NaN and the
+// ring D8 treats them as unknown (see ring_entries).
+template <class T, int R, int WK>
+__device__ __forceinline__ void stage_z(WSmem<T, R>& s, const PassArgs<T, WK>& P, int64_t y0, int64_t x0, int h,
+                                        int w) {
+  using WB = WBT<R>;
+  const Geom& g = P.g;
+  const int lane = lane_id();
+  const float qnan = __int_as_float(0x7fc00000);
+  const bool vec = w == WB::BC && x0 >= 4 && x0 + WB::BC + 4 <= g.W && ((x0 & 3) == 0) && ((g.W & 3) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(P.dem) & 15) == 0) &&
+                   (!P.dem_up || (reinterpret_cast<uintptr_t>(P.dem_up) & 15) == 0) &&
+                   (!P.dem_dn || (reinterpret_cast<uintptr_t>(P.dem_dn) & 15) == 0);
+  const int rows = h + 4;
+  if (vec) {
+    // per window row: 10 float4 covering columns x0-4 .. x0+35; lanes 0..29
+    // take 3 rows x 10 quads per round
+    const int rr = lane / 10, k = lane - rr * 10;
+    if (rr < 3) {
+      for (int r = rr; r < rows; r += 3) {
+        const float* row = dem_row(P.dem, P.dem_up, P.dem_dn, g.H, g.W, y0 + r - 2);
+        float4 v = make_float4(qnan, qnan, qnan, qnan);
+        if (row) {
+          v = __ldg(reinterpret_cast<const float4*>(row + x0 - 4) + k);
+          v.x = fa::stage_z(v.x, P.nodata);
+          v.y = fa::stage_z(v.y, P.nodata);
+          v.z = fa::stage_z(v.z, P.nodata);
+          v.w = fa::stage_z(v.w, P.nodata);
+        }
+        *reinterpret_cast<float4*>(&s.u.z[r * WB::ZS + 4 * k]) = v;
+      }
+    }
+  } else {
+    const int ww = w + 4;
+    for (int i = lane; i < rows * ww; i += 32) {
+      const int r = i / ww, c = i - r * ww, ly = r - 2, lx = c - 2;
+      const int64_t gx = x0 + lx;
+      const float* row = dem_row(P.dem, P.dem_up, P.dem_dn, g.H, g.W, y0 + ly);
+      float v = qnan;
+      if (row && gx >= 0 && gx < g.W) v = fa::stage_z(__ldg(row + gx), P.nodata);
+      s.u.z[WB::zidx(ly, lx)] = v;
+    }
+  }
+}
+
+// one in-block cell's D8 -> code + successor word
+template <class T, int R>
+__device__ __forceinline__ void d8_put(WSmem<T, R>& s, int ly, int lx, int d, uint32_t forb) {
+  using WB = WBT<R>;
+  s.dirh[WB::hidx(ly, lx)] = (uint8_t)(d == kNoData ? kNoData : (d & 15));
+  s.succ[ly * WB::BC + lx] = (uint16_t)succ_word<R>(ly * WB::BC + lx, d, forb);
+}
+
+// D8 down each column with a rolling 3x3 window (codes + successor words)
+template <class T, int R>
+__device__ __forceinline__ void d8_block(WSmem<T, R>& s, int h, int w) {
+  using WB = WBT<R>;
+  const int lx = lane_id();
+  if (lx >= w) return;
+  const float* z = s.u.z;
+  const uint32_t fc = forb_col(lx, w);
+  int zi = WB::zidx(-1, lx);
+  float u0 = z[zi - 1], u1 = z[zi], u2 = z[zi + 1];
+  zi += WB::ZS;
+  float c0 = z[zi - 1], c1 = z[zi], c2 = z[zi + 1];
+  if (h == WB::BR) {
+#pragma unroll 4
+    for (int ly = 0; ly < WB::BR; ++ly) {
+      zi += WB::ZS;
+      const float e0 = z[zi - 1], e1 = z[zi], e2 = z[zi + 1];
+      d8_put(s, ly, lx, d8_window(c1, u1, u2, c2, e2, e1, e0, c0, u0), fc | forb_row(ly, WB::BR));
+      u0 = c0; u1 = c1; u2 = c2;
+      c0 = e0; c1 = e1; c2 = e2;
+    }
+  } else {
+    for (int ly = 0; ly < h; ++ly) {
+      zi += WB::ZS;
+      const float e0 = z[zi - 1], e1 = z[zi], e2 = z[zi + 1];
+      d8_put(s, ly, lx, d8_window(c1, u1, u2, c2, e2, e1, e0, c0, u0), fc | forb_row(ly, h));
+      u0 = c0; u1 = c1; u2 = c2;
+      c0 = e0; c1 = e1; c2 = e2;
+    }
+  }
+}
+
+// ring cells around the block: NoData-ness into dirh (255 NoData / off-grid,
+// 254 data) and, from their D8, which perimeter cells are entries.  A ring
+// cell whose 3x3 window reaches a row this rank does not hold (beyond a strip
+// halo row) has an unknown code: all its in-block neighbours count as entries.
+template <class T, int R, int WK>
+__device__ __forceinline__ void ring_entries(WSmem<T, R>& s, const PassArgs<T, WK>& P, int64_t y0, int h, int w) {
+  using WB = WBT<R>;
+  const float* z = s.u.z;
+  const int rn = 2 * (w + 2) + 2 * h;
+  for (int i = lane_id(); i < rn; i += 32) {
+    int ly, lx;
+    if (i < w + 2) { ly = -1; lx = i - 1; }
+    else if (i < 2 * (w + 2)) { ly = h; lx = i - (w + 2) - 1; }
+    else { const int j = i - 2 * (w + 2); ly = j >> 1; lx = (j & 1) ? w : -1; }
+    const int zi = WB::zidx(ly, lx);
+    const bool nd = isnan(z[zi]);
+    s.dirh[WB::hidx(ly, lx)] = nd ? kNoData : kOut;
+    if (nd) continue;
+    const int64_t gy = y0 + ly;
+    const bool unknown = (gy == -1 && P.dem_up) || (gy == P.g.H && P.dem_dn);
+    uint32_t ks;  // codes whose target is marked
+    if (unknown) {
+      ks = 0x1FEu;
+    } else {
+      const int d = d8_window(z[zi], z[zi - WB::ZS], z[zi - WB::ZS + 1], z[zi + 1], z[zi + WB::ZS + 1],
+                              z[zi + WB::ZS], z[zi + WB::ZS - 1], z[zi - 1], z[zi - WB::ZS - 1]);
+      ks = (d >= 1 && d <= 8) ? (1u << d) : 0u;  // an outlet fallback (| 16) never points into the block
+    }
+    while (ks) {
+      const int k = __ffs(ks) - 1;
+      ks &= ks - 1;
+      const int ty = ly + dir_dy(k), tx = lx + dir_dx(k);
+      if ((unsigned)ty < (unsigned)h && (unsigned)tx < (unsigned)w) s.need[bperim_index(tx, ty, h, w)] = 1;
+    }
+  }
+}
+
+// directions from global (pass 2 and pass 1 from dirs) + halo ring; bad
+// codes -> NoData, flagged when `check`; with `entries`, ring codes that
+// point into the block mark entry slots
+template <class T, int R>
+__device__ __forceinline__ void load_dirs(WSmem<T, R>& s, const uint8_t* dirs, const uint8_t* dirs_up,
+                                          const uint8_t* dirs_dn, const Geom& g, int64_t y0, int64_t x0, int h,
+                                          int w, bool check, bool entries, uint32_t* status) {
+  using WB = WBT<R>;
+  const int lane = lane_id();
+  const bool vec = w == WB::BC && ((x0 & 15) == 0) && ((g.W & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(dirs) & 15) == 0);
+  bool bad = false;
+  if (vec) {
+    for (int q = lane; q < h * 2; q += 32) {
+      const int ly = q >> 1, lx = (q & 1) * 16;
+      uint4 v = __ldg(reinterpret_cast<const uint4*>(dirs + (y0 + ly) * g.W + x0 + lx));
+      uint32_t* vv = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        // bytes > 8 and != 255 are illegal (D1)
+        const uint32_t hi = __vcmpgtu4(vv[j], 0x08080808u) & ~__vcmpeq4(vv[j], 0xFFFFFFFFu);
+        if (hi) { bad = true; vv[j] |= hi; }
+      }
+      *reinterpret_cast<uint4*>(&s.dirh[WB::hidx(ly, lx)]) = v;
+    }
+  } else {
+    for (int i = lane; i < h * WB::BC; i += 32) {
+      const int ly = i >> 5, lx = i & 31;
+      if (lx >= w) continue;
+      uint8_t d = dirs[(y0 + ly) * g.W + x0 + lx];
+      if (d > 8 && d != kNoData) { bad = true; d = kNoData; }
+      s.dirh[WB::hidx(ly, lx)] = d;
+    }
+  }
+  if (check && bad) atomicOr(status, ST_BADCODE);
+  const int rn = 2 * (w + 2) + 2 * h;
+  for (int i = lane; i < rn; i += 32) {
+    int ly, lx;
+    if (i < w + 2) { ly = -1; lx = i - 1; }
+    else if (i < 2 * (w + 2)) { ly = h; lx = i - (w + 2) - 1; }
+    else { const int j = i - 2 * (w + 2); ly = j >> 1; lx = (j & 1) ? w : -1; }
+    const int64_t gy = y0 + ly, gx = x0 + lx;
+    int code = kNoData;
+    if (gx >= 0 && gx < g.W && gy >= -1 && gy <= g.H) {
+      const uint8_t* row = gy < 0 ? dirs_up : gy >= g.H ? dirs_dn : dirs + gy * g.W;
+      if (row) code = row[gx];
+    }
+    s.dirh[WB::hidx(ly, lx)] = code == kNoData ? kNoData : kOut;
+    if (entries && code >= 1 && code <= 8) {
+      const int ty = ly + dir_dy(code), tx = lx + dir_dx(code);
+      if ((unsigned)ty < (unsigned)h && (unsigned)tx < (unsigned)w) s.need[bperim_index(tx, ty, h, w)] = 1;
+    }
+  }
+}
+
+// successor words from the staged directions
+template <class T, int R>
+__device__ __forceinline__ void succ_from_dirs(WSmem<T, R>& s, int h, int w) {
+  using WB = WBT<R>;
+  const int lx = lane_id();
+  if (lx >= w) return;
+  const uint32_t fc = forb_col(lx, w);
+  for (int ly = 0; ly < h; ++ly) {
+    const int hi = WB::hidx(ly, lx);
+    int d = s.dirh[hi];
+    if (d >= 1 && d <= 8 && s.dirh[hi + WB::offH(d)] == kNoData) d |= 16;
+    s.succ[ly * WB::BC + lx] = (uint16_t)succ_word<R>(ly * WB::BC + lx, d, fc | forb_row(ly, h));
+  }
 }
 
 // ---------------------------------------------------------------- H2
 // Donor masks by an 8-neighbour gather, 4 cells per 32-bit SWAR word (no
-// atomics; Alg. 1 first loop P:L131-148), and the compacted source queue.
-// Ring codes (254/255) never equal a direction, so no bounds tests.
-template <class C>
-__device__ __forceinline__ void build_masks(Smem<C>& s, int h, int w) {
-  const int lane = threadIdx.x & 31;
+// atomics; Alg. 1 first loop P:L131-148) and the compacted source queue.
+// Sources whose successor is STOP are retired on the spot (their value is
+// final).  Returns this lane's data-cell count; nsrc (warp total) and
+// pre_retired (this lane) by reference.  Ring codes (254/255) never equal a
+// direction, so no bounds tests.
+template <class T, int R>
+__device__ __forceinline__ uint32_t build_masks(WSmem<T, R>& s, uint32_t& nsrc, uint32_t& pre_retired) {
+  using WB = WBT<R>;
+  constexpr int NQ = WB::BN / 128;  // words per lane
+  static_assert(NQ <= 8, "source bits: 4 per word, 32 per lane");
+  const int lane = lane_id();
   const uint32_t* D = reinterpret_cast<const uint32_t*>(s.dirh);
-  for (int q = threadIdx.x; q < C::BN / 4; q += C::NT) {
-    const int ly = (4 * q) / C::BC, lx = (4 * q) % C::BC;
-    const int hw = C::hidx(ly, lx) >> 2;  // word index of the 4 cells
-    constexpr int RW = C::HS / 4;
+  const uint2* S2 = reinterpret_cast<const uint2*>(s.succ);
+  constexpr int RW = WB::HS / 4;
+  uint32_t ndata = 0, pre = 0, srcbits = 0;
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) {
+    const int q = k * 32 + lane;  // word: row q/8, cells 4(q%8)..+3
+    const int ly = q >> 3, lx = (q & 7) * 4;
+    const int hw = WB::hidx(ly, lx) >> 2;
     const uint32_t u0 = D[hw - RW - 1], u1 = D[hw - RW], u2 = D[hw - RW + 1];
     const uint32_t c0 = D[hw - 1], c1 = D[hw], c2 = D[hw + 1];
     const uint32_t d0 = D[hw + RW - 1], d1 = D[hw + RW], d2 = D[hw + RW + 1];
-    // neighbour bytes for the 4 cells in each direction (byte j <-> cell j)
     const uint32_t nN = u1, nS = d1;
     const uint32_t nE = __funnelshift_r(c1, c2, 8), nW = __funnelshift_r(c0, c1, 24);
     const uint32_t nNE = __funnelshift_r(u1, u2, 8), nNW = __funnelshift_r(u0, u1, 24);
     const uint32_t nSE = __funnelshift_r(d1, d2, 8), nSW = __funnelshift_r(d0, d1, 24);
     uint32_t m = 0;
     // a neighbour in direction k is a donor iff its code points back: opp(k)
-    m |= (__vcmpeq4(nN, 0x05050505u) & 0x01010101u) << 0;   // k=1 N  -> S(5)
-    m |= (__vcmpeq4(nNE, 0x06060606u) & 0x01010101u) << 1;  // k=2 NE -> SW(6)
-    m |= (__vcmpeq4(nE, 0x07070707u) & 0x01010101u) << 2;   // k=3 E  -> W(7)
-    m |= (__vcmpeq4(nSE, 0x08080808u) & 0x01010101u) << 3;  // k=4 SE -> NW(8)
-    m |= (__vcmpeq4(nS, 0x01010101u) & 0x01010101u) << 4;   // k=5 S  -> N(1)
-    m |= (__vcmpeq4(nSW, 0x02020202u) & 0x01010101u) << 5;  // k=6 SW -> NE(2)
-    m |= (__vcmpeq4(nW, 0x03030303u) & 0x01010101u) << 6;   // k=7 W  -> E(3)
-    m |= (__vcmpeq4(nNW, 0x04040404u) & 0x01010101u) << 7;  // k=8 NW -> SE(4)
-    // NoData (255) and ring cells (254, inside the word when the block is
-    // ragged) are not cells of the block: no donors, never sources
+    m |= (__vcmpeq4(nN, 0x05050505u) & 0x01010101u) << 0;
+    m |= (__vcmpeq4(nNE, 0x06060606u) & 0x01010101u) << 1;
+    m |= (__vcmpeq4(nE, 0x07070707u) & 0x01010101u) << 2;
+    m |= (__vcmpeq4(nSE, 0x08080808u) & 0x01010101u) << 3;
+    m |= (__vcmpeq4(nS, 0x01010101u) & 0x01010101u) << 4;
+    m |= (__vcmpeq4(nSW, 0x02020202u) & 0x01010101u) << 5;
+    m |= (__vcmpeq4(nW, 0x03030303u) & 0x01010101u) << 6;
+    m |= (__vcmpeq4(nNW, 0x04040404u) & 0x01010101u) << 7;
+    // NoData (255) and cells outside a ragged block (254/255) are not cells
     const uint32_t nd = __vcmpgeu4(c1, 0xFEFEFEFEu);
     m &= ~nd;
     s.msk4[q] = m;
     s.pend[q] = m;
-    // sources: data cells without in-block donors
-    const uint32_t zero = __vcmpeq4(m, 0u) & ~nd;  // 0xFF per source byte
-    const uint32_t sb = zero & 0x80808080u;
-    const int cnt = __popc(sb);
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-    uint32_t base = 0;
-    if (lane == 31 && total) base = atomicAdd(&s.nsrc, (uint32_t)total);
-    base = __shfl_sync(0xFFFFFFFFu, base, 31) + (uint32_t)(incl - cnt);
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (sb & (0x80u << (8 * j))) s.src[base++] = (uint16_t)(4 * q + j);
+    ndata += 4 - (__popc(nd) >> 3);
+    // sources: one bit per cell (bit 7 of each byte of src4)
+    const uint32_t src4 = __vcmpeq4(m, 0u) & ~nd & 0x80808080u;
+    const uint2 sw = S2[q];  // successor words of the 4 cells: STOP bits at 15 / 31
+    const uint32_t stop4 = ((sw.x >> 8) & 0x80u) | ((sw.x >> 16) & 0x8000u) | ((sw.y << 8) & 0x800000u) |
+                           (sw.y & 0x80000000u);
+    pre += __popc(src4 & stop4);
+    const uint32_t walk4 = src4 & ~stop4;
+    srcbits |= (((walk4 >> 7) & 1u) | ((walk4 >> 14) & 2u) | ((walk4 >> 21) & 4u) | ((walk4 >> 28) & 8u)) << (4 * k);
   }
-  (void)h;
-  (void)w;
+  // compact: exclusive scan of the per-lane counts, then each lane writes its cells
+  const int cnt = __popc(srcbits);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += v;
+  }
+  nsrc = (uint32_t)__shfl_sync(kFull, incl, 31);
+  int pos = incl - cnt;
+  while (srcbits) {
+    const int bpos = __ffs(srcbits) - 1;
+    srcbits &= srcbits - 1;
+    const int k = bpos >> 2, j = bpos & 3;
+    s.src[pos++] = (uint16_t)(4 * (k * 32 + lane) + j);
+  }
+  pre_retired = pre;
+  return ndata;
 }
 
 // ---------------------------------------------------------------- H3
-// Walks from the shared source queue (both passes).  On entry dirh, masks,
-// pend, src/nsrc and A (= w [+ x]) are set and synced.  Returns the number of
-// cells this thread retired.
-__device__ __forceinline__ void fence_cta() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
-
-template <class C, class T>
-__device__ __forceinline__ uint32_t chain_follow(Smem<C>& s, T* A) {
-  const uint32_t nsrc = s.nsrc;
-  uint32_t retired = 0;
+// Lockstep walks (see the file comment).  On entry succ, masks, pend, the
+// source queue and A (= w [+ x]) are set and visible to the warp.  Returns
+// the number of cells this lane retired.
+template <class T, int R>
+__device__ __forceinline__ uint32_t walk_block(WSmem<T, R>& s, uint32_t nsrc) {
+  const int lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  T* A = s.u.A;
+  uint32_t head = 0, ret = 0;
   bool live = false;
-  int ch = 0, ca = 0, d = 0;
-  T a = (T)0;
-#ifdef FA_PHASE_CLOCKS
-  uint32_t iters = 0;
-  struct Tally {
-    uint32_t& it;
-    const uint32_t& ret;
-    __device__ ~Tally() {
-      uint32_t mx = it, sm = ret;
-      for (int o = 16; o; o >>= 1) {
-        mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
-        sm += __shfl_xor_sync(0xFFFFFFFFu, sm, o);
-      }
-      if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&g_phase[14], (unsigned long long)mx);
-        atomicAdd(&g_phase[15], (unsigned long long)sm);
-      }
-    }
-  } tally{iters, retired};
-#endif
+  uint32_t su = SU_STOP;  // successor word of the lane's current cell
+  T a = (T)0;             // value of the current cell (final)
   for (;;) {
-#ifdef FA_PHASE_CLOCKS
-    ++iters;
-#endif
+    __syncwarp();
+    const unsigned idle = __ballot_sync(kFull, !live);
+    if (idle == kFull && head >= nsrc) break;
     if (!live) {
-      // take the next source (per-lane shared atomic; no warp votes, so a
-      // lane never waits for the others of its warp)
-      const uint32_t q = atomicAdd(&s.qhead, 1u);
-      if (q >= nsrc) break;
-      ca = s.src[q];
-      ch = C::a2h(ca);
-      d = s.dirh[ch];
-      a = A[ca];
-      live = true;
-      ++retired;
-    }
-    // one step downstream
-    if (d == kNoFlow || d > 8) { live = false; continue; }
-    const int th = ch + C::offH(d);
-    const int ta = (ca + C::offA(d)) & (C::BN - 1);  // clamped; unused when the walk stops
-    const int dt = s.dirh[th];
-    const uint32_t m = s.msk(ta);
-    const T at = A[ta];  // w(t) [+ x(t)]: only the walk that finishes t writes A[t]
-    if (dt >= kOut) { live = false; continue; }  // leaves the block, or drops into NoData (D8)
-    if ((m & (m - 1)) == 0) {
-      a = at + a;  // sole in-block donor: no atomic
-    } else {
-      // junction: clear our bit; the last arrival gathers the donors
-      const uint32_t bit = 1u << ((d + 3) & 7);  // bit of the opposite direction
-      const int sh = (ta & 3) * 8;
-      fence_cta();  // release our value
-      const uint32_t old = atomicAnd(&s.pend[ta >> 2], ~(bit << sh));
-      if (((old >> sh) & 0xFFu) != bit) { live = false; continue; }  // others pending
-      fence_cta();  // acquire the other donors' values
-      uint32_t mm = m;
-      T acc = at;
-      do {  // donors in code order (fixed summation order)
-        const int k = __ffs(mm);
-        mm &= mm - 1;
-        acc = acc + A[ta + C::offA(k)];
-      } while (mm);
-      a = acc;
-    }
-    A[ta] = a;
-    ch = th;
-    ca = ta;
-    d = dt;
-    ++retired;
-  }
-  return retired;
-}
-
-// ---------------------------------------------------------------- shared stages
-template <class C>
-__device__ __forceinline__ void init_dirh(Smem<C>& s) {
-  uint32_t* D = reinterpret_cast<uint32_t*>(s.dirh);
-  for (int i = threadIdx.x; i < C::HN / 4; i += C::NT) D[i] = 0xFFFFFFFFu;
-}
-
-// interior directions from global (pass 2 and pass 1 from dirs); bad codes
-// -> NoData, flagged when `check`
-template <class C>
-__device__ __forceinline__ void load_dirs(Smem<C>& s, const uint8_t* dirs, const Geom& g, int64_t y0,
-                                          int64_t x0, int h, int w, bool check, uint32_t* status) {
-  const bool vec = w == C::BC && ((x0 & 3) == 0) && ((g.W & 3) == 0) &&
-                   ((reinterpret_cast<uintptr_t>(dirs) & 3) == 0);
-  bool bad = false;
-  if (vec) {
-    for (int q = threadIdx.x; q < h * (C::BC / 4); q += C::NT) {
-      const int ly = q / (C::BC / 4), lx = (q % (C::BC / 4)) * 4;
-      uint32_t v = __ldg(reinterpret_cast<const uint32_t*>(dirs + (y0 + ly) * g.W + x0 + lx));
-      // bytes > 8 and != 255 are illegal (D1)
-      const uint32_t hi = __vcmpgtu4(v, 0x08080808u) & ~__vcmpeq4(v, 0xFFFFFFFFu);
-      if (hi) { bad = true; v |= hi; }
-      *reinterpret_cast<uint32_t*>(&s.dirh[C::hidx(ly, lx)]) = v;
-    }
-  } else {
-    for (int i = threadIdx.x; i < h * C::BC; i += C::NT) {
-      const int ly = i / C::BC, lx = i % C::BC;
-      if (lx >= w) continue;
-      uint8_t d = dirs[(y0 + ly) * g.W + x0 + lx];
-      if (d > 8 && d != kNoData) { bad = true; d = kNoData; }
-      s.dirh[C::hidx(ly, lx)] = d;
-    }
-  }
-  if (check && bad) atomicOr(status, ST_BADCODE);
-}
-
-// Weights prefetched into registers at kernel entry (full, aligned blocks),
-// so their HBM latency overlaps the staging / D8 / mask phases.
-template <class C, int WK>
-struct WPre {
-  static constexpr int R = C::BN / (4 * C::NT);  // 16-byte groups per thread
-  uint4 r[WK == 0 ? 1 : R];
-  bool vec = false;
-  __device__ __forceinline__ void load(const void* wp, const Geom& g, int64_t y0, int64_t x0, int h, int w) {
-    if (WK == 0) return;
-    vec = h == C::BR && w == C::BC && ((x0 & 3) == 0) && ((g.W & 3) == 0) &&
-          ((reinterpret_cast<uintptr_t>(wp) & 15) == 0);
-    if (!vec) return;
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-      const int q = threadIdx.x + k * C::NT;
-      const int ly = q / (C::BC / 4), lx = (q % (C::BC / 4)) * 4;
-      r[k] = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint32_t*>(wp) + (y0 + ly) * g.W + x0 + lx));
-    }
-  }
-};
-
-// A = w (Eq. 1; Alg. 1 "A(c) <- A(c) + 1") for data cells
-template <class C, class T, int WK>
-__device__ __forceinline__ void init_values(Smem<C>& s, T* A, const void* wp, const WPre<C, WK>& pre,
-                                            const Geom& g, int64_t y0, int64_t x0, int h, int w,
-                                            uint32_t* status, unsigned long long* wsum_out) {
-  unsigned long long wsum = 0;
-  uint32_t nd = 0;
-  bool bad = false;
-  // store one group of 4 cells (raw weight bits in u[]) into A
-  auto put = [&](int q, const uint32_t u[4], bool have) {
-    const int ly = q / (C::BC / 4), lx = (q % (C::BC / 4)) * 4;
-    const uint32_t dw = *reinterpret_cast<const uint32_t*>(&s.dirh[C::hidx(ly, lx)]);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const bool data = ((dw >> (8 * j)) & 0xFF) < kOut;  // excludes NoData and the ring
-      if (!data) continue;
-      T v;
-      if constexpr (WK == 0) {
-        v = (T)1;
-      } else if constexpr (WK == 1) {
-        v = (T)u[j];
-      } else {
-        const float f = __uint_as_float(u[j]);
-        if (!weight_ok<WK>(f)) bad = true;
-        v = (T)f;
+      const uint32_t q = head + (uint32_t)__popc(idle & lt);
+      if (q < nsrc) {
+        const int c = s.src[q];
+        a = A[c];
+        su = s.succ[c];  // never STOP for a queued source
+        live = true;
+        ++ret;
       }
-      (void)have;
-      A[ly * C::BC + lx + j] = v;
-      ++nd;
-      if constexpr (!std::is_same<T, double>::value) wsum += (unsigned long long)v;
     }
-  };
-  if (WK != 0 && pre.vec) {
-#pragma unroll
-    for (int k = 0; k < WPre<C, WK>::R; ++k) {
-      const uint32_t u[4] = {pre.r[k].x, pre.r[k].y, pre.r[k].z, pre.r[k].w};
-      put(threadIdx.x + k * C::NT, u, true);
+    head += (uint32_t)__popc(idle);
+    bool jlast = false;
+    int n = 0;
+    if (live) {
+      n = (int)(su & SU_T);
+      const uint32_t m = s.msk(n);
+      const T an = A[n];  // w(n) [+ x(n)] [+ donors already added at a junction]
+      const uint32_t sn = s.succ[n];
+      if ((m & (m - 1)) == 0) {
+        a = an + a;  // sole in-block donor: plain store
+        A[n] = a;
+      } else {
+        sh_add(&A[n], a, an);  // junction: add our value, then clear our pending bit
+        const uint32_t bit = 1u << ((((su >> 11) & 7u) + 4u) & 7u);  // bit of the opposite direction
+        const int sh = (n & 3) * 8;
+        const uint32_t old = atomicAnd(&s.pend[n >> 2], ~(bit << sh));
+        jlast = ((old >> sh) & 0xFFu) == bit;  // we were the last pending donor
+        live = jlast;
+      }
+      if (live) {
+        su = sn;
+        ++ret;
+        live = (sn & SU_STOP) == 0u;
+        jlast = jlast && live;
+      }
     }
+    __syncwarp();
+    if (jlast) a = A[n];  // every donor's add is visible now
+  }
+  return ret;
+}
+
+// ---------------------------------------------------------------- values
+// A = w (Eq. 1; Alg. 1 "A(c) <- A(c) + 1"); returns Σw over data
+// cells (integer weights; the u32 overflow check, D10)
+template <class T, int R, int WK>
+__device__ __forceinline__ unsigned long long init_values(WSmem<T, R>& s, const void* wp, const Geom& g, int64_t y0,
+                                                          int64_t x0, int h, int w, uint32_t* status) {
+  using WB = WBT<R>;
+  const int lane = lane_id();
+  T* A = s.u.A;
+  unsigned long long wsum = 0;
+  bool bad = false;
+  if constexpr (WK == 0) {
+    for (int i = lane; i < WB::BN; i += 32) A[i] = (T)1;
+    return 0;  // Σw = number of data cells, counted by the caller
   } else {
-    for (int q = threadIdx.x; q < h * (C::BC / 4); q += C::NT) {
-      const int ly = q / (C::BC / 4), lx = (q % (C::BC / 4)) * 4;
-      const int64_t gi = (y0 + ly) * g.W + x0 + lx;
+    const bool vec = h == WB::BR && w == WB::BC && ((x0 & 3) == 0) && ((g.W & 3) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(wp) & 15) == 0);
+    const uint32_t* W32 = static_cast<const uint32_t*>(wp);
+#pragma unroll 4
+    for (int q = lane; q < WB::BN / 4; q += 32) {
+      const int ly = q >> 3, lx = (q & 7) * 4;
+      const uint32_t dw = *reinterpret_cast<const uint32_t*>(&s.dirh[WB::hidx(ly, lx)]);
       uint32_t u[4] = {0, 0, 0, 0};
-      if (WK != 0) {
+      if (vec) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(W32 + (y0 + ly) * g.W + x0 + lx));
+        u[0] = v.x; u[1] = v.y; u[2] = v.z; u[3] = v.w;
+      } else if (ly < h) {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (lx + j < w) u[j] = static_cast<const uint32_t*>(wp)[gi + j];
+          if (lx + j < w) u[j] = __ldg(W32 + (y0 + ly) * g.W + x0 + lx + j);
       }
-      put(q, u, true);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const bool data = ((dw >> (8 * j)) & 0xFF) < kOut;  // excludes NoData and cells outside
+        T v;
+        if constexpr (WK == 1) {
+          v = (T)u[j];
+          if (data) wsum += u[j];
+        } else {
+          const float f = __uint_as_float(u[j]);
+          if (data && !weight_ok<WK>(f)) bad = true;
+          v = (T)f;
+        }
+        A[4 * q + j] = v;
+      }
     }
   }
   if (bad) atomicOr(status, ST_BADWEIGHT);
-  if (!std::is_same<T, double>::value && wsum_out) {
-    for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(0xFFFFFFFFu, wsum, o);
-    if ((threadIdx.x & 31) == 0 && wsum) atomicAdd(wsum_out, wsum);
-  }
-  atomicAdd(&s.ndata, nd);
+  return wsum;
 }
 
 // write the block's values A (NoData marker D9), 16-byte stores when aligned
-template <class C, class T>
-__device__ __forceinline__ void write_block(const Smem<C>& s, const T* A, T* out, const Geom& g, int64_t y0,
-                                            int64_t x0, int h, int w) {
+template <class T, int R>
+__device__ __forceinline__ void write_block(const WSmem<T, R>& s, T* out, const Geom& g, int64_t y0, int64_t x0,
+                                            int h, int w) {
+  using WB = WBT<R>;
+  const int lane = lane_id();
+  const T* A = s.u.A;
   constexpr int V = 16 / sizeof(T);  // cells per 16-byte store
-  const bool vec = w == C::BC && ((x0 % V) == 0) && ((g.W % V) == 0) &&
+  constexpr int PR = WB::BC / V;     // stores per row
+  const bool vec = w == WB::BC && ((x0 % V) == 0) && ((g.W % V) == 0) &&
                    ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
   if (vec) {
-    for (int q = threadIdx.x; q < h * (C::BC / V); q += C::NT) {
-      const int ly = q / (C::BC / V), lx = (q % (C::BC / V)) * V;
+    for (int q = lane; q < h * PR; q += 32) {
+      const int ly = q / PR, lx = (q % PR) * V;
       alignas(16) T v[V];
 #pragma unroll
       for (int j = 0; j < V; ++j)
-        v[j] = s.dirh[C::hidx(ly, lx + j)] == kNoData ? AccT<T>::marker() : A[ly * C::BC + lx + j];
+        v[j] = s.dirh[WB::hidx(ly, lx + j)] == kNoData ? AccT<T>::marker() : A[ly * WB::BC + lx + j];
       *reinterpret_cast<uint4*>(out + (y0 + ly) * g.W + x0 + lx) = *reinterpret_cast<const uint4*>(v);
     }
   } else {
-    for (int i = threadIdx.x; i < h * C::BC; i += C::NT) {
-      const int ly = i / C::BC, lx = i % C::BC;
+    for (int i = lane; i < h * WB::BC; i += 32) {
+      const int ly = i >> 5, lx = i & 31;
       if (lx >= w) continue;
-      const bool nodata = s.dirh[C::hidx(ly, lx)] == kNoData;
+      const bool nodata = s.dirh[WB::hidx(ly, lx)] == kNoData;
       out[(y0 + ly) * g.W + x0 + lx] = nodata ? AccT<T>::marker() : A[i];
     }
   }
 }
 
-// ---------------------------------------------------------------- pass 1
-template <class C, class T, int WK, bool FROM_DEM>
-__global__ void __launch_bounds__(C::NT) k_pass1(PassArgs<T, WK> P) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  T* A = reinterpret_cast<T*>(smem);
-  float* zs = reinterpret_cast<float*>(smem);
-  Smem<C>& s = *reinterpret_cast<Smem<C>*>(smem + SmemSize<C, T>::region);
+// the block's D8 codes to global (16-byte rows when aligned)
+template <class T, int R>
+__device__ __forceinline__ void write_dirs(const WSmem<T, R>& s, uint8_t* dirs, const Geom& g, int64_t y0,
+                                           int64_t x0, int h, int w) {
+  using WB = WBT<R>;
+  const int lane = lane_id();
+  const bool vec = w == WB::BC && ((x0 & 15) == 0) && ((g.W & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(dirs) & 15) == 0);
+  if (vec) {
+    for (int q = lane; q < h * 2; q += 32) {
+      const int ly = q >> 1, lx = (q & 1) * 16;
+      *reinterpret_cast<uint4*>(dirs + (y0 + ly) * g.W + x0 + lx) =
+          *reinterpret_cast<const uint4*>(&s.dirh[WB::hidx(ly, lx)]);
+    }
+  } else {
+    for (int i = lane; i < h * WB::BC; i += 32) {
+      const int ly = i >> 5, lx = i & 31;
+      if (lx < w) dirs[(y0 + ly) * g.W + x0 + lx] = s.dirh[WB::hidx(ly, lx)];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- H4
+// Block exits -> graph nodes (compacted, one global atomic per warp), then
+// Alg. 2 FollowPath from the perimeter cells that need their exit (entries,
+// and in tile-records mode every slot on a tile edge) -> slot_root.  Lane l
+// handles slots l, l+32, l+64, l+96.
+template <class T, int R, int WK>
+__device__ __forceinline__ void block_records(WSmem<T, R>& s, const PassArgs<T, WK>& P, int64_t b, int64_t y0,
+                                              int64_t x0, int h, int w) {
+  using WB = WBT<R>;
+  constexpr int NJ = (WB::PB + 31) / 32;
   const Geom& g = P.g;
-  const int64_t b = blockIdx.x;
+  const int lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  const int np = bperim_count(h, w);
+  uint32_t* slot_nid = s.slot_nid();
+  int cell[NJ];
+  bool ex[NJ];
+  int nex = 0;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int p = lane + 32 * j;
+    cell[j] = -1;
+    ex[j] = false;
+    if (p < np) {
+      int px, py;
+      bperim_xy(p, h, w, px, py);
+      cell[j] = py * WB::BC + px;
+      ex[j] = (s.succ[cell[j]] & SU_EXIT) != 0u && s.dirh[WB::hidx(py, px)] != kNoData;
+    }
+    nex += __popc(__ballot_sync(kFull, ex[j]));
+  }
+  uint32_t base = 0;
+  if (lane == 0 && nex) base = atomicAdd(P.node_count, (uint32_t)nex);
+  base = __shfl_sync(kFull, base, 0);
+  int64_t t0y, t0x, th, tw;
+  g.tile_box(g.tile_of_block(b), t0y, t0x, th, tw);
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int p = lane + 32 * j;
+    const unsigned em = __ballot_sync(kFull, ex[j]);
+    uint32_t nid = kNone;
+    if (ex[j]) {
+      nid = base + (uint32_t)__popc(em & lt);
+      const int px = cell[j] & 31, py = cell[j] >> 5;
+      const int d = s.dirh[WB::hidx(py, px)];
+      const int ty = py + dir_dy(d), tx = px + dir_dx(d);
+      const bool dead = s.dirh[WB::hidx(ty, tx)] == kNoData;
+      const int64_t gy = y0 + ty, gx = x0 + tx;
+      uint8_t fl = dead ? NF_DEAD : 0;
+      if (gy < t0y || gx < t0x || gy >= t0y + th || gx >= t0x + tw) fl |= NF_OUT_TILE;
+      uint32_t tgt = kNone;  // none: dropped, or in another strip (carried by the tile records)
+      if (!dead && gy >= 0 && gy < g.H) {
+        int64_t tb;
+        int tly, tlx, bh, bw;
+        if (g.regular) {
+          // plain block grid: the target block is a neighbour of b
+          const int dby = ty < 0 ? -1 : ty >= h ? 1 : 0, dbx = tx < 0 ? -1 : tx >= w ? 1 : 0;
+          tb = b + (int64_t)dby * g.NBC + dbx;
+          tly = ty - dby * WB::BR;
+          tlx = tx - dbx * WB::BC;
+          const int64_t ty0 = y0 + (int64_t)dby * WB::BR, tx0 = x0 + (int64_t)dbx * WB::BC;
+          bh = (int)(g.H - ty0 < WB::BR ? g.H - ty0 : WB::BR);
+          bw = (int)(g.W - tx0 < WB::BC ? g.W - tx0 : WB::BC);
+        } else {
+          tb = g.block_of(gy, gx, tly, tlx);
+          int64_t by0, bx0;
+          g.block_box(tb, by0, bx0, bh, bw);
+        }
+        tgt = (uint32_t)(tb * WB::PB + bperim_index(tlx, tly, bh, bw));
+      }
+      P.node_val[nid] = s.u.A[cell[j]];
+      P.node_slot[nid] = (uint32_t)(b * WB::PB + p);
+      P.node_tgt[nid] = tgt;
+      P.node_flags[nid] = fl;
+    }
+    if (p < WB::PB) slot_nid[p] = nid;
+    base += (uint32_t)__popc(em);
+  }
+  // which non-exit slots need a walk
+  bool want[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int p = lane + 32 * j;
+    want[j] = false;
+    if (cell[j] >= 0 && !ex[j]) {
+      bool need = s.need[p] != 0;
+      if (P.cut && !need) {  // tile records: every slot on a tile edge
+        const int64_t gy = y0 + (cell[j] >> 5), gx = x0 + (cell[j] & 31);
+        need = gy == t0y || gx == t0x || gy == t0y + th - 1 || gx == t0x + tw - 1;
+      }
+      want[j] = need && s.dirh[WB::hidx(cell[j] >> 5, cell[j] & 31)] != kNoData;
+    }
+  }
+  __syncwarp();
+  // Alg. 2 FollowPath (lanes refill from a warp-uniform work list as they finish)
+  uint32_t wl[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) wl[j] = __ballot_sync(kFull, want[j]);
+  const int nw0 = __popc(wl[0]), nw1 = nw0 + __popc(wl[1]), nw2 = nw1 + __popc(wl[2]);
+  const int nwalk = nw2 + __popc(wl[3]);
+  int head = 0;
+  int p = -1, c = 0;
+  uint32_t su = SU_STOP;
+  for (;;) {
+    const unsigned idle = __ballot_sync(kFull, p < 0);
+    if (idle == kFull && head >= nwalk) break;
+    if (p < 0) {
+      const int r = head + __popc(idle & lt);
+      if (r < nwalk) {
+        // r-th wanted slot: the rr-th set bit of wl[j]
+        int j = 0, rr = r;
+        if (rr >= nw0) { j = 1; rr -= nw0; }
+        if (j == 1 && rr >= nw1 - nw0) { j = 2; rr -= nw1 - nw0; }
+        if (j == 2 && rr >= nw2 - nw1) { j = 3; rr -= nw2 - nw1; }
+        const uint32_t m = j == 0 ? wl[0] : j == 1 ? wl[1] : j == 2 ? wl[2] : wl[3];
+        const int l = __fns(m, 0, rr + 1);
+        p = l + 32 * j;
+        int px, py;
+        bperim_xy(p, h, w, px, py);
+        c = py * WB::BC + px;
+        su = s.succ[c];
+      }
+    }
+    head += __popc(idle);
+    if (p < 0) continue;
+    if (su & SU_STOP) {
+      uint32_t root = kNone;
+      if (su & SU_EXIT) root = slot_nid[bperim_index(c & 31, c >> 5, h, w)];
+      P.slot_root[b * WB::PB + p] = root;
+      p = -1;
+      continue;
+    }
+    c = (int)(su & SU_T);
+    su = s.succ[c];
+  }
+  // exits are their own roots; slots nobody drains into need none
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int p2 = lane + 32 * j;
+    if (p2 < WB::PB && !want[j]) P.slot_root[b * WB::PB + p2] = ex[j] ? slot_nid[p2] : kNone;
+  }
+}
+
+// ---------------------------------------------------------------- pass 1
+template <class T, int R, int WK, bool FROM_DEM>
+__global__ void __launch_bounds__(128) k_pass1(PassArgs<T, WK> P) {
+  using WB = WBT<R>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5;
+  WSmem<T, R>& s = reinterpret_cast<WSmem<T, R>*>(smem)[warp];
+  const Geom& g = P.g;
+  const int64_t b = (int64_t)blockIdx.x * g.nw + warp;
+  if (b >= g.nblocks) return;
+  const int lane = lane_id();
   int64_t y0, x0;
   int h, w;
   g.block_box(b, y0, x0, h, w);
-  const int tid = threadIdx.x;
   if (h <= 0 || w <= 0) {
-    for (int p = tid; p < C::PB; p += C::NT) P.slot_root[b * C::PB + p] = kNone;
+    for (int p = lane; p < WB::PB; p += 32) P.slot_root[b * WB::PB + p] = kNone;
     return;
   }
-  PH_T0;
-  WPre<C, WK> pre;
-  pre.load(P.w, g, y0, x0, h, w);  // in flight during staging, D8 and masks
-  if (tid == 0) s.cnt_exit = s.processed = s.ndata = s.nsrc = s.qhead = 0;
-  init_dirh(s);
+  init_smem(s);
   if (FROM_DEM) {
-    // ---- stage z with its halo (NoData and off-grid -> NaN), then D8 (H1)
-    // full, aligned blocks: each window row = BC/4 float4 loads + 2 halo
-    // scalars; otherwise one scalar per cell (compile-time strides only)
-    const bool zvec = w == C::BC && ((x0 & 3) == 0) && ((g.W & 3) == 0) &&
-                      ((reinterpret_cast<uintptr_t>(P.dem) & 15) == 0) &&
-                      (!P.dem_up || (reinterpret_cast<uintptr_t>(P.dem_up) & 15) == 0) &&
-                      (!P.dem_dn || (reinterpret_cast<uintptr_t>(P.dem_dn) & 15) == 0);
-    if (zvec) {
-      constexpr int Q = C::BC / 4 + 2;  // per window row: BC/4 quads + 2 halo cells
-      for (int i = tid; i < (C::BR + 2) * Q; i += C::NT) {
-        const int r = i / Q, k = i % Q, ly = r - 1;
-        const int64_t gy = y0 + ly;
-        const float* row = (ly > h) ? nullptr
-                           : gy < 0 ? (gy == -1 ? P.dem_up : nullptr)
-                           : gy >= g.H ? (gy == g.H ? P.dem_dn : nullptr)
-                                       : P.dem + gy * g.W;
-        float* zrow = zs + r * C::ZS;
-        if (k < C::BC / 4) {
-          float4 v = make_float4(__int_as_float(0x7fc00000), __int_as_float(0x7fc00000),
-                                 __int_as_float(0x7fc00000), __int_as_float(0x7fc00000));
-          if (row) {
-            v = __ldg(reinterpret_cast<const float4*>(row + x0) + k);
-            v.x = stage_z(v.x, P.nodata); v.y = stage_z(v.y, P.nodata);
-            v.z = stage_z(v.z, P.nodata); v.w = stage_z(v.w, P.nodata);
-          }
-          zrow[1 + 4 * k] = v.x; zrow[2 + 4 * k] = v.y; zrow[3 + 4 * k] = v.z; zrow[4 + 4 * k] = v.w;
-        } else {
-          const int lx = k == C::BC / 4 ? -1 : C::BC;
-          const int64_t gx = x0 + lx;
-          float v = __int_as_float(0x7fc00000);
-          if (row && gx >= 0 && gx < g.W) v = stage_z(row[gx], P.nodata);
-          zrow[lx + 1] = v;
-        }
-      }
-    } else {
-      for (int i = tid; i < C::ZN; i += C::NT) {
-        const int ly = i / C::ZS - 1, lx = i % C::ZS - 1;
-        float v = __int_as_float(0x7fc00000);
-        if (ly <= h && lx <= w) {
-          const int64_t gy = y0 + ly, gx = x0 + lx;
-          if (gx >= 0 && gx < g.W) {
-            const float* row = gy < 0 ? P.dem_up : gy >= g.H ? P.dem_dn : P.dem + gy * g.W;
-            if (row && gy >= -1 && gy <= g.H) v = stage_z(row[gx], P.nodata);
-          }
-        }
-        zs[i] = v;
-      }
-    }
-    __syncthreads();
-    PH_MARK(8);
-    // D8 for the block's cells, 4 per thread: one 32-bit shared store and one
-    // 32-bit global store of the packed codes
-    for (int q = tid; q < C::BN / 4; q += C::NT) {
-      const int ly = (4 * q) / C::BC, lx = (4 * q) % C::BC;
-      if (ly >= h) continue;
-      uint32_t packed = 0xFFFFFFFFu;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (lx + j < w) {
-          const uint32_t code = d8_code<C::ZS>(zs, (ly + 1) * C::ZS + lx + j + 1);
-          packed = (packed & ~(0xFFu << (8 * j))) | (code << (8 * j));
-        }
-      *reinterpret_cast<uint32_t*>(&s.dirh[C::hidx(ly, lx)]) = packed;
-      if (P.dirs_out) {
-        uint8_t* dst = P.dirs_out + (y0 + ly) * g.W + x0 + lx;
-        if (lx + 3 < w && (reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
-          *reinterpret_cast<uint32_t*>(dst) = packed;
-        } else {
-          for (int j = 0; j < 4 && lx + j < w; ++j) dst[j] = (uint8_t)(packed >> (8 * j));
-        }
-      }
-    }
-    __syncthreads();
-    // halo ring: NoData-ness only (after the packed stores, which may cover it)
-    const int rn = 2 * (w + 2) + 2 * h;
-    for (int i = tid; i < rn; i += C::NT) {
-      int ly, lx;
-      if (i < w + 2) { ly = -1; lx = i - 1; }
-      else if (i < 2 * (w + 2)) { ly = h; lx = i - (w + 2) - 1; }
-      else { const int j = i - 2 * (w + 2); ly = j >> 1; lx = (j & 1) ? w : -1; }
-      s.dirh[C::hidx(ly, lx)] = isnan(zs[(ly + 1) * C::ZS + lx + 1]) ? kNoData : kOut;
-    }
-    __syncthreads();  // zs dead from here on; A aliases it
-    PH_MARK(9);
+    stage_z(s, P, y0, x0, h, w);
+    __syncwarp();
+    d8_block(s, h, w);
+    ring_entries(s, P, y0, h, w);
+    __syncwarp();
+    if (P.dirs_out) write_dirs(s, P.dirs_out, g, y0, x0, h, w);
   } else {
-    __syncthreads();
-    load_dirs<C>(s, P.dirs_in, g, y0, x0, h, w, true, P.status);
-    // halo ring: 254 for data outside the block, 255 for NoData / off-grid
-    const int rn = 2 * (w + 2) + 2 * h;
-    for (int i = tid; i < rn; i += C::NT) {
-      int ly, lx;
-      if (i < w + 2) { ly = -1; lx = i - 1; }
-      else if (i < 2 * (w + 2)) { ly = h; lx = i - (w + 2) - 1; }
-      else { const int j = i - 2 * (w + 2); ly = j >> 1; lx = (j & 1) ? w : -1; }
-      const int64_t gy = y0 + ly, gx = x0 + lx;
-      uint8_t code = kNoData;
-      if (gx >= 0 && gx < g.W) {
-        const uint8_t* row = gy < 0 ? P.dirs_up : gy >= g.H ? P.dirs_dn : P.dirs_in + gy * g.W;
-        if (row && gy >= -1 && gy <= g.H && row[gx] != kNoData) code = kOut;
-      }
-      s.dirh[C::hidx(ly, lx)] = code;
-    }
-    __syncthreads();
+    __syncwarp();
+    load_dirs(s, P.dirs_in, P.dirs_up, P.dirs_dn, g, y0, x0, h, w, true, true, P.status);
+    __syncwarp();
+    succ_from_dirs(s, h, w);
   }
-  build_masks<C>(s, h, w);
-  init_values<C, T, WK>(s, A, P.w, pre, g, y0, x0, h, w, P.status, P.wsum);
-  __syncthreads();
-  PH_MARK(10);
-  const uint32_t ret = chain_follow<C, T>(s, A);
-  atomicAdd(&s.processed, ret);
-  __syncthreads();
-  PH_MARK(11);
-  if (tid == 0 && s.processed != s.ndata) atomicOr(P.status, ST_CYCLE);
+  __syncwarp();
+  uint32_t nsrc, pre;
+  const uint32_t ndata = build_masks(s, nsrc, pre);  // z is dead from here on; A aliases it
+  unsigned long long wsum = init_values<T, R, WK>(s, P.w, g, y0, x0, h, w, P.status);
+  const uint32_t ret = walk_block(s, nsrc) + pre;
+  __syncwarp();
+  const uint32_t tot_ret = __reduce_add_sync(kFull, ret), tot_data = __reduce_add_sync(kFull, ndata);
+  if (lane == 0 && tot_ret != tot_data) atomicOr(P.status, ST_CYCLE);
+  if (!std::is_same<T, double>::value && P.wsum) {
+    if (WK == 0) wsum = lane == 0 ? tot_data : 0;
+    for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
+    if (lane == 0 && wsum) atomicAdd(P.wsum, wsum);
+  }
   // RETAIN: the block-local accumulation goes straight to the output;
-  // pass 2 then only adds the offsets along the entry paths (k_retain)
-  if (P.retain) write_block<C, T>(s, A, P.acc, g, y0, x0, h, w);
-  // ---- H4: block exits -> graph nodes (compacted), perimeter links
-  const int np = (int)perim_count(h, w);
-  for (int p = tid; p < C::PB; p += C::NT) {
-    uint32_t r = kNone;
-    if (p < np) {
-      int64_t px, py;
-      perim_xy(p, h, w, px, py);
-      const int d = s.dirh[C::hidx((int)py, (int)px)];
-      if (d >= 1 && d <= 8) {
-        const int ty = (int)py + dir_dy(d), tx = (int)px + dir_dx(d);
-        if ((unsigned)ty >= (unsigned)h || (unsigned)tx >= (unsigned)w) r = atomicAdd(&s.cnt_exit, 1u);
-      }
-    }
-    s.slot_nid[p] = r;  // rank among the block's exits, for now
-  }
-  __syncthreads();
-  if (tid == 0) s.base = s.cnt_exit ? atomicAdd(P.node_count, s.cnt_exit) : 0;
-  __syncthreads();
-  int64_t t0y, t0x, th, tw;
-  g.tile_box(g.tile_of_block(b), t0y, t0x, th, tw);
-  for (int p = tid; p < np; p += C::NT) {
-    const uint32_t rank = s.slot_nid[p];
-    if (rank == kNone) continue;
-    const uint32_t nid = s.base + rank;
-    int64_t px, py;
-    perim_xy(p, h, w, px, py);
-    const int d = s.dirh[C::hidx((int)py, (int)px)];
-    const int ty = (int)py + dir_dy(d), tx = (int)px + dir_dx(d);
-    const bool dead = s.dirh[C::hidx(ty, tx)] == kNoData;
-    const int64_t gy = y0 + ty, gx = x0 + tx;
-    uint8_t fl = dead ? NF_DEAD : 0;
-    if (gy < t0y || gx < t0x || gy >= t0y + th || gx >= t0x + tw) fl |= NF_OUT_TILE;
-    uint32_t tgt = kNone;  // none: dropped, or in another strip (carried by the tile records)
-    if (!dead && gy >= 0 && gy < g.H) {
-      int tly, tlx;
-      const int64_t tb = g.block_of(gy, gx, tly, tlx);
-      int64_t by0, bx0;
-      int bh, bw;
-      g.block_box(tb, by0, bx0, bh, bw);
-      tgt = (uint32_t)(tb * C::PB + perim_index(tlx, tly, bh, bw));
-    }
-    P.node_val[nid] = A[py * C::BC + px];
-    P.node_slot[nid] = (uint32_t)(b * C::PB + p);
-    P.node_tgt[nid] = tgt;
-    P.node_flags[nid] = fl;
-    s.slot_nid[p] = nid;
-  }
-  __syncthreads();
-  PH_MARK(12);
-  // Alg. 2 FollowPath for every block perimeter cell (root exit node or none)
-  for (int p = tid; p < C::PB; p += C::NT) {
-    uint32_t root = kNone;
-    if (p < np) {
-      int64_t cx, cy;
-      perim_xy(p, h, w, cx, cy);
-      int ly = (int)cy, lx = (int)cx;
-      for (int steps = 0; steps <= h * w; ++steps) {
-        const int dd = s.dirh[C::hidx(ly, lx)];
-        if (dd == kNoFlow || dd > 8) break;  // FlowTerminates (NoFlow)
-        const int ny = ly + dir_dy(dd), nx = lx + dir_dx(dd);
-        if ((unsigned)ny >= (unsigned)h || (unsigned)nx >= (unsigned)w) {
-          root = s.slot_nid[perim_index(lx, ly, h, w)];  // (ly, lx) is a block exit
-          break;
-        }
-        if (s.dirh[C::hidx(ny, nx)] == kNoData) break;  // terminates in in-block NoData
-        ly = ny;
-        lx = nx;
-      }
-    }
-    P.slot_root[b * C::PB + p] = root;
-  }
-  __syncthreads();
-  PH_MARK(13);
+  // the finalize then only adds the offsets along the entry paths (k_retain)
+  if (P.retain) write_block(s, P.acc, g, y0, x0, h, w);
+  block_records(s, P, b, y0, x0, h, w);
 }
 
 // ---------------------------------------------------------------- pass 2
-template <class C, class T, int WK>
-__global__ void __launch_bounds__(C::NT) k_pass2(PassArgs<T, WK> P) {
+template <class T, int R, int WK>
+__global__ void __launch_bounds__(128) k_pass2(PassArgs<T, WK> P) {
+  using WB = WBT<R>;
   extern __shared__ __align__(16) unsigned char smem[];
-  T* A = reinterpret_cast<T*>(smem);
-  Smem<C>& s = *reinterpret_cast<Smem<C>*>(smem + SmemSize<C, T>::region);
+  const int warp = threadIdx.x >> 5;
+  WSmem<T, R>& s = reinterpret_cast<WSmem<T, R>*>(smem)[warp];
   const Geom& g = P.g;
-  const int64_t b = blockIdx.x;
+  const int64_t b = (int64_t)blockIdx.x * g.nw + warp;
+  if (b >= g.nblocks) return;
+  const int lane = lane_id();
   int64_t y0, x0;
   int h, w;
   g.block_box(b, y0, x0, h, w);
   if (h <= 0 || w <= 0) return;
-  const int tid = threadIdx.x;
-  PH_T0;
-  WPre<C, WK> pre;
-  pre.load(P.w, g, y0, x0, h, w);  // in flight during staging and masks
-  if (tid == 0) s.processed = s.ndata = s.nsrc = s.qhead = 0;
-  init_dirh(s);  // ring = 255: never a donor, stops walks
-  __syncthreads();
-  load_dirs<C>(s, P.dirs_in, g, y0, x0, h, w, false, P.status);
-  __syncthreads();
-  PH_MARK(0);
-  build_masks<C>(s, h, w);
-  __syncthreads();
-  PH_MARK(1);
-  init_values<C, T, WK>(s, A, P.w, pre, g, y0, x0, h, w, P.status, nullptr);
-  __syncthreads();
-  PH_MARK(2);
+  init_smem(s);
+  __syncwarp();
+  load_dirs(s, P.dirs_in, P.dirs_up, P.dirs_dn, g, y0, x0, h, w, false, false, P.status);
+  __syncwarp();
+  succ_from_dirs(s, h, w);
+  __syncwarp();
+  uint32_t nsrc, pre;
+  const uint32_t ndata = build_masks(s, nsrc, pre);
+  init_values<T, R, WK>(s, P.w, g, y0, x0, h, w, P.status);
+  __syncwarp();
   // inject x at the block perimeter (offset propagation; D12)
-  const int np = (int)perim_count(h, w);
-  for (int p = tid; p < np; p += C::NT) {
-    int64_t px, py;
-    perim_xy(p, h, w, px, py);
-    if (s.dirh[C::hidx((int)py, (int)px)] == kNoData) continue;
-    const T x = P.x_slot[b * C::PB + p];
-    A[py * C::BC + px] = A[py * C::BC + px] + x;
+  const int np = bperim_count(h, w);
+  for (int p = lane; p < np; p += 32) {
+    int px, py;
+    bperim_xy(p, h, w, px, py);
+    if (s.dirh[WB::hidx(py, px)] == kNoData) continue;
+    const T x = P.x_slot[b * WB::PB + p];
+    s.u.A[py * WB::BC + px] = s.u.A[py * WB::BC + px] + x;
   }
-  __syncthreads();
-  PH_MARK(3);
-  const uint32_t ret = chain_follow<C, T>(s, A);
-  atomicAdd(&s.processed, ret);
-  __syncthreads();
-  PH_MARK(4);
-  if (tid == 0 && s.processed != s.ndata) atomicOr(P.status, ST_CYCLE);
-  write_block<C, T>(s, A, P.acc, g, y0, x0, h, w);
-  PH_MARK(5);
+  const uint32_t ret = walk_block(s, nsrc) + pre;
+  __syncwarp();
+  const uint32_t tot_ret = __reduce_add_sync(kFull, ret), tot_data = __reduce_add_sync(kFull, ndata);
+  if (lane == 0 && tot_ret != tot_data) atomicOr(P.status, ST_CYCLE);
+  write_block(s, P.acc, g, y0, x0, h, w);
 }
 
 // ---------------------------------------------------------------- RETAIN finalize
@@ -689,9 +916,9 @@ __global__ void __launch_bounds__(256) k_retain(Geom g, const T* __restrict__ x_
     int h, w;
     g.block_box(b, y0, x0, h, w);
     if (p >= (uint32_t)perim_count(h, w)) continue;
-    int64_t px, py;
-    perim_xy(p, h, w, px, py);
-    int ly = (int)py, lx = (int)px;
+    int px, py;
+    bperim_xy((int)p, h, w, px, py);
+    int ly = py, lx = px;
     int64_t gi = (y0 + ly) * g.W + x0 + lx;
     int d = __ldg(dirs + gi);
     for (int steps = 0; steps <= h * w; ++steps) {
@@ -724,59 +951,45 @@ template cudaError_t launch_retain<unsigned long long>(const Geom&, const unsign
 template cudaError_t launch_retain<double>(const Geom&, const double*, const uint8_t*, double*, cudaStream_t);
 
 // ---------------------------------------------------------------- launchers
-template <class C, class T, int WK>
-cudaError_t launch_pass1_c(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t st) {
-  const size_t sm = SmemSize<C, T>::total;
+template <class T, int R, int WK>
+cudaError_t launch_pass1_r(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t st) {
+  const size_t sm = sizeof(WSmem<T, R>) * (size_t)a.g.nw;
+  const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
   if (from_dem) {
-    auto k = k_pass1<C, T, WK, true>;
+    auto k = k_pass1<T, R, WK, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<(unsigned)a.g.nblocks, C::NT, sm, st>>>(a);
+    k<<<grid, 32 * a.g.nw, sm, st>>>(a);
   } else {
-    auto k = k_pass1<C, T, WK, false>;
+    auto k = k_pass1<T, R, WK, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<(unsigned)a.g.nblocks, C::NT, sm, st>>>(a);
+    k<<<grid, 32 * a.g.nw, sm, st>>>(a);
   }
   return cudaGetLastError();
 }
 
-template <class C, class T, int WK>
-cudaError_t launch_pass2_c(const PassArgs<T, WK>& a, cudaStream_t st) {
-  const size_t sm = SmemSize<C, T>::total;
-  auto k = k_pass2<C, T, WK>;
+template <class T, int R, int WK>
+cudaError_t launch_pass2_r(const PassArgs<T, WK>& a, cudaStream_t st) {
+  const size_t sm = sizeof(WSmem<T, R>) * (size_t)a.g.nw;
+  const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
+  auto k = k_pass2<T, R, WK>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k<<<(unsigned)a.g.nblocks, C::NT, sm, st>>>(a);
+  k<<<grid, 32 * a.g.nw, sm, st>>>(a);
   return cudaGetLastError();
 }
 
-using Cfg32 = Cfg<32, 32, 2>;
-using Cfg32w1 = Cfg<32, 32, 1>;
-using Cfg32w4 = Cfg<32, 32, 4>;
-using Cfg3264 = Cfg<32, 64, 2>;
-using Cfg64 = Cfg<64, 64, 4>;
-using Cfg64w1 = Cfg<64, 64, 1>;
-using Cfg64w2 = Cfg<64, 64, 2>;
-
 template <class T, int WK>
 cudaError_t launch_pass1(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t st) {
-  if (a.g.br == 32 && a.g.bc == 32 && a.g.nw == 1) return launch_pass1_c<Cfg32w1, T, WK>(a, from_dem, st);
-  if (a.g.br == 32 && a.g.bc == 32 && a.g.nw == 4) return launch_pass1_c<Cfg32w4, T, WK>(a, from_dem, st);
-  if (a.g.br == 32 && a.g.bc == 32) return launch_pass1_c<Cfg32, T, WK>(a, from_dem, st);
-  if (a.g.br == 32 && a.g.bc == 64) return launch_pass1_c<Cfg3264, T, WK>(a, from_dem, st);
-  if (a.g.br == 64 && a.g.bc == 64 && a.g.nw == 1) return launch_pass1_c<Cfg64w1, T, WK>(a, from_dem, st);
-  if (a.g.br == 64 && a.g.bc == 64 && a.g.nw == 2) return launch_pass1_c<Cfg64w2, T, WK>(a, from_dem, st);
-  if (a.g.br == 64 && a.g.bc == 64) return launch_pass1_c<Cfg64, T, WK>(a, from_dem, st);
+  if (a.g.bc != 32 || a.g.nw < 1 || a.g.nw > 4) return cudaErrorInvalidValue;
+  if (a.g.br == 32) return launch_pass1_r<T, 32, WK>(a, from_dem, st);
+  if (a.g.br == 16) return launch_pass1_r<T, 16, WK>(a, from_dem, st);
   return cudaErrorInvalidValue;
 }
 
 template <class T, int WK>
 cudaError_t launch_pass2(const PassArgs<T, WK>& a, cudaStream_t st) {
-  if (a.g.br == 32 && a.g.bc == 32 && a.g.nw == 1) return launch_pass2_c<Cfg32w1, T, WK>(a, st);
-  if (a.g.br == 32 && a.g.bc == 32 && a.g.nw == 4) return launch_pass2_c<Cfg32w4, T, WK>(a, st);
-  if (a.g.br == 32 && a.g.bc == 32) return launch_pass2_c<Cfg32, T, WK>(a, st);
-  if (a.g.br == 32 && a.g.bc == 64) return launch_pass2_c<Cfg3264, T, WK>(a, st);
-  if (a.g.br == 64 && a.g.bc == 64 && a.g.nw == 1) return launch_pass2_c<Cfg64w1, T, WK>(a, st);
-  if (a.g.br == 64 && a.g.bc == 64 && a.g.nw == 2) return launch_pass2_c<Cfg64w2, T, WK>(a, st);
-  if (a.g.br == 64 && a.g.bc == 64) return launch_pass2_c<Cfg64, T, WK>(a, st);
+  if (a.g.bc != 32 || a.g.nw < 1 || a.g.nw > 4) return cudaErrorInvalidValue;
+  if (a.g.br == 32) return launch_pass2_r<T, 32, WK>(a, st);
+  if (a.g.br == 16) return launch_pass2_r<T, 16, WK>(a, st);
   return cudaErrorInvalidValue;
 }
 

@@ -22,7 +22,7 @@ constexpr uint32_t kFlowTerminates = 0xFFFFFFFFu;  // Alg. 2 sentinel
 // parameter of the block kernels (block.cu) and a run-time field of Geom.
 constexpr int kBR = 32;  // default block rows
 constexpr int kBC = 32;  // default block cols
-constexpr int kNW = 2;   // default warps per block
+constexpr int kNW = 2;   // default warps (one 32x32 block each) per CTA of the block kernels
 
 // status bits (device flag word)
 constexpr uint32_t ST_BADCODE = 1u;
@@ -65,6 +65,7 @@ struct Geom {
   int64_t GH;        // global raster rows (== H single GPU)
   int br, bc, pb;    // block shape and perimeter slots per block (2(br+bc)-4)
   int nw;            // warps per block kernel CTA
+  int regular;       // blocks tile the tiles exactly (TH % br == 0, TW % bc == 0): a plain block grid
 
   // Block / tile arithmetic in 32 bits (rows, columns, block ids < 2^32 per
   // device); 64-bit integer division is a long instruction sequence on GPUs.
@@ -222,6 +223,7 @@ struct PassArgs {
   T* acc;
   uint32_t* status;
   bool retain;  // pass 1 writes the block-local accumulation into acc (RETAIN)
+  bool cut;     // tile records wanted: slot roots also for every slot on a tile edge
 };
 
 // warp-aggregated append of `v` (if pred) to list[*count]

@@ -1,5 +1,8 @@
 """Tuning sweep (not the benchmark): time fa_accumulate on a config for several
-block shapes (FA_BLOCK) and print per-phase device times."""
+kernel variants and print per-phase device times.
+
+usage: python tools/sweep.py cfg rows "BR=32,WARPS=2,EVICT=0;BR=16,WARPS=4" [tile]
+each variant is a ';'-separated list of FA_* environment settings."""
 import os
 import sys
 import time
@@ -15,7 +18,7 @@ from paper_1608_04431_b200 import fa  # noqa: E402
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
     rows = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] != "0" else None
-    shapes = sys.argv[3].split(",") if len(sys.argv) > 3 else ["32x32", "32x64", "64x64"]
+    shapes = sys.argv[3].split(";") if len(sys.argv) > 3 else ["BR=32"]
     tiles = sys.argv[4] if len(sys.argv) > 4 else None
     t0 = time.time()
     cfg = inputs.make_config(name, rows, rows)
@@ -27,7 +30,9 @@ def main():
     out = torch.empty((cfg.rows, cfg.cols), dtype=fa.TORCH_ACC[fa.ATYPES[cfg.atype]], device="cuda")
     kw = dict(dem=src) if cfg.dem is not None else dict(dirs=src)
     for shape in shapes:
-        os.environ["FA_BLOCK"] = shape
+        for kv in shape.split(","):
+            k, v = kv.split("=")
+            os.environ["FA_" + k] = v
         with fa.Context(0, stream=st, tile=tile) as ctx:
             for _ in range(2):
                 ctx.accumulate(w=w, atype=cfg.atype, out=out, **kw)
