@@ -39,7 +39,8 @@ inline bool use_retain() {
   const char* e = getenv("FA_EVICT");
   return !(e && e[0] == '1');
 }
-cudaError_t launch_d8(const float* dem, int64_t H, int64_t W, float nodata, uint8_t* dirs,
+cudaError_t launch_d8(const float* dem, const float* dem_up, const float* dem_dn, int64_t H, int64_t W,
+                      float nodata, uint8_t* dirs,
                       cudaStream_t st);
 cudaError_t launch_g1_parent(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
                              const uint32_t* slot_root, bool cut, uint32_t* parent);
@@ -330,7 +331,17 @@ fa_status strip_pass1(fa_ctx* ctx, Strip<T>& s, bool cut) {
   CK(cudaMemsetAsync(s.x_slot, 0, slots * sizeof(T), st));
   fa::PassArgs<T, WK> pa = pass_args<T, WK>(ctx, s);
   pa.cut = cut;
-  CK(launch_pass1<T, WK>(pa, s.dem != nullptr, st));
+  // Whole raster on one device: H1 runs as its own kernel (high occupancy),
+  // then pass 1 starts from the directions.  Strips keep D8 fused into pass 1
+  // (its 2-cell halo stands in for the neighbour strip's codes).
+  const char* fused_env = getenv("FA_FUSED");
+  const bool split = s.dem && !cut && !s.dem_up && !s.dem_dn && !(fused_env && fused_env[0] == '1');
+  if (split) {
+    CK(launch_d8(s.dem, nullptr, nullptr, g.H, g.W, s.nodata, s.dirs_buf, st));
+    ++rt.launches;
+    pa.dirs_out = nullptr;
+  }
+  CK(launch_pass1<T, WK>(pa, s.dem != nullptr && !split, st));
   ++rt.launches;
   CK(rt.read(ctx->d_small, 4));
   s.nn = rt.h_cnt[0];
@@ -825,7 +836,7 @@ fa_status fa_flowdirs(fa_ctx* ctx, const float* dem, int64_t rows, int64_t cols,
   CK(stage_in(ctx->st, dem, n * 4, sd));
   CK(stage_out_alloc(ctx->st, dirs, n, so));
   CK(cudaEventRecord(ctx->ev[0], ctx->st));
-  CK(fa::launch_d8((const float*)sd.dev, rows, cols, nodata, (uint8_t*)so.dev, ctx->st));
+  CK(fa::launch_d8((const float*)sd.dev, nullptr, nullptr, rows, cols, nodata, (uint8_t*)so.dev, ctx->st));
   CK(cudaEventRecord(ctx->ev[1], ctx->st));
   if (so.owned) CK(cudaMemcpyAsync(dirs, so.dev, n, cudaMemcpyDeviceToHost, ctx->st));
   if (sd.owned) cudaFreeAsync(sd.dev, ctx->st);

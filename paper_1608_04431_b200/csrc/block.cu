@@ -23,34 +23,32 @@
 // block): only those need an Alg. 2 walk for the block-exit graph.
 //
 // Successor word (u16 per cell, block-local index i = 32*ly + lx):
-//   bit 15 STOP  -- no in-block successor (NoFlow, drops into in-block NoData,
-//                   or leaves the block);
+//   bit 15 STOP  -- no in-block successor (NoFlow, NoData, or leaves the block);
 //   bit 14 EXIT  -- (with STOP) the target is outside the block: a block exit;
+//   bit 13 ND    -- (with STOP) the cell is NoData;
 //   bits 11-13   -- code - 1 (without STOP);
 //   bits 0-10    -- target index (without STOP).
+// A cell draining into an in-block NoData cell keeps that cell as its
+// successor: NoData cells are sinks whose value is never output (D8, D9).
 //
-// H3 scheduling (differs from the paper's FIFO): lockstep
-// walks.  Every lane walks from a source (a data cell with no in-block
-// donor) downstream, adding its value into the next cell and continuing
-// while it is that cell's only donor (plain load/store).  At a junction the
-// walk adds its value into the junction cell with a shared-memory atomic and
-// clears its bit in the cell's pending-donor mask (atomicAnd); the arrival
-// that clears the last bit continues from the junction, whose value is then
-// complete.  Idle lanes take the next sources from the warp's compacted
-// source queue (one ballot per iteration, no atomics).  Visibility: each
-// iteration starts with __syncwarp, and a walk continuing from a junction
-// reads the junction's value only after a second __syncwarp at the end of
-// the iteration in which it cleared the last bit (memory ordering among the
-// warp's lanes).  fp64 sums at junctions follow the arrival order, which the
-// single-warp schedule fixes; results are within the D13 tolerance of any
-// order.
+// H3 scheduling: Alg. 1's queue, level-free.  The warp keeps
+// one FIFO of ready cells in shared memory, seeded with the sources (cells
+// with no in-block donor).  Each iteration every lane pops one ready cell
+// (its value is final), adds the value into its successor with a shared
+// atomic and clears its bit in the successor's pending-donor mask; the lane
+// that clears the last bit appends the successor (ballot + popc, no queue
+// atomics).  One branch-free path per iteration, so all 32 lanes do useful
+// work whenever 32 cells are ready.  Visibility: each iteration starts with
+// __syncwarp (memory ordering among the warp's lanes), and a cell appended
+// in one iteration is popped in a later one.  fp64 sums follow the arrival
+// order, which the single-warp schedule fixes; any order is within D13.
 #include "fa_internal.cuh"
 
 namespace fa {
 
 constexpr uint8_t kOut = 254;  // ring cell: outside the block, data
 
-constexpr uint32_t SU_STOP = 0x8000u, SU_EXIT = 0x4000u, SU_T = 0x07FFu;
+constexpr uint32_t SU_STOP = 0x8000u, SU_EXIT = 0x4000u, SU_ND = 0x2000u, SU_T = 0x07FFu;
 // direction codes (bit k) leaving a cell through its N / S / W / E side
 constexpr uint32_t DM_N = (1u << 1) | (1u << 2) | (1u << 8);
 constexpr uint32_t DM_S = (1u << 4) | (1u << 5) | (1u << 6);
@@ -95,12 +93,10 @@ struct __align__(16) WSmem {
     unsigned char raw[kA > kZ ? kA : kZ];
   } u;
   uint8_t dirh[WB::HN];
-  uint32_t msk4[WB::BN / 4];  // donor masks, one byte per cell
-  uint32_t pend[WB::BN / 4];  // pending-donor masks (atomicAnd); slot -> node id after the walks (PB <= BN/4)
+  uint32_t pend[WB::BN / 4];  // pending in-block donor counts, one byte per cell; slot -> node id afterwards (PB <= BN/4)
   alignas(8) uint16_t succ[WB::BN];
-  uint16_t src[WB::BN];       // source queue (cells with no in-block donor and an in-block successor)
+  uint16_t src[WB::BN];       // ready queue of Alg. 1 (sources first; each cell enters at most once)
   uint8_t need[128];          // perimeter slot needs its exit (an entry, or a tile-edge slot)
-  __device__ __forceinline__ uint8_t msk(int i) const { return reinterpret_cast<const uint8_t*>(msk4)[i]; }
   __device__ __forceinline__ uint32_t* slot_nid() { return pend; }
 };
 
@@ -161,8 +157,7 @@ __device__ __forceinline__ void sh_add(double* p, double v, double cur) {
 // D8 of one cell from its 3x3 window (NaN = NoData / off-grid): steepest
 // strictly-downhill data neighbour, drops fl32(zc - zn) (D5), cardinal vs
 // diagonal by the exact compare 2a^2 > b^2 in fp64 (D4), ties to the lowest
-// code (D2); none -> lowest NaN neighbour (outlet, D3; returned | 16 so the
-// caller knows the target is NoData), else NoFlow (D6).
+// code (D2); none -> lowest NaN neighbour (outlet, D3), else NoFlow (D6).
 __device__ __forceinline__ int d8_window(float zc, float zN, float zNE, float zE, float zSE, float zS,
                                          float zSW, float zW, float zNW) {
   if (isnan(zc)) return kNoData;
@@ -194,18 +189,17 @@ __device__ __forceinline__ int d8_window(float zc, float zN, float zNE, float zE
   else if (isnan(zSW)) k = 6;
   else if (isnan(zW)) k = 7;
   else if (isnan(zNW)) k = 8;
-  return k ? (k | 16) : kNoFlow;
+  return k;
 }
 
-// successor word of in-block cell i with code d (| 16: the target is NoData);
-// `forb` = direction codes that leave the block from this cell
+// successor word of in-block cell i with code d; `forb` = direction codes
+// that leave the block from this cell
 template <int R>
 __device__ __forceinline__ uint32_t succ_word(int i, int d, uint32_t forb) {
-  const int k = d & 15;
-  if (d == kNoData || k == 0) return SU_STOP;
-  if ((forb >> k) & 1u) return SU_STOP | SU_EXIT;
-  if (d & 16) return SU_STOP;  // drops into in-block NoData (D8)
-  return (uint32_t)(i + WBT<R>::offA(k)) | ((uint32_t)(k - 1) << 11);
+  if (d == kNoData) return SU_STOP | SU_ND;
+  if (d == kNoFlow) return SU_STOP;
+  if ((forb >> d) & 1u) return SU_STOP | SU_EXIT;
+  return (uint32_t)(i + WBT<R>::offA(d)) | ((uint32_t)(d - 1) << 11);
 }
 
 __device__ __forceinline__ uint32_t forb_col(int lx, int w) {
@@ -282,7 +276,7 @@ __device__ __forceinline__ void stage_z(WSmem<T, R>& s, const PassArgs<T, WK>& P
 template <class T, int R>
 __device__ __forceinline__ void d8_put(WSmem<T, R>& s, int ly, int lx, int d, uint32_t forb) {
   using WB = WBT<R>;
-  s.dirh[WB::hidx(ly, lx)] = (uint8_t)(d == kNoData ? kNoData : (d & 15));
+  s.dirh[WB::hidx(ly, lx)] = (uint8_t)d;
   s.succ[ly * WB::BC + lx] = (uint16_t)succ_word<R>(ly * WB::BC + lx, d, forb);
 }
 
@@ -344,7 +338,7 @@ __device__ __forceinline__ void ring_entries(WSmem<T, R>& s, const PassArgs<T, W
     } else {
       const int d = d8_window(z[zi], z[zi - WB::ZS], z[zi - WB::ZS + 1], z[zi + 1], z[zi + WB::ZS + 1],
                               z[zi + WB::ZS], z[zi + WB::ZS - 1], z[zi - 1], z[zi - WB::ZS - 1]);
-      ks = (d >= 1 && d <= 8) ? (1u << d) : 0u;  // an outlet fallback (| 16) never points into the block
+      ks = (d >= 1 && d <= 8) ? (1u << d) : 0u;
     }
     while (ks) {
       const int k = __ffs(ks) - 1;
@@ -418,30 +412,31 @@ __device__ __forceinline__ void succ_from_dirs(WSmem<T, R>& s, int h, int w) {
   if (lx >= w) return;
   const uint32_t fc = forb_col(lx, w);
   for (int ly = 0; ly < h; ++ly) {
-    const int hi = WB::hidx(ly, lx);
-    int d = s.dirh[hi];
-    if (d >= 1 && d <= 8 && s.dirh[hi + WB::offH(d)] == kNoData) d |= 16;
+    const int d = s.dirh[WB::hidx(ly, lx)];
     s.succ[ly * WB::BC + lx] = (uint16_t)succ_word<R>(ly * WB::BC + lx, d, fc | forb_row(ly, h));
   }
 }
 
 // ---------------------------------------------------------------- H2
 // Donor masks by an 8-neighbour gather, 4 cells per 32-bit SWAR word (no
-// atomics; Alg. 1 first loop P:L131-148) and the compacted source queue.
-// Sources whose successor is STOP are retired on the spot (their value is
-// final).  Returns this lane's data-cell count; nsrc (warp total) and
-// pre_retired (this lane) by reference.  Ring codes (254/255) never equal a
-// direction, so no bounds tests.
+// atomics; Alg. 1 first loop P:L131-148) and the ready queue seeded with the
+// sources (data cells without in-block donors).  NoData cells keep their
+// masks: they are sinks that become ready like any cell and drain nowhere.
+// The pending counts D(p) (Alg. 1 "dependencies") are the per-byte popcounts
+// of the donor masks.  Returns the number of cells this lane expects through
+// the queue: its data cells plus its NoData sinks (in-block NoData cells with
+// an in-block donor); by reference, the number of sources (warp total).  Ring
+// codes (254/255) never equal a direction, so no bounds tests.
 template <class T, int R>
-__device__ __forceinline__ uint32_t build_masks(WSmem<T, R>& s, uint32_t& nsrc, uint32_t& pre_retired) {
+__device__ __forceinline__ int build_masks(WSmem<T, R>& s, uint32_t& nsrc, int h, int w, int& ndata_out) {
   using WB = WBT<R>;
   constexpr int NQ = WB::BN / 128;  // words per lane
   static_assert(NQ <= 8, "source bits: 4 per word, 32 per lane");
   const int lane = lane_id();
   const uint32_t* D = reinterpret_cast<const uint32_t*>(s.dirh);
-  const uint2* S2 = reinterpret_cast<const uint2*>(s.succ);
   constexpr int RW = WB::HS / 4;
-  uint32_t ndata = 0, pre = 0, srcbits = 0;
+  int ndata = 0, nsink = 0;
+  uint32_t srcbits = 0;
 #pragma unroll
   for (int k = 0; k < NQ; ++k) {
     const int q = k * 32 + lane;  // word: row q/8, cells 4(q%8)..+3
@@ -464,20 +459,21 @@ __device__ __forceinline__ uint32_t build_masks(WSmem<T, R>& s, uint32_t& nsrc, 
     m |= (__vcmpeq4(nSW, 0x02020202u) & 0x01010101u) << 5;
     m |= (__vcmpeq4(nW, 0x03030303u) & 0x01010101u) << 6;
     m |= (__vcmpeq4(nNW, 0x04040404u) & 0x01010101u) << 7;
-    // NoData (255) and cells outside a ragged block (254/255) are not cells
+    // NoData (255) and cells outside a ragged block (254/255) are no sources
     const uint32_t nd = __vcmpgeu4(c1, 0xFEFEFEFEu);
-    m &= ~nd;
-    s.msk4[q] = m;
-    s.pend[q] = m;
+    // per-byte popcount of the masks
+    uint32_t cnt = m - ((m >> 1) & 0x55555555u);
+    cnt = (cnt & 0x33333333u) + ((cnt >> 2) & 0x33333333u);
+    cnt = (cnt + (cnt >> 4)) & 0x0F0F0F0Fu;
+    s.pend[q] = cnt;
+    // in-block positions of the word (a ragged block's outside cells are 255 too)
+    const uint32_t inb = ly >= h ? 0u : lx + 4 <= w ? 0xFFFFFFFFu : lx >= w ? 0u : (0xFFFFFFFFu >> (8 * (lx + 4 - w)));
+    const uint32_t sink = nd & ~__vcmpeq4(m, 0u) & inb;  // NoData with in-block donors
     ndata += 4 - (__popc(nd) >> 3);
+    nsink += __popc(sink) >> 3;
     // sources: one bit per cell (bit 7 of each byte of src4)
     const uint32_t src4 = __vcmpeq4(m, 0u) & ~nd & 0x80808080u;
-    const uint2 sw = S2[q];  // successor words of the 4 cells: STOP bits at 15 / 31
-    const uint32_t stop4 = ((sw.x >> 8) & 0x80u) | ((sw.x >> 16) & 0x8000u) | ((sw.y << 8) & 0x800000u) |
-                           (sw.y & 0x80000000u);
-    pre += __popc(src4 & stop4);
-    const uint32_t walk4 = src4 & ~stop4;
-    srcbits |= (((walk4 >> 7) & 1u) | ((walk4 >> 14) & 2u) | ((walk4 >> 21) & 4u) | ((walk4 >> 28) & 8u)) << (4 * k);
+    srcbits |= (((src4 >> 7) & 1u) | ((src4 >> 14) & 2u) | ((src4 >> 21) & 4u) | ((src4 >> 28) & 8u)) << (4 * k);
   }
   // compact: exclusive scan of the per-lane counts, then each lane writes its cells
   const int cnt = __popc(srcbits);
@@ -495,67 +491,48 @@ __device__ __forceinline__ uint32_t build_masks(WSmem<T, R>& s, uint32_t& nsrc, 
     const int k = bpos >> 2, j = bpos & 3;
     s.src[pos++] = (uint16_t)(4 * (k * 32 + lane) + j);
   }
-  pre_retired = pre;
-  return ndata;
+  ndata_out = ndata;
+  return ndata + nsink;
 }
 
 // ---------------------------------------------------------------- H3
-// Lockstep walks (see the file comment).  On entry succ, masks, pend, the
-// source queue and A (= w [+ x]) are set and visible to the warp.  Returns
-// the number of cells this lane retired.
+// Alg. 1 queue loop (see the file comment).  On entry succ, pend, the queue
+// (sources) and A (= w [+ x]) are set and visible to the warp.  Returns the
+// number of data cells this lane popped (retired).
 template <class T, int R>
-__device__ __forceinline__ uint32_t walk_block(WSmem<T, R>& s, uint32_t nsrc) {
+__device__ __forceinline__ uint32_t kahn_block(WSmem<T, R>& s, uint32_t nsrc) {
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   T* A = s.u.A;
-  uint32_t head = 0, ret = 0;
-  bool live = false;
-  uint32_t su = SU_STOP;  // successor word of the lane's current cell
-  T a = (T)0;             // value of the current cell (final)
-  for (;;) {
+  uint16_t* Q = s.src;
+  uint8_t* D = reinterpret_cast<uint8_t*>(s.pend);
+  uint32_t head = 0, tail = nsrc;
+  while (head < tail) {
     __syncwarp();
-    const unsigned idle = __ballot_sync(kFull, !live);
-    if (idle == kFull && head >= nsrc) break;
-    if (!live) {
-      const uint32_t q = head + (uint32_t)__popc(idle & lt);
-      if (q < nsrc) {
-        const int c = s.src[q];
-        a = A[c];
-        su = s.succ[c];  // never STOP for a queued source
-        live = true;
-        ++ret;
+    const uint32_t q = head + (uint32_t)lane;
+    const bool valid = q < tail;
+    head = tail - head < 32u ? tail : head + 32u;
+    bool ready = false;
+    int t = 0;
+    if (valid) {
+      const int c = Q[q];
+      const uint32_t su = s.succ[c];
+      if ((su & SU_STOP) == 0u) {
+        // "A(n) <- A(n) + A(c)" and "decrement D(n)" (Alg. 1);
+        // A(c) is final: every donor of c was popped in an earlier iteration
+        t = (int)(su & SU_T);
+        sh_add(&A[t], A[c], A[t]);
+        const int sh = (t & 3) * 8;
+        const uint32_t old = atomicAdd(&s.pend[t >> 2], 0u - (1u << sh));
+        ready = ((old >> sh) & 0xFFu) == 1u;  // the last pending donor: n joins the queue
       }
     }
-    head += (uint32_t)__popc(idle);
-    bool jlast = false;
-    int n = 0;
-    if (live) {
-      n = (int)(su & SU_T);
-      const uint32_t m = s.msk(n);
-      const T an = A[n];  // w(n) [+ x(n)] [+ donors already added at a junction]
-      const uint32_t sn = s.succ[n];
-      if ((m & (m - 1)) == 0) {
-        a = an + a;  // sole in-block donor: plain store
-        A[n] = a;
-      } else {
-        sh_add(&A[n], a, an);  // junction: add our value, then clear our pending bit
-        const uint32_t bit = 1u << ((((su >> 11) & 7u) + 4u) & 7u);  // bit of the opposite direction
-        const int sh = (n & 3) * 8;
-        const uint32_t old = atomicAnd(&s.pend[n >> 2], ~(bit << sh));
-        jlast = ((old >> sh) & 0xFFu) == bit;  // we were the last pending donor
-        live = jlast;
-      }
-      if (live) {
-        su = sn;
-        ++ret;
-        live = (sn & SU_STOP) == 0u;
-        jlast = jlast && live;
-      }
-    }
-    __syncwarp();
-    if (jlast) a = A[n];  // every donor's add is visible now
+    const unsigned bm = __ballot_sync(kFull, ready);
+    if (ready) Q[tail + (uint32_t)__popc(bm & lt)] = (uint16_t)t;
+    tail += (uint32_t)__popc(bm);
   }
-  return ret;
+  (void)D;
+  return tail;  // cells popped: data cells + NoData sinks (warp-uniform)
 }
 
 // ---------------------------------------------------------------- values
@@ -837,13 +814,16 @@ __global__ void __launch_bounds__(128) k_pass1(PassArgs<T, WK> P) {
     succ_from_dirs(s, h, w);
   }
   __syncwarp();
-  uint32_t nsrc, pre;
-  const uint32_t ndata = build_masks(s, nsrc, pre);  // z is dead from here on; A aliases it
+  uint32_t nsrc;
+  int ndata;
+  const int nexp = build_masks(s, nsrc, h, w, ndata);  // z is dead from here on; A aliases it
   unsigned long long wsum = init_values<T, R, WK>(s, P.w, g, y0, x0, h, w, P.status);
-  const uint32_t ret = walk_block(s, nsrc) + pre;
+  const uint32_t popped = kahn_block(s, nsrc);
   __syncwarp();
-  const uint32_t tot_ret = __reduce_add_sync(kFull, ret), tot_data = __reduce_add_sync(kFull, ndata);
-  if (lane == 0 && tot_ret != tot_data) atomicOr(P.status, ST_CYCLE);
+  // every data cell (and NoData sink) must pass the queue, else a cycle
+  const int tot_exp = __reduce_add_sync(kFull, nexp);
+  const int tot_data = __reduce_add_sync(kFull, ndata);
+  if (lane == 0 && (int)popped != tot_exp) atomicOr(P.status, ST_CYCLE);
   if (!std::is_same<T, double>::value && P.wsum) {
     if (WK == 0) wsum = lane == 0 ? tot_data : 0;
     for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
@@ -876,8 +856,9 @@ __global__ void __launch_bounds__(128) k_pass2(PassArgs<T, WK> P) {
   __syncwarp();
   succ_from_dirs(s, h, w);
   __syncwarp();
-  uint32_t nsrc, pre;
-  const uint32_t ndata = build_masks(s, nsrc, pre);
+  uint32_t nsrc;
+  int ndata;
+  const int nexp = build_masks(s, nsrc, h, w, ndata);
   init_values<T, R, WK>(s, P.w, g, y0, x0, h, w, P.status);
   __syncwarp();
   // inject x at the block perimeter (offset propagation; D12)
@@ -889,10 +870,10 @@ __global__ void __launch_bounds__(128) k_pass2(PassArgs<T, WK> P) {
     const T x = P.x_slot[b * WB::PB + p];
     s.u.A[py * WB::BC + px] = s.u.A[py * WB::BC + px] + x;
   }
-  const uint32_t ret = walk_block(s, nsrc) + pre;
+  const uint32_t ret = kahn_block(s, nsrc);
   __syncwarp();
-  const uint32_t tot_ret = __reduce_add_sync(kFull, ret), tot_data = __reduce_add_sync(kFull, ndata);
-  if (lane == 0 && tot_ret != tot_data) atomicOr(P.status, ST_CYCLE);
+  const int tot_exp = __reduce_add_sync(kFull, nexp);
+  if (lane == 0 && (int)ret != tot_exp) atomicOr(P.status, ST_CYCLE);
   write_block(s, P.acc, g, y0, x0, h, w);
 }
 
@@ -1004,45 +985,80 @@ FA_INST(double, 0)
 FA_INST(double, 2)
 #undef FA_INST
 
-// ---------------------------------------------------------------- standalone D8 (fa_flowdirs)
-constexpr int DR = 32, DC = 128;  // output tile per CTA
-__global__ void __launch_bounds__(256) k_d8(const float* __restrict__ dem, int64_t H, int64_t W,
-                                            float nodata, uint8_t* __restrict__ dirs) {
-  __shared__ float zs[(DR + 2) * (DC + 2)];
+// ---------------------------------------------------------------- standalone D8
+// H1 as its own kernel (fa_flowdirs, and the first step of the single-device
+// path): a CTA stages a 32 x 128 tile of z with a 1-cell halo (float4 rows),
+// then each thread runs the same d8_window down one column with a rolling
+// 3x3 register window.  No large shared state, so many warps per SM hide the
+// latency of the compare chains.  Rows -1 / H come from dem_up / dem_dn (a
+// strip's halo rows) or are off-grid.
+constexpr int DR = 32, DC = 128, DZS = DC + 8;  // tile rows / cols, staged row stride (interior at col 4)
+__global__ void __launch_bounds__(DC) k_d8(const float* __restrict__ dem, const float* __restrict__ dem_up,
+                                           const float* __restrict__ dem_dn, int64_t H, int64_t W, float nodata,
+                                           uint8_t* __restrict__ dirs) {
+  __shared__ __align__(16) float zs[(DR + 2) * DZS];
   const int64_t y0 = (int64_t)blockIdx.y * DR, x0 = (int64_t)blockIdx.x * DC;
-  for (int i = threadIdx.x; i < (DR + 2) * (DC + 2); i += 256) {
-    const int ly = i / (DC + 2) - 1, lx = i % (DC + 2) - 1;
-    const int64_t gy = y0 + ly, gx = x0 + lx;
-    float v = __int_as_float(0x7fc00000);
-    if (gy >= 0 && gx >= 0 && gy < H && gx < W) v = stage_z(dem[gy * W + gx], nodata);
-    zs[i] = v;
+  const int tid = threadIdx.x;
+  const float qnan = __int_as_float(0x7fc00000);
+  const bool vec = x0 + DC <= W && ((W & 3) == 0) && ((reinterpret_cast<uintptr_t>(dem) & 15) == 0) &&
+                   (!dem_up || (reinterpret_cast<uintptr_t>(dem_up) & 15) == 0) &&
+                   (!dem_dn || (reinterpret_cast<uintptr_t>(dem_dn) & 15) == 0);
+  if (vec) {
+    // per row: 32 float4 + 2 halo scalars
+    for (int i = tid; i < (DR + 2) * (DC / 4 + 2); i += DC) {
+      const int r = i / (DC / 4 + 2), k = i - r * (DC / 4 + 2);
+      const float* row = dem_row(dem, dem_up, dem_dn, H, W, y0 + r - 1);
+      if (k < DC / 4) {
+        float4 v = make_float4(qnan, qnan, qnan, qnan);
+        if (row) {
+          v = __ldg(reinterpret_cast<const float4*>(row + x0) + k);
+          v.x = stage_z(v.x, nodata);
+          v.y = stage_z(v.y, nodata);
+          v.z = stage_z(v.z, nodata);
+          v.w = stage_z(v.w, nodata);
+        }
+        *reinterpret_cast<float4*>(&zs[r * DZS + 4 + 4 * k]) = v;
+      } else {
+        const int lx = k == DC / 4 ? -1 : DC;
+        const int64_t gx = x0 + lx;
+        float v = qnan;
+        if (row && gx >= 0 && gx < W) v = stage_z(__ldg(row + gx), nodata);
+        zs[r * DZS + 4 + lx] = v;
+      }
+    }
+  } else {
+    for (int i = tid; i < (DR + 2) * (DC + 2); i += DC) {
+      const int r = i / (DC + 2), lx = i - r * (DC + 2) - 1;
+      const float* row = dem_row(dem, dem_up, dem_dn, H, W, y0 + r - 1);
+      const int64_t gx = x0 + lx;
+      float v = qnan;
+      if (row && gx >= 0 && gx < W) v = stage_z(__ldg(row + gx), nodata);
+      zs[r * DZS + 4 + lx] = v;
+    }
   }
   __syncthreads();
-  // each thread: 4 consecutive cells of one row -> one 32-bit store when aligned
-  for (int q = threadIdx.x; q < DR * DC / 4; q += 256) {
-    const int ly = q / (DC / 4), lx = (q % (DC / 4)) * 4;
-    const int64_t gy = y0 + ly, gx = x0 + lx;
-    if (gy >= H) continue;
-    uint32_t packed = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint8_t c = d8_code<DC + 2>(zs, (ly + 1) * (DC + 2) + lx + j + 1);
-      packed |= (uint32_t)c << (8 * j);
-    }
-    const int64_t gi = gy * W + gx;
-    if (gx + 3 < W && (gi & 3) == 0) {
-      *reinterpret_cast<uint32_t*>(dirs + gi) = packed;
-    } else {
-      for (int j = 0; j < 4; ++j)
-        if (gx + j < W) dirs[gi + j] = (uint8_t)(packed >> (8 * j));
-    }
+  const int64_t gx = x0 + tid;
+  if (gx >= W) return;
+  const int rows = (int)(H - y0 < DR ? H - y0 : DR);
+  int zi = 4 + tid;
+  float u0 = zs[zi - 1], u1 = zs[zi], u2 = zs[zi + 1];
+  zi += DZS;
+  float c0 = zs[zi - 1], c1 = zs[zi], c2 = zs[zi + 1];
+  uint8_t* out = dirs + y0 * W + gx;
+#pragma unroll 4
+  for (int ly = 0; ly < rows; ++ly) {
+    zi += DZS;
+    const float e0 = zs[zi - 1], e1 = zs[zi], e2 = zs[zi + 1];
+    out[ly * W] = (uint8_t)d8_window(c1, u1, u2, c2, e2, e1, e0, c0, u0);
+    u0 = c0; u1 = c1; u2 = c2;
+    c0 = e0; c1 = e1; c2 = e2;
   }
 }
 
-cudaError_t launch_d8(const float* dem, int64_t H, int64_t W, float nodata, uint8_t* dirs,
-                      cudaStream_t st) {
+cudaError_t launch_d8(const float* dem, const float* dem_up, const float* dem_dn, int64_t H, int64_t W,
+                      float nodata, uint8_t* dirs, cudaStream_t st) {
   dim3 grid((unsigned)((W + DC - 1) / DC), (unsigned)((H + DR - 1) / DR));
-  k_d8<<<grid, 256, 0, st>>>(dem, H, W, nodata, dirs);
+  k_d8<<<grid, DC, 0, st>>>(dem, dem_up, dem_dn, H, W, nodata, dirs);
   return cudaGetLastError();
 }
 

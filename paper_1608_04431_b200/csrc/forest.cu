@@ -17,6 +17,8 @@
 //     children), solved recursively; then S is expanded back.
 // This is rake (peel) + compress (chain jumping) tree contraction, O(log)
 // phases; each phase is a handful of grid-stride kernels.
+#include <cstdlib>
+
 #include "forest.cuh"
 
 namespace fa {
@@ -233,7 +235,7 @@ __global__ void k_set_flag(uint32_t* st, uint32_t f) { atomicOr(st, f); }
 
 constexpr int kMaxLevels = 64;
 constexpr int kMaxJump = 40;
-constexpr int kWalkCap = 512;  // steps per walk before re-queueing (deep chains -> contraction)
+constexpr int kWalkCap = 0;  // steps per walk before re-queueing; 0 = no walk launch (peel rounds, measured faster)
 
 template <class T>
 cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, int level) {
@@ -260,10 +262,14 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
   uint32_t nf = rt.h_cnt[0];
   uint64_t remaining = n;
   bool contracted = false;
-  if (nf > 0) {
+  static const int cap = [] {
+    const char* e = getenv("FA_WALKCAP");
+    return e ? atoi(e) : kWalkCap;
+  }();
+  if (nf > 0 && cap > 0) {
     // bulk of the forest: one launch of capped walks from every leaf
     cudaMemsetAsync(ctr + 1, 0, 2 * sizeof(uint32_t), st);
-    k_walk<T><<<grid_for(nf), 256, 0, st>>>(fa_, nf, parent, val, cnt, done, fb, ctr + 1, ctr + 2, kWalkCap);
+    k_walk<T><<<grid_for(nf), 256, 0, st>>>(fa_, nf, parent, val, cnt, done, fb, ctr + 1, ctr + 2, cap);
     ++rt.launches;
     ++rt.peel_rounds;
     std::swap(fa_, fb);

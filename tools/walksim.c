@@ -66,6 +66,28 @@ int main(int argc, char** argv) {
         int l = (srcq[k] / BC) % L;
         rowq[l * per + rown[l]++] = srcq[k];
       }
+      if (policy == 2) {  // FIFO Kahn: each iteration pops min(L, ready) cells
+        int* q = malloc(sizeof(int) * (BN + 1));
+        int h0 = 0, t0 = 0;
+        for (int k = 0; k < ns; ++k) q[t0++] = srcq[k];
+        long long it2 = 0;
+        while (h0 < t0) {
+          int n = t0 - h0 < L ? t0 - h0 : L;
+          int tt = t0;
+          for (int k = 0; k < n; ++k) {
+            int c = q[h0 + k];
+            int t = succ[c];
+            if (t >= 0 && --pend[t] == 0) q[tt++] = t;
+          }
+          h0 += n; t0 = tt; ++it2;
+          tot_busy += n;
+        }
+        free(q);
+        tot_iter += it2;
+        if (it2 > max_iter) max_iter = it2;
+        tot_cells += BN; tot_src += ns; nblk++;
+        continue;
+      }
       int qh = 0;
       for (int l = 0; l < L; ++l) lane_live[l] = 0;
       long long it = 0, retired = 0;
