@@ -245,6 +245,7 @@ struct Strip {
   T* acc = nullptr;
   float nodata = 0;
   // device state
+  T* acc_tmp = nullptr;   // in-place accumulation buffer when the caller wants no raster
   uint8_t* dirs_buf = nullptr;
   uint32_t* slot_root = nullptr;
   T* node_val = nullptr;
@@ -260,9 +261,11 @@ struct Strip {
   int64_t* dtbase = nullptr;      // local tile slot bases (device)
   void release(fa::Runtime& rt) {
     for (void* p : {(void*)dirs_buf, (void*)slot_root, (void*)node_val, (void*)node_slot, (void*)node_tgt,
-                    (void*)node_flags, (void*)x_slot, (void*)parent, (void*)S, (void*)troot, (void*)dtbase})
+                    (void*)node_flags, (void*)x_slot, (void*)parent, (void*)S, (void*)troot, (void*)dtbase,
+                    (void*)acc_tmp})
       rt.free(p);
     dirs_buf = nullptr;
+    acc_tmp = nullptr;
     slot_root = node_slot = node_tgt = parent = troot = nullptr;
     node_val = x_slot = S = nullptr;
     node_flags = nullptr;
@@ -293,7 +296,7 @@ fa::PassArgs<T, WK> pass_args(fa_ctx* ctx, Strip<T>& s) {
   a.node_flags = s.node_flags;
   a.slot_root = s.slot_root;
   a.x_slot = s.x_slot;
-  a.acc = s.acc;
+  a.acc = s.acc ? s.acc : s.acc_tmp;  // pass 1 accumulates in place (RETAIN)
   a.retain = s.acc != nullptr && fa::use_retain();
   return a;
 }
@@ -320,6 +323,7 @@ fa_status strip_pass1(fa_ctx* ctx, Strip<T>& s, bool cut) {
   if (slots >= (int64_t)0xFFFFFFF0ll)
     return set_err(ctx, FA_E_ARG, "raster too large for one device (block slots exceed 2^32)");
   if (s.dem) s.dirs_buf = rt.alloc<uint8_t>((size_t)(g.H * g.W));
+  if (!s.acc) s.acc_tmp = rt.alloc<T>((size_t)(g.H * g.W));
   s.slot_root = rt.alloc<uint32_t>(slots);
   s.node_val = rt.alloc<T>(slots);
   s.node_slot = rt.alloc<uint32_t>(slots);

@@ -23,25 +23,30 @@
 // block): only those need an Alg. 2 walk for the block-exit graph.
 //
 // Successor word (u16 per cell, block-local index i = 32*ly + lx):
-//   bit 15 STOP  -- no in-block successor (NoFlow, NoData, or leaves the block);
+//   bit 15 STOP  -- no in-block successor (NoFlow, NoData, drains into
+//                   in-block NoData (D8), or leaves the block);
 //   bit 14 EXIT  -- (with STOP) the target is outside the block: a block exit;
-//   bit 13 ND    -- (with STOP) the cell is NoData;
 //   bits 11-13   -- code - 1 (without STOP);
 //   bits 0-10    -- target index (without STOP).
-// A cell draining into an in-block NoData cell keeps that cell as its
-// successor: NoData cells are sinks whose value is never output (D8, D9).
+//
+// Values live in the output raster itself: the block's A(p) are accumulated
+// in place in acc (global memory; the block's rows stay in L2 while the warp
+// works on them), with native global atomics for the pushes.  Shared memory
+// holds only the 1-byte codes, successor words, pending counts and the
+// queue (~7 KB per warp), so many blocks are in flight per SM to hide the
+// L2 latency.  This is RETAIN: acc ends pass 1 holding A_blk.
 //
 // H3 scheduling: Alg. 1's queue, level-free.  The warp keeps
 // one FIFO of ready cells in shared memory, seeded with the sources (cells
 // with no in-block donor).  Each iteration every lane pops one ready cell
-// (its value is final), adds the value into its successor with a shared
-// atomic and clears its bit in the successor's pending-donor mask; the lane
-// that clears the last bit appends the successor (ballot + popc, no queue
+// (its value is final), adds the value into its successor with an atomic
+// and decrements the successor's pending-donor count; the lane that takes
+// the count to zero appends the successor (ballot + popc, no queue
 // atomics).  One branch-free path per iteration, so all 32 lanes do useful
 // work whenever 32 cells are ready.  Visibility: each iteration starts with
-// __syncwarp (memory ordering among the warp's lanes), and a cell appended
-// in one iteration is popped in a later one.  fp64 sums follow the arrival
-// order, which the single-warp schedule fixes; any order is within D13.
+// __syncwarp (memory ordering among the warp's lanes, global memory
+// included), and a cell appended in one iteration is popped in a later one.
+// fp64 sums follow the arrival order; any order is within D13.
 #include "fa_internal.cuh"
 
 namespace fa {
@@ -83,14 +88,11 @@ struct WBT {
   static_assert(BN <= 2048, "11-bit successor index");
 };
 
-template <class T, int R>
+template <class T, int R, bool Z>
 struct __align__(16) WSmem {
   using WB = WBT<R>;
-  static constexpr size_t kA = sizeof(T) * WB::BN, kZ = sizeof(float) * WB::ZN;
-  union __align__(16) {
-    T A[WB::BN];
-    float z[WB::ZN];
-    unsigned char raw[kA > kZ ? kA : kZ];
+  struct __align__(16) U {
+    float z[Z ? WB::ZN : 4];  // z window (fused D8 only)
   } u;
   uint8_t dirh[WB::HN];
   uint32_t pend[WB::BN / 4];  // pending in-block donor counts, one byte per cell; slot -> node id afterwards (PB <= BN/4)
@@ -157,7 +159,8 @@ __device__ __forceinline__ void sh_add(double* p, double v, double cur) {
 // D8 of one cell from its 3x3 window (NaN = NoData / off-grid): steepest
 // strictly-downhill data neighbour, drops fl32(zc - zn) (D5), cardinal vs
 // diagonal by the exact compare 2a^2 > b^2 in fp64 (D4), ties to the lowest
-// code (D2); none -> lowest NaN neighbour (outlet, D3), else NoFlow (D6).
+// code (D2); none -> lowest NaN neighbour (outlet, D3; returned | 16: the
+// target is NoData), else NoFlow (D6).
 __device__ __forceinline__ int d8_window(float zc, float zN, float zNE, float zE, float zSE, float zS,
                                          float zSW, float zW, float zNW) {
   if (isnan(zc)) return kNoData;
@@ -189,17 +192,18 @@ __device__ __forceinline__ int d8_window(float zc, float zN, float zNE, float zE
   else if (isnan(zSW)) k = 6;
   else if (isnan(zW)) k = 7;
   else if (isnan(zNW)) k = 8;
-  return k;
+  return k ? (k | 16) : kNoFlow;
 }
 
-// successor word of in-block cell i with code d; `forb` = direction codes
-// that leave the block from this cell
+// successor word of in-block cell i with code d (| 16: the target is
+// NoData); `forb` = direction codes that leave the block from this cell
 template <int R>
 __device__ __forceinline__ uint32_t succ_word(int i, int d, uint32_t forb) {
-  if (d == kNoData) return SU_STOP | SU_ND;
-  if (d == kNoFlow) return SU_STOP;
-  if ((forb >> d) & 1u) return SU_STOP | SU_EXIT;
-  return (uint32_t)(i + WBT<R>::offA(d)) | ((uint32_t)(d - 1) << 11);
+  const int k = d & 15;
+  if (d == kNoData || k == 0) return SU_STOP;
+  if ((forb >> k) & 1u) return SU_STOP | SU_EXIT;
+  if (d & 16) return SU_STOP;  // drains into in-block NoData: dropped (D8)
+  return (uint32_t)(i + WBT<R>::offA(k)) | ((uint32_t)(k - 1) << 11);
 }
 
 __device__ __forceinline__ uint32_t forb_col(int lx, int w) {
@@ -210,8 +214,8 @@ __device__ __forceinline__ uint32_t forb_row(int ly, int h) {
 }
 
 // ---------------------------------------------------------------- staging
-template <class T, int R>
-__device__ __forceinline__ void init_smem(WSmem<T, R>& s) {
+template <class T, int R, bool Z>
+__device__ __forceinline__ void init_smem(WSmem<T, R, Z>& s) {
   uint32_t* D = reinterpret_cast<uint32_t*>(s.dirh);
   const int lane = lane_id();
   for (int i = lane; i < WBT<R>::HN / 4; i += 32) D[i] = 0xFFFFFFFFu;
@@ -229,8 +233,8 @@ __device__ __forceinline__ const float* dem_row(const float* dem, const float* u
 // z window (block + 2-cell halo; NoData / off-grid -> NaN).  Rows of a strip
 // halo come from dem_up / dem_dn (H7); rows beyond those read as NaN and the
 // ring D8 treats them as unknown (see ring_entries).
-template <class T, int R, int WK>
-__device__ __forceinline__ void stage_z(WSmem<T, R>& s, const PassArgs<T, WK>& P, int64_t y0, int64_t x0, int h,
+template <class T, int R, bool Z, int WK>
+__device__ __forceinline__ void stage_z(WSmem<T, R, Z>& s, const PassArgs<T, WK>& P, int64_t y0, int64_t x0, int h,
                                         int w) {
   using WB = WBT<R>;
   const Geom& g = P.g;
@@ -273,16 +277,16 @@ __device__ __forceinline__ void stage_z(WSmem<T, R>& s, const PassArgs<T, WK>& P
 }
 
 // one in-block cell's D8 -> code + successor word
-template <class T, int R>
-__device__ __forceinline__ void d8_put(WSmem<T, R>& s, int ly, int lx, int d, uint32_t forb) {
+template <class T, int R, bool Z>
+__device__ __forceinline__ void d8_put(WSmem<T, R, Z>& s, int ly, int lx, int d, uint32_t forb) {
   using WB = WBT<R>;
-  s.dirh[WB::hidx(ly, lx)] = (uint8_t)d;
+  s.dirh[WB::hidx(ly, lx)] = (uint8_t)(d == kNoData ? kNoData : (d & 15));
   s.succ[ly * WB::BC + lx] = (uint16_t)succ_word<R>(ly * WB::BC + lx, d, forb);
 }
 
 // D8 down each column with a rolling 3x3 window (codes + successor words)
-template <class T, int R>
-__device__ __forceinline__ void d8_block(WSmem<T, R>& s, int h, int w) {
+template <class T, int R, bool Z>
+__device__ __forceinline__ void d8_block(WSmem<T, R, Z>& s, int h, int w) {
   using WB = WBT<R>;
   const int lx = lane_id();
   if (lx >= w) return;
@@ -316,8 +320,8 @@ __device__ __forceinline__ void d8_block(WSmem<T, R>& s, int h, int w) {
 // 254 data) and, from their D8, which perimeter cells are entries.  A ring
 // cell whose 3x3 window reaches a row this rank does not hold (beyond a strip
 // halo row) has an unknown code: all its in-block neighbours count as entries.
-template <class T, int R, int WK>
-__device__ __forceinline__ void ring_entries(WSmem<T, R>& s, const PassArgs<T, WK>& P, int64_t y0, int h, int w) {
+template <class T, int R, bool Z, int WK>
+__device__ __forceinline__ void ring_entries(WSmem<T, R, Z>& s, const PassArgs<T, WK>& P, int64_t y0, int h, int w) {
   using WB = WBT<R>;
   const float* z = s.u.z;
   const int rn = 2 * (w + 2) + 2 * h;
@@ -338,7 +342,7 @@ __device__ __forceinline__ void ring_entries(WSmem<T, R>& s, const PassArgs<T, W
     } else {
       const int d = d8_window(z[zi], z[zi - WB::ZS], z[zi - WB::ZS + 1], z[zi + 1], z[zi + WB::ZS + 1],
                               z[zi + WB::ZS], z[zi + WB::ZS - 1], z[zi - 1], z[zi - WB::ZS - 1]);
-      ks = (d >= 1 && d <= 8) ? (1u << d) : 0u;
+      ks = (d >= 1 && d <= 8) ? (1u << d) : 0u;  // an outlet fallback (| 16) drains into NoData
     }
     while (ks) {
       const int k = __ffs(ks) - 1;
@@ -352,8 +356,8 @@ __device__ __forceinline__ void ring_entries(WSmem<T, R>& s, const PassArgs<T, W
 // directions from global (pass 2 and pass 1 from dirs) + halo ring; bad
 // codes -> NoData, flagged when `check`; with `entries`, ring codes that
 // point into the block mark entry slots
-template <class T, int R>
-__device__ __forceinline__ void load_dirs(WSmem<T, R>& s, const uint8_t* dirs, const uint8_t* dirs_up,
+template <class T, int R, bool Z>
+__device__ __forceinline__ void load_dirs(WSmem<T, R, Z>& s, const uint8_t* dirs, const uint8_t* dirs_up,
                                           const uint8_t* dirs_dn, const Geom& g, int64_t y0, int64_t x0, int h,
                                           int w, bool check, bool entries, uint32_t* status) {
   using WB = WBT<R>;
@@ -405,14 +409,16 @@ __device__ __forceinline__ void load_dirs(WSmem<T, R>& s, const uint8_t* dirs, c
 }
 
 // successor words from the staged directions
-template <class T, int R>
-__device__ __forceinline__ void succ_from_dirs(WSmem<T, R>& s, int h, int w) {
+template <class T, int R, bool Z>
+__device__ __forceinline__ void succ_from_dirs(WSmem<T, R, Z>& s, int h, int w) {
   using WB = WBT<R>;
   const int lx = lane_id();
   if (lx >= w) return;
   const uint32_t fc = forb_col(lx, w);
   for (int ly = 0; ly < h; ++ly) {
-    const int d = s.dirh[WB::hidx(ly, lx)];
+    const int hi = WB::hidx(ly, lx);
+    int d = s.dirh[hi];
+    if (d >= 1 && d <= 8 && s.dirh[hi + WB::offH(d)] == kNoData) d |= 16;
     s.succ[ly * WB::BC + lx] = (uint16_t)succ_word<R>(ly * WB::BC + lx, d, fc | forb_row(ly, h));
   }
 }
@@ -420,28 +426,24 @@ __device__ __forceinline__ void succ_from_dirs(WSmem<T, R>& s, int h, int w) {
 // ---------------------------------------------------------------- H2
 // Donor masks by an 8-neighbour gather, 4 cells per 32-bit SWAR word (no
 // atomics; Alg. 1 first loop P:L131-148) and the ready queue seeded with the
-// sources (data cells without in-block donors).  NoData cells keep their
-// masks: they are sinks that become ready like any cell and drain nowhere.
-// The pending counts D(p) (Alg. 1 "dependencies") are the per-byte popcounts
-// of the donor masks.  Returns the number of cells this lane expects through
-// the queue: its data cells plus its NoData sinks (in-block NoData cells with
-// an in-block donor); by reference, the number of sources (warp total).  Ring
-// codes (254/255) never equal a direction, so no bounds tests.
-template <class T, int R>
-__device__ __forceinline__ int build_masks(WSmem<T, R>& s, uint32_t& nsrc, int h, int w, int& ndata_out) {
+// sources (data cells without in-block donors).  The pending counts D(p)
+// (Alg. 1 "dependencies") are the per-byte popcounts of the masks.  Returns
+// this lane's data-cell count; by reference, the number of sources (warp
+// total).  Ring codes (254/255) never equal a direction, so no bounds tests.
+template <class T, int R, bool Z>
+__device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc) {
   using WB = WBT<R>;
   constexpr int NQ = WB::BN / 128;  // words per lane
   static_assert(NQ <= 8, "source bits: 4 per word, 32 per lane");
   const int lane = lane_id();
   const uint32_t* D = reinterpret_cast<const uint32_t*>(s.dirh);
   constexpr int RW = WB::HS / 4;
-  int ndata = 0, nsink = 0;
+  int ndata = 0;
   uint32_t srcbits = 0;
 #pragma unroll
   for (int k = 0; k < NQ; ++k) {
     const int q = k * 32 + lane;  // word: row q/8, cells 4(q%8)..+3
-    const int ly = q >> 3, lx = (q & 7) * 4;
-    const int hw = WB::hidx(ly, lx) >> 2;
+    const int hw = WB::hidx(q >> 3, (q & 7) * 4) >> 2;
     const uint32_t u0 = D[hw - RW - 1], u1 = D[hw - RW], u2 = D[hw - RW + 1];
     const uint32_t c0 = D[hw - 1], c1 = D[hw], c2 = D[hw + 1];
     const uint32_t d0 = D[hw + RW - 1], d1 = D[hw + RW], d2 = D[hw + RW + 1];
@@ -459,20 +461,16 @@ __device__ __forceinline__ int build_masks(WSmem<T, R>& s, uint32_t& nsrc, int h
     m |= (__vcmpeq4(nSW, 0x02020202u) & 0x01010101u) << 5;
     m |= (__vcmpeq4(nW, 0x03030303u) & 0x01010101u) << 6;
     m |= (__vcmpeq4(nNW, 0x04040404u) & 0x01010101u) << 7;
-    // NoData (255) and cells outside a ragged block (254/255) are no sources
+    // NoData (255) and cells outside a ragged block (254/255) are not cells
     const uint32_t nd = __vcmpgeu4(c1, 0xFEFEFEFEu);
+    m &= ~nd;
     // per-byte popcount of the masks
     uint32_t cnt = m - ((m >> 1) & 0x55555555u);
     cnt = (cnt & 0x33333333u) + ((cnt >> 2) & 0x33333333u);
     cnt = (cnt + (cnt >> 4)) & 0x0F0F0F0Fu;
     s.pend[q] = cnt;
-    // in-block positions of the word (a ragged block's outside cells are 255 too)
-    const uint32_t inb = ly >= h ? 0u : lx + 4 <= w ? 0xFFFFFFFFu : lx >= w ? 0u : (0xFFFFFFFFu >> (8 * (lx + 4 - w)));
-    const uint32_t sink = nd & ~__vcmpeq4(m, 0u) & inb;  // NoData with in-block donors
     ndata += 4 - (__popc(nd) >> 3);
-    nsink += __popc(sink) >> 3;
-    // sources: one bit per cell (bit 7 of each byte of src4)
-    const uint32_t src4 = __vcmpeq4(m, 0u) & ~nd & 0x80808080u;
+    const uint32_t src4 = __vcmpeq4(m, 0u) & ~nd & 0x80808080u;  // sources: bit 7 of each byte
     srcbits |= (((src4 >> 7) & 1u) | ((src4 >> 14) & 2u) | ((src4 >> 21) & 4u) | ((src4 >> 28) & 8u)) << (4 * k);
   }
   // compact: exclusive scan of the per-lane counts, then each lane writes its cells
@@ -491,21 +489,22 @@ __device__ __forceinline__ int build_masks(WSmem<T, R>& s, uint32_t& nsrc, int h
     const int k = bpos >> 2, j = bpos & 3;
     s.src[pos++] = (uint16_t)(4 * (k * 32 + lane) + j);
   }
-  ndata_out = ndata;
-  return ndata + nsink;
+  return ndata;
 }
 
 // ---------------------------------------------------------------- H3
-// Alg. 1 queue loop (see the file comment).  On entry succ, pend, the queue
-// (sources) and A (= w [+ x]) are set and visible to the warp.  Returns the
-// number of data cells this lane popped (retired).
-template <class T, int R>
-__device__ __forceinline__ uint32_t kahn_block(WSmem<T, R>& s, uint32_t nsrc) {
+// Alg. 1 queue loop (see the file comment).  On entry succ, pend and the
+// queue (sources) are set and A (= w [+ x]) is in the block's rows of acc,
+// all visible to the warp.  Returns the number of cells popped (retired;
+// warp-uniform).
+template <class T>
+__device__ __forceinline__ void g_add(T* p, T v) { atomicAdd(p, v); }
+
+template <class T, int R, bool Z>
+__device__ __forceinline__ uint32_t kahn_block(WSmem<T, R, Z>& s, uint32_t nsrc, T* Ab, int64_t W) {
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
-  T* A = s.u.A;
   uint16_t* Q = s.src;
-  uint8_t* D = reinterpret_cast<uint8_t*>(s.pend);
   uint32_t head = 0, tail = nsrc;
   while (head < tail) {
     __syncwarp();
@@ -521,7 +520,8 @@ __device__ __forceinline__ uint32_t kahn_block(WSmem<T, R>& s, uint32_t nsrc) {
         // "A(n) <- A(n) + A(c)" and "decrement D(n)" (Alg. 1);
         // A(c) is final: every donor of c was popped in an earlier iteration
         t = (int)(su & SU_T);
-        sh_add(&A[t], A[c], A[t]);
+        const T a = __ldcg(Ab + (c >> 5) * W + (c & 31));
+        g_add(Ab + (t >> 5) * W + (t & 31), a);
         const int sh = (t & 3) * 8;
         const uint32_t old = atomicAdd(&s.pend[t >> 2], 0u - (1u << sh));
         ready = ((old >> sh) & 0xFFu) == 1u;  // the last pending donor: n joins the queue
@@ -531,94 +531,78 @@ __device__ __forceinline__ uint32_t kahn_block(WSmem<T, R>& s, uint32_t nsrc) {
     if (ready) Q[tail + (uint32_t)__popc(bm & lt)] = (uint16_t)t;
     tail += (uint32_t)__popc(bm);
   }
-  (void)D;
-  return tail;  // cells popped: data cells + NoData sinks (warp-uniform)
+  __syncwarp();
+  return tail;
 }
 
 // ---------------------------------------------------------------- values
-// A = w (Eq. 1; Alg. 1 "A(c) <- A(c) + 1"); returns Σw over data
-// cells (integer weights; the u32 overflow check, D10)
-template <class T, int R, int WK>
-__device__ __forceinline__ unsigned long long init_values(WSmem<T, R>& s, const void* wp, const Geom& g, int64_t y0,
-                                                          int64_t x0, int h, int w, uint32_t* status) {
+// A = w (Eq. 1; Alg. 1 "A(c) <- A(c) + 1") in the block's rows of
+// acc, NoData cells get the marker (D9); returns Σw over data cells (integer
+// weights; the u32 overflow check, D10)
+template <class T, int R, bool Z, int WK>
+__device__ __forceinline__ unsigned long long init_values(WSmem<T, R, Z>& s, const void* wp, const Geom& g,
+                                                          int64_t y0, int64_t x0, int h, int w, T* out,
+                                                          uint32_t* status) {
   using WB = WBT<R>;
   const int lane = lane_id();
-  T* A = s.u.A;
   unsigned long long wsum = 0;
   bool bad = false;
-  if constexpr (WK == 0) {
-    for (int i = lane; i < WB::BN; i += 32) A[i] = (T)1;
-    return 0;  // Σw = number of data cells, counted by the caller
-  } else {
-    const bool vec = h == WB::BR && w == WB::BC && ((x0 & 3) == 0) && ((g.W & 3) == 0) &&
-                     ((reinterpret_cast<uintptr_t>(wp) & 15) == 0);
-    const uint32_t* W32 = static_cast<const uint32_t*>(wp);
-#pragma unroll 4
-    for (int q = lane; q < WB::BN / 4; q += 32) {
-      const int ly = q >> 3, lx = (q & 7) * 4;
-      const uint32_t dw = *reinterpret_cast<const uint32_t*>(&s.dirh[WB::hidx(ly, lx)]);
-      uint32_t u[4] = {0, 0, 0, 0};
+  const bool vec = w == WB::BC && ((x0 & 3) == 0) && ((g.W & 3) == 0) &&
+                   (WK == 0 || (reinterpret_cast<uintptr_t>(wp) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  const uint32_t* W32 = static_cast<const uint32_t*>(wp);
+  for (int q = lane; q < h * (WB::BC / 4); q += 32) {
+    const int ly = q >> 3, lx = (q & 7) * 4;
+    const uint32_t dw = *reinterpret_cast<const uint32_t*>(&s.dirh[WB::hidx(ly, lx)]);
+    const int64_t gi = (y0 + ly) * g.W + x0 + lx;
+    uint32_t u[4] = {1u, 1u, 1u, 1u};
+    if (WK != 0) {
       if (vec) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(W32 + (y0 + ly) * g.W + x0 + lx));
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(W32 + gi));
         u[0] = v.x; u[1] = v.y; u[2] = v.z; u[3] = v.w;
-      } else if (ly < h) {
+      } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (lx + j < w) u[j] = __ldg(W32 + (y0 + ly) * g.W + x0 + lx + j);
+          if (lx + j < w) u[j] = __ldg(W32 + gi + j);
       }
+    }
+    alignas(16) T v[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const bool data = ((dw >> (8 * j)) & 0xFF) < kOut;  // excludes NoData and cells outside
-        T v;
-        if constexpr (WK == 1) {
-          v = (T)u[j];
-          if (data) wsum += u[j];
-        } else {
-          const float f = __uint_as_float(u[j]);
-          if (data && !weight_ok<WK>(f)) bad = true;
-          v = (T)f;
-        }
-        A[4 * q + j] = v;
+    for (int j = 0; j < 4; ++j) {
+      const int code = (dw >> (8 * j)) & 0xFF;
+      const bool data = code < kOut;  // excludes NoData and cells outside
+      if constexpr (WK == 0) {
+        v[j] = (T)1;
+      } else if constexpr (WK == 1) {
+        v[j] = (T)u[j];
+        if (data) wsum += u[j];
+      } else {
+        const float f = __uint_as_float(u[j]);
+        if (data && !weight_ok<WK>(f)) bad = true;
+        v[j] = (T)f;
       }
+      if (code == kNoData) v[j] = AccT<T>::marker();
+    }
+    if (vec) {
+      if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<uint4*>(out + gi) = *reinterpret_cast<const uint4*>(v);
+      } else {
+        reinterpret_cast<uint4*>(out + gi)[0] = *reinterpret_cast<const uint4*>(&v[0]);
+        reinterpret_cast<uint4*>(out + gi)[1] = *reinterpret_cast<const uint4*>(&v[2]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (lx + j < w) out[gi + j] = v[j];
     }
   }
   if (bad) atomicOr(status, ST_BADWEIGHT);
   return wsum;
 }
 
-// write the block's values A (NoData marker D9), 16-byte stores when aligned
-template <class T, int R>
-__device__ __forceinline__ void write_block(const WSmem<T, R>& s, T* out, const Geom& g, int64_t y0, int64_t x0,
-                                            int h, int w) {
-  using WB = WBT<R>;
-  const int lane = lane_id();
-  const T* A = s.u.A;
-  constexpr int V = 16 / sizeof(T);  // cells per 16-byte store
-  constexpr int PR = WB::BC / V;     // stores per row
-  const bool vec = w == WB::BC && ((x0 % V) == 0) && ((g.W % V) == 0) &&
-                   ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-  if (vec) {
-    for (int q = lane; q < h * PR; q += 32) {
-      const int ly = q / PR, lx = (q % PR) * V;
-      alignas(16) T v[V];
-#pragma unroll
-      for (int j = 0; j < V; ++j)
-        v[j] = s.dirh[WB::hidx(ly, lx + j)] == kNoData ? AccT<T>::marker() : A[ly * WB::BC + lx + j];
-      *reinterpret_cast<uint4*>(out + (y0 + ly) * g.W + x0 + lx) = *reinterpret_cast<const uint4*>(v);
-    }
-  } else {
-    for (int i = lane; i < h * WB::BC; i += 32) {
-      const int ly = i >> 5, lx = i & 31;
-      if (lx >= w) continue;
-      const bool nodata = s.dirh[WB::hidx(ly, lx)] == kNoData;
-      out[(y0 + ly) * g.W + x0 + lx] = nodata ? AccT<T>::marker() : A[i];
-    }
-  }
-}
-
 // the block's D8 codes to global (16-byte rows when aligned)
-template <class T, int R>
-__device__ __forceinline__ void write_dirs(const WSmem<T, R>& s, uint8_t* dirs, const Geom& g, int64_t y0,
+template <class T, int R, bool Z>
+__device__ __forceinline__ void write_dirs(const WSmem<T, R, Z>& s, uint8_t* dirs, const Geom& g, int64_t y0,
                                            int64_t x0, int h, int w) {
   using WB = WBT<R>;
   const int lane = lane_id();
@@ -643,8 +627,8 @@ __device__ __forceinline__ void write_dirs(const WSmem<T, R>& s, uint8_t* dirs, 
 // Alg. 2 FollowPath from the perimeter cells that need their exit (entries,
 // and in tile-records mode every slot on a tile edge) -> slot_root.  Lane l
 // handles slots l, l+32, l+64, l+96.
-template <class T, int R, int WK>
-__device__ __forceinline__ void block_records(WSmem<T, R>& s, const PassArgs<T, WK>& P, int64_t b, int64_t y0,
+template <class T, int R, bool Z, int WK>
+__device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<T, WK>& P, int64_t b, int64_t y0,
                                               int64_t x0, int h, int w) {
   using WB = WBT<R>;
   constexpr int NJ = (WB::PB + 31) / 32;
@@ -708,7 +692,7 @@ __device__ __forceinline__ void block_records(WSmem<T, R>& s, const PassArgs<T, 
         }
         tgt = (uint32_t)(tb * WB::PB + bperim_index(tlx, tly, bh, bw));
       }
-      P.node_val[nid] = s.u.A[cell[j]];
+      P.node_val[nid] = __ldcg(P.acc + (y0 + py) * g.W + x0 + px);
       P.node_slot[nid] = (uint32_t)(b * WB::PB + p);
       P.node_tgt[nid] = tgt;
       P.node_flags[nid] = fl;
@@ -785,9 +769,10 @@ __device__ __forceinline__ void block_records(WSmem<T, R>& s, const PassArgs<T, 
 template <class T, int R, int WK, bool FROM_DEM>
 __global__ void __launch_bounds__(128) k_pass1(PassArgs<T, WK> P) {
   using WB = WBT<R>;
+  constexpr bool Z = FROM_DEM;
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
-  WSmem<T, R>& s = reinterpret_cast<WSmem<T, R>*>(smem)[warp];
+  WSmem<T, R, Z>& s = reinterpret_cast<WSmem<T, R, Z>*>(smem)[warp];
   const Geom& g = P.g;
   const int64_t b = (int64_t)blockIdx.x * g.nw + warp;
   if (b >= g.nblocks) return;
@@ -815,23 +800,17 @@ __global__ void __launch_bounds__(128) k_pass1(PassArgs<T, WK> P) {
   }
   __syncwarp();
   uint32_t nsrc;
-  int ndata;
-  const int nexp = build_masks(s, nsrc, h, w, ndata);  // z is dead from here on; A aliases it
-  unsigned long long wsum = init_values<T, R, WK>(s, P.w, g, y0, x0, h, w, P.status);
-  const uint32_t popped = kahn_block(s, nsrc);
-  __syncwarp();
-  // every data cell (and NoData sink) must pass the queue, else a cycle
-  const int tot_exp = __reduce_add_sync(kFull, nexp);
+  const int ndata = build_masks(s, nsrc);
+  // RETAIN: the block-local accumulation is computed in place in acc
+  unsigned long long wsum = init_values<T, R, Z, WK>(s, P.w, g, y0, x0, h, w, P.acc, P.status);
+  const uint32_t popped = kahn_block(s, nsrc, P.acc + y0 * g.W + x0, g.W);
   const int tot_data = __reduce_add_sync(kFull, ndata);
-  if (lane == 0 && (int)popped != tot_exp) atomicOr(P.status, ST_CYCLE);
+  if (lane == 0 && (int)popped != tot_data) atomicOr(P.status, ST_CYCLE);  // a cell never became ready
   if (!std::is_same<T, double>::value && P.wsum) {
-    if (WK == 0) wsum = lane == 0 ? tot_data : 0;
+    if (WK == 0) wsum = lane == 0 ? (unsigned long long)tot_data : 0;
     for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
     if (lane == 0 && wsum) atomicAdd(P.wsum, wsum);
   }
-  // RETAIN: the block-local accumulation goes straight to the output;
-  // the finalize then only adds the offsets along the entry paths (k_retain)
-  if (P.retain) write_block(s, P.acc, g, y0, x0, h, w);
   block_records(s, P, b, y0, x0, h, w);
 }
 
@@ -841,7 +820,7 @@ __global__ void __launch_bounds__(128) k_pass2(PassArgs<T, WK> P) {
   using WB = WBT<R>;
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
-  WSmem<T, R>& s = reinterpret_cast<WSmem<T, R>*>(smem)[warp];
+  WSmem<T, R, false>& s = reinterpret_cast<WSmem<T, R, false>*>(smem)[warp];
   const Geom& g = P.g;
   const int64_t b = (int64_t)blockIdx.x * g.nw + warp;
   if (b >= g.nblocks) return;
@@ -857,9 +836,8 @@ __global__ void __launch_bounds__(128) k_pass2(PassArgs<T, WK> P) {
   succ_from_dirs(s, h, w);
   __syncwarp();
   uint32_t nsrc;
-  int ndata;
-  const int nexp = build_masks(s, nsrc, h, w, ndata);
-  init_values<T, R, WK>(s, P.w, g, y0, x0, h, w, P.status);
+  const int ndata = build_masks(s, nsrc);
+  init_values<T, R, false, WK>(s, P.w, g, y0, x0, h, w, P.acc, P.status);
   __syncwarp();
   // inject x at the block perimeter (offset propagation; D12)
   const int np = bperim_count(h, w);
@@ -867,14 +845,12 @@ __global__ void __launch_bounds__(128) k_pass2(PassArgs<T, WK> P) {
     int px, py;
     bperim_xy(p, h, w, px, py);
     if (s.dirh[WB::hidx(py, px)] == kNoData) continue;
-    const T x = P.x_slot[b * WB::PB + p];
-    s.u.A[py * WB::BC + px] = s.u.A[py * WB::BC + px] + x;
+    T* a = P.acc + (y0 + py) * g.W + x0 + px;
+    *a = *a + P.x_slot[b * WB::PB + p];
   }
-  const uint32_t ret = kahn_block(s, nsrc);
-  __syncwarp();
-  const int tot_exp = __reduce_add_sync(kFull, nexp);
-  if (lane == 0 && (int)ret != tot_exp) atomicOr(P.status, ST_CYCLE);
-  write_block(s, P.acc, g, y0, x0, h, w);
+  const uint32_t popped = kahn_block(s, nsrc, P.acc + y0 * g.W + x0, g.W);
+  const int tot_data = __reduce_add_sync(kFull, ndata);
+  if (lane == 0 && (int)popped != tot_data) atomicOr(P.status, ST_CYCLE);
 }
 
 // ---------------------------------------------------------------- RETAIN finalize
@@ -934,7 +910,7 @@ template cudaError_t launch_retain<double>(const Geom&, const double*, const uin
 // ---------------------------------------------------------------- launchers
 template <class T, int R, int WK>
 cudaError_t launch_pass1_r(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t st) {
-  const size_t sm = sizeof(WSmem<T, R>) * (size_t)a.g.nw;
+  const size_t sm = (from_dem ? sizeof(WSmem<T, R, true>) : sizeof(WSmem<T, R, false>)) * (size_t)a.g.nw;
   const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
   if (from_dem) {
     auto k = k_pass1<T, R, WK, true>;
@@ -950,7 +926,7 @@ cudaError_t launch_pass1_r(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t
 
 template <class T, int R, int WK>
 cudaError_t launch_pass2_r(const PassArgs<T, WK>& a, cudaStream_t st) {
-  const size_t sm = sizeof(WSmem<T, R>) * (size_t)a.g.nw;
+  const size_t sm = sizeof(WSmem<T, R, false>) * (size_t)a.g.nw;
   const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
   auto k = k_pass2<T, R, WK>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1049,7 +1025,8 @@ __global__ void __launch_bounds__(DC) k_d8(const float* __restrict__ dem, const 
   for (int ly = 0; ly < rows; ++ly) {
     zi += DZS;
     const float e0 = zs[zi - 1], e1 = zs[zi], e2 = zs[zi + 1];
-    out[ly * W] = (uint8_t)d8_window(c1, u1, u2, c2, e2, e1, e0, c0, u0);
+    const int d = d8_window(c1, u1, u2, c2, e2, e1, e0, c0, u0);
+    out[ly * W] = (uint8_t)(d == kNoData ? kNoData : (d & 15));
     u0 = c0; u1 = c1; u2 = c2;
     c0 = e0; c1 = e1; c2 = e2;
   }

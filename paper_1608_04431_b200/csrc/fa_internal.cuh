@@ -22,7 +22,7 @@ constexpr uint32_t kFlowTerminates = 0xFFFFFFFFu;  // Alg. 2 sentinel
 // parameter of the block kernels (block.cu) and a run-time field of Geom.
 constexpr int kBR = 32;  // default block rows
 constexpr int kBC = 32;  // default block cols
-constexpr int kNW = 2;   // default warps (one 32x32 block each) per CTA of the block kernels
+constexpr int kNW = 4;   // default warps (one block each) per CTA of the block kernels (measured best)
 
 // status bits (device flag word)
 constexpr uint32_t ST_BADCODE = 1u;
