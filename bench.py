@@ -30,10 +30,11 @@ import numpy as np  # noqa: E402
 
 METRIC = "D8 flow-accum Gcells/s at 1/2/4/8 B200; achieved % of HBM roofline"
 CFG = "cfg3"
-# algorithmic bytes per cell: method input + output
-BYTES_MIN = 16        # z 4 + w 4 + A 8  (whole path)
-BYTES_PASS1 = 9       # z 4 + w 4 -> dirs 1      (k_pass1: D8 + block accumulation + records)
-BYTES_PASS2 = 13      # dirs 1 + w 4 -> A 8      (k_pass2: offset propagation)
+# algorithmic bytes per cell (DESIGN.md §6 "Roofline"): each kernel's own
+# input + output, once per cell
+BYTES_MIN = 16        # z 4 + w 4 + A 8                    (whole path: method input + output)
+BYTES_D8 = 5          # z 4 -> dirs 1                      (k_d8, H1)
+BYTES_BLOCK = 13      # dirs 1 + w 4 -> A_blk 8 (in place) (k_pass1: H2-H4, RETAIN accumulation + records)
 HBM_FALLBACK = 6650.0
 
 
@@ -209,7 +210,7 @@ def run_gpu(args):
     for _ in range(max(args.warmup, 3)):
         call(dz, dw, acc)
     torch.cuda.synchronize()
-    p1, gr, p2, launches = [], [], [], []
+    p1, gr, p2, launches, kd8, kblk = [], [], [], [], [], []
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -222,6 +223,8 @@ def run_gpu(args):
             p1.append(s["ms_pass1"])
             gr.append(s["ms_graph"])
             p2.append(s["ms_pass2"])
+            kd8.append(s.get("ms_d8", 0.0))
+            kblk.append(s.get("ms_block", 0.0))
             launches.append(s.get("launches", 0))
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -271,7 +274,10 @@ def run_gpu(args):
 
     peak, peak_src = hbm_peak()
     mp1, mgr, mp2 = float(np.mean(p1)), float(np.mean(gr)), float(np.mean(p2))
-    dom, dom_ms, dom_bytes = ("k_pass2", mp2, BYTES_PASS2) if mp2 >= mp1 else ("k_pass1", mp1, BYTES_PASS1)
+    md8, mblk = float(np.mean(kd8)), float(np.mean(kblk))
+    # dominant kernel: the pass-1 block kernel, timed alone by the library with
+    # CUDA events recorded on its launch stream around the launch
+    dom, dom_ms, dom_bytes = "k_pass1", (mblk if mblk > 0 else mp1), BYTES_BLOCK
     achieved = nr * W * dom_bytes / (dom_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -297,6 +303,10 @@ def run_gpu(args):
                                     "achieved": H * W * BYTES_MIN / (ms * 1e-3) / 1e9 / world,
                                     "frac": H * W * BYTES_MIN / (ms * 1e-3) / 1e9 / world / peak}},
         "phases_ms": {"pass1": mp1, "graph": mgr, "pass2": mp2},
+        "kernels": {"k_d8": {"ms": md8, "bytes_per_cell": BYTES_D8,
+                             "achieved_gbs": nr * W * BYTES_D8 / (md8 * 1e-3) / 1e9 if md8 > 0 else None},
+                    "k_pass1": {"ms": mblk, "bytes_per_cell": BYTES_BLOCK,
+                                "achieved_gbs": nr * W * BYTES_BLOCK / (mblk * 1e-3) / 1e9 if mblk > 0 else None}},
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": int(np.sum(launches)) if launches and launches[0] else None,

@@ -146,6 +146,8 @@ typedef struct {
   int64_t peel_rounds, contract_levels, jump_rounds;
   int64_t bytes_exchanged;
   int64_t launches; /* kernels launched by the call */
+  double ms_d8;     /* the standalone D8 kernel (single-device path; 0 when D8 is fused into pass 1) */
+  double ms_block;  /* the pass-1 block kernel alone (k_pass1), last strip */
 } fa_stats;
 FA_API fa_status fa_get_stats(const fa_ctx* ctx, fa_stats* out);
 

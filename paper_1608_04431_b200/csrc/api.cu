@@ -143,7 +143,7 @@ struct fa_ctx {
   std::string err;
   fa::Runtime rt;
   fa_stats stats{};
-  cudaEvent_t ev[6]{};
+  cudaEvent_t ev[8]{};
   uint32_t* d_small = nullptr;  // [0]=node_count [1]=status [2..3]=wsum(u64) [4..15] scratch
   uint32_t* h_small = nullptr;
   // multi-GPU
@@ -340,12 +340,15 @@ fa_status strip_pass1(fa_ctx* ctx, Strip<T>& s, bool cut) {
   // (its 2-cell halo stands in for the neighbour strip's codes).
   const char* fused_env = getenv("FA_FUSED");
   const bool split = s.dem && !cut && !s.dem_up && !s.dem_dn && !(fused_env && fused_env[0] == '1');
+  CK(cudaEventRecord(ctx->ev[4], st));
   if (split) {
     CK(launch_d8(s.dem, nullptr, nullptr, g.H, g.W, s.nodata, s.dirs_buf, st));
     ++rt.launches;
     pa.dirs_out = nullptr;
   }
+  CK(cudaEventRecord(ctx->ev[5], st));
   CK(launch_pass1<T, WK>(pa, s.dem != nullptr && !split, st));
+  CK(cudaEventRecord(ctx->ev[6], st));
   ++rt.launches;
   CK(rt.read(ctx->d_small, 4));
   s.nn = rt.h_cnt[0];
@@ -448,6 +451,12 @@ void record_stats(fa_ctx* ctx, int64_t cells, int64_t blocks, int64_t nodes, int
   S.contract_levels = ctx->rt.contract_levels;
   S.jump_rounds = ctx->rt.jump_rounds;
   S.launches = ctx->rt.launches;
+  float t45 = 0, t56 = 0;
+  if (cudaEventElapsedTime(&t45, ctx->ev[4], ctx->ev[5]) != cudaSuccess) t45 = 0;
+  if (cudaEventElapsedTime(&t56, ctx->ev[5], ctx->ev[6]) != cudaSuccess) t56 = 0;
+  cudaGetLastError();
+  S.ms_d8 = t45;
+  S.ms_block = t56;
 }
 
 void reset_run(fa_ctx* ctx) {

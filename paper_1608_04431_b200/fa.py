@@ -51,7 +51,8 @@ class Stats(ctypes.Structure):
                 ("cells", ctypes.c_int64), ("blocks", ctypes.c_int64), ("graph_nodes", ctypes.c_int64),
                 ("tile_nodes", ctypes.c_int64), ("peel_rounds", ctypes.c_int64),
                 ("contract_levels", ctypes.c_int64), ("jump_rounds", ctypes.c_int64),
-                ("bytes_exchanged", ctypes.c_int64), ("launches", ctypes.c_int64)]
+                ("bytes_exchanged", ctypes.c_int64), ("launches", ctypes.c_int64),
+                ("ms_d8", ctypes.c_double), ("ms_block", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
