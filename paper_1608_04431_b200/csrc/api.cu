@@ -48,6 +48,8 @@ template <class T>
 cudaError_t launch_scatter_x(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
                              const T* S, T* x_slot, bool intra_tile);
 template <class T>
+cudaError_t launch_fold_leaves(cudaStream_t st, int64_t nslots, const T* x_slot, const uint32_t* slot_root, T* S);
+template <class T>
 cudaError_t launch_tile_records(cudaStream_t st, const Geom& g, int64_t nslots, const int64_t* tbase,
                                 const uint8_t* dirs, const uint32_t* slot_root, const uint32_t* troot,
                                 const uint8_t* flags, const uint32_t* node_slot, const T* S1,
@@ -508,6 +510,9 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
     r = check_status(ctx, stat & ~ST_CYCLE, wsum, std::is_same<T, uint32_t>::value);
     if (r != FA_OK) { s.release(rt); cudaStreamSynchronize(st); return r; }
     CK(cudaMemcpyAsync(s.S, s.node_val, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    // leaves were raked in pass 1: their values sit in the entry offsets
+    CK(launch_fold_leaves<T>(st, s.g.nblocks * s.g.pb, s.x_slot, s.slot_root, s.S));
+    ++rt.launches;
     CK(forest_solve<T>(rt, s.nn, s.parent, s.S));
     CK(launch_scatter_x<T>(st, s.nn, s.node_tgt, s.node_flags, s.S, s.x_slot, false));
     ++rt.launches;

@@ -95,10 +95,12 @@ struct __align__(16) WSmem {
     float z[Z ? WB::ZN : 4];  // z window (fused D8 only)
   } u;
   uint8_t dirh[WB::HN];
-  uint32_t pend[WB::BN / 4];  // pending in-block donor counts, one byte per cell; slot -> node id afterwards (PB <= BN/4)
+  // pending in-block donor counts, one byte per cell; after the queue loop:
+  // [0,128) slot -> node id, [128,256) per exit slot: outside donors
+  uint32_t pend[WB::BN / 4 > 256 ? WB::BN / 4 : 256];
   alignas(8) uint16_t succ[WB::BN];
   uint16_t src[WB::BN];       // ready queue of Alg. 1 (sources first; each cell enters at most once)
-  uint8_t need[128];          // perimeter slot needs its exit (an entry, or a tile-edge slot)
+  uint32_t need[128];         // per perimeter slot: donors outside the block (ring cells draining in)
   __device__ __forceinline__ uint32_t* slot_nid() { return pend; }
 };
 
@@ -219,7 +221,7 @@ __device__ __forceinline__ void init_smem(WSmem<T, R, Z>& s) {
   uint32_t* D = reinterpret_cast<uint32_t*>(s.dirh);
   const int lane = lane_id();
   for (int i = lane; i < WBT<R>::HN / 4; i += 32) D[i] = 0xFFFFFFFFu;
-  reinterpret_cast<uint32_t*>(s.need)[lane] = 0u;
+  for (int i = lane; i < 128; i += 32) s.need[i] = 0u;
 }
 
 __device__ __forceinline__ const float* dem_row(const float* dem, const float* up, const float* dn, int64_t H,
@@ -348,7 +350,7 @@ __device__ __forceinline__ void ring_entries(WSmem<T, R, Z>& s, const PassArgs<T
       const int k = __ffs(ks) - 1;
       ks &= ks - 1;
       const int ty = ly + dir_dy(k), tx = lx + dir_dx(k);
-      if ((unsigned)ty < (unsigned)h && (unsigned)tx < (unsigned)w) s.need[bperim_index(tx, ty, h, w)] = 1;
+      if ((unsigned)ty < (unsigned)h && (unsigned)tx < (unsigned)w) atomicAdd(&s.need[bperim_index(tx, ty, h, w)], 1u);
     }
   }
 }
@@ -403,7 +405,7 @@ __device__ __forceinline__ void load_dirs(WSmem<T, R, Z>& s, const uint8_t* dirs
     s.dirh[WB::hidx(ly, lx)] = code == kNoData ? kNoData : kOut;
     if (entries && code >= 1 && code <= 8) {
       const int ty = ly + dir_dy(code), tx = lx + dir_dx(code);
-      if ((unsigned)ty < (unsigned)h && (unsigned)tx < (unsigned)w) s.need[bperim_index(tx, ty, h, w)] = 1;
+      if ((unsigned)ty < (unsigned)h && (unsigned)tx < (unsigned)w) atomicAdd(&s.need[bperim_index(tx, ty, h, w)], 1u);
     }
   }
 }
@@ -623,100 +625,61 @@ __device__ __forceinline__ void write_dirs(const WSmem<T, R, Z>& s, uint8_t* dir
 }
 
 // ---------------------------------------------------------------- H4
-// Block exits -> graph nodes (compacted, one global atomic per warp), then
-// Alg. 2 FollowPath from the perimeter cells that need their exit (entries,
-// and in tile-records mode every slot on a tile edge) -> slot_root.  Lane l
+// Alg. 2 FollowPath from the perimeter cells that need their
+// exit (entries -- cells a ring cell drains into -- and, in tile-records mode,
+// every slot on a tile edge), then the block exits.  An exit's child count in
+// the block-exit graph is the number of outside donors over the entries whose
+// path reaches it; an exit with none (a leaf: ~75 % of exits on cfg3) has its
+// final value already, so outside tile-records mode it is not a graph node:
+// its value goes straight into the offset of its target slot (x_slot, the
+// entry's external inbound flow, D11).  Other exits become nodes (compacted,
+// one global atomic per warp).  slot_root[entry] = node of its exit.  Lane l
 // handles slots l, l+32, l+64, l+96.
 template <class T, int R, bool Z, int WK>
 __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<T, WK>& P, int64_t b, int64_t y0,
                                               int64_t x0, int h, int w) {
   using WB = WBT<R>;
   constexpr int NJ = (WB::PB + 31) / 32;
+  constexpr uint32_t kNoP = 0xFFu;
   const Geom& g = P.g;
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   const int np = bperim_count(h, w);
-  uint32_t* slot_nid = s.slot_nid();
+  uint32_t* slot_nid = s.pend;       // pend is dead after the queue loop
+  uint32_t* nchild = s.pend + 128;   // per exit slot: outside donors of the entries draining to it
+  for (int i = lane; i < 128; i += 32) nchild[i] = 0u;
+  int64_t t0y, t0x, th, tw;
+  g.tile_box(g.tile_of_block(b), t0y, t0x, th, tw);
   int cell[NJ];
-  bool ex[NJ];
-  int nex = 0;
+  bool ex[NJ], want[NJ];
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     const int p = lane + 32 * j;
     cell[j] = -1;
-    ex[j] = false;
+    ex[j] = want[j] = false;
     if (p < np) {
       int px, py;
       bperim_xy(p, h, w, px, py);
       cell[j] = py * WB::BC + px;
-      ex[j] = (s.succ[cell[j]] & SU_EXIT) != 0u && s.dirh[WB::hidx(py, px)] != kNoData;
-    }
-    nex += __popc(__ballot_sync(kFull, ex[j]));
-  }
-  uint32_t base = 0;
-  if (lane == 0 && nex) base = atomicAdd(P.node_count, (uint32_t)nex);
-  base = __shfl_sync(kFull, base, 0);
-  int64_t t0y, t0x, th, tw;
-  g.tile_box(g.tile_of_block(b), t0y, t0x, th, tw);
-#pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-    const int p = lane + 32 * j;
-    const unsigned em = __ballot_sync(kFull, ex[j]);
-    uint32_t nid = kNone;
-    if (ex[j]) {
-      nid = base + (uint32_t)__popc(em & lt);
-      const int px = cell[j] & 31, py = cell[j] >> 5;
-      const int d = s.dirh[WB::hidx(py, px)];
-      const int ty = py + dir_dy(d), tx = px + dir_dx(d);
-      const bool dead = s.dirh[WB::hidx(ty, tx)] == kNoData;
-      const int64_t gy = y0 + ty, gx = x0 + tx;
-      uint8_t fl = dead ? NF_DEAD : 0;
-      if (gy < t0y || gx < t0x || gy >= t0y + th || gx >= t0x + tw) fl |= NF_OUT_TILE;
-      uint32_t tgt = kNone;  // none: dropped, or in another strip (carried by the tile records)
-      if (!dead && gy >= 0 && gy < g.H) {
-        int64_t tb;
-        int tly, tlx, bh, bw;
-        if (g.regular) {
-          // plain block grid: the target block is a neighbour of b
-          const int dby = ty < 0 ? -1 : ty >= h ? 1 : 0, dbx = tx < 0 ? -1 : tx >= w ? 1 : 0;
-          tb = b + (int64_t)dby * g.NBC + dbx;
-          tly = ty - dby * WB::BR;
-          tlx = tx - dbx * WB::BC;
-          const int64_t ty0 = y0 + (int64_t)dby * WB::BR, tx0 = x0 + (int64_t)dbx * WB::BC;
-          bh = (int)(g.H - ty0 < WB::BR ? g.H - ty0 : WB::BR);
-          bw = (int)(g.W - tx0 < WB::BC ? g.W - tx0 : WB::BC);
-        } else {
-          tb = g.block_of(gy, gx, tly, tlx);
-          int64_t by0, bx0;
-          g.block_box(tb, by0, bx0, bh, bw);
-        }
-        tgt = (uint32_t)(tb * WB::PB + bperim_index(tlx, tly, bh, bw));
-      }
-      P.node_val[nid] = __ldcg(P.acc + (y0 + py) * g.W + x0 + px);
-      P.node_slot[nid] = (uint32_t)(b * WB::PB + p);
-      P.node_tgt[nid] = tgt;
-      P.node_flags[nid] = fl;
-    }
-    if (p < WB::PB) slot_nid[p] = nid;
-    base += (uint32_t)__popc(em);
-  }
-  // which non-exit slots need a walk
-  bool want[NJ];
-#pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-    const int p = lane + 32 * j;
-    want[j] = false;
-    if (cell[j] >= 0 && !ex[j]) {
-      bool need = s.need[p] != 0;
+      const bool data = s.dirh[WB::hidx(py, px)] != kNoData;
+      ex[j] = data && (s.succ[cell[j]] & SU_EXIT) != 0u;
+      bool need = s.need[p] != 0u;
       if (P.cut && !need) {  // tile records: every slot on a tile edge
-        const int64_t gy = y0 + (cell[j] >> 5), gx = x0 + (cell[j] & 31);
+        const int64_t gy = y0 + py, gx = x0 + px;
         need = gy == t0y || gx == t0x || gy == t0y + th - 1 || gx == t0x + tw - 1;
       }
-      want[j] = need && s.dirh[WB::hidx(cell[j] >> 5, cell[j] & 31)] != kNoData;
+      want[j] = data && !ex[j] && need;
     }
   }
   __syncwarp();
-  // Alg. 2 FollowPath (lanes refill from a warp-uniform work list as they finish)
+  // exits that are entries themselves count their own outside donors
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int p = lane + 32 * j;
+    if (ex[j] && s.need[p]) atomicAdd(&nchild[p], s.need[p]);
+  }
+  // walks (lanes refill from a warp-uniform work list as they finish); the
+  // root (exit slot or kNoP) of a walked slot p is kept in need[p] afterwards
   uint32_t wl[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
   for (int j = 0; j < NJ; ++j) wl[j] = __ballot_sync(kFull, want[j]);
@@ -748,20 +711,88 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
     head += __popc(idle);
     if (p < 0) continue;
     if (su & SU_STOP) {
-      uint32_t root = kNone;
-      if (su & SU_EXIT) root = slot_nid[bperim_index(c & 31, c >> 5, h, w)];
-      P.slot_root[b * WB::PB + p] = root;
+      uint32_t rp = kNoP;
+      if (su & SU_EXIT) {
+        rp = (uint32_t)bperim_index(c & 31, c >> 5, h, w);
+        const uint32_t k = s.need[p];
+        if (k) atomicAdd(&nchild[rp], k);
+      }
+      s.need[p] = rp;  // only this lane touches need[p] from here on
       p = -1;
       continue;
     }
     c = (int)(su & SU_T);
     su = s.succ[c];
   }
-  // exits are their own roots; slots nobody drains into need none
+  __syncwarp();
+  // exits: leaves push their value to the target slot, the rest become nodes
+  bool node[NJ];
+  int nex = 0;
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     const int p2 = lane + 32 * j;
-    if (p2 < WB::PB && !want[j]) P.slot_root[b * WB::PB + p2] = ex[j] ? slot_nid[p2] : kNone;
+    node[j] = ex[j] && (P.cut || nchild[p2] != 0u);
+    nex += __popc(__ballot_sync(kFull, node[j]));
+  }
+  uint32_t base = 0;
+  if (lane == 0 && nex) base = atomicAdd(P.node_count, (uint32_t)nex);
+  base = __shfl_sync(kFull, base, 0);
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int p2 = lane + 32 * j;
+    const unsigned em = __ballot_sync(kFull, node[j]);
+    uint32_t nid = kNone;
+    if (ex[j]) {
+      const int px = cell[j] & 31, py = cell[j] >> 5;
+      const int d = s.dirh[WB::hidx(py, px)];
+      const int ty = py + dir_dy(d), tx = px + dir_dx(d);
+      const bool dead = s.dirh[WB::hidx(ty, tx)] == kNoData;
+      const int64_t gy = y0 + ty, gx = x0 + tx;
+      uint8_t fl = dead ? NF_DEAD : 0;
+      if (gy < t0y || gx < t0x || gy >= t0y + th || gx >= t0x + tw) fl |= NF_OUT_TILE;
+      uint32_t tgt = kNone;  // none: dropped, or in another strip (carried by the tile records)
+      if (!dead && gy >= 0 && gy < g.H) {
+        int64_t tb;
+        int tly, tlx, bh, bw;
+        if (g.regular) {
+          // plain block grid: the target block is a neighbour of b
+          const int dby = ty < 0 ? -1 : ty >= h ? 1 : 0, dbx = tx < 0 ? -1 : tx >= w ? 1 : 0;
+          tb = b + (int64_t)dby * g.NBC + dbx;
+          tly = ty - dby * WB::BR;
+          tlx = tx - dbx * WB::BC;
+          const int64_t ty0 = y0 + (int64_t)dby * WB::BR, tx0 = x0 + (int64_t)dbx * WB::BC;
+          bh = (int)(g.H - ty0 < WB::BR ? g.H - ty0 : WB::BR);
+          bw = (int)(g.W - tx0 < WB::BC ? g.W - tx0 : WB::BC);
+        } else {
+          tb = g.block_of(gy, gx, tly, tlx);
+          int64_t by0, bx0;
+          g.block_box(tb, by0, bx0, bh, bw);
+        }
+        tgt = (uint32_t)(tb * WB::PB + bperim_index(tlx, tly, bh, bw));
+      }
+      const T a = __ldcg(P.acc + (y0 + py) * g.W + x0 + px);
+      if (node[j]) {
+        nid = base + (uint32_t)__popc(em & lt);
+        P.node_val[nid] = a;
+        P.node_slot[nid] = (uint32_t)(b * WB::PB + p2);
+        P.node_tgt[nid] = tgt;
+        P.node_flags[nid] = fl;
+      } else if (tgt != kNone) {
+        atomic_add(&P.x_slot[tgt], a);  // a leaf: S(e) = A_B(e), nothing flows in from upstream blocks
+      }
+    }
+    if (p2 < WB::PB) slot_nid[p2] = nid;
+    base += (uint32_t)__popc(em);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int p2 = lane + 32 * j;
+    if (p2 >= WB::PB) continue;
+    uint32_t root = kNone;
+    if (ex[j]) root = slot_nid[p2];
+    else if (want[j] && s.need[p2] != kNoP) root = slot_nid[s.need[p2]];
+    P.slot_root[b * WB::PB + p2] = root;
   }
 }
 

@@ -219,7 +219,7 @@ struct PassArgs {
   uint32_t* slot_root;
   unsigned long long* wsum;
   // pass 2 inputs / outputs
-  const T* x_slot;
+  T* x_slot;              // offsets per block slot (pass 1 adds leaf exits into it; pass 2 reads it)
   T* acc;
   uint32_t* status;
   bool retain;  // pass 1 writes the block-local accumulation into acc (RETAIN)

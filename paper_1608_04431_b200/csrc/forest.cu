@@ -17,6 +17,7 @@
 //     children), solved recursively; then S is expanded back.
 // This is rake (peel) + compress (chain jumping) tree contraction, O(log)
 // phases; each phase is a handful of grid-stride kernels.
+#include <cstdio>
 #include <cstdlib>
 
 #include "forest.cuh"
@@ -233,6 +234,12 @@ __global__ void k_expand(uint32_t m, const uint32_t* __restrict__ R, const uint3
 
 __global__ void k_set_flag(uint32_t* st, uint32_t f) { atomicOr(st, f); }
 
+inline int env_int(const char* name, int dflt, int lo = 0) {
+  const char* e = getenv(name);
+  const int v = e ? atoi(e) : dflt;
+  return v < lo ? dflt : v;
+}
+
 constexpr int kMaxLevels = 64;
 constexpr int kMaxJump = 40;
 constexpr int kWalkCap = 0;  // steps per walk before re-queueing; 0 = no walk launch (peel rounds, measured faster)
@@ -262,10 +269,7 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
   uint32_t nf = rt.h_cnt[0];
   uint64_t remaining = n;
   bool contracted = false;
-  static const int cap = [] {
-    const char* e = getenv("FA_WALKCAP");
-    return e ? atoi(e) : kWalkCap;
-  }();
+  const int cap = env_int("FA_WALKCAP", kWalkCap);  // tuning override (read per call)
   if (nf > 0 && cap > 0) {
     // bulk of the forest: one launch of capped walks from every leaf
     cudaMemsetAsync(ctr + 1, 0, 2 * sizeof(uint32_t), st);
@@ -278,7 +282,8 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
     remaining -= rt.h_cnt[1];
   }
   while (nf > 0 && !rt.err) {
-    if ((uint64_t)nf * 8 < remaining) {
+    const uint64_t ratio = (uint64_t)env_int("FA_CONTRACT_RATIO", 8, 1);  // tuning override
+    if ((uint64_t)nf * ratio < remaining) {
       // ---------------- contract the residual forest
       contracted = true;
       ++rt.contract_levels;
@@ -356,6 +361,8 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
     remaining -= nf;
     std::swap(fa_, fb);
     rt.read(ctr + 1, 1);
+    if (env_int("FA_DEBUG_GRAPH", 0)) fprintf(stderr, "level %d peel: frontier %u remaining %llu\n", level, nf,
+                                              (unsigned long long)remaining);
     nf = rt.h_cnt[0];
   }
   if (!contracted && remaining != 0) k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);

@@ -49,6 +49,23 @@ __global__ void k_scatter_x(uint32_t nn, const uint32_t* __restrict__ tgt, const
   }
 }
 
+// Leaf exits (no inflow from upstream blocks) are not graph nodes: pass 1
+// added their final value straight into the offset of their target slot.
+// Fold those offsets into the graph value of the node the entry drains to,
+// so the node's subtree sum includes them (P:L215-222 with the leaves
+// raked in pass 1).
+template <class T>
+__global__ void k_fold_leaves(int64_t nslots, const T* __restrict__ x_slot, const uint32_t* __restrict__ slot_root,
+                              T* S) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const T x = x_slot[s];
+    if (x == (T)0) continue;
+    const uint32_t e = slot_root[s];
+    if (e != kNone) atomic_add(&S[e], x);  // kNone: the entry's path ends in-block (NoFlow / NoData)
+  }
+}
+
 // H4 tile perimeter records of one strip: F (direction), L (Alg. 2 link) and
 // A_T (tile-local accumulation, at FlowExternal slots) per tile perimeter slot
 template <class T>
@@ -182,6 +199,16 @@ cudaError_t launch_g1_parent(cudaStream_t st, uint32_t nn, const uint32_t* tgt, 
   k_g1_parent<<<grid_for(nn), 256, 0, st>>>(nn, tgt, flags, slot_root, cut, parent);
   return cudaGetLastError();
 }
+
+template <class T>
+cudaError_t launch_fold_leaves(cudaStream_t st, int64_t nslots, const T* x_slot, const uint32_t* slot_root, T* S) {
+  k_fold_leaves<T><<<grid_for(nslots), 256, 0, st>>>(nslots, x_slot, slot_root, S);
+  return cudaGetLastError();
+}
+template cudaError_t launch_fold_leaves<uint32_t>(cudaStream_t, int64_t, const uint32_t*, const uint32_t*, uint32_t*);
+template cudaError_t launch_fold_leaves<unsigned long long>(cudaStream_t, int64_t, const unsigned long long*,
+                                                            const uint32_t*, unsigned long long*);
+template cudaError_t launch_fold_leaves<double>(cudaStream_t, int64_t, const double*, const uint32_t*, double*);
 
 template <class T>
 cudaError_t launch_scatter_x(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
