@@ -885,53 +885,127 @@ __global__ void __launch_bounds__(128) k_pass2(PassArgs<T, WK> P) {
 }
 
 // ---------------------------------------------------------------- RETAIN finalize
-// "add A' to every cell in its downstream flow path" (Alg. 3): one
-// thread per block entry slot with a non-zero offset x walks the entry's
-// in-block path, adding x to every cell up to the block exit (or the NoFlow
-// terminal; flow into NoData is dropped).  acc already holds the block-local
-// accumulation written by pass 1, so A = A_blk + sum of the offsets whose path
-// passes the cell (linearity, D12).  Offsets on shared path segments sum.
-template <class T>
-__global__ void __launch_bounds__(256) k_retain(Geom g, const T* __restrict__ x_slot,
-                                                const uint8_t* __restrict__ dirs, T* acc) {
-  const int64_t nslots = g.nblocks * g.pb;
-  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    const T x = x_slot[s];
-    if (x == (T)0) continue;
-    const uint32_t b = (uint32_t)s / (uint32_t)g.pb, p = (uint32_t)s - b * (uint32_t)g.pb;
-    int64_t y0, x0;
-    int h, w;
-    g.block_box(b, y0, x0, h, w);
-    if (p >= (uint32_t)perim_count(h, w)) continue;
-    int px, py;
-    bperim_xy((int)p, h, w, px, py);
-    int ly = py, lx = px;
-    int64_t gi = (y0 + ly) * g.W + x0 + lx;
-    int d = __ldg(dirs + gi);
-    for (int steps = 0; steps <= h * w; ++steps) {
-      atomic_add(&acc[gi], x);
-      if (d == kNoFlow || d > 8) break;
-      const int ny = ly + dir_dy(d), nx = lx + dir_dx(d);
-      if ((unsigned)ny >= (unsigned)h || (unsigned)nx >= (unsigned)w) break;  // leaves the block
-      const int64_t ni = gi + dir_dy(d) * g.W + dir_dx(d);
-      const int nd = __ldg(dirs + ni);
-      if (nd == kNoData) break;  // dropped (D8)
-      ly = ny;
-      lx = nx;
-      gi = ni;
-      d = nd;
+// "add A' to every cell in its downstream flow path" (Alg. 3): acc
+// already holds the block-local accumulation written by pass 1.  A warp owns
+// KB consecutive blocks: it stages their codes in shared memory, compacts
+// the entry slots with a non-zero offset x (x = external inbound flow, D11)
+// into a work list, and its lanes walk those entries' in-block paths, adding
+// x to every cell up to the block exit or the NoFlow terminal (flow into
+// NoData is dropped, D8) with fire-and-forget global atomics; a lane whose
+// walk ends takes the next entry.  A = A_B + the offsets whose path passes
+// the cell (linearity, D12).
+template <class T, int R, int KB>
+struct __align__(16) FSmem {
+  using WB = WBT<R>;
+  uint8_t d[KB][WB::BN];                 // codes of the KB blocks (row stride 32)
+  uint16_t item[KB * WB::PB];            // work list: (block-in-group << 8) | slot
+};
+
+template <class T, int R, int KB>
+__global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ x_slot, const uint8_t* __restrict__ dirs,
+                                                  T* acc) {
+  using WB = WBT<R>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5;
+  FSmem<T, R, KB>& s = reinterpret_cast<FSmem<T, R, KB>*>(smem)[warp];
+  const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * KB;
+  if (b0 >= g.nblocks) return;
+  const int lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  int64_t y0s[KB], x0s[KB];
+  int hs[KB], ws[KB];
+  int n = 0;  // work items (warp-uniform)
+#pragma unroll
+  for (int k = 0; k < KB; ++k) {
+    const int64_t b = b0 + k;
+    hs[k] = ws[k] = 0;
+    y0s[k] = x0s[k] = 0;
+    if (b < g.nblocks) g.block_box(b, y0s[k], x0s[k], hs[k], ws[k]);
+    const int np = bperim_count(hs[k], ws[k]);
+    for (int p0 = 0; p0 < WB::PB; p0 += 32) {
+      const int p = p0 + lane;
+      const bool act = p < np && x_slot[b * WB::PB + p] != (T)0;
+      const unsigned m = __ballot_sync(kFull, act);
+      if (act) s.item[n + __popc(m & lt)] = (uint16_t)((k << 8) | p);
+      n += __popc(m);
+    }
+    if (hs[k] <= 0 || ws[k] <= 0) continue;
+    // codes: 16-byte rows when aligned
+    const int h = hs[k], w = ws[k];
+    const bool vec = w == WB::BC && ((x0s[k] & 15) == 0) && ((g.W & 15) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(dirs) & 15) == 0);
+    if (vec) {
+      for (int q = lane; q < h * 2; q += 32) {
+        const int ly = q >> 1, lx = (q & 1) * 16;
+        *reinterpret_cast<uint4*>(&s.d[k][ly * WB::BC + lx]) =
+            __ldg(reinterpret_cast<const uint4*>(dirs + (y0s[k] + ly) * g.W + x0s[k] + lx));
+      }
+    } else {
+      for (int i = lane; i < h * WB::BC; i += 32) {
+        const int ly = i >> 5, lx = i & 31;
+        if (lx < w) s.d[k][i] = dirs[(y0s[k] + ly) * g.W + x0s[k] + lx];
+      }
+    }
+  }
+  __syncwarp();
+  // walks
+  int head = 0, k = -1, cy = 0, cx = 0, h = 0, w = 0;
+  T x = (T)0;
+  T* rowp = nullptr;  // acc + y0 * W + x0 of the walk's block
+  for (;;) {
+    const unsigned idle = __ballot_sync(kFull, k < 0);
+    if (idle == kFull && head >= n) break;
+    if (k < 0) {
+      const int r = head + __popc(idle & lt);
+      if (r < n) {
+        const int it = s.item[r];
+        k = it >> 8;
+        const int p = it & 0xFF;
+        int kk = 0;
+#pragma unroll
+        for (int j = 1; j < KB; ++j) kk = k == j ? j : kk;
+        h = hs[0]; w = ws[0];
+        int64_t yy = y0s[0], xx = x0s[0];
+#pragma unroll
+        for (int j = 1; j < KB; ++j)
+          if (kk == j) { h = hs[j]; w = ws[j]; yy = y0s[j]; xx = x0s[j]; }
+        x = x_slot[(b0 + k) * WB::PB + p];
+        rowp = acc + yy * g.W + xx;
+        bperim_xy(p, h, w, cx, cy);
+      }
+    }
+    head += __popc(idle);
+    if (k < 0) continue;
+    atomic_add(rowp + (int64_t)cy * g.W + cx, x);
+    const int d = s.d[k][cy * WB::BC + cx];
+    const int ty = cy + dir_dy(d), tx = cx + dir_dx(d);
+    if (d == kNoFlow || d > 8 || (unsigned)ty >= (unsigned)h || (unsigned)tx >= (unsigned)w ||
+        s.d[k][ty * WB::BC + tx] == kNoData) {
+      k = -1;  // terminal, block exit, or dropped into NoData
+    } else {
+      cy = ty;
+      cx = tx;
     }
   }
 }
 
+template <class T, int R>
+cudaError_t launch_finalize_r(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st) {
+  constexpr int KB = 4, NWC = 4;  // blocks per warp, warps per CTA
+  const size_t sm = sizeof(FSmem<T, R, KB>) * NWC;
+  auto k = k_finalize<T, R, KB>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int64_t groups = (g.nblocks + KB - 1) / KB;
+  k<<<(unsigned)((groups + NWC - 1) / NWC), 32 * NWC, sm, st>>>(g, x_slot, dirs, acc);
+  return cudaGetLastError();
+}
+
 template <class T>
 cudaError_t launch_retain(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st) {
-  const int64_t n = g.nblocks * g.pb;
-  int64_t grid = (n + 255) / 256;
-  if (grid > 148 * 32) grid = 148 * 32;
-  k_retain<T><<<(unsigned)(grid < 1 ? 1 : grid), 256, 0, st>>>(g, x_slot, dirs, acc);
-  return cudaGetLastError();
+  if (g.bc != 32) return cudaErrorInvalidValue;
+  if (g.br == 32) return launch_finalize_r<T, 32>(g, x_slot, dirs, acc, st);
+  if (g.br == 16) return launch_finalize_r<T, 16>(g, x_slot, dirs, acc, st);
+  return cudaErrorInvalidValue;
 }
 template cudaError_t launch_retain<uint32_t>(const Geom&, const uint32_t*, const uint8_t*, uint32_t*, cudaStream_t);
 template cudaError_t launch_retain<unsigned long long>(const Geom&, const unsigned long long*, const uint8_t*,
