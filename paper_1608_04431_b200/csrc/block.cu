@@ -47,6 +47,8 @@
 // __syncwarp (memory ordering among the warp's lanes, global memory
 // included), and a cell appended in one iteration is popped in a later one.
 // fp64 sums follow the arrival order; any order is within D13.
+#include <cstdlib>
+
 #include "fa_internal.cuh"
 
 namespace fa {
@@ -989,15 +991,25 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
   }
 }
 
-template <class T, int R>
-cudaError_t launch_finalize_r(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st) {
-  constexpr int KB = 4, NWC = 4;  // blocks per warp, warps per CTA
+template <class T, int R, int KB>
+cudaError_t launch_finalize_k(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st) {
+  constexpr int NWC = 4;  // warps per CTA
   const size_t sm = sizeof(FSmem<T, R, KB>) * NWC;
   auto k = k_finalize<T, R, KB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int64_t groups = (g.nblocks + KB - 1) / KB;
   k<<<(unsigned)((groups + NWC - 1) / NWC), 32 * NWC, sm, st>>>(g, x_slot, dirs, acc);
   return cudaGetLastError();
+}
+
+template <class T, int R>
+cudaError_t launch_finalize_r(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st) {
+  const char* e = getenv("FA_FINKB");  // tuning override: blocks per warp
+  const int kb = e ? atoi(e) : 2;
+  if (kb == 2) return launch_finalize_k<T, R, 2>(g, x_slot, dirs, acc, st);
+  if (kb == 8) return launch_finalize_k<T, R, 8>(g, x_slot, dirs, acc, st);
+  if (kb == 4) return launch_finalize_k<T, R, 4>(g, x_slot, dirs, acc, st);
+  return launch_finalize_k<T, R, 2>(g, x_slot, dirs, acc, st);
 }
 
 template <class T>
@@ -1137,10 +1149,141 @@ __global__ void __launch_bounds__(DC) k_d8(const float* __restrict__ dem, const 
   }
 }
 
+// D8 from precomputed drops (same rule as d8_window): centre NaN -> NoData;
+// a NaN drop means a NaN (NoData / off-grid) neighbour.
+__device__ __forceinline__ uint32_t d8_drops(bool cnan, float d1, float d2, float d3, float d4, float d5, float d6,
+                                             float d7, float d8) {
+  if (cnan) return kNoData;
+  float a = 0.0f, b = 0.0f;
+  uint32_t kc = 0, kd = 0;
+  if (d1 > a) { a = d1; kc = 1; }
+  if (d3 > a) { a = d3; kc = 3; }
+  if (d5 > a) { a = d5; kc = 5; }
+  if (d7 > a) { a = d7; kc = 7; }
+  if (d2 > b) { b = d2; kd = 2; }
+  if (d4 > b) { b = d4; kd = 4; }
+  if (d6 > b) { b = d6; kd = 6; }
+  if (d8 > b) { b = d8; kd = 8; }
+  if (kc && kd) {
+    const double da = (double)a, db = (double)b;
+    return __dmul_rn(__dmul_rn(2.0, da), da) > __dmul_rn(db, db) ? kc : kd;
+  }
+  if (kc | kd) return kc | kd;
+  // no downhill data neighbour: the lowest NaN neighbour (outlet, D3), else NoFlow
+  if (isnan(d1)) return 1;
+  if (isnan(d2)) return 2;
+  if (isnan(d3)) return 3;
+  if (isnan(d4)) return 4;
+  if (isnan(d5)) return 5;
+  if (isnan(d6)) return 6;
+  if (isnan(d7)) return 7;
+  if (isnan(d8)) return 8;
+  return kNoFlow;
+}
+
+// H1, vectorised: each lane owns 4 adjacent columns of a 128-column warp
+// strip and runs down RS rows.  Rows are read as one float4 per lane (the
+// two outer columns come from the neighbour lanes by shuffles, or from the
+// halo at the warp's edges), and every pairwise drop is computed once:
+// fl(z_a - z_b) = -fl(z_b - z_a) exactly under round-to-nearest, so the drop
+// to the N / NW / NE neighbour is the negated S / SE / SW drop of the row
+// above, and W is the negated E drop of the left cell (D5 unchanged).
+constexpr int DV_RS = 32;  // rows per warp
+__global__ void __launch_bounds__(128) k_d8v(const float* __restrict__ dem, const float* __restrict__ dem_up,
+                                             const float* __restrict__ dem_dn, int64_t H, int64_t W, float nodata,
+                                             uint8_t* __restrict__ dirs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t x0 = ((int64_t)blockIdx.x * 4 + (threadIdx.x >> 5)) * 128;
+  if (x0 >= W) return;
+  const int64_t y0 = (int64_t)blockIdx.y * DV_RS;
+  const int64_t gx = x0 + 4 * lane;
+  const bool own = gx < W;
+  const float qnan = __int_as_float(0x7fc00000);
+  auto loadrow = [&](int64_t gy, float (&R)[6]) {
+    const float* row = dem_row(dem, dem_up, dem_dn, H, W, gy);
+    float4 v = make_float4(qnan, qnan, qnan, qnan);
+    float hl = qnan, hr = qnan;
+    if (row) {
+      if (own) {
+        v = __ldg(reinterpret_cast<const float4*>(row + gx));
+        v.x = stage_z(v.x, nodata);
+        v.y = stage_z(v.y, nodata);
+        v.z = stage_z(v.z, nodata);
+        v.w = stage_z(v.w, nodata);
+      }
+      if (lane == 0 && x0 > 0) hl = stage_z(__ldg(row + x0 - 1), nodata);
+      if (lane == 31 && x0 + 128 < W) hr = stage_z(__ldg(row + x0 + 128), nodata);
+    }
+    const float l = __shfl_up_sync(kFull, v.w, 1), r = __shfl_down_sync(kFull, v.x, 1);
+    R[0] = lane == 0 ? hl : l;
+    R[1] = v.x;
+    R[2] = v.y;
+    R[3] = v.z;
+    R[4] = v.w;
+    R[5] = lane == 31 ? hr : r;
+  };
+  float P[6], C[6], D[6];
+  loadrow(y0 - 1, P);
+  loadrow(y0, C);
+  // drops between the row above and the current row
+  float pv[6], ps[6], pt[6];
+#pragma unroll
+  for (int j = 0; j < 6; ++j) pv[j] = ps[j] = pt[j] = 0.0f;
+#pragma unroll
+  for (int j = 1; j <= 4; ++j) pv[j] = __fsub_rn(P[j], C[j]);
+#pragma unroll
+  for (int j = 0; j <= 4; ++j) ps[j] = __fsub_rn(P[j], C[j + 1]);
+#pragma unroll
+  for (int j = 1; j <= 5; ++j) pt[j] = __fsub_rn(P[j], C[j - 1]);
+  const int rows = (int)(H - y0 < DV_RS ? H - y0 : DV_RS);
+  uint8_t* out = dirs + y0 * W + gx;
+  for (int r = 0; r < rows; ++r) {
+    loadrow(y0 + r + 1, D);
+    float v[6], sd[6], t[6], hh[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) v[j] = sd[j] = t[j] = hh[j] = 0.0f;
+#pragma unroll
+    for (int j = 1; j <= 4; ++j) v[j] = __fsub_rn(C[j], D[j]);
+#pragma unroll
+    for (int j = 0; j <= 4; ++j) sd[j] = __fsub_rn(C[j], D[j + 1]);
+#pragma unroll
+    for (int j = 1; j <= 5; ++j) t[j] = __fsub_rn(C[j], D[j - 1]);
+#pragma unroll
+    for (int j = 0; j <= 4; ++j) hh[j] = __fsub_rn(C[j], C[j + 1]);
+    uint32_t packed = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j = i + 1;
+      // N, NE, E, SE, S, SW, W, NW
+      const uint32_t code = d8_drops(isnan(C[j]), -pv[j], -pt[j + 1], hh[j], sd[j], v[j], t[j], -hh[j - 1],
+                                     -ps[j - 1]);
+      packed |= code << (8 * i);
+    }
+    if (own) *reinterpret_cast<uint32_t*>(out + (int64_t)r * W) = packed;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      pv[j] = v[j];
+      ps[j] = sd[j];
+      pt[j] = t[j];
+      C[j] = D[j];
+    }
+  }
+}
+
 cudaError_t launch_d8(const float* dem, const float* dem_up, const float* dem_dn, int64_t H, int64_t W,
                       float nodata, uint8_t* dirs, cudaStream_t st) {
-  dim3 grid((unsigned)((W + DC - 1) / DC), (unsigned)((H + DR - 1) / DR));
-  k_d8<<<grid, DC, 0, st>>>(dem, dem_up, dem_dn, H, W, nodata, dirs);
+  const bool vec = (W % 4) == 0 && ((reinterpret_cast<uintptr_t>(dem) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(dirs) & 3) == 0) &&
+                   (!dem_up || (reinterpret_cast<uintptr_t>(dem_up) & 15) == 0) &&
+                   (!dem_dn || (reinterpret_cast<uintptr_t>(dem_dn) & 15) == 0);
+  const char* e = getenv("FA_D8V");
+  if (vec && !(e && e[0] == '0')) {
+    dim3 grid((unsigned)((W + 511) / 512), (unsigned)((H + DV_RS - 1) / DV_RS));
+    k_d8v<<<grid, 128, 0, st>>>(dem, dem_up, dem_dn, H, W, nodata, dirs);
+  } else {
+    dim3 grid((unsigned)((W + DC - 1) / DC), (unsigned)((H + DR - 1) / DR));
+    k_d8<<<grid, DC, 0, st>>>(dem, dem_up, dem_dn, H, W, nodata, dirs);
+  }
   return cudaGetLastError();
 }
 

@@ -66,6 +66,17 @@ def test_d8_ties_and_nodata(fa_lib, seed, levels, pnd):
     assert (got == oracle.d8(z, ND)).all()
 
 
+@pytest.mark.parametrize("seed,H,W,levels,pnd", [(11, 257, 192, 3, 0.1), (12, 64, 512, 2, 0.0), (13, 33, 132, 5, 0.3),
+                                                 (14, 1, 640, 4, 0.05), (15, 300, 4, 3, 0.2)])
+def test_d8_vectorised_kernel_ties(fa_lib, seed, H, W, levels, pnd):
+    """W % 4 == 0 takes the 4-columns-per-lane kernel with shared drops."""
+    z = inputs.quantized_dem(seed, H, W, levels=levels, p_nodata=pnd)
+    z[::5] = (z[::5] * np.float32(math.sqrt(2.0))).astype(np.float32)
+    with fa_lib.Context(0) as ctx:
+        got = ctx.flowdirs(_cuda(z), ND).cpu().numpy()
+    assert (got == oracle.d8(z, ND)).all()
+
+
 def test_d8_exact_sqrt2_pin(fa_lib):
     s2 = np.float32(math.sqrt(2.0))
     z = np.full((5, 5), 3.0, np.float32)

@@ -40,10 +40,11 @@ def main():
             for _ in range(4):
                 ctx.accumulate(w=w, atype=cfg.atype, out=out, **kw)
                 res.append(ctx.stats())
-        p = {k: float(np.median([r[k] for r in res])) for k in ("ms_pass1", "ms_graph", "ms_pass2", "ms_total")}
+        p = {k: float(np.median([r[k] for r in res]))
+             for k in ("ms_pass1", "ms_graph", "ms_pass2", "ms_total", "ms_d8", "ms_block")}
         r = res[-1]
         print(f"{shape}: total {p['ms_total']:.2f} ms  pass1 {p['ms_pass1']:.2f}  graph {p['ms_graph']:.2f}  "
-              f"pass2 {p['ms_pass2']:.2f}  -> {cfg.cells / p['ms_total'] / 1e6:.1f} Gcells/s  "
+              f"pass2 {p['ms_pass2']:.2f} [d8 {p['ms_d8']:.2f} block {p['ms_block']:.2f}]  -> {cfg.cells / p['ms_total'] / 1e6:.1f} Gcells/s  "
               f"nodes {r['graph_nodes']} launches {r['launches']} peel {r['peel_rounds']} "
               f"contract {r['contract_levels']} jumps {r['jump_rounds']}", flush=True)
 
