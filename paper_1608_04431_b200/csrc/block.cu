@@ -1199,32 +1199,40 @@ __global__ void __launch_bounds__(128) k_d8v(const float* __restrict__ dem, cons
   const int64_t gx = x0 + 4 * lane;
   const bool own = gx < W;
   const float qnan = __int_as_float(0x7fc00000);
-  auto loadrow = [&](int64_t gy, float (&R)[6]) {
+  // a row in flight: raw float4 of the lane's columns + the two warp-edge halo values
+  struct Raw {
+    float4 v;
+    float hl, hr;
+  };
+  auto issue = [&](int64_t gy) {
+    Raw q{make_float4(qnan, qnan, qnan, qnan), qnan, qnan};
     const float* row = dem_row(dem, dem_up, dem_dn, H, W, gy);
-    float4 v = make_float4(qnan, qnan, qnan, qnan);
-    float hl = qnan, hr = qnan;
     if (row) {
-      if (own) {
-        v = __ldg(reinterpret_cast<const float4*>(row + gx));
-        v.x = stage_z(v.x, nodata);
-        v.y = stage_z(v.y, nodata);
-        v.z = stage_z(v.z, nodata);
-        v.w = stage_z(v.w, nodata);
-      }
-      if (lane == 0 && x0 > 0) hl = stage_z(__ldg(row + x0 - 1), nodata);
-      if (lane == 31 && x0 + 128 < W) hr = stage_z(__ldg(row + x0 + 128), nodata);
+      if (own) q.v = __ldg(reinterpret_cast<const float4*>(row + gx));
+      if (lane == 0 && x0 > 0) q.hl = __ldg(row + x0 - 1);
+      if (lane == 31 && x0 + 128 < W) q.hr = __ldg(row + x0 + 128);
     }
+    return q;
+  };
+  auto finish = [&](const Raw& q, float (&R)[6]) {
+    // NoData / non-finite -> NaN (off-grid values are NaN already)
+    const float4 v = make_float4(stage_z(q.v.x, nodata), stage_z(q.v.y, nodata), stage_z(q.v.z, nodata),
+                                 stage_z(q.v.w, nodata));
     const float l = __shfl_up_sync(kFull, v.w, 1), r = __shfl_down_sync(kFull, v.x, 1);
-    R[0] = lane == 0 ? hl : l;
+    R[0] = lane == 0 ? stage_z(q.hl, nodata) : l;
     R[1] = v.x;
     R[2] = v.y;
     R[3] = v.z;
     R[4] = v.w;
-    R[5] = lane == 31 ? hr : r;
+    R[5] = lane == 31 ? stage_z(q.hr, nodata) : r;
   };
   float P[6], C[6], D[6];
-  loadrow(y0 - 1, P);
-  loadrow(y0, C);
+  {
+    const Raw q0 = issue(y0 - 1), q1 = issue(y0);
+    finish(q0, P);
+    finish(q1, C);
+  }
+  Raw nxt = issue(y0 + 1);  // one row ahead of its use
   // drops between the row above and the current row
   float pv[6], ps[6], pt[6];
 #pragma unroll
@@ -1238,7 +1246,9 @@ __global__ void __launch_bounds__(128) k_d8v(const float* __restrict__ dem, cons
   const int rows = (int)(H - y0 < DV_RS ? H - y0 : DV_RS);
   uint8_t* out = dirs + y0 * W + gx;
   for (int r = 0; r < rows; ++r) {
-    loadrow(y0 + r + 1, D);
+    const Raw cur = nxt;
+    nxt = issue(y0 + r + 2);
+    finish(cur, D);
     float v[6], sd[6], t[6], hh[6];
 #pragma unroll
     for (int j = 0; j < 6; ++j) v[j] = sd[j] = t[j] = hh[j] = 0.0f;
