@@ -434,8 +434,14 @@ __device__ __forceinline__ void succ_from_dirs(WSmem<T, R, Z>& s, int h, int w) 
 // (Alg. 1 "dependencies") are the per-byte popcounts of the masks.  Returns
 // this lane's data-cell count; by reference, the number of sources (warp
 // total).  Ring codes (254/255) never equal a direction, so no bounds tests.
-template <class T, int R, bool Z>
-__device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc) {
+// With SUCC the successor words are computed here too, 4 cells at a time:
+// the offsets of the codes come from a byte-permute table lookup (biased to
+// bytes, zero-extended into 16-bit lanes) added with 16-bit SIMD adds; words
+// on the block border take the scalar path (a code may leave the block
+// there).  A cell draining into in-block NoData gets STOP afterwards, from
+// the NoData cell's own donor mask (D8: that flow is dropped).
+template <bool SUCC, class T, int R, bool Z>
+__device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc, int h, int w) {
   using WB = WBT<R>;
   constexpr int NQ = WB::BN / 128;  // words per lane
   static_assert(NQ <= 8, "source bits: 4 per word, 32 per lane");
@@ -443,11 +449,12 @@ __device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc) {
   const uint32_t* D = reinterpret_cast<const uint32_t*>(s.dirh);
   constexpr int RW = WB::HS / 4;
   int ndata = 0;
-  uint32_t srcbits = 0;
-#pragma unroll
+  uint32_t srcbits = 0, ndbits = 0;
+#pragma unroll 1
   for (int k = 0; k < NQ; ++k) {
     const int q = k * 32 + lane;  // word: row q/8, cells 4(q%8)..+3
-    const int hw = WB::hidx(q >> 3, (q & 7) * 4) >> 2;
+    const int ly = q >> 3, lx0 = (q & 7) * 4;
+    const int hw = WB::hidx(ly, lx0) >> 2;
     const uint32_t u0 = D[hw - RW - 1], u1 = D[hw - RW], u2 = D[hw - RW + 1];
     const uint32_t c0 = D[hw - 1], c1 = D[hw], c2 = D[hw + 1];
     const uint32_t d0 = D[hw + RW - 1], d1 = D[hw + RW], d2 = D[hw + RW + 1];
@@ -467,15 +474,72 @@ __device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc) {
     m |= (__vcmpeq4(nNW, 0x04040404u) & 0x01010101u) << 7;
     // NoData (255) and cells outside a ragged block (254/255) are not cells
     const uint32_t nd = __vcmpgeu4(c1, 0xFEFEFEFEu);
+    // in-block NoData cells with in-block donors: keep their raw mask (in
+    // pend, never touched by the queue) to stop their donors below
+    const uint32_t inb = ly >= h ? 0u : lx0 + 4 <= w ? 0xFFFFFFFFu : lx0 >= w ? 0u : (0xFFFFFFFFu >> (8 * (lx0 + 4 - w)));
+    const uint32_t sink = SUCC ? (nd & inb & ~__vcmpeq4(m, 0u)) : 0u;
+    const uint32_t mraw = m;
     m &= ~nd;
     // per-byte popcount of the masks
     uint32_t cnt = m - ((m >> 1) & 0x55555555u);
     cnt = (cnt & 0x33333333u) + ((cnt >> 2) & 0x33333333u);
     cnt = (cnt + (cnt >> 4)) & 0x0F0F0F0Fu;
-    s.pend[q] = cnt;
+    s.pend[q] = (cnt & ~sink) | (mraw & sink);
+    ndbits |= (sink ? 1u : 0u) << k;
     ndata += 4 - (__popc(nd) >> 3);
+    if constexpr (SUCC) {
+      uint2 sw;
+      if (ly > 0 && ly < h - 1 && lx0 > 0 && lx0 + 3 < w - 1) {
+        // interior word: every code 1..8 stays in the block.  Offsets of codes
+        // 1..8 (-32 -31 +1 +33 +32 +31 -1 -33, row stride 32) biased by +64
+        // to bytes, looked up 4 at a time, zero-extended to 16-bit lanes.
+        constexpr uint32_t T0 = 0x61412120u, T1 = 0x1F3F5F60u;
+        const uint32_t sel = __vsub4(c1, 0x01010101u) & 0x07070707u;  // code - 1 per byte (no borrow)
+        const uint32_t nib = (sel & 7u) | ((sel >> 4) & 0x70u) | ((sel >> 8) & 0x700u) | ((sel >> 12) & 0x7000u);
+        const uint32_t off4 = __byte_perm(T0, T1, nib);
+        const uint32_t i0 = 4u * (uint32_t)q - 64u;
+        const uint32_t ta = __vadd2((i0 & 0xFFFFu) | ((i0 + 1u) << 16), __byte_perm(off4, 0u, 0x4140u));
+        const uint32_t tb = __vadd2(((i0 + 2u) & 0xFFFFu) | ((i0 + 3u) << 16), __byte_perm(off4, 0u, 0x4342u));
+        const uint32_t ca = __byte_perm(sel, 0u, 0x4140u) << 11, cb = __byte_perm(sel, 0u, 0x4342u) << 11;
+        const uint32_t stop4 = __vcmpeq4(c1, 0u) | __vcmpeq4(c1, 0xFFFFFFFFu);
+        const uint32_t sa = __byte_perm(stop4, 0u, 0x1100u), sb = __byte_perm(stop4, 0u, 0x3322u);
+        sw.x = (sa & 0x80008000u) | (~sa & (ta | ca));
+        sw.y = (sb & 0x80008000u) | (~sb & (tb | cb));
+      } else {
+        uint32_t v[4];
+        const uint32_t fr = forb_row(ly, h);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          v[j] = succ_word<R>(4 * q + j, (c1 >> (8 * j)) & 0xFF, fr | forb_col(lx0 + j, w));
+        sw.x = v[0] | (v[1] << 16);
+        sw.y = v[2] | (v[3] << 16);
+      }
+      reinterpret_cast<uint2*>(s.succ)[q] = sw;
+    }
     const uint32_t src4 = __vcmpeq4(m, 0u) & ~nd & 0x80808080u;  // sources: bit 7 of each byte
     srcbits |= (((src4 >> 7) & 1u) | ((src4 >> 14) & 2u) | ((src4 >> 21) & 4u) | ((src4 >> 28) & 8u)) << (4 * k);
+  }
+  if constexpr (SUCC) {
+    // donors of in-block NoData cells: their flow is dropped (STOP)
+    __syncwarp();
+#pragma unroll 1
+    for (int k = 0; k < NQ; ++k) {
+      if (!((ndbits >> k) & 1u)) continue;
+      const int q = k * 32 + lane;
+      const uint32_t pw = s.pend[q];
+      const uint32_t nd = __vcmpgeu4(reinterpret_cast<const uint32_t*>(s.dirh)[WB::hidx(q >> 3, (q & 7) * 4) >> 2],
+                                     0xFEFEFEFEu);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!((nd >> (8 * j)) & 1u)) continue;
+        uint32_t mm = (pw >> (8 * j)) & 0xFFu;
+        while (mm) {
+          const int kk = __ffs(mm);
+          mm &= mm - 1;
+          s.succ[4 * q + j + WB::offA(kk)] = (uint16_t)SU_STOP;
+        }
+      }
+    }
   }
   // compact: exclusive scan of the per-lane counts, then each lane writes its cells
   const int cnt = __popc(srcbits);
@@ -800,7 +864,7 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
 
 // ---------------------------------------------------------------- pass 1
 template <class T, int R, int WK, bool FROM_DEM>
-__global__ void __launch_bounds__(128) k_pass1(PassArgs<T, WK> P) {
+__global__ void __launch_bounds__(128, 8) k_pass1(PassArgs<T, WK> P) {
   using WB = WBT<R>;
   constexpr bool Z = FROM_DEM;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -828,12 +892,10 @@ __global__ void __launch_bounds__(128) k_pass1(PassArgs<T, WK> P) {
   } else {
     __syncwarp();
     load_dirs(s, P.dirs_in, P.dirs_up, P.dirs_dn, g, y0, x0, h, w, true, true, P.status);
-    __syncwarp();
-    succ_from_dirs(s, h, w);
   }
   __syncwarp();
   uint32_t nsrc;
-  const int ndata = build_masks(s, nsrc);
+  const int ndata = build_masks<!FROM_DEM>(s, nsrc, h, w);
   // RETAIN: the block-local accumulation is computed in place in acc
   unsigned long long wsum = init_values<T, R, Z, WK>(s, P.w, g, y0, x0, h, w, P.acc, P.status);
   const uint32_t popped = kahn_block(s, nsrc, P.acc + y0 * g.W + x0, g.W);
@@ -866,10 +928,8 @@ __global__ void __launch_bounds__(128) k_pass2(PassArgs<T, WK> P) {
   __syncwarp();
   load_dirs(s, P.dirs_in, P.dirs_up, P.dirs_dn, g, y0, x0, h, w, false, false, P.status);
   __syncwarp();
-  succ_from_dirs(s, h, w);
-  __syncwarp();
   uint32_t nsrc;
-  const int ndata = build_masks(s, nsrc);
+  const int ndata = build_masks<true>(s, nsrc, h, w);
   init_values<T, R, false, WK>(s, P.w, g, y0, x0, h, w, P.acc, P.status);
   __syncwarp();
   // inject x at the block perimeter (offset propagation; D12)

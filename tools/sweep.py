@@ -33,18 +33,30 @@ def main():
         for kv in shape.split(","):
             k, v = kv.split("=")
             os.environ["FA_" + k] = v
+        nstrips = int(os.environ.get("FA_STRIPS", "0"))  # STRIPS=G: the multi-GPU strip pipeline, G strips on one device
+
+        def call(ctx):
+            if nstrips > 0:
+                ctx.accumulate_strips(nstrips, w=w, atype=cfg.atype, out=out, **kw)
+            else:
+                ctx.accumulate(w=w, atype=cfg.atype, out=out, **kw)
+
         with fa.Context(0, stream=st, tile=tile) as ctx:
             for _ in range(2):
-                ctx.accumulate(w=w, atype=cfg.atype, out=out, **kw)
+                call(ctx)
             res = []
             for _ in range(4):
-                ctx.accumulate(w=w, atype=cfg.atype, out=out, **kw)
-                res.append(ctx.stats())
+                t0 = time.perf_counter()
+                call(ctx)
+                st.synchronize()
+                r = ctx.stats()
+                r["wall_ms"] = (time.perf_counter() - t0) * 1e3
+                res.append(r)
         p = {k: float(np.median([r[k] for r in res]))
-             for k in ("ms_pass1", "ms_graph", "ms_pass2", "ms_total", "ms_d8", "ms_block")}
+             for k in ("ms_pass1", "ms_graph", "ms_pass2", "ms_total", "ms_d8", "ms_block", "wall_ms")}
         r = res[-1]
         print(f"{shape}: total {p['ms_total']:.2f} ms  pass1 {p['ms_pass1']:.2f}  graph {p['ms_graph']:.2f}  "
-              f"pass2 {p['ms_pass2']:.2f} [d8 {p['ms_d8']:.2f} block {p['ms_block']:.2f}]  -> {cfg.cells / p['ms_total'] / 1e6:.1f} Gcells/s  "
+              f"pass2 {p['ms_pass2']:.2f} [d8 {p['ms_d8']:.2f} block {p['ms_block']:.2f} wall {p['wall_ms']:.2f}]  -> {cfg.cells / p['ms_total'] / 1e6:.1f} Gcells/s  "
               f"nodes {r['graph_nodes']} launches {r['launches']} peel {r['peel_rounds']} "
               f"contract {r['contract_levels']} jumps {r['jump_rounds']}", flush=True)
 
