@@ -240,6 +240,9 @@ struct Strip {
   const float* dem = nullptr;
   const float* dem_up = nullptr;
   const float* dem_dn = nullptr;
+  const float* dem_up2 = nullptr;  // rows -2 / H+1 (null: off-grid) when halo2: the D8 of the halo rows
+  const float* dem_dn2 = nullptr;
+  bool halo2 = false;
   const uint8_t* dirs = nullptr;
   const uint8_t* dirs_up = nullptr;
   const uint8_t* dirs_dn = nullptr;
@@ -248,6 +251,7 @@ struct Strip {
   float nodata = 0;
   // device state
   T* acc_tmp = nullptr;   // in-place accumulation buffer when the caller wants no raster
+  uint8_t* halo_dirs = nullptr;  // D8 codes of rows -1 and H (split path, strips)
   uint8_t* dirs_buf = nullptr;
   uint32_t* slot_root = nullptr;
   T* node_val = nullptr;
@@ -264,10 +268,11 @@ struct Strip {
   void release(fa::Runtime& rt) {
     for (void* p : {(void*)dirs_buf, (void*)slot_root, (void*)node_val, (void*)node_slot, (void*)node_tgt,
                     (void*)node_flags, (void*)x_slot, (void*)parent, (void*)S, (void*)troot, (void*)dtbase,
-                    (void*)acc_tmp})
+                    (void*)acc_tmp, (void*)halo_dirs})
       rt.free(p);
     dirs_buf = nullptr;
     acc_tmp = nullptr;
+    halo_dirs = nullptr;
     slot_root = node_slot = node_tgt = parent = troot = nullptr;
     node_val = x_slot = S = nullptr;
     node_flags = nullptr;
@@ -337,16 +342,31 @@ fa_status strip_pass1(fa_ctx* ctx, Strip<T>& s, bool cut) {
   CK(cudaMemsetAsync(s.x_slot, 0, slots * sizeof(T), st));
   fa::PassArgs<T, WK> pa = pass_args<T, WK>(ctx, s);
   pa.cut = cut;
-  // Whole raster on one device: H1 runs as its own kernel (high occupancy),
-  // then pass 1 starts from the directions.  Strips keep D8 fused into pass 1
-  // (its 2-cell halo stands in for the neighbour strip's codes).
+  // H1 runs as its own kernel (high occupancy), then pass 1 starts from the
+  // directions.  A strip also computes the codes of its halo rows -1 and H
+  // (from the 2-row z halo), so pass 1 sees the neighbour strips' codes on
+  // its ring.  FA_FUSED=1 (or 1-row halos) keeps D8 fused into pass 1.
   const char* fused_env = getenv("FA_FUSED");
-  const bool split = s.dem && !cut && !s.dem_up && !s.dem_dn && !(fused_env && fused_env[0] == '1');
+  const bool split = s.dem && !(fused_env && fused_env[0] == '1') && (s.halo2 || (!s.dem_up && !s.dem_dn));
   CK(cudaEventRecord(ctx->ev[4], st));
   if (split) {
-    CK(launch_d8(s.dem, nullptr, nullptr, g.H, g.W, s.nodata, s.dirs_buf, st));
+    CK(launch_d8(s.dem, s.dem_up, s.dem_dn, g.H, g.W, s.nodata, s.dirs_buf, st));
     ++rt.launches;
     pa.dirs_out = nullptr;
+    if (s.dem_up || s.dem_dn) {
+      s.halo_dirs = rt.alloc<uint8_t>((size_t)(2 * g.W));
+      if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+    }
+    if (s.dem_up) {
+      CK(launch_d8(s.dem_up, s.dem_up2, s.dem, 1, g.W, s.nodata, s.halo_dirs, st));
+      ++rt.launches;
+    }
+    if (s.dem_dn) {
+      CK(launch_d8(s.dem_dn, s.dem + (g.H - 1) * g.W, s.dem_dn2, 1, g.W, s.nodata, s.halo_dirs + g.W, st));
+      ++rt.launches;
+    }
+    pa.dirs_up = s.dem_up ? s.halo_dirs : nullptr;
+    pa.dirs_dn = s.dem_dn ? s.halo_dirs + g.W : nullptr;
   }
   CK(cudaEventRecord(ctx->ev[5], st));
   CK(launch_pass1<T, WK>(pa, s.dem != nullptr && !split, st));
@@ -375,6 +395,8 @@ fa_status strip_records(fa_ctx* ctx, Strip<T>& s, uint32_t* links, uint8_t* fdir
   if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
   CK(cudaMemcpyAsync(s.dtbase, hb.data(), hb.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(s.S, s.node_val, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  CK(launch_fold_leaves<T>(st, s.g.nblocks * s.g.pb, s.x_slot, s.slot_root, s.S));  // leaves raked in pass 1
+  ++rt.launches;
   CK(forest_solve<T>(rt, s.nn, s.parent, s.S));  // A_T at every block exit (Alg. 1 on each tile)
   CK(forest_roots(rt, s.nn, s.parent, s.troot));
   CK(launch_tile_records<T>(st, s.g, s.nslots, s.dtbase, s.dirs_in(), s.slot_root, s.troot, s.node_flags,
@@ -417,6 +439,9 @@ fa_status strip_finish(fa_ctx* ctx, Strip<T>& s, const T* xT_global) {
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
   CK(cudaMemcpyAsync(s.S, s.node_val, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  // leaves first (x_slot holds only their pass-1 values here), then x_T
+  CK(launch_fold_leaves<T>(st, s.g.nblocks * s.g.pb, s.x_slot, s.slot_root, s.S));
+  ++rt.launches;
   CK(launch_inject_slots<T>(st, s.g, s.nslots, s.dtbase, xT_global + s.slot0, s.slot_root, s.S, s.x_slot));
   ++rt.launches;
   CK(forest_solve<T>(rt, s.nn, s.parent, s.S));  // true A at every block exit
@@ -557,6 +582,9 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
     s.dem = dem ? dem + r0 * W : nullptr;
     s.dem_up = dem && r0 > 0 ? dem + (r0 - 1) * W : nullptr;
     s.dem_dn = dem && r1 < H ? dem + r1 * W : nullptr;
+    s.dem_up2 = dem && r0 > 1 ? dem + (r0 - 2) * W : nullptr;
+    s.dem_dn2 = dem && r1 + 1 < H ? dem + (r1 + 1) * W : nullptr;
+    s.halo2 = true;
     s.dirs = dirs ? dirs + r0 * W : nullptr;
     s.dirs_up = dirs && r0 > 0 ? dirs + (r0 - 1) * W : nullptr;
     s.dirs_dn = dirs && r1 < H ? dirs + r1 * W : nullptr;
@@ -688,23 +716,25 @@ fa_status run_dist(fa_ctx* ctx, int64_t GH, int64_t W, int64_t row_begin, int64_
   cudaEvent_t ex0, ex1;
   cudaEventCreate(&ex0);
   cudaEventCreate(&ex1);
-  // ---- C1: halo rows (one row each way, grouped send/recv)
+  // ---- C1: halo rows, grouped send/recv: two rows of z each way (D8 of the
+  // neighbours' edge rows needs their next row too), or one row of codes
   const size_t esz = dem ? 4 : 1;
   const void* src = dem ? (const void*)dem : (const void*)dirs;
+  const int64_t nh = (dem && gg.TH >= 2) ? 2 : 1;  // strips are whole tile rows: >= 2 rows when TH >= 2
   void *up = nullptr, *dn = nullptr;
-  if (rank > 0) up = rt.alloc<uint8_t>(W * esz);
-  if (rank < nranks - 1) dn = rt.alloc<uint8_t>(W * esz);
+  if (rank > 0) up = rt.alloc<uint8_t>(nh * W * esz);
+  if (rank < nranks - 1) dn = rt.alloc<uint8_t>(nh * W * esz);
   if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
   CK(cudaEventRecord(ex0, st));
   NK(N.groupStart());
   const ncclDataType_t rt_row = dem ? ncclFloat32 : ncclUint8;
-  if (rank > 0) {
-    NK(N.send(src, W, rt_row, rank - 1, ctx->comm, st));
-    NK(N.recv(up, W, rt_row, rank - 1, ctx->comm, st));
+  if (rank > 0) {  // our first nh rows up, their last nh rows (rows -nh..-1) down to us
+    NK(N.send(src, nh * W, rt_row, rank - 1, ctx->comm, st));
+    NK(N.recv(up, nh * W, rt_row, rank - 1, ctx->comm, st));
   }
   if (rank < nranks - 1) {
-    NK(N.send(static_cast<const char*>(src) + (H - 1) * W * esz, W, rt_row, rank + 1, ctx->comm, st));
-    NK(N.recv(dn, W, rt_row, rank + 1, ctx->comm, st));
+    NK(N.send(static_cast<const char*>(src) + (H - nh) * W * esz, nh * W, rt_row, rank + 1, ctx->comm, st));
+    NK(N.recv(dn, nh * W, rt_row, rank + 1, ctx->comm, st));
   }
   NK(N.groupEnd());
   CK(cudaEventRecord(ex1, st));
@@ -722,8 +752,14 @@ fa_status run_dist(fa_ctx* ctx, int64_t GH, int64_t W, int64_t row_begin, int64_
   s.nodata = nodata;
   s.dem = dem;
   s.dirs = dirs;
-  s.dem_up = dem ? (const float*)up : nullptr;
+  // halo buffers: up = rows [-nh, -1], dn = rows [H, H + nh)
+  s.dem_up = dem && up ? (const float*)up + (nh - 1) * W : nullptr;
   s.dem_dn = dem ? (const float*)dn : nullptr;
+  if (nh == 2) {
+    s.dem_up2 = up ? (const float*)up : nullptr;
+    s.dem_dn2 = dn ? (const float*)dn + W : nullptr;
+    s.halo2 = true;
+  }
   s.dirs_up = dem ? nullptr : (const uint8_t*)up;
   s.dirs_dn = dem ? nullptr : (const uint8_t*)dn;
   s.w = w;
@@ -783,7 +819,7 @@ fa_status run_dist(fa_ctx* ctx, int64_t GH, int64_t W, int64_t row_begin, int64_
   cudaEventDestroy(ex0);
   cudaEventDestroy(ex1);
   ctx->stats.ms_exchange = exm;
-  ctx->stats.bytes_exchanged = (int64_t)(nslots * (4 + 1 + sizeof(T)) + 2 * W * esz);
+  ctx->stats.bytes_exchanged = (int64_t)(nslots * (4 + 1 + sizeof(T)) + 2 * nh * W * esz);
   if (r != FA_OK) return r;
   record_stats(ctx, H * W, s.g.nblocks, s.nn, nslots);
   return FA_OK;

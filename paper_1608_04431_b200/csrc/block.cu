@@ -717,24 +717,23 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
   int64_t t0y, t0x, th, tw;
   g.tile_box(g.tile_of_block(b), t0y, t0x, th, tw);
   int cell[NJ];
-  bool ex[NJ], want[NJ];
+  bool ex[NJ], want[NJ], tedge[NJ];
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     const int p = lane + 32 * j;
     cell[j] = -1;
-    ex[j] = want[j] = false;
+    ex[j] = want[j] = tedge[j] = false;
     if (p < np) {
       int px, py;
       bperim_xy(p, h, w, px, py);
       cell[j] = py * WB::BC + px;
       const bool data = s.dirh[WB::hidx(py, px)] != kNoData;
       ex[j] = data && (s.succ[cell[j]] & SU_EXIT) != 0u;
-      bool need = s.need[p] != 0u;
-      if (P.cut && !need) {  // tile records: every slot on a tile edge
+      if (P.cut) {  // tile records: every slot on a tile edge needs its link
         const int64_t gy = y0 + py, gx = x0 + px;
-        need = gy == t0y || gx == t0x || gy == t0y + th - 1 || gx == t0x + tw - 1;
+        tedge[j] = gy == t0y || gx == t0x || gy == t0y + th - 1 || gx == t0x + tw - 1;
       }
-      want[j] = data && !ex[j] && need;
+      want[j] = data && !ex[j] && (s.need[p] != 0u || tedge[j]);
     }
   }
   __syncwarp();
@@ -780,7 +779,8 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
       uint32_t rp = kNoP;
       if (su & SU_EXIT) {
         rp = (uint32_t)bperim_index(c & 31, c >> 5, h, w);
-        const uint32_t k = s.need[p];
+        // tile-records mode: an exit reached from a tile-edge slot is a node too
+        const uint32_t k = s.need[p] ? s.need[p] : (P.cut ? 1u : 0u);
         if (k) atomicAdd(&nchild[rp], k);
       }
       s.need[p] = rp;  // only this lane touches need[p] from here on
@@ -792,12 +792,27 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
   }
   __syncwarp();
   // exits: leaves push their value to the target slot, the rest become nodes
+  // (in tile-records mode also every exit leaving its tile: FlowExternal)
   bool node[NJ];
+  uint8_t flg[NJ];
+  int tyv[NJ], txv[NJ];
   int nex = 0;
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     const int p2 = lane + 32 * j;
-    node[j] = ex[j] && (P.cut || nchild[p2] != 0u);
+    flg[j] = 0;
+    tyv[j] = txv[j] = 0;
+    if (ex[j]) {
+      const int px = cell[j] & 31, py = cell[j] >> 5;
+      const int d = s.dirh[WB::hidx(py, px)];
+      tyv[j] = py + dir_dy(d);
+      txv[j] = px + dir_dx(d);
+      const bool dead = s.dirh[WB::hidx(tyv[j], txv[j])] == kNoData;
+      const int64_t gy = y0 + tyv[j], gx = x0 + txv[j];
+      flg[j] = dead ? NF_DEAD : 0;
+      if (gy < t0y || gx < t0x || gy >= t0y + th || gx >= t0x + tw) flg[j] |= NF_OUT_TILE;
+    }
+    node[j] = ex[j] && (nchild[p2] != 0u || (P.cut && ((flg[j] & NF_OUT_TILE) || tedge[j])));
     nex += __popc(__ballot_sync(kFull, node[j]));
   }
   uint32_t base = 0;
@@ -810,12 +825,10 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
     uint32_t nid = kNone;
     if (ex[j]) {
       const int px = cell[j] & 31, py = cell[j] >> 5;
-      const int d = s.dirh[WB::hidx(py, px)];
-      const int ty = py + dir_dy(d), tx = px + dir_dx(d);
-      const bool dead = s.dirh[WB::hidx(ty, tx)] == kNoData;
+      const int ty = tyv[j], tx = txv[j];
+      const uint8_t fl = flg[j];
+      const bool dead = (fl & NF_DEAD) != 0;
       const int64_t gy = y0 + ty, gx = x0 + tx;
-      uint8_t fl = dead ? NF_DEAD : 0;
-      if (gy < t0y || gx < t0x || gy >= t0y + th || gx >= t0x + tw) fl |= NF_OUT_TILE;
       uint32_t tgt = kNone;  // none: dropped, or in another strip (carried by the tile records)
       if (!dead && gy >= 0 && gy < g.H) {
         int64_t tb;
