@@ -19,6 +19,7 @@
 // phases; each phase is a handful of grid-stride kernels.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "forest.cuh"
 
@@ -64,6 +65,38 @@ __global__ void k_peel(const uint32_t* __restrict__ front, uint32_t nf,
       }
     }
     warp_append(push, p, next, ncount);
+  }
+}
+
+// The same round with the frontier size read on the device: rounds are
+// launched back to back without a host round trip.  Counters rotate over
+// three slots: round r reads c[r%3], appends into c[(r+1)%3] (zeroed by round
+// r-1) and zeroes c[(r+2)%3] for round r+1; `retired` accumulates the sizes.
+template <class T>
+__global__ void k_peel_dev(const uint32_t* __restrict__ front, const uint32_t* __restrict__ nf_in,
+                           const uint32_t* __restrict__ parent, T* val, uint32_t* cnt, uint8_t* done,
+                           uint32_t* next, uint32_t* nf_out, uint32_t* nf_clear,
+                           unsigned long long* retired) {
+  const uint32_t nf = *nf_in;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *nf_clear = 0u;
+    *retired += nf;
+  }
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < nf; base += stride) {
+    const uint32_t i = base + threadIdx.x;
+    bool push = false;
+    uint32_t p = kNone;
+    if (i < nf) {
+      const uint32_t v = front[i];
+      done[v] = 1;
+      p = parent[v];
+      if (p != kNone) {
+        atomic_add(&val[p], val[v]);
+        push = atomicSub(&cnt[p], 1u) == 1u;
+      }
+    }
+    warp_append(push, p, next, nf_out);
   }
 }
 
@@ -241,6 +274,7 @@ inline int env_int(const char* name, int dflt, int lo = 0) {
 }
 
 constexpr int kMaxLevels = 64;
+constexpr int kPeelBatch = 4;  // peel rounds per host check
 constexpr int kMaxJump = 40;
 constexpr int kWalkCap = 0;  // steps per walk before re-queueing; 0 = no walk launch (peel rounds, measured faster)
 
@@ -269,6 +303,7 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
   uint32_t nf = rt.h_cnt[0];
   uint64_t remaining = n;
   bool contracted = false;
+  uint32_t* pc = nullptr;  // device frontier counters of the batched peel rounds
   const int cap = env_int("FA_WALKCAP", kWalkCap);  // tuning override (read per call)
   if (nf > 0 && cap > 0) {
     // bulk of the forest: one launch of capped walks from every leaf
@@ -311,13 +346,17 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
       ++rt.launches;
       int rounds = 0;
       for (;;) {
+        // pointer jumping converges in ceil(log2(longest chain)) rounds; the
+        // "changed" flag is read back every 4 rounds (extra rounds are no-ops)
         cudaMemsetAsync(ctr + 2, 0, sizeof(uint32_t), st);
-        k_jump<T><<<grid_for(m), 256, 0, st>>>(m, lpc, nxa, aca, nxb, acb, ctr + 2);
-        ++rt.launches;
-        std::swap(nxa, nxb);
-        std::swap(aca, acb);
-        ++rounds;
-        ++rt.jump_rounds;
+        for (int j = 0; j < 4; ++j) {
+          k_jump<T><<<grid_for(m), 256, 0, st>>>(m, lpc, nxa, aca, nxb, acb, ctr + 2);
+          std::swap(nxa, nxb);
+          std::swap(aca, acb);
+        }
+        rt.launches += 4;
+        rounds += 4;
+        rt.jump_rounds += 4;
         rt.read(ctr + 2, 1);
         if (!rt.h_cnt[0] || rt.err) break;
         if (rounds > kMaxJump) {
@@ -353,18 +392,33 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
       remaining = 0;
       break;
     }
-    // ---------------- one peel round (Alg. 1 queue loop, level-synchronous)
-    cudaMemsetAsync(ctr + 1, 0, sizeof(uint32_t), st);
-    k_peel<T><<<grid_for(nf), 256, 0, st>>>(fa_, nf, parent, val, cnt, done, fb, ctr + 1);
-    ++rt.launches;
-    ++rt.peel_rounds;
-    remaining -= nf;
-    std::swap(fa_, fb);
-    rt.read(ctr + 1, 1);
-    if (env_int("FA_DEBUG_GRAPH", 0)) fprintf(stderr, "level %d peel: frontier %u remaining %llu\n", level, nf,
-                                              (unsigned long long)remaining);
-    nf = rt.h_cnt[0];
+    // ---------------- kPeelBatch peel rounds (Alg. 1 queue loop, level-
+    // synchronous), frontier sizes kept on the device; one read per batch
+    if (!pc) {
+      pc = rt.alloc<uint32_t>(8);  // [0..2] rotating frontier counters, [4..5] retired (u64)
+      if (rt.err) return rt.err;
+    }
+    cudaMemsetAsync(pc, 0, 8 * sizeof(uint32_t), st);
+    cudaMemcpyAsync(pc, ctr, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);  // c[0] = nf
+    unsigned long long* retired = reinterpret_cast<unsigned long long*>(pc + 4);
+    const unsigned grid = grid_for(nf);
+    for (int r = 0; r < kPeelBatch; ++r) {
+      k_peel_dev<T><<<grid, 256, 0, st>>>(fa_, pc + r % 3, parent, val, cnt, done, fb, pc + (r + 1) % 3,
+                                          pc + (r + 2) % 3, retired);
+      std::swap(fa_, fb);
+    }
+    rt.launches += kPeelBatch;
+    rt.peel_rounds += kPeelBatch;
+    cudaMemcpyAsync(ctr, pc + kPeelBatch % 3, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
+    rt.read(pc, 6);
+    nf = rt.h_cnt[kPeelBatch % 3];
+    unsigned long long ret = 0;
+    memcpy(&ret, &rt.h_cnt[4], sizeof(ret));
+    remaining -= ret;
+    if (env_int("FA_DEBUG_GRAPH", 0)) fprintf(stderr, "level %d peel x%d: frontier %u remaining %llu\n", level,
+                                              kPeelBatch, nf, (unsigned long long)remaining);
   }
+  rt.free(pc);
   if (!contracted && remaining != 0) k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);
   rt.free(cnt);
   rt.free(done);
@@ -413,10 +467,12 @@ cudaError_t forest_roots(Runtime& rt, uint32_t n, const uint32_t* parent, uint32
   int rounds = 0;
   for (;;) {
     cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st);
-    k_root_jump<<<grid_for(n), 256, 0, st>>>(n, a, b, ctr);
-    ++rt.launches;
-    std::swap(a, b);
-    ++rounds;
+    for (int j = 0; j < 4; ++j) {  // converged rounds are no-ops: check every 4
+      k_root_jump<<<grid_for(n), 256, 0, st>>>(n, a, b, ctr);
+      std::swap(a, b);
+    }
+    rt.launches += 4;
+    rounds += 4;
     rt.read(ctr, 1);
     if (!rt.h_cnt[0] || rt.err) break;
     if (rounds > kMaxJump) {
