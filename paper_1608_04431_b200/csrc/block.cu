@@ -26,7 +26,6 @@
 //   bit 15 STOP  -- no in-block successor (NoFlow, NoData, drains into
 //                   in-block NoData (D8), or leaves the block);
 //   bit 14 EXIT  -- (with STOP) the target is outside the block: a block exit;
-//   bits 11-13   -- code - 1 (without STOP);
 //   bits 0-10    -- target index (without STOP).
 //
 // Values live in the output raster itself: the block's A(p) are accumulated
@@ -55,7 +54,7 @@ namespace fa {
 
 constexpr uint8_t kOut = 254;  // ring cell: outside the block, data
 
-constexpr uint32_t SU_STOP = 0x8000u, SU_EXIT = 0x4000u, SU_ND = 0x2000u, SU_T = 0x07FFu;
+constexpr uint32_t SU_STOP = 0x8000u, SU_EXIT = 0x4000u, SU_T = 0x07FFu;
 // direction codes (bit k) leaving a cell through its N / S / W / E side
 constexpr uint32_t DM_N = (1u << 1) | (1u << 2) | (1u << 8);
 constexpr uint32_t DM_S = (1u << 4) | (1u << 5) | (1u << 6);
@@ -207,7 +206,7 @@ __device__ __forceinline__ uint32_t succ_word(int i, int d, uint32_t forb) {
   if (d == kNoData || k == 0) return SU_STOP;
   if ((forb >> k) & 1u) return SU_STOP | SU_EXIT;
   if (d & 16) return SU_STOP;  // drains into in-block NoData: dropped (D8)
-  return (uint32_t)(i + WBT<R>::offA(k)) | ((uint32_t)(k - 1) << 11);
+  return (uint32_t)(i + WBT<R>::offA(k));
 }
 
 __device__ __forceinline__ uint32_t forb_col(int lx, int w) {
@@ -500,11 +499,10 @@ __device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc, in
         const uint32_t i0 = 4u * (uint32_t)q - 64u;
         const uint32_t ta = __vadd2((i0 & 0xFFFFu) | ((i0 + 1u) << 16), __byte_perm(off4, 0u, 0x4140u));
         const uint32_t tb = __vadd2(((i0 + 2u) & 0xFFFFu) | ((i0 + 3u) << 16), __byte_perm(off4, 0u, 0x4342u));
-        const uint32_t ca = __byte_perm(sel, 0u, 0x4140u) << 11, cb = __byte_perm(sel, 0u, 0x4342u) << 11;
         const uint32_t stop4 = __vcmpeq4(c1, 0u) | __vcmpeq4(c1, 0xFFFFFFFFu);
         const uint32_t sa = __byte_perm(stop4, 0u, 0x1100u), sb = __byte_perm(stop4, 0u, 0x3322u);
-        sw.x = (sa & 0x80008000u) | (~sa & (ta | ca));
-        sw.y = (sb & 0x80008000u) | (~sb & (tb | cb));
+        sw.x = (sa & 0x80008000u) | (~sa & ta);
+        sw.y = (sb & 0x80008000u) | (~sb & tb);
       } else {
         uint32_t v[4];
         const uint32_t fr = forb_row(ly, h);
