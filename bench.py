@@ -116,6 +116,15 @@ def cpu_sample(cfg, max_rows=4096):
                       f"{dt:.1f} s"}
 
 
+def arm_config(cfg, world):
+    """The `config` object both arms print (the workload, no model keys)."""
+    return {"workload": f"{CFG}: {cfg.rows}x{cfg.cols} f32 DEM seed 4, 10% NoData, filled, f32 w -> f64, "
+                        f"{cfg.tile[0]}x{cfg.tile[1]} tiles",
+            "parallelism": f"row strips x{world} (NCCL)" if world > 1 else "single GPU",
+            "l2": "inputs 8 GiB + output 8 GiB >> 126 MB L2 (no flush needed)",
+            "nodata_frac": round(float(cfg.meta.get("nodata_frac", 0.0)), 4)}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -129,11 +138,12 @@ def run_reference(args):
     cb = dict(vals[0])
     cb["value"] = v
     ms = 1024 * cfg.cols / (v * 1e9) * 1e3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     line = {"metric": METRIC, "value": v, "unit": "Gcells/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{CFG} sample: rows [0,1024) x 32768 (oracle, CPU)",
-                       "global_batch": 1, "seq_len": 0, "parallelism": "none (1 CPU core)"},
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": arm_config(cfg, world),
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "Gcells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -291,11 +301,7 @@ def run_gpu(args):
         "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{CFG}: {H}x{W} f32 DEM seed 4, 10% NoData, filled, f32 w -> f64, "
-                               f"{cfg.tile[0]}x{cfg.tile[1]} tiles",
-                   "parallelism": f"row strips x{world} (NCCL)" if world > 1 else "single GPU",
-                   "l2": "inputs 8 GiB + output 8 GiB >> 126 MB L2 (no flush needed)",
-                   "nodata_frac": round(float(cfg.meta.get("nodata_frac", 0.0)), 4)},
+        "config": arm_config(cfg, world),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "bytes_per_cell": dom_bytes,
