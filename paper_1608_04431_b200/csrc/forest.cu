@@ -21,6 +21,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cuda/atomic>
+
 #include "forest.cuh"
 
 namespace fa {
@@ -124,9 +126,10 @@ __global__ void k_walk(const uint32_t* __restrict__ front, uint32_t nf, const ui
         const uint32_t p = parent[v];
         if (p == kNone) break;
         atomic_add(&val[p], s);
-        __threadfence();  // our contribution before our decrement
-        if (atomicSub(&cnt[p], 1u) != 1u) break;
-        __threadfence();  // every contribution to p is now visible
+        // acq_rel decrement: our contribution is released before it, and the
+        // last arrival acquires every other child's contribution
+        cuda::atomic_ref<uint32_t, cuda::thread_scope_device> cp(cnt[p]);
+        if (cp.fetch_sub(1u, cuda::memory_order_acq_rel) != 1u) break;
         if (steps + 1 >= cap) {
           push = true;
           pnode = p;
@@ -276,7 +279,7 @@ inline int env_int(const char* name, int dflt, int lo = 0) {
 constexpr int kMaxLevels = 64;
 constexpr int kPeelBatch = 4;  // peel rounds per host check
 constexpr int kMaxJump = 40;
-constexpr int kWalkCap = 0;  // steps per walk before re-queueing; 0 = no walk launch (peel rounds, measured faster)
+constexpr int kWalkCap = 32;  // steps per walk before re-queueing (deep chains -> contraction); 0 = peel only
 
 template <class T>
 cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, int level) {
@@ -312,6 +315,7 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
     ++rt.launches;
     ++rt.peel_rounds;
     std::swap(fa_, fb);
+    cudaMemcpyAsync(ctr, ctr + 1, sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);  // frontier size for the peel
     rt.read(ctr + 1, 2);
     nf = rt.h_cnt[0];
     remaining -= rt.h_cnt[1];
