@@ -1221,35 +1221,29 @@ __global__ void __launch_bounds__(DC) k_d8(const float* __restrict__ dem, const 
 }
 
 // D8 from precomputed drops (same rule as d8_window): centre NaN -> NoData;
-// a NaN drop means a NaN (NoData / off-grid) neighbour.
+// a NaN drop means a NaN (NoData / off-grid) neighbour.  The best cardinal
+// and diagonal drops are maxima (fmaxf ignores NaN), their codes the first
+// equal drop in code order (lowest code on ties, D2); strictly downhill
+// means > 0; then the exact fp64 compare 2a^2 > b^2 (D4).
 __device__ __forceinline__ uint32_t d8_drops(bool cnan, float d1, float d2, float d3, float d4, float d5, float d6,
                                              float d7, float d8) {
-  if (cnan) return kNoData;
-  float a = 0.0f, b = 0.0f;
-  uint32_t kc = 0, kd = 0;
-  if (d1 > a) { a = d1; kc = 1; }
-  if (d3 > a) { a = d3; kc = 3; }
-  if (d5 > a) { a = d5; kc = 5; }
-  if (d7 > a) { a = d7; kc = 7; }
-  if (d2 > b) { b = d2; kd = 2; }
-  if (d4 > b) { b = d4; kd = 4; }
-  if (d6 > b) { b = d6; kd = 6; }
-  if (d8 > b) { b = d8; kd = 8; }
-  if (kc && kd) {
+  const float a = fmaxf(fmaxf(d1, d3), fmaxf(d5, d7));
+  const float b = fmaxf(fmaxf(d2, d4), fmaxf(d6, d8));
+  const uint32_t kc = d1 == a ? 1u : d3 == a ? 3u : d5 == a ? 5u : 7u;
+  const uint32_t kd = d2 == b ? 2u : d4 == b ? 4u : d6 == b ? 6u : 8u;
+  const bool vc = a > 0.0f, vd = b > 0.0f;
+  uint32_t code;
+  if (vc && vd) {
     const double da = (double)a, db = (double)b;
-    return __dmul_rn(__dmul_rn(2.0, da), da) > __dmul_rn(db, db) ? kc : kd;
+    code = __dmul_rn(__dmul_rn(2.0, da), da) > __dmul_rn(db, db) ? kc : kd;
+  } else if (vc | vd) {
+    code = vc ? kc : kd;
+  } else {
+    // no downhill data neighbour: the lowest NaN neighbour (outlet, D3), else NoFlow
+    code = isnan(d1) ? 1u : isnan(d2) ? 2u : isnan(d3) ? 3u : isnan(d4) ? 4u : isnan(d5) ? 5u
+         : isnan(d6) ? 6u : isnan(d7) ? 7u : isnan(d8) ? 8u : (uint32_t)kNoFlow;
   }
-  if (kc | kd) return kc | kd;
-  // no downhill data neighbour: the lowest NaN neighbour (outlet, D3), else NoFlow
-  if (isnan(d1)) return 1;
-  if (isnan(d2)) return 2;
-  if (isnan(d3)) return 3;
-  if (isnan(d4)) return 4;
-  if (isnan(d5)) return 5;
-  if (isnan(d6)) return 6;
-  if (isnan(d7)) return 7;
-  if (isnan(d8)) return 8;
-  return kNoFlow;
+  return cnan ? (uint32_t)kNoData : code;
 }
 
 // H1, vectorised: each lane owns 4 adjacent columns of a 128-column warp
