@@ -52,6 +52,9 @@
 
 namespace fa {
 
+#ifndef FA_P1_MINB
+#define FA_P1_MINB 8
+#endif
 constexpr uint8_t kOut = 254;  // ring cell: outside the block, data
 
 constexpr uint32_t SU_STOP = 0x8000u, SU_EXIT = 0x4000u, SU_T = 0x07FFu;
@@ -488,10 +491,11 @@ __device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc, in
     ndata += 4 - (__popc(nd) >> 3);
     if constexpr (SUCC) {
       uint2 sw;
-      if (ly > 0 && ly < h - 1 && lx0 > 0 && lx0 + 3 < w - 1) {
-        // interior word: every code 1..8 stays in the block.  Offsets of codes
-        // 1..8 (-32 -31 +1 +33 +32 +31 -1 -33, row stride 32) biased by +64
-        // to bytes, looked up 4 at a time, zero-extended to 16-bit lanes.
+      if (h == WB::BR && w == WB::BC) {
+        // full block: SWAR.  Offsets of codes 1..8 (-32 -31 +1 +33 +32 +31
+        // -1 -33, row stride 32) biased by +64 to bytes, looked up 4 at a
+        // time, zero-extended to 16-bit lanes; on the block border a second
+        // lookup flags the codes that leave through that side (EXIT).
         constexpr uint32_t T0 = 0x61412120u, T1 = 0x1F3F5F60u;
         const uint32_t sel = __vsub4(c1, 0x01010101u) & 0x07070707u;  // code - 1 per byte (no borrow)
         const uint32_t nib = (sel & 7u) | ((sel >> 4) & 0x70u) | ((sel >> 8) & 0x700u) | ((sel >> 12) & 0x7000u);
@@ -500,9 +504,16 @@ __device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc, in
         const uint32_t ta = __vadd2((i0 & 0xFFFFu) | ((i0 + 1u) << 16), __byte_perm(off4, 0u, 0x4140u));
         const uint32_t tb = __vadd2(((i0 + 2u) & 0xFFFFu) | ((i0 + 3u) << 16), __byte_perm(off4, 0u, 0x4342u));
         const uint32_t stop4 = __vcmpeq4(c1, 0u) | __vcmpeq4(c1, 0xFFFFFFFFu);
+        uint32_t ex4 = 0;  // 0x01 in the bytes whose code leaves the block
+        if (ly == 0) ex4 |= __byte_perm(0x00000101u, 0x01000000u, nib);           // N, NE, NW
+        if (ly == WB::BR - 1) ex4 |= __byte_perm(0x01000000u, 0x00000101u, nib);  // SE, S, SW
+        if (lx0 == 0) ex4 |= __byte_perm(0u, 0x01010100u, nib) & 0xFFu;           // SW, W, NW (cell 0)
+        if (lx0 == WB::BC - 4) ex4 |= __byte_perm(0x01010100u, 0u, nib) & 0xFF000000u;  // NE, E, SE (cell 3)
+        ex4 &= ~stop4;
         const uint32_t sa = __byte_perm(stop4, 0u, 0x1100u), sb = __byte_perm(stop4, 0u, 0x3322u);
-        sw.x = (sa & 0x80008000u) | (~sa & ta);
-        sw.y = (sb & 0x80008000u) | (~sb & tb);
+        const uint32_t xa = __byte_perm(ex4, 0u, 0x4140u) * 0xFFFFu, xb = __byte_perm(ex4, 0u, 0x4342u) * 0xFFFFu;
+        sw.x = (sa & 0x80008000u) | (xa & 0xC000C000u) | (~(sa | xa) & ta);
+        sw.y = (sb & 0x80008000u) | (xb & 0xC000C000u) | (~(sb | xb) & tb);
       } else {
         uint32_t v[4];
         const uint32_t fr = forb_row(ly, h);
@@ -875,7 +886,7 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
 
 // ---------------------------------------------------------------- pass 1
 template <class T, int R, int WK, bool FROM_DEM>
-__global__ void __launch_bounds__(128, 8) k_pass1(PassArgs<T, WK> P) {
+__global__ void __launch_bounds__(128, FA_P1_MINB) k_pass1(PassArgs<T, WK> P) {
   using WB = WBT<R>;
   constexpr bool Z = FROM_DEM;
   extern __shared__ __align__(16) unsigned char smem[];
