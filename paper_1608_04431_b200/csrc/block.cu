@@ -582,29 +582,30 @@ __device__ __forceinline__ uint32_t kahn_block(WSmem<T, R, Z>& s, uint32_t nsrc,
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   uint16_t* Q = s.src;
+  // element offset of block cell c = 32*ly + lx in the raster rows: c + ly*(W-32)
+  const uint32_t wm = (uint32_t)W - 32u;
   uint32_t head = 0, tail = nsrc;
   while (head < tail) {
     __syncwarp();
     const uint32_t q = head + (uint32_t)lane;
     const bool valid = q < tail;
     head = tail - head < 32u ? tail : head + 32u;
-    bool ready = false;
-    int t = 0;
+    uint32_t ready = 0, t = 0;
     if (valid) {
-      const int c = Q[q];
+      const uint32_t c = Q[q];
       const uint32_t su = s.succ[c];
       if ((su & SU_STOP) == 0u) {
         // "A(n) <- A(n) + A(c)" and "decrement D(n)" (Alg. 1);
         // A(c) is final: every donor of c was popped in an earlier iteration
-        t = (int)(su & SU_T);
-        const T a = __ldcg(Ab + (c >> 5) * W + (c & 31));
-        g_add(Ab + (t >> 5) * W + (t & 31), a);
-        const int sh = (t & 3) * 8;
+        t = su & SU_T;
+        const T a = __ldcg(Ab + (c + (c >> 5) * wm));
+        g_add(Ab + (t + (t >> 5) * wm), a);
+        const uint32_t sh = (t & 3u) * 8u;
         const uint32_t old = atomicAdd(&s.pend[t >> 2], 0u - (1u << sh));
         ready = ((old >> sh) & 0xFFu) == 1u;  // the last pending donor: n joins the queue
       }
     }
-    const unsigned bm = __ballot_sync(kFull, ready);
+    const unsigned bm = __ballot_sync(kFull, ready != 0u);
     if (ready) Q[tail + (uint32_t)__popc(bm & lt)] = (uint16_t)t;
     tail += (uint32_t)__popc(bm);
   }
