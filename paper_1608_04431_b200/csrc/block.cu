@@ -104,11 +104,15 @@ struct __align__(16) WSmem {
   uint32_t pend[WB::BN / 4 > 256 ? WB::BN / 4 : 256];
   alignas(8) uint16_t succ[WB::BN];
   uint16_t src[WB::BN];       // ready queue of Alg. 1 (sources first; each cell enters at most once)
-  uint32_t need[128];         // per perimeter slot: donors outside the block (ring cells draining in)
+  alignas(4) uint8_t need[128];  // per perimeter slot: donors outside the block (ring cells draining in)
   __device__ __forceinline__ uint32_t* slot_nid() { return pend; }
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+// +1 on byte p of a 4-aligned byte array (counts stay < 256)
+__device__ __forceinline__ void need_inc(uint8_t* need, int p) {
+  atomicAdd(reinterpret_cast<uint32_t*>(need) + (p >> 2), 1u << (8 * (p & 3)));
+}
 constexpr unsigned kFull = 0xFFFFFFFFu;
 
 template <int WK>
@@ -225,7 +229,7 @@ __device__ __forceinline__ void init_smem(WSmem<T, R, Z>& s) {
   uint32_t* D = reinterpret_cast<uint32_t*>(s.dirh);
   const int lane = lane_id();
   for (int i = lane; i < WBT<R>::HN / 4; i += 32) D[i] = 0xFFFFFFFFu;
-  for (int i = lane; i < 128; i += 32) s.need[i] = 0u;
+  reinterpret_cast<uint32_t*>(s.need)[lane] = 0u;
 }
 
 __device__ __forceinline__ const float* dem_row(const float* dem, const float* up, const float* dn, int64_t H,
@@ -354,7 +358,7 @@ __device__ __forceinline__ void ring_entries(WSmem<T, R, Z>& s, const PassArgs<T
       const int k = __ffs(ks) - 1;
       ks &= ks - 1;
       const int ty = ly + dir_dy(k), tx = lx + dir_dx(k);
-      if ((unsigned)ty < (unsigned)h && (unsigned)tx < (unsigned)w) atomicAdd(&s.need[bperim_index(tx, ty, h, w)], 1u);
+      if ((unsigned)ty < (unsigned)h && (unsigned)tx < (unsigned)w) need_inc(s.need, bperim_index(tx, ty, h, w));
     }
   }
 }
@@ -409,7 +413,7 @@ __device__ __forceinline__ void load_dirs(WSmem<T, R, Z>& s, const uint8_t* dirs
     s.dirh[WB::hidx(ly, lx)] = code == kNoData ? kNoData : kOut;
     if (entries && code >= 1 && code <= 8) {
       const int ty = ly + dir_dy(code), tx = lx + dir_dx(code);
-      if ((unsigned)ty < (unsigned)h && (unsigned)tx < (unsigned)w) atomicAdd(&s.need[bperim_index(tx, ty, h, w)], 1u);
+      if ((unsigned)ty < (unsigned)h && (unsigned)tx < (unsigned)w) need_inc(s.need, bperim_index(tx, ty, h, w));
     }
   }
 }
@@ -751,7 +755,7 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     const int p = lane + 32 * j;
-    if (ex[j] && s.need[p]) atomicAdd(&nchild[p], s.need[p]);
+    if (ex[j] && s.need[p]) atomicAdd(&nchild[p], (uint32_t)s.need[p]);
   }
   // walks (lanes refill from a warp-uniform work list as they finish); the
   // root (exit slot or kNoP) of a walked slot p is kept in need[p] afterwards
@@ -793,7 +797,7 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
         const uint32_t k = s.need[p] ? s.need[p] : (P.cut ? 1u : 0u);
         if (k) atomicAdd(&nchild[rp], k);
       }
-      s.need[p] = rp;  // only this lane touches need[p] from here on
+      s.need[p] = (uint8_t)rp;  // only this lane touches need[p] from here on
       p = -1;
       continue;
     }
