@@ -53,7 +53,7 @@
 namespace fa {
 
 #ifndef FA_P1_MINB
-#define FA_P1_MINB 8
+#define FA_P1_MINB 9
 #endif
 constexpr uint8_t kOut = 254;  // ring cell: outside the block, data
 
@@ -76,7 +76,8 @@ template <int R>
 struct WBT {
   static constexpr int BR = R, BC = 32, BN = BR * BC;
   static constexpr int PB = 2 * (BR + BC) - 4;
-  static constexpr int HS = 48, HOFF = 16;  // dirh: row stride, interior column (16-B aligned rows)
+  static constexpr int HS = 36, HOFF = 4;   // dirh: row stride, interior column (4-B aligned rows); the right
+                                            // ring cell of a row is byte 0 of the next row
   static constexpr int HN = (BR + 2) * HS + 16;
   static constexpr int ZS = 40, ZOFF = 4;   // z window: row stride, interior column (16-B aligned)
   static constexpr int ZR = BR + 4;         // window rows: 2-cell halo
@@ -99,13 +100,15 @@ struct __align__(16) WSmem {
     float z[Z ? WB::ZN : 4];  // z window (fused D8 only)
   } u;
   uint8_t dirh[WB::HN];
-  // pending in-block donor counts, one byte per cell; after the queue loop:
-  // [0,128) slot -> node id, [128,256) per exit slot: outside donors
-  uint32_t pend[WB::BN / 4 > 256 ? WB::BN / 4 : 256];
+  uint32_t pend[WB::BN / 8];  // pending in-block donor counts, 4 bits per cell (<= 8)
   alignas(8) uint16_t succ[WB::BN];
-  uint16_t src[WB::BN];       // ready queue of Alg. 1 (sources first; each cell enters at most once)
+  // ready queue of Alg. 1 (sources first; each cell enters at most once);
+  // after the queue loop: [0,128) slot -> node id, [128,256) per exit slot:
+  // outside donors of the entries draining to it
+  alignas(16) uint16_t src[WB::BN];
   alignas(4) uint8_t need[128];  // per perimeter slot: donors outside the block (ring cells draining in)
-  __device__ __forceinline__ uint32_t* slot_nid() { return pend; }
+  __device__ __forceinline__ uint32_t* slot_nid() { return reinterpret_cast<uint32_t*>(src); }
+  static_assert(WB::BN * 2 >= 256 * 4, "records scratch lives in the queue");
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -386,7 +389,11 @@ __device__ __forceinline__ void load_dirs(WSmem<T, R, Z>& s, const uint8_t* dirs
         const uint32_t hi = __vcmpgtu4(vv[j], 0x08080808u) & ~__vcmpeq4(vv[j], 0xFFFFFFFFu);
         if (hi) { bad = true; vv[j] |= hi; }
       }
-      *reinterpret_cast<uint4*>(&s.dirh[WB::hidx(ly, lx)]) = v;
+      uint32_t* dst = reinterpret_cast<uint32_t*>(&s.dirh[WB::hidx(ly, lx)]);
+      dst[0] = vv[0];
+      dst[1] = vv[1];
+      dst[2] = vv[2];
+      dst[3] = vv[3];
     }
   } else {
     for (int i = lane; i < h * WB::BC; i += 32) {
@@ -434,6 +441,30 @@ __device__ __forceinline__ void succ_from_dirs(WSmem<T, R, Z>& s, int h, int w) 
 }
 
 // ---------------------------------------------------------------- H2
+// Donor masks of the 4 cells of dirh word hw: bit k-1 of byte j set iff the
+// neighbour of cell j in direction k drains into it (its code is opp(k)).
+template <int R>
+__device__ __forceinline__ uint32_t donor_masks(const uint32_t* D, int hw) {
+  constexpr int RW = WBT<R>::HS / 4;
+  const uint32_t u0 = D[hw - RW - 1], u1 = D[hw - RW], u2 = D[hw - RW + 1];
+  const uint32_t c0 = D[hw - 1], c1 = D[hw], c2 = D[hw + 1];
+  const uint32_t d0 = D[hw + RW - 1], d1 = D[hw + RW], d2 = D[hw + RW + 1];
+  const uint32_t nN = u1, nS = d1;
+  const uint32_t nE = __funnelshift_r(c1, c2, 8), nW = __funnelshift_r(c0, c1, 24);
+  const uint32_t nNE = __funnelshift_r(u1, u2, 8), nNW = __funnelshift_r(u0, u1, 24);
+  const uint32_t nSE = __funnelshift_r(d1, d2, 8), nSW = __funnelshift_r(d0, d1, 24);
+  uint32_t m = 0;
+  m |= (__vcmpeq4(nN, 0x05050505u) & 0x01010101u) << 0;
+  m |= (__vcmpeq4(nNE, 0x06060606u) & 0x01010101u) << 1;
+  m |= (__vcmpeq4(nE, 0x07070707u) & 0x01010101u) << 2;
+  m |= (__vcmpeq4(nSE, 0x08080808u) & 0x01010101u) << 3;
+  m |= (__vcmpeq4(nS, 0x01010101u) & 0x01010101u) << 4;
+  m |= (__vcmpeq4(nSW, 0x02020202u) & 0x01010101u) << 5;
+  m |= (__vcmpeq4(nW, 0x03030303u) & 0x01010101u) << 6;
+  m |= (__vcmpeq4(nNW, 0x04040404u) & 0x01010101u) << 7;
+  return m;
+}
+
 // Donor masks by an 8-neighbour gather, 4 cells per 32-bit SWAR word (no
 // atomics; Alg. 1 first loop P:L131-148) and the ready queue seeded with the
 // sources (data cells without in-block donors).  The pending counts D(p)
@@ -453,7 +484,6 @@ __device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc, in
   static_assert(NQ <= 8, "source bits: 4 per word, 32 per lane");
   const int lane = lane_id();
   const uint32_t* D = reinterpret_cast<const uint32_t*>(s.dirh);
-  constexpr int RW = WB::HS / 4;
   int ndata = 0;
   uint32_t srcbits = 0, ndbits = 0;
 #pragma unroll 1
@@ -461,36 +491,20 @@ __device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc, in
     const int q = k * 32 + lane;  // word: row q/8, cells 4(q%8)..+3
     const int ly = q >> 3, lx0 = (q & 7) * 4;
     const int hw = WB::hidx(ly, lx0) >> 2;
-    const uint32_t u0 = D[hw - RW - 1], u1 = D[hw - RW], u2 = D[hw - RW + 1];
-    const uint32_t c0 = D[hw - 1], c1 = D[hw], c2 = D[hw + 1];
-    const uint32_t d0 = D[hw + RW - 1], d1 = D[hw + RW], d2 = D[hw + RW + 1];
-    const uint32_t nN = u1, nS = d1;
-    const uint32_t nE = __funnelshift_r(c1, c2, 8), nW = __funnelshift_r(c0, c1, 24);
-    const uint32_t nNE = __funnelshift_r(u1, u2, 8), nNW = __funnelshift_r(u0, u1, 24);
-    const uint32_t nSE = __funnelshift_r(d1, d2, 8), nSW = __funnelshift_r(d0, d1, 24);
-    uint32_t m = 0;
-    // a neighbour in direction k is a donor iff its code points back: opp(k)
-    m |= (__vcmpeq4(nN, 0x05050505u) & 0x01010101u) << 0;
-    m |= (__vcmpeq4(nNE, 0x06060606u) & 0x01010101u) << 1;
-    m |= (__vcmpeq4(nE, 0x07070707u) & 0x01010101u) << 2;
-    m |= (__vcmpeq4(nSE, 0x08080808u) & 0x01010101u) << 3;
-    m |= (__vcmpeq4(nS, 0x01010101u) & 0x01010101u) << 4;
-    m |= (__vcmpeq4(nSW, 0x02020202u) & 0x01010101u) << 5;
-    m |= (__vcmpeq4(nW, 0x03030303u) & 0x01010101u) << 6;
-    m |= (__vcmpeq4(nNW, 0x04040404u) & 0x01010101u) << 7;
+    const uint32_t c1 = D[hw];
+    uint32_t m = donor_masks<R>(D, hw);
     // NoData (255) and cells outside a ragged block (254/255) are not cells
     const uint32_t nd = __vcmpgeu4(c1, 0xFEFEFEFEu);
-    // in-block NoData cells with in-block donors: keep their raw mask (in
-    // pend, never touched by the queue) to stop their donors below
+    // in-block NoData cells with in-block donors: their donors are stopped below
     const uint32_t inb = ly >= h ? 0u : lx0 + 4 <= w ? 0xFFFFFFFFu : lx0 >= w ? 0u : (0xFFFFFFFFu >> (8 * (lx0 + 4 - w)));
     const uint32_t sink = SUCC ? (nd & inb & ~__vcmpeq4(m, 0u)) : 0u;
-    const uint32_t mraw = m;
     m &= ~nd;
-    // per-byte popcount of the masks
+    // per-byte popcount of the masks, packed to 4 bits per cell
     uint32_t cnt = m - ((m >> 1) & 0x55555555u);
     cnt = (cnt & 0x33333333u) + ((cnt >> 2) & 0x33333333u);
     cnt = (cnt + (cnt >> 4)) & 0x0F0F0F0Fu;
-    s.pend[q] = (cnt & ~sink) | (mraw & sink);
+    reinterpret_cast<uint16_t*>(s.pend)[q] =
+        (uint16_t)((cnt & 0xFu) | ((cnt >> 4) & 0xF0u) | ((cnt >> 8) & 0xF00u) | ((cnt >> 12) & 0xF000u));
     ndbits |= (sink ? 1u : 0u) << k;
     ndata += 4 - (__popc(nd) >> 3);
     if constexpr (SUCC) {
@@ -539,9 +553,11 @@ __device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc, in
     for (int k = 0; k < NQ; ++k) {
       if (!((ndbits >> k) & 1u)) continue;
       const int q = k * 32 + lane;
-      const uint32_t pw = s.pend[q];
-      const uint32_t nd = __vcmpgeu4(reinterpret_cast<const uint32_t*>(s.dirh)[WB::hidx(q >> 3, (q & 7) * 4) >> 2],
-                                     0xFEFEFEFEu);
+      const int hw = WB::hidx(q >> 3, (q & 7) * 4) >> 2;
+      const uint32_t pw = donor_masks<R>(D, hw);  // raw masks (the NoData cells' too)
+      const int ly = q >> 3, lx0 = (q & 7) * 4;
+      const uint32_t inb = ly >= h ? 0u : lx0 + 4 <= w ? 0xFFFFFFFFu : lx0 >= w ? 0u : (0xFFFFFFFFu >> (8 * (lx0 + 4 - w)));
+      const uint32_t nd = __vcmpgeu4(D[hw], 0xFEFEFEFEu) & inb;  // in-block NoData only (not the ring)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (!((nd >> (8 * j)) & 1u)) continue;
@@ -604,9 +620,9 @@ __device__ __forceinline__ uint32_t kahn_block(WSmem<T, R, Z>& s, uint32_t nsrc,
         t = su & SU_T;
         const T a = __ldcg(Ab + (c + (c >> 5) * wm));
         g_add(Ab + (t + (t >> 5) * wm), a);
-        const uint32_t sh = (t & 3u) * 8u;
-        const uint32_t old = atomicAdd(&s.pend[t >> 2], 0u - (1u << sh));
-        ready = ((old >> sh) & 0xFFu) == 1u;  // the last pending donor: n joins the queue
+        const uint32_t sh = (t & 7u) * 4u;
+        const uint32_t old = atomicAdd(&s.pend[t >> 3], 0u - (1u << sh));
+        ready = ((old >> sh) & 0xFu) == 1u;  // the last pending donor: n joins the queue
       }
     }
     const unsigned bm = __ballot_sync(kFull, ready != 0u);
@@ -693,8 +709,8 @@ __device__ __forceinline__ void write_dirs(const WSmem<T, R, Z>& s, uint8_t* dir
   if (vec) {
     for (int q = lane; q < h * 2; q += 32) {
       const int ly = q >> 1, lx = (q & 1) * 16;
-      *reinterpret_cast<uint4*>(dirs + (y0 + ly) * g.W + x0 + lx) =
-          *reinterpret_cast<const uint4*>(&s.dirh[WB::hidx(ly, lx)]);
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(&s.dirh[WB::hidx(ly, lx)]);
+      *reinterpret_cast<uint4*>(dirs + (y0 + ly) * g.W + x0 + lx) = make_uint4(src[0], src[1], src[2], src[3]);
     }
   } else {
     for (int i = lane; i < h * WB::BC; i += 32) {
@@ -725,8 +741,8 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   const int np = bperim_count(h, w);
-  uint32_t* slot_nid = s.pend;       // pend is dead after the queue loop
-  uint32_t* nchild = s.pend + 128;   // per exit slot: outside donors of the entries draining to it
+  uint32_t* slot_nid = s.slot_nid();  // the queue is dead after the queue loop
+  uint32_t* nchild = slot_nid + 128;   // per exit slot: outside donors of the entries draining to it
   for (int i = lane; i < 128; i += 32) nchild[i] = 0u;
   int64_t t0y, t0x, th, tw;
   g.tile_box(g.tile_of_block(b), t0y, t0x, th, tw);
