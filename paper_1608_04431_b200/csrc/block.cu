@@ -992,7 +992,7 @@ __global__ void __launch_bounds__(128) k_pass2(PassArgs<T, WK> P) {
 // ---------------------------------------------------------------- RETAIN finalize
 // "add A' to every cell in its downstream flow path" (Alg. 3): acc
 // already holds the block-local accumulation written by pass 1.  A warp owns
-// KB consecutive blocks: it stages their codes in shared memory, compacts
+// KB consecutive blocks (1 by default): it stages their codes in shared memory, compacts
 // the entry slots with a non-zero offset x (x = external inbound flow, D11)
 // into a work list, and its lanes walk those entries' in-block paths, adding
 // x to every cell up to the block exit or the NoFlow terminal (flow into
@@ -1084,8 +1084,12 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
     atomic_add(rowp + (int64_t)cy * g.W + cx, x);
     const int d = s.d[k][cy * WB::BC + cx];
     const int ty = cy + dir_dy(d), tx = cx + dir_dx(d);
-    if (d == kNoFlow || d > 8 || (unsigned)ty >= (unsigned)h || (unsigned)tx >= (unsigned)w ||
-        s.d[k][ty * WB::BC + tx] == kNoData) {
+    bool stop = d == kNoFlow || d > 8 || (unsigned)ty >= (unsigned)h || (unsigned)tx >= (unsigned)w;
+    // Flow into NoData is dropped (D8).  For f64 the walk may step onto the
+    // NoData cell instead of checking it: NaN + x = NaN, and its code (255)
+    // ends the walk there; integer markers would change, so they check.
+    if (!std::is_same<T, double>::value) stop = stop || s.d[k][ty * WB::BC + tx] == kNoData;
+    if (stop) {
       k = -1;  // terminal, block exit, or dropped into NoData
     } else {
       cy = ty;
@@ -1097,7 +1101,12 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
 template <class T, int R, int KB>
 cudaError_t launch_finalize_k(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st) {
   constexpr int NWC = 4;  // warps per CTA
-  const size_t sm = sizeof(FSmem<T, R, KB>) * NWC;
+  // At least 24 KB of shared memory per CTA: at most 9 CTAs (36 warps) per
+  // SM, which keeps the acc rows the walks touch in L2 (measured on cfg3:
+  // 3.82 ms vs 3.92 ms at full occupancy).  FA_FINPAD overrides (tuning).
+  const char* pad = getenv("FA_FINPAD");
+  size_t sm = sizeof(FSmem<T, R, KB>) * NWC;
+  sm = pad ? sm + (size_t)atoi(pad) : (sm < 24576 ? 24576 : sm);
   auto k = k_finalize<T, R, KB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int64_t groups = (g.nblocks + KB - 1) / KB;
@@ -1108,11 +1117,10 @@ cudaError_t launch_finalize_k(const Geom& g, const T* x_slot, const uint8_t* dir
 template <class T, int R>
 cudaError_t launch_finalize_r(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st) {
   const char* e = getenv("FA_FINKB");  // tuning override: blocks per warp
-  const int kb = e ? atoi(e) : 2;
+  const int kb = e ? atoi(e) : 1;
   if (kb == 2) return launch_finalize_k<T, R, 2>(g, x_slot, dirs, acc, st);
-  if (kb == 8) return launch_finalize_k<T, R, 8>(g, x_slot, dirs, acc, st);
   if (kb == 4) return launch_finalize_k<T, R, 4>(g, x_slot, dirs, acc, st);
-  return launch_finalize_k<T, R, 2>(g, x_slot, dirs, acc, st);
+  return launch_finalize_k<T, R, 1>(g, x_slot, dirs, acc, st);
 }
 
 template <class T>

@@ -6,4 +6,5 @@ $CMD > gpurun_out/prof_plain.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_pass1 -s 3 -c 1 -o gpurun_out/full_pass1 $CMD > gpurun_out/ncu_full.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_d8v -s 3 -c 1 -o gpurun_out/full_d8 $CMD > gpurun_out/ncu_full_d8.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_finalize -s 0 -c 1 -o gpurun_out/full_fin $CMD > gpurun_out/ncu_full_fin.log 2>&1
 echo done
