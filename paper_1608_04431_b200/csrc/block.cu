@@ -48,7 +48,7 @@
 // fp64 sums follow the arrival order; any order is within D13.
 #include <cstdlib>
 
-#include "fa_internal.cuh"
+#include "d8.cuh"
 
 namespace fa {
 
@@ -116,7 +116,6 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ void need_inc(uint8_t* need, int p) {
   atomicAdd(reinterpret_cast<uint32_t*>(need) + (p >> 2), 1u << (8 * (p & 3)));
 }
-constexpr unsigned kFull = 0xFFFFFFFFu;
 
 template <int WK>
 __device__ __forceinline__ bool weight_ok(float v) {
@@ -168,48 +167,6 @@ __device__ __forceinline__ void sh_add(double* p, double v, double cur) {
   }
 }
 
-// ---------------------------------------------------------------- H1 core
-// D8 of one cell from its 3x3 window (NaN = NoData / off-grid): steepest
-// strictly-downhill data neighbour, drops fl32(zc - zn) (D5), cardinal vs
-// diagonal by the exact compare 2a^2 > b^2 in fp64 (D4), ties to the lowest
-// code (D2); none -> lowest NaN neighbour (outlet, D3; returned | 16: the
-// target is NoData), else NoFlow (D6).
-__device__ __forceinline__ int d8_window(float zc, float zN, float zNE, float zE, float zSE, float zS,
-                                         float zSW, float zW, float zNW) {
-  if (isnan(zc)) return kNoData;
-  const float d1 = __fsub_rn(zc, zN), d3 = __fsub_rn(zc, zE), d5 = __fsub_rn(zc, zS), d7 = __fsub_rn(zc, zW);
-  const float d2 = __fsub_rn(zc, zNE), d4 = __fsub_rn(zc, zSE), d6 = __fsub_rn(zc, zSW),
-              d8 = __fsub_rn(zc, zNW);
-  // NaN drops fail every comparison; strictly-larger replaces: lowest code wins ties
-  float a = 0.0f, b = 0.0f;
-  int kc = 0, kd = 0;
-  if (d1 > a) { a = d1; kc = 1; }
-  if (d3 > a) { a = d3; kc = 3; }
-  if (d5 > a) { a = d5; kc = 5; }
-  if (d7 > a) { a = d7; kc = 7; }
-  if (d2 > b) { b = d2; kd = 2; }
-  if (d4 > b) { b = d4; kd = 4; }
-  if (d6 > b) { b = d6; kd = 6; }
-  if (d8 > b) { b = d8; kd = 8; }
-  if (kc && kd) {
-    const double da = (double)a, db = (double)b;
-    return __dmul_rn(__dmul_rn(2.0, da), da) > __dmul_rn(db, db) ? kc : kd;
-  }
-  if (kc | kd) return kc | kd;
-  int k = kNoFlow;
-  if (isnan(zN)) k = 1;
-  else if (isnan(zNE)) k = 2;
-  else if (isnan(zE)) k = 3;
-  else if (isnan(zSE)) k = 4;
-  else if (isnan(zS)) k = 5;
-  else if (isnan(zSW)) k = 6;
-  else if (isnan(zW)) k = 7;
-  else if (isnan(zNW)) k = 8;
-  return k ? (k | 16) : kNoFlow;
-}
-
-// successor word of in-block cell i with code d (| 16: the target is
-// NoData); `forb` = direction codes that leave the block from this cell
 template <int R>
 __device__ __forceinline__ uint32_t succ_word(int i, int d, uint32_t forb) {
   const int k = d & 15;
@@ -235,13 +192,6 @@ __device__ __forceinline__ void init_smem(WSmem<T, R, Z>& s) {
   reinterpret_cast<uint32_t*>(s.need)[lane] = 0u;
 }
 
-__device__ __forceinline__ const float* dem_row(const float* dem, const float* up, const float* dn, int64_t H,
-                                                int64_t W, int64_t gy) {
-  if (gy < -1 || gy > H) return nullptr;
-  if (gy == -1) return up;
-  if (gy == H) return dn;
-  return dem + gy * W;
-}
 
 // z window (block + 2-cell halo; NoData / off-grid -> NaN).  Rows of a strip
 // halo come from dem_up / dem_dn (H7); rows beyond those read as NaN and the
@@ -1188,218 +1138,5 @@ FA_INST(unsigned long long, 1)
 FA_INST(double, 0)
 FA_INST(double, 2)
 #undef FA_INST
-
-// ---------------------------------------------------------------- standalone D8
-// H1 as its own kernel (fa_flowdirs, and the first step of the single-device
-// path): a CTA stages a 32 x 128 tile of z with a 1-cell halo (float4 rows),
-// then each thread runs the same d8_window down one column with a rolling
-// 3x3 register window.  No large shared state, so many warps per SM hide the
-// latency of the compare chains.  Rows -1 / H come from dem_up / dem_dn (a
-// strip's halo rows) or are off-grid.
-constexpr int DR = 32, DC = 128, DZS = DC + 8;  // tile rows / cols, staged row stride (interior at col 4)
-__global__ void __launch_bounds__(DC) k_d8(const float* __restrict__ dem, const float* __restrict__ dem_up,
-                                           const float* __restrict__ dem_dn, int64_t H, int64_t W, float nodata,
-                                           uint8_t* __restrict__ dirs) {
-  __shared__ __align__(16) float zs[(DR + 2) * DZS];
-  const int64_t y0 = (int64_t)blockIdx.y * DR, x0 = (int64_t)blockIdx.x * DC;
-  const int tid = threadIdx.x;
-  const float qnan = __int_as_float(0x7fc00000);
-  const bool vec = x0 + DC <= W && ((W & 3) == 0) && ((reinterpret_cast<uintptr_t>(dem) & 15) == 0) &&
-                   (!dem_up || (reinterpret_cast<uintptr_t>(dem_up) & 15) == 0) &&
-                   (!dem_dn || (reinterpret_cast<uintptr_t>(dem_dn) & 15) == 0);
-  if (vec) {
-    // per row: 32 float4 + 2 halo scalars
-    for (int i = tid; i < (DR + 2) * (DC / 4 + 2); i += DC) {
-      const int r = i / (DC / 4 + 2), k = i - r * (DC / 4 + 2);
-      const float* row = dem_row(dem, dem_up, dem_dn, H, W, y0 + r - 1);
-      if (k < DC / 4) {
-        float4 v = make_float4(qnan, qnan, qnan, qnan);
-        if (row) {
-          v = __ldg(reinterpret_cast<const float4*>(row + x0) + k);
-          v.x = stage_z(v.x, nodata);
-          v.y = stage_z(v.y, nodata);
-          v.z = stage_z(v.z, nodata);
-          v.w = stage_z(v.w, nodata);
-        }
-        *reinterpret_cast<float4*>(&zs[r * DZS + 4 + 4 * k]) = v;
-      } else {
-        const int lx = k == DC / 4 ? -1 : DC;
-        const int64_t gx = x0 + lx;
-        float v = qnan;
-        if (row && gx >= 0 && gx < W) v = stage_z(__ldg(row + gx), nodata);
-        zs[r * DZS + 4 + lx] = v;
-      }
-    }
-  } else {
-    for (int i = tid; i < (DR + 2) * (DC + 2); i += DC) {
-      const int r = i / (DC + 2), lx = i - r * (DC + 2) - 1;
-      const float* row = dem_row(dem, dem_up, dem_dn, H, W, y0 + r - 1);
-      const int64_t gx = x0 + lx;
-      float v = qnan;
-      if (row && gx >= 0 && gx < W) v = stage_z(__ldg(row + gx), nodata);
-      zs[r * DZS + 4 + lx] = v;
-    }
-  }
-  __syncthreads();
-  const int64_t gx = x0 + tid;
-  if (gx >= W) return;
-  const int rows = (int)(H - y0 < DR ? H - y0 : DR);
-  int zi = 4 + tid;
-  float u0 = zs[zi - 1], u1 = zs[zi], u2 = zs[zi + 1];
-  zi += DZS;
-  float c0 = zs[zi - 1], c1 = zs[zi], c2 = zs[zi + 1];
-  uint8_t* out = dirs + y0 * W + gx;
-#pragma unroll 4
-  for (int ly = 0; ly < rows; ++ly) {
-    zi += DZS;
-    const float e0 = zs[zi - 1], e1 = zs[zi], e2 = zs[zi + 1];
-    const int d = d8_window(c1, u1, u2, c2, e2, e1, e0, c0, u0);
-    out[ly * W] = (uint8_t)(d == kNoData ? kNoData : (d & 15));
-    u0 = c0; u1 = c1; u2 = c2;
-    c0 = e0; c1 = e1; c2 = e2;
-  }
-}
-
-// D8 from precomputed drops (same rule as d8_window): centre NaN -> NoData;
-// a NaN drop means a NaN (NoData / off-grid) neighbour.  The best cardinal
-// and diagonal drops are maxima (fmaxf ignores NaN), their codes the first
-// equal drop in code order (lowest code on ties, D2); strictly downhill
-// means > 0; then the exact fp64 compare 2a^2 > b^2 (D4).
-__device__ __forceinline__ uint32_t d8_drops(bool cnan, float d1, float d2, float d3, float d4, float d5, float d6,
-                                             float d7, float d8) {
-  const float a = fmaxf(fmaxf(d1, d3), fmaxf(d5, d7));
-  const float b = fmaxf(fmaxf(d2, d4), fmaxf(d6, d8));
-  const uint32_t kc = d1 == a ? 1u : d3 == a ? 3u : d5 == a ? 5u : 7u;
-  const uint32_t kd = d2 == b ? 2u : d4 == b ? 4u : d6 == b ? 6u : 8u;
-  const bool vc = a > 0.0f, vd = b > 0.0f;
-  uint32_t code;
-  if (vc && vd) {
-    const double da = (double)a, db = (double)b;
-    code = __dmul_rn(__dmul_rn(2.0, da), da) > __dmul_rn(db, db) ? kc : kd;
-  } else if (vc | vd) {
-    code = vc ? kc : kd;
-  } else {
-    // no downhill data neighbour: the lowest NaN neighbour (outlet, D3), else NoFlow
-    code = isnan(d1) ? 1u : isnan(d2) ? 2u : isnan(d3) ? 3u : isnan(d4) ? 4u : isnan(d5) ? 5u
-         : isnan(d6) ? 6u : isnan(d7) ? 7u : isnan(d8) ? 8u : (uint32_t)kNoFlow;
-  }
-  return cnan ? (uint32_t)kNoData : code;
-}
-
-// H1, vectorised: each lane owns 4 adjacent columns of a 128-column warp
-// strip and runs down RS rows.  Rows are read as one float4 per lane (the
-// two outer columns come from the neighbour lanes by shuffles, or from the
-// halo at the warp's edges), and every pairwise drop is computed once:
-// fl(z_a - z_b) = -fl(z_b - z_a) exactly under round-to-nearest, so the drop
-// to the N / NW / NE neighbour is the negated S / SE / SW drop of the row
-// above, and W is the negated E drop of the left cell (D5 unchanged).
-constexpr int DV_RS = 32;  // rows per warp
-__global__ void __launch_bounds__(128) k_d8v(const float* __restrict__ dem, const float* __restrict__ dem_up,
-                                             const float* __restrict__ dem_dn, int64_t H, int64_t W, float nodata,
-                                             uint8_t* __restrict__ dirs) {
-  const int lane = threadIdx.x & 31;
-  const int64_t x0 = ((int64_t)blockIdx.x * 4 + (threadIdx.x >> 5)) * 128;
-  if (x0 >= W) return;
-  const int64_t y0 = (int64_t)blockIdx.y * DV_RS;
-  const int64_t gx = x0 + 4 * lane;
-  const bool own = gx < W;
-  const float qnan = __int_as_float(0x7fc00000);
-  // a row in flight: raw float4 of the lane's columns + the two warp-edge halo values
-  struct Raw {
-    float4 v;
-    float hl, hr;
-  };
-  auto issue = [&](int64_t gy) {
-    Raw q{make_float4(qnan, qnan, qnan, qnan), qnan, qnan};
-    const float* row = dem_row(dem, dem_up, dem_dn, H, W, gy);
-    if (row) {
-      if (own) q.v = __ldg(reinterpret_cast<const float4*>(row + gx));
-      if (lane == 0 && x0 > 0) q.hl = __ldg(row + x0 - 1);
-      if (lane == 31 && x0 + 128 < W) q.hr = __ldg(row + x0 + 128);
-    }
-    return q;
-  };
-  auto finish = [&](const Raw& q, float (&R)[6]) {
-    // NoData / non-finite -> NaN (off-grid values are NaN already)
-    const float4 v = make_float4(stage_z(q.v.x, nodata), stage_z(q.v.y, nodata), stage_z(q.v.z, nodata),
-                                 stage_z(q.v.w, nodata));
-    const float l = __shfl_up_sync(kFull, v.w, 1), r = __shfl_down_sync(kFull, v.x, 1);
-    R[0] = lane == 0 ? stage_z(q.hl, nodata) : l;
-    R[1] = v.x;
-    R[2] = v.y;
-    R[3] = v.z;
-    R[4] = v.w;
-    R[5] = lane == 31 ? stage_z(q.hr, nodata) : r;
-  };
-  float P[6], C[6], D[6];
-  {
-    const Raw q0 = issue(y0 - 1), q1 = issue(y0);
-    finish(q0, P);
-    finish(q1, C);
-  }
-  Raw nxt = issue(y0 + 1);  // one row ahead of its use
-  // drops between the row above and the current row
-  float pv[6], ps[6], pt[6];
-#pragma unroll
-  for (int j = 0; j < 6; ++j) pv[j] = ps[j] = pt[j] = 0.0f;
-#pragma unroll
-  for (int j = 1; j <= 4; ++j) pv[j] = __fsub_rn(P[j], C[j]);
-#pragma unroll
-  for (int j = 0; j <= 4; ++j) ps[j] = __fsub_rn(P[j], C[j + 1]);
-#pragma unroll
-  for (int j = 1; j <= 5; ++j) pt[j] = __fsub_rn(P[j], C[j - 1]);
-  const int rows = (int)(H - y0 < DV_RS ? H - y0 : DV_RS);
-  uint8_t* out = dirs + y0 * W + gx;
-  for (int r = 0; r < rows; ++r) {
-    const Raw cur = nxt;
-    nxt = issue(y0 + r + 2);
-    finish(cur, D);
-    float v[6], sd[6], t[6], hh[6];
-#pragma unroll
-    for (int j = 0; j < 6; ++j) v[j] = sd[j] = t[j] = hh[j] = 0.0f;
-#pragma unroll
-    for (int j = 1; j <= 4; ++j) v[j] = __fsub_rn(C[j], D[j]);
-#pragma unroll
-    for (int j = 0; j <= 4; ++j) sd[j] = __fsub_rn(C[j], D[j + 1]);
-#pragma unroll
-    for (int j = 1; j <= 5; ++j) t[j] = __fsub_rn(C[j], D[j - 1]);
-#pragma unroll
-    for (int j = 0; j <= 4; ++j) hh[j] = __fsub_rn(C[j], C[j + 1]);
-    uint32_t packed = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int j = i + 1;
-      // N, NE, E, SE, S, SW, W, NW
-      const uint32_t code = d8_drops(isnan(C[j]), -pv[j], -pt[j + 1], hh[j], sd[j], v[j], t[j], -hh[j - 1],
-                                     -ps[j - 1]);
-      packed |= code << (8 * i);
-    }
-    if (own) *reinterpret_cast<uint32_t*>(out + (int64_t)r * W) = packed;
-#pragma unroll
-    for (int j = 0; j < 6; ++j) {
-      pv[j] = v[j];
-      ps[j] = sd[j];
-      pt[j] = t[j];
-      C[j] = D[j];
-    }
-  }
-}
-
-cudaError_t launch_d8(const float* dem, const float* dem_up, const float* dem_dn, int64_t H, int64_t W,
-                      float nodata, uint8_t* dirs, cudaStream_t st) {
-  const bool vec = (W % 4) == 0 && ((reinterpret_cast<uintptr_t>(dem) & 15) == 0) &&
-                   ((reinterpret_cast<uintptr_t>(dirs) & 3) == 0) &&
-                   (!dem_up || (reinterpret_cast<uintptr_t>(dem_up) & 15) == 0) &&
-                   (!dem_dn || (reinterpret_cast<uintptr_t>(dem_dn) & 15) == 0);
-  const char* e = getenv("FA_D8V");
-  if (vec && !(e && e[0] == '0')) {
-    dim3 grid((unsigned)((W + 511) / 512), (unsigned)((H + DV_RS - 1) / DV_RS));
-    k_d8v<<<grid, 128, 0, st>>>(dem, dem_up, dem_dn, H, W, nodata, dirs);
-  } else {
-    dim3 grid((unsigned)((W + DC - 1) / DC), (unsigned)((H + DR - 1) / DR));
-    k_d8<<<grid, DC, 0, st>>>(dem, dem_up, dem_dn, H, W, nodata, dirs);
-  }
-  return cudaGetLastError();
-}
 
 }  // namespace fa
