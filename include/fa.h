@@ -101,6 +101,24 @@ FA_API fa_status fa_accumulate_strips(fa_ctx* ctx, int nstrips, int64_t rows, in
                                       const float* dem, float nodata, const uint8_t* dirs,
                                       const void* w, fa_wtype wtype, void* acc, fa_atype atype);
 
+/* Out-of-core accumulation (the paper's EVICT strategy, P:L79-81,
+ * P:L255): dem / dirs / w / acc are HOST buffers (pinned memory
+ * gives full-speed copies; pageable works) and the raster may exceed device
+ * memory.  Only strips of whole tile rows are resident: `strip_rows` raster
+ * rows per strip (rounded up to the tile height; <= 0: sized from free
+ * device memory, ~40 B per resident cell).  Phase A uploads each strip (z
+ * with two halo rows per side, or dirs with one; w), runs D8 + pass 1 + the
+ * tile records and drops the strip; the perimeter graph is solved once;
+ * phase B uploads each strip again, recomputes pass 1, injects the offsets,
+ * finalizes and downloads A.  Copies of neighbouring strips overlap the
+ * compute (an upload and a download stream).  PCIe traffic per cell: 2x(z or dirs, w) in,
+ * A out.  Same results and errors as fa_accumulate; device pointers are
+ * rejected with FA_E_ARG. */
+FA_API fa_status fa_accumulate_streamed(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem,
+                                        float nodata, const uint8_t* dirs, const void* w,
+                                        fa_wtype wtype, void* acc, fa_atype atype,
+                                        int64_t strip_rows);
+
 /* H4/H5 intermediates for tests and tools: number of tile perimeter slots
  * for a rows x cols raster under the context's tiling (tiles row-major,
  * slots per tile in clockwise perimeter order from the tile's top-left,

@@ -148,6 +148,9 @@ struct fa_ctx {
   cudaEvent_t ev[8]{};
   uint32_t* d_small = nullptr;  // [0]=node_count [1]=status [2..3]=wsum(u64) [4..15] scratch
   uint32_t* h_small = nullptr;
+  // out-of-core streaming (fa_accumulate_streamed): copy stream + buffer events
+  cudaStream_t cs = nullptr, cs_out = nullptr;  // uploads / downloads (PCIe is full duplex)
+  cudaEvent_t ev_in[2]{}, ev_used[2]{}, ev_out[2]{};
   // multi-GPU
   ncclComm_t comm = nullptr;
   int rank = -1, nranks = 0;
@@ -693,6 +696,201 @@ fa_status accumulate_impl(fa_ctx* ctx, int64_t rows, int64_t cols, const float* 
   return s;
 }
 
+// ---------------------------------------------------------------- out-of-core (N2)
+// The raster lives in host memory and only one strip of whole tile rows (two,
+// double-buffered) is resident at a time: the paper's EVICT strategy
+// ("only the producer's information and a single tile need be in
+// RAM", P:L255 pass 2 recomputes the tile).  Phase A per strip:
+// upload z (+2 halo rows each side) or dirs (+1), and w; D8, pass 1 cut at
+// tile edges, tile records into the device-resident perimeter arrays; the
+// strip's raster state is dropped.  The producer's graph G2 is solved once
+// (H5).  Phase B per strip: upload again, recompute pass 1 (A_T in the
+// device strip buffer), inject x_T, solve the strip's tile-cut graph, the
+// finalize (H6), download A.  Uploads of strip i+1 (one copy stream) and the
+// download of strip i-1 (another: PCIe is full duplex) overlap strip i.
+template <class T, int WK>
+fa_status run_streamed(fa_ctx* ctx, int64_t H, int64_t W, const float* dem_h, float nodata,
+                       const uint8_t* dirs_h, const void* w_h, T* acc_h, int64_t strip_rows) {
+  using namespace fa;
+  cudaStream_t st = ctx->st;
+  Runtime& rt = ctx->rt;
+  reset_run(ctx);
+  if (!ctx->cs) {
+    CK(cudaStreamCreateWithFlags(&ctx->cs, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->cs_out, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaEventCreateWithFlags(&ctx->ev_in[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_used[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ctx->ev_out[b], cudaEventDisableTiming));
+    }
+  }
+  cudaStream_t cs = ctx->cs;
+  CK(cudaMemsetAsync(ctx->d_small, 0, 16 * sizeof(uint32_t), st));
+  CK(cudaEventRecord(ctx->ev[0], st));
+  const Geom gg = make_geom(H, W, ctx->tile_r, ctx->tile_c);
+  // strip height in tile rows: requested, else from free device memory
+  // (~40 B per resident cell: two z, w and A buffers plus pass-1 state)
+  int64_t sr_tiles;
+  if (strip_rows > 0) {
+    sr_tiles = (strip_rows + gg.TH - 1) / gg.TH;
+  } else {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot));
+    const int64_t rows_fit = (int64_t)((double)fr * 0.6 / (40.0 * (double)W));
+    sr_tiles = rows_fit / gg.TH;
+  }
+  if (sr_tiles < 1) sr_tiles = 1;
+  if (sr_tiles > gg.TR) sr_tiles = gg.TR;
+  const int64_t nst = (gg.TR + sr_tiles - 1) / sr_tiles;
+  const int64_t SRr = sr_tiles * gg.TH;  // rows per strip (the last may be shorter)
+  std::vector<int64_t> hbase;
+  const int64_t nslots = tile_perim_total(gg, &hbase);
+  uint32_t* links = rt.alloc<uint32_t>(nslots);
+  uint8_t* fdir = rt.alloc<uint8_t>(nslots);
+  T* tile_acc = rt.alloc<T>(nslots);
+  T* xT = rt.alloc<T>(nslots);
+  float* zb[2] = {nullptr, nullptr};
+  uint8_t* db[2] = {nullptr, nullptr};
+  float* wb[2] = {nullptr, nullptr};
+  T* ab[2] = {nullptr, nullptr};
+  const bool hasw = WK != 0;
+  for (int b = 0; b < 2; ++b) {
+    if (dem_h) zb[b] = rt.alloc<float>((size_t)((SRr + 4) * W));
+    else db[b] = rt.alloc<uint8_t>((size_t)((SRr + 2) * W));
+    if (hasw) wb[b] = rt.alloc<float>((size_t)(SRr * W));
+    ab[b] = rt.alloc<T>((size_t)(SRr * W));
+  }
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(cs);
+    cudaStreamSynchronize(ctx->cs_out);
+    for (void* p : {(void*)links, (void*)fdir, (void*)tile_acc, (void*)xT, (void*)zb[0], (void*)zb[1], (void*)db[0],
+                    (void*)db[1], (void*)wb[0], (void*)wb[1], (void*)ab[0], (void*)ab[1]})
+      rt.free(p);
+  };
+  if (rt.err) { cleanup(); return set_err(ctx, FA_E_NOMEM, "device allocation failed (lower strip_rows)"); }
+  auto strip_span = [&](int64_t i, int64_t& r0, int64_t& r1) {
+    r0 = i * SRr;
+    r1 = r0 + SRr < H ? r0 + SRr : H;
+  };
+  // enqueue the uploads of strip i into buffer b (after its last reader)
+  auto upload = [&](int64_t i, int b) -> fa_status {
+    int64_t r0, r1;
+    strip_span(i, r0, r1);
+    CK(cudaStreamWaitEvent(cs, ctx->ev_used[b], 0));
+    if (dem_h) {
+      // buffer row k holds raster row r0 - 2 + k (rows off the raster are never read)
+      const int64_t a = r0 - 2 > 0 ? r0 - 2 : 0, e = r1 + 2 < H ? r1 + 2 : H;
+      CK(cudaMemcpyAsync(zb[b] + (a - (r0 - 2)) * W, dem_h + a * W, (size_t)((e - a) * W) * 4,
+                         cudaMemcpyHostToDevice, cs));
+    } else {
+      const int64_t a = r0 - 1 > 0 ? r0 - 1 : 0, e = r1 + 1 < H ? r1 + 1 : H;
+      CK(cudaMemcpyAsync(db[b] + (a - (r0 - 1)) * W, dirs_h + a * W, (size_t)((e - a) * W), cudaMemcpyHostToDevice,
+                         cs));
+    }
+    if (hasw)
+      CK(cudaMemcpyAsync(wb[b], static_cast<const float*>(w_h) + r0 * W, (size_t)((r1 - r0) * W) * 4,
+                         cudaMemcpyHostToDevice, cs));
+    CK(cudaEventRecord(ctx->ev_in[b], cs));
+    return FA_OK;
+  };
+  auto make_strip = [&](int64_t i, int b, Strip<T>& s) {
+    int64_t r0, r1;
+    strip_span(i, r0, r1);
+    const int64_t h = r1 - r0;
+    s.g = make_geom(h, W, gg.TH, gg.TW);
+    s.row_begin = r0;
+    s.nodata = nodata;
+    if (dem_h) {
+      const float* z = zb[b] + 2 * W;  // raster row r0
+      s.dem = z;
+      s.dem_up = r0 > 0 ? z - W : nullptr;
+      s.dem_up2 = r0 > 1 ? z - 2 * W : nullptr;
+      s.dem_dn = r1 < H ? z + h * W : nullptr;
+      s.dem_dn2 = r1 + 1 < H ? z + (h + 1) * W : nullptr;
+      s.halo2 = true;
+    } else {
+      const uint8_t* d = db[b] + W;
+      s.dirs = d;
+      s.dirs_up = r0 > 0 ? d - W : nullptr;
+      s.dirs_dn = r1 < H ? d + h * W : nullptr;
+    }
+    s.w = hasw ? wb[b] : nullptr;
+    s.acc = ab[b];  // pass 1 accumulates in place (phase A: scratch)
+    s.slot0 = hbase[(r0 / gg.TH) * gg.TC];
+  };
+  int64_t blocks = 0, nodes = 0;
+  // ---- phase A
+  FS(upload(0, 0));
+  for (int64_t i = 0; i < nst; ++i) {
+    const int b = (int)(i & 1);
+    if (i + 1 < nst) FS(upload(i + 1, b ^ 1));
+    CK(cudaStreamWaitEvent(st, ctx->ev_in[b], 0));
+    Strip<T> s;
+    make_strip(i, b, s);
+    fa_status r = strip_pass1<T, WK>(ctx, s, true);
+    if (r == FA_OK) r = strip_records<T>(ctx, s, links, fdir, tile_acc);
+    blocks += s.g.nblocks;
+    nodes += s.nn;
+    s.release(rt);
+    if (r != FA_OK) { cleanup(); return r; }
+    CK(cudaEventRecord(ctx->ev_used[b], st));
+  }
+  CK(cudaEventRecord(ctx->ev[1], st));
+  CK(rt.read(ctx->d_small + 1, 3));
+  {
+    unsigned long long wsum = 0;
+    memcpy(&wsum, &rt.h_cnt[1], 8);
+    fa_status r = check_status(ctx, rt.h_cnt[0] & ~ST_CYCLE, wsum, std::is_same<T, uint32_t>::value);
+    if (r != FA_OK) { cleanup(); cudaStreamSynchronize(st); return r; }
+  }
+  fa_status r = solve_g2<T>(ctx, gg, nslots, hbase, links, fdir, tile_acc, xT);
+  if (r != FA_OK) { cleanup(); return r; }
+  CK(cudaEventRecord(ctx->ev[2], st));
+  // ---- phase B
+  FS(upload(0, 0));
+  for (int64_t i = 0; i < nst; ++i) {
+    const int b = (int)(i & 1);
+    if (i + 1 < nst) FS(upload(i + 1, b ^ 1));
+    CK(cudaStreamWaitEvent(st, ctx->ev_in[b], 0));
+    if (i >= 2) CK(cudaStreamWaitEvent(st, ctx->ev_out[b], 0));  // A of strip i-2 is downloaded
+    Strip<T> s;
+    make_strip(i, b, s);
+    r = strip_pass1<T, WK>(ctx, s, true);
+    if (r == FA_OK) {
+      std::vector<int64_t> hb;
+      s.nslots = tile_perim_total(s.g, &hb);
+      s.dtbase = rt.alloc<int64_t>(hb.size());
+      if (rt.err) r = set_err(ctx, FA_E_NOMEM, "device allocation failed");
+      else {
+        CK(cudaMemcpyAsync(s.dtbase, hb.data(), hb.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        r = strip_finish<T, WK>(ctx, s, xT);
+        CK(cudaStreamSynchronize(st));  // hb must outlive the async copy
+      }
+    }
+    s.release(rt);
+    if (r != FA_OK) { cleanup(); return r; }
+    CK(cudaEventRecord(ctx->ev_used[b], st));
+    int64_t r0, r1;
+    strip_span(i, r0, r1);
+    CK(cudaStreamWaitEvent(ctx->cs_out, ctx->ev_used[b], 0));
+    CK(cudaMemcpyAsync(acc_h + r0 * W, ab[b], (size_t)((r1 - r0) * W) * sizeof(T), cudaMemcpyDeviceToHost,
+                       ctx->cs_out));
+    CK(cudaEventRecord(ctx->ev_out[b], ctx->cs_out));
+  }
+  CK(cudaStreamWaitEvent(st, ctx->ev_out[(nst - 1) & 1], 0));
+  if (nst >= 2) CK(cudaStreamWaitEvent(st, ctx->ev_out[nst & 1], 0));
+  CK(cudaEventRecord(ctx->ev[3], st));
+  cleanup();
+  if (rt.err) return set_err(ctx, FA_E_CUDA, cudaGetErrorString(rt.err));
+  CK(rt.read(ctx->d_small + 1, 1));
+  r = check_status(ctx, rt.h_cnt[0], 0, false);
+  if (r != FA_OK) return r;
+  record_stats(ctx, H * W, blocks, nodes, nslots);
+  ctx->stats.bytes_exchanged = (int64_t)(2 * H * W * ((dem_h ? 4 : 1) + (hasw ? 4 : 0)) + H * W * (int64_t)sizeof(T));
+  CK(cudaStreamSynchronize(st));
+  return FA_OK;
+}
+
 // ---------------------------------------------------------------- multi-GPU (H7)
 template <class T>
 ncclDataType_t nccl_type() {
@@ -871,6 +1069,11 @@ fa_status fa_destroy(fa_ctx* ctx) {
   if (ctx->comm) fa::nccl().commDestroy(ctx->comm);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  for (int b = 0; b < 2; ++b)
+    for (cudaEvent_t e : {ctx->ev_in[b], ctx->ev_used[b], ctx->ev_out[b]})
+      if (e) cudaEventDestroy(e);
+  if (ctx->cs) cudaStreamDestroy(ctx->cs);
+  if (ctx->cs_out) cudaStreamDestroy(ctx->cs_out);
   cudaFree(ctx->d_small);
   cudaFreeHost(ctx->h_small);
   delete ctx;
@@ -919,6 +1122,30 @@ fa_status fa_accumulate_strips(fa_ctx* ctx, int nstrips, int64_t rows, int64_t c
   if (!acc) return set_err(ctx, FA_E_ARG, "acc is NULL");
   if (nstrips < 1) return set_err(ctx, FA_E_ARG, "nstrips must be >= 1");
   return accumulate_impl(ctx, rows, cols, dem, nodata, dirs, w, wtype, acc, atype, rec, nstrips);
+}
+
+fa_status fa_accumulate_streamed(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem, float nodata,
+                                 const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc, fa_atype atype,
+                                 int64_t strip_rows) {
+  if (!ctx) return FA_E_ARG;
+  ctx->err.clear();
+  if (rows <= 0 || cols <= 0) return set_err(ctx, FA_E_ARG, "rows and cols must be > 0");
+  if (!acc) return set_err(ctx, FA_E_ARG, "acc is NULL");
+  FS(check_types(ctx, dem, dirs, w, wtype, atype));
+  for (const void* p : {(const void*)dem, (const void*)dirs, w, (const void*)acc})
+    if (p && is_device_ptr(p)) return set_err(ctx, FA_E_ARG, "fa_accumulate_streamed takes host buffers");
+  CK(cudaSetDevice(ctx->device));
+  if (atype == FA_A_U32) {
+    return wtype == FA_W_NONE ? run_streamed<uint32_t, 0>(ctx, rows, cols, dem, nodata, dirs, w, (uint32_t*)acc, strip_rows)
+                              : run_streamed<uint32_t, 1>(ctx, rows, cols, dem, nodata, dirs, w, (uint32_t*)acc, strip_rows);
+  }
+  if (atype == FA_A_U64) {
+    using U = unsigned long long;
+    return wtype == FA_W_NONE ? run_streamed<U, 0>(ctx, rows, cols, dem, nodata, dirs, w, (U*)acc, strip_rows)
+                              : run_streamed<U, 1>(ctx, rows, cols, dem, nodata, dirs, w, (U*)acc, strip_rows);
+  }
+  return wtype == FA_W_NONE ? run_streamed<double, 0>(ctx, rows, cols, dem, nodata, dirs, w, (double*)acc, strip_rows)
+                            : run_streamed<double, 2>(ctx, rows, cols, dem, nodata, dirs, w, (double*)acc, strip_rows);
 }
 
 int64_t fa_perimeter_slots(const fa_ctx* ctx, int64_t rows, int64_t cols) {

@@ -26,7 +26,7 @@ FLOW_TERMINATES = 0xFFFFFFFF
 
 EXPORTS = ["fa_create", "fa_destroy", "fa_last_error", "fa_flowdirs", "fa_accumulate",
            "fa_accumulate_strips", "fa_perimeter_slots", "fa_perimeter_records", "fa_nccl_unique_id",
-           "fa_accumulate_dist", "fa_get_stats"]
+           "fa_accumulate_dist", "fa_get_stats", "fa_accumulate_streamed"]
 
 
 def nccl_unique_id() -> bytes:
@@ -77,6 +77,7 @@ def load() -> ctypes.CDLL:
     lib.fa_flowdirs.argtypes = [P, P, I, I, F, P]
     lib.fa_accumulate.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int]
     lib.fa_accumulate_strips.argtypes = [P, ctypes.c_int, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int]
+    lib.fa_accumulate_streamed.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int, I]
     lib.fa_perimeter_slots.argtypes = [P, I, I]
     lib.fa_perimeter_slots.restype = I
     lib.fa_perimeter_records.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, ctypes.c_int, P, P, P, P]
@@ -190,6 +191,25 @@ class Context:
             out = torch.empty((rows, cols), dtype=TORCH_ACC[a], device=src.device)
         self._check(self.lib.fa_accumulate_strips(self.h, int(nstrips), rows, cols, _ptr(dem), float(nodata),
                                                   _ptr(dirs), _ptr(w), _wtype(w), _ptr(out), a))
+        return out
+
+    def accumulate_streamed(self, dem=None, dirs=None, w=None, atype: str = "u32", nodata: float = -9999.0,
+                            strip_rows: int = 0, out=None):
+        """Out-of-core accumulation (N2): host arrays in and out (numpy, or CPU / pinned torch
+        tensors); only `strip_rows`-row strips are resident on the device (0: sized from free
+        device memory)."""
+        src = dem if dem is not None else dirs
+        rows, cols = src.shape
+        a = ATYPES[atype]
+        if out is None:
+            if isinstance(src, torch.Tensor):
+                out = torch.empty((rows, cols), dtype=TORCH_ACC[a], pin_memory=src.is_pinned())
+            else:
+                import numpy as np
+
+                out = np.empty((rows, cols), {A_U32: np.uint32, A_U64: np.uint64, A_F64: np.float64}[a])
+        self._check(self.lib.fa_accumulate_streamed(self.h, rows, cols, _ptr(dem), float(nodata), _ptr(dirs),
+                                                    _ptr(w), _wtype(w), _ptr(out), a, int(strip_rows)))
         return out
 
     def accumulate_dist(self, nccl_id: bytes, rank: int, nranks: int, global_rows: int, row_begin: int,
