@@ -45,14 +45,15 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
-    """variant "prof": -DFA_PHASE_CLOCKS per-phase cycle counters -> libfa_prof.so
-    (a tuning tool; never the product library)."""
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """variant "prof": -DFA_PHASE_CLOCKS per-phase cycle counters -> libfa_prof.so;
+    other variants build libfa_<variant>.so with the given -D defines (tuning
+    builds loaded through FA_LIB; never the product library)."""
     lib = LIB if not variant else os.path.join(HERE, f"libfa_{variant}.so")
     if not force and not variant and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    extra = ["-DFA_PHASE_CLOCKS"] if variant == "prof" else []
+    extra = (["-DFA_PHASE_CLOCKS"] if variant == "prof" else []) + [f"-D{d}" for d in defines]
     inc = ["-I", os.path.join(ROOT, "include"), "-I", nccl_include()]
     objdir = os.path.join(HERE, "build", variant or "release")
     os.makedirs(objdir, exist_ok=True)

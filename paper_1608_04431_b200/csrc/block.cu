@@ -52,6 +52,12 @@
 
 namespace fa {
 
+#ifndef FA_FIN_STEPS
+#define FA_FIN_STEPS 1
+#endif
+#ifndef FA_REC_STEPS
+#define FA_REC_STEPS 4
+#endif
 #ifndef FA_P1_MINB
 #define FA_P1_MINB 9
 #endif
@@ -769,6 +775,12 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
     }
     c = (int)(su & SU_T);
     su = s.succ[c];
+#pragma unroll
+    for (int u = 1; u < FA_REC_STEPS; ++u) {  // more steps per refill round
+      if (su & SU_STOP) break;
+      c = (int)(su & SU_T);
+      su = s.succ[c];
+    }
   }
   __syncwarp();
   // exits: leaves push their value to the target slot, the rest become nodes
@@ -1031,17 +1043,22 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
     }
     head += __popc(idle);
     if (k < 0) continue;
-    atomic_add(rowp + (int64_t)cy * g.W + cx, x);
-    const int d = s.d[k][cy * WB::BC + cx];
-    const int ty = cy + dir_dy(d), tx = cx + dir_dx(d);
-    bool stop = d == kNoFlow || d > 8 || (unsigned)ty >= (unsigned)h || (unsigned)tx >= (unsigned)w;
-    // Flow into NoData is dropped (D8).  For f64 the walk may step onto the
-    // NoData cell instead of checking it: NaN + x = NaN, and its code (255)
-    // ends the walk there; integer markers would change, so they check.
-    if (!std::is_same<T, double>::value) stop = stop || s.d[k][ty * WB::BC + tx] == kNoData;
-    if (stop) {
-      k = -1;  // terminal, block exit, or dropped into NoData
-    } else {
+    // FA_FIN_STEPS path steps per refill round (the refill bookkeeping is
+    // paid once per round)
+#pragma unroll
+    for (int u = 0; u < FA_FIN_STEPS; ++u) {
+      atomic_add(rowp + (int64_t)cy * g.W + cx, x);
+      const int d = s.d[k][cy * WB::BC + cx];
+      const int ty = cy + dir_dy(d), tx = cx + dir_dx(d);
+      bool stop = d == kNoFlow || d > 8 || (unsigned)ty >= (unsigned)h || (unsigned)tx >= (unsigned)w;
+      // Flow into NoData is dropped (D8).  For f64 the walk may step onto the
+      // NoData cell instead of checking it: NaN + x = NaN, and its code (255)
+      // ends the walk there; integer markers would change, so they check.
+      if (!std::is_same<T, double>::value) stop = stop || s.d[k][ty * WB::BC + tx] == kNoData;
+      if (stop) {
+        k = -1;  // terminal, block exit, or dropped into NoData
+        break;
+      }
       cy = ty;
       cx = tx;
     }
