@@ -98,11 +98,14 @@ __device__ __forceinline__ uint32_t d8_drops(bool cnan, float d1, float d2, floa
   } else if (vc | vd) {
     code = vc ? kc : kd;
   } else {
-    // no downhill data neighbour: the lowest NaN neighbour (outlet, D3), else NoFlow
+    // no downhill data neighbour: the lowest NaN neighbour (outlet, D3), else
+    // NoFlow.  A NoData centre (all drops NaN) always lands here, so its
+    // check costs nothing on the common path.
     code = isnan(d1) ? 1u : isnan(d2) ? 2u : isnan(d3) ? 3u : isnan(d4) ? 4u : isnan(d5) ? 5u
          : isnan(d6) ? 6u : isnan(d7) ? 7u : isnan(d8) ? 8u : (uint32_t)kNoFlow;
+    if (cnan) code = kNoData;
   }
-  return cnan ? (uint32_t)kNoData : code;
+  return code;
 }
 
 // H1, vectorised: each lane owns 4 adjacent columns of a 128-column warp
@@ -124,17 +127,20 @@ __global__ void __launch_bounds__(128) k_d8v(const float* __restrict__ dem, cons
   const bool own = gx < W;
   const float qnan = __int_as_float(0x7fc00000);
   // a row in flight: raw float4 of the lane's columns + the two warp-edge halo values
+  // one halo value per row: lane 0 reads the column left of the strip, lane
+  // 31 the column right of it (staged once, for both)
   struct Raw {
     float4 v;
-    float hl, hr;
+    float h;
   };
+  const bool hl_ok = lane == 0 && x0 > 0, hr_ok = lane == 31 && x0 + 128 < W;
+  const int64_t hx = lane == 0 ? x0 - 1 : x0 + 128;
   auto issue = [&](int64_t gy) {
-    Raw q{make_float4(qnan, qnan, qnan, qnan), qnan, qnan};
+    Raw q{make_float4(qnan, qnan, qnan, qnan), qnan};
     const float* row = dem_row(dem, dem_up, dem_dn, H, W, gy);
     if (row) {
       if (own) q.v = __ldg(reinterpret_cast<const float4*>(row + gx));
-      if (lane == 0 && x0 > 0) q.hl = __ldg(row + x0 - 1);
-      if (lane == 31 && x0 + 128 < W) q.hr = __ldg(row + x0 + 128);
+      if (hl_ok || hr_ok) q.h = __ldg(row + hx);
     }
     return q;
   };
@@ -142,13 +148,14 @@ __global__ void __launch_bounds__(128) k_d8v(const float* __restrict__ dem, cons
     // NoData / non-finite -> NaN (off-grid values are NaN already)
     const float4 v = make_float4(stage_z(q.v.x, nodata), stage_z(q.v.y, nodata), stage_z(q.v.z, nodata),
                                  stage_z(q.v.w, nodata));
+    const float hz = stage_z(q.h, nodata);
     const float l = __shfl_up_sync(kFull, v.w, 1), r = __shfl_down_sync(kFull, v.x, 1);
-    R[0] = lane == 0 ? stage_z(q.hl, nodata) : l;
+    R[0] = lane == 0 ? hz : l;
     R[1] = v.x;
     R[2] = v.y;
     R[3] = v.z;
     R[4] = v.w;
-    R[5] = lane == 31 ? stage_z(q.hr, nodata) : r;
+    R[5] = lane == 31 ? hz : r;
   };
   float P[6], C[6], D[6];
   {
@@ -191,7 +198,7 @@ __global__ void __launch_bounds__(128) k_d8v(const float* __restrict__ dem, cons
       // N, NE, E, SE, S, SW, W, NW
       const uint32_t code = d8_drops(isnan(C[j]), -pv[j], -pt[j + 1], hh[j], sd[j], v[j], t[j], -hh[j - 1],
                                      -ps[j - 1]);
-      packed |= code << (8 * i);
+      packed += code * (1u << (8 * i));  // an FMA-pipe multiply-add, not ALU shifts/ors
     }
     if (own) *reinterpret_cast<uint32_t*>(out + (int64_t)r * W) = packed;
 #pragma unroll

@@ -176,7 +176,10 @@ __device__ __forceinline__ uint8_t d8_code(const float* zs, int i) {
 }
 
 __device__ __forceinline__ float stage_z(float v, float nodata) {
-  return (isfinite(v) && v != nodata) ? v : __int_as_float(0x7fc00000);
+  // v*0 + v is v for finite v and NaN for +-inf and NaN (one FMA-pipe op
+  // instead of a compare and a select on the ALU pipe, which bounds k_d8v)
+  const float f = __fmaf_rn(v, 0.0f, v);
+  return v != nodata ? f : __int_as_float(0x7fc00000);
 }
 
 // ---------------------------------------------------------------- accumulator traits
