@@ -88,15 +88,23 @@ __device__ __forceinline__ uint32_t d8_drops(bool cnan, float d1, float d2, floa
                                              float d7, float d8) {
   const float a = fmaxf(fmaxf(d1, d3), fmaxf(d5, d7));
   const float b = fmaxf(fmaxf(d2, d4), fmaxf(d6, d8));
-  const uint32_t kc = d1 == a ? 1u : d3 == a ? 3u : d5 == a ? 5u : 7u;
-  const uint32_t kd = d2 == b ? 2u : d4 == b ? 4u : d6 == b ? 6u : 8u;
   const bool vc = a > 0.0f, vd = b > 0.0f;
   uint32_t code;
-  if (vc && vd) {
-    const double da = (double)a, db = (double)b;
-    code = __dmul_rn(__dmul_rn(2.0, da), da) > __dmul_rn(db, db) ? kc : kd;
-  } else if (vc | vd) {
-    code = vc ? kc : kd;
+  if (vc | vd) {
+    bool card = vc;
+    if (vc && vd) {
+      const double da = (double)a, db = (double)b;
+      card = __dmul_rn(__dmul_rn(2.0, da), da) > __dmul_rn(db, db);
+    }
+    // only the winning group's code is searched: its first drop equal to the
+    // group maximum (selects instead of a second compare chain; the ALU pipe
+    // bounds this kernel)
+    const float m = card ? a : b;
+    const float e1 = card ? d1 : d2, e3 = card ? d3 : d4, e5 = card ? d5 : d6;
+    uint32_t c = e5 == m ? 5u : 7u;
+    c = e3 == m ? 3u : c;
+    c = e1 == m ? 1u : c;
+    code = c + (card ? 0u : 1u);
   } else {
     // no downhill data neighbour: the lowest NaN neighbour (outlet, D3), else
     // NoFlow.  A NoData centre (all drops NaN) always lands here, so its
