@@ -59,7 +59,7 @@ namespace fa {
 #define FA_REC_STEPS 4
 #endif
 #ifndef FA_P1_MINB
-#define FA_P1_MINB 9
+#define FA_P1_MINB 8
 #endif
 constexpr uint8_t kOut = 254;  // ring cell: outside the block, data
 
