@@ -40,6 +40,9 @@ def _check_f64(got, d, exp, ex):
     assert rel.max() <= 1e-9, rel.max()
     exact = ex[data].astype(np.float64) * 2.0 ** -23
     assert (np.abs(g - exact) / exact).max() <= 1e-9
+    # Σw ≈ 9.7e8 < 2^30: every fp64 partial sum of grid weights is exact (P11),
+    # so the result is the exact sum bit for bit, in any summation order
+    assert (g == exact).all()
 
 
 def test_cfg3_full_single_device(fa_lib, cfg3_full):

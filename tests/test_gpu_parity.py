@@ -197,6 +197,29 @@ def test_acc_dem_weighted_f64_cfg3_recipe(fa_lib, size, tile):
     assert (np.abs(got[data] - ex) / ex).max() <= 1e-9
 
 
+@pytest.mark.parametrize("path", ["single", "strips", "streamed"])
+def test_f64_grid_weights_bit_exact(fa_lib, path):
+    """cfg3's weights lie on the grid 0.5 + k*2^-23 (P11): every partial sum
+    is a multiple of 2^-23 below 2^30 (here Σw ≈ 1e6; cfg3 ≈ 9.7e8), so each
+    fp64 addition is exact in any order and all three paths must equal the
+    oracle's exact fixed-point sum bit for bit -- the D13 tolerance is not
+    needed for this recipe (deterministic fp64)."""
+    cfg = inputs.make_config("cfg3", 1024, 1024)
+    d = oracle.d8(cfg.dem)
+    ex = oracle.accumulate(d, cfg.w, kind="fix23")
+    assert ex.max() < 2 ** 53
+    with fa_lib.Context(0, tile=(256, 256)) as ctx:
+        if path == "single":
+            got = ctx.accumulate(dem=_cuda(cfg.dem), w=_cuda(cfg.w), atype="f64").cpu().numpy()
+        elif path == "strips":
+            got = ctx.accumulate_strips(4, dem=_cuda(cfg.dem), w=_cuda(cfg.w), atype="f64").cpu().numpy()
+        else:
+            got = ctx.accumulate_streamed(dem=cfg.dem, w=cfg.w, atype="f64", strip_rows=256)
+    data = d != 255
+    assert np.isnan(got[~data]).all()
+    assert (got[data] == ex[data].astype(np.float64) * 2.0 ** -23).all()
+
+
 def test_acc_host_buffers(fa_lib):
     d = inputs.random_dirs(21, 300, 200, p_nodata=0.1)
     with fa_lib.Context(0, tile=(64, 100)) as ctx:
