@@ -36,15 +36,40 @@ __global__ void k_count_children(uint32_t n, const uint32_t* __restrict__ parent
   }
 }
 
-// frontier = {v : cnt[v] == 0}; done[v] = 0.  All lanes iterate uniformly.
-__global__ void k_init_frontier(uint32_t n, const uint32_t* __restrict__ cnt, uint8_t* done,
-                                uint32_t* front, uint32_t* fcount) {
+// CTA-aggregated append (every thread of the CTA calls it): one global
+// atomic per CTA instead of one per warp -- the frontier of the first round
+// holds most nodes, and per-warp atomics on one counter serialise in L2
+template <int NT>
+__device__ __forceinline__ void cta_append(bool pred, uint32_t v, uint32_t* list, uint32_t* count,
+                                           uint32_t* s_tmp /* NT/32 + 1 words of shared memory */) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned mask = __ballot_sync(0xFFFFFFFFu, pred);
+  if (lane == 0) s_tmp[w] = (uint32_t)__popc(mask);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t tot = 0;
+    for (int i = 0; i < NT / 32; ++i) {
+      const uint32_t c = s_tmp[i];
+      s_tmp[i] = tot;
+      tot += c;
+    }
+    s_tmp[NT / 32] = tot ? atomicAdd(count, tot) : 0u;
+  }
+  __syncthreads();
+  if (pred) list[s_tmp[NT / 32] + s_tmp[w] + (uint32_t)__popc(mask & ((1u << lane) - 1u))] = v;
+  __syncthreads();  // s_tmp is reused by the next call
+}
+
+// frontier = {v : cnt[v] == 0}; done[v] = 0.  All threads iterate uniformly.
+__global__ void __launch_bounds__(256) k_init_frontier(uint32_t n, const uint32_t* __restrict__ cnt, uint8_t* done,
+                                                       uint32_t* front, uint32_t* fcount) {
+  __shared__ uint32_t s_tmp[256 / 32 + 1];
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
     const uint32_t v = base + threadIdx.x;
     const bool ok = v < n && cnt[v] == 0;
     if (v < n) done[v] = 0;
-    warp_append(ok, v, front, fcount);
+    cta_append<256>(ok, v, front, fcount, s_tmp);
   }
 }
 
