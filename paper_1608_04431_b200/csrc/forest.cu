@@ -166,8 +166,14 @@ __global__ void k_walk(const uint32_t* __restrict__ front, uint32_t nf, const ui
     }
     warp_append(push, pnode, next, ncount);
   }
+  // one global atomic per CTA (the retired count is a single counter)
+  __shared__ uint32_t s_ret;
+  if (threadIdx.x == 0) s_ret = 0u;
+  __syncthreads();
   for (int o = 16; o; o >>= 1) retired += __shfl_xor_sync(0xFFFFFFFFu, retired, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(nretired, retired);
+  if ((threadIdx.x & 31) == 0 && retired) atomicAdd(&s_ret, retired);
+  __syncthreads();
+  if (threadIdx.x == 0 && s_ret) atomicAdd(nretired, s_ret);
 }
 
 __global__ void k_compact_residual(uint32_t n, const uint8_t* __restrict__ done, uint32_t* R,
