@@ -385,6 +385,20 @@ fa_status strip_pass1(fa_ctx* ctx, Strip<T>& s, bool cut) {
   return FA_OK;
 }
 
+// local tile slot bases of a strip (prefix sums of the tiles' perimeter
+// counts), computed on the device so no host buffer has to outlive a copy
+__global__ void k_tile_bases(fa::Geom g, int64_t* base) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  int64_t tot = 0;
+  for (int64_t t = 0; t < g.TR * g.TC; ++t) {
+    int64_t y0, x0, h, w;
+    g.tile_box(t, y0, x0, h, w);
+    base[t] = tot;
+    tot += fa::perim_count(h, w);
+  }
+  base[g.TR * g.TC] = tot;
+}
+
 // phase A tail: A_T at block exits, tile roots, tile perimeter records
 template <class T>
 fa_status strip_records(fa_ctx* ctx, Strip<T>& s, uint32_t* links, uint8_t* fdir, T* tile_acc) {
@@ -392,11 +406,11 @@ fa_status strip_records(fa_ctx* ctx, Strip<T>& s, uint32_t* links, uint8_t* fdir
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
   s.troot = rt.alloc<uint32_t>(s.nn);
-  std::vector<int64_t> hb;
-  s.nslots = tile_perim_total(s.g, &hb);
-  s.dtbase = rt.alloc<int64_t>(hb.size());
+  s.nslots = tile_perim_total(s.g, nullptr);
+  s.dtbase = rt.alloc<int64_t>((size_t)(s.g.TR * s.g.TC + 1));
   if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
-  CK(cudaMemcpyAsync(s.dtbase, hb.data(), hb.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  k_tile_bases<<<1, 32, 0, st>>>(s.g, s.dtbase);
+  ++rt.launches;
   CK(cudaMemcpyAsync(s.S, s.node_val, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
   CK(launch_fold_leaves<T>(st, s.g.nblocks * s.g.pb, s.x_slot, s.slot_root, s.S));  // leaves raked in pass 1
   ++rt.launches;
@@ -405,7 +419,6 @@ fa_status strip_records(fa_ctx* ctx, Strip<T>& s, uint32_t* links, uint8_t* fdir
   CK(launch_tile_records<T>(st, s.g, s.nslots, s.dtbase, s.dirs_in(), s.slot_root, s.troot, s.node_flags,
                             s.node_slot, s.S, links + s.slot0, fdir + s.slot0, tile_acc + s.slot0));
   ++rt.launches;
-  CK(cudaStreamSynchronize(st));  // hb must outlive the async copy
   return FA_OK;
 }
 
@@ -857,14 +870,13 @@ fa_status run_streamed(fa_ctx* ctx, int64_t H, int64_t W, const float* dem_h, fl
     make_strip(i, b, s);
     r = strip_pass1<T, WK>(ctx, s, true);
     if (r == FA_OK) {
-      std::vector<int64_t> hb;
-      s.nslots = tile_perim_total(s.g, &hb);
-      s.dtbase = rt.alloc<int64_t>(hb.size());
+      s.nslots = tile_perim_total(s.g, nullptr);
+      s.dtbase = rt.alloc<int64_t>((size_t)(s.g.TR * s.g.TC + 1));
       if (rt.err) r = set_err(ctx, FA_E_NOMEM, "device allocation failed");
       else {
-        CK(cudaMemcpyAsync(s.dtbase, hb.data(), hb.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        k_tile_bases<<<1, 32, 0, st>>>(s.g, s.dtbase);
+        ++rt.launches;
         r = strip_finish<T, WK>(ctx, s, xT);
-        CK(cudaStreamSynchronize(st));  // hb must outlive the async copy
       }
     }
     s.release(rt);

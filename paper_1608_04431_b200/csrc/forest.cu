@@ -133,9 +133,10 @@ __global__ void k_peel_dev(const uint32_t* __restrict__ front, const uint32_t* _
 // the wide rounds of level-synchronous peeling; a walk stops after `cap`
 // steps and re-queues the ready node, leaving deep chains to contraction.
 template <class T>
-__global__ void k_walk(const uint32_t* __restrict__ front, uint32_t nf, const uint32_t* __restrict__ parent,
-                       T* val, uint32_t* cnt, uint8_t* done, uint32_t* next, uint32_t* ncount,
-                       uint32_t* nretired, int cap) {
+__global__ void k_walk(const uint32_t* __restrict__ front, const uint32_t* __restrict__ nf_dev,
+                       const uint32_t* __restrict__ parent, T* val, uint32_t* cnt, uint8_t* done, uint32_t* next,
+                       uint32_t* ncount, uint32_t* nretired, int cap) {
+  const uint32_t nf = *nf_dev;  // frontier size read on the device: no host round trip before the launch
   const uint32_t stride = gridDim.x * blockDim.x;
   uint32_t retired = 0;
   for (uint32_t base = blockIdx.x * blockDim.x; base < nf; base += stride) {
@@ -333,16 +334,19 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
   ++rt.launches;
   k_init_frontier<<<grid_for(n), 256, 0, st>>>(n, cnt, done, fa_, ctr);
   ++rt.launches;
-  rt.read(ctr, 1);
-  uint32_t nf = rt.h_cnt[0];
+  uint32_t nf = 1;  // the frontier size stays on the device until after the walks
   uint64_t remaining = n;
   bool contracted = false;
   uint32_t* pc = nullptr;  // device frontier counters of the batched peel rounds
   const int cap = env_int("FA_WALKCAP", kWalkCap);  // tuning override (read per call)
-  if (nf > 0 && cap > 0) {
-    // bulk of the forest: one launch of capped walks from every leaf
+  if (cap <= 0) {
+    rt.read(ctr, 1);
+    nf = rt.h_cnt[0];
+  } else {
+    // bulk of the forest: one launch of capped walks from every leaf (a
+    // grid for all n nodes; the walks read the frontier size themselves)
     cudaMemsetAsync(ctr + 1, 0, 2 * sizeof(uint32_t), st);
-    k_walk<T><<<grid_for(nf), 256, 0, st>>>(fa_, nf, parent, val, cnt, done, fb, ctr + 1, ctr + 2, cap);
+    k_walk<T><<<grid_for(n), 256, 0, st>>>(fa_, ctr, parent, val, cnt, done, fb, ctr + 1, ctr + 2, cap);
     ++rt.launches;
     ++rt.peel_rounds;
     std::swap(fa_, fb);
@@ -380,18 +384,19 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
       k_jump_init<T><<<grid_for(m), 256, 0, st>>>(m, lpc, up, lval, nxa, aca);
       ++rt.launches;
       int rounds = 0;
-      for (;;) {
+      for (int batch = 8;; batch = 4) {
         // pointer jumping converges in ceil(log2(longest chain)) rounds; the
-        // "changed" flag is read back every 4 rounds (extra rounds are no-ops)
+        // "changed" flag is read back after 8 rounds, then every 4 (extra
+        // rounds are no-ops)
         cudaMemsetAsync(ctr + 2, 0, sizeof(uint32_t), st);
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < batch; ++j) {
           k_jump<T><<<grid_for(m), 256, 0, st>>>(m, lpc, nxa, aca, nxb, acb, ctr + 2);
           std::swap(nxa, nxb);
           std::swap(aca, acb);
         }
-        rt.launches += 4;
-        rounds += 4;
-        rt.jump_rounds += 4;
+        rt.launches += batch;
+        rounds += batch;
+        rt.jump_rounds += batch;
         rt.read(ctr + 2, 1);
         if (!rt.h_cnt[0] || rt.err) break;
         if (rounds > kMaxJump) {
@@ -500,14 +505,16 @@ cudaError_t forest_roots(Runtime& rt, uint32_t n, const uint32_t* parent, uint32
   uint32_t* a = root;
   uint32_t* b = tmp;
   int rounds = 0;
-  for (;;) {
+  for (int batch = 8;; batch = 4) {
+    // converged rounds are no-ops: 8 rounds (depth 256) before the first
+    // host check, then a check every 4
     cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st);
-    for (int j = 0; j < 4; ++j) {  // converged rounds are no-ops: check every 4
+    for (int j = 0; j < batch; ++j) {
       k_root_jump<<<grid_for(n), 256, 0, st>>>(n, a, b, ctr);
       std::swap(a, b);
     }
-    rt.launches += 4;
-    rounds += 4;
+    rt.launches += batch;
+    rounds += batch;
     rt.read(ctr, 1);
     if (!rt.h_cnt[0] || rt.err) break;
     if (rounds > kMaxJump) {
