@@ -129,15 +129,15 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg, _ = make_inputs()
-    sample_rows = 1024
+    cfg, _ = make_inputs(args.rows)
+    sample_rows = min(1024, cfg.rows)
     for _ in range(args.warmup):
         cpu_sample(cfg, sample_rows)
     vals = [cpu_sample(cfg, sample_rows) for _ in range(args.steps)]
     v = float(np.median([x["value"] for x in vals]))
     cb = dict(vals[0])
     cb["value"] = v
-    ms = 1024 * cfg.cols / (v * 1e9) * 1e3
+    ms = sample_rows * cfg.cols / (v * 1e9) * 1e3
     world = int(os.environ.get("WORLD_SIZE", "1"))
     line = {"metric": METRIC, "value": v, "unit": "Gcells/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
