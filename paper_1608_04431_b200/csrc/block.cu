@@ -361,6 +361,40 @@ __device__ __forceinline__ void load_dirs(WSmem<T, R, Z>& s, const uint8_t* dirs
     }
   }
   if (check && bad) atomicOr(status, ST_BADCODE);
+  // ring codes -> dirh (data ring cells 254, NoData / off-grid 255); entries
+  // count their outside donors
+  auto ring_cell = [&](int ly, int lx, int code) {
+    s.dirh[WB::hidx(ly, lx)] = code == kNoData ? kNoData : kOut;
+    if (entries && code >= 1 && code <= 8) {
+      const int ty = ly + dir_dy(code), tx = lx + dir_dx(code);
+      if ((unsigned)ty < (unsigned)h && (unsigned)tx < (unsigned)w) need_inc(s.need, bperim_index(tx, ty, h, w));
+    }
+  };
+  if (WB::BR == 32 && w == WB::BC && h == WB::BR) {
+    // full block: the top and bottom ring rows are one coalesced byte per
+    // lane, the side columns one byte per lane and row, corners on lanes 0-3
+    const int64_t gu = y0 - 1, gd = y0 + h;
+    const uint8_t* ru = gu < 0 ? dirs_up : gu >= g.H ? dirs_dn : dirs + gu * g.W;
+    const uint8_t* rd = gd < 0 ? dirs_up : gd >= g.H ? dirs_dn : dirs + gd * g.W;
+    const bool lok = x0 > 0, rok = x0 + WB::BC < g.W;
+    const int cu = ru ? ru[x0 + lane] : kNoData, cd = rd ? rd[x0 + lane] : kNoData;
+    const uint8_t* rl = dirs + (y0 + lane) * g.W;
+    const int cl = lok ? rl[x0 - 1] : kNoData, cr = rok ? rl[x0 + WB::BC] : kNoData;
+    int cc = kNoData, cy = -1, cx = -1;  // corners
+    if (lane < 4) {
+      cy = (lane & 1) ? h : -1;
+      cx = (lane & 2) ? WB::BC : -1;
+      const uint8_t* rc = (lane & 1) ? rd : ru;
+      const bool ok = (lane & 2) ? rok : lok;
+      if (rc && ok) cc = rc[x0 + cx];
+    }
+    ring_cell(-1, lane, cu);
+    ring_cell(h, lane, cd);
+    ring_cell(lane, -1, cl);
+    ring_cell(lane, WB::BC, cr);
+    if (lane < 4) ring_cell(cy, cx, cc);
+    return;
+  }
   const int rn = 2 * (w + 2) + 2 * h;
   for (int i = lane; i < rn; i += 32) {
     int ly, lx;
