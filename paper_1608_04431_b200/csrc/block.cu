@@ -15,7 +15,10 @@
 //     from the directions with w + x at the block perimeter cells (x =
 //     external inbound flow, D11/D12), write A.
 //
-// Lane layout.  Lane l owns column l of the block: the D8 stencil runs down
+// By default H1 runs first as its own kernel (d8.cu, k_d8v) and pass 1 reads
+// the codes (FROM_DEM = false); FA_FUSED=1 keeps D8 inside pass 1:
+//
+// Lane layout (fused D8).  Lane l owns column l of the block: the D8 stencil runs down
 // the column with a rolling 3x3 register window (3 shared loads per cell
 // instead of 9), writing the code and the cell's successor word.  The 2-cell
 // halo lets the warp also evaluate D8 on the ring of cells around the block,
@@ -32,7 +35,7 @@
 // in place in acc (global memory; the block's rows stay in L2 while the warp
 // works on them), with native global atomics for the pushes.  Shared memory
 // holds only the 1-byte codes, successor words, pending counts and the
-// queue (~7 KB per warp), so many blocks are in flight per SM to hide the
+// queue (~6 KB per warp), so many blocks are in flight per SM to hide the
 // L2 latency.  This is RETAIN: acc ends pass 1 holding A_blk.
 //
 // H3 scheduling: Alg. 1's queue, level-free.  The warp keeps
