@@ -737,8 +737,10 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
   uint32_t* slot_nid = s.slot_nid();  // the queue is dead after the queue loop
   uint32_t* nchild = slot_nid + 128;   // per exit slot: outside donors of the entries draining to it
   for (int i = lane; i < 128; i += 32) nchild[i] = 0u;
-  int64_t t0y, t0x, th, tw;
-  g.tile_box(g.tile_of_block(b), t0y, t0x, th, tw);
+  // the block's tile: only tile-records mode (cut) uses tile edges and the
+  // out-of-tile flag (two integer divisions saved per block otherwise)
+  int64_t t0y = 0, t0x = 0, th = 0, tw = 0;
+  if (P.cut) g.tile_box(g.tile_of_block(b), t0y, t0x, th, tw);
   int cell[NJ];
   bool ex[NJ], want[NJ], tedge[NJ];
 #pragma unroll
@@ -839,7 +841,7 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
       const bool dead = s.dirh[WB::hidx(tyv[j], txv[j])] == kNoData;
       const int64_t gy = y0 + tyv[j], gx = x0 + txv[j];
       flg[j] = dead ? NF_DEAD : 0;
-      if (gy < t0y || gx < t0x || gy >= t0y + th || gx >= t0x + tw) flg[j] |= NF_OUT_TILE;
+      if (P.cut && (gy < t0y || gx < t0x || gy >= t0y + th || gx >= t0x + tw)) flg[j] |= NF_OUT_TILE;
     }
     node[j] = ex[j] && (nchild[p2] != 0u || (P.cut && ((flg[j] & NF_OUT_TILE) || tedge[j])));
     nex += __popc(__ballot_sync(kFull, node[j]));
