@@ -62,6 +62,8 @@ def _L():
             "or_acc_region_f64": ([_P, _I, _I, _I, _I, _I, _I, _P, _P], ctypes.c_int),
             "or_acc_region_fix": ([_P, _I, _I, _I, _I, _I, _I, _P, ctypes.c_int, _P], ctypes.c_int),
             "or_brute_u64": ([_P, _I, _I, _P, _P], ctypes.c_int),
+            "or_acc_alpha_f64": ([_P, _I, _I, _P, _P, _P], ctypes.c_int),
+            "or_brute_alpha_f64": ([_P, _I, _I, _P, _P, _P], ctypes.c_int),
             "or_perim_count": ([_I, _I], _I),
             "or_perim_xy": ([_I, _I, _I, _P, _P], ctypes.c_int),
             "or_perim_index": ([_I, _I, _I, _I], _I),
@@ -148,6 +150,21 @@ def brute(dirs: np.ndarray, w: np.ndarray | None = None) -> np.ndarray:
     H, W = dirs.shape
     A = np.zeros((H, W), np.uint64)
     _chk(_L().or_brute_u64(_p(dirs), H, W, _p(_w_u32(w)), _p(A)), "or_brute")
+    return A
+
+
+def accumulate_alpha(dirs: np.ndarray, alpha: np.ndarray, w: np.ndarray | None = None,
+                     brute_force: bool = False) -> np.ndarray:
+    """O-ACC with absorption (Eq. 1 with a per-cell alpha in [0,1]):
+    A(p) = w(p) + sum_{target(n)=p} alpha(n) A(n); fp64; NoData -> NaN.
+    brute_force=True: the independent path-walk form (small rasters)."""
+    dirs = np.ascontiguousarray(dirs, np.uint8)
+    H, W = dirs.shape
+    al = np.ascontiguousarray(alpha, np.float32)
+    wf = None if w is None else np.ascontiguousarray(w, np.float32)
+    A = np.zeros((H, W), np.float64)
+    fn = _L().or_brute_alpha_f64 if brute_force else _L().or_acc_alpha_f64
+    _chk(fn(_p(dirs), H, W, _p(wf), _p(al), _p(A)), "or_acc_alpha")
     return A
 
 

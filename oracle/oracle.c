@@ -212,6 +212,79 @@ int or_acc_region_fix(const uint8_t* dirs, int64_t H, int64_t W, int64_t y0, int
   OR_ACC_BODY(int64_t, (int64_t)((double)wt[i] * scale), INT64_MIN)
 }
 
+/* ======================================================================
+ * O-ACC with absorption: Eq. 1 with a per-cell
+ * fraction alpha(n) in [0,1] of A(n) passed on to its single (non-divergent)
+ * target, "flow may be absorbed during its downhill movement ... so alpha is
+ * constrained such that sum_p alpha(n,p) <= 1", "most forms of
+ * absorption represent a simple extension":
+ *   A(p) = w(p) + sum_{n : target(n) = p} alpha(n) A(n)
+ * Same Kahn schedule as O-ACC; only the push is scaled.  Returns 1 if an
+ * alpha of a data cell is not a finite value in [0,1].
+ * ==================================================================== */
+int or_acc_alpha_f64(const uint8_t* dirs, int64_t H, int64_t W, const float* wt, const float* alpha,
+                     double* A) {
+  const int64_t y0 = 0, x0 = 0, h = H, w = W;
+  for (int64_t i = 0; i < H * W; ++i)
+    if (dirs[i] != OR_NODATA && !(alpha[i] >= 0.0f && alpha[i] <= 1.0f)) return 1;
+  const int64_t N = h * w;
+  for (int64_t i = 0; i < N; ++i)
+    if (dirs[i] > 8 && dirs[i] != OR_NODATA) return 2;
+  uint8_t* D = (uint8_t*)calloc((size_t)N, 1);
+  if (!D) return 5;
+  int64_t ndata = 0;
+  for (int64_t yy = y0; yy < y0 + h; ++yy)
+    for (int64_t xx = x0; xx < x0 + w; ++xx) {
+      int64_t i = yy * W + xx;
+      if (dirs[i] == OR_NODATA) continue;
+      ++ndata;
+      int64_t t = o_target(dirs, W, xx, yy, y0, x0, h, w);
+      if (t >= 0) D[t]++;
+    }
+  for (int64_t i = 0; i < N; ++i) A[i] = dirs[i] == OR_NODATA ? NAN : (wt ? (double)wt[i] : 1.0);
+  int64_t retired = 0;
+  for (int64_t q = 0; q < N; ++q) {
+    if (dirs[q] == OR_NODATA || D[q] != 0) continue;
+    int64_t c = q;
+    for (;;) {
+      D[c] = 255;
+      ++retired;
+      int64_t t = o_target(dirs, W, c % W, c / W, y0, x0, h, w);
+      if (t < 0) break;
+      A[t] += (double)alpha[c] * A[c];
+      if (--D[t] > 0) break;
+      c = t;
+    }
+  }
+  free(D);
+  return retired == ndata ? 0 : 3;
+}
+
+/* O-BRUTE with absorption: Eq. 1 unrolled -- every data cell q sends w(q)
+ * down its path, scaled by alpha of every cell it leaves:
+ *   A(p) = sum_{q upstream of p (or p)} w(q) prod_{u on q..p, u != p} alpha(u).
+ * Independent of Kahn; small rasters only. */
+int or_brute_alpha_f64(const uint8_t* dirs, int64_t H, int64_t W, const float* wt, const float* alpha,
+                       double* A) {
+  const int64_t N = H * W;
+  for (int64_t i = 0; i < N; ++i) {
+    if (dirs[i] > 8 && dirs[i] != OR_NODATA) return 2;
+    A[i] = dirs[i] == OR_NODATA ? NAN : 0.0;
+  }
+  for (int64_t q = 0; q < N; ++q) {
+    if (dirs[q] == OR_NODATA) continue;
+    double v = wt ? (double)wt[q] : 1.0;
+    int64_t c = q, steps = 0;
+    while (c >= 0) {
+      A[c] += v;
+      if (++steps > N) return 3;
+      v *= (double)alpha[c];
+      c = o_target(dirs, W, c % W, c / W, 0, 0, H, W);
+    }
+  }
+  return 0;
+}
+
 int or_acc_u64(const uint8_t* dirs, int64_t H, int64_t W, const uint32_t* wt, uint64_t* A) {
   return or_acc_region_u64(dirs, H, W, 0, 0, H, W, wt, A);
 }
