@@ -101,6 +101,22 @@ FA_API fa_status fa_accumulate_strips(fa_ctx* ctx, int nstrips, int64_t rows, in
                                       const float* dem, float nodata, const uint8_t* dirs,
                                       const void* w, fa_wtype wtype, void* acc, fa_atype atype);
 
+/* Absorption (Eq. 1 with a per-cell alpha: "flow may
+ * be absorbed during its downhill movement ... alpha is constrained such
+ * that sum_p alpha(n,p) <= 1"; "most forms of absorption represent a simple
+ * extension of the algorithm"):
+ *   A(p) = w(p) + sum_{n : target(n) = p} alpha(n) A(n)
+ * alpha: f32 rows x cols (same layout as the raster), the fraction of a
+ * cell's accumulation passed to its D8 target; data cells need a finite
+ * value in [0, 1] (else FA_E_ARG); NoData cells' alpha is ignored.  Output
+ * f64 (NoData = quiet NaN); wtype FA_W_NONE (w = 1) or FA_W_F32.  Device or
+ * host buffers.  Single device, 32x32 blocks (the default tiling); the
+ * block-exit graph is solved with multiplicative edges by last-arrival walks
+ * without contraction, so a very deep single chain is walked serially. */
+FA_API fa_status fa_accumulate_absorb(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem,
+                                      float nodata, const uint8_t* dirs, const void* w,
+                                      fa_wtype wtype, const float* alpha, double* acc);
+
 /* Out-of-core accumulation (the paper's EVICT strategy, P:L79-81,
  * P:L255): dem / dirs / w / acc are HOST buffers (pinned memory
  * gives full-speed copies; pageable works) and the raster may exceed device

@@ -44,6 +44,16 @@ cudaError_t launch_d8(const float* dem, const float* dem_up, const float* dem_dn
                       cudaStream_t st);
 cudaError_t launch_g1_parent(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
                              const uint32_t* slot_root, bool cut, uint32_t* parent);
+// absorption: block.cu / graph.cu
+cudaError_t launch_pass1_absorb(const PassArgs<double, 0>* a0, const PassArgs<double, 2>* a2, bool from_dem,
+                                cudaStream_t st);
+cudaError_t launch_retain_absorb(const Geom& g, const double* x_slot, const uint8_t* dirs, double* acc,
+                                 const float* alpha, cudaStream_t st);
+cudaError_t launch_absorb_graph(cudaStream_t st, uint32_t nn, int64_t nslots, const float* node_alpha,
+                                const uint32_t* tgt, const double* slot_f, const double* x_slot,
+                                const uint32_t* slot_root, double* wv, double* S);
+cudaError_t launch_scatter_x_absorb(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const float* node_alpha,
+                                    const double* S, double* x_slot);
 template <class T>
 cudaError_t launch_scatter_x(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
                              const T* S, T* x_slot, bool intra_tile);
@@ -255,6 +265,9 @@ struct Strip {
   // device state
   T* acc_tmp = nullptr;   // in-place accumulation buffer when the caller wants no raster
   uint8_t* halo_dirs = nullptr;  // D8 codes of rows -1 and H (split path, strips)
+  const float* alpha = nullptr;  // absorption (N3): per-cell alpha, or null
+  T* slot_f = nullptr;           // absorption: alpha product along each entry slot's path
+  float* node_alpha = nullptr;   // absorption: alpha at each node's exit cell
   uint8_t* dirs_buf = nullptr;
   uint32_t* slot_root = nullptr;
   T* node_val = nullptr;
@@ -271,11 +284,13 @@ struct Strip {
   void release(fa::Runtime& rt) {
     for (void* p : {(void*)dirs_buf, (void*)slot_root, (void*)node_val, (void*)node_slot, (void*)node_tgt,
                     (void*)node_flags, (void*)x_slot, (void*)parent, (void*)S, (void*)troot, (void*)dtbase,
-                    (void*)acc_tmp, (void*)halo_dirs})
+                    (void*)acc_tmp, (void*)halo_dirs, (void*)slot_f, (void*)node_alpha})
       rt.free(p);
     dirs_buf = nullptr;
     acc_tmp = nullptr;
     halo_dirs = nullptr;
+    slot_f = nullptr;
+    node_alpha = nullptr;
     slot_root = node_slot = node_tgt = parent = troot = nullptr;
     node_val = x_slot = S = nullptr;
     node_flags = nullptr;
@@ -316,6 +331,7 @@ fa_status check_status(fa_ctx* ctx, uint32_t stat, unsigned long long wsum, bool
   using namespace fa;
   if (stat & ST_BADCODE) return set_err(ctx, FA_E_DIRCODE, "direction raster holds a byte outside {0..8,255}");
   if (stat & ST_BADWEIGHT) return set_err(ctx, FA_E_ARG, "f32 weights must be finite and >= 0");
+  if (stat & ST_BADALPHA) return set_err(ctx, FA_E_ARG, "alpha must be a finite value in [0, 1] at data cells");
   if (is_u32 && wsum >= 0xFFFFFFFFull)
     return set_err(ctx, FA_E_OVERFLOW, "sum of weights reaches the u32 range (NoData marker); use u64");
   if (stat & ST_CYCLE) return set_err(ctx, FA_E_CYCLE, "direction graph has a cycle (some cells never retire)");
@@ -372,7 +388,22 @@ fa_status strip_pass1(fa_ctx* ctx, Strip<T>& s, bool cut) {
     pa.dirs_dn = s.dem_dn ? s.halo_dirs + g.W : nullptr;
   }
   CK(cudaEventRecord(ctx->ev[5], st));
-  CK(launch_pass1<T, WK>(pa, s.dem != nullptr && !split, st));
+  if (s.alpha) {
+    if constexpr (std::is_same<T, double>::value && (WK == 0 || WK == 2)) {
+      s.slot_f = rt.alloc<T>(slots);
+      s.node_alpha = rt.alloc<float>(slots);
+      if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+      pa.alpha = s.alpha;
+      pa.slot_f = s.slot_f;
+      pa.node_alpha = s.node_alpha;
+      if constexpr (WK == 0) CK(launch_pass1_absorb(&pa, nullptr, s.dem != nullptr && !split, st));
+      else CK(launch_pass1_absorb(nullptr, &pa, s.dem != nullptr && !split, st));
+    } else {
+      return set_err(ctx, FA_E_ARG, "absorption needs f64 output and f32 or no weights");
+    }
+  } else {
+    CK(launch_pass1<T, WK>(pa, s.dem != nullptr && !split, st));
+  }
   CK(cudaEventRecord(ctx->ev[6], st));
   ++rt.launches;
   CK(rt.read(ctx->d_small, 4));
@@ -707,6 +738,61 @@ fa_status accumulate_impl(fa_ctx* ctx, int64_t rows, int64_t cols, const float* 
   cudaError_t e = cudaStreamSynchronize(st);
   if (s == FA_OK && e != cudaSuccess) return set_err(ctx, FA_E_CUDA, std::string("stream: ") + cudaGetErrorString(e));
   return s;
+}
+
+// ---------------------------------------------------------------- absorption (N3)
+// Eq. 1 with a per-cell alpha in [0,1] ("most forms of absorption
+// represent a simple extension"), on one device with 32x32 blocks:
+// pass 1 scales every push by alpha of the pushing cell and records, per
+// entry slot, the product f of alpha along its in-block path before the exit;
+// the block-exit graph becomes a forest with multiplicative edges
+// (alpha(exit) f(target entry)); the finalize scales the carried offset by
+// alpha of every cell it leaves.  Linear in w, so the tiling stays exact.
+template <int WK>
+fa_status run_absorb(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nodata, const uint8_t* dirs,
+                     const void* w, const float* alpha, double* acc) {
+  using namespace fa;
+  using T = double;
+  cudaStream_t st = ctx->st;
+  Runtime& rt = ctx->rt;
+  reset_run(ctx);
+  CK(cudaMemsetAsync(ctx->d_small, 0, 16 * sizeof(uint32_t), st));
+  CK(cudaEventRecord(ctx->ev[0], st));
+  Strip<T> s;
+  s.g = make_geom(H, W, ctx->tile_r, ctx->tile_c);
+  if (s.g.br != 32 || s.g.bc != 32) return set_err(ctx, FA_E_ARG, "absorption runs with 32x32 blocks");
+  s.dem = dem;
+  s.dirs = dirs;
+  s.w = w;
+  s.acc = acc;
+  s.nodata = nodata;
+  s.alpha = alpha;
+  fa_status r = strip_pass1<T, WK>(ctx, s, false);
+  if (r != FA_OK) { s.release(rt); return r; }
+  CK(cudaEventRecord(ctx->ev[1], st));
+  r = check_status(ctx, rt.h_cnt[1] & ~ST_CYCLE, 0, false);
+  if (r != FA_OK) { s.release(rt); cudaStreamSynchronize(st); return r; }
+  const int64_t slots = s.g.nblocks * s.g.pb;
+  double* wv = rt.alloc<double>(s.nn ? s.nn : 1);
+  if (rt.err) { s.release(rt); return set_err(ctx, FA_E_NOMEM, "device allocation failed"); }
+  CK(cudaMemcpyAsync(s.S, s.node_val, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  CK(launch_absorb_graph(st, s.nn, slots, s.node_alpha, s.node_tgt, s.slot_f, s.x_slot, s.slot_root, wv, s.S));
+  rt.launches += 2;
+  CK(forest_solve_weighted(rt, s.nn, s.parent, wv, s.S));
+  CK(launch_scatter_x_absorb(st, s.nn, s.node_tgt, s.node_alpha, s.S, s.x_slot));
+  ++rt.launches;
+  CK(cudaEventRecord(ctx->ev[2], st));
+  CK(launch_retain_absorb(s.g, s.x_slot, s.dirs_in(), acc, alpha, st));
+  ++rt.launches;
+  CK(cudaEventRecord(ctx->ev[3], st));
+  rt.free(wv);
+  s.release(rt);
+  if (rt.err) return set_err(ctx, FA_E_CUDA, cudaGetErrorString(rt.err));
+  CK(rt.read(ctx->d_small + 1, 1));
+  r = check_status(ctx, rt.h_cnt[0], 0, false);
+  if (r != FA_OK) return r;
+  record_stats(ctx, H * W, s.g.nblocks, s.nn, 0);
+  return FA_OK;
 }
 
 // ---------------------------------------------------------------- out-of-core (N2)
@@ -1134,6 +1220,38 @@ fa_status fa_accumulate_strips(fa_ctx* ctx, int nstrips, int64_t rows, int64_t c
   if (!acc) return set_err(ctx, FA_E_ARG, "acc is NULL");
   if (nstrips < 1) return set_err(ctx, FA_E_ARG, "nstrips must be >= 1");
   return accumulate_impl(ctx, rows, cols, dem, nodata, dirs, w, wtype, acc, atype, rec, nstrips);
+}
+
+fa_status fa_accumulate_absorb(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem, float nodata,
+                               const uint8_t* dirs, const void* w, fa_wtype wtype, const float* alpha,
+                               double* acc) {
+  if (!ctx) return FA_E_ARG;
+  ctx->err.clear();
+  if (rows <= 0 || cols <= 0) return set_err(ctx, FA_E_ARG, "rows and cols must be > 0");
+  if (!acc || !alpha) return set_err(ctx, FA_E_ARG, "acc and alpha must be given");
+  if (wtype == FA_W_U32) return set_err(ctx, FA_E_ARG, "absorption takes f32 weights or none (f64 output)");
+  FS(check_types(ctx, dem, dirs, w, wtype, FA_A_F64));
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->st;
+  const size_t n = (size_t)rows * (size_t)cols;
+  Staged sdem, sdirs, sw, sal, sacc;
+  CK(stage_in(st, dem, n * 4, sdem));
+  CK(stage_in(st, dirs, n, sdirs));
+  CK(stage_in(st, wtype == FA_W_NONE ? nullptr : w, n * 4, sw));
+  CK(stage_in(st, alpha, n * 4, sal));
+  CK(stage_out_alloc(st, acc, n * 8, sacc));
+  const float* d_dem = (const float*)sdem.dev;
+  const uint8_t* d_dirs = (const uint8_t*)sdirs.dev;
+  const float* d_al = (const float*)sal.dev;
+  fa_status s = wtype == FA_W_NONE
+                    ? run_absorb<0>(ctx, rows, cols, d_dem, nodata, d_dirs, nullptr, d_al, (double*)sacc.dev)
+                    : run_absorb<2>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, d_al, (double*)sacc.dev);
+  if (s == FA_OK && sacc.owned) CK(cudaMemcpyAsync(acc, sacc.dev, n * 8, cudaMemcpyDeviceToHost, st));
+  for (Staged* p : {&sdem, &sdirs, &sw, &sal, &sacc})
+    if (p->owned) cudaFreeAsync(p->dev, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (s == FA_OK && e != cudaSuccess) return set_err(ctx, FA_E_CUDA, std::string("stream: ") + cudaGetErrorString(e));
+  return s;
 }
 
 fa_status fa_accumulate_streamed(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem, float nodata,

@@ -590,8 +590,9 @@ __device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc, in
 template <class T>
 __device__ __forceinline__ void g_add(T* p, T v) { atomicAdd(p, v); }
 
-template <class T, int R, bool Z>
-__device__ __forceinline__ uint32_t kahn_block(WSmem<T, R, Z>& s, uint32_t nsrc, T* Ab, int64_t W) {
+template <class T, int R, bool Z, bool ABS = false>
+__device__ __forceinline__ uint32_t kahn_block(WSmem<T, R, Z>& s, uint32_t nsrc, T* Ab, int64_t W,
+                                               const float* Alb = nullptr) {
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   uint16_t* Q = s.src;
@@ -611,7 +612,8 @@ __device__ __forceinline__ uint32_t kahn_block(WSmem<T, R, Z>& s, uint32_t nsrc,
         // "A(n) <- A(n) + A(c)" and "decrement D(n)" (Alg. 1);
         // A(c) is final: every donor of c was popped in an earlier iteration
         t = su & SU_T;
-        const T a = __ldcg(Ab + (c + (c >> 5) * wm));
+        T a = __ldcg(Ab + (c + (c >> 5) * wm));
+        if constexpr (ABS) a *= (T)__ldg(Alb + (c + (c >> 5) * wm));  // "alpha(n) A(n)"
         g_add(Ab + (t + (t >> 5) * wm), a);
         const uint32_t sh = (t & 7u) * 4u;
         const uint32_t old = atomicAdd(&s.pend[t >> 3], 0u - (1u << sh));
@@ -724,7 +726,7 @@ __device__ __forceinline__ void write_dirs(const WSmem<T, R, Z>& s, uint8_t* dir
 // entry's external inbound flow, D11).  Other exits become nodes (compacted,
 // one global atomic per warp).  slot_root[entry] = node of its exit.  Lane l
 // handles slots l, l+32, l+64, l+96.
-template <class T, int R, bool Z, int WK>
+template <class T, int R, bool Z, int WK, bool ABS = false>
 __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<T, WK>& P, int64_t b, int64_t y0,
                                               int64_t x0, int h, int w) {
   using WB = WBT<R>;
@@ -733,6 +735,10 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
   const Geom& g = P.g;
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
+  // absorption: alpha of block cell c (same row-major layout as acc)
+  const float* Alb = ABS ? P.alpha + y0 * g.W + x0 : nullptr;
+  const uint32_t wmA = (uint32_t)g.W - 32u;
+  auto alpha_of = [&](int c) -> T { return (T)__ldg(Alb + ((uint32_t)c + ((uint32_t)c >> 5) * wmA)); };
   const int np = bperim_count(h, w);
   uint32_t* slot_nid = s.slot_nid();  // the queue is dead after the queue loop
   uint32_t* nchild = slot_nid + 128;   // per exit slot: outside donors of the entries draining to it
@@ -760,6 +766,8 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
       }
       want[j] = data && !ex[j] && (s.need[p] != 0u || tedge[j]);
     }
+    // path products start at 1 (exits that are entries keep it: no cell before the exit)
+    if (ABS && p < WB::PB) P.slot_f[b * WB::PB + p] = (T)1;
   }
   __syncwarp();
   // exits that are entries themselves count their own outside donors
@@ -778,6 +786,7 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
   int head = 0;
   int p = -1, c = 0;
   uint32_t su = SU_STOP;
+  T f = (T)1;  // absorption: product of alpha along the walked path so far
   for (;;) {
     const unsigned idle = __ballot_sync(kFull, p < 0);
     if (idle == kFull && head >= nwalk) break;
@@ -796,11 +805,13 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
         bperim_xy(p, h, w, px, py);
         c = py * WB::BC + px;
         su = s.succ[c];
+        f = (T)1;
       }
     }
     head += __popc(idle);
     if (p < 0) continue;
     if (su & SU_STOP) {
+      if (ABS) P.slot_f[b * WB::PB + p] = f;  // the entry's offset reaches its exit scaled by f
       uint32_t rp = kNoP;
       if (su & SU_EXIT) {
         rp = (uint32_t)bperim_index(c & 31, c >> 5, h, w);
@@ -812,11 +823,13 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
       p = -1;
       continue;
     }
+    if (ABS) f *= alpha_of(c);
     c = (int)(su & SU_T);
     su = s.succ[c];
 #pragma unroll
     for (int u = 1; u < FA_REC_STEPS; ++u) {  // more steps per refill round
       if (su & SU_STOP) break;
+      if (ABS) f *= alpha_of(c);
       c = (int)(su & SU_T);
       su = s.succ[c];
     }
@@ -883,12 +896,14 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
       const T a = __ldcg(P.acc + (y0 + py) * g.W + x0 + px);
       if (node[j]) {
         nid = base + (uint32_t)__popc(em & lt);
+        if (ABS) P.node_alpha[nid] = (float)alpha_of(cell[j]);
         P.node_val[nid] = a;
         P.node_slot[nid] = (uint32_t)(b * WB::PB + p2);
         P.node_tgt[nid] = tgt;
         P.node_flags[nid] = fl;
       } else if (tgt != kNone) {
-        atomic_add(&P.x_slot[tgt], a);  // a leaf: S(e) = A_B(e), nothing flows in from upstream blocks
+        // a leaf: S(e) = A_B(e), nothing flows in from upstream blocks
+        atomic_add(&P.x_slot[tgt], ABS ? a * alpha_of(cell[j]) : a);
       }
     }
     if (p2 < WB::PB) slot_nid[p2] = nid;
@@ -907,7 +922,7 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
 }
 
 // ---------------------------------------------------------------- pass 1
-template <class T, int R, int WK, bool FROM_DEM>
+template <class T, int R, int WK, bool FROM_DEM, bool ABS = false>
 __global__ void __launch_bounds__(128, FA_P1_MINB) k_pass1(PassArgs<T, WK> P) {
   using WB = WBT<R>;
   constexpr bool Z = FROM_DEM;
@@ -942,7 +957,19 @@ __global__ void __launch_bounds__(128, FA_P1_MINB) k_pass1(PassArgs<T, WK> P) {
   const int ndata = build_masks<!FROM_DEM>(s, nsrc, h, w);
   // RETAIN: the block-local accumulation is computed in place in acc
   unsigned long long wsum = init_values<T, R, Z, WK>(s, P.w, g, y0, x0, h, w, P.acc, P.status);
-  const uint32_t popped = kahn_block(s, nsrc, P.acc + y0 * g.W + x0, g.W);
+  if constexpr (ABS) {
+    // D21-like validation of alpha: data cells need a value in [0, 1]
+    bool bad = false;
+    for (int i = lane; i < h * WB::BC; i += 32) {
+      const int ly = i >> 5, lx = i & 31;
+      if (lx >= w || s.dirh[WB::hidx(ly, lx)] >= kOut) continue;
+      const float al = __ldg(P.alpha + (y0 + ly) * g.W + x0 + lx);
+      if (!(al >= 0.0f && al <= 1.0f)) bad = true;
+    }
+    if (__any_sync(kFull, bad) && lane == 0) atomicOr(P.status, ST_BADALPHA);
+  }
+  const uint32_t popped = kahn_block<T, R, Z, ABS>(s, nsrc, P.acc + y0 * g.W + x0, g.W,
+                                                   ABS ? P.alpha + y0 * g.W + x0 : nullptr);
   const int tot_data = __reduce_add_sync(kFull, ndata);
   if (lane == 0 && (int)popped != tot_data) atomicOr(P.status, ST_CYCLE);  // a cell never became ready
   if (!std::is_same<T, double>::value && P.wsum) {
@@ -950,7 +977,7 @@ __global__ void __launch_bounds__(128, FA_P1_MINB) k_pass1(PassArgs<T, WK> P) {
     for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
     if (lane == 0 && wsum) atomicAdd(P.wsum, wsum);
   }
-  block_records(s, P, b, y0, x0, h, w);
+  block_records<T, R, Z, WK, ABS>(s, P, b, y0, x0, h, w);
 }
 
 // ---------------------------------------------------------------- pass 2
@@ -1007,9 +1034,9 @@ struct __align__(16) FSmem {
   uint16_t item[KB * WB::PB];            // work list: (block-in-group << 8) | slot
 };
 
-template <class T, int R, int KB>
+template <class T, int R, int KB, bool ABS = false>
 __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ x_slot, const uint8_t* __restrict__ dirs,
-                                                  T* acc) {
+                                                  T* acc, const float* __restrict__ alpha = nullptr) {
   using WB = WBT<R>;
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
@@ -1058,6 +1085,7 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
   int head = 0, k = -1, cy = 0, cx = 0, h = 0, w = 0;
   T x = (T)0;
   T* rowp = nullptr;  // acc + y0 * W + x0 of the walk's block
+  const float* arow = nullptr;  // absorption: alpha + y0 * W + x0
   for (;;) {
     const unsigned idle = __ballot_sync(kFull, k < 0);
     if (idle == kFull && head >= n) break;
@@ -1077,6 +1105,7 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
           if (kk == j) { h = hs[j]; w = ws[j]; yy = y0s[j]; xx = x0s[j]; }
         x = x_slot[(b0 + k) * WB::PB + p];
         rowp = acc + yy * g.W + xx;
+        if (ABS) arow = alpha + yy * g.W + xx;
         bperim_xy(p, h, w, cx, cy);
       }
     }
@@ -1098,6 +1127,7 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
         k = -1;  // terminal, block exit, or dropped into NoData
         break;
       }
+      if (ABS) x *= (T)__ldg(arow + (int64_t)cy * g.W + cx);  // the cell passes on alpha of it
       cy = ty;
       cx = tx;
     }
@@ -1116,7 +1146,7 @@ cudaError_t launch_finalize_k(const Geom& g, const T* x_slot, const uint8_t* dir
   auto k = k_finalize<T, R, KB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int64_t groups = (g.nblocks + KB - 1) / KB;
-  k<<<(unsigned)((groups + NWC - 1) / NWC), 32 * NWC, sm, st>>>(g, x_slot, dirs, acc);
+  k<<<(unsigned)((groups + NWC - 1) / NWC), 32 * NWC, sm, st>>>(g, x_slot, dirs, acc, nullptr);
   return cudaGetLastError();
 }
 
@@ -1127,6 +1157,39 @@ cudaError_t launch_finalize_r(const Geom& g, const T* x_slot, const uint8_t* dir
   if (kb == 2) return launch_finalize_k<T, R, 2>(g, x_slot, dirs, acc, st);
   if (kb == 4) return launch_finalize_k<T, R, 4>(g, x_slot, dirs, acc, st);
   return launch_finalize_k<T, R, 1>(g, x_slot, dirs, acc, st);
+}
+
+// absorption (f64, 32x32 blocks): pass 1 and the finalize with alpha
+cudaError_t launch_pass1_absorb(const PassArgs<double, 0>* a0, const PassArgs<double, 2>* a2, bool from_dem,
+                                cudaStream_t st) {
+  auto go = [&](auto k, const auto& a) {
+    const size_t sm = (from_dem ? sizeof(WSmem<double, 32, true>) : sizeof(WSmem<double, 32, false>)) * (size_t)a.g.nw;
+    const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<grid, 32 * a.g.nw, sm, st>>>(a);
+  };
+  if (a0) {
+    if (a0->g.br != 32 || a0->g.bc != 32) return cudaErrorInvalidValue;
+    if (from_dem) go(k_pass1<double, 32, 0, true, true>, *a0);
+    else go(k_pass1<double, 32, 0, false, true>, *a0);
+  } else {
+    if (a2->g.br != 32 || a2->g.bc != 32) return cudaErrorInvalidValue;
+    if (from_dem) go(k_pass1<double, 32, 2, true, true>, *a2);
+    else go(k_pass1<double, 32, 2, false, true>, *a2);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_retain_absorb(const Geom& g, const double* x_slot, const uint8_t* dirs, double* acc,
+                                 const float* alpha, cudaStream_t st) {
+  if (g.br != 32 || g.bc != 32) return cudaErrorInvalidValue;
+  constexpr int NWC = 4;
+  size_t sm = sizeof(FSmem<double, 32, 1>) * NWC;
+  sm = sm < 24576 ? 24576 : sm;
+  auto k = k_finalize<double, 32, 1, true>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k<<<(unsigned)((g.nblocks + NWC - 1) / NWC), 32 * NWC, sm, st>>>(g, x_slot, dirs, acc, alpha);
+  return cudaGetLastError();
 }
 
 template <class T>

@@ -28,6 +28,7 @@ constexpr int kNW = 4;   // default warps (one block each) per CTA of the block 
 constexpr uint32_t ST_BADCODE = 1u;
 constexpr uint32_t ST_BADWEIGHT = 2u;
 constexpr uint32_t ST_CYCLE = 4u;
+constexpr uint32_t ST_BADALPHA = 8u;  // absorption: an alpha of a data cell outside [0,1]
 
 // node flags (per block-exit node)
 constexpr uint8_t NF_OUT_TILE = 1;  // target outside the node's tile (FlowExternal at tile level, D22)
@@ -227,6 +228,12 @@ struct PassArgs {
   uint32_t* status;
   bool retain;  // pass 1 writes the block-local accumulation into acc (RETAIN)
   bool cut;     // tile records wanted: slot roots also for every slot on a tile edge
+  // absorption: per-cell fraction of A passed on
+  // (row-major like acc), the product of alpha along each entry slot's
+  // in-block path before its exit, and alpha at each node's exit cell
+  const float* alpha;
+  T* slot_f;
+  float* node_alpha;
 };
 
 // warp-aggregated append of `v` (if pred) to list[*count]

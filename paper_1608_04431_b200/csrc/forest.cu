@@ -530,4 +530,56 @@ cudaError_t forest_roots(Runtime& rt, uint32_t n, const uint32_t* parent, uint32
   return rt.err ? rt.err : cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- weighted forest (absorption)
+// S(v) = val(v) + sum_children w(c) S(c): last-arrival walks without a step
+// cap (every node retires in one launch; a deep chain is walked by one
+// thread, so this solver is meant for the absorption variant only).
+namespace {
+__global__ void k_walk_w(const uint32_t* __restrict__ front, const uint32_t* __restrict__ nf_dev,
+                         const uint32_t* __restrict__ parent, const double* __restrict__ wv, double* val,
+                         uint32_t* cnt, uint32_t* nretired) {
+  const uint32_t nf = *nf_dev;
+  uint32_t retired = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+    uint32_t v = front[i];
+    double s = __ldcg(&val[v]);
+    for (;;) {
+      ++retired;
+      const uint32_t p = parent[v];
+      if (p == kNone) break;
+      atomic_add(&val[p], wv[v] * s);
+      cuda::atomic_ref<uint32_t, cuda::thread_scope_device> cp(cnt[p]);
+      if (cp.fetch_sub(1u, cuda::memory_order_acq_rel) != 1u) break;
+      s = __ldcg(&val[p]);
+      v = p;
+    }
+  }
+  for (int o = 16; o; o >>= 1) retired += __shfl_xor_sync(0xFFFFFFFFu, retired, o);
+  if ((threadIdx.x & 31) == 0 && retired) atomicAdd(nretired, retired);
+}
+}  // namespace
+
+cudaError_t forest_solve_weighted(Runtime& rt, uint32_t n, const uint32_t* parent, const double* wv, double* val) {
+  if (n == 0) return cudaSuccess;
+  cudaStream_t st = rt.st;
+  uint32_t* cnt = rt.alloc<uint32_t>(n);
+  uint8_t* done = rt.alloc<uint8_t>(n);
+  uint32_t* fa_ = rt.alloc<uint32_t>(n);
+  uint32_t* ctr = rt.alloc<uint32_t>(4);
+  if (rt.err) return rt.err;
+  cudaMemsetAsync(cnt, 0, n * sizeof(uint32_t), st);
+  cudaMemsetAsync(ctr, 0, 4 * sizeof(uint32_t), st);
+  k_count_children<<<grid_for(n), 256, 0, st>>>(n, parent, cnt);
+  k_init_frontier<<<grid_for(n), 256, 0, st>>>(n, cnt, done, fa_, ctr);
+  k_walk_w<<<grid_for(n), 256, 0, st>>>(fa_, ctr, parent, wv, val, cnt, ctr + 1);
+  rt.launches += 3;
+  rt.read(ctr + 1, 1);
+  if (rt.h_cnt[0] != n) k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);
+  rt.free(cnt);
+  rt.free(done);
+  rt.free(fa_);
+  rt.free(ctr);
+  return rt.err ? rt.err : cudaGetLastError();
+}
+
 }  // namespace fa

@@ -271,4 +271,51 @@ FA_INST(unsigned long long)
 FA_INST(double)
 #undef FA_INST
 
+// ---------------------------------------------------------------- absorption (N3)
+// Block-exit graph with multiplicative edges: exit node v sends
+// alpha(v) S(v) into its target entry slot t, and the entry's offset reaches
+// the exit its path drains to scaled by f(t), the product of alpha along
+// that in-block path before the exit (pass 1 records): edge weight
+// alpha(v) f(t).
+__global__ void k_node_weights(uint32_t nn, const float* __restrict__ node_alpha, const uint32_t* __restrict__ tgt,
+                               const double* __restrict__ slot_f, double* wv) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += gridDim.x * blockDim.x) {
+    const uint32_t t = tgt[v];
+    wv[v] = t == kNone ? 0.0 : (double)node_alpha[v] * slot_f[t];
+  }
+}
+// leaves' pushes (already alpha(leaf) A_B(leaf)) into the node their entry drains to
+__global__ void k_fold_leaves_w(int64_t nslots, const double* __restrict__ x_slot,
+                                const uint32_t* __restrict__ slot_root, const double* __restrict__ slot_f,
+                                double* S) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const double x = x_slot[s];
+    if (x == 0.0) continue;
+    const uint32_t e = slot_root[s];
+    if (e != kNone) atomic_add(&S[e], x * slot_f[s]);
+  }
+}
+// offsets at entry slots from the finished exits: alpha(v) S(v)
+__global__ void k_scatter_x_w(uint32_t nn, const uint32_t* __restrict__ tgt, const float* __restrict__ node_alpha,
+                              const double* __restrict__ S, double* x_slot) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += gridDim.x * blockDim.x) {
+    const uint32_t t = tgt[v];
+    if (t != kNone) atomic_add(&x_slot[t], (double)node_alpha[v] * S[v]);
+  }
+}
+
+cudaError_t launch_absorb_graph(cudaStream_t st, uint32_t nn, int64_t nslots, const float* node_alpha,
+                                const uint32_t* tgt, const double* slot_f, const double* x_slot,
+                                const uint32_t* slot_root, double* wv, double* S) {
+  k_node_weights<<<grid_for(nn), 256, 0, st>>>(nn, node_alpha, tgt, slot_f, wv);
+  k_fold_leaves_w<<<grid_for(nslots), 256, 0, st>>>(nslots, x_slot, slot_root, slot_f, S);
+  return cudaGetLastError();
+}
+cudaError_t launch_scatter_x_absorb(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const float* node_alpha,
+                                    const double* S, double* x_slot) {
+  k_scatter_x_w<<<grid_for(nn), 256, 0, st>>>(nn, tgt, node_alpha, S, x_slot);
+  return cudaGetLastError();
+}
+
 }  // namespace fa

@@ -26,7 +26,8 @@ FLOW_TERMINATES = 0xFFFFFFFF
 
 EXPORTS = ["fa_create", "fa_destroy", "fa_last_error", "fa_flowdirs", "fa_accumulate",
            "fa_accumulate_strips", "fa_perimeter_slots", "fa_perimeter_records", "fa_nccl_unique_id",
-           "fa_accumulate_dist", "fa_get_stats", "fa_accumulate_streamed"]
+           "fa_accumulate_dist", "fa_get_stats", "fa_accumulate_streamed",
+           "fa_accumulate_absorb"]
 
 
 def nccl_unique_id() -> bytes:
@@ -78,6 +79,7 @@ def load() -> ctypes.CDLL:
     lib.fa_accumulate.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int]
     lib.fa_accumulate_strips.argtypes = [P, ctypes.c_int, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int]
     lib.fa_accumulate_streamed.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int, I]
+    lib.fa_accumulate_absorb.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, P]
     lib.fa_perimeter_slots.argtypes = [P, I, I]
     lib.fa_perimeter_slots.restype = I
     lib.fa_perimeter_records.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, ctypes.c_int, P, P, P, P]
@@ -210,6 +212,22 @@ class Context:
                 out = np.empty((rows, cols), {A_U32: np.uint32, A_U64: np.uint64, A_F64: np.float64}[a])
         self._check(self.lib.fa_accumulate_streamed(self.h, rows, cols, _ptr(dem), float(nodata), _ptr(dirs),
                                                     _ptr(w), _wtype(w), _ptr(out), a, int(strip_rows)))
+        return out
+
+    def accumulate_absorb(self, alpha, dem=None, dirs=None, w=None, nodata: float = -9999.0, out=None):
+        """Absorption (N3): A(p) = w(p) + sum alpha(n) A(n) over donors n; f64 output.
+        alpha: f32 raster in [0,1] (device or host, like the other inputs)."""
+        src = dem if dem is not None else dirs
+        rows, cols = src.shape
+        if out is None:
+            if isinstance(src, torch.Tensor):
+                out = torch.empty((rows, cols), dtype=torch.float64, device=src.device)
+            else:
+                import numpy as np
+
+                out = np.empty((rows, cols), np.float64)
+        self._check(self.lib.fa_accumulate_absorb(self.h, rows, cols, _ptr(dem), float(nodata), _ptr(dirs),
+                                                  _ptr(w), _wtype(w), _ptr(alpha), _ptr(out)))
         return out
 
     def accumulate_dist(self, nccl_id: bytes, rank: int, nranks: int, global_rows: int, row_begin: int,
