@@ -111,8 +111,8 @@ FA_API fa_status fa_accumulate_strips(fa_ctx* ctx, int nstrips, int64_t rows, in
  * value in [0, 1] (else FA_E_ARG); NoData cells' alpha is ignored.  Output
  * f64 (NoData = quiet NaN); wtype FA_W_NONE (w = 1) or FA_W_F32.  Device or
  * host buffers.  Single device, 32x32 blocks (the default tiling); the
- * block-exit graph is solved with multiplicative edges by last-arrival walks
- * without contraction, so a very deep single chain is walked serially. */
+ * block-exit graph is solved with multiplicative edges (walks, peeling and
+ * affine chain contraction). */
 FA_API fa_status fa_accumulate_absorb(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem,
                                       float nodata, const uint8_t* dirs, const void* w,
                                       fa_wtype wtype, const float* alpha, double* acc);

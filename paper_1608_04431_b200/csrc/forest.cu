@@ -99,11 +99,11 @@ __global__ void k_peel(const uint32_t* __restrict__ front, uint32_t nf,
 // launched back to back without a host round trip.  Counters rotate over
 // three slots: round r reads c[r%3], appends into c[(r+1)%3] (zeroed by round
 // r-1) and zeroes c[(r+2)%3] for round r+1; `retired` accumulates the sizes.
-template <class T>
+template <class T, bool WG = false>
 __global__ void k_peel_dev(const uint32_t* __restrict__ front, const uint32_t* __restrict__ nf_in,
                            const uint32_t* __restrict__ parent, T* val, uint32_t* cnt, uint8_t* done,
                            uint32_t* next, uint32_t* nf_out, uint32_t* nf_clear,
-                           unsigned long long* retired) {
+                           unsigned long long* retired, const T* __restrict__ wv) {
   const uint32_t nf = *nf_in;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *nf_clear = 0u;
@@ -119,7 +119,7 @@ __global__ void k_peel_dev(const uint32_t* __restrict__ front, const uint32_t* _
       done[v] = 1;
       p = parent[v];
       if (p != kNone) {
-        atomic_add(&val[p], val[v]);
+        atomic_add(&val[p], WG ? wv[v] * val[v] : val[v]);  // absorption: edge weight
         push = atomicSub(&cnt[p], 1u) == 1u;
       }
     }
@@ -132,10 +132,10 @@ __global__ void k_peel_dev(const uint32_t* __restrict__ front, const uint32_t* _
 // parent's last pending child continues from the parent.  One launch replaces
 // the wide rounds of level-synchronous peeling; a walk stops after `cap`
 // steps and re-queues the ready node, leaving deep chains to contraction.
-template <class T>
+template <class T, bool WG = false>
 __global__ void k_walk(const uint32_t* __restrict__ front, const uint32_t* __restrict__ nf_dev,
                        const uint32_t* __restrict__ parent, T* val, uint32_t* cnt, uint8_t* done, uint32_t* next,
-                       uint32_t* ncount, uint32_t* nretired, int cap) {
+                       uint32_t* ncount, uint32_t* nretired, int cap, const T* __restrict__ wv) {
   const uint32_t nf = *nf_dev;  // frontier size read on the device: no host round trip before the launch
   const uint32_t stride = gridDim.x * blockDim.x;
   uint32_t retired = 0;
@@ -151,7 +151,7 @@ __global__ void k_walk(const uint32_t* __restrict__ front, const uint32_t* __res
         ++retired;
         const uint32_t p = parent[v];
         if (p == kNone) break;
-        atomic_add(&val[p], s);
+        atomic_add(&val[p], WG ? wv[v] * s : s);
         // acq_rel decrement: our contribution is released before it, and the
         // last arrival acquires every other child's contribution
         cuda::atomic_ref<uint32_t, cuda::thread_scope_device> cp(cnt[p]);
@@ -199,13 +199,15 @@ __global__ void k_compact_residual(uint32_t n, const uint8_t* __restrict__ done,
   }
 }
 
-template <class T>
+template <class T, bool WG = false>
 __global__ void k_build_local(uint32_t m, const uint32_t* __restrict__ R,
                               const uint32_t* __restrict__ parent, const T* __restrict__ val,
                               const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ rid,
-                              uint32_t* lpar, T* lval, uint32_t* lpc, uint32_t* up) {
+                              uint32_t* lpar, T* lval, uint32_t* lpc, uint32_t* up,
+                              const T* __restrict__ wv, T* lw) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
     const uint32_t v = R[r];
+    if (WG) lw[r] = wv[v];  // weight of r's edge to its parent
     const uint32_t p = parent[v];
     lpar[r] = p == kNone ? kNone : rid[p];
     lval[r] = val[v];
@@ -222,28 +224,38 @@ __global__ void k_set_up(uint32_t m, const uint32_t* __restrict__ lpar, const ui
   }
 }
 
-template <class T>
+// weighted (absorption): S(r) = acc(r) + mul(r) S(nxt(r)); a chain node's
+// single pending child c contributes w(c) S(c)
+template <class T, bool WG = false>
 __global__ void k_jump_init(uint32_t m, const uint32_t* __restrict__ lpc, const uint32_t* __restrict__ up,
-                            const T* __restrict__ lval, uint32_t* nxt, T* acc) {
+                            const T* __restrict__ lval, uint32_t* nxt, T* acc, const T* __restrict__ lw, T* mul) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
     const bool start = lpc[r] != 1u;
     nxt[r] = start ? r : up[r];
     acc[r] = start ? (T)0 : lval[r];
+    if (WG) mul[r] = start ? (T)1 : lw[up[r]];
   }
 }
 
-template <class T>
+template <class T, bool WG = false>
 __global__ void k_jump(uint32_t m, const uint32_t* __restrict__ lpc, const uint32_t* __restrict__ nxt_in,
-                       const T* __restrict__ acc_in, uint32_t* nxt_out, T* acc_out, uint32_t* changed) {
+                       const T* __restrict__ acc_in, uint32_t* nxt_out, T* acc_out, uint32_t* changed,
+                       const T* __restrict__ mul_in, T* mul_out) {
   bool ch = false;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
     const uint32_t n1 = nxt_in[r];
     if (lpc[n1] != 1u) {  // reached a segment start
       nxt_out[r] = n1;
       acc_out[r] = acc_in[r];
+      if (WG) mul_out[r] = mul_in[r];
     } else {
       nxt_out[r] = nxt_in[n1];
-      acc_out[r] = acc_in[r] + acc_in[n1];
+      if (WG) {
+        acc_out[r] = acc_in[r] + mul_in[r] * acc_in[n1];
+        mul_out[r] = mul_in[r] * mul_in[n1];
+      } else {
+        acc_out[r] = acc_in[r] + acc_in[n1];
+      }
       ch = true;
     }
   }
@@ -275,10 +287,11 @@ __global__ void k_seg_ids(uint32_t m, const uint32_t* __restrict__ lpc, const T*
 
 // every segment end r (parent is a junction or none) links its segment start
 // to the junction and hands the junction its chain prefix pre(r)
-template <class T>
+template <class T, bool WG = false>
 __global__ void k_seg_build(uint32_t m, const uint32_t* __restrict__ lpar, const uint32_t* __restrict__ lpc,
                             const uint32_t* __restrict__ nxt, const T* __restrict__ acc,
-                            const uint32_t* __restrict__ sid, uint32_t* spar, T* sval) {
+                            const uint32_t* __restrict__ sid, uint32_t* spar, T* sval,
+                            const T* __restrict__ lw, const T* __restrict__ mul, T* sw) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
     const uint32_t q = lpar[r];
     if (q != kNone && lpc[q] == 1u) continue;  // not an end
@@ -287,17 +300,23 @@ __global__ void k_seg_build(uint32_t m, const uint32_t* __restrict__ lpar, const
       spar[s] = kNone;
     } else {
       spar[s] = sid[q];
-      atomic_add(&sval[sid[q]], acc[r]);
+      if (WG) {
+        // S(q) += w(r) S(r) = w(r) acc(r) + w(r) mul(r) S(start): the segment edge weight
+        sw[s] = lw[r] * mul[r];
+        atomic_add(&sval[sid[q]], lw[r] * acc[r]);
+      } else {
+        atomic_add(&sval[sid[q]], acc[r]);
+      }
     }
   }
 }
 
-template <class T>
+template <class T, bool WG = false>
 __global__ void k_expand(uint32_t m, const uint32_t* __restrict__ R, const uint32_t* __restrict__ nxt,
                          const T* __restrict__ acc, const uint32_t* __restrict__ sid,
-                         const T* __restrict__ sval, T* val) {
+                         const T* __restrict__ sval, T* val, const T* __restrict__ mul) {
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x)
-    val[R[r]] = sval[sid[nxt[r]]] + acc[r];
+    val[R[r]] = WG ? acc[r] + mul[r] * sval[sid[nxt[r]]] : sval[sid[nxt[r]]] + acc[r];
 }
 
 __global__ void k_set_flag(uint32_t* st, uint32_t f) { atomicOr(st, f); }
@@ -314,8 +333,11 @@ constexpr int kMaxJump = 40;
 constexpr int kWalkCap = 128;  // steps per walk before re-queueing (deep chains -> contraction); 0 = peel only.
                                // 128 vs 32: cfg3 graph 1.54 vs 1.57 ms, 8 strips 29.9 vs 31.1 ms, cfg2 (one 16.7M chain) 1.04 vs 0.95 ms
 
-template <class T>
-cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, int level) {
+// WG (absorption): edge weights wv (S(parent) += wv(v) S(v)); chains are
+// contracted with affine (acc, mul) pairs instead of sums
+template <class T, bool WG = false>
+cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, int level,
+                        const T* wv = nullptr) {
   if (n == 0) return cudaSuccess;
   if (level > kMaxLevels) {
     k_set_flag<<<1, 1, 0, rt.st>>>(rt.d_status, ST_CYCLE);
@@ -347,7 +369,7 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
     // bulk of the forest: one launch of capped walks from every leaf (a
     // grid for all n nodes; the walks read the frontier size themselves)
     cudaMemsetAsync(ctr + 1, 0, 2 * sizeof(uint32_t), st);
-    k_walk<T><<<grid_for(n), 256, 0, st>>>(fa_, ctr, parent, val, cnt, done, fb, ctr + 1, ctr + 2, cap);
+    k_walk<T, WG><<<grid_for(n), 256, 0, st>>>(fa_, ctr, parent, val, cnt, done, fb, ctr + 1, ctr + 2, cap, wv);
     ++rt.launches;
     ++rt.peel_rounds;
     std::swap(fa_, fb);
@@ -377,12 +399,15 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
       T* lval = rt.alloc<T>(m);
       T* aca = rt.alloc<T>(m);
       T* acb = rt.alloc<T>(m);
+      T* lw = WG ? rt.alloc<T>(m) : nullptr;
+      T* mua = WG ? rt.alloc<T>(m) : nullptr;
+      T* mub = WG ? rt.alloc<T>(m) : nullptr;
       if (rt.err) return rt.err;
-      k_build_local<T><<<grid_for(m), 256, 0, st>>>(m, R, parent, val, cnt, rid, lpar, lval, lpc, up);
+      k_build_local<T, WG><<<grid_for(m), 256, 0, st>>>(m, R, parent, val, cnt, rid, lpar, lval, lpc, up, wv, lw);
       ++rt.launches;
       k_set_up<<<grid_for(m), 256, 0, st>>>(m, lpar, lpc, up);
       ++rt.launches;
-      k_jump_init<T><<<grid_for(m), 256, 0, st>>>(m, lpc, up, lval, nxa, aca);
+      k_jump_init<T, WG><<<grid_for(m), 256, 0, st>>>(m, lpc, up, lval, nxa, aca, lw, mua);
       ++rt.launches;
       int rounds = 0;
       for (int batch = 8;; batch = 4) {
@@ -391,9 +416,10 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
         // rounds are no-ops)
         cudaMemsetAsync(ctr + 2, 0, sizeof(uint32_t), st);
         for (int j = 0; j < batch; ++j) {
-          k_jump<T><<<grid_for(m), 256, 0, st>>>(m, lpc, nxa, aca, nxb, acb, ctr + 2);
+          k_jump<T, WG><<<grid_for(m), 256, 0, st>>>(m, lpc, nxa, aca, nxb, acb, ctr + 2, mua, mub);
           std::swap(nxa, nxb);
           std::swap(aca, acb);
+          std::swap(mua, mub);
         }
         rt.launches += batch;
         rounds += batch;
@@ -410,25 +436,27 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
       cudaMemsetAsync(ctr + 3, 0, sizeof(uint32_t), st);
       T* sval = rt.alloc<T>(m);
       uint32_t* spar = rt.alloc<uint32_t>(m);
+      T* sw = WG ? rt.alloc<T>(m) : nullptr;
       if (rt.err) return rt.err;
+      if (WG) cudaMemsetAsync(sw, 0, m * sizeof(T), st);
       k_seg_ids<T><<<grid_for(m), 256, 0, st>>>(m, lpc, lval, sid, ctr + 3, sval, spar);
       ++rt.launches;
-      k_seg_build<T><<<grid_for(m), 256, 0, st>>>(m, lpar, lpc, nxa, aca, sid, spar, sval);
+      k_seg_build<T, WG><<<grid_for(m), 256, 0, st>>>(m, lpar, lpc, nxa, aca, sid, spar, sval, lw, mua, sw);
       ++rt.launches;
       rt.read(ctr + 3, 1);
       const uint32_t ms = rt.h_cnt[0];
       if (rounds <= kMaxJump && ms < m) {
-        solve_level<T>(rt, ms, spar, sval, level + 1);
+        solve_level<T, WG>(rt, ms, spar, sval, level + 1, sw);
       } else if (ms >= m) {
         // no chain node: cannot happen with a thin frontier unless cyclic
         k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);
         ++rt.launches;
       }
-      k_expand<T><<<grid_for(m), 256, 0, st>>>(m, R, nxa, aca, sid, sval, val);
+      k_expand<T, WG><<<grid_for(m), 256, 0, st>>>(m, R, nxa, aca, sid, sval, val, mua);
       ++rt.launches;
       for (void* p : {(void*)R, (void*)rid, (void*)lpar, (void*)lpc, (void*)up, (void*)nxa,
                       (void*)nxb, (void*)sid, (void*)lval, (void*)aca, (void*)acb, (void*)sval,
-                      (void*)spar})
+                      (void*)spar, (void*)lw, (void*)mua, (void*)mub, (void*)sw})
         rt.free(p);
       remaining = 0;
       break;
@@ -444,8 +472,8 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
     unsigned long long* retired = reinterpret_cast<unsigned long long*>(pc + 4);
     const unsigned grid = grid_for(nf);
     for (int r = 0; r < kPeelBatch; ++r) {
-      k_peel_dev<T><<<grid, 256, 0, st>>>(fa_, pc + r % 3, parent, val, cnt, done, fb, pc + (r + 1) % 3,
-                                          pc + (r + 2) % 3, retired);
+      k_peel_dev<T, WG><<<grid, 256, 0, st>>>(fa_, pc + r % 3, parent, val, cnt, done, fb, pc + (r + 1) % 3,
+                                              pc + (r + 2) % 3, retired, wv);
       std::swap(fa_, fb);
     }
     rt.launches += kPeelBatch;
@@ -531,55 +559,10 @@ cudaError_t forest_roots(Runtime& rt, uint32_t n, const uint32_t* parent, uint32
 }
 
 // ---------------------------------------------------------------- weighted forest (absorption)
-// S(v) = val(v) + sum_children w(c) S(c): last-arrival walks without a step
-// cap (every node retires in one launch; a deep chain is walked by one
-// thread, so this solver is meant for the absorption variant only).
-namespace {
-__global__ void k_walk_w(const uint32_t* __restrict__ front, const uint32_t* __restrict__ nf_dev,
-                         const uint32_t* __restrict__ parent, const double* __restrict__ wv, double* val,
-                         uint32_t* cnt, uint32_t* nretired) {
-  const uint32_t nf = *nf_dev;
-  uint32_t retired = 0;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
-    uint32_t v = front[i];
-    double s = __ldcg(&val[v]);
-    for (;;) {
-      ++retired;
-      const uint32_t p = parent[v];
-      if (p == kNone) break;
-      atomic_add(&val[p], wv[v] * s);
-      cuda::atomic_ref<uint32_t, cuda::thread_scope_device> cp(cnt[p]);
-      if (cp.fetch_sub(1u, cuda::memory_order_acq_rel) != 1u) break;
-      s = __ldcg(&val[p]);
-      v = p;
-    }
-  }
-  for (int o = 16; o; o >>= 1) retired += __shfl_xor_sync(0xFFFFFFFFu, retired, o);
-  if ((threadIdx.x & 31) == 0 && retired) atomicAdd(nretired, retired);
-}
-}  // namespace
-
+// S(v) = val(v) + sum_children wv(c) S(c): the same walk / peel / contract
+// solver with edge weights (affine chain contraction)
 cudaError_t forest_solve_weighted(Runtime& rt, uint32_t n, const uint32_t* parent, const double* wv, double* val) {
-  if (n == 0) return cudaSuccess;
-  cudaStream_t st = rt.st;
-  uint32_t* cnt = rt.alloc<uint32_t>(n);
-  uint8_t* done = rt.alloc<uint8_t>(n);
-  uint32_t* fa_ = rt.alloc<uint32_t>(n);
-  uint32_t* ctr = rt.alloc<uint32_t>(4);
-  if (rt.err) return rt.err;
-  cudaMemsetAsync(cnt, 0, n * sizeof(uint32_t), st);
-  cudaMemsetAsync(ctr, 0, 4 * sizeof(uint32_t), st);
-  k_count_children<<<grid_for(n), 256, 0, st>>>(n, parent, cnt);
-  k_init_frontier<<<grid_for(n), 256, 0, st>>>(n, cnt, done, fa_, ctr);
-  k_walk_w<<<grid_for(n), 256, 0, st>>>(fa_, ctr, parent, wv, val, cnt, ctr + 1);
-  rt.launches += 3;
-  rt.read(ctr + 1, 1);
-  if (rt.h_cnt[0] != n) k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);
-  rt.free(cnt);
-  rt.free(done);
-  rt.free(fa_);
-  rt.free(ctr);
-  return rt.err ? rt.err : cudaGetLastError();
+  return solve_level<double, true>(rt, n, parent, val, 0, wv);
 }
 
 }  // namespace fa

@@ -75,3 +75,24 @@ def test_absorb_rejects_bad_alpha(fa_lib):
         al[d == 255] = np.nan  # ignored at NoData cells
         got = ctx.accumulate_absorb(_cuda(al), dirs=_cuda(d)).cpu().numpy()
     _check(got, d, oracle.accumulate_alpha(d, al))
+
+
+@pytest.mark.parametrize("cap", ["1", "4", "128"])
+def test_absorb_weighted_contraction(fa_lib, cap, monkeypatch):
+    """Deep block-exit chains: the serpentine's river crosses every block row
+    (~32K chained nodes at 1024^2), so the weighted solver contracts chains
+    with affine (acc, mul) pointer jumping; small walk caps force contraction
+    on a random raster's forest too (FA_WALKCAP is read per call)."""
+    monkeypatch.setenv("FA_WALKCAP", cap)
+    rng = np.random.default_rng(int(cap))
+    d = inputs.serpentine(1024, 1024)
+    al = (0.999 + 0.001 * rng.random(d.shape)).astype(np.float32)
+    r = inputs.random_dirs(17, 300, 257, p_nodata=0.1, p_noflow=0.02)
+    ar = rng.random(r.shape).astype(np.float32)
+    w = inputs.weights_f32(17, r.shape)
+    with fa_lib.Context(0) as ctx:
+        got = ctx.accumulate_absorb(_cuda(al), dirs=_cuda(d)).cpu().numpy()
+        assert ctx.stats()["contract_levels"] > 0  # the weighted chain contraction ran
+        gr = ctx.accumulate_absorb(_cuda(ar), dirs=_cuda(r), w=_cuda(w)).cpu().numpy()
+    _check(got, d, oracle.accumulate_alpha(d, al))
+    _check(gr, r, oracle.accumulate_alpha(r, ar, w))
