@@ -156,25 +156,6 @@ __device__ __forceinline__ int bperim_index(int x, int y, int h, int w) {
   return w + (h - 1) + (w - 1) + (h - 2 - y);
 }
 
-// shared-memory accumulate at a junction (u32: native atomic; 64-bit: CAS,
-// starting from the value just read)
-__device__ __forceinline__ void sh_add(uint32_t* p, uint32_t v, uint32_t) { atomicAdd(p, v); }
-__device__ __forceinline__ void sh_add(unsigned long long* p, unsigned long long v, unsigned long long cur) {
-  for (;;) {
-    const unsigned long long prev = atomicCAS(p, cur, cur + v);
-    if (prev == cur) return;
-    cur = prev;
-  }
-}
-__device__ __forceinline__ void sh_add(double* p, double v, double cur) {
-  unsigned long long* q = reinterpret_cast<unsigned long long*>(p);
-  unsigned long long c = __double_as_longlong(cur);
-  for (;;) {
-    const unsigned long long prev = atomicCAS(q, c, __double_as_longlong(__longlong_as_double(c) + v));
-    if (prev == c) return;
-    c = prev;
-  }
-}
 
 template <int R>
 __device__ __forceinline__ uint32_t succ_word(int i, int d, uint32_t forb) {
@@ -418,20 +399,6 @@ __device__ __forceinline__ void load_dirs(WSmem<T, R, Z>& s, const uint8_t* dirs
   }
 }
 
-// successor words from the staged directions
-template <class T, int R, bool Z>
-__device__ __forceinline__ void succ_from_dirs(WSmem<T, R, Z>& s, int h, int w) {
-  using WB = WBT<R>;
-  const int lx = lane_id();
-  if (lx >= w) return;
-  const uint32_t fc = forb_col(lx, w);
-  for (int ly = 0; ly < h; ++ly) {
-    const int hi = WB::hidx(ly, lx);
-    int d = s.dirh[hi];
-    if (d >= 1 && d <= 8 && s.dirh[hi + WB::offH(d)] == kNoData) d |= 16;
-    s.succ[ly * WB::BC + lx] = (uint16_t)succ_word<R>(ly * WB::BC + lx, d, fc | forb_row(ly, h));
-  }
-}
 
 // ---------------------------------------------------------------- H2
 // Donor masks of the 4 cells of dirh word hw: bit k-1 of byte j set iff the

@@ -73,29 +73,8 @@ __global__ void __launch_bounds__(256) k_init_frontier(uint32_t n, const uint32_
   }
 }
 
-template <class T>
-__global__ void k_peel(const uint32_t* __restrict__ front, uint32_t nf,
-                       const uint32_t* __restrict__ parent, T* val, uint32_t* cnt, uint8_t* done,
-                       uint32_t* next, uint32_t* ncount) {
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t base = blockIdx.x * blockDim.x; base < nf; base += stride) {
-    const uint32_t i = base + threadIdx.x;
-    bool push = false;
-    uint32_t p = kNone;
-    if (i < nf) {
-      const uint32_t v = front[i];
-      done[v] = 1;
-      p = parent[v];
-      if (p != kNone) {
-        atomic_add(&val[p], val[v]);
-        push = atomicSub(&cnt[p], 1u) == 1u;
-      }
-    }
-    warp_append(push, p, next, ncount);
-  }
-}
-
-// The same round with the frontier size read on the device: rounds are
+// One level-synchronous peel round (Alg. 1's queue loop over the forest)
+// with the frontier size read on the device: rounds are
 // launched back to back without a host round trip.  Counters rotate over
 // three slots: round r reads c[r%3], appends into c[(r+1)%3] (zeroed by round
 // r-1) and zeroes c[(r+2)%3] for round r+1; `retired` accumulates the sizes.
