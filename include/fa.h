@@ -110,12 +110,16 @@ FA_API fa_status fa_accumulate_strips(fa_ctx* ctx, int nstrips, int64_t rows, in
  * cell's accumulation passed to its D8 target; data cells need a finite
  * value in [0, 1] (else FA_E_ARG); NoData cells' alpha is ignored.  Output
  * f64 (NoData = quiet NaN); wtype FA_W_NONE (w = 1) or FA_W_F32.  Device or
- * host buffers.  Single device, 32x32 blocks (the default tiling); the
- * block-exit graph is solved with multiplicative edges (walks, peeling and
- * affine chain contraction). */
-FA_API fa_status fa_accumulate_absorb(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem,
-                                      float nodata, const uint8_t* dirs, const void* w,
-                                      fa_wtype wtype, const float* alpha, double* acc);
+ * host buffers.  32x32 blocks (the default); the block-exit graph is solved
+ * with multiplicative edges (walks, peeling and affine chain contraction).
+ * nstrips <= 1: one device, uncut; nstrips > 1: the row-strip pipeline of
+ * the multi-GPU path on this device, with the tile links carrying their
+ * alpha path factors (tile records, the producer graph G2 and the offsets
+ * all weighted). */
+FA_API fa_status fa_accumulate_absorb(fa_ctx* ctx, int nstrips, int64_t rows, int64_t cols,
+                                      const float* dem, float nodata, const uint8_t* dirs,
+                                      const void* w, fa_wtype wtype, const float* alpha,
+                                      double* acc);
 
 /* Out-of-core accumulation (the paper's EVICT strategy, P:L79-81,
  * P:L255): dem / dirs / w / acc are HOST buffers (pinned memory

@@ -53,7 +53,8 @@ cudaError_t launch_absorb_graph(cudaStream_t st, uint32_t nn, int64_t nslots, co
                                 const uint32_t* tgt, const double* slot_f, const double* x_slot,
                                 const uint32_t* slot_root, double* wv, double* S);
 cudaError_t launch_scatter_x_absorb(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const float* node_alpha,
-                                    const double* S, double* x_slot);
+                                    const double* S, double* x_slot, const uint8_t* flags, bool intra_tile);
+cudaError_t launch_g1_weights_cut(cudaStream_t st, uint32_t nn, const uint8_t* flags, double* wv);
 template <class T>
 cudaError_t launch_scatter_x(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
                              const T* S, T* x_slot, bool intra_tile);
@@ -63,17 +64,19 @@ template <class T>
 cudaError_t launch_tile_records(cudaStream_t st, const Geom& g, int64_t nslots, const int64_t* tbase,
                                 const uint8_t* dirs, const uint32_t* slot_root, const uint32_t* troot,
                                 const uint8_t* flags, const uint32_t* node_slot, const T* S1,
-                                uint32_t* links, uint8_t* fdir, T* tile_acc);
+                                uint32_t* links, uint8_t* fdir, T* tile_acc, const T* slot_f = nullptr,
+                                const T* ptroot = nullptr, const float* alpha = nullptr, T* tile_f = nullptr);
 template <class T>
 cudaError_t launch_g2_slots(cudaStream_t st, const Geom& gg, int64_t nslots, const int64_t* tbase,
                             const uint32_t* links, const uint8_t* fdir, const T* tile_acc, uint32_t* parent,
-                            T* val);
+                            T* val, const T* tile_f = nullptr, T* wv2 = nullptr);
 template <class T>
 cudaError_t launch_xT(cudaStream_t st, int64_t nslots, const uint32_t* parent, const uint32_t* links,
-                      const T* S2, T* xT);
+                      const T* S2, T* xT, const T* tile_f = nullptr);
 template <class T>
 cudaError_t launch_inject_slots(cudaStream_t st, const Geom& g, int64_t nslots, const int64_t* tbase,
-                                const T* xT, const uint32_t* slot_root, T* val1, T* x_slot);
+                                const T* xT, const uint32_t* slot_root, T* val1, T* x_slot,
+                                const T* slot_f = nullptr);
 
 Geom make_geom(int64_t H, int64_t W, int64_t th, int64_t tw) {
   Geom g{};
@@ -268,6 +271,8 @@ struct Strip {
   const float* alpha = nullptr;  // absorption (N3): per-cell alpha, or null
   T* slot_f = nullptr;           // absorption: alpha product along each entry slot's path
   float* node_alpha = nullptr;   // absorption: alpha at each node's exit cell
+  double* wv = nullptr;          // absorption: block-exit edge weights (tile-cut graph)
+  double* ptroot = nullptr;      // absorption: edge-weight product from each node to its tile root
   uint8_t* dirs_buf = nullptr;
   uint32_t* slot_root = nullptr;
   T* node_val = nullptr;
@@ -284,8 +289,10 @@ struct Strip {
   void release(fa::Runtime& rt) {
     for (void* p : {(void*)dirs_buf, (void*)slot_root, (void*)node_val, (void*)node_slot, (void*)node_tgt,
                     (void*)node_flags, (void*)x_slot, (void*)parent, (void*)S, (void*)troot, (void*)dtbase,
-                    (void*)acc_tmp, (void*)halo_dirs, (void*)slot_f, (void*)node_alpha})
+                    (void*)acc_tmp, (void*)halo_dirs, (void*)slot_f, (void*)node_alpha, (void*)wv,
+                    (void*)ptroot})
       rt.free(p);
+    wv = ptroot = nullptr;
     dirs_buf = nullptr;
     acc_tmp = nullptr;
     halo_dirs = nullptr;
@@ -432,7 +439,8 @@ __global__ void k_tile_bases(fa::Geom g, int64_t* base) {
 
 // phase A tail: A_T at block exits, tile roots, tile perimeter records
 template <class T>
-fa_status strip_records(fa_ctx* ctx, Strip<T>& s, uint32_t* links, uint8_t* fdir, T* tile_acc) {
+fa_status strip_records(fa_ctx* ctx, Strip<T>& s, uint32_t* links, uint8_t* fdir, T* tile_acc,
+                        T* tile_f = nullptr) {
   using namespace fa;
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
@@ -443,6 +451,25 @@ fa_status strip_records(fa_ctx* ctx, Strip<T>& s, uint32_t* links, uint8_t* fdir
   k_tile_bases<<<1, 32, 0, st>>>(s.g, s.dtbase);
   ++rt.launches;
   CK(cudaMemcpyAsync(s.S, s.node_val, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  if constexpr (std::is_same<T, double>::value) {
+    if (s.alpha) {
+      // absorption: weighted tile-cut graph; tile records carry the path factors
+      s.wv = rt.alloc<double>(s.nn ? s.nn : 1);
+      s.ptroot = rt.alloc<double>(s.nn ? s.nn : 1);
+      if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+      CK(launch_absorb_graph(st, s.nn, s.g.nblocks * s.g.pb, s.node_alpha, s.node_tgt, s.slot_f, s.x_slot,
+                             s.slot_root, s.wv, s.S));
+      CK(launch_g1_weights_cut(st, s.nn, s.node_flags, s.wv));
+      rt.launches += 3;
+      CK(forest_solve_weighted(rt, s.nn, s.parent, s.wv, s.S));
+      CK(forest_roots_weighted(rt, s.nn, s.parent, s.wv, s.troot, s.ptroot));
+      CK(launch_tile_records<T>(st, s.g, s.nslots, s.dtbase, s.dirs_in(), s.slot_root, s.troot, s.node_flags,
+                                s.node_slot, s.S, links + s.slot0, fdir + s.slot0, tile_acc + s.slot0, s.slot_f,
+                                s.ptroot, s.alpha, tile_f + s.slot0));
+      ++rt.launches;
+      return FA_OK;
+    }
+  }
   CK(launch_fold_leaves<T>(st, s.g.nblocks * s.g.pb, s.x_slot, s.slot_root, s.S));  // leaves raked in pass 1
   ++rt.launches;
   CK(forest_solve<T>(rt, s.nn, s.parent, s.S));  // A_T at every block exit (Alg. 1 on each tile)
@@ -456,7 +483,8 @@ fa_status strip_records(fa_ctx* ctx, Strip<T>& s, uint32_t* links, uint8_t* fdir
 // the producer's global graph over all tile slots -> offsets x_T (all slots)
 template <class T>
 fa_status solve_g2(fa_ctx* ctx, const Geom& gg, int64_t nslots, const std::vector<int64_t>& hbase,
-                   const uint32_t* links, const uint8_t* fdir, const T* tile_acc, T* xT) {
+                   const uint32_t* links, const uint8_t* fdir, const T* tile_acc, T* xT,
+                   const T* tile_f = nullptr) {
   using namespace fa;
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
@@ -466,14 +494,22 @@ fa_status solve_g2(fa_ctx* ctx, const Geom& gg, int64_t nslots, const std::vecto
   T* val = rt.alloc<T>(nslots);
   if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
   CK(cudaMemcpyAsync(db, hbase.data(), hbase.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  CK(launch_g2_slots<T>(st, gg, nslots, db, links, fdir, tile_acc, par, val));
+  T* wv2 = tile_f ? rt.alloc<T>(nslots) : nullptr;
+  if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+  CK(launch_g2_slots<T>(st, gg, nslots, db, links, fdir, tile_acc, par, val, tile_f, wv2));
   ++rt.launches;
-  CK(forest_solve<T>(rt, (uint32_t)nslots, par, val));
+  if constexpr (std::is_same<T, double>::value) {
+    if (tile_f) CK(forest_solve_weighted(rt, (uint32_t)nslots, par, wv2, val));  // absorption: weighted G2
+    else CK(forest_solve<T>(rt, (uint32_t)nslots, par, val));
+  } else {
+    CK(forest_solve<T>(rt, (uint32_t)nslots, par, val));
+  }
   CK(cudaMemsetAsync(xT, 0, nslots * sizeof(T), st));
-  CK(launch_xT<T>(st, nslots, par, links, val, xT));
+  CK(launch_xT<T>(st, nslots, par, links, val, xT, tile_f));
   ++rt.launches;
   CK(cudaStreamSynchronize(st));
   rt.free(db);
+  rt.free(wv2);
   rt.free(par);
   rt.free(val);
   return FA_OK;
@@ -486,6 +522,31 @@ fa_status strip_finish(fa_ctx* ctx, Strip<T>& s, const T* xT_global) {
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
   CK(cudaMemcpyAsync(s.S, s.node_val, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  if constexpr (std::is_same<T, double>::value) {
+    if (s.alpha) {
+      // absorption: weighted fold, injection scaled by the entry path factor,
+      // weighted tile-cut solve, weighted intra-tile scatter, alpha finalize
+      if (!s.wv) {
+        s.wv = rt.alloc<double>(s.nn ? s.nn : 1);
+        if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+      }
+      CK(launch_absorb_graph(st, s.nn, s.g.nblocks * s.g.pb, s.node_alpha, s.node_tgt, s.slot_f, s.x_slot,
+                             s.slot_root, s.wv, s.S));
+      CK(launch_g1_weights_cut(st, s.nn, s.node_flags, s.wv));
+      rt.launches += 3;
+      CK(launch_inject_slots<T>(st, s.g, s.nslots, s.dtbase, xT_global + s.slot0, s.slot_root, s.S, s.x_slot,
+                                s.slot_f));
+      ++rt.launches;
+      CK(forest_solve_weighted(rt, s.nn, s.parent, s.wv, s.S));
+      CK(launch_scatter_x_absorb(st, s.nn, s.node_tgt, s.node_alpha, s.S, s.x_slot, s.node_flags, true));
+      ++rt.launches;
+      if (s.acc) {
+        CK(launch_retain_absorb(s.g, s.x_slot, s.dirs_in(), s.acc, s.alpha, st));
+        ++rt.launches;
+      }
+      return FA_OK;
+    }
+  }
   // leaves first (x_slot holds only their pass-1 values here), then x_T
   CK(launch_fold_leaves<T>(st, s.g.nblocks * s.g.pb, s.x_slot, s.slot_root, s.S));
   ++rt.launches;
@@ -553,7 +614,7 @@ struct Records {
 
 template <class T, int WK>
 fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nodata, const uint8_t* dirs,
-                  const void* w, T* acc, Records& rec, int nstrips) {
+                  const void* w, T* acc, Records& rec, int nstrips, const float* alpha = nullptr) {
   using namespace fa;
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
@@ -608,13 +669,14 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
   uint8_t* fdir = rt.alloc<uint8_t>(nslots);
   T* tile_acc = rt.alloc<T>(nslots);
   T* xT = rt.alloc<T>(nslots);
+  T* tile_f = alpha ? rt.alloc<T>(nslots) : nullptr;  // absorption: path factors per tile slot
   if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
   const int G = nstrips < 1 ? 1 : (int)(nstrips > gg.TR ? gg.TR : nstrips);
   std::vector<Strip<T>> strips(G);
   int64_t blocks = 0, nodes = 0;
   auto cleanup = [&]() {
     for (auto& s : strips) s.release(rt);
-    for (void* p : {(void*)links, (void*)fdir, (void*)tile_acc, (void*)xT}) rt.free(p);
+    for (void* p : {(void*)links, (void*)fdir, (void*)tile_acc, (void*)xT, (void*)tile_f}) rt.free(p);
   };
   for (int i = 0; i < G; ++i) {
     // strip i: tile rows [i*TR/G, (i+1)*TR/G)
@@ -638,9 +700,10 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
     s.w = w ? static_cast<const char*>(w) + r0 * W * (WK == 0 ? 0 : 4) : nullptr;
     s.acc = acc ? acc + r0 * W : nullptr;
     s.slot0 = hbase[tr0 * gg.TC];
+    s.alpha = alpha ? alpha + r0 * W : nullptr;
     fa_status r = strip_pass1<T, WK>(ctx, s, true);
     if (r != FA_OK) { cleanup(); return r; }
-    r = strip_records<T>(ctx, s, links, fdir, tile_acc);
+    r = strip_records<T>(ctx, s, links, fdir, tile_acc, tile_f);
     if (r != FA_OK) { cleanup(); return r; }
     blocks += s.g.nblocks;
     nodes += s.nn;
@@ -653,7 +716,7 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
     fa_status r = check_status(ctx, rt.h_cnt[0] & ~ST_CYCLE, wsum, std::is_same<T, uint32_t>::value);
     if (r != FA_OK) { cleanup(); cudaStreamSynchronize(st); return r; }
   }
-  fa_status r = solve_g2<T>(ctx, gg, nslots, hbase, links, fdir, tile_acc, xT);
+  fa_status r = solve_g2<T>(ctx, gg, nslots, hbase, links, fdir, tile_acc, xT, tile_f);
   if (r != FA_OK) { cleanup(); return r; }
   CK(cudaEventRecord(ctx->ev[2], st));
   for (auto& s : strips) {
@@ -779,7 +842,7 @@ fa_status run_absorb(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float 
   CK(launch_absorb_graph(st, s.nn, slots, s.node_alpha, s.node_tgt, s.slot_f, s.x_slot, s.slot_root, wv, s.S));
   rt.launches += 2;
   CK(forest_solve_weighted(rt, s.nn, s.parent, wv, s.S));
-  CK(launch_scatter_x_absorb(st, s.nn, s.node_tgt, s.node_alpha, s.S, s.x_slot));
+  CK(launch_scatter_x_absorb(st, s.nn, s.node_tgt, s.node_alpha, s.S, s.x_slot, s.node_flags, false));
   ++rt.launches;
   CK(cudaEventRecord(ctx->ev[2], st));
   CK(launch_retain_absorb(s.g, s.x_slot, s.dirs_in(), acc, alpha, st));
@@ -1222,9 +1285,9 @@ fa_status fa_accumulate_strips(fa_ctx* ctx, int nstrips, int64_t rows, int64_t c
   return accumulate_impl(ctx, rows, cols, dem, nodata, dirs, w, wtype, acc, atype, rec, nstrips);
 }
 
-fa_status fa_accumulate_absorb(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem, float nodata,
-                               const uint8_t* dirs, const void* w, fa_wtype wtype, const float* alpha,
-                               double* acc) {
+fa_status fa_accumulate_absorb(fa_ctx* ctx, int nstrips, int64_t rows, int64_t cols, const float* dem,
+                               float nodata, const uint8_t* dirs, const void* w, fa_wtype wtype,
+                               const float* alpha, double* acc) {
   if (!ctx) return FA_E_ARG;
   ctx->err.clear();
   if (rows <= 0 || cols <= 0) return set_err(ctx, FA_E_ARG, "rows and cols must be > 0");
@@ -1243,9 +1306,18 @@ fa_status fa_accumulate_absorb(fa_ctx* ctx, int64_t rows, int64_t cols, const fl
   const float* d_dem = (const float*)sdem.dev;
   const uint8_t* d_dirs = (const uint8_t*)sdirs.dev;
   const float* d_al = (const float*)sal.dev;
-  fa_status s = wtype == FA_W_NONE
-                    ? run_absorb<0>(ctx, rows, cols, d_dem, nodata, d_dirs, nullptr, d_al, (double*)sacc.dev)
-                    : run_absorb<2>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, d_al, (double*)sacc.dev);
+  fa_status s;
+  if (nstrips > 1) {
+    // the multi-GPU strip pipeline on this device, with weighted tile links
+    Records rec;
+    s = wtype == FA_W_NONE
+            ? run_acc<double, 0>(ctx, rows, cols, d_dem, nodata, d_dirs, nullptr, (double*)sacc.dev, rec, nstrips, d_al)
+            : run_acc<double, 2>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, (double*)sacc.dev, rec, nstrips, d_al);
+  } else {
+    s = wtype == FA_W_NONE
+            ? run_absorb<0>(ctx, rows, cols, d_dem, nodata, d_dirs, nullptr, d_al, (double*)sacc.dev)
+            : run_absorb<2>(ctx, rows, cols, d_dem, nodata, d_dirs, sw.dev, d_al, (double*)sacc.dev);
+  }
   if (s == FA_OK && sacc.owned) CK(cudaMemcpyAsync(acc, sacc.dev, n * 8, cudaMemcpyDeviceToHost, st));
   for (Staged* p : {&sdem, &sdirs, &sw, &sal, &sacc})
     if (p->owned) cudaFreeAsync(p->dev, st);

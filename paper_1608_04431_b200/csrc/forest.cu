@@ -544,4 +544,70 @@ cudaError_t forest_solve_weighted(Runtime& rt, uint32_t n, const uint32_t* paren
   return solve_level<double, true>(rt, n, parent, val, 0, wv);
 }
 
+// roots with path products (absorption): root(v) and prod(v) = the product of
+// the edge weights wv on the path from v up to its root
+namespace {
+__global__ void k_root_init_w(uint32_t n, const uint32_t* __restrict__ parent, const double* __restrict__ wv,
+                              uint32_t* r, double* pr) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const bool top = parent[v] == kNone;
+    r[v] = top ? v : parent[v];
+    pr[v] = top ? 1.0 : wv[v];
+  }
+}
+__global__ void k_root_jump_w(uint32_t n, const uint32_t* __restrict__ in, const double* __restrict__ pin,
+                              uint32_t* out, double* pout, uint32_t* changed) {
+  bool ch = false;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t a = in[v], b = in[a];
+    out[v] = b;
+    pout[v] = a == b ? pin[v] : pin[v] * pin[a];  // the root's own product is 1
+    ch |= a != b;
+  }
+  if (__syncthreads_or(ch) && threadIdx.x == 0) atomicOr(changed, 1u);
+}
+}  // namespace
+
+cudaError_t forest_roots_weighted(Runtime& rt, uint32_t n, const uint32_t* parent, const double* wv,
+                                  uint32_t* root, double* prod) {
+  if (n == 0) return cudaSuccess;
+  cudaStream_t st = rt.st;
+  uint32_t* tmp = rt.alloc<uint32_t>(n);
+  double* ptmp = rt.alloc<double>(n);
+  uint32_t* ctr = rt.alloc<uint32_t>(1);
+  if (rt.err) return rt.err;
+  k_root_init_w<<<grid_for(n), 256, 0, st>>>(n, parent, wv, root, prod);
+  ++rt.launches;
+  uint32_t* a = root;
+  uint32_t* b = tmp;
+  double* pa = prod;
+  double* pb = ptmp;
+  int rounds = 0;
+  for (int batch = 8;; batch = 4) {
+    cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st);
+    for (int j = 0; j < batch; ++j) {
+      k_root_jump_w<<<grid_for(n), 256, 0, st>>>(n, a, pa, b, pb, ctr);
+      std::swap(a, b);
+      std::swap(pa, pb);
+    }
+    rt.launches += batch;
+    rounds += batch;
+    rt.read(ctr, 1);
+    if (!rt.h_cnt[0] || rt.err) break;
+    if (rounds > kMaxJump) {
+      k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);
+      ++rt.launches;
+      break;
+    }
+  }
+  if (a != root) {
+    cudaMemcpyAsync(root, a, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(prod, pa, n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  }
+  rt.free(tmp);
+  rt.free(ptmp);
+  rt.free(ctr);
+  return rt.err ? rt.err : cudaGetLastError();
+}
+
 }  // namespace fa

@@ -40,6 +40,9 @@ template <class T>
 cudaError_t forest_solve(Runtime& rt, uint32_t n, const uint32_t* parent, T* val);
 // absorption: S(v) = val(v) + sum_children wv(c) S(c)
 cudaError_t forest_solve_weighted(Runtime& rt, uint32_t n, const uint32_t* parent, const double* wv, double* val);
+// absorption: roots plus the product of edge weights from each node up to its root
+cudaError_t forest_roots_weighted(Runtime& rt, uint32_t n, const uint32_t* parent, const double* wv,
+                                  uint32_t* root, double* prod);
 
 // root of every node in a forest (pointer jumping); cycles -> ST_CYCLE
 cudaError_t forest_roots(Runtime& rt, uint32_t n, const uint32_t* parent, uint32_t* root);

@@ -68,12 +68,17 @@ __global__ void k_fold_leaves(int64_t nslots, const T* __restrict__ x_slot, cons
 
 // H4 tile perimeter records of one strip: F (direction), L (Alg. 2 link) and
 // A_T (tile-local accumulation, at FlowExternal slots) per tile perimeter slot
-template <class T>
+// absorption (ABS): also tile_f per slot -- a linked slot's factor to its
+// tile exit (alpha product along the in-block path, slot_f, times the
+// product of block-exit edge weights up to the tile root, ptroot), a
+// FlowExternal slot's own alpha (the weight of its edge into the next tile)
+template <class T, bool ABS = false>
 __global__ void k_tile_records(Geom g, int64_t nslots, const int64_t* __restrict__ tbase,
                                const uint8_t* __restrict__ dirs, const uint32_t* __restrict__ slot_root,
                                const uint32_t* __restrict__ troot, const uint8_t* __restrict__ flags,
                                const uint32_t* __restrict__ node_slot, const T* __restrict__ S1,
-                               uint32_t* links, uint8_t* fdir, T* tile_acc) {
+                               uint32_t* links, uint8_t* fdir, T* tile_acc, const T* __restrict__ slot_f,
+                               const T* __restrict__ ptroot, const float* __restrict__ alpha, T* tile_f) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots;
        s += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = tile_of_slot(tbase, g.TR * g.TC, s), p = s - tbase[t];
@@ -90,12 +95,14 @@ __global__ void k_tile_records(Geom g, int64_t nslots, const int64_t* __restrict
     const int64_t bslot = b * g.pb + perim_index(lx, ly, bh, bw);
     uint32_t L = kFlowTerminates;  // Alg. 2: NoData / NoFlow / path ends inside
     T at = (T)0;
+    T tf = (T)0;
     if (d >= 1 && d <= 8) {
       const int64_t ny = py + dir_dy(d), nx = px + dir_dx(d);
       const uint32_t e = slot_root[bslot];
       if (ny < 0 || nx < 0 || ny >= th || nx >= tw) {
         L = kFlowExternal;  // "c_n is outside the tile" and c = c0 (D22)
         if (e != kNone) at = S1[e];  // the cell is its own block exit
+        if (ABS) tf = (T)alpha[gy * g.W + gx];
       } else if (e != kNone) {
         const uint32_t r = troot[e];
         if (flags[r] & NF_OUT_TILE) {  // the path leaves the tile at exit r
@@ -107,12 +114,14 @@ __global__ void k_tile_records(Geom g, int64_t nslots, const int64_t* __restrict
           int64_t rx, ryy;
           perim_xy(rp, rh, rw, rx, ryy);
           L = (uint32_t)perim_index(rx0 + rx - tx0, ry0 + ryy - ty0, th, tw);
+          if (ABS) tf = slot_f[bslot] * ptroot[e];
         }
       }
     }
     links[s] = L;
     fdir[s] = d;
     tile_acc[s] = at;
+    if (ABS) tile_f[s] = tf;
   }
 }
 
@@ -121,10 +130,11 @@ __global__ void k_tile_records(Geom g, int64_t nslots, const int64_t* __restrict
 // tile's perimeter cell (edges or corners) unless that is NoData or off the
 // DEM; a linked slot drains into its exit; the value is A_T at FlowExternal
 // slots and 0 elsewhere ("set to A = 0").
-template <class T>
+template <class T, bool ABS = false>
 __global__ void k_g2_slots(Geom gg, int64_t nslots, const int64_t* __restrict__ tbase,
                            const uint32_t* __restrict__ links, const uint8_t* __restrict__ fdir,
-                           const T* __restrict__ tile_acc, uint32_t* parent, T* val) {
+                           const T* __restrict__ tile_acc, uint32_t* parent, T* val,
+                           const T* __restrict__ tile_f, T* wv2) {
   const int64_t ntiles = gg.TR * gg.TC;
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots;
        s += (int64_t)gridDim.x * blockDim.x) {
@@ -152,26 +162,27 @@ __global__ void k_g2_slots(Geom gg, int64_t nslots, const int64_t* __restrict__ 
     }
     parent[s] = par;
     val[s] = v;
+    if (ABS) wv2[s] = par == kNone ? (T)0 : tile_f[s];  // absorption: alpha (external) or path factor (linked)
   }
 }
 
 // offsets x_T(u) = sum of S over FlowExternal slots draining into u (a_in)
-template <class T>
+template <class T, bool ABS = false>
 __global__ void k_xT(int64_t nslots, const uint32_t* __restrict__ parent, const uint32_t* __restrict__ links,
-                     const T* __restrict__ S2, T* xT) {
+                     const T* __restrict__ S2, T* xT, const T* __restrict__ tile_f) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots;
        s += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t u = parent[s];
-    if (u != kNone && links[s] == kFlowExternal) atomic_add(&xT[u], S2[s]);
+    if (u != kNone && links[s] == kFlowExternal) atomic_add(&xT[u], ABS ? S2[s] * tile_f[s] : S2[s]);
   }
 }
 
 // inject the offsets of a strip's tile slots: into pass 2 at the entry cell,
 // and into the tile-cut block-exit graph at the exit its in-block path reaches
-template <class T>
+template <class T, bool ABS = false>
 __global__ void k_inject_slots(Geom g, int64_t nslots, const int64_t* __restrict__ tbase,
                                const T* __restrict__ xT, const uint32_t* __restrict__ slot_root, T* val1,
-                               T* x_slot) {
+                               T* x_slot, const T* __restrict__ slot_f) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslots;
        s += (int64_t)gridDim.x * blockDim.x) {
     const T x = xT[s];
@@ -188,7 +199,7 @@ __global__ void k_inject_slots(Geom g, int64_t nslots, const int64_t* __restrict
     const int64_t bslot = b * g.pb + perim_index(lx, ly, bh, bw);
     atomic_add(&x_slot[bslot], x);
     const uint32_t e = slot_root[bslot];
-    if (e != kNone) atomic_add(&val1[e], x);
+    if (e != kNone) atomic_add(&val1[e], ABS ? x * slot_f[bslot] : x);  // reaches the block exit scaled by f
   }
 }
 
@@ -221,35 +232,51 @@ template <class T>
 cudaError_t launch_tile_records(cudaStream_t st, const Geom& g, int64_t nslots, const int64_t* tbase,
                                 const uint8_t* dirs, const uint32_t* slot_root, const uint32_t* troot,
                                 const uint8_t* flags, const uint32_t* node_slot, const T* S1,
-                                uint32_t* links, uint8_t* fdir, T* tile_acc) {
+                                uint32_t* links, uint8_t* fdir, T* tile_acc, const T* slot_f, const T* ptroot,
+                                const float* alpha, T* tile_f) {
   if (nslots <= 0) return cudaSuccess;
-  k_tile_records<T><<<grid_for(nslots), 256, 0, st>>>(g, nslots, tbase, dirs, slot_root, troot, flags,
-                                                       node_slot, S1, links, fdir, tile_acc);
+  if (tile_f)
+    k_tile_records<T, true><<<grid_for(nslots), 256, 0, st>>>(g, nslots, tbase, dirs, slot_root, troot, flags,
+                                                               node_slot, S1, links, fdir, tile_acc, slot_f,
+                                                               ptroot, alpha, tile_f);
+  else
+    k_tile_records<T><<<grid_for(nslots), 256, 0, st>>>(g, nslots, tbase, dirs, slot_root, troot, flags,
+                                                         node_slot, S1, links, fdir, tile_acc, nullptr, nullptr,
+                                                         nullptr, nullptr);
   return cudaGetLastError();
 }
 
 template <class T>
 cudaError_t launch_g2_slots(cudaStream_t st, const Geom& gg, int64_t nslots, const int64_t* tbase,
                             const uint32_t* links, const uint8_t* fdir, const T* tile_acc, uint32_t* parent,
-                            T* val) {
+                            T* val, const T* tile_f, T* wv2) {
   if (nslots <= 0) return cudaSuccess;
-  k_g2_slots<T><<<grid_for(nslots), 256, 0, st>>>(gg, nslots, tbase, links, fdir, tile_acc, parent, val);
+  if (tile_f)
+    k_g2_slots<T, true><<<grid_for(nslots), 256, 0, st>>>(gg, nslots, tbase, links, fdir, tile_acc, parent, val,
+                                                           tile_f, wv2);
+  else
+    k_g2_slots<T><<<grid_for(nslots), 256, 0, st>>>(gg, nslots, tbase, links, fdir, tile_acc, parent, val,
+                                                     nullptr, nullptr);
   return cudaGetLastError();
 }
 
 template <class T>
 cudaError_t launch_xT(cudaStream_t st, int64_t nslots, const uint32_t* parent, const uint32_t* links,
-                      const T* S2, T* xT) {
+                      const T* S2, T* xT, const T* tile_f) {
   if (nslots <= 0) return cudaSuccess;
-  k_xT<T><<<grid_for(nslots), 256, 0, st>>>(nslots, parent, links, S2, xT);
+  if (tile_f) k_xT<T, true><<<grid_for(nslots), 256, 0, st>>>(nslots, parent, links, S2, xT, tile_f);
+  else k_xT<T><<<grid_for(nslots), 256, 0, st>>>(nslots, parent, links, S2, xT, nullptr);
   return cudaGetLastError();
 }
 
 template <class T>
 cudaError_t launch_inject_slots(cudaStream_t st, const Geom& g, int64_t nslots, const int64_t* tbase,
-                                const T* xT, const uint32_t* slot_root, T* val1, T* x_slot) {
+                                const T* xT, const uint32_t* slot_root, T* val1, T* x_slot, const T* slot_f) {
   if (nslots <= 0) return cudaSuccess;
-  k_inject_slots<T><<<grid_for(nslots), 256, 0, st>>>(g, nslots, tbase, xT, slot_root, val1, x_slot);
+  if (slot_f)
+    k_inject_slots<T, true><<<grid_for(nslots), 256, 0, st>>>(g, nslots, tbase, xT, slot_root, val1, x_slot, slot_f);
+  else
+    k_inject_slots<T><<<grid_for(nslots), 256, 0, st>>>(g, nslots, tbase, xT, slot_root, val1, x_slot, nullptr);
   return cudaGetLastError();
 }
 
@@ -259,13 +286,14 @@ cudaError_t launch_inject_slots(cudaStream_t st, const Geom& g, int64_t nslots, 
   template cudaError_t launch_tile_records<T>(cudaStream_t, const Geom&, int64_t, const int64_t*,   \
                                               const uint8_t*, const uint32_t*, const uint32_t*,     \
                                               const uint8_t*, const uint32_t*, const T*, uint32_t*, \
-                                              uint8_t*, T*);                                        \
+                                              uint8_t*, T*, const T*, const T*, const float*, T*);  \
   template cudaError_t launch_g2_slots<T>(cudaStream_t, const Geom&, int64_t, const int64_t*,       \
-                                          const uint32_t*, const uint8_t*, const T*, uint32_t*, T*); \
+                                          const uint32_t*, const uint8_t*, const T*, uint32_t*, T*,  \
+                                          const T*, T*);                                            \
   template cudaError_t launch_xT<T>(cudaStream_t, int64_t, const uint32_t*, const uint32_t*, const T*, \
-                                    T*);                                                            \
+                                    T*, const T*);                                                  \
   template cudaError_t launch_inject_slots<T>(cudaStream_t, const Geom&, int64_t, const int64_t*,   \
-                                              const T*, const uint32_t*, T*, T*);
+                                              const T*, const uint32_t*, T*, T*, const T*);
 FA_INST(uint32_t)
 FA_INST(unsigned long long)
 FA_INST(double)
@@ -298,10 +326,11 @@ __global__ void k_fold_leaves_w(int64_t nslots, const double* __restrict__ x_slo
 }
 // offsets at entry slots from the finished exits: alpha(v) S(v)
 __global__ void k_scatter_x_w(uint32_t nn, const uint32_t* __restrict__ tgt, const float* __restrict__ node_alpha,
-                              const double* __restrict__ S, double* x_slot) {
+                              const double* __restrict__ S, double* x_slot, const uint8_t* __restrict__ flags,
+                              bool intra_tile) {
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += gridDim.x * blockDim.x) {
     const uint32_t t = tgt[v];
-    if (t != kNone) atomic_add(&x_slot[t], (double)node_alpha[v] * S[v]);
+    if (t != kNone && !(intra_tile && (flags[v] & NF_OUT_TILE))) atomic_add(&x_slot[t], (double)node_alpha[v] * S[v]);
   }
 }
 
@@ -312,9 +341,18 @@ cudaError_t launch_absorb_graph(cudaStream_t st, uint32_t nn, int64_t nslots, co
   k_fold_leaves_w<<<grid_for(nslots), 256, 0, st>>>(nslots, x_slot, slot_root, slot_f, S);
   return cudaGetLastError();
 }
+// tile-cut graphs: edges leaving a tile are not edges of the strip graph
+__global__ void k_g1_weights_cut(uint32_t nn, const uint8_t* __restrict__ flags, double* wv) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += gridDim.x * blockDim.x)
+    if (flags[v] & NF_OUT_TILE) wv[v] = 0.0;
+}
+cudaError_t launch_g1_weights_cut(cudaStream_t st, uint32_t nn, const uint8_t* flags, double* wv) {
+  k_g1_weights_cut<<<grid_for(nn), 256, 0, st>>>(nn, flags, wv);
+  return cudaGetLastError();
+}
 cudaError_t launch_scatter_x_absorb(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const float* node_alpha,
-                                    const double* S, double* x_slot) {
-  k_scatter_x_w<<<grid_for(nn), 256, 0, st>>>(nn, tgt, node_alpha, S, x_slot);
+                                    const double* S, double* x_slot, const uint8_t* flags, bool intra_tile) {
+  k_scatter_x_w<<<grid_for(nn), 256, 0, st>>>(nn, tgt, node_alpha, S, x_slot, flags, intra_tile);
   return cudaGetLastError();
 }
 

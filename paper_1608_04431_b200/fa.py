@@ -79,7 +79,7 @@ def load() -> ctypes.CDLL:
     lib.fa_accumulate.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int]
     lib.fa_accumulate_strips.argtypes = [P, ctypes.c_int, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int]
     lib.fa_accumulate_streamed.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int, I]
-    lib.fa_accumulate_absorb.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, P]
+    lib.fa_accumulate_absorb.argtypes = [P, ctypes.c_int, I, I, P, F, P, P, ctypes.c_int, P, P]
     lib.fa_perimeter_slots.argtypes = [P, I, I]
     lib.fa_perimeter_slots.restype = I
     lib.fa_perimeter_records.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, ctypes.c_int, P, P, P, P]
@@ -214,7 +214,8 @@ class Context:
                                                     _ptr(w), _wtype(w), _ptr(out), a, int(strip_rows)))
         return out
 
-    def accumulate_absorb(self, alpha, dem=None, dirs=None, w=None, nodata: float = -9999.0, out=None):
+    def accumulate_absorb(self, alpha, dem=None, dirs=None, w=None, nodata: float = -9999.0, out=None,
+                          nstrips: int = 1):
         """Absorption (N3): A(p) = w(p) + sum alpha(n) A(n) over donors n; f64 output.
         alpha: f32 raster in [0,1] (device or host, like the other inputs)."""
         src = dem if dem is not None else dirs
@@ -226,7 +227,8 @@ class Context:
                 import numpy as np
 
                 out = np.empty((rows, cols), np.float64)
-        self._check(self.lib.fa_accumulate_absorb(self.h, rows, cols, _ptr(dem), float(nodata), _ptr(dirs),
+        self._check(self.lib.fa_accumulate_absorb(self.h, int(nstrips), rows, cols, _ptr(dem), float(nodata),
+                                                  _ptr(dirs),
                                                   _ptr(w), _wtype(w), _ptr(alpha), _ptr(out)))
         return out
 

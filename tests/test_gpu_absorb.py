@@ -96,3 +96,33 @@ def test_absorb_weighted_contraction(fa_lib, cap, monkeypatch):
         gr = ctx.accumulate_absorb(_cuda(ar), dirs=_cuda(r), w=_cuda(w)).cpu().numpy()
     _check(got, d, oracle.accumulate_alpha(d, al))
     _check(gr, r, oracle.accumulate_alpha(r, ar, w))
+
+
+@pytest.mark.parametrize("seed,H,W,tile,G", [(1, 300, 257, (64, 64), 2), (2, 300, 257, (64, 96), 5),
+                                             (3, 129, 333, (32, 64), 4), (4, 513, 200, (96, 64), 3)])
+def test_absorb_strips_random_dirs(fa_lib, seed, H, W, tile, G):
+    """The multi-GPU strip pipeline with weighted tile links: tile records
+    carry each slot's alpha path factor, G2 and the offsets are weighted."""
+    rng = np.random.default_rng(seed)
+    d = inputs.random_dirs(seed, H, W, p_nodata=0.12, p_noflow=0.02)
+    al = rng.random((H, W)).astype(np.float32)
+    al[rng.random((H, W)) < 0.3] = 1.0
+    w = inputs.weights_f32(seed, (H, W))
+    with fa_lib.Context(0, tile=tile) as ctx:
+        got = ctx.accumulate_absorb(_cuda(al), dirs=_cuda(d), w=_cuda(w), nstrips=G).cpu().numpy()
+    _check(got, d, oracle.accumulate_alpha(d, al, w))
+
+
+def test_absorb_strips_dem_and_serpentine(fa_lib):
+    cfg = inputs.make_config("cfg3", 1024, 1024)
+    d = oracle.d8(cfg.dem)
+    rng = np.random.default_rng(3)
+    al = (0.9 + 0.1 * rng.random(d.shape)).astype(np.float32)
+    s = inputs.serpentine(512, 384, transposed=True)
+    als = (0.999 + 0.001 * rng.random(s.shape)).astype(np.float32)
+    with fa_lib.Context(0, tile=(256, 256)) as ctx:
+        got = ctx.accumulate_absorb(_cuda(al), dem=_cuda(cfg.dem), w=_cuda(cfg.w), nstrips=4).cpu().numpy()
+    with fa_lib.Context(0, tile=(64, 64)) as ctx:
+        gs = ctx.accumulate_absorb(_cuda(als), dirs=_cuda(s), nstrips=8).cpu().numpy()
+    _check(got, d, oracle.accumulate_alpha(d, al, cfg.w))
+    _check(gs, s, oracle.accumulate_alpha(s, als))
