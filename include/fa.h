@@ -177,6 +177,16 @@ FA_API fa_status fa_accumulate_dist(fa_ctx* ctx, const void* nccl_id128, int ran
                              const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc,
                              fa_atype atype);
 
+/* fa_accumulate_dist with absorption (N3, see fa_accumulate_absorb): alpha
+ * is the rank's strip (device buffer, f32 in [0,1]), output f64, w none or
+ * f32.  The tile records all-gather also carries each slot's alpha path
+ * factor; collective like fa_accumulate_dist. */
+FA_API fa_status fa_accumulate_absorb_dist(fa_ctx* ctx, const void* nccl_id128, int rank, int nranks,
+                                           int64_t global_rows, int64_t cols, int64_t row_begin,
+                                           int64_t local_rows, const float* dem, float nodata,
+                                           const uint8_t* dirs, const void* w, fa_wtype wtype,
+                                           const float* alpha, double* acc);
+
 /* Per-phase statistics of the last call (device-timed with CUDA events). */
 typedef struct {
   double ms_total, ms_pass1, ms_graph, ms_pass2, ms_exchange;

@@ -1060,7 +1060,8 @@ ncclDataType_t nccl_type() {
 
 template <class T, int WK>
 fa_status run_dist(fa_ctx* ctx, int64_t GH, int64_t W, int64_t row_begin, int64_t H, const float* dem,
-                   float nodata, const uint8_t* dirs, const void* w, T* acc) {
+                   float nodata, const uint8_t* dirs, const void* w, T* acc,
+                   const float* alpha = nullptr) {
   using namespace fa;
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
@@ -1104,6 +1105,7 @@ fa_status run_dist(fa_ctx* ctx, int64_t GH, int64_t W, int64_t row_begin, int64_
   uint8_t* fdir = rt.alloc<uint8_t>(nslots);
   T* tile_acc = rt.alloc<T>(nslots);
   T* xT = rt.alloc<T>(nslots);
+  T* tile_f = alpha ? rt.alloc<T>(nslots) : nullptr;  // absorption: path factors per tile slot
   if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
   Strip<T> s;
   s.g = make_geom(H, W, gg.TH, gg.TW);
@@ -1124,12 +1126,13 @@ fa_status run_dist(fa_ctx* ctx, int64_t GH, int64_t W, int64_t row_begin, int64_
   s.w = w;
   s.acc = acc;
   s.slot0 = hbase[(row_begin / gg.TH) * gg.TC];
+  s.alpha = alpha;
   auto cleanup = [&]() {
     s.release(rt);
-    for (void* p : {(void*)links, (void*)fdir, (void*)tile_acc, (void*)xT, up, dn}) rt.free(p);
+    for (void* p : {(void*)links, (void*)fdir, (void*)tile_acc, (void*)xT, (void*)tile_f, up, dn}) rt.free(p);
   };
   fa_status r = strip_pass1<T, WK>(ctx, s, true);
-  if (r == FA_OK) r = strip_records<T>(ctx, s, links, fdir, tile_acc);
+  if (r == FA_OK) r = strip_records<T>(ctx, s, links, fdir, tile_acc, tile_f);
   if (r != FA_OK) { cleanup(); return r; }
   CK(cudaEventRecord(ctx->ev[1], st));
   // ---- C3 status all-reduce (max) + C2 exchange of the tile records
@@ -1155,6 +1158,7 @@ fa_status run_dist(fa_ctx* ctx, int64_t GH, int64_t W, int64_t row_begin, int64_
     NK(N.broadcast(links + s0[q], links + s0[q], cnt, ncclUint32, q, ctx->comm, st));
     NK(N.broadcast(fdir + s0[q], fdir + s0[q], cnt, ncclUint8, q, ctx->comm, st));
     NK(N.broadcast(tile_acc + s0[q], tile_acc + s0[q], cnt, nccl_type<T>(), q, ctx->comm, st));
+    if (tile_f) NK(N.broadcast(tile_f + s0[q], tile_f + s0[q], cnt, nccl_type<T>(), q, ctx->comm, st));
   }
   NK(N.groupEnd());
   CK(cudaEventRecord(ex1, st));
@@ -1162,7 +1166,7 @@ fa_status run_dist(fa_ctx* ctx, int64_t GH, int64_t W, int64_t row_begin, int64_
   r = check_status(ctx, rt.h_cnt[0] & ~ST_CYCLE, 0, false);
   if (r != FA_OK) { cleanup(); return r; }
   // ---- phase B: global graph redundantly on every rank, then this strip
-  r = solve_g2<T>(ctx, gg, nslots, hbase, links, fdir, tile_acc, xT);
+  r = solve_g2<T>(ctx, gg, nslots, hbase, links, fdir, tile_acc, xT, tile_f);
   if (r == FA_OK) {
     CK(cudaEventRecord(ctx->ev[2], st));
     r = strip_finish<T, WK>(ctx, s, xT);
@@ -1178,12 +1182,19 @@ fa_status run_dist(fa_ctx* ctx, int64_t GH, int64_t W, int64_t row_begin, int64_
   cudaEventDestroy(ex0);
   cudaEventDestroy(ex1);
   ctx->stats.ms_exchange = exm;
-  ctx->stats.bytes_exchanged = (int64_t)(nslots * (4 + 1 + sizeof(T)) + 2 * nh * W * esz);
+  ctx->stats.bytes_exchanged = (int64_t)(nslots * (4 + 1 + sizeof(T) * (tile_f ? 2 : 1)) + 2 * nh * W * esz);
   if (r != FA_OK) return r;
   record_stats(ctx, H * W, s.g.nblocks, s.nn, nslots);
   return FA_OK;
 }
 
+}  // namespace
+
+namespace {
+fa_status dist_impl(fa_ctx* ctx, const void* nccl_id128, int rank, int nranks, int64_t global_rows,
+                    int64_t cols, int64_t row_begin, int64_t local_rows, const float* dem, float nodata,
+                    const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc, fa_atype atype,
+                    const float* alpha);
 }  // namespace
 
 extern "C" {
@@ -1382,9 +1393,31 @@ fa_status fa_nccl_unique_id(void* out128) {
   return FA_OK;
 }
 
+fa_status fa_accumulate_absorb_dist(fa_ctx* ctx, const void* nccl_id128, int rank, int nranks,
+                                    int64_t global_rows, int64_t cols, int64_t row_begin, int64_t local_rows,
+                                    const float* dem, float nodata, const uint8_t* dirs, const void* w,
+                                    fa_wtype wtype, const float* alpha, double* acc) {
+  if (!ctx) return FA_E_ARG;
+  if (!alpha || !is_device_ptr(alpha)) return set_err(ctx, FA_E_ARG, "alpha must be a device buffer");
+  if (wtype == FA_W_U32) return set_err(ctx, FA_E_ARG, "absorption takes f32 weights or none (f64 output)");
+  return dist_impl(ctx, nccl_id128, rank, nranks, global_rows, cols, row_begin, local_rows, dem, nodata, dirs, w,
+                   wtype, acc, FA_A_F64, alpha);
+}
+
 fa_status fa_accumulate_dist(fa_ctx* ctx, const void* nccl_id128, int rank, int nranks, int64_t global_rows,
                              int64_t cols, int64_t row_begin, int64_t local_rows, const float* dem, float nodata,
                              const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc, fa_atype atype) {
+  return dist_impl(ctx, nccl_id128, rank, nranks, global_rows, cols, row_begin, local_rows, dem, nodata, dirs, w,
+                   wtype, acc, atype, nullptr);
+}
+
+}  // extern "C"
+
+namespace {
+fa_status dist_impl(fa_ctx* ctx, const void* nccl_id128, int rank, int nranks, int64_t global_rows,
+                    int64_t cols, int64_t row_begin, int64_t local_rows, const float* dem, float nodata,
+                    const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc, fa_atype atype,
+                    const float* alpha) {
   if (!ctx) return FA_E_ARG;
   ctx->err.clear();
   if (!nccl_id128 || nranks < 1 || rank < 0 || rank >= nranks || global_rows <= 0 || cols <= 0 ||
@@ -1417,12 +1450,11 @@ fa_status fa_accumulate_dist(fa_ctx* ctx, const void* nccl_id128, int rank, int 
     s = wtype == FA_W_NONE ? run_dist<U, 0>(ctx, global_rows, cols, row_begin, local_rows, dem, nodata, dirs, w, (U*)acc)
                            : run_dist<U, 1>(ctx, global_rows, cols, row_begin, local_rows, dem, nodata, dirs, w, (U*)acc);
   } else {
-    s = wtype == FA_W_NONE ? run_dist<double, 0>(ctx, global_rows, cols, row_begin, local_rows, dem, nodata, dirs, w, (double*)acc)
-                           : run_dist<double, 2>(ctx, global_rows, cols, row_begin, local_rows, dem, nodata, dirs, w, (double*)acc);
+    s = wtype == FA_W_NONE ? run_dist<double, 0>(ctx, global_rows, cols, row_begin, local_rows, dem, nodata, dirs, w, (double*)acc, alpha)
+                           : run_dist<double, 2>(ctx, global_rows, cols, row_begin, local_rows, dem, nodata, dirs, w, (double*)acc, alpha);
   }
   cudaError_t e = cudaStreamSynchronize(ctx->st);
   if (s == FA_OK && e != cudaSuccess) return set_err(ctx, FA_E_CUDA, std::string("stream: ") + cudaGetErrorString(e));
   return s;
 }
-
-}  // extern "C"
+}  // namespace

@@ -27,7 +27,7 @@ FLOW_TERMINATES = 0xFFFFFFFF
 EXPORTS = ["fa_create", "fa_destroy", "fa_last_error", "fa_flowdirs", "fa_accumulate",
            "fa_accumulate_strips", "fa_perimeter_slots", "fa_perimeter_records", "fa_nccl_unique_id",
            "fa_accumulate_dist", "fa_get_stats", "fa_accumulate_streamed",
-           "fa_accumulate_absorb"]
+           "fa_accumulate_absorb", "fa_accumulate_absorb_dist"]
 
 
 def nccl_unique_id() -> bytes:
@@ -80,6 +80,8 @@ def load() -> ctypes.CDLL:
     lib.fa_accumulate_strips.argtypes = [P, ctypes.c_int, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int]
     lib.fa_accumulate_streamed.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int, I]
     lib.fa_accumulate_absorb.argtypes = [P, ctypes.c_int, I, I, P, F, P, P, ctypes.c_int, P, P]
+    lib.fa_accumulate_absorb_dist.argtypes = [P, P, ctypes.c_int, ctypes.c_int, I, I, I, I, P, F, P, P,
+                                              ctypes.c_int, P, P]
     lib.fa_perimeter_slots.argtypes = [P, I, I]
     lib.fa_perimeter_slots.restype = I
     lib.fa_perimeter_records.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, ctypes.c_int, P, P, P, P]
@@ -244,6 +246,19 @@ class Context:
         self._check(self.lib.fa_accumulate_dist(self.h, buf, rank, nranks, global_rows, cols, row_begin, rows,
                                                 _ptr(dem), float(nodata), _ptr(dirs), _ptr(w), _wtype(w),
                                                 _ptr(out), a))
+        return out
+
+    def accumulate_absorb_dist(self, nccl_id: bytes, rank: int, nranks: int, global_rows: int, row_begin: int,
+                               alpha, dem=None, dirs=None, w=None, nodata: float = -9999.0, out=None):
+        """One rank's strip of the multi-GPU absorption accumulation (collective; f64 output)."""
+        src = dem if dem is not None else dirs
+        rows, cols = src.shape
+        if out is None:
+            out = torch.empty((rows, cols), dtype=torch.float64, device=src.device)
+        buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+        self._check(self.lib.fa_accumulate_absorb_dist(self.h, buf, rank, nranks, global_rows, cols, row_begin,
+                                                       rows, _ptr(dem), float(nodata), _ptr(dirs), _ptr(w),
+                                                       _wtype(w), _ptr(alpha), _ptr(out)))
         return out
 
     def perimeter_slots(self, rows: int, cols: int) -> int:

@@ -126,3 +126,19 @@ def test_absorb_strips_dem_and_serpentine(fa_lib):
         gs = ctx.accumulate_absorb(_cuda(als), dirs=_cuda(s), nstrips=8).cpu().numpy()
     _check(got, d, oracle.accumulate_alpha(d, al, cfg.w))
     _check(gs, s, oracle.accumulate_alpha(s, als))
+
+
+def test_absorb_dist_single_rank_nccl(fa_lib):
+    """fa_accumulate_absorb_dist (NCCL, one rank): the records all-gather
+    carries the alpha path factors; same result as the oracle."""
+    cfg = inputs.make_config("cfg3", 1024, 1024)
+    d = oracle.d8(cfg.dem)
+    rng = np.random.default_rng(13)
+    al = (0.9 + 0.1 * rng.random(d.shape)).astype(np.float32)
+    nid = fa_lib.nccl_unique_id()
+    with fa_lib.Context(0, tile=(256, 256)) as ctx:
+        got = ctx.accumulate_absorb_dist(nid, 0, 1, 1024, 0, _cuda(al), dem=_cuda(cfg.dem),
+                                         w=_cuda(cfg.w)).cpu().numpy()
+        st = ctx.stats()
+    _check(got, d, oracle.accumulate_alpha(d, al, cfg.w))
+    assert st["bytes_exchanged"] > 0
