@@ -139,6 +139,14 @@ FA_API fa_status fa_accumulate_streamed(fa_ctx* ctx, int64_t rows, int64_t cols,
                                         fa_wtype wtype, void* acc, fa_atype atype,
                                         int64_t strip_rows);
 
+/* fa_accumulate_streamed with absorption (N3, see fa_accumulate_absorb):
+ * alpha is a HOST buffer streamed with the strips (4 more bytes per cell and
+ * pass); output f64, w none or f32. */
+FA_API fa_status fa_accumulate_absorb_streamed(fa_ctx* ctx, int64_t rows, int64_t cols,
+                                               const float* dem, float nodata, const uint8_t* dirs,
+                                               const void* w, fa_wtype wtype, const float* alpha,
+                                               double* acc, int64_t strip_rows);
+
 /* H4/H5 intermediates for tests and tools: number of tile perimeter slots
  * for a rows x cols raster under the context's tiling (tiles row-major,
  * slots per tile in clockwise perimeter order from the tile's top-left,

@@ -872,7 +872,8 @@ fa_status run_absorb(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float 
 // download of strip i-1 (another: PCIe is full duplex) overlap strip i.
 template <class T, int WK>
 fa_status run_streamed(fa_ctx* ctx, int64_t H, int64_t W, const float* dem_h, float nodata,
-                       const uint8_t* dirs_h, const void* w_h, T* acc_h, int64_t strip_rows) {
+                       const uint8_t* dirs_h, const void* w_h, T* acc_h, int64_t strip_rows,
+                       const float* alpha_h = nullptr) {
   using namespace fa;
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
@@ -911,6 +912,8 @@ fa_status run_streamed(fa_ctx* ctx, int64_t H, int64_t W, const float* dem_h, fl
   uint8_t* fdir = rt.alloc<uint8_t>(nslots);
   T* tile_acc = rt.alloc<T>(nslots);
   T* xT = rt.alloc<T>(nslots);
+  T* tile_f = alpha_h ? rt.alloc<T>(nslots) : nullptr;  // absorption: path factors per tile slot
+  float* alb[2] = {nullptr, nullptr};                     // absorption: alpha strips
   float* zb[2] = {nullptr, nullptr};
   uint8_t* db[2] = {nullptr, nullptr};
   float* wb[2] = {nullptr, nullptr};
@@ -920,13 +923,15 @@ fa_status run_streamed(fa_ctx* ctx, int64_t H, int64_t W, const float* dem_h, fl
     if (dem_h) zb[b] = rt.alloc<float>((size_t)((SRr + 4) * W));
     else db[b] = rt.alloc<uint8_t>((size_t)((SRr + 2) * W));
     if (hasw) wb[b] = rt.alloc<float>((size_t)(SRr * W));
+    if (alpha_h) alb[b] = rt.alloc<float>((size_t)(SRr * W));
     ab[b] = rt.alloc<T>((size_t)(SRr * W));
   }
   auto cleanup = [&]() {
     cudaStreamSynchronize(cs);
     cudaStreamSynchronize(ctx->cs_out);
     for (void* p : {(void*)links, (void*)fdir, (void*)tile_acc, (void*)xT, (void*)zb[0], (void*)zb[1], (void*)db[0],
-                    (void*)db[1], (void*)wb[0], (void*)wb[1], (void*)ab[0], (void*)ab[1]})
+                    (void*)db[1], (void*)wb[0], (void*)wb[1], (void*)ab[0], (void*)ab[1], (void*)tile_f,
+                    (void*)alb[0], (void*)alb[1]})
       rt.free(p);
   };
   if (rt.err) { cleanup(); return set_err(ctx, FA_E_NOMEM, "device allocation failed (lower strip_rows)"); }
@@ -952,6 +957,8 @@ fa_status run_streamed(fa_ctx* ctx, int64_t H, int64_t W, const float* dem_h, fl
     if (hasw)
       CK(cudaMemcpyAsync(wb[b], static_cast<const float*>(w_h) + r0 * W, (size_t)((r1 - r0) * W) * 4,
                          cudaMemcpyHostToDevice, cs));
+    if (alpha_h)
+      CK(cudaMemcpyAsync(alb[b], alpha_h + r0 * W, (size_t)((r1 - r0) * W) * 4, cudaMemcpyHostToDevice, cs));
     CK(cudaEventRecord(ctx->ev_in[b], cs));
     return FA_OK;
   };
@@ -977,6 +984,7 @@ fa_status run_streamed(fa_ctx* ctx, int64_t H, int64_t W, const float* dem_h, fl
       s.dirs_dn = r1 < H ? d + h * W : nullptr;
     }
     s.w = hasw ? wb[b] : nullptr;
+    s.alpha = alpha_h ? alb[b] : nullptr;
     s.acc = ab[b];  // pass 1 accumulates in place (phase A: scratch)
     s.slot0 = hbase[(r0 / gg.TH) * gg.TC];
   };
@@ -990,7 +998,7 @@ fa_status run_streamed(fa_ctx* ctx, int64_t H, int64_t W, const float* dem_h, fl
     Strip<T> s;
     make_strip(i, b, s);
     fa_status r = strip_pass1<T, WK>(ctx, s, true);
-    if (r == FA_OK) r = strip_records<T>(ctx, s, links, fdir, tile_acc);
+    if (r == FA_OK) r = strip_records<T>(ctx, s, links, fdir, tile_acc, tile_f);
     blocks += s.g.nblocks;
     nodes += s.nn;
     s.release(rt);
@@ -1005,7 +1013,7 @@ fa_status run_streamed(fa_ctx* ctx, int64_t H, int64_t W, const float* dem_h, fl
     fa_status r = check_status(ctx, rt.h_cnt[0] & ~ST_CYCLE, wsum, std::is_same<T, uint32_t>::value);
     if (r != FA_OK) { cleanup(); cudaStreamSynchronize(st); return r; }
   }
-  fa_status r = solve_g2<T>(ctx, gg, nslots, hbase, links, fdir, tile_acc, xT);
+  fa_status r = solve_g2<T>(ctx, gg, nslots, hbase, links, fdir, tile_acc, xT, tile_f);
   if (r != FA_OK) { cleanup(); return r; }
   CK(cudaEventRecord(ctx->ev[2], st));
   // ---- phase B
@@ -1047,7 +1055,8 @@ fa_status run_streamed(fa_ctx* ctx, int64_t H, int64_t W, const float* dem_h, fl
   r = check_status(ctx, rt.h_cnt[0], 0, false);
   if (r != FA_OK) return r;
   record_stats(ctx, H * W, blocks, nodes, nslots);
-  ctx->stats.bytes_exchanged = (int64_t)(2 * H * W * ((dem_h ? 4 : 1) + (hasw ? 4 : 0)) + H * W * (int64_t)sizeof(T));
+  ctx->stats.bytes_exchanged =
+      (int64_t)(2 * H * W * ((dem_h ? 4 : 1) + (hasw ? 4 : 0) + (alpha_h ? 4 : 0)) + H * W * (int64_t)sizeof(T));
   CK(cudaStreamSynchronize(st));
   return FA_OK;
 }
@@ -1335,6 +1344,22 @@ fa_status fa_accumulate_absorb(fa_ctx* ctx, int nstrips, int64_t rows, int64_t c
   cudaError_t e = cudaStreamSynchronize(st);
   if (s == FA_OK && e != cudaSuccess) return set_err(ctx, FA_E_CUDA, std::string("stream: ") + cudaGetErrorString(e));
   return s;
+}
+
+fa_status fa_accumulate_absorb_streamed(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem,
+                                        float nodata, const uint8_t* dirs, const void* w, fa_wtype wtype,
+                                        const float* alpha, double* acc, int64_t strip_rows) {
+  if (!ctx) return FA_E_ARG;
+  ctx->err.clear();
+  if (rows <= 0 || cols <= 0) return set_err(ctx, FA_E_ARG, "rows and cols must be > 0");
+  if (!acc || !alpha) return set_err(ctx, FA_E_ARG, "acc and alpha must be given");
+  if (wtype == FA_W_U32) return set_err(ctx, FA_E_ARG, "absorption takes f32 weights or none (f64 output)");
+  FS(check_types(ctx, dem, dirs, w, wtype, FA_A_F64));
+  for (const void* p : {(const void*)dem, (const void*)dirs, w, (const void*)alpha, (const void*)acc})
+    if (p && is_device_ptr(p)) return set_err(ctx, FA_E_ARG, "fa_accumulate_absorb_streamed takes host buffers");
+  CK(cudaSetDevice(ctx->device));
+  return wtype == FA_W_NONE ? run_streamed<double, 0>(ctx, rows, cols, dem, nodata, dirs, w, acc, strip_rows, alpha)
+                            : run_streamed<double, 2>(ctx, rows, cols, dem, nodata, dirs, w, acc, strip_rows, alpha);
 }
 
 fa_status fa_accumulate_streamed(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem, float nodata,

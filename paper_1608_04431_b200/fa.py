@@ -27,7 +27,7 @@ FLOW_TERMINATES = 0xFFFFFFFF
 EXPORTS = ["fa_create", "fa_destroy", "fa_last_error", "fa_flowdirs", "fa_accumulate",
            "fa_accumulate_strips", "fa_perimeter_slots", "fa_perimeter_records", "fa_nccl_unique_id",
            "fa_accumulate_dist", "fa_get_stats", "fa_accumulate_streamed",
-           "fa_accumulate_absorb", "fa_accumulate_absorb_dist"]
+           "fa_accumulate_absorb", "fa_accumulate_absorb_dist", "fa_accumulate_absorb_streamed"]
 
 
 def nccl_unique_id() -> bytes:
@@ -80,6 +80,7 @@ def load() -> ctypes.CDLL:
     lib.fa_accumulate_strips.argtypes = [P, ctypes.c_int, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int]
     lib.fa_accumulate_streamed.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int, I]
     lib.fa_accumulate_absorb.argtypes = [P, ctypes.c_int, I, I, P, F, P, P, ctypes.c_int, P, P]
+    lib.fa_accumulate_absorb_streamed.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, P, I]
     lib.fa_accumulate_absorb_dist.argtypes = [P, P, ctypes.c_int, ctypes.c_int, I, I, I, I, P, F, P, P,
                                               ctypes.c_int, P, P]
     lib.fa_perimeter_slots.argtypes = [P, I, I]
@@ -246,6 +247,23 @@ class Context:
         self._check(self.lib.fa_accumulate_dist(self.h, buf, rank, nranks, global_rows, cols, row_begin, rows,
                                                 _ptr(dem), float(nodata), _ptr(dirs), _ptr(w), _wtype(w),
                                                 _ptr(out), a))
+        return out
+
+    def accumulate_absorb_streamed(self, alpha, dem=None, dirs=None, w=None, nodata: float = -9999.0,
+                                   strip_rows: int = 0, out=None):
+        """Out-of-core absorption: host arrays in and out (numpy / CPU or pinned tensors)."""
+        src = dem if dem is not None else dirs
+        rows, cols = src.shape
+        if out is None:
+            if isinstance(src, torch.Tensor):
+                out = torch.empty((rows, cols), dtype=torch.float64, pin_memory=src.is_pinned())
+            else:
+                import numpy as np
+
+                out = np.empty((rows, cols), np.float64)
+        self._check(self.lib.fa_accumulate_absorb_streamed(self.h, rows, cols, _ptr(dem), float(nodata), _ptr(dirs),
+                                                           _ptr(w), _wtype(w), _ptr(alpha), _ptr(out),
+                                                           int(strip_rows)))
         return out
 
     def accumulate_absorb_dist(self, nccl_id: bytes, rank: int, nranks: int, global_rows: int, row_begin: int,

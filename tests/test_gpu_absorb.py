@@ -142,3 +142,21 @@ def test_absorb_dist_single_rank_nccl(fa_lib):
         st = ctx.stats()
     _check(got, d, oracle.accumulate_alpha(d, al, cfg.w))
     assert st["bytes_exchanged"] > 0
+
+
+@pytest.mark.parametrize("strip_rows", [64, 250, 0])
+def test_absorb_streamed(fa_lib, strip_rows):
+    """Out of core with absorption: alpha streamed with the strips (host buffers)."""
+    rng = np.random.default_rng(strip_rows + 1)
+    d = inputs.random_dirs(21, 513, 200, p_nodata=0.1, p_noflow=0.02)
+    al = rng.random(d.shape).astype(np.float32)
+    w = inputs.weights_f32(21, d.shape)
+    with fa_lib.Context(0, tile=(64, 64)) as ctx:
+        got = ctx.accumulate_absorb_streamed(al, dirs=d, w=w, strip_rows=strip_rows)
+    _check(got, d, oracle.accumulate_alpha(d, al, w))
+    cfg = inputs.make_config("cfg3", 512, 512)
+    dd = oracle.d8(cfg.dem)
+    a2 = (0.9 + 0.1 * rng.random(dd.shape)).astype(np.float32)
+    with fa_lib.Context(0, tile=(128, 128)) as ctx:
+        g2 = ctx.accumulate_absorb_streamed(a2, dem=cfg.dem, w=cfg.w, strip_rows=strip_rows)
+    _check(g2, dd, oracle.accumulate_alpha(dd, a2, cfg.w))
