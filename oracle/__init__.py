@@ -63,6 +63,7 @@ def _L():
             "or_acc_region_fix": ([_P, _I, _I, _I, _I, _I, _I, _P, ctypes.c_int, _P], ctypes.c_int),
             "or_brute_u64": ([_P, _I, _I, _P, _P], ctypes.c_int),
             "or_acc_alpha_f64": ([_P, _I, _I, _P, _P, _P], ctypes.c_int),
+            "or_fill": ([_P, _I, _I, ctypes.c_float, _P], ctypes.c_int),
             "or_brute_alpha_f64": ([_P, _I, _I, _P, _P, _P], ctypes.c_int),
             "or_perim_count": ([_I, _I], _I),
             "or_perim_xy": ([_I, _I, _I, _P, _P], ctypes.c_int),
@@ -151,6 +152,15 @@ def brute(dirs: np.ndarray, w: np.ndarray | None = None) -> np.ndarray:
     A = np.zeros((H, W), np.uint64)
     _chk(_L().or_brute_u64(_p(dirs), H, W, _p(_w_u32(w)), _p(A)), "or_brute")
     return A
+
+
+def fill(z: np.ndarray, nodata: float = -9999.0) -> np.ndarray:
+    """O-FILL: Priority-Flood + epsilon (D15), literally; returns the filled copy."""
+    z = np.ascontiguousarray(z, np.float32)
+    H, W = z.shape
+    out = np.empty_like(z)
+    _chk(_L().or_fill(_p(z), H, W, float(nodata), _p(out)), "or_fill")
+    return out
 
 
 def accumulate_alpha(dirs: np.ndarray, alpha: np.ndarray, w: np.ndarray | None = None,

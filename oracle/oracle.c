@@ -285,6 +285,89 @@ int or_brute_alpha_f64(const uint8_t* dirs, int64_t H, int64_t W, const float* w
   return 0;
 }
 
+/* ======================================================================
+ * O-FILL ("the depressions can be filled to the level of
+ * their lowest outlets ... Priority-Flood", D15): Priority-Flood + epsilon,
+ * literally.  Seeds (data cells on the grid edge or 8-adjacent to NoData)
+ * enter a min-priority queue keyed (W, linear index) with W = z; popping a
+ * cell c closes each unvisited data neighbour n with
+ * W(n) = max(z(n), nextafterf(W(c), +inf)) and pushes it.  NoData (z ==
+ * nodata or non-finite) is copied unchanged.  Plain binary heap of
+ * (value, index) pairs compared as floats; single-threaded.
+ * ==================================================================== */
+typedef struct {
+  float v;
+  int64_t i;
+} o_item;
+static int o_less(o_item a, o_item b) { return a.v < b.v || (a.v == b.v && a.i < b.i); }
+
+int or_fill(const float* z, int64_t H, int64_t W, float nodata, float* out) {
+  const int64_t N = H * W;
+  o_item* heap = (o_item*)malloc((size_t)N * sizeof(o_item));
+  uint8_t* seen = (uint8_t*)calloc((size_t)N, 1);
+  if (!heap || !seen) { free(heap); free(seen); return 5; }
+  int64_t hn = 0;
+  for (int64_t i = 0; i < N; ++i) out[i] = z[i];
+  for (int64_t y = 0; y < H; ++y)
+    for (int64_t x = 0; x < W; ++x) {
+      const int64_t i = y * W + x;
+      if (o_is_nodata(z[i], nodata)) continue;
+      int seed = (y == 0 || x == 0 || y == H - 1 || x == W - 1);
+      for (int k = 1; k <= 8 && !seed; ++k) {
+        const int64_t ny = y + ODY[k], nx = x + ODX[k];
+        if (o_is_nodata(z[ny * W + nx], nodata)) seed = 1;
+      }
+      if (!seed) continue;
+      seen[i] = 1;
+      /* push */
+      o_item it = {z[i], i};
+      int64_t c = hn++;
+      while (c > 0) {
+        int64_t p = (c - 1) / 2;
+        if (!o_less(it, heap[p])) break;
+        heap[c] = heap[p];
+        c = p;
+      }
+      heap[c] = it;
+    }
+  while (hn > 0) {
+    o_item top = heap[0];
+    o_item last = heap[--hn];
+    int64_t c = 0;
+    for (;;) { /* sift down */
+      int64_t l = 2 * c + 1;
+      if (l >= hn) break;
+      int64_t r = l + 1, m = (r < hn && o_less(heap[r], heap[l])) ? r : l;
+      if (!o_less(heap[m], last)) break;
+      heap[c] = heap[m];
+      c = m;
+    }
+    if (hn > 0) heap[c] = last;
+    const int64_t y = top.i / W, x = top.i % W;
+    for (int k = 1; k <= 8; ++k) {
+      const int64_t ny = y + ODY[k], nx = x + ODX[k];
+      if (ny < 0 || nx < 0 || ny >= H || nx >= W) continue;
+      const int64_t n = ny * W + nx;
+      if (seen[n] || o_is_nodata(z[n], nodata)) continue;
+      seen[n] = 1;
+      const float up = nextafterf(top.v, INFINITY);
+      out[n] = z[n] > up ? z[n] : up;
+      o_item it = {out[n], n};
+      int64_t cc = hn++;
+      while (cc > 0) {
+        int64_t p = (cc - 1) / 2;
+        if (!o_less(it, heap[p])) break;
+        heap[cc] = heap[p];
+        cc = p;
+      }
+      heap[cc] = it;
+    }
+  }
+  free(heap);
+  free(seen);
+  return 0;
+}
+
 int or_acc_u64(const uint8_t* dirs, int64_t H, int64_t W, const uint32_t* wt, uint64_t* A) {
   return or_acc_region_u64(dirs, H, W, 0, 0, H, W, wt, A);
 }
