@@ -87,6 +87,17 @@ FA_API fa_status fa_flowdirs(fa_ctx* ctx, const float* dem, int64_t rows, int64_
  * 1e-9 relative of the exact sum (D13).  f32 weights must be finite and
  * >= 0 (D21); weights of NoData cells are ignored.
  *   acc : rows x cols of u32 / u64 / f64 according to atype, out. */
+/* Depression filling ("the depressions can be filled to the
+ * level of their lowest outlets ... Priority-Flood"; D15): out = the
+ * Priority-Flood+epsilon surface W of dem -- W = z at seeds (data cells on
+ * the grid edge or 8-adjacent to NoData), W(p) = max(z(p), nextafterf(min
+ * of the data neighbours' W, +inf)) elsewhere (unique; the input the D8 of
+ * fa_flowdirs / fa_accumulate expects).  NoData (== nodata or non-finite)
+ * is copied.  rows x cols f32, device or host buffers; out may not alias dem.
+ * stats: ms_total, launches. */
+FA_API fa_status fa_fill(fa_ctx* ctx, const float* dem, int64_t rows, int64_t cols, float nodata,
+                         float* out);
+
 FA_API fa_status fa_accumulate(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem, float nodata,
                         const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc,
                         fa_atype atype);

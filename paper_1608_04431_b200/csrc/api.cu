@@ -55,6 +55,8 @@ cudaError_t launch_absorb_graph(cudaStream_t st, uint32_t nn, int64_t nslots, co
 cudaError_t launch_scatter_x_absorb(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const float* node_alpha,
                                     const double* S, double* x_slot, const uint8_t* flags, bool intra_tile);
 cudaError_t launch_g1_weights_cut(cudaStream_t st, uint32_t nn, const uint8_t* flags, double* wv);
+// depression filling (N4): fill.cu
+cudaError_t fill_depressions(Runtime& rt, const float* z, int64_t H, int64_t W, float nodata, float* out);
 template <class T>
 cudaError_t launch_scatter_x(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
                              const T* S, T* x_slot, bool intra_tile);
@@ -1286,6 +1288,35 @@ fa_status fa_flowdirs(fa_ctx* ctx, const float* dem, int64_t rows, int64_t cols,
   ctx->stats.ms_total = ctx->stats.ms_pass1 = ms;
   ctx->stats.cells = rows * cols;
   ctx->stats.launches = 1;
+  return FA_OK;
+}
+
+fa_status fa_fill(fa_ctx* ctx, const float* dem, int64_t rows, int64_t cols, float nodata, float* out) {
+  if (!ctx) return FA_E_ARG;
+  ctx->err.clear();
+  if (!dem || !out || rows <= 0 || cols <= 0) return set_err(ctx, FA_E_ARG, "bad arguments");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->st;
+  const size_t n = (size_t)rows * (size_t)cols;
+  Staged sz, so;
+  CK(stage_in(st, dem, n * 4, sz));
+  CK(stage_out_alloc(st, out, n * 4, so));
+  reset_run(ctx);
+  CK(cudaEventRecord(ctx->ev[0], st));
+  cudaError_t e = fa::fill_depressions(ctx->rt, (const float*)sz.dev, rows, cols, nodata, (float*)so.dev);
+  CK(cudaEventRecord(ctx->ev[1], st));
+  if (e == cudaSuccess && so.owned) e = cudaMemcpyAsync(out, so.dev, n * 4, cudaMemcpyDeviceToHost, st);
+  for (Staged* p : {&sz, &so})
+    if (p->owned) cudaFreeAsync(p->dev, st);
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  if (e != cudaSuccess || e2 != cudaSuccess)
+    return set_err(ctx, FA_E_CUDA, std::string("fill: ") + cudaGetErrorString(e != cudaSuccess ? e : e2));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+  ctx->stats = fa_stats{};
+  ctx->stats.ms_total = ms;
+  ctx->stats.cells = rows * cols;
+  ctx->stats.launches = ctx->rt.launches;
   return FA_OK;
 }
 

@@ -27,7 +27,7 @@ FLOW_TERMINATES = 0xFFFFFFFF
 EXPORTS = ["fa_create", "fa_destroy", "fa_last_error", "fa_flowdirs", "fa_accumulate",
            "fa_accumulate_strips", "fa_perimeter_slots", "fa_perimeter_records", "fa_nccl_unique_id",
            "fa_accumulate_dist", "fa_get_stats", "fa_accumulate_streamed",
-           "fa_accumulate_absorb", "fa_accumulate_absorb_dist", "fa_accumulate_absorb_streamed"]
+           "fa_accumulate_absorb", "fa_accumulate_absorb_dist", "fa_accumulate_absorb_streamed", "fa_fill"]
 
 
 def nccl_unique_id() -> bytes:
@@ -80,6 +80,7 @@ def load() -> ctypes.CDLL:
     lib.fa_accumulate_strips.argtypes = [P, ctypes.c_int, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int]
     lib.fa_accumulate_streamed.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, ctypes.c_int, I]
     lib.fa_accumulate_absorb.argtypes = [P, ctypes.c_int, I, I, P, F, P, P, ctypes.c_int, P, P]
+    lib.fa_fill.argtypes = [P, P, I, I, F, P]
     lib.fa_accumulate_absorb_streamed.argtypes = [P, I, I, P, F, P, P, ctypes.c_int, P, P, I]
     lib.fa_accumulate_absorb_dist.argtypes = [P, P, ctypes.c_int, ctypes.c_int, I, I, I, I, P, F, P, P,
                                               ctypes.c_int, P, P]
@@ -167,6 +168,15 @@ class Context:
             out = torch.empty((rows, cols), dtype=torch.uint8, device=dem.device) if isinstance(
                 dem, torch.Tensor) else __import__("numpy").empty((rows, cols), "uint8")
         self._check(self.lib.fa_flowdirs(self.h, _ptr(dem), rows, cols, float(nodata), _ptr(out)))
+        return out
+
+    # ---------------------------------------------------------------- N4
+    def fill(self, dem, nodata: float = -9999.0, out=None):
+        """Depression filling (Priority-Flood+epsilon surface) of a f32 DEM; device or host."""
+        rows, cols = dem.shape
+        if out is None:
+            out = torch.empty_like(dem) if isinstance(dem, torch.Tensor) else __import__("numpy").empty_like(dem)
+        self._check(self.lib.fa_fill(self.h, _ptr(dem), rows, cols, float(nodata), _ptr(out)))
         return out
 
     # ---------------------------------------------------------------- H1-H6
