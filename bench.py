@@ -317,6 +317,29 @@ def run_gpu(args):
                   "alpha": "U[0.9,1) seed 5", "call": "fa_accumulate_absorb (device buffers)"}
         del al
 
+    # ---- depression filling (N4): fa_fill on cfg3's unfilled terrain (G2 + G3)
+    fillm = None
+    if world == 1 and not args.no_ooc and args.rows is None:
+        import inputs
+
+        zr = inputs.terrain(4, H, W)
+        inputs.coast(zr, 4, 0.10)
+        with torch.cuda.stream(stream):
+            dzr = torch.from_numpy(zr).cuda()
+            zf = torch.empty_like(dzr)
+        stream.synchronize()
+        ctx.fill(dzr, out=zf)  # warm-up
+        fts = []
+        for _ in range(2):
+            ctx.fill(dzr, out=zf)
+            fts.append(ctx.stats())
+        fms = float(np.median([t["ms_total"] for t in fts]))
+        ok = bool(torch.equal(zf, dz))  # the bench DEM is this terrain filled on the CPU (G4)
+        fillm = {"value": H * W / (fms * 1e-3) / 1e9, "unit": "Gcells/s", "ms_per_step": fms,
+                 "launches": int(fts[-1]["launches"]), "equals_cpu_fill": ok,
+                 "call": "fa_fill (device buffers, unfilled cfg3 terrain)"}
+        del dzr, zf
+
     peak, peak_src = hbm_peak()
     mp1, mgr, mp2 = float(np.mean(p1)), float(np.mean(gr)), float(np.mean(p2))
     md8, mblk = float(np.mean(kd8)), float(np.mean(kblk))
@@ -352,6 +375,7 @@ def run_gpu(args):
         "e2e": e2e,
         "out_of_core": ooc,
         "absorption": absorb,
+        "fill": fillm,
         "gpu_launches": int(np.sum(launches)) if launches and launches[0] else None,
         "input_gen_s": round(gen_s, 1),
     }
