@@ -413,15 +413,22 @@ __device__ __forceinline__ uint32_t donor_masks(const uint32_t* D, int hw) {
   const uint32_t nE = __funnelshift_r(c1, c2, 8), nW = __funnelshift_r(c0, c1, 24);
   const uint32_t nNE = __funnelshift_r(u1, u2, 8), nNW = __funnelshift_r(u0, u1, 24);
   const uint32_t nSE = __funnelshift_r(d1, d2, 8), nSW = __funnelshift_r(d0, d1, 24);
-  uint32_t m = 0;
-  m |= (__vcmpeq4(nN, 0x05050505u) & 0x01010101u) << 0;
-  m |= (__vcmpeq4(nNE, 0x06060606u) & 0x01010101u) << 1;
-  m |= (__vcmpeq4(nE, 0x07070707u) & 0x01010101u) << 2;
-  m |= (__vcmpeq4(nSE, 0x08080808u) & 0x01010101u) << 3;
-  m |= (__vcmpeq4(nS, 0x01010101u) & 0x01010101u) << 4;
-  m |= (__vcmpeq4(nSW, 0x02020202u) & 0x01010101u) << 5;
-  m |= (__vcmpeq4(nW, 0x03030303u) & 0x01010101u) << 6;
-  m |= (__vcmpeq4(nNW, 0x04040404u) & 0x01010101u) << 7;
+  // byte j of eq(n, c): bit 7 set iff byte j of n equals c (c < 0x80).  Exact
+  // zero-byte test of n ^ c: the low 7 bits of a byte are non-zero iff adding
+  // 0x7F sets its bit 7 (no carry between bytes), and bit 7 of n ^ c is bit 7
+  // of n (codes 0..8, ring 254 / 255).  4 ops instead of __vcmpeq4's 7.
+  auto eq7 = [](uint32_t n, uint32_t c) {
+    const uint32_t y = ((n ^ c) & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+    return ~(y | n) & 0x80808080u;
+  };
+  uint32_t m = eq7(nN, 0x05050505u) >> 7;
+  m |= eq7(nNE, 0x06060606u) >> 6;
+  m |= eq7(nE, 0x07070707u) >> 5;
+  m |= eq7(nSE, 0x08080808u) >> 4;
+  m |= eq7(nS, 0x01010101u) >> 3;
+  m |= eq7(nSW, 0x02020202u) >> 2;
+  m |= eq7(nW, 0x03030303u) >> 1;
+  m |= eq7(nNW, 0x04040404u);
   return m;
 }
 
