@@ -61,6 +61,12 @@ namespace fa {
 #ifndef FA_REC_STEPS
 #define FA_REC_STEPS 4
 #endif
+#ifndef FA_CHAIN_TAIL
+#define FA_CHAIN_TAIL 32  // queue width below which the loop switches to chain bursts (0: never)
+#endif
+#ifndef FA_CHAIN_K
+#define FA_CHAIN_K 4
+#endif
 #ifndef FA_P1_MINB
 #define FA_P1_MINB 8
 #endif
@@ -564,6 +570,105 @@ __device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc, in
 template <class T>
 __device__ __forceinline__ void g_add(T* p, T v) { atomicAdd(p, v); }
 
+// Tail of Alg. 1's queue loop with chain bursts.  When few cells are ready
+// the block is working through its long in-block chains, one L2 round trip
+// per cell.  A successor whose only pending donor is the lane's own cell
+// (count 1 at the start of the iteration) is final as soon as that cell is:
+// A(succ) already holds w plus every earlier donor, so the lane follows the
+// chain up to K cells per iteration with all K loads in flight at once and
+// writes the values with plain stores.  Junction successors (count > 1) take
+// the RED + shared-count path and are queued by the lane that takes the
+// count to zero.  Counts are read in phase 1 and decremented in phase 2,
+// separated by __syncwarp, so every chain decision sees the counts of the
+// iteration start (no other lane can push into a chain cell: its one pending
+// donor is the lane's own cell).  Returns the number of cells processed.
+template <int K, class T, int R, bool Z>
+__device__ __forceinline__ uint32_t kahn_chain_tail(WSmem<T, R, Z>& s, uint32_t head, uint32_t tail, T* Ab,
+                                                    int64_t W) {
+  const int lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  uint16_t* Q = s.src;
+  const uint32_t wm = (uint32_t)W - 32u;
+  uint32_t done = 0;
+  int c = -1;          // the lane's cell (its value a is final once loaded)
+  bool fresh = false;  // c was just taken from the queue: a must be loaded
+  T a = (T)0;
+  for (;;) {
+    __syncwarp();
+    const unsigned idle = __ballot_sync(kFull, c < 0);
+    const uint32_t avail = tail - head;
+    if (idle == kFull && avail == 0u) break;
+    if (c < 0) {
+      const uint32_t r = (uint32_t)__popc(idle & lt);
+      if (r < avail) {
+        c = Q[head + r];
+        fresh = true;
+      }
+    }
+    head += min((uint32_t)__popc(idle), avail);
+    // phase 1: the chain ahead of c
+    uint32_t cc[K];
+    uint32_t cur = (uint32_t)c, su_end = SU_STOP;
+    int n = 0;
+    bool go = c >= 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      cc[k] = 0u;
+      if (go) {
+        const uint32_t su = s.succ[cur];
+        const uint32_t t = su & SU_T;
+        go = (su & SU_STOP) == 0u && ((s.pend[t >> 3] >> ((t & 7u) * 4u)) & 0xFu) == 1u;
+        if (go) {
+          cc[k] = t;
+          cur = t;
+          n = k + 1;
+        } else {
+          su_end = su;
+        }
+      }
+    }
+    __syncwarp();
+    // phase 2: one round of loads, the chain's prefix sums, then the junction push
+    uint32_t ready = 0u, t = 0u;
+    if (c >= 0) {
+      T x[K];
+      T* pk[K];
+      if (fresh) a = __ldcg(Ab + ((uint32_t)c + ((uint32_t)c >> 5) * wm));
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        pk[k] = Ab + (cc[k] + (cc[k] >> 5) * wm);
+        if (k < n) x[k] = __ldcg(pk[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (k < n) {
+          a += x[k];
+          *pk[k] = a;
+        }
+      done += (fresh ? 1u : 0u) + (uint32_t)n;
+      fresh = false;
+      if (go) {
+        c = (int)cur;  // the chain goes on: continue from its last cell next iteration
+      } else {
+        c = -1;
+        if ((su_end & SU_STOP) == 0u) {
+          // "A(n) <- A(n) + A(c)", "decrement D(n)" (Alg. 1)
+          t = su_end & SU_T;
+          g_add(Ab + (t + (t >> 5) * wm), a);
+          const uint32_t sh = (t & 7u) * 4u;
+          const uint32_t old = atomicAdd(&s.pend[t >> 3], 0u - (1u << sh));
+          ready = ((old >> sh) & 0xFu) == 1u;
+        }
+      }
+    }
+    const unsigned bm = __ballot_sync(kFull, ready != 0u);
+    if (ready) Q[tail + (uint32_t)__popc(bm & lt)] = (uint16_t)t;
+    tail += (uint32_t)__popc(bm);
+  }
+  __syncwarp();
+  return __reduce_add_sync(kFull, done);
+}
+
 template <class T, int R, bool Z, bool ABS = false>
 __device__ __forceinline__ uint32_t kahn_block(WSmem<T, R, Z>& s, uint32_t nsrc, T* Ab, int64_t W,
                                                const float* Alb = nullptr) {
@@ -574,6 +679,17 @@ __device__ __forceinline__ uint32_t kahn_block(WSmem<T, R, Z>& s, uint32_t nsrc,
   const uint32_t wm = (uint32_t)W - 32u;
   uint32_t head = 0, tail = nsrc;
   while (head < tail) {
+#if FA_CHAIN_TAIL
+    // the queue has narrowed to the block's long in-block chains: finish
+    // with chain bursts (kahn_chain_tail), which carry values along chains
+    // instead of one L2 round trip per cell
+    if constexpr (!ABS) {
+      if (tail - head < FA_CHAIN_TAIL) {
+        __syncwarp();
+        return head + kahn_chain_tail<FA_CHAIN_K>(s, head, tail, Ab, W);
+      }
+    }
+#endif
     __syncwarp();
     const uint32_t q = head + (uint32_t)lane;
     const bool valid = q < tail;
