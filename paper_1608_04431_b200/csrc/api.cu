@@ -80,6 +80,14 @@ cudaError_t launch_inject_slots(cudaStream_t st, const Geom& g, int64_t nslots, 
                                 const T* xT, const uint32_t* slot_root, T* val1, T* x_slot,
                                 const T* slot_f = nullptr);
 
+// absorption entry points run with the default 32-row blocks whatever the
+// FA_BR tuning override says (set for the duration of the call)
+thread_local bool g_force_br32 = false;
+struct ForceBR32 {
+  ForceBR32() { g_force_br32 = true; }
+  ~ForceBR32() { g_force_br32 = false; }
+};
+
 Geom make_geom(int64_t H, int64_t W, int64_t th, int64_t tw) {
   Geom g{};
   g.H = H;
@@ -99,7 +107,7 @@ Geom make_geom(int64_t H, int64_t W, int64_t th, int64_t tw) {
   }
   if (const char* e = getenv("FA_BR")) {
     const int v = atoi(e);
-    if (v == 16 || v == 32) g.br = v;
+    if ((v == 16 || v == 32) && !g_force_br32) g.br = v;
   }
   g.pb = 2 * (g.br + g.bc) - 4;
   g.regular = (g.TH % g.br == 0 && g.TW % g.bc == 0) ? 1 : 0;
@@ -1339,6 +1347,7 @@ fa_status fa_accumulate_strips(fa_ctx* ctx, int nstrips, int64_t rows, int64_t c
 fa_status fa_accumulate_absorb(fa_ctx* ctx, int nstrips, int64_t rows, int64_t cols, const float* dem,
                                float nodata, const uint8_t* dirs, const void* w, fa_wtype wtype,
                                const float* alpha, double* acc) {
+  fa::ForceBR32 force_br32;
   if (!ctx) return FA_E_ARG;
   ctx->err.clear();
   if (rows <= 0 || cols <= 0) return set_err(ctx, FA_E_ARG, "rows and cols must be > 0");
@@ -1380,6 +1389,7 @@ fa_status fa_accumulate_absorb(fa_ctx* ctx, int nstrips, int64_t rows, int64_t c
 fa_status fa_accumulate_absorb_streamed(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem,
                                         float nodata, const uint8_t* dirs, const void* w, fa_wtype wtype,
                                         const float* alpha, double* acc, int64_t strip_rows) {
+  fa::ForceBR32 force_br32;
   if (!ctx) return FA_E_ARG;
   ctx->err.clear();
   if (rows <= 0 || cols <= 0) return set_err(ctx, FA_E_ARG, "rows and cols must be > 0");
@@ -1453,6 +1463,7 @@ fa_status fa_accumulate_absorb_dist(fa_ctx* ctx, const void* nccl_id128, int ran
                                     int64_t global_rows, int64_t cols, int64_t row_begin, int64_t local_rows,
                                     const float* dem, float nodata, const uint8_t* dirs, const void* w,
                                     fa_wtype wtype, const float* alpha, double* acc) {
+  fa::ForceBR32 force_br32;
   if (!ctx) return FA_E_ARG;
   if (!alpha || !is_device_ptr(alpha)) return set_err(ctx, FA_E_ARG, "alpha must be a device buffer");
   if (wtype == FA_W_U32) return set_err(ctx, FA_E_ARG, "absorption takes f32 weights or none (f64 output)");
