@@ -44,7 +44,8 @@ typedef struct fa_ctx fa_ctx;
 
 typedef enum {
   FA_OK = 0,
-  FA_E_ARG = 1,      /* NULL/negative sizes, dem and dirs both or neither, bad wtype/atype, bad weight (D21) */
+  FA_E_ARG = 1,      /* NULL/negative sizes, dem and dirs both or neither, bad wtype/atype, bad weight (D21),
+                        alpha outside [0,1] (absorption), device/host buffer kind not accepted by the call */
   FA_E_DIRCODE = 2,  /* a direction byte not in {0..8, 255} (D1) */
   FA_E_CYCLE = 3,    /* some data cell never retires: the direction graph has a cycle */
   FA_E_OVERFLOW = 4, /* integer accumulation could exceed the output type (D10) */
