@@ -21,6 +21,12 @@
 #include "fa_internal.cuh"
 #include "forest.cuh"
 
+// Gauss-Seidel sweeps inside a tile (values written as soon as they fall);
+// 0 = Jacobi (two-phase, one extra barrier per sweep)
+#ifndef FA_FILL_GS
+#define FA_FILL_GS 1
+#endif
+
 namespace fa {
 
 namespace {
@@ -46,10 +52,12 @@ __global__ void k_fill_init(const float* __restrict__ z, int64_t H, int64_t W, f
   }
 }
 
-// one launch: every tile whose own values or a neighbour tile's changed in
-// the previous launch (dirty_in) relaxes to its local fixed point given the
-// halo values of the launch start; a tile that decreases marks itself in
-// dirty_out and sets *changed.  A CTA of 32x32 threads owns an FT x FT tile
+// one launch: every tile next to a border that fell in the previous launch
+// (dirty_in) relaxes to its local fixed point given the halo values it
+// stages (a neighbour may already have lowered them this launch: any staged
+// value is an upper bound of the fixed point, so the relaxation stays
+// monotone); a tile whose border cells fall records those sides in dirty_out
+// and sets *changed.  A CTA of 32x32 threads owns an FT x FT tile
 // (C = FT/32 cells per thread and axis): larger tiles carry the fill further
 // per launch.
 template <int FT>
@@ -63,11 +71,22 @@ __global__ void __launch_bounds__(1024) k_fill_relax(const float* __restrict__ z
   {
     // settled neighbourhood: nothing can change here this launch
     const int bx = (int)blockIdx.x, by = (int)blockIdx.y, nbx = (int)gridDim.x, nby = (int)gridDim.y;
+    // a tile is at its local fixed point for the halo it last saw: it runs
+    // again only if a neighbour changed a border cell facing it (dirty_in
+    // holds per tile the sides whose cells fell: 1 top, 2 bottom, 4 left,
+    // 8 right; a corner needs both of its sides, a conservative test; 16
+    // runs the tile itself, set for the first launch)
     bool dirty = false;
     for (int dy = -1; dy <= 1; ++dy)
       for (int dx = -1; dx <= 1; ++dx) {
         const int yy = by + dy, xx = bx + dx;
-        if (yy >= 0 && xx >= 0 && yy < nby && xx < nbx && dirty_in[(int64_t)yy * nbx + xx]) dirty = true;
+        if ((dy | dx) == 0) {
+          if (dirty_in[(int64_t)by * nbx + bx] & 16u) dirty = true;  // the first launch
+          continue;
+        }
+        if (yy < 0 || xx < 0 || yy >= nby || xx >= nbx) continue;
+        const uint32_t need = (dy < 0 ? 2u : dy > 0 ? 1u : 0u) | (dx < 0 ? 8u : dx > 0 ? 4u : 0u);
+        if ((dirty_in[(int64_t)yy * nbx + xx] & need) == need) dirty = true;
       }
     if (!dirty) return;  // block-uniform
   }
@@ -82,7 +101,7 @@ __global__ void __launch_bounds__(1024) k_fill_relax(const float* __restrict__ z
     }
     s[ly + 1][lx + 1] = v;
   }
-  float zc[C][C], cur[C][C];
+  float zc[C][C], cur[C][C], init[C][C];
   bool active[C][C];
 #pragma unroll
   for (int i = 0; i < C; ++i)
@@ -91,13 +110,13 @@ __global__ void __launch_bounds__(1024) k_fill_relax(const float* __restrict__ z
       const int ly = ty + 32 * i, lx = tx + 32 * j;
       const int64_t gy = y0 + ly, gx = x0 + lx;
       zc[i][j] = 0.0f;
-      cur[i][j] = INFINITY;
+      cur[i][j] = init[i][j] = INFINITY;
       active[i][j] = false;
       if (gy < H && gx < W) {
         const float zz = z[gy * W + gx];
         if (!f_nodata(zz, nodata)) {
           zc[i][j] = zz;
-          cur[i][j] = Wg[gy * W + gx];
+          cur[i][j] = init[i][j] = Wg[gy * W + gx];
           active[i][j] = true;  // seeds hold z, their fixed value: relaxing them is a no-op
         }
       }
@@ -124,9 +143,14 @@ __global__ void __launch_bounds__(1024) k_fill_relax(const float* __restrict__ z
           if (c < cur[i][j]) {
             cand[i][j] = c;
             ch = true;
+#if FA_FILL_GS
+            cur[i][j] = c;
+            s[ly + 1][lx + 1] = c;
+#endif
           }
         }
       }
+#if !FA_FILL_GS
     __syncthreads();
     if (ch) {
 #pragma unroll
@@ -138,18 +162,29 @@ __global__ void __launch_bounds__(1024) k_fill_relax(const float* __restrict__ z
             s[ty + 32 * i + 1][tx + 32 * j + 1] = cand[i][j];
           }
     }
+#endif
     if (!__syncthreads_or(ch)) break;
     any = true;
   }
-  if (any) {
+  if (any) {  // block-uniform
+    __shared__ uint32_t sides;
+    if (threadIdx.x == 0) sides = 0u;
+    __syncthreads();
+    uint32_t mine = 0u;
 #pragma unroll
     for (int i = 0; i < C; ++i)
 #pragma unroll
       for (int j = 0; j < C; ++j)
-        if (active[i][j]) Wg[(y0 + ty + 32 * i) * W + x0 + tx + 32 * j] = cur[i][j];
-    if (threadIdx.x == 0) {
+        if (active[i][j] && cur[i][j] != init[i][j]) {
+          const int ly = ty + 32 * i, lx = tx + 32 * j;
+          Wg[(y0 + ly) * W + x0 + lx] = cur[i][j];
+          mine |= (ly == 0 ? 1u : 0u) | (ly == FT - 1 ? 2u : 0u) | (lx == 0 ? 4u : 0u) | (lx == FT - 1 ? 8u : 0u);
+        }
+    if (mine) atomicOr(&sides, mine);
+    __syncthreads();
+    if (threadIdx.x == 0 && sides) {
       atomicOr(changed, 1u);
-      dirty_out[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = 1;
+      dirty_out[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = (uint8_t)sides;
     }
   }
 }
@@ -170,7 +205,7 @@ cudaError_t fill_depressions(Runtime& rt, const float* z, int64_t H, int64_t W, 
   uint8_t* da = rt.alloc<uint8_t>(nt);
   uint8_t* db = rt.alloc<uint8_t>(nt);
   if (rt.err) return rt.err;
-  cudaMemsetAsync(da, 1, nt, st);  // every tile is dirty at the start
+  cudaMemsetAsync(da, 0x1F, nt, st);  // every tile is dirty at the start
   for (int64_t round = 0;; round += 4) {
     cudaMemsetAsync(flag, 0, sizeof(uint32_t), st);
     for (int j = 0; j < 4; ++j) {
