@@ -8,10 +8,11 @@
 //   W(p) = max(z(p), nextafterf(min_{data n in N8(p)} W(n), +inf))  otherwise,
 // (each step strictly raises the cost, so it is a shortest-path fixpoint and
 // any schedule converges to the same bits).  The GPU computes it by monotone
-// relaxation from W = +inf: a CTA owns a 64x64 tile, stages W with a 1-cell
-// halo in shared memory and runs Jacobi sweeps until the tile is stable;
-// tiles exchange through global memory between launches, and the host
-// repeats launches until no tile changes.  NoData (z == nodata or
+// relaxation from W = +inf: a CTA owns a 32x32 tile, stages W with a 1-cell
+// halo in shared memory and runs Gauss-Seidel sweeps until the tile is
+// stable; tiles exchange through global memory between launches, each
+// launch works through a list of the tiles next to a border that fell in the
+// previous one, and the host repeats launches until the list is empty.  NoData (z == nodata or
 // non-finite) is copied unchanged and never relaxed.
 #include <algorithm>
 #include <cstdlib>
@@ -21,10 +22,12 @@
 #include "fa_internal.cuh"
 #include "forest.cuh"
 
-// Gauss-Seidel sweeps inside a tile (values written as soon as they fall);
-// 0 = Jacobi (two-phase, one extra barrier per sweep)
-#ifndef FA_FILL_GS
-#define FA_FILL_GS 1
+// warps per CTA (rows of threads) for 32x32 and 64x64 tiles
+#ifndef FA_FILL_TY32
+#define FA_FILL_TY32 4
+#endif
+#ifndef FA_FILL_TY64
+#define FA_FILL_TY64 16
 #endif
 
 namespace fa {
@@ -52,141 +55,121 @@ __global__ void k_fill_init(const float* __restrict__ z, int64_t H, int64_t W, f
   }
 }
 
-// one launch: every tile next to a border that fell in the previous launch
-// (dirty_in) relaxes to its local fixed point given the halo values it
-// stages (a neighbour may already have lowered them this launch: any staged
-// value is an upper bound of the fixed point, so the relaxation stays
-// monotone); a tile whose border cells fall records those sides in dirty_out
-// and sets *changed.  A CTA of 32x32 threads owns an FT x FT tile
-// (C = FT/32 cells per thread and axis): larger tiles carry the fill further
-// per launch.
-template <int FT>
-__global__ void __launch_bounds__(1024) k_fill_relax(const float* __restrict__ z, int64_t H, int64_t W,
-                                                     float nodata, float* Wg, uint32_t* changed,
-                                                     const uint8_t* __restrict__ dirty_in, uint8_t* dirty_out) {
-  constexpr int C = FT / 32;
+// one launch over a worklist of tiles (a persistent grid strides over
+// list_in): each listed tile relaxes to its local fixed point given the
+// halo values it stages (a neighbour may already have lowered them this
+// launch: any staged value is an upper bound of the fixed point, so the
+// relaxation stays monotone).  A tile is at its local fixed point for the
+// halo it saw, so it is listed again only when a neighbour lowers a border
+// cell facing it: a tile whose border cells fall appends the neighbours on
+// those sides to list_out (a corner neighbour needs both of its sides, a
+// conservative test), deduplicated by stamping them with the next launch's
+// epoch.  A CTA of 32 x TY threads owns an FT x FT tile (FT/TY rows and
+// FT/32 columns of cells per thread).
+template <int FT, int TY>
+__global__ void __launch_bounds__(32 * TY) k_fill_relax(const float* __restrict__ z, int64_t H, int64_t W,
+                                                     float nodata, float* Wg, int nbx, int nby,
+                                                     const uint32_t* __restrict__ list_in,
+                                                     const uint32_t* __restrict__ cnt_in, uint32_t* list_out,
+                                                     uint32_t* cnt_out, uint32_t* stamp, uint32_t epoch) {
+  constexpr int CY = FT / TY, CX = FT / 32;
   __shared__ float s[FT + 2][FT + 3];
+  __shared__ uint32_t sides;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t x0 = (int64_t)blockIdx.x * FT, y0 = (int64_t)blockIdx.y * FT;
-  {
-    // settled neighbourhood: nothing can change here this launch
-    const int bx = (int)blockIdx.x, by = (int)blockIdx.y, nbx = (int)gridDim.x, nby = (int)gridDim.y;
-    // a tile is at its local fixed point for the halo it last saw: it runs
-    // again only if a neighbour changed a border cell facing it (dirty_in
-    // holds per tile the sides whose cells fell: 1 top, 2 bottom, 4 left,
-    // 8 right; a corner needs both of its sides, a conservative test; 16
-    // runs the tile itself, set for the first launch)
-    bool dirty = false;
-    for (int dy = -1; dy <= 1; ++dy)
-      for (int dx = -1; dx <= 1; ++dx) {
-        const int yy = by + dy, xx = bx + dx;
-        if ((dy | dx) == 0) {
-          if (dirty_in[(int64_t)by * nbx + bx] & 16u) dirty = true;  // the first launch
-          continue;
-        }
-        if (yy < 0 || xx < 0 || yy >= nby || xx >= nbx) continue;
-        const uint32_t need = (dy < 0 ? 2u : dy > 0 ? 1u : 0u) | (dx < 0 ? 8u : dx > 0 ? 4u : 0u);
-        if ((dirty_in[(int64_t)yy * nbx + xx] & need) == need) dirty = true;
-      }
-    if (!dirty) return;  // block-uniform
-  }
-  // stage W (NoData and off-grid act as +inf: never a minimising neighbour)
-  for (int i = threadIdx.x; i < (FT + 2) * (FT + 2); i += blockDim.x) {
-    const int ly = i / (FT + 2) - 1, lx = i % (FT + 2) - 1;
-    const int64_t gy = y0 + ly, gx = x0 + lx;
-    float v = INFINITY;
-    if (gy >= 0 && gx >= 0 && gy < H && gx < W) {
-      const float zz = z[gy * W + gx];
-      if (!f_nodata(zz, nodata)) v = Wg[gy * W + gx];
-    }
-    s[ly + 1][lx + 1] = v;
-  }
-  float zc[C][C], cur[C][C], init[C][C];
-  bool active[C][C];
-#pragma unroll
-  for (int i = 0; i < C; ++i)
-#pragma unroll
-    for (int j = 0; j < C; ++j) {
-      const int ly = ty + 32 * i, lx = tx + 32 * j;
-      const int64_t gy = y0 + ly, gx = x0 + lx;
-      zc[i][j] = 0.0f;
-      cur[i][j] = init[i][j] = INFINITY;
-      active[i][j] = false;
-      if (gy < H && gx < W) {
-        const float zz = z[gy * W + gx];
-        if (!f_nodata(zz, nodata)) {
-          zc[i][j] = zz;
-          cur[i][j] = init[i][j] = Wg[gy * W + gx];
-          active[i][j] = true;  // seeds hold z, their fixed value: relaxing them is a no-op
-        }
-      }
-    }
-  __syncthreads();
-  bool any = false;
-  for (int it = 0; it < FT * FT; ++it) {
-    float cand[C][C];
-    bool ch = false;
-#pragma unroll
-    for (int i = 0; i < C; ++i)
-#pragma unroll
-      for (int j = 0; j < C; ++j) {
-        cand[i][j] = cur[i][j];
-        if (active[i][j]) {
-          const int ly = ty + 32 * i, lx = tx + 32 * j;
-          float m = INFINITY;
-#pragma unroll
-          for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-            for (int dx = 0; dx < 3; ++dx)
-              if (dy != 1 || dx != 1) m = fminf(m, s[ly + dy][lx + dx]);
-          const float c = fmaxf(zc[i][j], nextafterf(m, INFINITY));
-          if (c < cur[i][j]) {
-            cand[i][j] = c;
-            ch = true;
-#if FA_FILL_GS
-            cur[i][j] = c;
-            s[ly + 1][lx + 1] = c;
-#endif
-          }
-        }
-      }
-#if !FA_FILL_GS
-    __syncthreads();
-    if (ch) {
-#pragma unroll
-      for (int i = 0; i < C; ++i)
-#pragma unroll
-        for (int j = 0; j < C; ++j)
-          if (cand[i][j] < cur[i][j]) {
-            cur[i][j] = cand[i][j];
-            s[ty + 32 * i + 1][tx + 32 * j + 1] = cand[i][j];
-          }
-    }
-#endif
-    if (!__syncthreads_or(ch)) break;
-    any = true;
-  }
-  if (any) {  // block-uniform
-    __shared__ uint32_t sides;
+  const uint32_t ntile = *cnt_in;
+  for (uint32_t idx = blockIdx.x; idx < ntile; idx += gridDim.x) {
+    const uint32_t tile = list_in[idx];
+    const int by = (int)(tile / (uint32_t)nbx), bx = (int)(tile - (uint32_t)by * (uint32_t)nbx);
+    const int64_t x0 = (int64_t)bx * FT, y0 = (int64_t)by * FT;
+    __syncthreads();  // the previous tile's shared reads are done
     if (threadIdx.x == 0) sides = 0u;
+    // stage W (NoData and off-grid act as +inf: never a minimising neighbour)
+    for (int i = threadIdx.x; i < (FT + 2) * (FT + 2); i += blockDim.x) {
+      const int ly = i / (FT + 2) - 1, lx = i % (FT + 2) - 1;
+      const int64_t gy = y0 + ly, gx = x0 + lx;
+      float v = INFINITY;
+      if (gy >= 0 && gx >= 0 && gy < H && gx < W) {
+        const float zz = z[gy * W + gx];
+        if (!f_nodata(zz, nodata)) v = Wg[gy * W + gx];
+      }
+      s[ly + 1][lx + 1] = v;
+    }
+    float zc[CY][CX], cur[CY][CX], init[CY][CX];
+    bool active[CY][CX];
+#pragma unroll
+    for (int i = 0; i < CY; ++i)
+#pragma unroll
+      for (int j = 0; j < CX; ++j) {
+        const int ly = ty + TY * i, lx = tx + 32 * j;
+        const int64_t gy = y0 + ly, gx = x0 + lx;
+        zc[i][j] = 0.0f;
+        cur[i][j] = init[i][j] = INFINITY;
+        active[i][j] = false;
+        if (gy < H && gx < W) {
+          const float zz = z[gy * W + gx];
+          if (!f_nodata(zz, nodata)) {
+            zc[i][j] = zz;
+            cur[i][j] = init[i][j] = Wg[gy * W + gx];
+            active[i][j] = true;  // seeds hold z, their fixed value: relaxing them is a no-op
+          }
+        }
+      }
     __syncthreads();
+    bool any = false;
+    for (int it = 0; it < FT * FT; ++it) {
+      // Gauss-Seidel: a value is written as soon as it falls
+      bool ch = false;
+#pragma unroll
+      for (int i = 0; i < CY; ++i)
+#pragma unroll
+        for (int j = 0; j < CX; ++j)
+          if (active[i][j]) {
+            const int ly = ty + TY * i, lx = tx + 32 * j;
+            float m = INFINITY;
+#pragma unroll
+            for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+              for (int dx = 0; dx < 3; ++dx)
+                if (dy != 1 || dx != 1) m = fminf(m, s[ly + dy][lx + dx]);
+            const float c = fmaxf(zc[i][j], nextafterf(m, INFINITY));
+            if (c < cur[i][j]) {
+              cur[i][j] = c;
+              s[ly + 1][lx + 1] = c;
+              ch = true;
+            }
+          }
+      if (!__syncthreads_or(ch)) break;
+      any = true;
+    }
+    if (!any) continue;  // block-uniform
     uint32_t mine = 0u;
 #pragma unroll
-    for (int i = 0; i < C; ++i)
+    for (int i = 0; i < CY; ++i)
 #pragma unroll
-      for (int j = 0; j < C; ++j)
+      for (int j = 0; j < CX; ++j)
         if (active[i][j] && cur[i][j] != init[i][j]) {
-          const int ly = ty + 32 * i, lx = tx + 32 * j;
+          const int ly = ty + TY * i, lx = tx + 32 * j;
           Wg[(y0 + ly) * W + x0 + lx] = cur[i][j];
           mine |= (ly == 0 ? 1u : 0u) | (ly == FT - 1 ? 2u : 0u) | (lx == 0 ? 4u : 0u) | (lx == FT - 1 ? 8u : 0u);
         }
     if (mine) atomicOr(&sides, mine);
     __syncthreads();
-    if (threadIdx.x == 0 && sides) {
-      atomicOr(changed, 1u);
-      dirty_out[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = (uint8_t)sides;
+    if (threadIdx.x < 9 && threadIdx.x != 4) {
+      // sides: 1 top, 2 bottom, 4 left, 8 right
+      const int dy = (int)threadIdx.x / 3 - 1, dx = (int)threadIdx.x % 3 - 1;
+      const uint32_t need = (dy < 0 ? 1u : dy > 0 ? 2u : 0u) | (dx < 0 ? 4u : dx > 0 ? 8u : 0u);
+      const int yy = by + dy, xx = bx + dx;
+      if ((sides & need) == need && yy >= 0 && xx >= 0 && yy < nby && xx < nbx) {
+        const uint32_t nt = (uint32_t)yy * (uint32_t)nbx + (uint32_t)xx;
+        if (atomicExch(&stamp[nt], epoch) != epoch) list_out[atomicAdd(cnt_out, 1u)] = nt;
+      }
     }
   }
+}
+
+__global__ void k_fill_iota(uint32_t* list, uint32_t* cnt, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) list[i] = i;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *cnt = n;
 }
 
 }  // namespace
@@ -197,34 +180,49 @@ cudaError_t fill_depressions(Runtime& rt, const float* z, int64_t H, int64_t W, 
   const int64_t n = H * W;
   k_fill_init<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 64), 256, 0, st>>>(z, H, W, nodata, out);
   ++rt.launches;
-  uint32_t* flag = rt.alloc<uint32_t>(1);
-  const char* e = getenv("FA_FILL_TILE");  // tuning: 32 or 64 (default)
-  const int FT = e && atoi(e) == 32 ? 32 : 64;
-  const dim3 grid((unsigned)((W + FT - 1) / FT), (unsigned)((H + FT - 1) / FT));
-  const int64_t nt = (int64_t)grid.x * grid.y;
-  uint8_t* da = rt.alloc<uint8_t>(nt);
-  uint8_t* db = rt.alloc<uint8_t>(nt);
+  const char* e = getenv("FA_FILL_TILE");  // tuning: 32 (default) or 64
+  const int FT = e && atoi(e) == 64 ? 64 : 32;
+  const int nbx = (int)((W + FT - 1) / FT), nby = (int)((H + FT - 1) / FT);
+  const uint32_t nt = (uint32_t)nbx * (uint32_t)nby;
+  uint32_t* la = rt.alloc<uint32_t>(nt);
+  uint32_t* lb = rt.alloc<uint32_t>(nt);
+  uint32_t* stamp = rt.alloc<uint32_t>(nt);
+  uint32_t* cnt = rt.alloc<uint32_t>(2);
   if (rt.err) return rt.err;
-  cudaMemsetAsync(da, 0x1F, nt, st);  // every tile is dirty at the start
-  for (int64_t round = 0;; round += 4) {
-    cudaMemsetAsync(flag, 0, sizeof(uint32_t), st);
+  cudaMemsetAsync(stamp, 0, sizeof(uint32_t) * nt, st);
+  k_fill_iota<<<(unsigned)std::min<uint32_t>((nt + 255) / 256, 148 * 8), 256, 0, st>>>(la, cnt, nt);  // every tile
+  ++rt.launches;
+  uint32_t *ca = cnt, *cb = cnt + 1;
+  // persistent grid: as many CTAs as fit per SM (threads and shared memory)
+  const int ty = FT == 32 ? FA_FILL_TY32 : FA_FILL_TY64;
+  const int per_sm = std::min(2048 / (32 * ty), (228 * 1024) / (int)(sizeof(float) * (FT + 2) * (FT + 3) + 1024));
+  const unsigned grid = 148u * (unsigned)std::min(per_sm, 32);
+  uint32_t epoch = 0;
+  for (;;) {
     for (int j = 0; j < 4; ++j) {
-      cudaMemsetAsync(db, 0, nt, st);
-      if (FT == 32) k_fill_relax<32><<<grid, 1024, 0, st>>>(z, H, W, nodata, out, flag, da, db);
-      else k_fill_relax<64><<<grid, 1024, 0, st>>>(z, H, W, nodata, out, flag, da, db);
-      std::swap(da, db);
+      cudaMemsetAsync(cb, 0, sizeof(uint32_t), st);
+      ++epoch;
+      if (FT == 32)
+        k_fill_relax<32, FA_FILL_TY32><<<grid, 32 * FA_FILL_TY32, 0, st>>>(z, H, W, nodata, out, nbx, nby, la, ca,
+                                                                            lb, cb, stamp, epoch);
+      else
+        k_fill_relax<64, FA_FILL_TY64><<<grid, 32 * FA_FILL_TY64, 0, st>>>(z, H, W, nodata, out, nbx, nby, la, ca,
+                                                                            lb, cb, stamp, epoch);
+      std::swap(la, lb);
+      std::swap(ca, cb);
     }
     rt.launches += 4;
-    rt.read(flag, 1);
+    rt.read(ca, 1);  // the next launch's worklist size
     if (!rt.h_cnt[0] || rt.err) break;
-    if (round > 4 * (H + W)) {  // cannot happen: each pass settles at least one more tile ring
+    if (epoch > 4u * (uint32_t)(H + W) + 64u) {  // cannot happen: each launch settles at least one more tile ring
       rt.err = cudaErrorUnknown;
       break;
     }
   }
-  rt.free(flag);
-  rt.free(da);
-  rt.free(db);
+  rt.free(la);
+  rt.free(lb);
+  rt.free(stamp);
+  rt.free(cnt);
   return rt.err ? rt.err : cudaGetLastError();
 }
 

@@ -42,9 +42,12 @@ def test_fill_negative_nodata_blobs_and_host_buffers(fa_lib):
     assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
 
 
-def test_fill_deep_bowl_crosses_many_tiles(fa_lib):
+@pytest.mark.parametrize("tile", ["32", "64"])
+def test_fill_deep_bowl_crosses_many_tiles(fa_lib, tile, monkeypatch):
     # an L1 bowl: every interior cell is raised, the fill propagates inwards
-    # across ~16 tiles from the edge
+    # across 8-16 tiles from the edge (FA_FILL_TILE: the 32x32 default and
+    # the 64x64 tile kernel)
+    monkeypatch.setenv("FA_FILL_TILE", tile)
     H = W = 1024
     y, x = np.mgrid[0:H, 0:W]
     z = (np.abs(x - W // 2) + np.abs(y - H // 2)).astype(np.float32) * 0.01
