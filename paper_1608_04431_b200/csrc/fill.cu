@@ -23,6 +23,16 @@
 #include "forest.cuh"
 
 // warps per CTA (rows of threads) for 32x32 and 64x64 tiles
+// rows of a thread: consecutive (1, sweeps alternate down / up) or strided
+// by TY (0)
+#ifndef FA_FILL_CONTIG
+#define FA_FILL_CONTIG 1
+#endif
+#if FA_FILL_CONTIG
+#define FILL_ROW(i) (ty * CY + (i))
+#else
+#define FILL_ROW(i) (ty + TY * (i))
+#endif
 #ifndef FA_FILL_TY32
 #define FA_FILL_TY32 4
 #endif
@@ -64,8 +74,8 @@ __global__ void k_fill_init(const float* __restrict__ z, int64_t H, int64_t W, f
 // cell facing it: a tile whose border cells fall appends the neighbours on
 // those sides to list_out (a corner neighbour needs both of its sides, a
 // conservative test), deduplicated by stamping them with the next launch's
-// epoch.  A CTA of 32 x TY threads owns an FT x FT tile (FT/TY rows and
-// FT/32 columns of cells per thread).
+// epoch.  A CTA of 32 x TY threads owns an FT x FT tile (FT/TY consecutive
+// rows and FT/32 columns of cells per thread).
 template <int FT, int TY>
 __global__ void __launch_bounds__(32 * TY) k_fill_relax(const float* __restrict__ z, int64_t H, int64_t W,
                                                      float nodata, float* Wg, int nbx, int nby,
@@ -100,7 +110,7 @@ __global__ void __launch_bounds__(32 * TY) k_fill_relax(const float* __restrict_
     for (int i = 0; i < CY; ++i)
 #pragma unroll
       for (int j = 0; j < CX; ++j) {
-        const int ly = ty + TY * i, lx = tx + 32 * j;
+        const int ly = FILL_ROW(i), lx = tx + 32 * j;
         const int64_t gy = y0 + ly, gx = x0 + lx;
         zc[i][j] = 0.0f;
         cur[i][j] = init[i][j] = INFINITY;
@@ -117,27 +127,38 @@ __global__ void __launch_bounds__(32 * TY) k_fill_relax(const float* __restrict_
     __syncthreads();
     bool any = false;
     for (int it = 0; it < FT * FT; ++it) {
-      // Gauss-Seidel: a value is written as soon as it falls
+      // Gauss-Seidel: a value is written as soon as it falls; a thread owns
+      // CY consecutive rows and walks them down on even sweeps and up on
+      // odd ones, so one sweep carries a value across all of them
       bool ch = false;
+      auto relax = [&](const int i, const int j) {
+        if (active[i][j]) {
+          const int ly = FILL_ROW(i), lx = tx + 32 * j;
+          float m = INFINITY;
 #pragma unroll
-      for (int i = 0; i < CY; ++i)
+          for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-        for (int j = 0; j < CX; ++j)
-          if (active[i][j]) {
-            const int ly = ty + TY * i, lx = tx + 32 * j;
-            float m = INFINITY;
-#pragma unroll
-            for (int dy = 0; dy < 3; ++dy)
-#pragma unroll
-              for (int dx = 0; dx < 3; ++dx)
-                if (dy != 1 || dx != 1) m = fminf(m, s[ly + dy][lx + dx]);
-            const float c = fmaxf(zc[i][j], nextafterf(m, INFINITY));
-            if (c < cur[i][j]) {
-              cur[i][j] = c;
-              s[ly + 1][lx + 1] = c;
-              ch = true;
-            }
+            for (int dx = 0; dx < 3; ++dx)
+              if (dy != 1 || dx != 1) m = fminf(m, s[ly + dy][lx + dx]);
+          const float c = fmaxf(zc[i][j], nextafterf(m, INFINITY));
+          if (c < cur[i][j]) {
+            cur[i][j] = c;
+            s[ly + 1][lx + 1] = c;
+            ch = true;
           }
+        }
+      };
+      if (FA_FILL_CONTIG && (it & 1)) {
+#pragma unroll
+        for (int i = CY - 1; i >= 0; --i)
+#pragma unroll
+          for (int j = 0; j < CX; ++j) relax(i, j);
+      } else {
+#pragma unroll
+        for (int i = 0; i < CY; ++i)
+#pragma unroll
+          for (int j = 0; j < CX; ++j) relax(i, j);
+      }
       if (!__syncthreads_or(ch)) break;
       any = true;
     }
@@ -148,7 +169,7 @@ __global__ void __launch_bounds__(32 * TY) k_fill_relax(const float* __restrict_
 #pragma unroll
       for (int j = 0; j < CX; ++j)
         if (active[i][j] && cur[i][j] != init[i][j]) {
-          const int ly = ty + TY * i, lx = tx + 32 * j;
+          const int ly = FILL_ROW(i), lx = tx + 32 * j;
           Wg[(y0 + ly) * W + x0 + lx] = cur[i][j];
           mine |= (ly == 0 ? 1u : 0u) | (ly == FT - 1 ? 2u : 0u) | (lx == 0 ? 4u : 0u) | (lx == FT - 1 ? 8u : 0u);
         }
