@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(32 * TY) k_fill_relax(const float* __restrict_
                                                      uint32_t* cnt_out, uint32_t* stamp, uint32_t epoch) {
   constexpr int CY = FT / TY, CX = FT / 32;
   __shared__ float s[FT + 2][FT + 3];
+  __shared__ float zs[FT][FT + 1];  // the tile's elevations (staged once)
   __shared__ uint32_t sides;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const uint32_t ntile = *cnt_in;
@@ -97,13 +98,16 @@ __global__ void __launch_bounds__(32 * TY) k_fill_relax(const float* __restrict_
     for (int i = threadIdx.x; i < (FT + 2) * (FT + 2); i += blockDim.x) {
       const int ly = i / (FT + 2) - 1, lx = i % (FT + 2) - 1;
       const int64_t gy = y0 + ly, gx = x0 + lx;
-      float v = INFINITY;
+      float v = INFINITY, zz = INFINITY;
       if (gy >= 0 && gx >= 0 && gy < H && gx < W) {
-        const float zz = z[gy * W + gx];
-        if (!f_nodata(zz, nodata)) v = Wg[gy * W + gx];
+        zz = z[gy * W + gx];
+        const float w = Wg[gy * W + gx];  // both loads in flight together
+        if (!f_nodata(zz, nodata)) v = w;
       }
       s[ly + 1][lx + 1] = v;
+      if (ly >= 0 && lx >= 0 && ly < FT && lx < FT) zs[ly][lx] = zz;
     }
+    __syncthreads();
     float zc[CY][CX], cur[CY][CX], init[CY][CX];
     bool active[CY][CX];
 #pragma unroll
@@ -111,20 +115,11 @@ __global__ void __launch_bounds__(32 * TY) k_fill_relax(const float* __restrict_
 #pragma unroll
       for (int j = 0; j < CX; ++j) {
         const int ly = FILL_ROW(i), lx = tx + 32 * j;
-        const int64_t gy = y0 + ly, gx = x0 + lx;
-        zc[i][j] = 0.0f;
-        cur[i][j] = init[i][j] = INFINITY;
-        active[i][j] = false;
-        if (gy < H && gx < W) {
-          const float zz = z[gy * W + gx];
-          if (!f_nodata(zz, nodata)) {
-            zc[i][j] = zz;
-            cur[i][j] = init[i][j] = Wg[gy * W + gx];
-            active[i][j] = true;  // seeds hold z, their fixed value: relaxing them is a no-op
-          }
-        }
+        const float zz = zs[ly][lx];  // +inf off the grid
+        active[i][j] = !f_nodata(zz, nodata);  // seeds hold z, their fixed value: relaxing them is a no-op
+        zc[i][j] = active[i][j] ? zz : 0.0f;
+        cur[i][j] = init[i][j] = active[i][j] ? s[ly + 1][lx + 1] : INFINITY;
       }
-    __syncthreads();
     bool any = false;
     for (int it = 0; it < FT * FT; ++it) {
       // Gauss-Seidel: a value is written as soon as it falls; a thread owns
