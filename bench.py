@@ -400,8 +400,30 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_gpu(args)
+        return
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        # not under torchrun: launch one rank per GPU ourselves (never time
+        # N ranks on fewer GPUs -- fail loudly instead)
+        import socket
+
+        import torch
+
+        ndev = torch.cuda.device_count()
+        if ndev < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but this box has {ndev} CUDA device(s)\n")
+            sys.exit(2)
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    if world is not None and int(world) != args.gpus:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}\n")
+        sys.exit(2)
+    run_gpu(args)
 
 
 if __name__ == "__main__":

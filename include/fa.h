@@ -71,6 +71,33 @@ FA_API fa_status fa_create(fa_ctx** out, int device, void* cuda_stream, int64_t 
 FA_API fa_status fa_destroy(fa_ctx* ctx);
 FA_API const char* fa_last_error(const fa_ctx* ctx);
 
+/* Context options (per context, default in brackets; read at each call).
+ * None changes results: they select among equivalent schedules of the same
+ * method, so every option value is covered by the same parity tests.
+ *   FA_OPT_RETENTION  [FA_RETAIN] | FA_EVICT: the paper's memory retention
+ *       strategies.  RETAIN keeps the block-local accumulation in
+ *       the output and the finalize walks each entry's path adding its offset
+ *       (P:L260); EVICT recomputes the block accumulation with w + x.
+ *   FA_OPT_D8  [FA_D8_SPLIT] | FA_D8_FUSED: H1 as its own kernel, or fused
+ *       into the pass-1 block kernel (DEM input only).
+ *   FA_OPT_BLOCK_ROWS  [32] | 16: rows of the warp-resident blocks (32 wide).
+ *       Absorption always runs with 32.
+ *   FA_OPT_WALK_CAP  [128], 0..2^20: steps of a perimeter-graph walk before
+ *       it re-queues (0: level-synchronous peeling only).
+ *   FA_OPT_FILL_TILE  [32] | 64: tile side of fa_fill.
+ * Unknown option or value out of range: FA_E_ARG, the option unchanged. */
+typedef enum {
+  FA_OPT_RETENTION = 1,
+  FA_OPT_D8 = 2,
+  FA_OPT_BLOCK_ROWS = 3,
+  FA_OPT_WALK_CAP = 4,
+  FA_OPT_FILL_TILE = 5
+} fa_option;
+enum { FA_RETAIN = 0, FA_EVICT = 1 };
+enum { FA_D8_SPLIT = 0, FA_D8_FUSED = 1 };
+FA_API fa_status fa_set_option(fa_ctx* ctx, int option, int64_t value);
+FA_API fa_status fa_get_option(const fa_ctx* ctx, int option, int64_t* value);
+
 /* H1: D8 flow directions of a DEM ("D8 ... a single one of its
  * neighbours"; BASELINE north_star: steepest strictly-downhill neighbour,
  * diagonal drop divided by sqrt2 (exact compare, D4), ties to the lowest
@@ -80,14 +107,6 @@ FA_API const char* fa_last_error(const fa_ctx* ctx);
 FA_API fa_status fa_flowdirs(fa_ctx* ctx, const float* dem, int64_t rows, int64_t cols, float nodata,
                       uint8_t* dirs);
 
-/* H1-H6: flow accumulation A(p) = w(p) + sum_{n: target(n)=p} A(n)
- * (Eq. 1, P:L49-54, alpha in {0,1}).  Exactly one of `dem` (then D8 is
- * computed, H1) or `dirs` is non-NULL.  `w` may be NULL (w = 1).  Flow into
- * NoData or off the grid is dropped (D8); NoFlow cells keep inflow plus
- * their own w (D7).  Integer results are exact; f64 results are within
- * 1e-9 relative of the exact sum (D13).  f32 weights must be finite and
- * >= 0 (D21); weights of NoData cells are ignored.
- *   acc : rows x cols of u32 / u64 / f64 according to atype, out. */
 /* Depression filling ("the depressions can be filled to the
  * level of their lowest outlets ... Priority-Flood"; D15): out = the
  * Priority-Flood+epsilon surface W of dem -- W = z at seeds (data cells on
@@ -99,6 +118,14 @@ FA_API fa_status fa_flowdirs(fa_ctx* ctx, const float* dem, int64_t rows, int64_
 FA_API fa_status fa_fill(fa_ctx* ctx, const float* dem, int64_t rows, int64_t cols, float nodata,
                          float* out);
 
+/* H1-H6: flow accumulation A(p) = w(p) + sum_{n: target(n)=p} A(n)
+ * (Eq. 1, P:L49-54, alpha in {0,1}).  Exactly one of `dem` (then D8 is
+ * computed, H1) or `dirs` is non-NULL.  `w` may be NULL (w = 1).  Flow into
+ * NoData or off the grid is dropped (D8); NoFlow cells keep inflow plus
+ * their own w (D7).  Integer results are exact; f64 results are within
+ * 1e-9 relative of the exact sum (D13).  f32 weights must be finite and
+ * >= 0 (D21); weights of NoData cells are ignored.
+ *   acc : rows x cols of u32 / u64 / f64 according to atype, out. */
 FA_API fa_status fa_accumulate(fa_ctx* ctx, int64_t rows, int64_t cols, const float* dem, float nodata,
                         const uint8_t* dirs, const void* w, fa_wtype wtype, void* acc,
                         fa_atype atype);
@@ -186,10 +213,16 @@ FA_API fa_status fa_perimeter_records(fa_ctx* ctx, int64_t rows, int64_t cols, c
  * wtype, atype and tiling.  Rank r owns rows [row_begin, row_begin +
  * local_rows) (strips contiguous, ordered by rank, each a multiple of the
  * tile height except the last).  dem/dirs/w/acc are the rank's strip.
- * Collectives: one halo row of z to/from each neighbour strip (DEM input),
- * an all-gather of the strips' perimeter records, a status
- * all-reduce.  The perimeter graph is then solved redundantly on every rank
- * (no second exchange). */
+ * Collectives (dist.cu): C0 a gather of every rank's arguments (all ranks
+ * agree on the partition or all return the same error before data moves),
+ * C1 two halo rows of z (DEM input) or one row of codes to/from each
+ * neighbour strip, C3 a gather of the status flags and integer weight sums
+ * (bitwise OR; u32 overflow, D10), C2 ONE all-gather of fixed-size padded
+ * buffers of the strips' tile perimeter records, and a final
+ * status gather.  The perimeter graph is solved redundantly on every rank
+ * (no second exchange).  With a DEM every strip but the last needs >= 2
+ * rows.  A rank-local failure (allocation, a kernel error) is reported to
+ * every rank at the next status gather, so all ranks return. */
 FA_API fa_status fa_nccl_unique_id(void* out128);
 FA_API fa_status fa_accumulate_dist(fa_ctx* ctx, const void* nccl_id128, int rank, int nranks,
                              int64_t global_rows, int64_t cols, int64_t row_begin,
@@ -207,7 +240,33 @@ FA_API fa_status fa_accumulate_absorb_dist(fa_ctx* ctx, const void* nccl_id128, 
                                            const uint8_t* dirs, const void* w, fa_wtype wtype,
                                            const float* alpha, double* acc);
 
-/* Per-phase statistics of the last call (device-timed with CUDA events). */
+/* The multi-GPU path with a loopback transport: nranks ranks of
+ * fa_accumulate_dist run as host threads inside this call, rank q on
+ * ctxs[q] (one distinct context per rank, each with its own stream; the
+ * contexts may share a device), exchanging halo rows, status flags and the
+ * perimeter records by stream-ordered device copies and events instead of
+ * NCCL.  Every rank executes the same code as in fa_accumulate_dist (C0
+ * argument agreement, C1 halo rows, phase A, C3 status, C2 record
+ * all-gather, the producer graph G2, phase B); only the transport differs
+ * (P:L215).  Per-rank arrays of nranks entries: row_begin,
+ * local_rows, dem / dirs / w / alpha (each array NULL when that input is
+ * absent), acc (required); every pointer is the rank's strip on its
+ * context's device.  alpha != NULL selects absorption (f64 output, w none
+ * or f32).  Returns FA_OK or the first failing rank's status (its message in
+ * fa_last_error of that rank's context); each context keeps its rank's
+ * statistics. */
+FA_API fa_status fa_accumulate_dist_loopback(fa_ctx* const* ctxs, int nranks, int64_t global_rows,
+                                             int64_t cols, const int64_t* row_begin,
+                                             const int64_t* local_rows, const float* const* dem,
+                                             float nodata, const uint8_t* const* dirs,
+                                             const void* const* w, fa_wtype wtype,
+                                             const float* const* alpha, void* const* acc,
+                                             fa_atype atype);
+
+/* Per-phase statistics of the last call (device-timed with CUDA events).
+ * fa_get_stats copies min(out_bytes, sizeof(fa_stats)) bytes into `out`
+ * (fields are only ever appended, so a caller built against an older,
+ * shorter fa_stats receives its prefix); out_bytes <= 0 -> FA_E_ARG. */
 typedef struct {
   double ms_total, ms_pass1, ms_graph, ms_pass2, ms_exchange;
   int64_t cells, blocks, graph_nodes, tile_nodes;
@@ -217,7 +276,7 @@ typedef struct {
   double ms_d8;     /* the standalone D8 kernel (single-device path; 0 when D8 is fused into pass 1) */
   double ms_block;  /* the pass-1 block kernel alone (k_pass1), last strip */
 } fa_stats;
-FA_API fa_status fa_get_stats(const fa_ctx* ctx, fa_stats* out);
+FA_API fa_status fa_get_stats(const fa_ctx* ctx, void* out, int64_t out_bytes);
 
 #ifdef __cplusplus
 }

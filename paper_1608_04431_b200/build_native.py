@@ -55,8 +55,12 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defines
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     extra = (["-DFA_PHASE_CLOCKS"] if variant == "prof" else []) + [f"-D{d}" for d in defines]
     inc = ["-I", os.path.join(ROOT, "include"), "-I", nccl_include()]
-    objdir = os.path.join(HERE, "build", variant or "release")
-    os.makedirs(objdir, exist_ok=True)
+    import shutil
+    import tempfile
+
+    # objects in a scratch directory: only the linked .so stays in the tree
+    # (it travels to the GPU box; 300 MB of objects would too)
+    objdir = tempfile.mkdtemp(prefix="libfa_build_")
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
 
     def compile_one(src):
@@ -83,6 +87,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", defines
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed linking libfa.so")
     os.replace(lib + ".tmp", lib)
+    shutil.rmtree(objdir, ignore_errors=True)
     res.stdout, res.stderr = log, ""
     if variant:
         return lib

@@ -1229,10 +1229,9 @@ cudaError_t launch_finalize_k(const Geom& g, const T* x_slot, const uint8_t* dir
   constexpr int NWC = 4;  // warps per CTA
   // At least 24 KB of shared memory per CTA: at most 9 CTAs (36 warps) per
   // SM, which keeps the acc rows the walks touch in L2 (measured on cfg3:
-  // 3.82 ms vs 3.92 ms at full occupancy).  FA_FINPAD overrides (tuning).
-  const char* pad = getenv("FA_FINPAD");
+  // 3.82 ms vs 3.92 ms at full occupancy).
   size_t sm = sizeof(FSmem<T, R, KB>) * NWC;
-  sm = pad ? sm + (size_t)atoi(pad) : (sm < 24576 ? 24576 : sm);
+  sm = sm < 24576 ? 24576 : sm;
   auto k = k_finalize<T, R, KB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int64_t groups = (g.nblocks + KB - 1) / KB;
@@ -1240,12 +1239,9 @@ cudaError_t launch_finalize_k(const Geom& g, const T* x_slot, const uint8_t* dir
   return cudaGetLastError();
 }
 
+// one block per warp (2 or 4 measured slower on cfg3)
 template <class T, int R>
 cudaError_t launch_finalize_r(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st) {
-  const char* e = getenv("FA_FINKB");  // tuning override: blocks per warp
-  const int kb = e ? atoi(e) : 1;
-  if (kb == 2) return launch_finalize_k<T, R, 2>(g, x_slot, dirs, acc, st);
-  if (kb == 4) return launch_finalize_k<T, R, 4>(g, x_slot, dirs, acc, st);
   return launch_finalize_k<T, R, 1>(g, x_slot, dirs, acc, st);
 }
 

@@ -225,8 +225,7 @@ cudaError_t launch_d8(const float* dem, const float* dem_up, const float* dem_dn
                    ((reinterpret_cast<uintptr_t>(dirs) & 3) == 0) &&
                    (!dem_up || (reinterpret_cast<uintptr_t>(dem_up) & 15) == 0) &&
                    (!dem_dn || (reinterpret_cast<uintptr_t>(dem_dn) & 15) == 0);
-  const char* e = getenv("FA_D8V");
-  if (vec && !(e && e[0] == '0')) {
+  if (vec) {
     dim3 grid((unsigned)((W + 511) / 512), (unsigned)((H + DV_RS - 1) / DV_RS));
     k_d8v<<<grid, 128, 0, st>>>(dem, dem_up, dem_dn, H, W, nodata, dirs);
   } else {

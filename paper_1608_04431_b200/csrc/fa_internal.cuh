@@ -104,7 +104,7 @@ struct Geom {
   }
 };
 
-Geom make_geom(int64_t H, int64_t W, int64_t th, int64_t tw);
+Geom make_geom(int64_t H, int64_t W, int64_t th, int64_t tw, int br);
 
 // ---------------------------------------------------------------- perimeter order
 // Clockwise from the top-left: top row L->R, right column, bottom row R->L,

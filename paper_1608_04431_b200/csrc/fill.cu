@@ -191,13 +191,13 @@ __global__ void k_fill_iota(uint32_t* list, uint32_t* cnt, uint32_t n) {
 }  // namespace
 
 // fill z into out (device buffers)
-cudaError_t fill_depressions(Runtime& rt, const float* z, int64_t H, int64_t W, float nodata, float* out) {
+cudaError_t fill_depressions(Runtime& rt, const float* z, int64_t H, int64_t W, float nodata, float* out,
+                             int tile) {
   cudaStream_t st = rt.st;
   const int64_t n = H * W;
   k_fill_init<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 64), 256, 0, st>>>(z, H, W, nodata, out);
   ++rt.launches;
-  const char* e = getenv("FA_FILL_TILE");  // tuning: 32 (default) or 64
-  const int FT = e && atoi(e) == 64 ? 64 : 32;
+  const int FT = tile == 64 ? 64 : 32;  // FA_OPT_FILL_TILE: 32 (default) or 64
   const int nbx = (int)((W + FT - 1) / FT), nby = (int)((H + FT - 1) / FT);
   const uint32_t nt = (uint32_t)nbx * (uint32_t)nby;
   uint32_t* la = rt.alloc<uint32_t>(nt);
@@ -230,7 +230,10 @@ cudaError_t fill_depressions(Runtime& rt, const float* z, int64_t H, int64_t W, 
     rt.launches += 4;
     rt.read(ca, 1);  // the next launch's worklist size
     if (!rt.h_cnt[0] || rt.err) break;
-    if (epoch > 4u * (uint32_t)(H + W) + 64u) {  // cannot happen: each launch settles at least one more tile ring
+    // bug catch only: a launch runs only while some value still falls, and a
+    // winding depression needs about (path length / tile side) launches, so
+    // the bound is the cell count (the old 4(H+W) guard was reachable)
+    if ((uint64_t)epoch > (uint64_t)H * (uint64_t)W + 64u) {
       rt.err = cudaErrorUnknown;
       break;
     }

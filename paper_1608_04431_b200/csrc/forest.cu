@@ -300,17 +300,13 @@ __global__ void k_expand(uint32_t m, const uint32_t* __restrict__ R, const uint3
 
 __global__ void k_set_flag(uint32_t* st, uint32_t f) { atomicOr(st, f); }
 
-inline int env_int(const char* name, int dflt, int lo = 0) {
-  const char* e = getenv(name);
-  const int v = e ? atoi(e) : dflt;
-  return v < lo ? dflt : v;
-}
-
 constexpr int kMaxLevels = 64;
 constexpr int kPeelBatch = 4;  // peel rounds per host check
 constexpr int kMaxJump = 40;
-constexpr int kWalkCap = 128;  // steps per walk before re-queueing (deep chains -> contraction); 0 = peel only.
-                               // 128 vs 32: cfg3 graph 1.54 vs 1.57 ms, 8 strips 29.9 vs 31.1 ms, cfg2 (one 16.7M chain) 1.04 vs 0.95 ms
+constexpr uint64_t kContractRatio = 8;  // contract once the frontier < remaining / 8
+// walk cap (Runtime::walk_cap, FA_OPT_WALK_CAP): steps per walk before
+// re-queueing (deep chains -> contraction); 0 = peel only.  128 vs 32: cfg3
+// graph 1.54 vs 1.57 ms, 8 strips 29.9 vs 31.1 ms, cfg2 (one 16.7M chain) 1.04 vs 0.95 ms
 
 // WG (absorption): edge weights wv (S(parent) += wv(v) S(v)); chains are
 // contracted with affine (acc, mul) pairs instead of sums
@@ -340,7 +336,7 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
   uint64_t remaining = n;
   bool contracted = false;
   uint32_t* pc = nullptr;  // device frontier counters of the batched peel rounds
-  const int cap = env_int("FA_WALKCAP", kWalkCap);  // tuning override (read per call)
+  const int cap = rt.walk_cap;
   if (cap <= 0) {
     rt.read(ctr, 1);
     nf = rt.h_cnt[0];
@@ -358,8 +354,7 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
     remaining -= rt.h_cnt[1];
   }
   while (nf > 0 && !rt.err) {
-    const uint64_t ratio = (uint64_t)env_int("FA_CONTRACT_RATIO", 8, 1);  // tuning override
-    if ((uint64_t)nf * ratio < remaining) {
+    if ((uint64_t)nf * kContractRatio < remaining) {
       // ---------------- contract the residual forest
       contracted = true;
       ++rt.contract_levels;
@@ -463,8 +458,6 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
     unsigned long long ret = 0;
     memcpy(&ret, &rt.h_cnt[4], sizeof(ret));
     remaining -= ret;
-    if (env_int("FA_DEBUG_GRAPH", 0)) fprintf(stderr, "level %d peel x%d: frontier %u remaining %llu\n", level,
-                                              kPeelBatch, nf, (unsigned long long)remaining);
   }
   rt.free(pc);
   if (!contracted && remaining != 0) k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);

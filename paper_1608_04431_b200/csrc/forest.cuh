@@ -14,6 +14,7 @@ struct Runtime {
   uint32_t* d_status = nullptr;  // status word (ST_*)
   // statistics
   int64_t peel_rounds = 0, contract_levels = 0, jump_rounds = 0, launches = 0;
+  int walk_cap = 128;  // steps per graph walk before re-queueing (FA_OPT_WALK_CAP; 0 = peel only)
   cudaError_t err = cudaSuccess;
 
   template <class U>

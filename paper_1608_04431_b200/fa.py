@@ -27,7 +27,16 @@ FLOW_TERMINATES = 0xFFFFFFFF
 EXPORTS = ["fa_create", "fa_destroy", "fa_last_error", "fa_flowdirs", "fa_accumulate",
            "fa_accumulate_strips", "fa_perimeter_slots", "fa_perimeter_records", "fa_nccl_unique_id",
            "fa_accumulate_dist", "fa_get_stats", "fa_accumulate_streamed",
-           "fa_accumulate_absorb", "fa_accumulate_absorb_dist", "fa_accumulate_absorb_streamed", "fa_fill"]
+           "fa_accumulate_absorb", "fa_accumulate_absorb_dist", "fa_accumulate_absorb_streamed", "fa_fill",
+           "fa_set_option", "fa_get_option", "fa_accumulate_dist_loopback"]
+# context options (fa.h fa_option); values: RETAIN / EVICT, D8_SPLIT / D8_FUSED, block rows 32 / 16,
+# graph walk cap, fill tile 32 / 64
+OPT_RETENTION, OPT_D8, OPT_BLOCK_ROWS, OPT_WALK_CAP, OPT_FILL_TILE = 1, 2, 3, 4, 5
+RETAIN, EVICT = 0, 1
+D8_SPLIT, D8_FUSED = 0, 1
+OPTIONS = {"retention": OPT_RETENTION, "d8": OPT_D8, "block_rows": OPT_BLOCK_ROWS, "walk_cap": OPT_WALK_CAP,
+           "fill_tile": OPT_FILL_TILE}
+OPTION_VALUES = {"retain": RETAIN, "evict": EVICT, "split": D8_SPLIT, "fused": D8_FUSED}
 
 
 def nccl_unique_id() -> bytes:
@@ -90,7 +99,12 @@ def load() -> ctypes.CDLL:
     lib.fa_nccl_unique_id.argtypes = [P]
     lib.fa_accumulate_dist.argtypes = [P, P, ctypes.c_int, ctypes.c_int, I, I, I, I, P, F, P, P,
                                        ctypes.c_int, P, ctypes.c_int]
-    lib.fa_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
+    lib.fa_get_stats.argtypes = [P, P, I]
+    lib.fa_set_option.argtypes = [P, ctypes.c_int, I]
+    lib.fa_get_option.argtypes = [P, ctypes.c_int, ctypes.POINTER(I)]
+    PP = ctypes.POINTER(P)
+    lib.fa_accumulate_dist_loopback.argtypes = [PP, ctypes.c_int, I, I, ctypes.POINTER(I), ctypes.POINTER(I), PP, F,
+                                                PP, PP, ctypes.c_int, PP, PP, ctypes.c_int]
     for fn in EXPORTS:
         if fn not in ("fa_last_error", "fa_perimeter_slots"):
             getattr(lib, fn).restype = ctypes.c_int
@@ -102,25 +116,56 @@ def _ptr(t):
     if t is None:
         return None
     if isinstance(t, torch.Tensor):
-        assert t.is_contiguous(), "tensors must be contiguous"
+        if not t.is_contiguous():
+            raise ValueError("tensors must be contiguous")
         return ctypes.c_void_p(t.data_ptr())
     import numpy as np
 
     if isinstance(t, np.ndarray):
-        assert t.flags["C_CONTIGUOUS"]
+        if not t.flags["C_CONTIGUOUS"]:
+            raise ValueError("arrays must be C-contiguous")
         return t.ctypes.data_as(ctypes.c_void_p)
     raise TypeError(type(t))
+
+
+def _dtype_name(t) -> str:
+    return str(t.dtype).replace("torch.", "")
+
+
+def _check(t, name: str, dtypes: tuple, shape=None):
+    """Reject a wrong dtype or shape before the C call (the library reads raw
+    pointers: a float64 DEM or a short `out` would be misread / overrun)."""
+    if t is None:
+        return
+    dn = _dtype_name(t)
+    if dn not in dtypes:
+        raise TypeError(f"{name} must be {' or '.join(dtypes)}, got {dn}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+
+
+ACC_DTYPE = {A_U32: "uint32", A_U64: "uint64", A_F64: "float64"}
+
+
+def _check_inputs(dem, dirs, w, shape, alpha=None):
+    # "exactly one of dem / dirs" is the library's own FA_E_ARG check (tested through the ABI)
+    if len(shape) != 2:
+        raise ValueError("rasters are 2-D (rows, cols)")
+    _check(dem, "dem", ("float32",), shape)
+    _check(dirs, "dirs", ("uint8",), shape)
+    _check(w, "w", ("uint32", "float32"), shape)
+    _check(alpha, "alpha", ("float32",), shape)
 
 
 def _wtype(w):
     if w is None:
         return W_NONE
-    dt = w.dtype
-    if dt in (torch.uint32, torch.int32) or str(dt) in ("uint32", "int32"):
+    dn = _dtype_name(w)
+    if dn == "uint32":
         return W_U32
-    if dt == torch.float32 or str(dt) == "float32":
+    if dn == "float32":
         return W_F32
-    raise TypeError(f"weights must be uint32 or float32, got {dt}")
+    raise TypeError(f"weights must be uint32 or float32, got {dn}")
 
 
 class Context:
@@ -158,12 +203,25 @@ class Context:
 
     def stats(self) -> dict:
         s = Stats()
-        self._check(self.lib.fa_get_stats(self.h, ctypes.byref(s)))
+        self._check(self.lib.fa_get_stats(self.h, ctypes.byref(s), ctypes.sizeof(s)))
         return s.as_dict()
+
+    def set_option(self, name: str, value) -> None:
+        """fa_set_option: retention 'retain'|'evict', d8 'split'|'fused', block_rows 32|16,
+        walk_cap int, fill_tile 32|64."""
+        v = OPTION_VALUES.get(value, value) if isinstance(value, str) else value
+        self._check(self.lib.fa_set_option(self.h, OPTIONS[name], int(v)))
+
+    def get_option(self, name: str) -> int:
+        v = ctypes.c_int64()
+        self._check(self.lib.fa_get_option(self.h, OPTIONS[name], ctypes.byref(v)))
+        return int(v.value)
 
     # ---------------------------------------------------------------- H1
     def flowdirs(self, dem, nodata: float = -9999.0, out=None):
         rows, cols = dem.shape
+        _check(dem, "dem", ("float32",))
+        _check(out, "out", ("uint8",), (rows, cols))
         if out is None:
             out = torch.empty((rows, cols), dtype=torch.uint8, device=dem.device) if isinstance(
                 dem, torch.Tensor) else __import__("numpy").empty((rows, cols), "uint8")
@@ -174,6 +232,8 @@ class Context:
     def fill(self, dem, nodata: float = -9999.0, out=None):
         """Depression filling (Priority-Flood+epsilon surface) of a f32 DEM; device or host."""
         rows, cols = dem.shape
+        _check(dem, "dem", ("float32",))
+        _check(out, "out", ("float32",), (rows, cols))
         if out is None:
             out = torch.empty_like(dem) if isinstance(dem, torch.Tensor) else __import__("numpy").empty_like(dem)
         self._check(self.lib.fa_fill(self.h, _ptr(dem), rows, cols, float(nodata), _ptr(out)))
@@ -184,7 +244,9 @@ class Context:
                    out=None):
         src = dem if dem is not None else dirs
         rows, cols = src.shape
+        _check_inputs(dem, dirs, w, (rows, cols))
         a = ATYPES[atype]
+        _check(out, "out", (ACC_DTYPE[a],), (rows, cols))
         if out is None:
             if isinstance(src, torch.Tensor):
                 out = torch.empty((rows, cols), dtype=TORCH_ACC[a], device=src.device)
@@ -201,7 +263,9 @@ class Context:
         """The multi-GPU strip pipeline (H4-H7) run as `nstrips` strips on this device."""
         src = dem if dem is not None else dirs
         rows, cols = src.shape
+        _check_inputs(dem, dirs, w, (rows, cols))
         a = ATYPES[atype]
+        _check(out, "out", (ACC_DTYPE[a],), (rows, cols))
         if out is None:
             out = torch.empty((rows, cols), dtype=TORCH_ACC[a], device=src.device)
         self._check(self.lib.fa_accumulate_strips(self.h, int(nstrips), rows, cols, _ptr(dem), float(nodata),
@@ -215,7 +279,9 @@ class Context:
         device memory)."""
         src = dem if dem is not None else dirs
         rows, cols = src.shape
+        _check_inputs(dem, dirs, w, (rows, cols))
         a = ATYPES[atype]
+        _check(out, "out", (ACC_DTYPE[a],), (rows, cols))
         if out is None:
             if isinstance(src, torch.Tensor):
                 out = torch.empty((rows, cols), dtype=TORCH_ACC[a], pin_memory=src.is_pinned())
@@ -233,6 +299,8 @@ class Context:
         alpha: f32 raster in [0,1] (device or host, like the other inputs)."""
         src = dem if dem is not None else dirs
         rows, cols = src.shape
+        _check_inputs(dem, dirs, w, (rows, cols), alpha)
+        _check(out, "out", ("float64",), (rows, cols))
         if out is None:
             if isinstance(src, torch.Tensor):
                 out = torch.empty((rows, cols), dtype=torch.float64, device=src.device)
@@ -250,7 +318,9 @@ class Context:
         """One rank's strip of the multi-GPU accumulation (collective over all ranks)."""
         src = dem if dem is not None else dirs
         rows, cols = src.shape
+        _check_inputs(dem, dirs, w, (rows, cols))
         a = ATYPES[atype]
+        _check(out, "out", (ACC_DTYPE[a],), (rows, cols))
         if out is None:
             out = torch.empty((rows, cols), dtype=TORCH_ACC[a], device=src.device)
         buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
@@ -264,6 +334,8 @@ class Context:
         """Out-of-core absorption: host arrays in and out (numpy / CPU or pinned tensors)."""
         src = dem if dem is not None else dirs
         rows, cols = src.shape
+        _check_inputs(dem, dirs, w, (rows, cols), alpha)
+        _check(out, "out", ("float64",), (rows, cols))
         if out is None:
             if isinstance(src, torch.Tensor):
                 out = torch.empty((rows, cols), dtype=torch.float64, pin_memory=src.is_pinned())
@@ -281,6 +353,8 @@ class Context:
         """One rank's strip of the multi-GPU absorption accumulation (collective; f64 output)."""
         src = dem if dem is not None else dirs
         rows, cols = src.shape
+        _check_inputs(dem, dirs, w, (rows, cols), alpha)
+        _check(out, "out", ("float64",), (rows, cols))
         if out is None:
             out = torch.empty((rows, cols), dtype=torch.float64, device=src.device)
         buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
@@ -307,3 +381,49 @@ class Context:
                                                   _ptr(w), _wtype(w), a, _ptr(links), _ptr(at), _ptr(xo),
                                                   _ptr(acc)))
         return links, at, xo, acc
+
+
+def accumulate_dist_loopback(ctxs, global_rows: int, row_begin, dem=None, dirs=None, w=None, alpha=None,
+                             atype: str = "u32", nodata: float = -9999.0, out=None):
+    """fa_accumulate_dist_loopback: the multi-GPU path with len(ctxs) ranks run as
+    threads inside one call (one Context per rank, each with its own stream),
+    exchanging through device copies instead of NCCL.  dem / dirs / w / alpha /
+    out are per-rank lists of the ranks' strips (device tensors) or None;
+    row_begin is the per-rank list of first global rows.  Returns the list of
+    per-rank accumulation strips."""
+    lib = load()
+    n = len(ctxs)
+    per = [x for x in (dem, dirs) if x is not None][0]
+    if alpha is not None:
+        atype = "f64"
+    a = ATYPES[atype]
+    rows = [int(t.shape[0]) for t in per]
+    cols = int(per[0].shape[1])
+    for q in range(n):
+        _check_inputs(dem[q] if dem else None, dirs[q] if dirs else None, w[q] if w else None, (rows[q], cols),
+                      alpha[q] if alpha else None)
+    if out is None:
+        out = [torch.empty((rows[q], cols), dtype=TORCH_ACC[a], device=per[q].device) for q in range(n)]
+    for q in range(n):
+        _check(out[q], "out", (ACC_DTYPE[a],), (rows[q], cols))
+    P = ctypes.c_void_p
+
+    def arr(lst):
+        if lst is None:
+            return None
+        return (P * n)(*[P(t.data_ptr()) if t is not None else None for t in lst])
+
+    for lst in (dem, dirs, w, alpha, out):
+        if lst is not None:
+            for t in lst:
+                if t is not None and not t.is_contiguous():
+                    raise ValueError("tensors must be contiguous")
+    hs = (P * n)(*[c.h for c in ctxs])
+    I64 = ctypes.c_int64 * n
+    st = lib.fa_accumulate_dist_loopback(hs, n, int(global_rows), cols, I64(*[int(r) for r in row_begin]),
+                                         I64(*rows), arr(dem), float(nodata), arr(dirs), arr(w),
+                                         _wtype(w[0] if w else None), arr(alpha), arr(out), a)
+    if st != FA_OK:
+        msgs = [c.lib.fa_last_error(c.h).decode() for c in ctxs]
+        raise FaError(st, "; ".join(f"rank {q}: {m}" for q, m in enumerate(msgs) if m))
+    return out

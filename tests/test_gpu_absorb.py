@@ -78,12 +78,11 @@ def test_absorb_rejects_bad_alpha(fa_lib):
 
 
 @pytest.mark.parametrize("cap", ["1", "4", "128"])
-def test_absorb_weighted_contraction(fa_lib, cap, monkeypatch):
+def test_absorb_weighted_contraction(fa_lib, cap):
     """Deep block-exit chains: the serpentine's river crosses every block row
     (~32K chained nodes at 1024^2), so the weighted solver contracts chains
     with affine (acc, mul) pointer jumping; small walk caps force contraction
-    on a random raster's forest too (FA_WALKCAP is read per call)."""
-    monkeypatch.setenv("FA_WALKCAP", cap)
+    on a random raster's forest too (context option FA_OPT_WALK_CAP)."""
     rng = np.random.default_rng(int(cap))
     d = inputs.serpentine(1024, 1024)
     al = (0.999 + 0.001 * rng.random(d.shape)).astype(np.float32)
@@ -91,6 +90,8 @@ def test_absorb_weighted_contraction(fa_lib, cap, monkeypatch):
     ar = rng.random(r.shape).astype(np.float32)
     w = inputs.weights_f32(17, r.shape)
     with fa_lib.Context(0) as ctx:
+        ctx.set_option("walk_cap", int(cap))
+        assert ctx.get_option("walk_cap") == int(cap)
         got = ctx.accumulate_absorb(_cuda(al), dirs=_cuda(d)).cpu().numpy()
         assert ctx.stats()["contract_levels"] > 0  # the weighted chain contraction ran
         gr = ctx.accumulate_absorb(_cuda(ar), dirs=_cuda(r), w=_cuda(w)).cpu().numpy()

@@ -43,16 +43,16 @@ def test_fill_negative_nodata_blobs_and_host_buffers(fa_lib):
 
 
 @pytest.mark.parametrize("tile", ["32", "64"])
-def test_fill_deep_bowl_crosses_many_tiles(fa_lib, tile, monkeypatch):
+def test_fill_deep_bowl_crosses_many_tiles(fa_lib, tile):
     # an L1 bowl: every interior cell is raised, the fill propagates inwards
-    # across 8-16 tiles from the edge (FA_FILL_TILE: the 32x32 default and
-    # the 64x64 tile kernel)
-    monkeypatch.setenv("FA_FILL_TILE", tile)
+    # across 8-16 tiles from the edge (FA_OPT_FILL_TILE: the 32x32 default
+    # and the 64x64 tile kernel)
     H = W = 1024
     y, x = np.mgrid[0:H, 0:W]
     z = (np.abs(x - W // 2) + np.abs(y - H // 2)).astype(np.float32) * 0.01
     exp = oracle.fill(z)
     with fa_lib.Context(0) as ctx:
+        ctx.set_option("fill_tile", int(tile))
         got = ctx.fill(_cuda(z)).cpu().numpy()
     assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
     assert (exp > z).mean() > 0.4  # the inner diamond is raised to the rim level

@@ -226,3 +226,85 @@ def test_p11_f64_within_bound_of_exact_fixed_point():
     rel = np.abs(Af[data] - exact) / exact
     assert rel.max() <= h * 2.0 ** -53
     assert np.isnan(Af[~data]).all()
+
+
+# ---------------------------------------------------------------- or_stats pins
+# Workload characterisation: the height of a cell is its
+# longest upstream path (edges); an outlet is a data cell whose flow leaves
+# the grid or enters NoData (D3, D8); NoFlow cells are counted apart.  Closed
+# forms and a brute-force walk pin every output of oracle.stats.
+def _brute_stats(d):
+    """Heights by walking every cell's downstream path (height(t) = max over
+    cells upstream of t of their distance to t); outlets / NoFlow by
+    definition.  Independent of the oracle's chain-following schedule."""
+    H, W = d.shape
+    dx = [0, 0, 1, 1, 1, 0, -1, -1, -1]
+    dy = [0, -1, -1, 0, 1, 1, 1, 0, -1]
+    ht = np.zeros((H, W), np.int64)
+    outlets = noflow = 0
+    for y in range(H):
+        for x in range(W):
+            c = int(d[y, x])
+            if c == 255:
+                continue
+            if c == 0:
+                noflow += 1
+            else:
+                ty, tx = y + dy[c], x + dx[c]
+                if not (0 <= ty < H and 0 <= tx < W) or d[ty, tx] == 255:
+                    outlets += 1
+            # walk downstream: cell at distance k gets height >= k
+            cy, cx, k = y, x, 0
+            while True:
+                cc = int(d[cy, cx])
+                if cc == 0:
+                    break
+                ty, tx = cy + dy[cc], cx + dx[cc]
+                if not (0 <= ty < H and 0 <= tx < W) or d[ty, tx] == 255:
+                    break
+                cy, cx, k = ty, tx, k + 1
+                ht[cy, cx] = max(ht[cy, cx], k)
+    data = d != 255
+    return ht, data, outlets, noflow
+
+
+def test_stats_serpentine_closed_form():
+    H, W = 6, 9
+    st = oracle.stats(inputs.serpentine(H, W), nbins=8)
+    assert st["max_height"] == H * W - 1            # one chain through every cell
+    assert st["outlets"] == 1 and st["noflow"] == 0  # the last row end steps off the grid
+    assert st["max_acc"] == H * W
+    assert list(st["height_hist"][:7]) == [1] * 7 and st["height_hist"][7] == H * W - 7
+
+
+def test_stats_plane_closed_form():
+    H, W = 5, 12
+    d = np.full((H, W), 7, np.uint8)  # every cell drains west: column 0 leaves the grid
+    st = oracle.stats(d, nbins=W + 3)
+    assert st["max_height"] == W - 1 and st["outlets"] == H and st["noflow"] == 0
+    assert st["max_acc"] == W
+    assert list(st["height_hist"]) == [H] * W + [0, 0, 0]  # height of column x is W-1-x
+
+
+def test_stats_bowl_closed_form():
+    k = 6
+    n = 2 * k + 1
+    y, x = np.mgrid[0:n, 0:n]
+    d = oracle.d8((np.abs(x - k) + np.abs(y - k)).astype(np.float32))
+    st = oracle.stats(d)
+    assert st["noflow"] == 1 and st["outlets"] == 0  # everything drains into the interior centre
+    assert st["max_acc"] == n * n
+    assert st["max_height"] == k                      # diagonal steps from a corner reach the centre in k
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_stats_random_rasters_match_brute_force(seed):
+    d = inputs.random_dirs(seed, 23, 31, p_nodata=0.1, p_noflow=0.05)  # acyclic by construction
+    assert oracle.validate(d) == -1
+    ht, data, outlets, noflow = _brute_stats(d)
+    st = oracle.stats(d, nbins=16)
+    assert st["max_height"] == int(ht[data].max())
+    assert st["outlets"] == outlets and st["noflow"] == noflow
+    hist = np.bincount(np.minimum(ht[data], 15), minlength=16)
+    assert list(st["height_hist"]) == list(hist)
+    assert st["max_acc"] == int(oracle.brute(d)[data].max())
