@@ -85,16 +85,22 @@ FA_API const char* fa_last_error(const fa_ctx* ctx);
  *   FA_OPT_WALK_CAP  [128], 0..2^20: steps of a perimeter-graph walk before
  *       it re-queues (0: level-synchronous peeling only).
  *   FA_OPT_FILL_TILE  [32] | 64: tile side of fa_fill.
+ *   FA_OPT_VALUES  [FA_VALUES_L2] | FA_VALUES_SMEM: where the pass-1 /
+ *       EVICT pass-2 block kernels keep the block's values while Alg. 1 runs:
+ *       in the output raster (L2-resident, pushes as global atomics, many
+ *       warps per SM) or in shared memory (no global round trip, fewer warps).
  * Unknown option or value out of range: FA_E_ARG, the option unchanged. */
 typedef enum {
   FA_OPT_RETENTION = 1,
   FA_OPT_D8 = 2,
   FA_OPT_BLOCK_ROWS = 3,
   FA_OPT_WALK_CAP = 4,
-  FA_OPT_FILL_TILE = 5
+  FA_OPT_FILL_TILE = 5,
+  FA_OPT_VALUES = 6
 } fa_option;
 enum { FA_RETAIN = 0, FA_EVICT = 1 };
 enum { FA_D8_SPLIT = 0, FA_D8_FUSED = 1 };
+enum { FA_VALUES_L2 = 0, FA_VALUES_SMEM = 1 };
 FA_API fa_status fa_set_option(fa_ctx* ctx, int option, int64_t value);
 FA_API fa_status fa_get_option(const fa_ctx* ctx, int option, int64_t* value);
 

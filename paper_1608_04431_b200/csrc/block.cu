@@ -73,6 +73,7 @@ namespace fa {
 constexpr uint8_t kOut = 254;  // ring cell: outside the block, data
 
 constexpr uint32_t SU_STOP = 0x8000u, SU_EXIT = 0x4000u, SU_T = 0x07FFu;
+constexpr int SU_CODE_SHIFT = 11;  // bits 11-13 of an in-block successor word: its code - 1
 // direction codes (bit k) leaving a cell through its N / S / W / E side
 constexpr uint32_t DM_N = (1u << 1) | (1u << 2) | (1u << 8);
 constexpr uint32_t DM_S = (1u << 4) | (1u << 5) | (1u << 6);
@@ -111,6 +112,9 @@ struct WBT {
 template <class T, int R, bool Z>
 struct __align__(16) WSmem {
   using WB = WBT<R>;
+  using VT = T;
+  static constexpr int RR = R;
+  static constexpr bool kValues = false;  // values live in global memory (acc), not here
   struct __align__(16) U {
     float z[Z ? WB::ZN : 4];  // z window (fused D8 only)
   } u;
@@ -169,7 +173,7 @@ __device__ __forceinline__ uint32_t succ_word(int i, int d, uint32_t forb) {
   if (d == kNoData || k == 0) return SU_STOP;
   if ((forb >> k) & 1u) return SU_STOP | SU_EXIT;
   if (d & 16) return SU_STOP;  // drains into in-block NoData: dropped (D8)
-  return (uint32_t)(i + WBT<R>::offA(k));
+  return (uint32_t)(i + WBT<R>::offA(k)) | ((uint32_t)(k - 1) << SU_CODE_SHIFT);
 }
 
 __device__ __forceinline__ uint32_t forb_col(int lx, int w) {
@@ -180,8 +184,9 @@ __device__ __forceinline__ uint32_t forb_row(int ly, int h) {
 }
 
 // ---------------------------------------------------------------- staging
-template <class T, int R, bool Z>
-__device__ __forceinline__ void init_smem(WSmem<T, R, Z>& s) {
+template <class S>
+__device__ __forceinline__ void init_smem(S& s) {
+  constexpr int R = S::RR;
   uint32_t* D = reinterpret_cast<uint32_t*>(s.dirh);
   const int lane = lane_id();
   for (int i = lane; i < WBT<R>::HN / 4; i += 32) D[i] = 0xFFFFFFFFu;
@@ -315,11 +320,11 @@ __device__ __forceinline__ void ring_entries(WSmem<T, R, Z>& s, const PassArgs<T
 // directions from global (pass 2 and pass 1 from dirs) + halo ring; bad
 // codes -> NoData, flagged when `check`; with `entries`, ring codes that
 // point into the block mark entry slots
-template <class T, int R, bool Z>
-__device__ __forceinline__ void load_dirs(WSmem<T, R, Z>& s, const uint8_t* dirs, const uint8_t* dirs_up,
+template <class S>
+__device__ __forceinline__ void load_dirs(S& s, const uint8_t* dirs, const uint8_t* dirs_up,
                                           const uint8_t* dirs_dn, const Geom& g, int64_t y0, int64_t x0, int h,
                                           int w, bool check, bool entries, uint32_t* status) {
-  using WB = WBT<R>;
+  using WB = typename S::WB;
   const int lane = lane_id();
   const bool vec = w == WB::BC && ((x0 & 15) == 0) && ((g.W & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(dirs) & 15) == 0);
@@ -450,9 +455,10 @@ __device__ __forceinline__ uint32_t donor_masks(const uint32_t* D, int hw) {
 // on the block border take the scalar path (a code may leave the block
 // there).  A cell draining into in-block NoData gets STOP afterwards, from
 // the NoData cell's own donor mask (D8: that flow is dropped).
-template <bool SUCC, class T, int R, bool Z>
-__device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc, int h, int w) {
-  using WB = WBT<R>;
+template <bool SUCC, class S>
+__device__ __forceinline__ int build_masks(S& s, uint32_t& nsrc, int h, int w) {
+  using WB = typename S::WB;
+  constexpr int R = S::RR;
   constexpr int NQ = WB::BN / 128;  // words per lane
   static_assert(NQ <= 8, "source bits: 4 per word, 32 per lane");
   const int lane = lane_id();
@@ -503,8 +509,11 @@ __device__ __forceinline__ int build_masks(WSmem<T, R, Z>& s, uint32_t& nsrc, in
         ex4 &= ~stop4;
         const uint32_t sa = __byte_perm(stop4, 0u, 0x1100u), sb = __byte_perm(stop4, 0u, 0x3322u);
         const uint32_t xa = __byte_perm(ex4, 0u, 0x4140u) * 0xFFFFu, xb = __byte_perm(ex4, 0u, 0x4342u) * 0xFFFFu;
-        sw.x = (sa & 0x80008000u) | (xa & 0xC000C000u) | (~(sa | xa) & ta);
-        sw.y = (sb & 0x80008000u) | (xb & 0xC000C000u) | (~(sb | xb) & tb);
+        // code - 1 into bits 11-13 of each 16-bit word (the donor's bit in its target's mask)
+        const uint32_t cba = ((sel & 0x7u) << 11) | ((sel & 0x700u) << 19);
+        const uint32_t cbb = ((sel & 0x70000u) >> 5) | ((sel & 0x7000000u) << 3);
+        sw.x = (sa & 0x80008000u) | (xa & 0xC000C000u) | (~(sa | xa) & (ta | cba));
+        sw.y = (sb & 0x80008000u) | (xb & 0xC000C000u) | (~(sb | xb) & (tb | cbb));
       } else {
         uint32_t v[4];
         const uint32_t fr = forb_row(ly, h);
@@ -816,8 +825,8 @@ __device__ __forceinline__ void write_dirs(const WSmem<T, R, Z>& s, uint8_t* dir
 // entry's external inbound flow, D11).  Other exits become nodes (compacted,
 // one global atomic per warp).  slot_root[entry] = node of its exit.  Lane l
 // handles slots l, l+32, l+64, l+96.
-template <class T, int R, bool Z, int WK, bool ABS = false>
-__device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<T, WK>& P, int64_t b, int64_t y0,
+template <class T, int R, class S, int WK, bool ABS = false>
+__device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, int64_t b, int64_t y0,
                                               int64_t x0, int h, int w) {
   using WB = WBT<R>;
   constexpr int NJ = (WB::PB + 31) / 32;
@@ -983,7 +992,9 @@ __device__ __forceinline__ void block_records(WSmem<T, R, Z>& s, const PassArgs<
         }
         tgt = (uint32_t)(tb * WB::PB + bperim_index(tlx, tly, bh, bw));
       }
-      const T a = __ldcg(P.acc + (y0 + py) * g.W + x0 + px);
+      T a;
+      if constexpr (S::kValues) a = s.a[cell[j]];  // the block's values are on chip
+      else a = __ldcg(P.acc + (y0 + py) * g.W + x0 + px);
       if (node[j]) {
         nid = base + (uint32_t)__popc(em & lt);
         if (ABS) P.node_alpha[nid] = (float)alpha_of(cell[j]);
@@ -1067,7 +1078,7 @@ __global__ void __launch_bounds__(128, FA_P1_MINB) k_pass1(PassArgs<T, WK> P) {
     for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
     if (lane == 0 && wsum) atomicAdd(P.wsum, wsum);
   }
-  block_records<T, R, Z, WK, ABS>(s, P, b, y0, x0, h, w);
+  block_records<T, R, WSmem<T, R, Z>, WK, ABS>(s, P, b, y0, x0, h, w);
 }
 
 // ---------------------------------------------------------------- pass 2
@@ -1105,6 +1116,367 @@ __global__ void __launch_bounds__(128) k_pass2(PassArgs<T, WK> P) {
   const uint32_t popped = kahn_block(s, nsrc, P.acc + y0 * g.W + x0, g.W);
   const int tot_data = __reduce_add_sync(kFull, ndata);
   if (lane == 0 && (int)popped != tot_data) atomicOr(P.status, ST_CYCLE);
+}
+
+// ---------------------------------------------------------------- pass 1 / pass 2, values on chip
+// The block's values live in shared memory (VSmem, ~14 KB per warp for f64),
+// so the whole of Alg. 1 runs without a global-memory round trip:
+//   * in-block donor counts (one byte per cell) and successor words are
+//     built by an 8-neighbour SWAR gather, 4 cells per 32-bit word (no
+//     atomics; Alg. 1's first loop);
+//   * A = w is staged once (coalesced), NoData cells get the marker;
+//   * the queue of Alg. 1 becomes "the last donor continues": a
+//     lane takes a source and pushes its value along its successors, adding
+//     it into A(n) and decrementing n's count; when the count reaches zero
+//     A(n) is final and the lane continues from n with the value in a
+//     register; otherwise it takes the next source.  Two lanes pushing into
+//     the same cell in one iteration are ordered through a claim byte (each
+//     writes its lane, the one read back pushes, the others retry next
+//     iteration) -- so every push is a plain read-modify-write of shared
+//     memory (no atomics at all in the loop);
+//   * visibility: every iteration starts with __syncwarp (memory ordering
+//     among the warp's lanes), and within an iteration each cell's value and
+//     count are touched by one lane only;
+//   * the final values are written to the output once, coalesced (RETAIN);
+//     with EVICT pass 1 writes nothing and pass 2 reruns the block with
+//     w + x injected at its entries.
+template <class T, int R>
+struct __align__(16) VSmem {
+  using WB = WBT<R>;
+  using VT = T;
+  static constexpr int RR = R;
+  static constexpr bool kValues = true;
+  T a[WB::BN];                     // A(p): w(p) plus the pushes received so far
+  uint8_t dirh[WB::HN];            // codes + ring (as WSmem)
+  alignas(16) uint8_t cnt[WB::BN];  // pending in-block donors, one byte per cell
+  uint8_t claim[WB::BN];            // per iteration: the lane pushing into the cell
+  alignas(8) uint16_t succ[WB::BN];
+  alignas(16) uint16_t src[WB::BN];  // sources (Alg. 1's initial queue); records scratch afterwards
+  alignas(4) uint8_t need[128];
+  __device__ __forceinline__ uint32_t* slot_nid() { return reinterpret_cast<uint32_t*>(src); }
+  static_assert(WB::BN * 2 >= 256 * 4, "records scratch lives in the queue");
+};
+
+constexpr int kNWV = 2;  // warps (blocks) per CTA of the on-chip-values kernels
+
+// A = w (Eq. 1) into shared memory, NoData -> marker (D9); returns
+// sum w over data cells (integer weights: the u32 overflow check, D10)
+template <class T, int WK, class S>
+__device__ __forceinline__ unsigned long long init_values_v(S& s, const void* wp, const Geom& g, int64_t y0,
+                                                            int64_t x0, int h, int w, uint32_t* status) {
+  using WB = typename S::WB;
+  const int lane = lane_id();
+  unsigned long long wsum = 0;
+  bool bad = false;
+  const bool vec = WK != 0 && w == WB::BC && ((x0 & 3) == 0) && ((g.W & 3) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(wp) & 15) == 0);
+  const uint32_t* W32 = static_cast<const uint32_t*>(wp);
+  for (int q = lane; q < h * (WB::BC / 4); q += 32) {
+    const int ly = q >> 3, lx = (q & 7) * 4;
+    const uint32_t dw = *reinterpret_cast<const uint32_t*>(&s.dirh[WB::hidx(ly, lx)]);
+    const int64_t gi = (y0 + ly) * g.W + x0 + lx;
+    uint32_t u[4] = {1u, 1u, 1u, 1u};
+    if (WK != 0) {
+      if (vec) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(W32 + gi));
+        u[0] = v.x; u[1] = v.y; u[2] = v.z; u[3] = v.w;
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (lx + j < w) u[j] = __ldg(W32 + gi + j);
+      }
+    }
+    alignas(16) T v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int code = (dw >> (8 * j)) & 0xFF;
+      const bool data = code < kOut;
+      if constexpr (WK == 0) {
+        v[j] = (T)1;
+      } else if constexpr (WK == 1) {
+        v[j] = (T)u[j];
+        if (data) wsum += u[j];
+      } else {
+        const float f = __uint_as_float(u[j]);
+        if (data && !weight_ok<WK>(f)) bad = true;
+        v[j] = (T)f;
+      }
+      if (code == kNoData) v[j] = AccT<T>::marker();
+    }
+    if constexpr (sizeof(T) == 4) {
+      *reinterpret_cast<uint4*>(&s.a[4 * q]) = *reinterpret_cast<const uint4*>(v);
+    } else {
+      reinterpret_cast<uint4*>(&s.a[4 * q])[0] = *reinterpret_cast<const uint4*>(&v[0]);
+      reinterpret_cast<uint4*>(&s.a[4 * q])[1] = *reinterpret_cast<const uint4*>(&v[2]);
+    }
+  }
+  if (bad) atomicOr(status, ST_BADWEIGHT);
+  return wsum;
+}
+
+// In-block donor counts (one byte per cell) by an 8-neighbour SWAR gather --
+// 4 cells per 32-bit word, no atomics (Alg. 1's first loop) --
+// plus the successor words (as build_masks) and the sources queue.  Returns
+// this lane's data-cell count; nsrc = number of sources (warp total).
+template <class S>
+__device__ __forceinline__ int build_counts_v(S& s, uint32_t& nsrc, int h, int w) {
+  using WB = typename S::WB;
+  constexpr int R = S::RR;
+  constexpr int NQ = WB::BN / 128;
+  constexpr int RW = WB::HS / 4;
+  const int lane = lane_id();
+  const uint32_t* D = reinterpret_cast<const uint32_t*>(s.dirh);
+  uint32_t* C = reinterpret_cast<uint32_t*>(s.cnt);
+  int ndata = 0;
+  uint32_t srcbits = 0, ndbits = 0;
+  auto eq7 = [](uint32_t n, uint32_t c) {  // bit 7 of byte j set iff byte j of n equals c (see donor_masks)
+    const uint32_t y = ((n ^ c) & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
+    return (~(y | n) & 0x80808080u) >> 7;
+  };
+#pragma unroll 2
+  for (int k = 0; k < NQ; ++k) {
+    const int q = k * 32 + lane;
+    const int ly = q >> 3, lx0 = (q & 7) * 4;
+    const int hw = WB::hidx(ly, lx0) >> 2;
+    const uint32_t u0 = D[hw - RW - 1], u1 = D[hw - RW], u2 = D[hw - RW + 1];
+    const uint32_t c0 = D[hw - 1], c1 = D[hw], c2 = D[hw + 1];
+    const uint32_t d0 = D[hw + RW - 1], d1 = D[hw + RW], d2 = D[hw + RW + 1];
+    // count = number of neighbours n whose code is opp(direction to n)
+    uint32_t cnt = eq7(u1, 0x05050505u) + eq7(__funnelshift_r(u1, u2, 8), 0x06060606u) +
+                   eq7(__funnelshift_r(c1, c2, 8), 0x07070707u) + eq7(__funnelshift_r(d1, d2, 8), 0x08080808u) +
+                   eq7(d1, 0x01010101u) + eq7(__funnelshift_r(d0, d1, 24), 0x02020202u) +
+                   eq7(__funnelshift_r(c0, c1, 24), 0x03030303u) + eq7(__funnelshift_r(u0, u1, 24), 0x04040404u);
+    const uint32_t nd = __vcmpgeu4(c1, 0xFEFEFEFEu);  // NoData / outside the block: not a cell
+    const uint32_t inb = ly >= h ? 0u : lx0 + 4 <= w ? 0xFFFFFFFFu : lx0 >= w ? 0u : (0xFFFFFFFFu >> (8 * (lx0 + 4 - w)));
+    const uint32_t sink = nd & inb & ~__vcmpeq4(cnt, 0u);  // in-block NoData with donors: stop them below
+    ndbits |= (sink ? 1u : 0u) << k;
+    cnt &= ~nd;
+    C[q] = cnt;
+    ndata += 4 - (__popc(nd) >> 3);
+    uint2 sw;
+    if (h == WB::BR && w == WB::BC) {
+      // full block: SWAR successor words (see build_masks)
+      constexpr uint32_t T0 = 0x61412120u, T1 = 0x1F3F5F60u;
+      const uint32_t sel = __vsub4(c1, 0x01010101u) & 0x07070707u;
+      const uint32_t nib = (sel & 7u) | ((sel >> 4) & 0x70u) | ((sel >> 8) & 0x700u) | ((sel >> 12) & 0x7000u);
+      const uint32_t off4 = __byte_perm(T0, T1, nib);
+      const uint32_t i0 = 4u * (uint32_t)q - 64u;
+      const uint32_t ta = __vadd2((i0 & 0xFFFFu) | ((i0 + 1u) << 16), __byte_perm(off4, 0u, 0x4140u));
+      const uint32_t tb = __vadd2(((i0 + 2u) & 0xFFFFu) | ((i0 + 3u) << 16), __byte_perm(off4, 0u, 0x4342u));
+      const uint32_t stop4 = __vcmpeq4(c1, 0u) | __vcmpeq4(c1, 0xFFFFFFFFu);
+      uint32_t ex4 = 0;
+      if (ly == 0) ex4 |= __byte_perm(0x00000101u, 0x01000000u, nib);
+      if (ly == WB::BR - 1) ex4 |= __byte_perm(0x01000000u, 0x00000101u, nib);
+      if (lx0 == 0) ex4 |= __byte_perm(0u, 0x01010100u, nib) & 0xFFu;
+      if (lx0 == WB::BC - 4) ex4 |= __byte_perm(0x01010100u, 0u, nib) & 0xFF000000u;
+      ex4 &= ~stop4;
+      const uint32_t sa = __byte_perm(stop4, 0u, 0x1100u), sb = __byte_perm(stop4, 0u, 0x3322u);
+      const uint32_t xa = __byte_perm(ex4, 0u, 0x4140u) * 0xFFFFu, xb = __byte_perm(ex4, 0u, 0x4342u) * 0xFFFFu;
+      sw.x = (sa & 0x80008000u) | (xa & 0xC000C000u) | (~(sa | xa) & ta);
+      sw.y = (sb & 0x80008000u) | (xb & 0xC000C000u) | (~(sb | xb) & tb);
+    } else {
+      uint32_t v[4];
+      const uint32_t fr = forb_row(ly, h);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        v[j] = succ_word<R>(4 * q + j, (c1 >> (8 * j)) & 0xFF, fr | forb_col(lx0 + j, w));
+      sw.x = v[0] | (v[1] << 16);
+      sw.y = v[2] | (v[3] << 16);
+    }
+    reinterpret_cast<uint2*>(s.succ)[q] = sw;
+    const uint32_t src4 = __vcmpeq4(cnt, 0u) & ~nd & 0x80808080u;
+    srcbits |= (((src4 >> 7) & 1u) | ((src4 >> 14) & 2u) | ((src4 >> 21) & 4u) | ((src4 >> 28) & 8u)) << (4 * k);
+  }
+  if (__any_sync(kFull, ndbits != 0u)) {
+    // donors of in-block NoData cells: their flow is dropped (STOP, D8)
+    __syncwarp();
+#pragma unroll 1
+    for (int k = 0; k < NQ; ++k) {
+      if (!((ndbits >> k) & 1u)) continue;
+      const int q = k * 32 + lane;
+      const int hw = WB::hidx(q >> 3, (q & 7) * 4) >> 2;
+      const uint32_t pw = donor_masks<R>(D, hw);
+      const int ly = q >> 3, lx0 = (q & 7) * 4;
+      const uint32_t inb = ly >= h ? 0u : lx0 + 4 <= w ? 0xFFFFFFFFu : lx0 >= w ? 0u : (0xFFFFFFFFu >> (8 * (lx0 + 4 - w)));
+      const uint32_t nd = __vcmpgeu4(D[hw], 0xFEFEFEFEu) & inb;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (!((nd >> (8 * j)) & 1u)) continue;
+        uint32_t mm = (pw >> (8 * j)) & 0xFFu;
+        while (mm) {
+          const int kk = __ffs(mm);
+          mm &= mm - 1;
+          s.succ[4 * q + j + WB::offA(kk)] = (uint16_t)SU_STOP;
+        }
+      }
+    }
+  }
+  const int c = __popc(srcbits);
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += v;
+  }
+  nsrc = (uint32_t)__shfl_sync(kFull, incl, 31);
+  int pos = incl - c;
+  while (srcbits) {
+    const int bpos = __ffs(srcbits) - 1;
+    srcbits &= srcbits - 1;
+    s.src[pos++] = (uint16_t)(4 * ((bpos >> 2) * 32 + lane) + (bpos & 3));
+  }
+  return ndata;
+}
+
+// Alg. 1, "the last donor continues" with conflict-free pushes (see above).
+// Returns the number of cells retired (sources + cells whose count reached
+// zero), warp total.
+template <class S>
+__device__ __forceinline__ uint32_t kahn_push(S& s, uint32_t nsrc) {
+  using T = typename S::VT;
+  const int lane = lane_id();
+  const unsigned lt = (1u << lane) - 1u;
+  uint32_t head = 0, done = 0;
+  int cur = -1;
+  T a = (T)0;
+  for (;;) {
+    __syncwarp();
+    const unsigned idle = __ballot_sync(kFull, cur < 0);
+    if (idle == kFull && head >= nsrc) break;
+    if (cur < 0) {
+      const uint32_t r = head + (uint32_t)__popc(idle & lt);
+      if (r < nsrc) {
+        cur = s.src[r];
+        a = s.a[cur];  // a source: A = w, final
+        ++done;
+      }
+    }
+    head = min(head + (uint32_t)__popc(idle), nsrc);
+    const uint32_t su = cur >= 0 ? (uint32_t)s.succ[cur] : SU_STOP;
+    const bool go = (su & SU_STOP) == 0u;
+    if (!go) cur = -1;  // NoFlow, NoData target or a block exit: A(cur) is final and stored
+    // one pusher per target cell and iteration: every pusher writes its lane
+    // into the target's claim byte, the lane read back pushes, the others retry
+    const uint32_t t = su & SU_T;
+    if (go) s.claim[t] = (uint8_t)lane;
+    __syncwarp();
+    if (go && s.claim[t] == (uint8_t)lane) {
+      // "A(n) <- A(n) + A(c)", "decrement D(n)" (Alg. 1)
+      const T at = s.a[t] + a;
+      s.a[t] = at;
+      const uint32_t c = (uint32_t)s.cnt[t] - 1u;
+      s.cnt[t] = (uint8_t)c;
+      if (c == 0u) {  // the last donor: A(n) is final, continue from n
+        cur = (int)t;
+        a = at;
+        ++done;
+      } else {
+        cur = -1;
+      }
+    }
+  }
+  __syncwarp();
+  return __reduce_add_sync(kFull, done);
+}
+
+// the block's values to the output (16-byte rows when aligned)
+template <class T, class S>
+__device__ __forceinline__ void write_values(const S& s, T* out, const Geom& g, int64_t y0, int64_t x0, int h,
+                                             int w) {
+  using WB = typename S::WB;
+  const int lane = lane_id();
+  const bool vec = w == WB::BC && ((x0 & 3) == 0) && ((g.W & 3) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  if (vec) {
+    for (int q = lane; q < h * (WB::BC / 4); q += 32) {
+      const int ly = q >> 3, lx = (q & 7) * 4;
+      T* dst = out + (y0 + ly) * g.W + x0 + lx;
+      if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(&s.a[4 * q]);
+      } else {
+        reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(&s.a[4 * q])[0];
+        reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(&s.a[4 * q])[1];
+      }
+    }
+  } else {
+    for (int i = lane; i < h * WB::BC; i += 32) {
+      const int ly = i >> 5, lx = i & 31;
+      if (lx < w) out[(y0 + ly) * g.W + x0 + lx] = s.a[i];
+    }
+  }
+}
+
+template <class T, int R, int WK>
+__global__ void __launch_bounds__(32 * kNWV) k_pass1v(PassArgs<T, WK> P) {
+  using WB = WBT<R>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5;
+  VSmem<T, R>& s = reinterpret_cast<VSmem<T, R>*>(smem)[warp];
+  const Geom& g = P.g;
+  const int64_t b = (int64_t)blockIdx.x * kNWV + warp;
+  if (b >= g.nblocks) return;
+  const int lane = lane_id();
+  int64_t y0, x0;
+  int h, w;
+  g.block_box(b, y0, x0, h, w);
+  if (h <= 0 || w <= 0) {
+    for (int p = lane; p < WB::PB; p += 32) P.slot_root[b * WB::PB + p] = kNone;
+    return;
+  }
+  init_smem(s);
+  __syncwarp();
+  load_dirs(s, P.dirs_in, P.dirs_up, P.dirs_dn, g, y0, x0, h, w, true, true, P.status);
+  __syncwarp();
+  uint32_t nsrc;
+  const int ndata = build_counts_v(s, nsrc, h, w);
+  unsigned long long wsum = init_values_v<T, WK>(s, P.w, g, y0, x0, h, w, P.status);
+  const uint32_t popped = kahn_push(s, nsrc);
+  const int tot_data = __reduce_add_sync(kFull, ndata);
+  if (lane == 0 && (int)popped != tot_data) atomicOr(P.status, ST_CYCLE);  // a cell never became ready
+  if (!std::is_same<T, double>::value && P.wsum) {
+    if (WK == 0) wsum = lane == 0 ? (unsigned long long)tot_data : 0;
+    for (int o = 16; o; o >>= 1) wsum += __shfl_xor_sync(kFull, wsum, o);
+    if (lane == 0 && wsum) atomicAdd(P.wsum, wsum);
+  }
+  if (P.retain) write_values(s, P.acc, g, y0, x0, h, w);  // RETAIN: A_B into the output
+  block_records<T, R, VSmem<T, R>, WK>(s, P, b, y0, x0, h, w);
+}
+
+// EVICT pass 2: the block again with w + x, x = the external
+// inbound flow of each entry slot (D11, D12), values on chip
+template <class T, int R, int WK>
+__global__ void __launch_bounds__(32 * kNWV) k_pass2v(PassArgs<T, WK> P) {
+  using WB = WBT<R>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5;
+  VSmem<T, R>& s = reinterpret_cast<VSmem<T, R>*>(smem)[warp];
+  const Geom& g = P.g;
+  const int64_t b = (int64_t)blockIdx.x * kNWV + warp;
+  if (b >= g.nblocks) return;
+  const int lane = lane_id();
+  int64_t y0, x0;
+  int h, w;
+  g.block_box(b, y0, x0, h, w);
+  if (h <= 0 || w <= 0) return;
+  init_smem(s);
+  __syncwarp();
+  load_dirs(s, P.dirs_in, P.dirs_up, P.dirs_dn, g, y0, x0, h, w, false, false, P.status);
+  __syncwarp();
+  uint32_t nsrc;
+  const int ndata = build_counts_v(s, nsrc, h, w);
+  init_values_v<T, WK>(s, P.w, g, y0, x0, h, w, P.status);
+  __syncwarp();
+  const int np = bperim_count(h, w);
+  for (int p = lane; p < np; p += 32) {  // inject x at the block perimeter (distinct cells per lane)
+    int px, py;
+    bperim_xy(p, h, w, px, py);
+    if (s.dirh[WB::hidx(py, px)] == kNoData) continue;
+    s.a[py * WB::BC + px] += P.x_slot[b * WB::PB + p];
+  }
+  const uint32_t popped = kahn_push(s, nsrc);
+  const int tot_data = __reduce_add_sync(kFull, ndata);
+  if (lane == 0 && (int)popped != tot_data) atomicOr(P.status, ST_CYCLE);
+  write_values(s, P.acc, g, y0, x0, h, w);
 }
 
 // ---------------------------------------------------------------- RETAIN finalize
@@ -1291,15 +1663,27 @@ template cudaError_t launch_retain<unsigned long long>(const Geom&, const unsign
 template cudaError_t launch_retain<double>(const Geom&, const double*, const uint8_t*, double*, cudaStream_t);
 
 // ---------------------------------------------------------------- launchers
+// pass 1 from a D8 raster: the block's values on chip (k_pass1v) or in the
+// output raster (k_pass1, FA_OPT_VALUES); with D8 fused (FA_OPT_D8 =
+// FA_D8_FUSED) the z window takes the room, so the values stay in the output
+// raster (k_pass1<.., true>)
 template <class T, int R, int WK>
 cudaError_t launch_pass1_r(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t st) {
-  const size_t sm = (from_dem ? sizeof(WSmem<T, R, true>) : sizeof(WSmem<T, R, false>)) * (size_t)a.g.nw;
-  const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
   if (from_dem) {
+    const size_t sm = sizeof(WSmem<T, R, true>) * (size_t)a.g.nw;
+    const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
     auto k = k_pass1<T, R, WK, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<grid, 32 * a.g.nw, sm, st>>>(a);
+  } else if (a.vsmem) {
+    const size_t sm = sizeof(VSmem<T, R>) * (size_t)kNWV;
+    const unsigned grid = (unsigned)((a.g.nblocks + kNWV - 1) / kNWV);
+    auto k = k_pass1v<T, R, WK>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<grid, 32 * kNWV, sm, st>>>(a);
   } else {
+    const size_t sm = sizeof(WSmem<T, R, false>) * (size_t)a.g.nw;
+    const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
     auto k = k_pass1<T, R, WK, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<grid, 32 * a.g.nw, sm, st>>>(a);
@@ -1309,11 +1693,19 @@ cudaError_t launch_pass1_r(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t
 
 template <class T, int R, int WK>
 cudaError_t launch_pass2_r(const PassArgs<T, WK>& a, cudaStream_t st) {
-  const size_t sm = sizeof(WSmem<T, R, false>) * (size_t)a.g.nw;
-  const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
-  auto k = k_pass2<T, R, WK>;
+  if (!a.vsmem) {
+    const size_t sm = sizeof(WSmem<T, R, false>) * (size_t)a.g.nw;
+    const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
+    auto k = k_pass2<T, R, WK>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<grid, 32 * a.g.nw, sm, st>>>(a);
+    return cudaGetLastError();
+  }
+  const size_t sm = sizeof(VSmem<T, R>) * (size_t)kNWV;
+  const unsigned grid = (unsigned)((a.g.nblocks + kNWV - 1) / kNWV);
+  auto k = k_pass2v<T, R, WK>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k<<<grid, 32 * a.g.nw, sm, st>>>(a);
+  k<<<grid, 32 * kNWV, sm, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -142,6 +142,7 @@ struct fa_ctx {
   int opt_br = fa::kBR;
   int opt_walk_cap = 128;
   int opt_fill_tile = 32;
+  int opt_values = FA_VALUES_L2;
   bool retain() const { return opt_evict == 0; }
 };
 
@@ -305,6 +306,7 @@ fa::PassArgs<T, WK> pass_args(fa_ctx* ctx, Strip<T>& s) {
   a.x_slot = s.x_slot;
   a.acc = s.acc ? s.acc : s.acc_tmp;  // pass 1 accumulates in place (RETAIN)
   a.retain = s.acc != nullptr && ctx->retain();
+  a.vsmem = ctx->opt_values == FA_VALUES_SMEM;
   return a;
 }
 

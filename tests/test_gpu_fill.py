@@ -67,3 +67,26 @@ def test_fill_then_accumulate_pipeline(fa_lib):
         zf = ctx.fill(_cuda(z))
         A = ctx.accumulate(dem=zf, atype="u64").cpu().numpy()
     assert (A == oracle.accumulate(d)).all()
+
+
+def test_fill_serpentine_corridor_needs_many_launches(fa_lib):
+    """A 1-cell corridor snaking through the whole raster, walls 1000 m high,
+    its only outlet on the west edge: the filled surface rises one ulp per
+    corridor cell from the outlet (~512K cells), so the fill front must travel
+    the whole path -- far more launches than the old 4(H+W) guard allowed
+    (a winding depression needs ~ path length / tile side launches)."""
+    H = W = 1024
+    z = np.full((H, W), 1000.0, np.float32)
+    for y in range(1, H - 1, 2):
+        z[y, 1:W - 1] = 0.0                      # corridor rows
+        if y + 2 < H - 1:
+            x = W - 2 if (y // 2) % 2 == 0 else 1
+            z[y + 1, x] = 0.0                    # the bend to the next corridor row
+    z[1, 0] = 0.0                                # the outlet (an edge seed)
+    exp = oracle.fill(z)
+    with fa_lib.Context(0) as ctx:
+        got = ctx.fill(_cuda(z)).cpu().numpy()
+        launches = ctx.stats()["launches"]
+    assert np.array_equal(got.view(np.uint32), exp.view(np.uint32))
+    assert launches > 4 * (H + W) + 64
+    assert (exp[z == 0.0] > 0).sum() >= (z == 0.0).sum() - 1  # every corridor cell but the outlet was raised

@@ -4,7 +4,8 @@ The paper tests "with each of its memory retention strategies" (P:L654,
 strategies P:L79-81); here every shipped schedule variant -- RETAIN / EVICT,
 D8 split / fused into pass 1, 32- / 16-row blocks -- runs the same end-to-end
 cases on the single-device path, the tiled strip pipeline and the out-of-core
-path, against the CPU oracle (integers bit-exact, f64 within D13).
+path, against the CPU oracle (integers bit-exact, f64 within D13); the block
+values kept in the output raster (L2) or on chip (shared memory) as well.
 """
 import itertools
 
@@ -18,8 +19,8 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 U32M = np.uint32(0xFFFFFFFF)
-COMBOS = list(itertools.product(["retain", "evict"], ["split", "fused"], [32, 16]))
-IDS = [f"{r}-{d}-br{b}" for r, d, b in COMBOS]
+COMBOS = list(itertools.product(["retain", "evict"], ["split", "fused"], [32, 16], ["l2", "smem"]))
+IDS = [f"{r}-{d}-br{b}-{v}" for r, d, b, v in COMBOS]
 
 
 def _cuda(a):
@@ -28,12 +29,13 @@ def _cuda(a):
 
 def _ctx(fa_lib, combo, tile=(0, 0)):
     c = fa_lib.Context(0, tile=tile)
-    r, d, b = combo
+    r, d, b, v = combo
     c.set_option("retention", r)
     c.set_option("d8", d)
     c.set_option("block_rows", b)
-    assert (c.get_option("retention"), c.get_option("d8"), c.get_option("block_rows")) == (
-        fa_lib.OPTION_VALUES[r], fa_lib.OPTION_VALUES[d], b)
+    c.set_option("values", v)
+    assert (c.get_option("retention"), c.get_option("d8"), c.get_option("block_rows"), c.get_option("values")) == (
+        fa_lib.OPTION_VALUES[r], fa_lib.OPTION_VALUES[d], b, fa_lib.OPTION_VALUES[v])
     return c
 
 
@@ -92,7 +94,8 @@ def test_options_serpentine_deep_chain(fa_lib, combo):
 
 def test_option_validation(fa_lib):
     with fa_lib.Context(0) as ctx:
-        for name, bad in (("retention", 2), ("d8", 5), ("block_rows", 8), ("walk_cap", -1), ("fill_tile", 16)):
+        for name, bad in (("retention", 2), ("d8", 5), ("block_rows", 8), ("walk_cap", -1), ("fill_tile", 16),
+                          ("values", 3)):
             with pytest.raises(fa_lib.FaError) as e:
                 ctx.set_option(name, bad)
             assert e.value.status == fa_lib.FA_E_ARG
