@@ -99,9 +99,22 @@ def make_inputs(rows=None):
     return cfg, time.time() - t0
 
 
-def cpu_sample(cfg, max_rows=4096):
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_sample(cfg, max_rows=4096, characterise=False):
     """The oracle (as it stands) on a bounded sample: the first `max_rows` rows
-    of the workload, full width, D8 + fp64 accumulation (single thread)."""
+    of the workload, full width, D8 + fp64 accumulation (single thread).
+    With `characterise`, the oracle's workload statistics of the same sample
+    (longest flow path, outlets, NoFlow, max A, height
+    histogram) are added."""
     import oracle
 
     r = min(max_rows, cfg.rows)
@@ -109,11 +122,26 @@ def cpu_sample(cfg, max_rows=4096):
     w = np.ascontiguousarray(cfg.w[:r])
     t0 = time.perf_counter()
     d = oracle.d8(z)
+    t1 = time.perf_counter()
     oracle.accumulate(d, w, kind="f64")
-    dt = time.perf_counter() - t0
-    return {"value": r * cfg.cols / dt / 1e9, "unit": "Gcells/s", "cores": 1, "kind": "oracle",
-            "sample": f"rows [0,{r}) x {cfg.cols} cols of {CFG} (D8 + fp64 Kahn accumulation), "
-                      f"{dt:.1f} s"}
+    t2 = time.perf_counter()
+    cells = r * cfg.cols
+    out = {"value": cells / (t2 - t0) / 1e9, "unit": "Gcells/s", "cores": 1, "kind": "oracle",
+           "sample": f"rows [0,{r}) x {cfg.cols} cols of {CFG} (O-D8 + O-ACC fp64 Kahn, one thread), "
+                     f"{t2 - t0:.1f} s",
+           "d8_gcells_s": cells / (t1 - t0) / 1e9, "acc_gcells_s": cells / (t2 - t1) / 1e9,
+           "nproc": os.cpu_count(), "cpu_model": cpu_model()}
+    if characterise:
+        st = oracle.stats(d, nbins=16)
+        hist = [int(x) for x in st["height_hist"]]
+        data = int((d != 255).sum())
+        out["workload"] = {
+            "sample_cells": cells, "data_cells": data, "nodata_frac": round(1 - data / cells, 4),
+            "longest_flow_path": int(st["max_height"]), "outlets": int(st["outlets"]),
+            "noflow": int(st["noflow"]), "max_acc_unit_w": int(st["max_acc"]),
+            "height_hist_0_to_14_and_15plus": hist,
+            "sources_frac": round(hist[0] / data, 4)}
+    return out
 
 
 def arm_config(cfg, world):
@@ -121,6 +149,10 @@ def arm_config(cfg, world):
     return {"workload": f"{CFG}: {cfg.rows}x{cfg.cols} f32 DEM seed 4, 10% NoData, filled, f32 w -> f64, "
                         f"{cfg.tile[0]}x{cfg.tile[1]} tiles",
             "parallelism": f"row strips x{world} (NCCL)" if world > 1 else "single GPU",
+            "tiling": ("one GPU: every tile is resident, so the tiles and the perimeter graph are solved as "
+                       "one uncut graph over the 32x32 block exits (identical results, linearity); the "
+                       f"{cfg.tile[0]}x{cfg.tile[1]} tiles set the records and the strip / multi-GPU exchange")
+            if world == 1 else f"{cfg.tile[0]}x{cfg.tile[1]} tiles, tile records all-gathered (C2)",
             "l2": "inputs 8 GiB + output 8 GiB >> 126 MB L2 (no flush needed)",
             "nodata_frac": round(float(cfg.meta.get("nodata_frac", 0.0)), 4)}
 
@@ -177,6 +209,96 @@ def shared_inputs(args, world, rank):
                         dem=np.load(base + "_z.npy", mmap_mode="r"), w=np.load(base + "_w.npy", mmap_mode="r"),
                         meta={"nodata_frac": ndf})
     return cfg, gen_s
+
+
+def gpu_numa_affinity(index: int):
+    """Bind this process to the CPUs of the GPU's NUMA node, so pinned host
+    buffers are first touched (allocated) on that node; returns the node."""
+    try:
+        import torch
+
+        bus = torch.cuda.get_device_properties(index).pci_bus_id if hasattr(
+            torch.cuda.get_device_properties(index), "pci_bus_id") else None
+        if bus is None:
+            import pynvml
+
+            pynvml.nvmlInit()
+            bus = pynvml.nvmlDeviceGetPciInfo(pynvml.nvmlDeviceGetHandleByIndex(index)).busId
+            bus = bus.decode() if isinstance(bus, bytes) else bus
+        bus = bus.lower()
+        if len(bus.split(":")[0]) == 8:  # nvml: 00000000:1B:00.0 -> sysfs 0000:1b:00.0
+            bus = bus[4:]
+        node = int(open(f"/sys/bus/pci/devices/{bus}/numa_node").read())
+        if node < 0:
+            return None
+        cpus = set()
+        for part in open(f"/sys/devices/system/node/node{node}/cpulist").read().strip().split(","):
+            a, _, e = part.partition("-")
+            cpus.update(range(int(a), int(e or a) + 1))
+        os.sched_setaffinity(0, cpus)
+        return node
+    except Exception:
+        return None
+
+
+def pcie_rates(torch, stream, h_in, d_in, h_out, d_out):
+    """Copy bandwidth per direction on the bench's own pinned buffers (GB/s)."""
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    with torch.cuda.stream(stream):
+        for t, s in zip(d_in, h_in):
+            t.copy_(s, non_blocking=True)  # warm-up
+        ev[0].record(stream)
+        for t, s in zip(d_in, h_in):
+            t.copy_(s, non_blocking=True)
+        ev[1].record(stream)
+        ev[2].record(stream)
+        h_out.copy_(d_out, non_blocking=True)
+        ev[3].record(stream)
+    stream.synchronize()
+    nin = sum(t.numel() * t.element_size() for t in h_in)
+    nout = h_out.numel() * h_out.element_size()
+    return {"h2d_gbs": nin / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9,
+            "d2h_gbs": nout / (ev[2].elapsed_time(ev[3]) * 1e-3) / 1e9}
+
+
+SMALL = (("cfg0", 8, "512^2 DEM seed 1, filled, w=1 -> u32, 1 tile (launch-bound; no roofline claim)"),
+         ("cfg1", 8, "8192^2 DEM seed 2, 5% NoData, filled, w=1 -> u32, 2048^2 tiles"),
+         ("cfg2", 5, "4096^2 D8 serpentine (depth 16.7M), w=1 -> u32, 1 tile"))
+
+
+def small_configs(torch, fa, local, stream, peak, steps=10):
+    """BASELINE.json configs 0-2 on this GPU (the parity configs, timed the
+    same way as the headline: device-resident inputs, CUDA events around
+    `steps` calls of fa_accumulate, each call returning after completion)."""
+    import inputs
+
+    out = {}
+    for name, bpc, desc in SMALL:
+        cfg = inputs.make_config(name)
+        with torch.cuda.stream(stream):
+            src = torch.from_numpy(cfg.dem if cfg.dem is not None else cfg.dirs).cuda()
+            acc = torch.empty((cfg.rows, cfg.cols), dtype=torch.uint32, device="cuda")
+        stream.synchronize()
+        kw = {"dem": src} if cfg.dem is not None else {"dirs": src}
+        with fa.Context(local, stream=stream, tile=cfg.tile) as c:
+            for _ in range(3):
+                c.accumulate(atype="u32", out=acc, **kw)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(steps):
+                c.accumulate(atype="u32", out=acc, **kw)
+            e1.record(stream)
+            e1.synchronize()
+            st = c.stats()
+        ms = e0.elapsed_time(e1) / steps
+        cells = cfg.rows * cfg.cols
+        gbs = cells * bpc / (ms * 1e-3) / 1e9
+        out[name] = {"workload": desc, "value": cells / (ms * 1e-3) / 1e9, "unit": "Gcells/s", "ms_per_step": ms,
+                     "bytes_per_cell": bpc, "roofline_frac": gbs / peak,
+                     "phases_ms": {"pass1": st["ms_pass1"], "graph": st["ms_graph"], "pass2": st["ms_pass2"]},
+                     "graph_nodes": int(st["graph_nodes"]), "launches": int(st["launches"])}
+        del src, acc
+    return out
 
 
 def run_gpu(args):
@@ -249,9 +371,11 @@ def run_gpu(args):
     # z and w and D2H of A inside the timed region (the library stages host
     # buffers itself on one GPU; the multi-GPU call takes device buffers, so
     # the copies are issued here on the same stream)
+    numa = gpu_numa_affinity(local)  # pinned buffers on the GPU's NUMA node
     hz = torch.from_numpy(z_np).pin_memory()
     hw = torch.from_numpy(w_np).pin_memory()
     ha = torch.empty((nr, W), dtype=torch.float64).pin_memory()
+    pcie = pcie_rates(torch, stream, [hz, hw], [dz, dw], ha, acc)
 
     def e2e_call():
         if world > 1:
@@ -280,7 +404,10 @@ def run_gpu(args):
         e2e_ms = float(t.item())
     e2e = {"value": H * W / (e2e_ms * 1e-3) / 1e9, "unit": "Gcells/s",
            "h2d_bytes_per_step": int(hz.numel() * 4 + hw.numel() * 4) * world,
-           "d2h_bytes_per_step": int(ha.numel() * 8) * world, "ms_per_step": e2e_ms}
+           "d2h_bytes_per_step": int(ha.numel() * 8) * world, "ms_per_step": e2e_ms,
+           "pcie_h2d_gbs": round(pcie["h2d_gbs"], 1), "pcie_d2h_gbs": round(pcie["d2h_gbs"], 1),
+           "pinned_numa_node": numa,
+           "call": "fa_accumulate with pinned host buffers (the library stages them through the device)"}
 
     # ---- out-of-core path (N2): the same workload streamed from the pinned
     # host buffers one tile row (4096 rows) at a time, z and w uploaded twice
@@ -296,6 +423,7 @@ def run_gpu(args):
         so = ctx.stats()
         ooc = {"value": H * W / (ooc_ms * 1e-3) / 1e9, "unit": "Gcells/s", "ms_per_step": ooc_ms,
                "strip_rows": sr, "strips": -(-H // sr), "pcie_bytes_per_step": so["bytes_exchanged"],
+               "pcie_gbs_both_directions": so["bytes_exchanged"] / (ooc_ms * 1e-3) / 1e9,
                "call": "fa_accumulate_streamed (host buffers, pinned)"}
 
     # ---- absorption (N3): the same workload with a per-cell alpha ~ U[0.9, 1)
@@ -379,8 +507,11 @@ def run_gpu(args):
         "gpu_launches": int(np.sum(launches)) if launches and launches[0] else None,
         "input_gen_s": round(gen_s, 1),
     }
+    if world == 1 and not args.no_ooc:
+        line["configs"] = small_configs(torch, fa, local, stream, peak)
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_sample(cfg, 4096 if args.rows is None else min(4096, args.rows))
+        line["cpu_baseline"] = cpu_sample(cfg, 4096 if args.rows is None else min(4096, args.rows),
+                                          characterise=True)
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
