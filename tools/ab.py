@@ -12,8 +12,8 @@ import inputs  # noqa: E402
 from paper_1608_04431_b200 import fa  # noqa: E402
 
 rows = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
-VARIANTS = [{"values": "l2"}, {"values": "smem"}, {"values": "l2", "retention": "evict"},
-            {"values": "smem", "retention": "evict"}]
+VARIANTS = json.loads(sys.argv[2]) if len(sys.argv) > 2 else [{"values": "l2"}, {"values": "smem"}]
+NAMES = sys.argv[3].split(",") if len(sys.argv) > 3 else ["cfg1", "cfg2", "cfg3"]
 
 
 def run(ctx, kw, n=5):
@@ -27,7 +27,7 @@ def run(ctx, kw, n=5):
 
 
 out = {}
-for name in ("cfg1", "cfg2", "cfg3"):
+for name in NAMES:
     r = rows if name != "cfg2" else min(rows, 4096)
     cfg = inputs.make_config(name, r, r)
     kw = {"atype": cfg.atype}
