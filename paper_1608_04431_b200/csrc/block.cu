@@ -118,6 +118,7 @@ struct __align__(16) WSmem {
   struct __align__(16) U {
     float z[Z ? WB::ZN : 4];  // z window (fused D8 only)
   } u;
+  __device__ __forceinline__ float* zwin() { return u.z; }
   uint8_t dirh[WB::HN];
   uint32_t pend[WB::BN / 8];  // pending in-block donor counts, 4 bits per cell (<= 8)
   alignas(8) uint16_t succ[WB::BN];
@@ -197,10 +198,10 @@ __device__ __forceinline__ void init_smem(S& s) {
 // z window (block + 2-cell halo; NoData / off-grid -> NaN).  Rows of a strip
 // halo come from dem_up / dem_dn (H7); rows beyond those read as NaN and the
 // ring D8 treats them as unknown (see ring_entries).
-template <class T, int R, bool Z, int WK>
-__device__ __forceinline__ void stage_z(WSmem<T, R, Z>& s, const PassArgs<T, WK>& P, int64_t y0, int64_t x0, int h,
-                                        int w) {
-  using WB = WBT<R>;
+template <class T, int WK, class S>
+__device__ __forceinline__ void stage_z(S& s, const PassArgs<T, WK>& P, int64_t y0, int64_t x0, int h, int w) {
+  using WB = typename S::WB;
+  float* zw = s.zwin();
   const Geom& g = P.g;
   const int lane = lane_id();
   const float qnan = __int_as_float(0x7fc00000);
@@ -224,7 +225,7 @@ __device__ __forceinline__ void stage_z(WSmem<T, R, Z>& s, const PassArgs<T, WK>
           v.z = fa::stage_z(v.z, P.nodata);
           v.w = fa::stage_z(v.w, P.nodata);
         }
-        *reinterpret_cast<float4*>(&s.u.z[r * WB::ZS + 4 * k]) = v;
+        *reinterpret_cast<float4*>(&zw[r * WB::ZS + 4 * k]) = v;
       }
     }
   } else {
@@ -235,26 +236,27 @@ __device__ __forceinline__ void stage_z(WSmem<T, R, Z>& s, const PassArgs<T, WK>
       const float* row = dem_row(P.dem, P.dem_up, P.dem_dn, g.H, g.W, y0 + ly);
       float v = qnan;
       if (row && gx >= 0 && gx < g.W) v = fa::stage_z(__ldg(row + gx), P.nodata);
-      s.u.z[WB::zidx(ly, lx)] = v;
+      zw[WB::zidx(ly, lx)] = v;
     }
   }
 }
 
 // one in-block cell's D8 -> code + successor word
-template <class T, int R, bool Z>
-__device__ __forceinline__ void d8_put(WSmem<T, R, Z>& s, int ly, int lx, int d, uint32_t forb) {
-  using WB = WBT<R>;
+template <class S>
+__device__ __forceinline__ void d8_put(S& s, int ly, int lx, int d, uint32_t forb) {
+  using WB = typename S::WB;
+  constexpr int R = S::RR;
   s.dirh[WB::hidx(ly, lx)] = (uint8_t)(d == kNoData ? kNoData : (d & 15));
   s.succ[ly * WB::BC + lx] = (uint16_t)succ_word<R>(ly * WB::BC + lx, d, forb);
 }
 
 // D8 down each column with a rolling 3x3 window (codes + successor words)
-template <class T, int R, bool Z>
-__device__ __forceinline__ void d8_block(WSmem<T, R, Z>& s, int h, int w) {
-  using WB = WBT<R>;
+template <class S>
+__device__ __forceinline__ void d8_block(S& s, int h, int w) {
+  using WB = typename S::WB;
   const int lx = lane_id();
   if (lx >= w) return;
-  const float* z = s.u.z;
+  const float* z = s.zwin();
   const uint32_t fc = forb_col(lx, w);
   int zi = WB::zidx(-1, lx);
   float u0 = z[zi - 1], u1 = z[zi], u2 = z[zi + 1];
@@ -284,10 +286,10 @@ __device__ __forceinline__ void d8_block(WSmem<T, R, Z>& s, int h, int w) {
 // 254 data) and, from their D8, which perimeter cells are entries.  A ring
 // cell whose 3x3 window reaches a row this rank does not hold (beyond a strip
 // halo row) has an unknown code: all its in-block neighbours count as entries.
-template <class T, int R, bool Z, int WK>
-__device__ __forceinline__ void ring_entries(WSmem<T, R, Z>& s, const PassArgs<T, WK>& P, int64_t y0, int h, int w) {
-  using WB = WBT<R>;
-  const float* z = s.u.z;
+template <class T, int WK, class S>
+__device__ __forceinline__ void ring_entries(S& s, const PassArgs<T, WK>& P, int64_t y0, int h, int w) {
+  using WB = typename S::WB;
+  const float* z = s.zwin();
   const int rn = 2 * (w + 2) + 2 * h;
   for (int i = lane_id(); i < rn; i += 32) {
     int ly, lx;
@@ -793,10 +795,10 @@ __device__ __forceinline__ unsigned long long init_values(WSmem<T, R, Z>& s, con
 }
 
 // the block's D8 codes to global (16-byte rows when aligned)
-template <class T, int R, bool Z>
-__device__ __forceinline__ void write_dirs(const WSmem<T, R, Z>& s, uint8_t* dirs, const Geom& g, int64_t y0,
-                                           int64_t x0, int h, int w) {
-  using WB = WBT<R>;
+template <class S>
+__device__ __forceinline__ void write_dirs(const S& s, uint8_t* dirs, const Geom& g, int64_t y0, int64_t x0, int h,
+                                           int w) {
+  using WB = typename S::WB;
   const int lane = lane_id();
   const bool vec = w == WB::BC && ((x0 & 15) == 0) && ((g.W & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(dirs) & 15) == 0);
@@ -1146,7 +1148,12 @@ struct __align__(16) VSmem {
   using VT = T;
   static constexpr int RR = R;
   static constexpr bool kValues = true;
-  T a[WB::BN];                     // A(p): w(p) plus the pushes received so far
+  // A(p): w(p) plus the pushes received so far.  With D8 fused the 2-cell
+  // halo z window of the block lives here first (dead once the codes are made)
+  static constexpr int NA = (int)((WB::BN * sizeof(T) > WB::ZN * sizeof(float) ? WB::BN * sizeof(T)
+                                                                              : WB::ZN * sizeof(float)) / sizeof(T));
+  T a[NA];
+  __device__ __forceinline__ float* zwin() { return reinterpret_cast<float*>(a); }
   uint8_t dirh[WB::HN];            // codes + ring (as WSmem)
   alignas(16) uint8_t cnt[WB::BN];  // pending in-block donors, one byte per cell
   uint8_t claim[WB::BN];            // per iteration: the lane pushing into the cell
@@ -1218,7 +1225,7 @@ __device__ __forceinline__ unsigned long long init_values_v(S& s, const void* wp
 // 4 cells per 32-bit word, no atomics (Alg. 1's first loop) --
 // plus the successor words (as build_masks) and the sources queue.  Returns
 // this lane's data-cell count; nsrc = number of sources (warp total).
-template <class S>
+template <bool SUCC, class S>
 __device__ __forceinline__ int build_counts_v(S& s, uint32_t& nsrc, int h, int w) {
   using WB = typename S::WB;
   constexpr int R = S::RR;
@@ -1248,11 +1255,16 @@ __device__ __forceinline__ int build_counts_v(S& s, uint32_t& nsrc, int h, int w
                    eq7(__funnelshift_r(c0, c1, 24), 0x03030303u) + eq7(__funnelshift_r(u0, u1, 24), 0x04040404u);
     const uint32_t nd = __vcmpgeu4(c1, 0xFEFEFEFEu);  // NoData / outside the block: not a cell
     const uint32_t inb = ly >= h ? 0u : lx0 + 4 <= w ? 0xFFFFFFFFu : lx0 >= w ? 0u : (0xFFFFFFFFu >> (8 * (lx0 + 4 - w)));
-    const uint32_t sink = nd & inb & ~__vcmpeq4(cnt, 0u);  // in-block NoData with donors: stop them below
+    // in-block NoData with donors: stop them below (with fused D8 their
+    // successor words say so already: d8_put, the | 16 of an outlet code)
+    const uint32_t sink = SUCC ? (nd & inb & ~__vcmpeq4(cnt, 0u)) : 0u;
     ndbits |= (sink ? 1u : 0u) << k;
     cnt &= ~nd;
     C[q] = cnt;
     ndata += 4 - (__popc(nd) >> 3);
+    const uint32_t src4 = __vcmpeq4(cnt, 0u) & ~nd & 0x80808080u;
+    srcbits |= (((src4 >> 7) & 1u) | ((src4 >> 14) & 2u) | ((src4 >> 21) & 4u) | ((src4 >> 28) & 8u)) << (4 * k);
+    if constexpr (!SUCC) continue;
     uint2 sw;
     if (h == WB::BR && w == WB::BC) {
       // full block: SWAR successor words (see build_masks)
@@ -1284,10 +1296,8 @@ __device__ __forceinline__ int build_counts_v(S& s, uint32_t& nsrc, int h, int w
       sw.y = v[2] | (v[3] << 16);
     }
     reinterpret_cast<uint2*>(s.succ)[q] = sw;
-    const uint32_t src4 = __vcmpeq4(cnt, 0u) & ~nd & 0x80808080u;
-    srcbits |= (((src4 >> 7) & 1u) | ((src4 >> 14) & 2u) | ((src4 >> 21) & 4u) | ((src4 >> 28) & 8u)) << (4 * k);
   }
-  if (__any_sync(kFull, ndbits != 0u)) {
+  if (SUCC && __any_sync(kFull, ndbits != 0u)) {
     // donors of in-block NoData cells: their flow is dropped (STOP, D8)
     __syncwarp();
 #pragma unroll 1
@@ -1406,7 +1416,7 @@ __device__ __forceinline__ void write_values(const S& s, T* out, const Geom& g, 
   }
 }
 
-template <class T, int R, int WK>
+template <class T, int R, int WK, bool FROM_DEM = false>
 __global__ void __launch_bounds__(32 * kNWV) k_pass1v(PassArgs<T, WK> P) {
   using WB = WBT<R>;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1424,11 +1434,24 @@ __global__ void __launch_bounds__(32 * kNWV) k_pass1v(PassArgs<T, WK> P) {
     return;
   }
   init_smem(s);
-  __syncwarp();
-  load_dirs(s, P.dirs_in, P.dirs_up, P.dirs_dn, g, y0, x0, h, w, true, true, P.status);
+  if constexpr (FROM_DEM) {
+    // N1: H1 fused -- the z window is staged in the values' room, the codes
+    // and successor words come from the D8 stencil, the ring's D8 marks the
+    // entries; the codes also go to the output for the finalize
+    stage_z(s, P, y0, x0, h, w);
+    __syncwarp();
+    d8_block(s, h, w);
+    ring_entries(s, P, y0, h, w);
+    __syncwarp();
+    if (P.dirs_out) write_dirs(s, P.dirs_out, g, y0, x0, h, w);
+  } else {
+    __syncwarp();
+    load_dirs(s, P.dirs_in, P.dirs_up, P.dirs_dn, g, y0, x0, h, w, true, true, P.status);
+  }
   __syncwarp();
   uint32_t nsrc;
-  const int ndata = build_counts_v(s, nsrc, h, w);
+  const int ndata = build_counts_v<!FROM_DEM>(s, nsrc, h, w);
+  __syncwarp();  // the z window (fused D8) is dead: A = w takes its place
   unsigned long long wsum = init_values_v<T, WK>(s, P.w, g, y0, x0, h, w, P.status);
   const uint32_t popped = kahn_push(s, nsrc);
   const int tot_data = __reduce_add_sync(kFull, ndata);
@@ -1463,7 +1486,7 @@ __global__ void __launch_bounds__(32 * kNWV) k_pass2v(PassArgs<T, WK> P) {
   load_dirs(s, P.dirs_in, P.dirs_up, P.dirs_dn, g, y0, x0, h, w, false, false, P.status);
   __syncwarp();
   uint32_t nsrc;
-  const int ndata = build_counts_v(s, nsrc, h, w);
+  const int ndata = build_counts_v<true>(s, nsrc, h, w);
   init_values_v<T, WK>(s, P.w, g, y0, x0, h, w, P.status);
   __syncwarp();
   const int np = bperim_count(h, w);
@@ -1663,24 +1686,23 @@ template cudaError_t launch_retain<unsigned long long>(const Geom&, const unsign
 template cudaError_t launch_retain<double>(const Geom&, const double*, const uint8_t*, double*, cudaStream_t);
 
 // ---------------------------------------------------------------- launchers
-// pass 1 from a D8 raster: the block's values on chip (k_pass1v) or in the
-// output raster (k_pass1, FA_OPT_VALUES); with D8 fused (FA_OPT_D8 =
-// FA_D8_FUSED) the z window takes the room, so the values stay in the output
-// raster (k_pass1<.., true>)
+// pass 1: the block's values on chip (k_pass1v) or in the output raster
+// (k_pass1), FA_OPT_VALUES; either with D8 fused (FA_OPT_D8 = FA_D8_FUSED:
+// the z window staged in shared memory) or from the D8 raster
 template <class T, int R, int WK>
 cudaError_t launch_pass1_r(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t st) {
-  if (from_dem) {
+  if (a.vsmem) {
+    const size_t sm = sizeof(VSmem<T, R>) * (size_t)kNWV;
+    const unsigned grid = (unsigned)((a.g.nblocks + kNWV - 1) / kNWV);
+    auto k = from_dem ? k_pass1v<T, R, WK, true> : k_pass1v<T, R, WK, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<grid, 32 * kNWV, sm, st>>>(a);
+  } else if (from_dem) {
     const size_t sm = sizeof(WSmem<T, R, true>) * (size_t)a.g.nw;
     const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
     auto k = k_pass1<T, R, WK, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<grid, 32 * a.g.nw, sm, st>>>(a);
-  } else if (a.vsmem) {
-    const size_t sm = sizeof(VSmem<T, R>) * (size_t)kNWV;
-    const unsigned grid = (unsigned)((a.g.nblocks + kNWV - 1) / kNWV);
-    auto k = k_pass1v<T, R, WK>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<grid, 32 * kNWV, sm, st>>>(a);
   } else {
     const size_t sm = sizeof(WSmem<T, R, false>) * (size_t)a.g.nw;
     const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
