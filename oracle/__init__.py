@@ -78,6 +78,7 @@ def _L():
             "or_paper_f64": ([_P, _I, _I, _I, _I, _P, _P], ctypes.c_int),
             "or_certify_u64": ([_P, _I, _I, _P, _P], _I),
             "or_certify_f64": ([_P, _I, _I, _P, _P, ctypes.c_double, _P], _I),
+            "or_certify_rows_u64": ([_P, _I, _I, _P, _P, _I, _I, _P], _I),
             "or_stats": ([_P, _I, _I, _P, _I, _P], _I),
         }
         for name, (args, res) in sig.items():
@@ -284,3 +285,27 @@ def stats(dirs: np.ndarray, nbins: int = 64) -> dict:
         raise OracleError(5, "or_stats")
     return dict(max_height=int(mh), height_hist=hist, outlets=int(out[0]), noflow=int(out[1]),
                 max_acc=int(out[2]))
+
+
+def certify_strips(dirs_rows, acc_rows, H: int, W: int, strip: int, w_rows=None):
+    """P8 donor identity + mass balance, streamed: the raster is visited in
+    strips of `strip` rows, each with its halo rows, so host memory holds
+    O(strip * W) cells.  dirs_rows(a, b) / acc_rows(a, b) / w_rows(a, b)
+    return rows [a, b) as arrays (u8 codes; u64 or u32 accumulation; u32
+    weights or None).  Returns the number of violating cells (+1 if the mass
+    balance fails) -- equal to certify() on the whole raster."""
+    bad = 0
+    acc = np.zeros(2, np.uint64)
+    for r0 in range(0, H, strip):
+        r1 = min(H, r0 + strip)
+        a, b = max(0, r0 - 1), min(H, r1 + 1)
+        d = np.ascontiguousarray(dirs_rows(a, b), np.uint8)
+        A = np.asarray(acc_rows(a, b))
+        if A.dtype == np.uint32:
+            A64 = A.astype(np.uint64)
+            A64[A == np.uint32(0xFFFFFFFF)] = np.uint64(0xFFFFFFFFFFFFFFFF)
+        else:
+            A64 = np.ascontiguousarray(A, np.uint64)
+        wv = None if w_rows is None else np.ascontiguousarray(w_rows(a, b), np.uint32)
+        bad += int(_L().or_certify_rows_u64(_p(d), b - a, W, _p(wv), _p(A64), r0 - a, r1 - a, _p(acc)))
+    return bad + int(acc[0] != acc[1])

@@ -790,6 +790,38 @@ int64_t or_certify_u64(const uint8_t* dirs, int64_t H, int64_t W, const uint32_t
   return bad + (so != sw);
 }
 
+/* Streamed form of or_certify_u64 (P8), for rasters too large for one host
+ * buffer: the caller passes a window of nb rows (a strip plus the halo rows
+ * that exist: the row above it unless it starts the raster, the row below it
+ * unless it ends it) and checks rows [c0, c1) of the window.  Rows outside
+ * the window are off the raster for this check, which is exact because the
+ * window holds every row a checked cell's donors or target can lie in.
+ * Adds the checked cells' sum w to acc[0] and the sum of A over the checked
+ * terminal cells to acc[1]; the caller compares the totals after the last
+ * strip (mass balance).  Returns the number of violating cells.           */
+int64_t or_certify_rows_u64(const uint8_t* dirs, int64_t nb, int64_t W, const uint32_t* wt,
+                            const uint64_t* A, int64_t c0, int64_t c1, uint64_t* acc) {
+  int64_t bad = 0;
+  for (int64_t y = c0; y < c1; ++y)
+    for (int64_t x = 0; x < W; ++x) {
+      int64_t i = y * W + x;
+      if (dirs[i] == OR_NODATA) {
+        bad += A[i] != UINT64_MAX;
+        continue;
+      }
+      uint64_t wi = wt ? wt[i] : 1, s = 0;
+      acc[0] += wi;
+      for (int k = 1; k <= 8; ++k) {
+        int64_t nx = x + ODX[k], ny = y + ODY[k];
+        if (nx < 0 || ny < 0 || nx >= W || ny >= nb) continue;
+        if (o_target(dirs, W, nx, ny, 0, 0, nb, W) == i) s += A[ny * W + nx];
+      }
+      bad += A[i] != wi + s;
+      if (o_target(dirs, W, x, y, 0, 0, nb, W) < 0) acc[1] += A[i];
+    }
+  return bad;
+}
+
 /* f64 variant: |A(p) - (w(p) + sum donors)| <= rtol * A(p); returns #bad and
  * the max relative residual in *maxrel. */
 int64_t or_certify_f64(const uint8_t* dirs, int64_t H, int64_t W, const float* wt,

@@ -168,3 +168,39 @@ def test_loopback_cfg4_recipe_u64_8_ranks(fa_lib):
     exp = oracle.accumulate(d)
     exp[d == 255] = np.uint64(0xFFFFFFFFFFFFFFFF)
     assert (got == exp).all()
+
+
+@pytest.mark.slow
+def test_loopback_cfg4_recipe_32768_streamed_certificate(fa_lib):
+    """The cfg4 recipe (30 % NoData ocean, w = 1, u64, 4096^2 tiles) at 1/16
+    of cfg4's cells (32768^2) on 8 ranks, one tile row each -- the parity
+    plan of the 8-GPU run, where the host cannot hold the whole-raster
+    oracle: the streamed donor-identity certificate (P8) checks every cell
+    strip by strip (the identity with acyclicity is a complete certificate,
+    SURVEY §8(c)), with the oracle's own D8 codes."""
+    cfg = inputs.make_config("cfg4", 32768, 32768)
+    H, W = cfg.rows, cfg.cols
+    N, tile = 8, (4096, 4096)
+    bounds = [strip_bounds(H, tile[0], q, N) for q in range(N)]
+    ctxs = [fa_lib.Context(0, stream=torch.cuda.Stream(), tile=tile) for _ in range(N)]
+    try:
+        out = fa_lib.accumulate_dist_loopback(ctxs, H, [b[0] for b in bounds], dem=_split(cfg.dem, bounds),
+                                              atype="u64")
+        torch.cuda.synchronize()
+    finally:
+        for c in ctxs:
+            c.close()
+
+    def acc_rows(a, b):
+        parts = []
+        for (r0, n), o in zip(bounds, out):
+            lo, hi = max(a, r0), min(b, r0 + n)
+            if lo < hi:
+                parts.append(o[lo - r0:hi - r0].cpu().numpy())
+        return np.concatenate(parts)
+
+    def dirs_rows(a, b):
+        lo, hi = max(0, a - 1), min(H, b + 1)
+        return oracle.d8(cfg.dem[lo:hi])[a - lo:a - lo + (b - a)]
+
+    assert oracle.certify_strips(dirs_rows, acc_rows, H, W, 4096) == 0
