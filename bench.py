@@ -31,10 +31,23 @@ import numpy as np  # noqa: E402
 METRIC = "D8 flow-accum Gcells/s at 1/2/4/8 B200; achieved % of HBM roofline"
 CFG = "cfg3"
 # algorithmic bytes per cell (DESIGN.md §6 "Roofline"): each kernel's own
-# input + output, once per cell
+# input + output, once per cell.  cfg3: f32 w -> f64; cfg4: w = 1 -> u64.
+SPECS = {
+    "cfg3": {"atype": "f64", "weighted": True, "bytes_min": 16, "bytes_d8": 5, "bytes_block": 13,
+             "desc": "32768x32768 f32 DEM seed 4, 10% NoData, filled, f32 w -> f64"},
+    "cfg4": {"atype": "u64", "weighted": False, "bytes_min": 12, "bytes_d8": 5, "bytes_block": 9,
+             "desc": "131072x131072 f32 DEM seed 5, 30% NoData, filled, w = 1 -> u64"},
+}
 BYTES_MIN = 16        # z 4 + w 4 + A 8                    (whole path: method input + output)
 BYTES_D8 = 5          # z 4 -> dirs 1                      (k_d8, H1)
 BYTES_BLOCK = 13      # dirs 1 + w 4 -> A_blk 8 (in place) (k_pass1: H2-H4, RETAIN accumulation + records)
+
+
+def select_config(name):
+    global CFG, BYTES_MIN, BYTES_D8, BYTES_BLOCK
+    CFG = name
+    s = SPECS[name]
+    BYTES_MIN, BYTES_D8, BYTES_BLOCK = s["bytes_min"], s["bytes_d8"], s["bytes_block"]
 HBM_FALLBACK = 6650.0
 
 
@@ -119,15 +132,19 @@ def cpu_sample(cfg, max_rows=4096, characterise=False):
 
     r = min(max_rows, cfg.rows)
     z = np.ascontiguousarray(cfg.dem[:r])
-    w = np.ascontiguousarray(cfg.w[:r])
+    w = np.ascontiguousarray(cfg.w[:r]) if cfg.w is not None else None
     t0 = time.perf_counter()
     d = oracle.d8(z)
     t1 = time.perf_counter()
-    oracle.accumulate(d, w, kind="f64")
+    if w is not None:
+        oracle.accumulate(d, w, kind="f64")
+    else:
+        oracle.accumulate(d)
     t2 = time.perf_counter()
     cells = r * cfg.cols
     out = {"value": cells / (t2 - t0) / 1e9, "unit": "Gcells/s", "cores": 1, "kind": "oracle",
-           "sample": f"rows [0,{r}) x {cfg.cols} cols of {CFG} (O-D8 + O-ACC fp64 Kahn, one thread), "
+           "sample": f"rows [0,{r}) x {cfg.cols} cols of {CFG} (O-D8 + O-ACC "
+                     f"{'fp64' if w is not None else 'u64'} Kahn, one thread), "
                      f"{t2 - t0:.1f} s",
            "d8_gcells_s": cells / (t1 - t0) / 1e9, "acc_gcells_s": cells / (t2 - t1) / 1e9,
            "nproc": os.cpu_count(), "cpu_model": cpu_model()}
@@ -146,14 +163,15 @@ def cpu_sample(cfg, max_rows=4096, characterise=False):
 
 def arm_config(cfg, world):
     """The `config` object both arms print (the workload, no model keys)."""
-    return {"workload": f"{CFG}: {cfg.rows}x{cfg.cols} f32 DEM seed 4, 10% NoData, filled, f32 w -> f64, "
-                        f"{cfg.tile[0]}x{cfg.tile[1]} tiles",
+    return {"workload": f"{CFG}: {SPECS[CFG]['desc'].split(' ', 1)[1]}"
+                        + (f" (run at {cfg.rows}x{cfg.cols})" if cfg.rows != int(SPECS[CFG]['desc'].split('x')[0]) else "")
+                        + f", {cfg.tile[0]}x{cfg.tile[1]} tiles",
             "parallelism": f"row strips x{world} (NCCL)" if world > 1 else "single GPU",
             "tiling": ("one GPU: every tile is resident, so the tiles and the perimeter graph are solved as "
                        "one uncut graph over the 32x32 block exits (identical results, linearity); the "
                        f"{cfg.tile[0]}x{cfg.tile[1]} tiles set the records and the strip / multi-GPU exchange")
             if world == 1 else f"{cfg.tile[0]}x{cfg.tile[1]} tiles, tile records all-gathered (C2)",
-            "l2": "inputs 8 GiB + output 8 GiB >> 126 MB L2 (no flush needed)",
+            "l2": "inputs and output (GiBs) >> 126 MB L2 (no flush needed)",
             "nodata_frac": round(float(cfg.meta.get("nodata_frac", 0.0)), 4)}
 
 
@@ -173,7 +191,7 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     line = {"metric": METRIC, "value": v, "unit": "Gcells/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": SPECS[CFG]["atype"],
             "data": "synthetic", "impl": "reference",
             "config": arm_config(cfg, world),
             "cpu_baseline": cb,
@@ -195,7 +213,8 @@ def shared_inputs(args, world, rank):
     if rank == 0:
         cfg, gen_s = make_inputs(args.rows)
         np.save(base + "_z.npy", cfg.dem)
-        np.save(base + "_w.npy", cfg.w)
+        if cfg.w is not None:
+            np.save(base + "_w.npy", cfg.w)
         meta = [cfg.rows, cfg.cols, cfg.tile[0], cfg.tile[1], cfg.meta.get("nodata_frac", 0.0)]
     else:
         meta = None
@@ -205,8 +224,10 @@ def shared_inputs(args, world, rank):
     import inputs
 
     rows, cols, tr, tc, ndf = obj[0]
-    cfg = inputs.Config(name=CFG, rows=rows, cols=cols, tile=(tr, tc), atype="f64",
-                        dem=np.load(base + "_z.npy", mmap_mode="r"), w=np.load(base + "_w.npy", mmap_mode="r"),
+    spec = SPECS[CFG]
+    cfg = inputs.Config(name=CFG, rows=rows, cols=cols, tile=(tr, tc), atype=spec["atype"],
+                        dem=np.load(base + "_z.npy", mmap_mode="r"),
+                        w=np.load(base + "_w.npy", mmap_mode="r") if spec["weighted"] else None,
                         meta={"nodata_frac": ndf})
     return cfg, gen_s
 
@@ -323,21 +344,30 @@ def run_gpu(args):
         nid = fdist.broadcast_nccl_id()
     else:
         r0, nr = 0, H
+    atype = SPECS[CFG]["atype"]
+    adt = torch.float64 if atype == "f64" else torch.uint64
+    # memory: z 4 + A 8 + dirs 1 B per cell, plus ~10 B of pass-1 / graph state
+    need = nr * W * 23
+    free = torch.cuda.mem_get_info(local)[0]
+    if need > free:
+        sys.stderr.write(f"bench.py: {CFG} needs ~{need / 1e9:.0f} GB per GPU at {world} GPU(s); "
+                         f"{free / 1e9:.0f} GB free (cfg4 runs on 8 GPUs)\n")
+        sys.exit(2)
     z_np = np.ascontiguousarray(cfg.dem[r0:r0 + nr])
-    w_np = np.ascontiguousarray(cfg.w[r0:r0 + nr])
+    w_np = np.ascontiguousarray(cfg.w[r0:r0 + nr]) if cfg.w is not None else None
     stream = torch.cuda.Stream()
     ctx = fa.Context(local, stream=stream, tile=cfg.tile)
     with torch.cuda.stream(stream):
         dz = torch.from_numpy(z_np).cuda()
-        dw = torch.from_numpy(w_np).cuda()
-        acc = torch.empty((nr, W), dtype=torch.float64, device="cuda")
+        dw = torch.from_numpy(w_np).cuda() if w_np is not None else None
+        acc = torch.empty((nr, W), dtype=adt, device="cuda")
     stream.synchronize()
 
     def call(dem, w, out):
         if world > 1:
-            ctx.accumulate_dist(nid, rank, world, H, r0, dem=dem, w=w, atype="f64", out=out)
+            ctx.accumulate_dist(nid, rank, world, H, r0, dem=dem, w=w, atype=atype, out=out)
         else:
-            ctx.accumulate(dem=dem, w=w, atype="f64", out=out)
+            ctx.accumulate(dem=dem, w=w, atype=atype, out=out)
 
     for _ in range(max(args.warmup, 3)):
         call(dz, dw, acc)
@@ -373,15 +403,17 @@ def run_gpu(args):
     # the copies are issued here on the same stream)
     numa = gpu_numa_affinity(local)  # pinned buffers on the GPU's NUMA node
     hz = torch.from_numpy(z_np).pin_memory()
-    hw = torch.from_numpy(w_np).pin_memory()
-    ha = torch.empty((nr, W), dtype=torch.float64).pin_memory()
-    pcie = pcie_rates(torch, stream, [hz, hw], [dz, dw], ha, acc)
+    hw = torch.from_numpy(w_np).pin_memory() if w_np is not None else None
+    ha = torch.empty((nr, W), dtype=adt).pin_memory()
+    pcie = pcie_rates(torch, stream, [x for x in (hz, hw) if x is not None], [x for x in (dz, dw) if x is not None],
+                      ha, acc)
 
     def e2e_call():
         if world > 1:
             with torch.cuda.stream(stream):
                 dz.copy_(hz, non_blocking=True)
-                dw.copy_(hw, non_blocking=True)
+                if dw is not None:
+                    dw.copy_(hw, non_blocking=True)
             call(dz, dw, acc)
             with torch.cuda.stream(stream):
                 ha.copy_(acc, non_blocking=True)
@@ -403,7 +435,7 @@ def run_gpu(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e = {"value": H * W / (e2e_ms * 1e-3) / 1e9, "unit": "Gcells/s",
-           "h2d_bytes_per_step": int(hz.numel() * 4 + hw.numel() * 4) * world,
+           "h2d_bytes_per_step": int(hz.numel() * 4 + (hw.numel() * 4 if hw is not None else 0)) * world,
            "d2h_bytes_per_step": int(ha.numel() * 8) * world, "ms_per_step": e2e_ms,
            "pcie_h2d_gbs": round(pcie["h2d_gbs"], 1), "pcie_d2h_gbs": round(pcie["d2h_gbs"], 1),
            "pinned_numa_node": numa,
@@ -412,7 +444,8 @@ def run_gpu(args):
     # ---- out-of-core path (N2): the same workload streamed from the pinned
     # host buffers one tile row (4096 rows) at a time, z and w uploaded twice
     ooc = None
-    if world == 1 and not args.no_ooc:
+    extras = world == 1 and not args.no_ooc and CFG == "cfg3"
+    if extras:
         sr = cfg.tile[0]
         ctx.accumulate_streamed(dem=hz, w=hw, atype="f64", strip_rows=sr, out=ha)  # warm-up
         torch.cuda.synchronize()
@@ -429,7 +462,7 @@ def run_gpu(args):
     # ---- absorption (N3): the same workload with a per-cell alpha ~ U[0.9, 1)
     # (seeded, generated on the device), device-resident, library CUDA events
     absorb = None
-    if world == 1 and not args.no_ooc:
+    if extras:
         g = torch.Generator(device="cuda")
         g.manual_seed(5)
         with torch.cuda.stream(stream):
@@ -447,7 +480,7 @@ def run_gpu(args):
 
     # ---- depression filling (N4): fa_fill on cfg3's unfilled terrain (G2 + G3)
     fillm = None
-    if world == 1 and not args.no_ooc and args.rows is None:
+    if extras and args.rows is None:
         import inputs
 
         zr = inputs.terrain(4, H, W)
@@ -485,7 +518,7 @@ def run_gpu(args):
     line = {
         "metric": METRIC, "value": value, "unit": "Gcells/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": atype,
         "data": "synthetic",
         "config": arm_config(cfg, world),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -507,7 +540,7 @@ def run_gpu(args):
         "gpu_launches": int(np.sum(launches)) if launches and launches[0] else None,
         "input_gen_s": round(gen_s, 1),
     }
-    if world == 1 and not args.no_ooc:
+    if extras:
         line["configs"] = small_configs(torch, fa, local, stream, peak)
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_sample(cfg, 4096 if args.rows is None else min(4096, args.rows),
@@ -528,7 +561,17 @@ def main():
     ap.add_argument("--rows", type=int, default=None, help="smaller square variant (debug only)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ooc", action="store_true", help="skip the out-of-core and absorption measurements")
+    ap.add_argument("--config", default="cfg3", choices=sorted(SPECS),
+                    help="cfg3 (default; 1/2/4/8 GPUs) or cfg4 (17.2G cells, ~50 GB per GPU at 8 GPUs)")
+    ap.add_argument("--gen-only", action="store_true", help="time the input generation on the host and exit")
     args = ap.parse_args()
+    select_config(args.config)
+    if args.gen_only:
+        cfg, gen_s = make_inputs(args.rows)
+        print(json.dumps({"config": CFG, "rows": cfg.rows, "cols": cfg.cols, "input_gen_s": round(gen_s, 1),
+                          "cells": cfg.rows * cfg.cols, "nproc": os.cpu_count(),
+                          "nodata_frac": round(float(cfg.meta.get("nodata_frac", 0.0)), 4)}), flush=True)
+        return
     if args.impl == "reference":
         run_reference(args)
         return
