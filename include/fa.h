@@ -89,6 +89,10 @@ FA_API const char* fa_last_error(const fa_ctx* ctx);
  *       EVICT pass-2 block kernels keep the block's values while Alg. 1 runs:
  *       in the output raster (L2-resident, pushes as global atomics, many
  *       warps per SM) or in shared memory (no global round trip, fewer warps).
+ *   FA_OPT_GRAPH  [FA_GRAPH_DEVICE] | FA_GRAPH_HOST: the perimeter-graph
+ *       solver (H5) as one cooperative persistent kernel with every decision
+ *       taken on the device, or as kernels driven from the host (a device-to-
+ *       host read per decision).
  * Unknown option or value out of range: FA_E_ARG, the option unchanged. */
 typedef enum {
   FA_OPT_RETENTION = 1,
@@ -96,11 +100,13 @@ typedef enum {
   FA_OPT_BLOCK_ROWS = 3,
   FA_OPT_WALK_CAP = 4,
   FA_OPT_FILL_TILE = 5,
-  FA_OPT_VALUES = 6
+  FA_OPT_VALUES = 6,
+  FA_OPT_GRAPH = 7
 } fa_option;
 enum { FA_RETAIN = 0, FA_EVICT = 1 };
 enum { FA_D8_SPLIT = 0, FA_D8_FUSED = 1 };
 enum { FA_VALUES_L2 = 0, FA_VALUES_SMEM = 1 };
+enum { FA_GRAPH_HOST = 0, FA_GRAPH_DEVICE = 1 };
 FA_API fa_status fa_set_option(fa_ctx* ctx, int option, int64_t value);
 FA_API fa_status fa_get_option(const fa_ctx* ctx, int option, int64_t* value);
 

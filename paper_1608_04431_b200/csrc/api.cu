@@ -752,6 +752,10 @@ fa_status fa_set_option(fa_ctx* ctx, int option, int64_t value) {
       if (value != FA_VALUES_L2 && value != FA_VALUES_SMEM) break;
       ctx->opt_values = (int)value;
       return FA_OK;
+    case FA_OPT_GRAPH:
+      if (value != FA_GRAPH_HOST && value != FA_GRAPH_DEVICE) break;
+      ctx->opt_graph = (int)value;
+      return FA_OK;
     default:
       return set_err(ctx, FA_E_ARG, "unknown option");
   }
@@ -767,6 +771,7 @@ fa_status fa_get_option(const fa_ctx* ctx, int option, int64_t* value) {
     case FA_OPT_WALK_CAP: *value = ctx->opt_walk_cap; return FA_OK;
     case FA_OPT_FILL_TILE: *value = ctx->opt_fill_tile; return FA_OK;
     case FA_OPT_VALUES: *value = ctx->opt_values; return FA_OK;
+    case FA_OPT_GRAPH: *value = ctx->opt_graph; return FA_OK;
     default: return FA_E_ARG;
   }
 }

@@ -58,6 +58,9 @@ namespace fa {
 #ifndef FA_FIN_STEPS
 #define FA_FIN_STEPS 1
 #endif
+#ifndef FA_FIN_PREFETCH
+#define FA_FIN_PREFETCH 0  // L2 prefetches per block row in the finalize (0: none)
+#endif
 #ifndef FA_REC_STEPS
 #define FA_REC_STEPS 4
 #endif
@@ -1539,6 +1542,16 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
     hs[k] = ws[k] = 0;
     y0s[k] = x0s[k] = 0;
     if (b < g.nblocks) g.block_box(b, y0s[k], x0s[k], hs[k], ws[k]);
+#if FA_FIN_PREFETCH
+    // pull the block's output rows into L2 before the walks' reductions
+    // reach them (a reduction on a line not in L2 waits for its DRAM fill)
+    for (int i = lane; i < hs[k] * FA_FIN_PREFETCH; i += 32) {
+      const int ly = i / FA_FIN_PREFETCH, part = i - ly * FA_FIN_PREFETCH;
+      const T* row = acc + (y0s[k] + ly) * g.W + x0s[k];
+      const char* ptr = reinterpret_cast<const char*>(row) + part * (WB::BC * (int)sizeof(T) / FA_FIN_PREFETCH);
+      if (part * (WB::BC / FA_FIN_PREFETCH) < ws[k]) asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+    }
+#endif
     const int np = bperim_count(hs[k], ws[k]);
     for (int p0 = 0; p0 < WB::PB; p0 += 32) {
       const int p = p0 + lane;

@@ -15,6 +15,7 @@ struct Runtime {
   // statistics
   int64_t peel_rounds = 0, contract_levels = 0, jump_rounds = 0, launches = 0;
   int walk_cap = 128;  // steps per graph walk before re-queueing (FA_OPT_WALK_CAP; 0 = peel only)
+  bool device_solver = true;  // forest_dev.cu: one cooperative launch per solve (FA_OPT_GRAPH)
   cudaError_t err = cudaSuccess;
 
   template <class U>
@@ -39,6 +40,12 @@ struct Runtime {
 
 template <class T>
 cudaError_t forest_solve(Runtime& rt, uint32_t n, const uint32_t* parent, T* val);
+// the same solve as one cooperative persistent kernel (forest_dev.cu); done =
+// false when it could not run (no cooperative launch, scratch pool too small)
+template <class T>
+cudaError_t forest_solve_device(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, bool& done);
+cudaError_t forest_solve_weighted_device(Runtime& rt, uint32_t n, const uint32_t* parent, const double* wv,
+                                         double* val, bool& done);
 // absorption: S(v) = val(v) + sum_children wv(c) S(c)
 cudaError_t forest_solve_weighted(Runtime& rt, uint32_t n, const uint32_t* parent, const double* wv, double* val);
 // absorption: roots plus the product of edge weights from each node up to its root

@@ -143,6 +143,7 @@ struct fa_ctx {
   int opt_walk_cap = 128;
   int opt_fill_tile = 32;
   int opt_values = FA_VALUES_L2;
+  int opt_graph = FA_GRAPH_DEVICE;
   bool retain() const { return opt_evict == 0; }
 };
 
@@ -575,6 +576,7 @@ void reset_run(fa_ctx* ctx) {
   fa::Runtime& rt = ctx->rt;
   rt.st = ctx->st;
   rt.walk_cap = ctx->opt_walk_cap;
+  rt.device_solver = ctx->opt_graph == FA_GRAPH_DEVICE;
   rt.err = cudaSuccess;
   rt.peel_rounds = rt.contract_levels = rt.jump_rounds = rt.launches = 0;
   rt.d_status = ctx->d_small + 1;
