@@ -89,10 +89,12 @@ FA_API const char* fa_last_error(const fa_ctx* ctx);
  *       EVICT pass-2 block kernels keep the block's values while Alg. 1 runs:
  *       in the output raster (L2-resident, pushes as global atomics, many
  *       warps per SM) or in shared memory (no global round trip, fewer warps).
- *   FA_OPT_GRAPH  [FA_GRAPH_DEVICE] | FA_GRAPH_HOST: the perimeter-graph
- *       solver (H5) as one cooperative persistent kernel with every decision
- *       taken on the device, or as kernels driven from the host (a device-to-
- *       host read per decision).
+ *   FA_OPT_GRAPH  [FA_GRAPH_HOST] | FA_GRAPH_DEVICE: the perimeter-graph
+ *       solver (H5) as kernels driven from the host (a device-to-host read per
+ *       decision: frontier size, residual size, jump convergence, segments),
+ *       or as one cooperative persistent kernel taking every decision on the
+ *       device (no host round trip inside the solve; measured slower on the
+ *       large graphs: fewer walks in flight than the host-driven launches).
  * Unknown option or value out of range: FA_E_ARG, the option unchanged. */
 typedef enum {
   FA_OPT_RETENTION = 1,

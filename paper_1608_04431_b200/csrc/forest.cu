@@ -488,7 +488,7 @@ __global__ void k_root_jump(uint32_t n, const uint32_t* __restrict__ in, uint32_
 
 template <class T>
 cudaError_t forest_solve(Runtime& rt, uint32_t n, const uint32_t* parent, T* val) {
-  if (rt.device_solver) {  // one cooperative launch, no host round trip (forest_dev.cu)
+  if (rt.use_device_solver(n)) {  // one cooperative launch, no host round trip (forest_dev.cu)
     bool done = false;
     const cudaError_t e = forest_solve_device<T>(rt, n, parent, val, done);
     if (e != cudaSuccess || done) return e;
@@ -539,7 +539,7 @@ cudaError_t forest_roots(Runtime& rt, uint32_t n, const uint32_t* parent, uint32
 // S(v) = val(v) + sum_children wv(c) S(c): the same walk / peel / contract
 // solver with edge weights (affine chain contraction)
 cudaError_t forest_solve_weighted(Runtime& rt, uint32_t n, const uint32_t* parent, const double* wv, double* val) {
-  if (rt.device_solver) {
+  if (rt.use_device_solver(n)) {
     bool done = false;
     const cudaError_t e = forest_solve_weighted_device(rt, n, parent, wv, val, done);
     if (e != cudaSuccess || done) return e;

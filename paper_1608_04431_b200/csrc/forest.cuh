@@ -15,7 +15,8 @@ struct Runtime {
   // statistics
   int64_t peel_rounds = 0, contract_levels = 0, jump_rounds = 0, launches = 0;
   int walk_cap = 128;  // steps per graph walk before re-queueing (FA_OPT_WALK_CAP; 0 = peel only)
-  bool device_solver = true;  // forest_dev.cu: one cooperative launch per solve (FA_OPT_GRAPH)
+  bool device_solver = false;  // FA_OPT_GRAPH: forest_dev.cu (one cooperative launch per solve)
+  bool use_device_solver(uint32_t) const { return device_solver; }
   cudaError_t err = cudaSuccess;
 
   template <class U>

@@ -15,6 +15,12 @@
 // pool the host sizes from n; a level that would not fit sets a flag and the
 // host reruns the solve with forest.cu (never observed: the residual after
 // the walks is a small fraction of the nodes).
+//
+// Measured (FA_OPT_GRAPH = device vs the host-driven default): cfg3 32768^2
+// 3.15 vs 1.54 ms (9.26 M nodes), cfg1 8192^2 0.41 vs 0.41 ms, cfg2 0.49 vs
+// 0.51 ms, the 8-strip pipeline 31.7 vs 29.2 ms: one persistent grid keeps
+// fewer L2-latency-bound walks in flight than the host-driven launches, and
+// the host round trips it removes were not the bottleneck.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -28,6 +34,9 @@ namespace cg = cooperative_groups;
 namespace fa {
 namespace {
 
+#ifndef FA_FOREST_MINB
+#define FA_FOREST_MINB 8  // CTAs of 256 per SM: 2048 resident threads (the walks are latency-bound)
+#endif
 constexpr int kDevMaxLevels = 32;
 constexpr int kDevMaxJump = 40;
 constexpr uint64_t kDevContractRatio = 8;
@@ -100,7 +109,7 @@ __device__ __forceinline__ T* carve(uint8_t* pool, size_t& off, size_t count, si
 }
 
 template <class T, bool WG>
-__global__ void __launch_bounds__(256) k_forest_dev(DevArgs<T, WG> A) {
+__global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, WG> A) {
   cg::grid_group grid = cg::this_grid();
   const uint32_t tid = (uint32_t)grid.thread_rank();
   const uint32_t nth = (uint32_t)grid.size();
@@ -414,7 +423,7 @@ cudaError_t solve_dev(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, c
   a.cap = rt.walk_cap > 0 ? rt.walk_cap : 1;  // walk cap 0 ("peel only"): one step per round
   if (rt.err) return rt.err;
   cudaMemsetAsync(a.ctr, 0, 64 * sizeof(uint32_t), st);
-  const unsigned grid = (unsigned)(sms * std::min(per_sm, 8));
+  const unsigned grid = (unsigned)(sms * per_sm);
   void* args[] = {&a};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, grid, 256, args, 0, st);
   ++rt.launches;

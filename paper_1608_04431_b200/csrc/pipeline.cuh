@@ -143,7 +143,7 @@ struct fa_ctx {
   int opt_walk_cap = 128;
   int opt_fill_tile = 32;
   int opt_values = FA_VALUES_L2;
-  int opt_graph = FA_GRAPH_DEVICE;
+  int opt_graph = FA_GRAPH_HOST;
   bool retain() const { return opt_evict == 0; }
 };
 

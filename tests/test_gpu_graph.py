@@ -1,7 +1,7 @@
 """The perimeter-graph solver (H5; "solved using the same strategy
 described in Algorithm 1") both ways: one cooperative persistent
-kernel that takes every decision on the device (FA_OPT_GRAPH = device, the
-default) and the host-driven kernels (host).  Deep graphs force the chain
+kernel that takes every decision on the device (FA_OPT_GRAPH = device) and
+the host-driven kernels (host, the default).  Deep graphs force the chain
 contraction and its recursion; cycles must be reported; results equal the
 oracle exactly (integers) or within D13 (f64, absorption)."""
 import numpy as np

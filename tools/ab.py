@@ -16,10 +16,13 @@ VARIANTS = json.loads(sys.argv[2]) if len(sys.argv) > 2 else [{"values": "l2"}, 
 NAMES = sys.argv[3].split(",") if len(sys.argv) > 3 else ["cfg1", "cfg2", "cfg3"]
 
 
-def run(ctx, kw, n=5):
+def run(ctx, kw, n=5, strips=0):
     ts = []
     for i in range(n + 2):
-        ctx.accumulate(**kw)
+        if strips:
+            ctx.accumulate_strips(strips, **kw)
+        else:
+            ctx.accumulate(**kw)
         s = ctx.stats()
         if i >= 2:
             ts.append((s["ms_total"], s["ms_block"], s["ms_d8"], s["ms_graph"], s["ms_pass2"]))
@@ -40,8 +43,9 @@ for name in NAMES:
     for v in VARIANTS:
         with fa.Context(0, tile=cfg.tile) as ctx:
             for k, x in v.items():
-                ctx.set_option(k, x)
-            t = run(ctx, kw)
+                if k != "strips":
+                    ctx.set_option(k, x)
+            t = run(ctx, kw, strips=int(v.get("strips", 0)))
         key = f"{name}:{','.join(f'{k}={x}' for k, x in v.items())}"
         out[key] = [round(float(x), 3) for x in t]
         print(key, "total %.3f block %.3f d8 %.3f graph %.3f pass2 %.3f" % tuple(t), flush=True)
