@@ -75,8 +75,13 @@ namespace fa {
 #endif
 constexpr uint8_t kOut = 254;  // ring cell: outside the block, data
 
-constexpr uint32_t SU_STOP = 0x8000u, SU_EXIT = 0x4000u, SU_T = 0x07FFu;
-constexpr int SU_CODE_SHIFT = 11;  // bits 11-13 of an in-block successor word: its code - 1
+// Successor byte of an in-block cell: its D8 code (bits 0-3) plus
+// SB_DROP (it drains into in-block NoData: the flow is dropped, D8) and
+// SB_EXIT (its code leaves the block); NoData cells keep 255.  The cell
+// continues to an in-block data target iff the byte is a bare code 1..8,
+// and the target is the cell index plus the code's offset (sb_target).
+constexpr uint32_t SB_DROP = 0x10u, SB_EXIT = 0x20u;
+__device__ __forceinline__ bool sb_go(uint32_t sb) { return sb - 1u < 8u; }
 // direction codes (bit k) leaving a cell through its N / S / W / E side
 constexpr uint32_t DM_N = (1u << 1) | (1u << 2) | (1u << 8);
 constexpr uint32_t DM_S = (1u << 4) | (1u << 5) | (1u << 6);
@@ -105,6 +110,11 @@ struct WBT {
   static constexpr uint64_t OFFA = pack_offsets(BC);
   __device__ static __forceinline__ int offH(int d) { return (int)(int8_t)(OFFH >> (8 * (d - 1))); }
   __device__ static __forceinline__ int offA(int d) { return (int)(int8_t)(OFFA >> (8 * (d - 1))); }
+  // in-block target of cell c with bare code d (1..8): a PRMT picks the
+  // code's signed offset byte, then a sign extension
+  __device__ static __forceinline__ uint32_t target(uint32_t c, uint32_t d) {
+    return c + (uint32_t)(int32_t)(int8_t)__byte_perm((uint32_t)OFFA, (uint32_t)(OFFA >> 32), d - 1u);
+  }
   __device__ static __forceinline__ int hidx(int ly, int lx) { return (ly + 1) * HS + HOFF + lx; }
   __device__ static __forceinline__ int zidx(int ly, int lx) { return (ly + 2) * ZS + ZOFF + lx; }
   static_assert(HS <= 120 && ZS <= 120, "int8 offsets");
@@ -124,7 +134,7 @@ struct __align__(16) WSmem {
   __device__ __forceinline__ float* zwin() { return u.z; }
   uint8_t dirh[WB::HN];
   uint32_t pend[WB::BN / 8];  // pending in-block donor counts, 4 bits per cell (<= 8)
-  alignas(8) uint16_t succ[WB::BN];
+  alignas(8) uint8_t sb[WB::BN];  // successor bytes
   // ready queue of Alg. 1 (sources first; each cell enters at most once);
   // after the queue loop: [0,128) slot -> node id, [128,256) per exit slot:
   // outside donors of the entries draining to it
@@ -171,13 +181,14 @@ __device__ __forceinline__ int bperim_index(int x, int y, int h, int w) {
 }
 
 
-template <int R>
-__device__ __forceinline__ uint32_t succ_word(int i, int d, uint32_t forb) {
+// successor byte from a D8 result d (| 16: the outlet fallback, the target
+// is NoData) and the codes that leave the block from this cell (forb)
+__device__ __forceinline__ uint32_t succ_byte(int d, uint32_t forb) {
   const int k = d & 15;
-  if (d == kNoData || k == 0) return SU_STOP;
-  if ((forb >> k) & 1u) return SU_STOP | SU_EXIT;
-  if (d & 16) return SU_STOP;  // drains into in-block NoData: dropped (D8)
-  return (uint32_t)(i + WBT<R>::offA(k)) | ((uint32_t)(k - 1) << SU_CODE_SHIFT);
+  if (d == kNoData || k == 0) return (uint32_t)(d == kNoData ? kNoData : 0);
+  if ((forb >> k) & 1u) return (uint32_t)k | SB_EXIT;
+  if (d & 16) return (uint32_t)k | SB_DROP;  // drains into in-block NoData: dropped (D8)
+  return (uint32_t)k;
 }
 
 __device__ __forceinline__ uint32_t forb_col(int lx, int w) {
@@ -250,7 +261,7 @@ __device__ __forceinline__ void d8_put(S& s, int ly, int lx, int d, uint32_t for
   using WB = typename S::WB;
   constexpr int R = S::RR;
   s.dirh[WB::hidx(ly, lx)] = (uint8_t)(d == kNoData ? kNoData : (d & 15));
-  s.succ[ly * WB::BC + lx] = (uint16_t)succ_word<R>(ly * WB::BC + lx, d, forb);
+  s.sb[ly * WB::BC + lx] = (uint8_t)succ_byte(d, forb);
 }
 
 // D8 down each column with a rolling 3x3 window (codes + successor words)
@@ -492,43 +503,27 @@ __device__ __forceinline__ int build_masks(S& s, uint32_t& nsrc, int h, int w) {
     ndbits |= (sink ? 1u : 0u) << k;
     ndata += 4 - (__popc(nd) >> 3);
     if constexpr (SUCC) {
-      uint2 sw;
+      uint32_t sbw;
       if (h == WB::BR && w == WB::BC) {
-        // full block: SWAR.  Offsets of codes 1..8 (-32 -31 +1 +33 +32 +31
-        // -1 -33, row stride 32) biased by +64 to bytes, looked up 4 at a
-        // time, zero-extended to 16-bit lanes; on the block border a second
-        // lookup flags the codes that leave through that side (EXIT).
-        constexpr uint32_t T0 = 0x61412120u, T1 = 0x1F3F5F60u;
+        // full block: the successor bytes are the codes themselves, plus
+        // SB_EXIT on the block border -- a per-byte lookup (selector = code
+        // - 1) of the codes that leave the block through that side
         const uint32_t sel = __vsub4(c1, 0x01010101u) & 0x07070707u;  // code - 1 per byte (no borrow)
         const uint32_t nib = (sel & 7u) | ((sel >> 4) & 0x70u) | ((sel >> 8) & 0x700u) | ((sel >> 12) & 0x7000u);
-        const uint32_t off4 = __byte_perm(T0, T1, nib);
-        const uint32_t i0 = 4u * (uint32_t)q - 64u;
-        const uint32_t ta = __vadd2((i0 & 0xFFFFu) | ((i0 + 1u) << 16), __byte_perm(off4, 0u, 0x4140u));
-        const uint32_t tb = __vadd2(((i0 + 2u) & 0xFFFFu) | ((i0 + 3u) << 16), __byte_perm(off4, 0u, 0x4342u));
-        const uint32_t stop4 = __vcmpeq4(c1, 0u) | __vcmpeq4(c1, 0xFFFFFFFFu);
         uint32_t ex4 = 0;  // 0x01 in the bytes whose code leaves the block
         if (ly == 0) ex4 |= __byte_perm(0x00000101u, 0x01000000u, nib);           // N, NE, NW
         if (ly == WB::BR - 1) ex4 |= __byte_perm(0x01000000u, 0x00000101u, nib);  // SE, S, SW
         if (lx0 == 0) ex4 |= __byte_perm(0u, 0x01010100u, nib) & 0xFFu;           // SW, W, NW (cell 0)
         if (lx0 == WB::BC - 4) ex4 |= __byte_perm(0x01010100u, 0u, nib) & 0xFF000000u;  // NE, E, SE (cell 3)
-        ex4 &= ~stop4;
-        const uint32_t sa = __byte_perm(stop4, 0u, 0x1100u), sb = __byte_perm(stop4, 0u, 0x3322u);
-        const uint32_t xa = __byte_perm(ex4, 0u, 0x4140u) * 0xFFFFu, xb = __byte_perm(ex4, 0u, 0x4342u) * 0xFFFFu;
-        // code - 1 into bits 11-13 of each 16-bit word (the donor's bit in its target's mask)
-        const uint32_t cba = ((sel & 0x7u) << 11) | ((sel & 0x700u) << 19);
-        const uint32_t cbb = ((sel & 0x70000u) >> 5) | ((sel & 0x7000000u) << 3);
-        sw.x = (sa & 0x80008000u) | (xa & 0xC000C000u) | (~(sa | xa) & (ta | cba));
-        sw.y = (sb & 0x80008000u) | (xb & 0xC000C000u) | (~(sb | xb) & (tb | cbb));
+        const uint32_t nz = ((((c1 & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | c1) >> 7) & 0x01010101u;  // bytes != 0 (NoFlow stays 0)
+        sbw = c1 | ((ex4 & nz) << 5);  // NoData bytes stay 255
       } else {
-        uint32_t v[4];
+        sbw = 0u;
         const uint32_t fr = forb_row(ly, h);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          v[j] = succ_word<R>(4 * q + j, (c1 >> (8 * j)) & 0xFF, fr | forb_col(lx0 + j, w));
-        sw.x = v[0] | (v[1] << 16);
-        sw.y = v[2] | (v[3] << 16);
+        for (int j = 0; j < 4; ++j) sbw |= succ_byte((c1 >> (8 * j)) & 0xFF, fr | forb_col(lx0 + j, w)) << (8 * j);
       }
-      reinterpret_cast<uint2*>(s.succ)[q] = sw;
+      reinterpret_cast<uint32_t*>(s.sb)[q] = sbw;
     }
     const uint32_t src4 = __vcmpeq4(m, 0u) & ~nd & 0x80808080u;  // sources: bit 7 of each byte
     srcbits |= (((src4 >> 7) & 1u) | ((src4 >> 14) & 2u) | ((src4 >> 21) & 4u) | ((src4 >> 28) & 8u)) << (4 * k);
@@ -552,7 +547,7 @@ __device__ __forceinline__ int build_masks(S& s, uint32_t& nsrc, int h, int w) {
         while (mm) {
           const int kk = __ffs(mm);
           mm &= mm - 1;
-          s.succ[4 * q + j + WB::offA(kk)] = (uint16_t)SU_STOP;
+          s.sb[4 * q + j + WB::offA(kk)] |= (uint8_t)SB_DROP;
         }
       }
     }
@@ -622,22 +617,25 @@ __device__ __forceinline__ uint32_t kahn_chain_tail(WSmem<T, R, Z>& s, uint32_t 
     head += min((uint32_t)__popc(idle), avail);
     // phase 1: the chain ahead of c
     uint32_t cc[K];
-    uint32_t cur = (uint32_t)c, su_end = SU_STOP;
+    uint32_t cur = (uint32_t)c, end_t = 0u;
+    bool end_ok = false;  // the chain ends at a junction target end_t (else at a stop)
     int n = 0;
     bool go = c >= 0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       cc[k] = 0u;
       if (go) {
-        const uint32_t su = s.succ[cur];
-        const uint32_t t = su & SU_T;
-        go = (su & SU_STOP) == 0u && ((s.pend[t >> 3] >> ((t & 7u) * 4u)) & 0xFu) == 1u;
+        const uint32_t sbv = s.sb[cur];
+        const bool ok = sb_go(sbv);
+        const uint32_t t = ok ? WBT<R>::target(cur, sbv) : 0u;
+        go = ok && ((s.pend[t >> 3] >> ((t & 7u) * 4u)) & 0xFu) == 1u;
         if (go) {
           cc[k] = t;
           cur = t;
           n = k + 1;
         } else {
-          su_end = su;
+          end_ok = ok;
+          end_t = t;
         }
       }
     }
@@ -665,9 +663,9 @@ __device__ __forceinline__ uint32_t kahn_chain_tail(WSmem<T, R, Z>& s, uint32_t 
         c = (int)cur;  // the chain goes on: continue from its last cell next iteration
       } else {
         c = -1;
-        if ((su_end & SU_STOP) == 0u) {
+        if (end_ok) {
           // "A(n) <- A(n) + A(c)", "decrement D(n)" (Alg. 1)
-          t = su_end & SU_T;
+          t = end_t;
           g_add(Ab + (t + (t >> 5) * wm), a);
           const uint32_t sh = (t & 7u) * 4u;
           const uint32_t old = atomicAdd(&s.pend[t >> 3], 0u - (1u << sh));
@@ -711,11 +709,11 @@ __device__ __forceinline__ uint32_t kahn_block(WSmem<T, R, Z>& s, uint32_t nsrc,
     uint32_t ready = 0, t = 0;
     if (valid) {
       const uint32_t c = Q[q];
-      const uint32_t su = s.succ[c];
-      if ((su & SU_STOP) == 0u) {
+      const uint32_t sbv = s.sb[c];
+      if (sb_go(sbv)) {
         // "A(n) <- A(n) + A(c)" and "decrement D(n)" (Alg. 1);
         // A(c) is final: every donor of c was popped in an earlier iteration
-        t = su & SU_T;
+        t = WBT<R>::target(c, sbv);
         T a = __ldcg(Ab + (c + (c >> 5) * wm));
         if constexpr (ABS) a *= (T)__ldg(Alb + (c + (c >> 5) * wm));  // "alpha(n) A(n)"
         g_add(Ab + (t + (t >> 5) * wm), a);
@@ -863,7 +861,7 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
       bperim_xy(p, h, w, px, py);
       cell[j] = py * WB::BC + px;
       const bool data = s.dirh[WB::hidx(py, px)] != kNoData;
-      ex[j] = data && (s.succ[cell[j]] & SU_EXIT) != 0u;
+      ex[j] = data && (s.sb[cell[j]] & SB_EXIT) != 0u;
       if (P.cut) {  // tile records: every slot on a tile edge needs its link
         const int64_t gy = y0 + py, gx = x0 + px;
         tedge[j] = gy == t0y || gx == t0x || gy == t0y + th - 1 || gx == t0x + tw - 1;
@@ -889,7 +887,7 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
   const int nwalk = nw2 + __popc(wl[3]);
   int head = 0;
   int p = -1, c = 0;
-  uint32_t su = SU_STOP;
+  uint32_t sbv = 0u;  // successor byte of the walk's cell
   T f = (T)1;  // absorption: product of alpha along the walked path so far
   for (;;) {
     const unsigned idle = __ballot_sync(kFull, p < 0);
@@ -908,16 +906,16 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
         int px, py;
         bperim_xy(p, h, w, px, py);
         c = py * WB::BC + px;
-        su = s.succ[c];
+        sbv = s.sb[c];
         f = (T)1;
       }
     }
     head += __popc(idle);
     if (p < 0) continue;
-    if (su & SU_STOP) {
+    if (!sb_go(sbv)) {
       if (ABS) P.slot_f[b * WB::PB + p] = f;  // the entry's offset reaches its exit scaled by f
       uint32_t rp = kNoP;
-      if (su & SU_EXIT) {
+      if (sbv & SB_EXIT) {
         rp = (uint32_t)bperim_index(c & 31, c >> 5, h, w);
         // tile-records mode: an exit reached from a tile-edge slot is a node too
         const uint32_t k = s.need[p] ? s.need[p] : (P.cut ? 1u : 0u);
@@ -928,14 +926,14 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
       continue;
     }
     if (ABS) f *= alpha_of(c);
-    c = (int)(su & SU_T);
-    su = s.succ[c];
+    c = (int)WB::target((uint32_t)c, sbv);
+    sbv = s.sb[c];
 #pragma unroll
     for (int u = 1; u < FA_REC_STEPS; ++u) {  // more steps per refill round
-      if (su & SU_STOP) break;
+      if (!sb_go(sbv)) break;
       if (ABS) f *= alpha_of(c);
-      c = (int)(su & SU_T);
-      su = s.succ[c];
+      c = (int)WB::target((uint32_t)c, sbv);
+      sbv = s.sb[c];
     }
   }
   __syncwarp();
@@ -1160,7 +1158,7 @@ struct __align__(16) VSmem {
   uint8_t dirh[WB::HN];            // codes + ring (as WSmem)
   alignas(16) uint8_t cnt[WB::BN];  // pending in-block donors, one byte per cell
   uint8_t claim[WB::BN];            // per iteration: the lane pushing into the cell
-  alignas(8) uint16_t succ[WB::BN];
+  alignas(8) uint8_t sb[WB::BN];   // successor bytes
   alignas(16) uint16_t src[WB::BN];  // sources (Alg. 1's initial queue); records scratch afterwards
   alignas(4) uint8_t need[128];
   __device__ __forceinline__ uint32_t* slot_nid() { return reinterpret_cast<uint32_t*>(src); }
@@ -1268,37 +1266,25 @@ __device__ __forceinline__ int build_counts_v(S& s, uint32_t& nsrc, int h, int w
     const uint32_t src4 = __vcmpeq4(cnt, 0u) & ~nd & 0x80808080u;
     srcbits |= (((src4 >> 7) & 1u) | ((src4 >> 14) & 2u) | ((src4 >> 21) & 4u) | ((src4 >> 28) & 8u)) << (4 * k);
     if constexpr (!SUCC) continue;
-    uint2 sw;
+    uint32_t sbw;
     if (h == WB::BR && w == WB::BC) {
-      // full block: SWAR successor words (see build_masks)
-      constexpr uint32_t T0 = 0x61412120u, T1 = 0x1F3F5F60u;
+      // full block: the codes plus SB_EXIT on the border (see build_masks)
       const uint32_t sel = __vsub4(c1, 0x01010101u) & 0x07070707u;
       const uint32_t nib = (sel & 7u) | ((sel >> 4) & 0x70u) | ((sel >> 8) & 0x700u) | ((sel >> 12) & 0x7000u);
-      const uint32_t off4 = __byte_perm(T0, T1, nib);
-      const uint32_t i0 = 4u * (uint32_t)q - 64u;
-      const uint32_t ta = __vadd2((i0 & 0xFFFFu) | ((i0 + 1u) << 16), __byte_perm(off4, 0u, 0x4140u));
-      const uint32_t tb = __vadd2(((i0 + 2u) & 0xFFFFu) | ((i0 + 3u) << 16), __byte_perm(off4, 0u, 0x4342u));
-      const uint32_t stop4 = __vcmpeq4(c1, 0u) | __vcmpeq4(c1, 0xFFFFFFFFu);
       uint32_t ex4 = 0;
       if (ly == 0) ex4 |= __byte_perm(0x00000101u, 0x01000000u, nib);
       if (ly == WB::BR - 1) ex4 |= __byte_perm(0x01000000u, 0x00000101u, nib);
       if (lx0 == 0) ex4 |= __byte_perm(0u, 0x01010100u, nib) & 0xFFu;
       if (lx0 == WB::BC - 4) ex4 |= __byte_perm(0x01010100u, 0u, nib) & 0xFF000000u;
-      ex4 &= ~stop4;
-      const uint32_t sa = __byte_perm(stop4, 0u, 0x1100u), sb = __byte_perm(stop4, 0u, 0x3322u);
-      const uint32_t xa = __byte_perm(ex4, 0u, 0x4140u) * 0xFFFFu, xb = __byte_perm(ex4, 0u, 0x4342u) * 0xFFFFu;
-      sw.x = (sa & 0x80008000u) | (xa & 0xC000C000u) | (~(sa | xa) & ta);
-      sw.y = (sb & 0x80008000u) | (xb & 0xC000C000u) | (~(sb | xb) & tb);
+      const uint32_t nz = ((((c1 & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | c1) >> 7) & 0x01010101u;
+      sbw = c1 | ((ex4 & nz) << 5);
     } else {
-      uint32_t v[4];
+      sbw = 0u;
       const uint32_t fr = forb_row(ly, h);
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        v[j] = succ_word<R>(4 * q + j, (c1 >> (8 * j)) & 0xFF, fr | forb_col(lx0 + j, w));
-      sw.x = v[0] | (v[1] << 16);
-      sw.y = v[2] | (v[3] << 16);
+      for (int j = 0; j < 4; ++j) sbw |= succ_byte((c1 >> (8 * j)) & 0xFF, fr | forb_col(lx0 + j, w)) << (8 * j);
     }
-    reinterpret_cast<uint2*>(s.succ)[q] = sw;
+    reinterpret_cast<uint32_t*>(s.sb)[q] = sbw;
   }
   if (SUCC && __any_sync(kFull, ndbits != 0u)) {
     // donors of in-block NoData cells: their flow is dropped (STOP, D8)
@@ -1319,7 +1305,7 @@ __device__ __forceinline__ int build_counts_v(S& s, uint32_t& nsrc, int h, int w
         while (mm) {
           const int kk = __ffs(mm);
           mm &= mm - 1;
-          s.succ[4 * q + j + WB::offA(kk)] = (uint16_t)SU_STOP;
+          s.sb[4 * q + j + WB::offA(kk)] |= (uint8_t)SB_DROP;
         }
       }
     }
@@ -1347,6 +1333,7 @@ __device__ __forceinline__ int build_counts_v(S& s, uint32_t& nsrc, int h, int w
 template <class S>
 __device__ __forceinline__ uint32_t kahn_push(S& s, uint32_t nsrc) {
   using T = typename S::VT;
+  using WB = typename S::WB;
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   uint32_t head = 0, done = 0;
@@ -1365,12 +1352,12 @@ __device__ __forceinline__ uint32_t kahn_push(S& s, uint32_t nsrc) {
       }
     }
     head = min(head + (uint32_t)__popc(idle), nsrc);
-    const uint32_t su = cur >= 0 ? (uint32_t)s.succ[cur] : SU_STOP;
-    const bool go = (su & SU_STOP) == 0u;
+    const uint32_t sbv = cur >= 0 ? (uint32_t)s.sb[cur] : 0u;
+    const bool go = sb_go(sbv);
     if (!go) cur = -1;  // NoFlow, NoData target or a block exit: A(cur) is final and stored
     // one pusher per target cell and iteration: every pusher writes its lane
     // into the target's claim byte, the lane read back pushes, the others retry
-    const uint32_t t = su & SU_T;
+    const uint32_t t = go ? WB::target((uint32_t)cur, sbv) : 0u;
     if (go) s.claim[t] = (uint8_t)lane;
     __syncwarp();
     if (go && s.claim[t] == (uint8_t)lane) {
