@@ -59,7 +59,9 @@ namespace fa {
 #define FA_FIN_STEPS 1
 #endif
 #ifndef FA_FIN_PREFETCH
-#define FA_FIN_PREFETCH 0  // L2 prefetches per block row in the finalize (0: none)
+// L2 prefetches per block row at the start of the finalize (0: none).  cfg3:
+// 0 / 1 / 2 / 4 / 8 -> 3.85 / 3.81 / 3.11 / 3.07 / 3.10 ms
+#define FA_FIN_PREFETCH 4
 #endif
 #ifndef FA_REC_STEPS
 #define FA_REC_STEPS 4
@@ -1531,7 +1533,9 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
     if (b < g.nblocks) g.block_box(b, y0s[k], x0s[k], hs[k], ws[k]);
 #if FA_FIN_PREFETCH
     // pull the block's output rows into L2 before the walks' reductions
-    // reach them (a reduction on a line not in L2 waits for its DRAM fill)
+    // reach them: a reduction on a line that is not in L2 waits for its DRAM
+    // fill inside the L2 atomic unit, while prefetches stream (the rows were
+    // written by pass 1 long ago and are cold)
     for (int i = lane; i < hs[k] * FA_FIN_PREFETCH; i += 32) {
       const int ly = i / FA_FIN_PREFETCH, part = i - ly * FA_FIN_PREFETCH;
       const T* row = acc + (y0s[k] + ly) * g.W + x0s[k];
