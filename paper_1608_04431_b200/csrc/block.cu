@@ -75,6 +75,9 @@ namespace fa {
 #ifndef FA_P1_MINB
 #define FA_P1_MINB 8
 #endif
+#ifndef FA_P1_PREFETCH
+#define FA_P1_PREFETCH 1  // pass 1 L2 prefetches: 1 the block's weight rows, 2 the neighbours' entry offsets
+#endif
 constexpr uint8_t kOut = 254;  // ring cell: outside the block, data
 
 // Successor byte of an in-block cell: its D8 code (bits 0-3) plus
@@ -1046,6 +1049,25 @@ __global__ void __launch_bounds__(128, FA_P1_MINB) k_pass1(PassArgs<T, WK> P) {
     for (int p = lane; p < WB::PB; p += 32) P.slot_root[b * WB::PB + p] = kNone;
     return;
   }
+#if FA_P1_PREFETCH & 1
+  // the block's weight rows are read only after the codes are staged and the
+  // donor masks built: start their DRAM reads now
+  if (WK != 0 && lane < h) {
+    const char* wrow = static_cast<const char*>(P.w) + ((y0 + lane) * g.W + x0) * 4;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(wrow));
+  }
+#endif
+#if FA_P1_PREFETCH & 2
+  // the entry offsets of the 4 neighbour blocks: the leaf exits' reductions
+  // (block_records) land there
+  {
+    constexpr int LINES = (WB::PB * (int)sizeof(T) + 127) / 128;
+    const int nb = lane / 8, ln = lane % 8;
+    const int64_t tb = nb == 0 ? b - 1 : nb == 1 ? b + 1 : nb == 2 ? b - g.NBC : b + g.NBC;
+    if (ln < LINES && tb >= 0 && tb < g.nblocks)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(P.x_slot + tb * WB::PB) + ln * 128));
+  }
+#endif
   init_smem(s);
   if (FROM_DEM) {
     stage_z(s, P, y0, x0, h, w);
