@@ -95,6 +95,12 @@ FA_API const char* fa_last_error(const fa_ctx* ctx);
  *       or as one cooperative persistent kernel taking every decision on the
  *       device (no host round trip inside the solve; measured slower on the
  *       large graphs: fewer walks in flight than the host-driven launches).
+ *   FA_OPT_DIST_RECORDS  [FA_DIST_STRIPS] | FA_DIST_TILES: the record
+ *       granularity of the multi-GPU exchange -- each rank's strip as one
+ *       tile (the strip's block-exit graph cut only at its edges, records =
+ *       the strip perimeter, the producer graph over N strips; needs equal
+ *       strips, the last may be shorter, else the tiles are used) or the
+ *       context's tiles (every tile's perimeter all-gathered).
  * Unknown option or value out of range: FA_E_ARG, the option unchanged. */
 typedef enum {
   FA_OPT_RETENTION = 1,
@@ -103,12 +109,14 @@ typedef enum {
   FA_OPT_WALK_CAP = 4,
   FA_OPT_FILL_TILE = 5,
   FA_OPT_VALUES = 6,
-  FA_OPT_GRAPH = 7
+  FA_OPT_GRAPH = 7,
+  FA_OPT_DIST_RECORDS = 8
 } fa_option;
 enum { FA_RETAIN = 0, FA_EVICT = 1 };
 enum { FA_D8_SPLIT = 0, FA_D8_FUSED = 1 };
 enum { FA_VALUES_L2 = 0, FA_VALUES_SMEM = 1 };
 enum { FA_GRAPH_HOST = 0, FA_GRAPH_DEVICE = 1 };
+enum { FA_DIST_TILES = 0, FA_DIST_STRIPS = 1 };
 FA_API fa_status fa_set_option(fa_ctx* ctx, int option, int64_t value);
 FA_API fa_status fa_get_option(const fa_ctx* ctx, int option, int64_t* value);
 

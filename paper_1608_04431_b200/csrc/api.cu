@@ -756,6 +756,10 @@ fa_status fa_set_option(fa_ctx* ctx, int option, int64_t value) {
       if (value != FA_GRAPH_HOST && value != FA_GRAPH_DEVICE) break;
       ctx->opt_graph = (int)value;
       return FA_OK;
+    case FA_OPT_DIST_RECORDS:
+      if (value != FA_DIST_TILES && value != FA_DIST_STRIPS) break;
+      ctx->opt_dist_records = (int)value;
+      return FA_OK;
     default:
       return set_err(ctx, FA_E_ARG, "unknown option");
   }
@@ -772,6 +776,7 @@ fa_status fa_get_option(const fa_ctx* ctx, int option, int64_t* value) {
     case FA_OPT_FILL_TILE: *value = ctx->opt_fill_tile; return FA_OK;
     case FA_OPT_VALUES: *value = ctx->opt_values; return FA_OK;
     case FA_OPT_GRAPH: *value = ctx->opt_graph; return FA_OK;
+    case FA_OPT_DIST_RECORDS: *value = ctx->opt_dist_records; return FA_OK;
     default: return FA_E_ARG;
   }
 }

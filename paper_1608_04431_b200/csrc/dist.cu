@@ -209,7 +209,7 @@ struct LoopTransport final : Transport {
 // C0: one rank's call, as every rank must see it
 struct DistHdr {
   int64_t global_rows, cols, row_begin, local_rows, tile_r, tile_c;
-  int32_t wtype, atype, from_dem, alpha, br, ok;
+  int32_t wtype, atype, from_dem, alpha, br, ok, records, pad;
 };
 // C3: after phase A / at the end
 struct DistStat {
@@ -301,7 +301,22 @@ fa_status run_dist(fa_ctx* ctx, Transport& tp, const DistCall& c) {
   reset_run(ctx);
   CK(cudaMemsetAsync(ctx->d_small, 0, 16 * sizeof(uint32_t), st));
   CK(cudaEventRecord(ctx->ev[0], st));
-  const Geom gg = make_geom(GH, W, ctx->tile_r, ctx->tile_c, c.alpha ? kBR : ctx->opt_br);
+  // Record granularity (FA_OPT_DIST_RECORDS): the context's tiles, or each
+  // strip as ONE tile (strip-level records): the block-exit
+  // graph is then cut only at strip edges, the records are the strips'
+  // perimeters and the producer graph G2 has N tiles instead of TR x TC.
+  // Strip tiles need equal strips (the last may be shorter); otherwise the
+  // context's tiling is used.
+  int64_t th = ctx->tile_r, tw = ctx->tile_c;
+  if (ctx->opt_dist_records == FA_DIST_STRIPS && nranks > 1) {
+    bool equal = true;
+    for (int q = 0; q + 1 < nranks; ++q) equal = equal && c.hdr[q].local_rows == c.hdr[0].local_rows;
+    if (equal && (nranks == 1 || c.hdr[nranks - 1].local_rows <= c.hdr[0].local_rows)) {
+      th = c.hdr[0].local_rows;
+      tw = W;
+    }
+  }
+  const Geom gg = make_geom(GH, W, th, tw, c.alpha ? kBR : ctx->opt_br);
   // every rank's first slot, from the agreed partition (C0)
   std::vector<int64_t> hbase;
   const int64_t nslots = tile_perim_total(gg, &hbase);
@@ -457,7 +472,8 @@ fa_status run_dist(fa_ctx* ctx, Transport& tp, const DistCall& c) {
 // by rank.  All ranks return the same verdict.
 fa_status agree_call(fa_ctx* ctx, Transport& tp, DistCall& c, fa_wtype wtype, fa_atype atype, bool local_ok) {
   DistHdr h{c.GH, c.W, c.row_begin, c.H, ctx->tile_r, ctx->tile_c, (int32_t)wtype, (int32_t)atype,
-            c.dem != nullptr, c.alpha != nullptr, c.alpha ? fa::kBR : ctx->opt_br, local_ok ? 1 : 0};
+            c.dem != nullptr, c.alpha != nullptr, c.alpha ? fa::kBR : ctx->opt_br, local_ok ? 1 : 0,
+            ctx->opt_dist_records, 0};
   const std::string own_err = ctx->err;
   c.hdr.assign(tp.nranks, DistHdr{});
   FS(tp.gather_host(ctx, &h, c.hdr.data(), sizeof(DistHdr)));
@@ -472,7 +488,8 @@ fa_status agree_call(fa_ctx* ctx, Transport& tp, DistCall& c, fa_wtype wtype, fa
   for (int q = 0; q < tp.nranks; ++q) {
     const DistHdr& b = c.hdr[q];
     if (b.global_rows != a.global_rows || b.cols != a.cols || b.tile_r != a.tile_r || b.tile_c != a.tile_c ||
-        b.wtype != a.wtype || b.atype != a.atype || b.from_dem != a.from_dem || b.alpha != a.alpha || b.br != a.br)
+        b.wtype != a.wtype || b.atype != a.atype || b.from_dem != a.from_dem || b.alpha != a.alpha || b.br != a.br ||
+        b.records != a.records)
       return set_err(ctx, FA_E_STATE, "ranks disagree on the global raster, tiling, types or options (rank " +
                                           std::to_string(q) + ")");
     const bool last = q == tp.nranks - 1;

@@ -144,6 +144,7 @@ struct fa_ctx {
   int opt_fill_tile = 32;
   int opt_values = FA_VALUES_L2;
   int opt_graph = FA_GRAPH_HOST;
+  int opt_dist_records = FA_DIST_STRIPS;
   bool retain() const { return opt_evict == 0; }
 };
 

@@ -31,15 +31,17 @@ EXPORTS = ["fa_create", "fa_destroy", "fa_last_error", "fa_flowdirs", "fa_accumu
            "fa_set_option", "fa_get_option", "fa_accumulate_dist_loopback"]
 # context options (fa.h fa_option); values: RETAIN / EVICT, D8_SPLIT / D8_FUSED, block rows 32 / 16,
 # graph walk cap, fill tile 32 / 64
-OPT_RETENTION, OPT_D8, OPT_BLOCK_ROWS, OPT_WALK_CAP, OPT_FILL_TILE, OPT_VALUES, OPT_GRAPH = 1, 2, 3, 4, 5, 6, 7
+OPT_RETENTION, OPT_D8, OPT_BLOCK_ROWS, OPT_WALK_CAP, OPT_FILL_TILE, OPT_VALUES, OPT_GRAPH, OPT_DIST_RECORDS = range(1, 9)
 RETAIN, EVICT = 0, 1
 D8_SPLIT, D8_FUSED = 0, 1
 OPTIONS = {"retention": OPT_RETENTION, "d8": OPT_D8, "block_rows": OPT_BLOCK_ROWS, "walk_cap": OPT_WALK_CAP,
-           "fill_tile": OPT_FILL_TILE, "values": OPT_VALUES, "graph": OPT_GRAPH}
+           "fill_tile": OPT_FILL_TILE, "values": OPT_VALUES, "graph": OPT_GRAPH, "dist_records": OPT_DIST_RECORDS}
 VALUES_L2, VALUES_SMEM = 0, 1
 GRAPH_HOST, GRAPH_DEVICE = 0, 1
+DIST_TILES, DIST_STRIPS = 0, 1
 OPTION_VALUES = {"retain": RETAIN, "evict": EVICT, "split": D8_SPLIT, "fused": D8_FUSED, "l2": VALUES_L2,
-                 "smem": VALUES_SMEM, "host": GRAPH_HOST, "device": GRAPH_DEVICE}
+                 "smem": VALUES_SMEM, "host": GRAPH_HOST, "device": GRAPH_DEVICE, "tiles": DIST_TILES,
+                 "strips": DIST_STRIPS}
 
 
 def nccl_unique_id() -> bytes:

@@ -71,12 +71,15 @@ def test_loopback_dem_u32_cfg1_recipe(fa_lib, N):
     assert all(s["bytes_exchanged"] > 0 for s in st)
 
 
+@pytest.mark.parametrize("records", ["strips", "tiles"])
 @pytest.mark.parametrize("N", [2, 5])
-def test_loopback_dirs_ragged_tiles_and_strips(fa_lib, N):
+def test_loopback_dirs_ragged_tiles_and_strips(fa_lib, N, records):
     # 300 rows in 64-row tiles: the last tile row (and strip) is 44 rows; 257 cols in 50-col tiles
+    # (5 ranks: equal 64-row strips + a 44-row last one -> strip-level records; 2 ranks: 128 + 172
+    # rows, unequal -> the tiles are exchanged)
     d = inputs.random_dirs(11, 300, 257, p_nodata=0.12, p_noflow=0.02)
     w = inputs.weights_u32(11, d.shape, 0, 50)
-    got, _ = _run(fa_lib, N, (64, 50), dirs=d, w=w, atype="u64")
+    got, st = _run(fa_lib, N, (64, 50), dirs=d, w=w, atype="u64", options={"dist_records": records})
     assert (got == oracle.accumulate(d, w)).all()
 
 
@@ -89,19 +92,25 @@ def test_loopback_dem_one_row_last_strip(fa_lib):
     assert (got == _exp_u32(d)).all()
 
 
-def test_loopback_transposed_serpentine_crosses_every_strip(fa_lib):
+@pytest.mark.parametrize("records", ["strips", "tiles"])
+def test_loopback_transposed_serpentine_crosses_every_strip(fa_lib, records):
     d = inputs.serpentine(512, 384, transposed=True)
-    got, _ = _run(fa_lib, 8, (64, 64), dirs=d)
+    got, _ = _run(fa_lib, 8, (64, 64), dirs=d, options={"dist_records": records})
     assert (got == oracle.accumulate(d).astype(np.uint32)).all()
     assert got.max() == 512 * 384
 
 
+@pytest.mark.parametrize("records", ["strips", "tiles"])
 @pytest.mark.parametrize("N", [2, 4, 8])
-def test_loopback_cfg3_recipe_f64(fa_lib, N):
+def test_loopback_cfg3_recipe_f64(fa_lib, N, records):
     cfg = inputs.make_config("cfg3", 1024, 1024)
     d = oracle.d8(cfg.dem)
-    got, _ = _run(fa_lib, N, (128, 128), dem=cfg.dem, w=cfg.w, atype="f64")
+    got, st = _run(fa_lib, N, (128, 128), dem=cfg.dem, w=cfg.w, atype="f64", options={"dist_records": records})
     _check_f64(got, d, oracle.accumulate(d, cfg.w, kind="f64"))
+    # strip-level records: the producer graph holds each strip's perimeter (N
+    # tiles of 1024/N x 1024), else the perimeters of the 8 x 8 tiles
+    slots = N * (2 * (1024 // N + 1024) - 4) if records == "strips" else 64 * (4 * 128 - 4)
+    assert all(s["tile_nodes"] == slots for s in st)
 
 
 def test_loopback_f64_off_grid_weights_deep_chains(fa_lib):
