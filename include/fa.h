@@ -101,6 +101,8 @@ FA_API const char* fa_last_error(const fa_ctx* ctx);
  *       the strip perimeter, the producer graph over N strips; needs equal
  *       strips, the last may be shorter, else the tiles are used) or the
  *       context's tiles (every tile's perimeter all-gathered).
+ *       fa_accumulate_strips / fa_accumulate_absorb with nstrips > 1 follow
+ *       the same option (strips of ceil(rows / nstrips) rows as tiles).
  * Unknown option or value out of range: FA_E_ARG, the option unchanged. */
 typedef enum {
   FA_OPT_RETENTION = 1,

@@ -55,7 +55,11 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
   CK(cudaMemsetAsync(ctx->d_small, 0, 16 * sizeof(uint32_t), st));
   CK(cudaEventRecord(ctx->ev[0], st));
   // absorption (alpha) runs with 32-row blocks whatever FA_OPT_BLOCK_ROWS says
-  const Geom gg = make_geom(H, W, ctx->tile_r, ctx->tile_c, alpha ? kBR : ctx->opt_br);
+  // the strip pipeline with strip-level records (FA_OPT_DIST_RECORDS, as the
+  // multi-GPU path): each of the nstrips strips is one tile
+  const bool strip_tiles = !rec.want && nstrips > 1 && ctx->opt_dist_records == FA_DIST_STRIPS;
+  const int64_t sth = strip_tiles ? (H + nstrips - 1) / nstrips : ctx->tile_r;
+  const Geom gg = make_geom(H, W, sth, strip_tiles ? W : ctx->tile_c, alpha ? kBR : ctx->opt_br);
   if (!rec.want && nstrips <= 1) {
     // On one device every tile is resident, so the per-tile problems and the
     // global perimeter graph are solved jointly as one uncut block-exit graph
