@@ -571,6 +571,7 @@ __device__ __forceinline__ int build_masks(S& s, uint32_t& nsrc, int h, int w) {
     const int bpos = __ffs(srcbits) - 1;
     srcbits &= srcbits - 1;
     const int k = bpos >> 2, j = bpos & 3;
+    FA_CHECK(pos < WB::BN);
     s.src[pos++] = (uint16_t)(4 * (k * 32 + lane) + j);
   }
   return ndata;
@@ -615,6 +616,7 @@ __device__ __forceinline__ uint32_t kahn_chain_tail(WSmem<T, R, Z>& s, uint32_t 
     if (c < 0) {
       const uint32_t r = (uint32_t)__popc(idle & lt);
       if (r < avail) {
+        FA_CHECK(head + r < (uint32_t)WSmem<T, R, Z>::WB::BN);
         c = Q[head + r];
         fresh = true;
       }
@@ -633,6 +635,7 @@ __device__ __forceinline__ uint32_t kahn_chain_tail(WSmem<T, R, Z>& s, uint32_t 
         const uint32_t sbv = s.sb[cur];
         const bool ok = sb_go(sbv);
         const uint32_t t = ok ? WBT<R>::target(cur, sbv) : 0u;
+        FA_CHECK(t < (uint32_t)WBT<R>::BN);
         go = ok && ((s.pend[t >> 3] >> ((t & 7u) * 4u)) & 0xFu) == 1u;
         if (go) {
           cc[k] = t;
@@ -679,6 +682,7 @@ __device__ __forceinline__ uint32_t kahn_chain_tail(WSmem<T, R, Z>& s, uint32_t 
       }
     }
     const unsigned bm = __ballot_sync(kFull, ready != 0u);
+    FA_CHECK(!ready || (t < (uint32_t)WBT<R>::BN && tail + (uint32_t)__popc(bm & lt) < (uint32_t)WBT<R>::BN));
     if (ready) Q[tail + (uint32_t)__popc(bm & lt)] = (uint16_t)t;
     tail += (uint32_t)__popc(bm);
   }
@@ -719,6 +723,7 @@ __device__ __forceinline__ uint32_t kahn_block(WSmem<T, R, Z>& s, uint32_t nsrc,
         // "A(n) <- A(n) + A(c)" and "decrement D(n)" (Alg. 1);
         // A(c) is final: every donor of c was popped in an earlier iteration
         t = WBT<R>::target(c, sbv);
+        FA_CHECK(c < (uint32_t)WBT<R>::BN && t < (uint32_t)WBT<R>::BN);
         T a = __ldcg(Ab + (c + (c >> 5) * wm));
         if constexpr (ABS) a *= (T)__ldg(Alb + (c + (c >> 5) * wm));  // "alpha(n) A(n)"
         g_add(Ab + (t + (t >> 5) * wm), a);
@@ -728,6 +733,7 @@ __device__ __forceinline__ uint32_t kahn_block(WSmem<T, R, Z>& s, uint32_t nsrc,
       }
     }
     const unsigned bm = __ballot_sync(kFull, ready != 0u);
+    FA_CHECK(!ready || (t < (uint32_t)WBT<R>::BN && tail + (uint32_t)__popc(bm & lt) < (uint32_t)WBT<R>::BN));
     if (ready) Q[tail + (uint32_t)__popc(bm & lt)] = (uint16_t)t;
     tail += (uint32_t)__popc(bm);
   }
@@ -924,6 +930,7 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
         rp = (uint32_t)bperim_index(c & 31, c >> 5, h, w);
         // tile-records mode: an exit reached from a tile-edge slot is a node too
         const uint32_t k = s.need[p] ? s.need[p] : (P.cut ? 1u : 0u);
+        FA_CHECK(rp < 128u);
         if (k) atomicAdd(&nchild[rp], k);
       }
       s.need[p] = (uint8_t)rp;  // only this lane touches need[p] from here on
@@ -932,6 +939,7 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
     }
     if (ABS) f *= alpha_of(c);
     c = (int)WB::target((uint32_t)c, sbv);
+    FA_CHECK((unsigned)c < (unsigned)WB::BN);
     sbv = s.sb[c];
 #pragma unroll
     for (int u = 1; u < FA_REC_STEPS; ++u) {  // more steps per refill round
@@ -1006,12 +1014,14 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
       if (node[j]) {
         nid = base + (uint32_t)__popc(em & lt);
         if (ABS) P.node_alpha[nid] = (float)alpha_of(cell[j]);
+        FA_CHECK(nid < (uint32_t)(g.nblocks * WB::PB));
         P.node_val[nid] = a;
         P.node_slot[nid] = (uint32_t)(b * WB::PB + p2);
         P.node_tgt[nid] = tgt;
         P.node_flags[nid] = fl;
       } else if (tgt != kNone) {
         // a leaf: S(e) = A_B(e), nothing flows in from upstream blocks
+        FA_CHECK(tgt < (uint32_t)(g.nblocks * WB::PB));
         atomic_add(&P.x_slot[tgt], ABS ? a * alpha_of(cell[j]) : a);
       }
     }
@@ -1025,7 +1035,10 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
     if (p2 >= WB::PB) continue;
     uint32_t root = kNone;
     if (ex[j]) root = slot_nid[p2];
-    else if (want[j] && s.need[p2] != kNoP) root = slot_nid[s.need[p2]];
+    else if (want[j] && s.need[p2] != kNoP) {
+      FA_CHECK(s.need[p2] < WB::PB);
+      root = slot_nid[s.need[p2]];
+    }
     P.slot_root[b * WB::PB + p2] = root;
   }
 }
@@ -1346,6 +1359,7 @@ __device__ __forceinline__ int build_counts_v(S& s, uint32_t& nsrc, int h, int w
   while (srcbits) {
     const int bpos = __ffs(srcbits) - 1;
     srcbits &= srcbits - 1;
+    FA_CHECK(pos < WB::BN);
     s.src[pos++] = (uint16_t)(4 * ((bpos >> 2) * 32 + lane) + (bpos & 3));
   }
   return ndata;
@@ -1382,6 +1396,7 @@ __device__ __forceinline__ uint32_t kahn_push(S& s, uint32_t nsrc) {
     // one pusher per target cell and iteration: every pusher writes its lane
     // into the target's claim byte, the lane read back pushes, the others retry
     const uint32_t t = go ? WB::target((uint32_t)cur, sbv) : 0u;
+    FA_CHECK(t < (uint32_t)WB::BN);
     if (go) s.claim[t] = (uint8_t)lane;
     __syncwarp();
     if (go && s.claim[t] == (uint8_t)lane) {
@@ -1626,6 +1641,7 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
     // paid once per round)
 #pragma unroll
     for (int u = 0; u < FA_FIN_STEPS; ++u) {
+      FA_CHECK((unsigned)cy < (unsigned)h && (unsigned)cx < (unsigned)w);
       atomic_add(rowp + (int64_t)cy * g.W + cx, x);
       const int d = s.d[k][cy * WB::BC + cx];
       const int ty = cy + dir_dy(d), tx = cx + dir_dx(d);

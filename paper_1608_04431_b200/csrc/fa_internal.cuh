@@ -8,6 +8,17 @@
 
 #include <cmath>
 
+// FA_CHECK: device-side bounds / invariant assertions of the checked build
+// (tools/build_variant.py checked FA_CHECKED=1, run by tools/check_build.sh);
+// compiled out of the product library.  A failed check traps with the file
+// and line (cudaErrorAssert), so the checked test run fails loudly.
+#ifdef FA_CHECKED
+#include <cassert>
+#define FA_CHECK(...) assert((__VA_ARGS__))
+#else
+#define FA_CHECK(...) ((void)0)
+#endif
+
 namespace fa {
 
 // ---------------------------------------------------------------- constants

@@ -34,6 +34,7 @@ __global__ void k_g1_parent(uint32_t nn, const uint32_t* __restrict__ tgt,
     const uint32_t t = tgt[v];
     uint32_t p = kNone;
     if (t != kNone && !(cut && (flags[v] & NF_OUT_TILE))) p = slot_root[t];
+    FA_CHECK(p == kNone || p < nn);  // a parent is a node of the same graph
     parent[v] = p;
   }
 }
