@@ -89,12 +89,16 @@ FA_API const char* fa_last_error(const fa_ctx* ctx);
  *       EVICT pass-2 block kernels keep the block's values while Alg. 1 runs:
  *       in the output raster (L2-resident, pushes as global atomics, many
  *       warps per SM) or in shared memory (no global round trip, fewer warps).
- *   FA_OPT_GRAPH  [FA_GRAPH_HOST] | FA_GRAPH_DEVICE: the perimeter-graph
- *       solver (H5) as kernels driven from the host (a device-to-host read per
- *       decision: frontier size, residual size, jump convergence, segments),
- *       or as one cooperative persistent kernel taking every decision on the
- *       device (no host round trip inside the solve; measured slower on the
- *       large graphs: fewer walks in flight than the host-driven launches).
+ *   FA_OPT_GRAPH  [FA_GRAPH_AUTO] | FA_GRAPH_HOST | FA_GRAPH_DEVICE: the
+ *       perimeter-graph solver (H5) as kernels driven from the host (a
+ *       device-to-host read per decision: frontier size, residual size, jump
+ *       convergence, segments), or as one cooperative persistent kernel
+ *       taking every decision on the device (no host round trip; slower on
+ *       large graphs: fewer walks in flight).  AUTO: single-device calls with
+ *       at most 2^24 block slots (~134 M cells) run without any host round
+ *       trip before the final status read (the node count stays on the
+ *       device, the device solver reads it); larger ones use the host-driven
+ *       solver.
  *   FA_OPT_DIST_RECORDS  [FA_DIST_STRIPS] | FA_DIST_TILES: the record
  *       granularity of the multi-GPU exchange -- each rank's strip as one
  *       tile (the strip's block-exit graph cut only at its edges, records =
@@ -117,7 +121,7 @@ typedef enum {
 enum { FA_RETAIN = 0, FA_EVICT = 1 };
 enum { FA_D8_SPLIT = 0, FA_D8_FUSED = 1 };
 enum { FA_VALUES_L2 = 0, FA_VALUES_SMEM = 1 };
-enum { FA_GRAPH_HOST = 0, FA_GRAPH_DEVICE = 1 };
+enum { FA_GRAPH_HOST = 0, FA_GRAPH_DEVICE = 1, FA_GRAPH_AUTO = 2 };
 enum { FA_DIST_TILES = 0, FA_DIST_STRIPS = 1 };
 FA_API fa_status fa_set_option(fa_ctx* ctx, int option, int64_t value);
 FA_API fa_status fa_get_option(const fa_ctx* ctx, int option, int64_t* value);

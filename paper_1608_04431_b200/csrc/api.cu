@@ -45,6 +45,10 @@ struct Records {
   bool want = false;
 };
 
+// block slots up to which the single-device call runs without a host round
+// trip (the device solver's scratch is sized for every slot)
+constexpr int64_t kSyncFreeSlots = int64_t(1) << 24;
+
 template <class T, int WK>
 fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nodata, const uint8_t* dirs,
                   const void* w, T* acc, Records& rec, int nstrips, const float* alpha = nullptr) {
@@ -60,6 +64,62 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
   const bool strip_tiles = !rec.want && nstrips > 1 && ctx->opt_dist_records == FA_DIST_STRIPS;
   const int64_t sth = strip_tiles ? (H + nstrips - 1) / nstrips : ctx->tile_r;
   const Geom gg = make_geom(H, W, sth, strip_tiles ? W : ctx->tile_c, alpha ? kBR : ctx->opt_br);
+  const int64_t slots = gg.nblocks * gg.pb;
+  if (!rec.want && nstrips <= 1 && !alpha && ctx->opt_graph != FA_GRAPH_HOST && slots <= kSyncFreeSlots &&
+      !ctx->no_sync_free) {
+    // Small rasters (cfg0-cfg2 sizes): the same uncut pipeline without a host
+    // round trip until the final status read -- the node count stays on the
+    // device and the cooperative device solver (forest_dev.cu) reads it there.
+    // Data-dependent errors are reported after the whole call.
+    Strip<T> s;
+    s.g = gg;
+    s.dem = dem;
+    s.dirs = dirs;
+    s.w = w;
+    s.acc = acc;
+    s.nodata = nodata;
+    CK(cudaMemsetAsync(ctx->d_small + 32, 0, 4 * sizeof(uint32_t), st));
+    fa_status r = strip_pass1<T, WK>(ctx, s, false, true);
+    if (r != FA_OK) { s.release(rt); return r; }
+    CK(cudaEventRecord(ctx->ev[1], st));
+    const uint32_t* d_nn = ctx->d_small;
+    CK(launch_copy_n<T>(st, s.nn, d_nn, s.node_val, s.S));
+    CK(launch_fold_leaves<T>(st, slots, s.x_slot, s.slot_root, s.S));
+    rt.launches += 2;
+    cudaError_t e = forest_solve_device_async<T>(rt, s.nn, d_nn, s.parent, s.S, ctx->d_small + 32);
+    if (e == cudaErrorNotSupported) {  // no cooperative launch: the host-driven solver
+      cudaGetLastError();
+      CK(rt.read(d_nn, 1));
+      CK(forest_solve<T>(rt, rt.h_cnt[0], s.parent, s.S));
+    } else {
+      CK(e);
+    }
+    CK(launch_scatter_x<T>(st, s.nn, s.node_tgt, s.node_flags, s.S, s.x_slot, false, d_nn));
+    ++rt.launches;
+    CK(cudaEventRecord(ctx->ev[2], st));
+    if (ctx->retain()) CK(launch_retain<T>(s.g, s.x_slot, s.dirs_in(), s.acc, st));
+    else CK(launch_pass2<T, WK>(pass_args<T, WK>(ctx, s), st));
+    ++rt.launches;
+    CK(cudaEventRecord(ctx->ev[3], st));
+    s.release(rt);
+    CK(rt.read(ctx->d_small, 36));
+    const uint32_t nn = rt.h_cnt[0], stat = rt.h_cnt[1];
+    unsigned long long wsum = 0;
+    memcpy(&wsum, &rt.h_cnt[2], 8);
+    rt.contract_levels += rt.h_cnt[32];
+    rt.jump_rounds += rt.h_cnt[33];
+    rt.peel_rounds += rt.h_cnt[34];
+    if (stat & ST_RETRY) {  // the solver's scratch did not fit (never observed): once more, host-driven
+      ctx->no_sync_free = true;
+      r = run_acc<T, WK>(ctx, H, W, dem, nodata, dirs, w, acc, rec, nstrips, alpha);
+      ctx->no_sync_free = false;
+      return r;
+    }
+    r = check_status(ctx, stat, wsum, std::is_same<T, uint32_t>::value);
+    if (r != FA_OK) return r;
+    record_stats(ctx, H * W, gg.nblocks, nn, 0);
+    return FA_OK;
+  }
   if (!rec.want && nstrips <= 1) {
     // On one device every tile is resident, so the per-tile problems and the
     // global perimeter graph are solved jointly as one uncut block-exit graph
@@ -757,7 +817,7 @@ fa_status fa_set_option(fa_ctx* ctx, int option, int64_t value) {
       ctx->opt_values = (int)value;
       return FA_OK;
     case FA_OPT_GRAPH:
-      if (value != FA_GRAPH_HOST && value != FA_GRAPH_DEVICE) break;
+      if (value != FA_GRAPH_HOST && value != FA_GRAPH_DEVICE && value != FA_GRAPH_AUTO) break;
       ctx->opt_graph = (int)value;
       return FA_OK;
     case FA_OPT_DIST_RECORDS:

@@ -40,6 +40,7 @@ constexpr uint32_t ST_BADCODE = 1u;
 constexpr uint32_t ST_BADWEIGHT = 2u;
 constexpr uint32_t ST_CYCLE = 4u;
 constexpr uint32_t ST_BADALPHA = 8u;  // absorption: an alpha of a data cell outside [0,1]
+constexpr uint32_t ST_RETRY = 16u;    // the device graph solver ran out of scratch: rerun host-driven
 
 // node flags (per block-exit node)
 constexpr uint8_t NF_OUT_TILE = 1;  // target outside the node's tile (FlowExternal at tile level, D22)

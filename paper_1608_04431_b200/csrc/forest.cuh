@@ -47,6 +47,12 @@ template <class T>
 cudaError_t forest_solve_device(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, bool& done);
 cudaError_t forest_solve_weighted_device(Runtime& rt, uint32_t n, const uint32_t* parent, const double* wv,
                                          double* val, bool& done);
+// the same without a host read: node count *n_dev (<= n_max), statistics to
+// stats_out[0..2] (device), scratch overflow -> ST_RETRY in the status word;
+// cudaErrorNotSupported when a cooperative launch is not possible
+template <class T>
+cudaError_t forest_solve_device_async(Runtime& rt, uint32_t n_max, const uint32_t* n_dev, const uint32_t* parent,
+                                      T* val, uint32_t* stats_out);
 // absorption: S(v) = val(v) + sum_children wv(c) S(c)
 cudaError_t forest_solve_weighted(Runtime& rt, uint32_t n, const uint32_t* parent, const double* wv, double* val);
 // absorption: roots plus the product of edge weights from each node up to its root

@@ -70,6 +70,8 @@ struct DevArgs {
   DevLevel<T>* lv;    // [kDevMaxLevels]
   uint32_t* status;   // ST_CYCLE
   int cap;            // walk cap (steps before re-queueing)
+  const uint32_t* n_dev;  // optional: the node count in device memory (n0 is then a bound)
+  uint32_t* stats_out;    // optional: levels, jump rounds, walk rounds (async solves); overflow -> ST_RETRY
 };
 
 // counters
@@ -117,7 +119,7 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
   // warp-collective appends need whole warps)
   auto trips = [&](uint32_t n) { return (n + nth - 1) / nth; };
   uint32_t* C = A.ctr;
-  uint32_t n = A.n0;
+  uint32_t n = A.n_dev ? min(__ldcg(A.n_dev), A.n0) : A.n0;
   const uint32_t* parent = A.parent0;
   T* val = A.val0;
   const T* wv = A.wv0;
@@ -225,7 +227,10 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
     uint32_t* spar = carve<uint32_t>(A.pool, off, mcap, A.pool_bytes, ovf);
     T* sw = WG ? carve<T>(A.pool, off, mcap, A.pool_bytes, ovf) : nullptr;
     if (ovf) {  // the host falls back to forest.cu
-      if (tid == 0) C[C_OVF] = 1u;
+      if (tid == 0) {
+        C[C_OVF] = 1u;
+        if (A.stats_out) atomicOr(A.status, ST_RETRY);
+      }
       break;
     }
     for (uint32_t t = 0, v = tid; t < trips(n); ++t, v += nth) {
@@ -370,6 +375,11 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
     C[C_STATS] = nlevels;
     C[C_STATS + 1] = njump;
     C[C_STATS + 2] = nwalk;
+    if (A.stats_out) {
+      A.stats_out[0] = nlevels;
+      A.stats_out[1] = njump;
+      A.stats_out[2] = nwalk;
+    }
   }
   grid.sync();
   // ---------------- expand, deepest level first
@@ -423,7 +433,7 @@ cudaError_t solve_dev(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, c
   a.cap = rt.walk_cap > 0 ? rt.walk_cap : 1;  // walk cap 0 ("peel only"): one step per round
   if (rt.err) return rt.err;
   cudaMemsetAsync(a.ctr, 0, 64 * sizeof(uint32_t), st);
-  const unsigned grid = (unsigned)(sms * per_sm);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * per_sm, ((int64_t)n + 255) / 256));
   void* args[] = {&a};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, grid, 256, args, 0, st);
   ++rt.launches;
@@ -451,7 +461,67 @@ cudaError_t solve_dev(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, c
   return cudaSuccess;
 }
 
+// the same solve without any host read: the node count is read on the device,
+// scratch is sized for the bound n_max, statistics go to stats_out, and a
+// scratch overflow raises ST_RETRY in the status word instead of a fallback
+template <class T>
+cudaError_t solve_dev_async(Runtime& rt, uint32_t n_max, const uint32_t* n_dev, const uint32_t* parent, T* val,
+                            uint32_t* stats_out) {
+  if (n_max == 0) return cudaSuccess;
+  int dev = 0, sms = 0, coop = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  auto k = k_forest_dev<T, false>;
+  if (!coop || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return cudaErrorNotSupported;
+  }
+  cudaStream_t st = rt.st;
+  DevArgs<T, false> a{};
+  a.n0 = n_max;
+  a.n_dev = n_dev;
+  a.stats_out = stats_out;
+  a.parent0 = parent;
+  a.val0 = val;
+  a.cnt = rt.alloc<uint32_t>(n_max);
+  a.done = rt.alloc<uint8_t>(n_max);
+  a.fa = rt.alloc<uint32_t>(n_max);
+  a.fb = rt.alloc<uint32_t>(n_max);
+  a.rid = rt.alloc<uint32_t>(n_max);
+  a.ctr = rt.alloc<uint32_t>(64);
+  const size_t per = 4 * 7 + sizeof(T) * 4 + 64;
+  a.pool_bytes = per * ((size_t)n_max + 4096) + (size_t)n_max * per / 2;
+  a.pool = rt.alloc<uint8_t>(a.pool_bytes);
+  a.lv = rt.alloc<DevLevel<T>>(kDevMaxLevels);
+  a.status = rt.d_status;
+  a.cap = rt.walk_cap > 0 ? rt.walk_cap : 1;
+  if (rt.err) return rt.err;
+  cudaMemsetAsync(a.ctr, 0, 64 * sizeof(uint32_t), st);
+  // a small graph gets a small grid: its barriers are cheaper
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * per_sm, ((int64_t)n_max + 255) / 256));
+  void* args[] = {&a};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, grid, 256, args, 0, st);
+  ++rt.launches;
+  for (void* p : {(void*)a.cnt, (void*)a.done, (void*)a.fa, (void*)a.fb, (void*)a.rid, (void*)a.ctr, (void*)a.pool,
+                  (void*)a.lv})
+    rt.free(p);
+  return e;
+}
+
 }  // namespace
+
+template <class T>
+cudaError_t forest_solve_device_async(Runtime& rt, uint32_t n_max, const uint32_t* n_dev, const uint32_t* parent,
+                                      T* val, uint32_t* stats_out) {
+  return solve_dev_async<T>(rt, n_max, n_dev, parent, val, stats_out);
+}
+template cudaError_t forest_solve_device_async<uint32_t>(Runtime&, uint32_t, const uint32_t*, const uint32_t*,
+                                                         uint32_t*, uint32_t*);
+template cudaError_t forest_solve_device_async<unsigned long long>(Runtime&, uint32_t, const uint32_t*,
+                                                                   const uint32_t*, unsigned long long*, uint32_t*);
+template cudaError_t forest_solve_device_async<double>(Runtime&, uint32_t, const uint32_t*, const uint32_t*, double*,
+                                                       uint32_t*);
 
 template <class T>
 cudaError_t forest_solve_device(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, bool& done) {

@@ -27,9 +27,12 @@ __device__ __forceinline__ int64_t tile_of_slot(const int64_t* __restrict__ tbas
   return lo;
 }
 
+// nn_dev (optional): the node count in device memory (the sync-free path;
+// nn is then only the bound the grid was sized for)
 __global__ void k_g1_parent(uint32_t nn, const uint32_t* __restrict__ tgt,
                             const uint8_t* __restrict__ flags, const uint32_t* __restrict__ slot_root,
-                            bool cut, uint32_t* parent) {
+                            bool cut, uint32_t* parent, const uint32_t* __restrict__ nn_dev) {
+  if (nn_dev) nn = *nn_dev;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += gridDim.x * blockDim.x) {
     const uint32_t t = tgt[v];
     uint32_t p = kNone;
@@ -43,7 +46,8 @@ __global__ void k_g1_parent(uint32_t nn, const uint32_t* __restrict__ tgt,
 // edges inside a tile; cross-tile flow then arrives through x_T)
 template <class T>
 __global__ void k_scatter_x(uint32_t nn, const uint32_t* __restrict__ tgt, const uint8_t* __restrict__ flags,
-                            const T* __restrict__ S, T* x_slot, bool intra_tile) {
+                            const T* __restrict__ S, T* x_slot, bool intra_tile, const uint32_t* __restrict__ nn_dev) {
+  if (nn_dev) nn = *nn_dev;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += gridDim.x * blockDim.x) {
     const uint32_t t = tgt[v];
     if (t != kNone && !(intra_tile && (flags[v] & NF_OUT_TILE))) atomic_add(&x_slot[t], S[v]);
@@ -207,10 +211,30 @@ __global__ void k_inject_slots(Geom g, int64_t nslots, const int64_t* __restrict
 }  // namespace
 
 cudaError_t launch_g1_parent(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
-                             const uint32_t* slot_root, bool cut, uint32_t* parent) {
-  k_g1_parent<<<grid_for(nn), 256, 0, st>>>(nn, tgt, flags, slot_root, cut, parent);
+                             const uint32_t* slot_root, bool cut, uint32_t* parent, const uint32_t* nn_dev) {
+  k_g1_parent<<<grid_for(nn), 256, 0, st>>>(nn, tgt, flags, slot_root, cut, parent, nn_dev);
   return cudaGetLastError();
 }
+
+namespace {
+template <class T>
+__global__ void k_copy_n(uint32_t nmax, const uint32_t* __restrict__ n_dev, const T* __restrict__ src, T* dst) {
+  const uint32_t n = *n_dev;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n && v < nmax; v += gridDim.x * blockDim.x)
+    dst[v] = src[v];
+}
+}  // namespace
+
+// dst[0, *n_dev) = src (the node values, with the node count on the device)
+template <class T>
+cudaError_t launch_copy_n(cudaStream_t st, uint32_t nmax, const uint32_t* n_dev, const T* src, T* dst) {
+  k_copy_n<T><<<grid_for(nmax), 256, 0, st>>>(nmax, n_dev, src, dst);
+  return cudaGetLastError();
+}
+template cudaError_t launch_copy_n<uint32_t>(cudaStream_t, uint32_t, const uint32_t*, const uint32_t*, uint32_t*);
+template cudaError_t launch_copy_n<unsigned long long>(cudaStream_t, uint32_t, const uint32_t*,
+                                                       const unsigned long long*, unsigned long long*);
+template cudaError_t launch_copy_n<double>(cudaStream_t, uint32_t, const uint32_t*, const double*, double*);
 
 template <class T>
 cudaError_t launch_fold_leaves(cudaStream_t st, int64_t nslots, const T* x_slot, const uint32_t* slot_root, T* S) {
@@ -224,8 +248,8 @@ template cudaError_t launch_fold_leaves<double>(cudaStream_t, int64_t, const dou
 
 template <class T>
 cudaError_t launch_scatter_x(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
-                             const T* S, T* x_slot, bool intra_tile) {
-  k_scatter_x<T><<<grid_for(nn), 256, 0, st>>>(nn, tgt, flags, S, x_slot, intra_tile);
+                             const T* S, T* x_slot, bool intra_tile, const uint32_t* nn_dev) {
+  k_scatter_x<T><<<grid_for(nn), 256, 0, st>>>(nn, tgt, flags, S, x_slot, intra_tile, nn_dev);
   return cudaGetLastError();
 }
 
@@ -283,7 +307,7 @@ cudaError_t launch_inject_slots(cudaStream_t st, const Geom& g, int64_t nslots, 
 
 #define FA_INST(T)                                                                                  \
   template cudaError_t launch_scatter_x<T>(cudaStream_t, uint32_t, const uint32_t*, const uint8_t*,  \
-                                           const T*, T*, bool);                                     \
+                                           const T*, T*, bool, const uint32_t*);                                     \
   template cudaError_t launch_tile_records<T>(cudaStream_t, const Geom&, int64_t, const int64_t*,   \
                                               const uint8_t*, const uint32_t*, const uint32_t*,     \
                                               const uint8_t*, const uint32_t*, const T*, uint32_t*, \

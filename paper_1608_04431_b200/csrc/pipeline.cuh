@@ -36,7 +36,10 @@ cudaError_t launch_d8(const float* dem, const float* dem_up, const float* dem_dn
                       float nodata, uint8_t* dirs,
                       cudaStream_t st);
 cudaError_t launch_g1_parent(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
-                             const uint32_t* slot_root, bool cut, uint32_t* parent);
+                             const uint32_t* slot_root, bool cut, uint32_t* parent,
+                             const uint32_t* nn_dev = nullptr);
+template <class T>
+cudaError_t launch_copy_n(cudaStream_t st, uint32_t nmax, const uint32_t* n_dev, const T* src, T* dst);
 // absorption: block.cu / graph.cu
 cudaError_t launch_pass1_absorb(const PassArgs<double, 0>* a0, const PassArgs<double, 2>* a2, bool from_dem,
                                 cudaStream_t st);
@@ -52,7 +55,7 @@ cudaError_t launch_g1_weights_cut(cudaStream_t st, uint32_t nn, const uint8_t* f
 cudaError_t fill_depressions(Runtime& rt, const float* z, int64_t H, int64_t W, float nodata, float* out, int tile);
 template <class T>
 cudaError_t launch_scatter_x(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,
-                             const T* S, T* x_slot, bool intra_tile);
+                             const T* S, T* x_slot, bool intra_tile, const uint32_t* nn_dev = nullptr);
 template <class T>
 cudaError_t launch_fold_leaves(cudaStream_t st, int64_t nslots, const T* x_slot, const uint32_t* slot_root, T* S);
 template <class T>
@@ -143,8 +146,9 @@ struct fa_ctx {
   int opt_walk_cap = 128;
   int opt_fill_tile = 32;
   int opt_values = FA_VALUES_L2;
-  int opt_graph = FA_GRAPH_HOST;
+  int opt_graph = FA_GRAPH_AUTO;
   int opt_dist_records = FA_DIST_STRIPS;
+  bool no_sync_free = false;  // set while a small-raster call reruns host-driven
   bool retain() const { return opt_evict == 0; }
 };
 
@@ -325,8 +329,11 @@ fa_status check_status(fa_ctx* ctx, uint32_t stat, unsigned long long wsum, bool
 }
 
 // pass 1 of a strip + block-exit graph parents (cut at tile edges when `cut`)
+// sync_free: the node count stays on the device (d_small[0]); parent / S are
+// sized for every block slot and the kernels after pass 1 read the count
+// themselves (the small-raster path of run_acc: no host round trip)
 template <class T, int WK>
-fa_status strip_pass1(fa_ctx* ctx, Strip<T>& s, bool cut) {
+fa_status strip_pass1(fa_ctx* ctx, Strip<T>& s, bool cut, bool sync_free = false) {
   using namespace fa;
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
@@ -391,6 +398,15 @@ fa_status strip_pass1(fa_ctx* ctx, Strip<T>& s, bool cut) {
   }
   CK(cudaEventRecord(ctx->ev[6], st));
   ++rt.launches;
+  if (sync_free) {
+    s.nn = (uint32_t)slots;  // a bound: the count is ctx->d_small[0]
+    s.parent = rt.alloc<uint32_t>(s.nn);
+    s.S = rt.alloc<T>(s.nn);
+    if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+    CK(launch_g1_parent(st, s.nn, s.node_tgt, s.node_flags, s.slot_root, cut, s.parent, ctx->d_small));
+    ++rt.launches;
+    return FA_OK;
+  }
   CK(rt.read(ctx->d_small, 4));
   s.nn = rt.h_cnt[0];
   s.parent = rt.alloc<uint32_t>(s.nn);
@@ -577,7 +593,7 @@ void reset_run(fa_ctx* ctx) {
   fa::Runtime& rt = ctx->rt;
   rt.st = ctx->st;
   rt.walk_cap = ctx->opt_walk_cap;
-  rt.device_solver = ctx->opt_graph == FA_GRAPH_DEVICE;
+  rt.device_solver = ctx->opt_graph == FA_GRAPH_DEVICE;  // AUTO: the small-raster path of run_acc only
   rt.err = cudaSuccess;
   rt.peel_rounds = rt.contract_levels = rt.jump_rounds = rt.launches = 0;
   rt.d_status = ctx->d_small + 1;

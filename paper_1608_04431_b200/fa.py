@@ -37,10 +37,10 @@ D8_SPLIT, D8_FUSED = 0, 1
 OPTIONS = {"retention": OPT_RETENTION, "d8": OPT_D8, "block_rows": OPT_BLOCK_ROWS, "walk_cap": OPT_WALK_CAP,
            "fill_tile": OPT_FILL_TILE, "values": OPT_VALUES, "graph": OPT_GRAPH, "dist_records": OPT_DIST_RECORDS}
 VALUES_L2, VALUES_SMEM = 0, 1
-GRAPH_HOST, GRAPH_DEVICE = 0, 1
+GRAPH_HOST, GRAPH_DEVICE, GRAPH_AUTO = 0, 1, 2
 DIST_TILES, DIST_STRIPS = 0, 1
 OPTION_VALUES = {"retain": RETAIN, "evict": EVICT, "split": D8_SPLIT, "fused": D8_FUSED, "l2": VALUES_L2,
-                 "smem": VALUES_SMEM, "host": GRAPH_HOST, "device": GRAPH_DEVICE, "tiles": DIST_TILES,
+                 "smem": VALUES_SMEM, "host": GRAPH_HOST, "device": GRAPH_DEVICE, "auto": GRAPH_AUTO, "tiles": DIST_TILES,
                  "strips": DIST_STRIPS}
 
 

@@ -18,7 +18,7 @@ def _cuda(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-@pytest.fixture(params=["device", "host"])
+@pytest.fixture(params=["device", "host", "auto"])
 def graph(request):
     return request.param
 

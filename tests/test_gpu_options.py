@@ -95,7 +95,7 @@ def test_options_serpentine_deep_chain(fa_lib, combo):
 def test_option_validation(fa_lib):
     with fa_lib.Context(0) as ctx:
         for name, bad in (("retention", 2), ("d8", 5), ("block_rows", 8), ("walk_cap", -1), ("fill_tile", 16),
-                          ("values", 3), ("graph", 2)):
+                          ("values", 3), ("graph", 3)):
             with pytest.raises(fa_lib.FaError) as e:
                 ctx.set_option(name, bad)
             assert e.value.status == fa_lib.FA_E_ARG
