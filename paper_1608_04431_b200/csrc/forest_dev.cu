@@ -115,6 +115,12 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
   cg::grid_group grid = cg::this_grid();
   const uint32_t tid = (uint32_t)grid.thread_rank();
   const uint32_t nth = (uint32_t)grid.size();
+  // a one-CTA grid (small graphs) synchronises with the CTA barrier
+  const bool one_cta = gridDim.x == 1;
+  auto sync_all = [&]() {
+    if (one_cta) __syncthreads();
+    else grid.sync();
+  };
   // grid-stride loops in which every thread runs the same trip count (the
   // warp-collective appends need whole warps)
   auto trips = [&](uint32_t n) { return (n + nth - 1) / nth; };
@@ -136,17 +142,17 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
       A.cnt[v] = 0u;
       A.done[v] = 0u;
     }
-    grid.sync();
+    sync_all();
     for (uint32_t v = tid; v < n; v += nth) {
       const uint32_t p = parent[v];
       if (p != kNone) atomicAdd(&A.cnt[p], 1u);
     }
-    grid.sync();
+    sync_all();
     for (uint32_t t = 0, v = tid; t < trips(n); ++t, v += nth) {
       const bool leaf = v < n && ld(&A.cnt[v]) == 0u;
       append(leaf, v, A.fa, &C[C_F + 0]);
     }
-    grid.sync();
+    sync_all();
     // rounds of capped walks ("the last arrival continues"); round r reads
     // the frontier count in slot r%3, appends to slot (r+1)%3 and zeroes
     // slot (r+2)%3 (read two barriers ago)
@@ -190,7 +196,7 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
       for (int o = 16; o; o >>= 1) ret += __shfl_xor_sync(0xFFFFFFFFu, ret, o);
       if ((threadIdx.x & 31) == 0 && ret) atomicAdd(reinterpret_cast<unsigned long long*>(&C[C_RET]), ret);
       if (tid == 0) C[C_F + (r + 2) % 3] = 0u;
-      grid.sync();
+      sync_all();
       ++r;
       ++nwalk;
       nf = ld(&C[C_F + r % 3]);
@@ -247,7 +253,7 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
         A.rid[v] = q;
       }
     }
-    grid.sync();
+    sync_all();
     const uint32_t m = ld(&C[C_M]);
     L.m = m;
     L.val = val;
@@ -260,19 +266,19 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
       lpc[q] = __ldcg(&A.cnt[v]);
       up[q] = kNone;
     }
-    grid.sync();
+    sync_all();
     for (uint32_t q = tid; q < m; q += nth) {
       const uint32_t pq = lpar[q];
       if (pq != kNone && lpc[pq] == 1u) up[pq] = q;  // the unique pending child of a chain node
     }
-    grid.sync();
+    sync_all();
     for (uint32_t q = tid; q < m; q += nth) {
       const bool start = lpc[q] != 1u;
       nxa[q] = start ? q : up[q];
       aca[q] = start ? (T)0 : lval[q];
       if (WG) mua[q] = start ? (T)1 : lw[up[q]];
     }
-    grid.sync();
+    sync_all();
     // pointer jumping along the unique-pending-child links
     for (int j = 0;; ++j) {
       bool ch = false;
@@ -297,7 +303,7 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
       // slot (j+1)%3 was last read after the barrier before the previous
       // round: zeroing it now cannot race a read; round j+1 sets it
       if (tid == 0) C[C_CH + (j + 1) % 3] = 0u;
-      grid.sync();
+      sync_all();
       {
         uint32_t* t1 = nxa;
         nxa = nxb;
@@ -338,7 +344,7 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
         if (WG) sw[s] = (T)0;
       }
     }
-    grid.sync();
+    sync_all();
     for (uint32_t q = tid; q < m; q += nth) {
       const uint32_t pq = lpar[q];
       if (pq != kNone && lpc[pq] == 1u) continue;  // not a segment end
@@ -355,7 +361,7 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
         }
       }
     }
-    grid.sync();
+    sync_all();
     const uint32_t ms = ld(&C[C_MS]);
     if (ms >= m) {  // no chain node in a thin residual: a cycle
       if (tid == 0) atomicOr(A.status, ST_CYCLE);
@@ -369,7 +375,7 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
     parent = spar;
     val = L.sval;
     wv = WG ? sw : nullptr;
-    grid.sync();  // every thread has read the level's counters before they are reset
+    sync_all();  // every thread has read the level's counters before they are reset
   }
   if (tid == 0) {
     C[C_STATS] = nlevels;
@@ -381,7 +387,7 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
       A.stats_out[2] = nwalk;
     }
   }
-  grid.sync();
+  sync_all();
   // ---------------- expand, deepest level first
   while (level > 0) {
     --level;
@@ -390,7 +396,7 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
       const T sv = L.sval[L.sid[L.nxt[q]]];
       L.val[L.R[q]] = WG ? L.acc[q] + L.mul[q] * sv : sv + L.acc[q];
     }
-    grid.sync();
+    sync_all();
   }
 }
 
@@ -498,7 +504,8 @@ cudaError_t solve_dev_async(Runtime& rt, uint32_t n_max, const uint32_t* n_dev, 
   a.cap = rt.walk_cap > 0 ? rt.walk_cap : 1;
   if (rt.err) return rt.err;
   cudaMemsetAsync(a.ctr, 0, 64 * sizeof(uint32_t), st);
-  // a small graph gets a small grid: its barriers are cheaper
+  // a small graph gets a small grid: its barriers are cheaper (one CTA per
+  // 256 nodes; a single CTA synchronises with its own barrier)
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * per_sm, ((int64_t)n_max + 255) / 256));
   void* args[] = {&a};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, grid, 256, args, 0, st);
