@@ -80,8 +80,8 @@ FA_API const char* fa_last_error(const fa_ctx* ctx);
  *       (P:L260); EVICT recomputes the block accumulation with w + x.
  *   FA_OPT_D8  [FA_D8_SPLIT] | FA_D8_FUSED: H1 as its own kernel, or fused
  *       into the pass-1 block kernel (DEM input only).
- *   FA_OPT_BLOCK_ROWS  [32] | 16: rows of the warp-resident blocks (32 wide).
- *       Absorption always runs with 32.
+ *   FA_OPT_BLOCK_ROWS  [32] | 16 | 64: rows of the warp-resident blocks
+ *       (32 wide).  Absorption always runs with 32.
  *   FA_OPT_WALK_CAP  [128], 0..2^20: steps of a perimeter-graph walk before
  *       it re-queues (0: level-synchronous peeling only).
  *   FA_OPT_FILL_TILE  [32] | 64: tile side of fa_fill.

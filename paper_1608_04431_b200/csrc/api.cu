@@ -18,7 +18,7 @@ Geom make_geom(int64_t H, int64_t W, int64_t th, int64_t tw, int br) {
   g.TW = (tw > 0 && tw < W) ? tw : W;
   g.TR = (H + g.TH - 1) / g.TH;
   g.TC = (W + g.TW - 1) / g.TW;
-  g.br = br == 16 ? 16 : kBR;  // blocks are br x 32, one per warp (FA_OPT_BLOCK_ROWS)
+  g.br = (br == 16 || br == 64) ? br : kBR;  // blocks are br x 32, one per warp (FA_OPT_BLOCK_ROWS)
   g.bc = kBC;
   g.nw = kNW;
   g.pb = 2 * (g.br + g.bc) - 4;
@@ -801,7 +801,7 @@ fa_status fa_set_option(fa_ctx* ctx, int option, int64_t value) {
       ctx->opt_fused = value == FA_D8_FUSED;
       return FA_OK;
     case FA_OPT_BLOCK_ROWS:
-      if (value != 16 && value != 32) break;
+      if (value != 16 && value != 32 && value != 64) break;
       ctx->opt_br = (int)value;
       return FA_OK;
     case FA_OPT_WALK_CAP:

@@ -122,8 +122,10 @@ struct WBT {
   }
   __device__ static __forceinline__ int hidx(int ly, int lx) { return (ly + 1) * HS + HOFF + lx; }
   __device__ static __forceinline__ int zidx(int ly, int lx) { return (ly + 2) * ZS + ZOFF + lx; }
+  static constexpr int NJ = (PB + 31) / 32;  // perimeter slots per lane
+  static constexpr int NP = NJ * 32;         // perimeter slots rounded to whole warps
   static_assert(HS <= 120 && ZS <= 120, "int8 offsets");
-  static_assert(PB <= 128, "perimeter slots: at most 4 per lane");
+  static_assert(PB < 255 && NJ <= 8, "perimeter slots: u8 indices (0xFF = none), at most 8 per lane");
   static_assert(BN <= 2048, "11-bit successor index");
 };
 
@@ -141,12 +143,12 @@ struct __align__(16) WSmem {
   uint32_t pend[WB::BN / 8];  // pending in-block donor counts, 4 bits per cell (<= 8)
   alignas(8) uint8_t sb[WB::BN];  // successor bytes
   // ready queue of Alg. 1 (sources first; each cell enters at most once);
-  // after the queue loop: [0,128) slot -> node id, [128,256) per exit slot:
+  // after the queue loop: [0,NP) slot -> node id, [NP,2NP) per exit slot:
   // outside donors of the entries draining to it
   alignas(16) uint16_t src[WB::BN];
-  alignas(4) uint8_t need[128];  // per perimeter slot: donors outside the block (ring cells draining in)
+  alignas(4) uint8_t need[WB::NP];  // per perimeter slot: donors outside the block (ring cells draining in)
   __device__ __forceinline__ uint32_t* slot_nid() { return reinterpret_cast<uint32_t*>(src); }
-  static_assert(WB::BN * 2 >= 256 * 4, "records scratch lives in the queue");
+  static_assert(WB::BN * 2 >= 2 * WB::NP * 4, "records scratch lives in the queue");
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -210,7 +212,7 @@ __device__ __forceinline__ void init_smem(S& s) {
   uint32_t* D = reinterpret_cast<uint32_t*>(s.dirh);
   const int lane = lane_id();
   for (int i = lane; i < WBT<R>::HN / 4; i += 32) D[i] = 0xFFFFFFFFu;
-  reinterpret_cast<uint32_t*>(s.need)[lane] = 0u;
+  for (int i = lane; i < WBT<R>::NP / 4; i += 32) reinterpret_cast<uint32_t*>(s.need)[i] = 0u;
 }
 
 
@@ -481,11 +483,13 @@ __device__ __forceinline__ int build_masks(S& s, uint32_t& nsrc, int h, int w) {
   using WB = typename S::WB;
   constexpr int R = S::RR;
   constexpr int NQ = WB::BN / 128;  // words per lane
-  static_assert(NQ <= 8, "source bits: 4 per word, 32 per lane");
+  static_assert(NQ <= 16, "source bits: 4 per word, 64 per lane");
+  using SrcBits = typename std::conditional<(NQ > 8), unsigned long long, uint32_t>::type;
   const int lane = lane_id();
   const uint32_t* D = reinterpret_cast<const uint32_t*>(s.dirh);
   int ndata = 0;
-  uint32_t srcbits = 0, ndbits = 0;
+  SrcBits srcbits = 0;
+  uint32_t ndbits = 0;
 #pragma unroll 1
   for (int k = 0; k < NQ; ++k) {
     const int q = k * 32 + lane;  // word: row q/8, cells 4(q%8)..+3
@@ -531,7 +535,8 @@ __device__ __forceinline__ int build_masks(S& s, uint32_t& nsrc, int h, int w) {
       reinterpret_cast<uint32_t*>(s.sb)[q] = sbw;
     }
     const uint32_t src4 = __vcmpeq4(m, 0u) & ~nd & 0x80808080u;  // sources: bit 7 of each byte
-    srcbits |= (((src4 >> 7) & 1u) | ((src4 >> 14) & 2u) | ((src4 >> 21) & 4u) | ((src4 >> 28) & 8u)) << (4 * k);
+    srcbits |= (SrcBits)(((src4 >> 7) & 1u) | ((src4 >> 14) & 2u) | ((src4 >> 21) & 4u) | ((src4 >> 28) & 8u))
+               << (4 * k);
   }
   if constexpr (SUCC) {
     // donors of in-block NoData cells: their flow is dropped (STOP)
@@ -558,7 +563,7 @@ __device__ __forceinline__ int build_masks(S& s, uint32_t& nsrc, int h, int w) {
     }
   }
   // compact: exclusive scan of the per-lane counts, then each lane writes its cells
-  const int cnt = __popc(srcbits);
+  const int cnt = sizeof(SrcBits) == 8 ? __popcll((unsigned long long)srcbits) : __popc((uint32_t)srcbits);
   int incl = cnt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -568,7 +573,7 @@ __device__ __forceinline__ int build_masks(S& s, uint32_t& nsrc, int h, int w) {
   nsrc = (uint32_t)__shfl_sync(kFull, incl, 31);
   int pos = incl - cnt;
   while (srcbits) {
-    const int bpos = __ffs(srcbits) - 1;
+    const int bpos = sizeof(SrcBits) == 8 ? __ffsll((long long)srcbits) - 1 : __ffs((int)srcbits) - 1;
     srcbits &= srcbits - 1;
     const int k = bpos >> 2, j = bpos & 3;
     FA_CHECK(pos < WB::BN);
@@ -843,7 +848,7 @@ template <class T, int R, class S, int WK, bool ABS = false>
 __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, int64_t b, int64_t y0,
                                               int64_t x0, int h, int w) {
   using WB = WBT<R>;
-  constexpr int NJ = (WB::PB + 31) / 32;
+  constexpr int NJ = WB::NJ;
   constexpr uint32_t kNoP = 0xFFu;
   const Geom& g = P.g;
   const int lane = lane_id();
@@ -854,8 +859,8 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
   auto alpha_of = [&](int c) -> T { return (T)__ldg(Alb + ((uint32_t)c + ((uint32_t)c >> 5) * wmA)); };
   const int np = bperim_count(h, w);
   uint32_t* slot_nid = s.slot_nid();  // the queue is dead after the queue loop
-  uint32_t* nchild = slot_nid + 128;   // per exit slot: outside donors of the entries draining to it
-  for (int i = lane; i < 128; i += 32) nchild[i] = 0u;
+  uint32_t* nchild = slot_nid + WB::NP;  // per exit slot: outside donors of the entries draining to it
+  for (int i = lane; i < WB::NP; i += 32) nchild[i] = 0u;
   // the block's tile: only tile-records mode (cut) uses tile edges and the
   // out-of-tile flag (two integer divisions saved per block otherwise)
   int64_t t0y = 0, t0x = 0, th = 0, tw = 0;
@@ -891,11 +896,13 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
   }
   // walks (lanes refill from a warp-uniform work list as they finish); the
   // root (exit slot or kNoP) of a walked slot p is kept in need[p] afterwards
-  uint32_t wl[4] = {0u, 0u, 0u, 0u};
+  uint32_t wl[NJ];
+  int nwalk = 0;
 #pragma unroll
-  for (int j = 0; j < NJ; ++j) wl[j] = __ballot_sync(kFull, want[j]);
-  const int nw0 = __popc(wl[0]), nw1 = nw0 + __popc(wl[1]), nw2 = nw1 + __popc(wl[2]);
-  const int nwalk = nw2 + __popc(wl[3]);
+  for (int j = 0; j < NJ; ++j) {
+    wl[j] = __ballot_sync(kFull, want[j]);
+    nwalk += __popc(wl[j]);
+  }
   int head = 0;
   int p = -1, c = 0;
   uint32_t sbv = 0u;  // successor byte of the walk's cell
@@ -908,10 +915,16 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
       if (r < nwalk) {
         // r-th wanted slot: the rr-th set bit of wl[j]
         int j = 0, rr = r;
-        if (rr >= nw0) { j = 1; rr -= nw0; }
-        if (j == 1 && rr >= nw1 - nw0) { j = 2; rr -= nw1 - nw0; }
-        if (j == 2 && rr >= nw2 - nw1) { j = 3; rr -= nw2 - nw1; }
-        const uint32_t m = j == 0 ? wl[0] : j == 1 ? wl[1] : j == 2 ? wl[2] : wl[3];
+        uint32_t m = wl[0];
+#pragma unroll
+        for (int jj = 1; jj < NJ; ++jj) {
+          const int c0 = __popc(m);
+          if (j == jj - 1 && rr >= c0) {
+            j = jj;
+            rr -= c0;
+            m = wl[jj];
+          }
+        }
         const int l = __fns(m, 0, rr + 1);
         p = l + 32 * j;
         int px, py;
@@ -1197,9 +1210,9 @@ struct __align__(16) VSmem {
   uint8_t claim[WB::BN];            // per iteration: the lane pushing into the cell
   alignas(8) uint8_t sb[WB::BN];   // successor bytes
   alignas(16) uint16_t src[WB::BN];  // sources (Alg. 1's initial queue); records scratch afterwards
-  alignas(4) uint8_t need[128];
+  alignas(4) uint8_t need[WB::NP];
   __device__ __forceinline__ uint32_t* slot_nid() { return reinterpret_cast<uint32_t*>(src); }
-  static_assert(WB::BN * 2 >= 256 * 4, "records scratch lives in the queue");
+  static_assert(WB::BN * 2 >= 2 * WB::NP * 4, "records scratch lives in the queue");
 };
 
 constexpr int kNWV = 2;  // warps (blocks) per CTA of the on-chip-values kernels
@@ -1720,6 +1733,7 @@ cudaError_t launch_retain(const Geom& g, const T* x_slot, const uint8_t* dirs, T
   if (g.bc != 32) return cudaErrorInvalidValue;
   if (g.br == 32) return launch_finalize_r<T, 32>(g, x_slot, dirs, acc, st);
   if (g.br == 16) return launch_finalize_r<T, 16>(g, x_slot, dirs, acc, st);
+  if (g.br == 64) return launch_finalize_r<T, 64>(g, x_slot, dirs, acc, st);
   return cudaErrorInvalidValue;
 }
 template cudaError_t launch_retain<uint32_t>(const Geom&, const uint32_t*, const uint8_t*, uint32_t*, cudaStream_t);
@@ -1778,6 +1792,7 @@ cudaError_t launch_pass1(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t s
   if (a.g.bc != 32 || a.g.nw < 1 || a.g.nw > 4) return cudaErrorInvalidValue;
   if (a.g.br == 32) return launch_pass1_r<T, 32, WK>(a, from_dem, st);
   if (a.g.br == 16) return launch_pass1_r<T, 16, WK>(a, from_dem, st);
+  if (a.g.br == 64) return launch_pass1_r<T, 64, WK>(a, from_dem, st);
   return cudaErrorInvalidValue;
 }
 
@@ -1786,6 +1801,7 @@ cudaError_t launch_pass2(const PassArgs<T, WK>& a, cudaStream_t st) {
   if (a.g.bc != 32 || a.g.nw < 1 || a.g.nw > 4) return cudaErrorInvalidValue;
   if (a.g.br == 32) return launch_pass2_r<T, 32, WK>(a, st);
   if (a.g.br == 16) return launch_pass2_r<T, 16, WK>(a, st);
+  if (a.g.br == 64) return launch_pass2_r<T, 64, WK>(a, st);
   return cudaErrorInvalidValue;
 }
 

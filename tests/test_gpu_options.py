@@ -100,3 +100,23 @@ def test_option_validation(fa_lib):
                 ctx.set_option(name, bad)
             assert e.value.status == fa_lib.FA_E_ARG
         assert ctx.get_option("retention") == fa_lib.RETAIN and ctx.get_option("block_rows") == 32
+
+
+@pytest.mark.parametrize("retention", ["retain", "evict"])
+def test_options_64_row_blocks(fa_lib, retention):
+    """64 x 32 blocks (6 perimeter slots per lane, 64-bit source masks):
+    measured slower than 32 x 32 on cfg3 (20 vs 32 warps/SM), kept as an
+    option and checked like the others."""
+    z = inputs.filled_dem(43, 515, 333, coast_frac=0.1)
+    d = oracle.d8(z)
+    r = inputs.random_dirs(44, 300, 257, p_nodata=0.12, p_noflow=0.02)
+    w = inputs.weights_u32(44, r.shape, 0, 100)
+    with fa_lib.Context(0, tile=(128, 96)) as ctx:
+        ctx.set_option("block_rows", 64)
+        ctx.set_option("retention", retention)
+        assert (ctx.accumulate(dem=_cuda(z), atype="u32").cpu().numpy() == _u32(d)).all()
+        assert (ctx.accumulate_strips(3, dirs=_cuda(r), w=_cuda(w), atype="u64").cpu().numpy()
+                == oracle.accumulate(r, w)).all()
+        links, at, xo, acc = ctx.perimeter_records(dirs=_cuda(r), w=_cuda(w), atype="u64")
+        assert (links.cpu().numpy() == oracle.links(r, 128, 96)).all()
+        assert (acc.cpu().numpy() == oracle.accumulate(r, w)).all()
