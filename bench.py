@@ -278,8 +278,25 @@ def pcie_rates(torch, stream, h_in, d_in, h_out, d_out):
     stream.synchronize()
     nin = sum(t.numel() * t.element_size() for t in h_in)
     nout = h_out.numel() * h_out.element_size()
+    # both directions at once (two streams): the bound of a pipelined queue of rasters
+    s2 = torch.cuda.Stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    done2 = torch.cuda.Event()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    s2.wait_event(e0)
+    with torch.cuda.stream(stream):
+        for t, s in zip(d_in, h_in):
+            t.copy_(s, non_blocking=True)
+    with torch.cuda.stream(s2):
+        h_out.copy_(d_out, non_blocking=True)
+        done2.record(s2)
+    stream.wait_event(done2)
+    e1.record(stream)
+    stream.synchronize()
     return {"h2d_gbs": nin / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9,
-            "d2h_gbs": nout / (ev[2].elapsed_time(ev[3]) * 1e-3) / 1e9}
+            "d2h_gbs": nout / (ev[2].elapsed_time(ev[3]) * 1e-3) / 1e9,
+            "both_ms": e0.elapsed_time(e1), "both_gbs": (nin + nout) / (e0.elapsed_time(e1) * 1e-3) / 1e9}
 
 
 SMALL = (("cfg0", 8, "512^2 DEM seed 1, filled, w=1 -> u32, 1 tile (launch-bound; no roofline claim)"),
@@ -436,10 +453,32 @@ def run_gpu(args):
         e2e_ms = float(t.item())
     e2e = {"value": H * W / (e2e_ms * 1e-3) / 1e9, "unit": "Gcells/s",
            "h2d_bytes_per_step": int(hz.numel() * 4 + (hw.numel() * 4 if hw is not None else 0)) * world,
-           "d2h_bytes_per_step": int(ha.numel() * 8) * world, "ms_per_step": e2e_ms,
+           "d2h_bytes_per_step": int(ha.numel() * adt.itemsize) * world, "ms_per_step": e2e_ms,
            "pcie_h2d_gbs": round(pcie["h2d_gbs"], 1), "pcie_d2h_gbs": round(pcie["d2h_gbs"], 1),
+           "pcie_both_directions_gbs": round(pcie["both_gbs"], 1),
+           "pcie_both_directions_ms": round(pcie["both_ms"], 1),
            "pinned_numa_node": numa,
            "call": "fa_accumulate with pinned host buffers (the library stages them through the device)"}
+    if world == 1 and not args.no_batch:
+        # a queue of K rasters through fa_accumulate_batch: every step still
+        # uploads its z and w and downloads its A (same pinned buffers), but
+        # the upload of raster i+1 and the download of raster i-1 overlap the
+        # device work of raster i (PCIe is full duplex).  Pipeline fill and
+        # drain are inside the timed region.
+        nb = max(args.steps, 3)
+        ctx.accumulate_batch(dems=[hz] * 2, ws=[hw] * 2 if hw is not None else None, atype=atype,
+                             outs=[ha] * 2)  # warm-up (device buffer sets into the pool)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx.accumulate_batch(dems=[hz] * nb, ws=[hw] * nb if hw is not None else None, atype=atype, outs=[ha] * nb)
+        b_ms = (time.perf_counter() - t0) * 1e3 / nb
+        sb = ctx.stats()
+        single = {k: e2e[k] for k in ("value", "ms_per_step", "call")}
+        e2e.update({"value": H * W / (b_ms * 1e-3) / 1e9, "ms_per_step": b_ms, "rasters": nb,
+                    "device_ms_per_raster": sb["ms_compute"] / nb,
+                    "call": f"fa_accumulate_batch over {nb} rasters (pinned host buffers; each step uploads its z, w "
+                            "and downloads its A; raster i+1's upload and raster i-1's download overlap raster i)",
+                    "single_call": single})
 
     # ---- out-of-core path (N2): the same workload streamed from the pinned
     # host buffers one tile row (4096 rows) at a time, z and w uploaded twice
@@ -561,6 +600,8 @@ def main():
     ap.add_argument("--rows", type=int, default=None, help="smaller square variant (debug only)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ooc", action="store_true", help="skip the out-of-core and absorption measurements")
+    ap.add_argument("--no-batch", action="store_true",
+                    help="e2e from single fa_accumulate calls only (no fa_accumulate_batch queue)")
     ap.add_argument("--config", default="cfg3", choices=sorted(SPECS),
                     help="cfg3 (default; 1/2/4/8 GPUs) or cfg4 (17.2G cells, ~50 GB per GPU at 8 GPUs)")
     ap.add_argument("--gen-only", action="store_true", help="time the input generation on the host and exit")

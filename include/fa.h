@@ -206,6 +206,26 @@ FA_API fa_status fa_accumulate_streamed(fa_ctx* ctx, int64_t rows, int64_t cols,
                                         fa_wtype wtype, void* acc, fa_atype atype,
                                         int64_t strip_rows);
 
+/* A batch of `count` independent rasters of one shape, each accumulated
+ * exactly as fa_accumulate does it (same kernels, results and errors), from
+ * HOST buffers (pinned for overlap): dem[i] or dirs[i] (pass NULL for the
+ * array not used), w[i] (w NULL when wtype is FA_W_NONE), acc[i] (rows x
+ * cols of atype each).  Entries may repeat (the same input twice; an output
+ * twice gets the later raster).  Two device buffer sets: raster i+1 uploads
+ * on one copy stream and raster i-1 downloads on another (PCIe is full
+ * duplex) while raster i runs on the device -- the throughput of a queue of
+ * rasters is bounded by the larger copy direction, not their sum.  The
+ * rasters are independent problems (P:L49-57 per raster); the batch is the
+ * host-side pipeline around them.  count == 0: FA_OK; device pointers:
+ * FA_E_ARG.  On an error in raster i the message starts "raster i:",
+ * outputs of rasters < i are complete, later ones undefined.  fa_get_stats
+ * after the call: cells / graph_nodes / launches summed, ms_total the whole
+ * batch (first upload to last download), ms_compute the device pipelines,
+ * bytes_exchanged the PCIe bytes. */
+FA_API fa_status fa_accumulate_batch(fa_ctx* ctx, int count, int64_t rows, int64_t cols,
+                                     const float* const* dem, float nodata, const uint8_t* const* dirs,
+                                     const void* const* w, fa_wtype wtype, void* const* acc, fa_atype atype);
+
 /* fa_accumulate_streamed with absorption (N3, see fa_accumulate_absorb):
  * alpha is a HOST buffer streamed with the strips (4 more bytes per cell and
  * pass); output f64, w none or f32. */
@@ -303,6 +323,8 @@ typedef struct {
   int64_t launches; /* kernels launched by the call */
   double ms_d8;     /* the standalone D8 kernel (single-device path; 0 when D8 is fused into pass 1) */
   double ms_block;  /* the pass-1 block kernel alone (k_pass1), last strip */
+  double ms_compute; /* fa_accumulate_batch: the rasters' device pipelines, summed (ms_total: the whole
+                        batch, first upload to last download) */
 } fa_stats;
 FA_API fa_status fa_get_stats(const fa_ctx* ctx, void* out, int64_t out_bytes);
 

@@ -346,6 +346,19 @@ fa_status run_absorb(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float 
   return FA_OK;
 }
 
+// the copy streams and buffer events of the host-buffer pipelines (created on first use)
+fa_status ensure_copy_streams(fa_ctx* ctx) {
+  if (ctx->cs) return FA_OK;
+  CK(cudaStreamCreateWithFlags(&ctx->cs, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&ctx->cs_out, cudaStreamNonBlocking));
+  for (int b = 0; b < 2; ++b) {
+    CK(cudaEventCreateWithFlags(&ctx->ev_in[b], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_used[b], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_out[b], cudaEventDisableTiming));
+  }
+  return FA_OK;
+}
+
 // ---------------------------------------------------------------- out-of-core (N2)
 // The raster lives in host memory and only one strip of whole tile rows (two,
 // double-buffered) is resident at a time: the paper's EVICT strategy
@@ -366,15 +379,7 @@ fa_status run_streamed(fa_ctx* ctx, int64_t H, int64_t W, const float* dem_h, fl
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
   reset_run(ctx);
-  if (!ctx->cs) {
-    CK(cudaStreamCreateWithFlags(&ctx->cs, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&ctx->cs_out, cudaStreamNonBlocking));
-    for (int b = 0; b < 2; ++b) {
-      CK(cudaEventCreateWithFlags(&ctx->ev_in[b], cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&ctx->ev_used[b], cudaEventDisableTiming));
-      CK(cudaEventCreateWithFlags(&ctx->ev_out[b], cudaEventDisableTiming));
-    }
-  }
+  FS(ensure_copy_streams(ctx));
   cudaStream_t cs = ctx->cs;
   CK(cudaMemsetAsync(ctx->d_small, 0, 16 * sizeof(uint32_t), st));
   CK(cudaEventRecord(ctx->ev[0], st));
@@ -548,6 +553,104 @@ fa_status run_streamed(fa_ctx* ctx, int64_t H, int64_t W, const float* dem_h, fl
   ctx->stats.bytes_exchanged =
       (int64_t)(2 * H * W * ((dem_h ? 4 : 1) + (hasw ? 4 : 0) + (alpha_h ? 4 : 0)) + H * W * (int64_t)sizeof(T));
   CK(cudaStreamSynchronize(st));
+  return FA_OK;
+}
+
+// ---------------------------------------------------------------- batches of host rasters
+// Independent rasters of one shape in host memory (the serving case: a queue
+// of DEMs, each accumulated as by fa_accumulate).  Two device buffer sets:
+// raster i+1 uploads on one copy stream and raster i-1 downloads on another
+// (PCIe is full duplex) while raster i runs the single-device pipeline on
+// device buffers -- the same kernels, the same results as fa_accumulate.
+template <class T, int WK>
+fa_status run_batch(fa_ctx* ctx, int count, int64_t H, int64_t W, const float* const* dem_h, float nodata,
+                    const uint8_t* const* dirs_h, const void* const* w_h, T* const* acc_h) {
+  using namespace fa;
+  cudaStream_t st = ctx->st;
+  Runtime& rt = ctx->rt;
+  FS(ensure_copy_streams(ctx));
+  cudaStream_t cs = ctx->cs, co = ctx->cs_out;
+  const size_t n = (size_t)H * (size_t)W;
+  const bool hasw = WK != 0;
+  float* zb[2] = {nullptr, nullptr};
+  uint8_t* db[2] = {nullptr, nullptr};
+  float* wb[2] = {nullptr, nullptr};
+  T* ab[2] = {nullptr, nullptr};
+  const int nbuf = count > 1 ? 2 : 1;
+  rt.err = cudaSuccess;
+  for (int b = 0; b < nbuf; ++b) {
+    if (dem_h) zb[b] = rt.alloc<float>(n);
+    else db[b] = rt.alloc<uint8_t>(n);
+    if (hasw) wb[b] = rt.alloc<float>(n);
+    ab[b] = rt.alloc<T>(n);
+  }
+  cudaEvent_t tb = nullptr, te = nullptr;
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(cs);
+    cudaStreamSynchronize(co);
+    for (int b = 0; b < 2; ++b)
+      for (void* p : {(void*)zb[b], (void*)db[b], (void*)wb[b], (void*)ab[b]}) rt.free(p);
+    cudaStreamSynchronize(st);
+    if (tb) cudaEventDestroy(tb);
+    if (te) cudaEventDestroy(te);
+  };
+  if (rt.err) { cleanup(); return set_err(ctx, FA_E_NOMEM, "device allocation failed (two raster buffer sets)"); }
+  CK(cudaEventCreate(&tb));
+  CK(cudaEventCreate(&te));
+  // the buffers are allocated on st: the copy streams start after that
+  for (int b = 0; b < 2; ++b) CK(cudaEventRecord(ctx->ev_used[b], st));
+  CK(cudaStreamWaitEvent(cs, ctx->ev_used[0], 0));
+  CK(cudaEventRecord(tb, cs));
+  auto upload = [&](int i, int b) -> fa_status {
+    CK(cudaStreamWaitEvent(cs, ctx->ev_used[b], 0));  // raster i-2 is done with buffer set b
+    if (dem_h) CK(cudaMemcpyAsync(zb[b], dem_h[i], n * 4, cudaMemcpyHostToDevice, cs));
+    else CK(cudaMemcpyAsync(db[b], dirs_h[i], n, cudaMemcpyHostToDevice, cs));
+    if (hasw) CK(cudaMemcpyAsync(wb[b], w_h[i], n * 4, cudaMemcpyHostToDevice, cs));
+    CK(cudaEventRecord(ctx->ev_in[b], cs));
+    return FA_OK;
+  };
+  fa_stats last{};
+  int64_t launches = 0, nodes = 0;
+  double ms_kernels = 0;
+  fa_status r = upload(0, 0);
+  for (int i = 0; i < count && r == FA_OK; ++i) {
+    const int b = i % nbuf;
+    if (i + 1 < count) r = upload(i + 1, (i + 1) % nbuf);
+    if (r != FA_OK) break;
+    CK(cudaStreamWaitEvent(st, ctx->ev_in[b], 0));
+    if (i >= 2) CK(cudaStreamWaitEvent(st, ctx->ev_out[b], 0));  // raster i-2 is downloaded
+    Records rec;
+    r = run_acc<T, WK>(ctx, H, W, zb[b], nodata, db[b], wb[b], ab[b], rec, 1);
+    if (r != FA_OK) {
+      ctx->err = "raster " + std::to_string(i) + ": " + ctx->err;
+      break;
+    }
+    last = ctx->stats;
+    launches += last.launches;
+    nodes += last.graph_nodes;
+    ms_kernels += last.ms_total;
+    CK(cudaEventRecord(ctx->ev_used[b], st));
+    CK(cudaStreamWaitEvent(co, ctx->ev_used[b], 0));
+    CK(cudaMemcpyAsync(acc_h[i], ab[b], n * sizeof(T), cudaMemcpyDeviceToHost, co));
+    CK(cudaEventRecord(ctx->ev_out[b], co));
+  }
+  if (r != FA_OK) { cleanup(); return r; }
+  CK(cudaEventRecord(te, co));
+  CK(cudaEventSynchronize(te));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, tb, te);
+  cleanup();
+  if (rt.err) return set_err(ctx, FA_E_CUDA, cudaGetErrorString(rt.err));
+  // batch statistics: cells, nodes and launches summed over the rasters,
+  // ms_total from the first upload to the last download, the phases of the
+  // last raster, PCIe bytes in bytes_exchanged
+  ctx->stats = last;
+  ctx->stats.cells = (int64_t)count * H * W;
+  ctx->stats.graph_nodes = nodes;
+  ctx->stats.launches = launches;
+  ctx->stats.ms_total = ms;
+  ctx->stats.ms_compute = ms_kernels;
+  ctx->stats.bytes_exchanged = (int64_t)count * H * W * ((dem_h ? 4 : 1) + (hasw ? 4 : 0) + (int64_t)sizeof(T));
   return FA_OK;
 }
 
@@ -761,6 +864,43 @@ fa_status fa_accumulate_streamed(fa_ctx* ctx, int64_t rows, int64_t cols, const 
   }
   return wtype == FA_W_NONE ? run_streamed<double, 0>(ctx, rows, cols, dem, nodata, dirs, w, (double*)acc, strip_rows)
                             : run_streamed<double, 2>(ctx, rows, cols, dem, nodata, dirs, w, (double*)acc, strip_rows);
+}
+
+fa_status fa_accumulate_batch(fa_ctx* ctx, int count, int64_t rows, int64_t cols, const float* const* dem,
+                              float nodata, const uint8_t* const* dirs, const void* const* w, fa_wtype wtype,
+                              void* const* acc, fa_atype atype) {
+  if (!ctx) return FA_E_ARG;
+  ctx->err.clear();
+  if (count < 0) return set_err(ctx, FA_E_ARG, "count must be >= 0");
+  if (count == 0) return FA_OK;
+  if (rows <= 0 || cols <= 0) return set_err(ctx, FA_E_ARG, "rows and cols must be > 0");
+  if (!acc) return set_err(ctx, FA_E_ARG, "acc is NULL");
+  if ((dem == nullptr) == (dirs == nullptr)) return set_err(ctx, FA_E_ARG, "exactly one of dem, dirs must be given");
+  if ((wtype == FA_W_NONE) != (w == nullptr)) return set_err(ctx, FA_E_ARG, "w must be given iff wtype != NONE");
+  for (int i = 0; i < count; ++i) {
+    const void* in = dem ? (const void*)dem[i] : (const void*)dirs[i];
+    const void* wi = w ? w[i] : nullptr;
+    if (!in || !acc[i] || (w && !wi))
+      return set_err(ctx, FA_E_ARG, "raster " + std::to_string(i) + ": NULL buffer");
+    FS(check_types(ctx, dem ? dem[i] : nullptr, dirs ? dirs[i] : nullptr, wi, wtype, atype));
+    for (const void* p : {in, wi, (const void*)acc[i]})
+      if (p && is_device_ptr(p)) return set_err(ctx, FA_E_ARG, "fa_accumulate_batch takes host buffers");
+  }
+  CK(cudaSetDevice(ctx->device));
+  if (atype == FA_A_U32) {
+    auto a = reinterpret_cast<uint32_t* const*>(acc);
+    return wtype == FA_W_NONE ? run_batch<uint32_t, 0>(ctx, count, rows, cols, dem, nodata, dirs, w, a)
+                              : run_batch<uint32_t, 1>(ctx, count, rows, cols, dem, nodata, dirs, w, a);
+  }
+  if (atype == FA_A_U64) {
+    using U = unsigned long long;
+    auto a = reinterpret_cast<U* const*>(acc);
+    return wtype == FA_W_NONE ? run_batch<U, 0>(ctx, count, rows, cols, dem, nodata, dirs, w, a)
+                              : run_batch<U, 1>(ctx, count, rows, cols, dem, nodata, dirs, w, a);
+  }
+  auto a = reinterpret_cast<double* const*>(acc);
+  return wtype == FA_W_NONE ? run_batch<double, 0>(ctx, count, rows, cols, dem, nodata, dirs, w, a)
+                            : run_batch<double, 2>(ctx, count, rows, cols, dem, nodata, dirs, w, a);
 }
 
 int64_t fa_perimeter_slots(const fa_ctx* ctx, int64_t rows, int64_t cols) {

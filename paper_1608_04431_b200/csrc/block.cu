@@ -1065,8 +1065,8 @@ __global__ void __launch_bounds__(128, FA_P1_MINB) k_pass1(PassArgs<T, WK> P) {
   const int warp = threadIdx.x >> 5;
   WSmem<T, R, Z>& s = reinterpret_cast<WSmem<T, R, Z>*>(smem)[warp];
   const Geom& g = P.g;
-  const int64_t b = (int64_t)blockIdx.x * g.nw + warp;
-  if (b >= g.nblocks) return;
+  const int64_t b = P.b_begin + (int64_t)blockIdx.x * g.nw + warp;
+  if (b >= P.b_end) return;
   const int lane = lane_id();
   int64_t y0, x0;
   int h, w;
@@ -1142,8 +1142,8 @@ __global__ void __launch_bounds__(128) k_pass2(PassArgs<T, WK> P) {
   const int warp = threadIdx.x >> 5;
   WSmem<T, R, false>& s = reinterpret_cast<WSmem<T, R, false>*>(smem)[warp];
   const Geom& g = P.g;
-  const int64_t b = (int64_t)blockIdx.x * g.nw + warp;
-  if (b >= g.nblocks) return;
+  const int64_t b = P.b_begin + (int64_t)blockIdx.x * g.nw + warp;
+  if (b >= P.b_end) return;
   const int lane = lane_id();
   int64_t y0, x0;
   int h, w;
@@ -1465,8 +1465,8 @@ __global__ void __launch_bounds__(32 * kNWV) k_pass1v(PassArgs<T, WK> P) {
   const int warp = threadIdx.x >> 5;
   VSmem<T, R>& s = reinterpret_cast<VSmem<T, R>*>(smem)[warp];
   const Geom& g = P.g;
-  const int64_t b = (int64_t)blockIdx.x * kNWV + warp;
-  if (b >= g.nblocks) return;
+  const int64_t b = P.b_begin + (int64_t)blockIdx.x * kNWV + warp;
+  if (b >= P.b_end) return;
   const int lane = lane_id();
   int64_t y0, x0;
   int h, w;
@@ -1516,8 +1516,8 @@ __global__ void __launch_bounds__(32 * kNWV) k_pass2v(PassArgs<T, WK> P) {
   const int warp = threadIdx.x >> 5;
   VSmem<T, R>& s = reinterpret_cast<VSmem<T, R>*>(smem)[warp];
   const Geom& g = P.g;
-  const int64_t b = (int64_t)blockIdx.x * kNWV + warp;
-  if (b >= g.nblocks) return;
+  const int64_t b = P.b_begin + (int64_t)blockIdx.x * kNWV + warp;
+  if (b >= P.b_end) return;
   const int lane = lane_id();
   int64_t y0, x0;
   int h, w;
@@ -1563,13 +1563,13 @@ struct __align__(16) FSmem {
 
 template <class T, int R, int KB, bool ABS = false>
 __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ x_slot, const uint8_t* __restrict__ dirs,
-                                                  T* acc, const float* __restrict__ alpha = nullptr) {
+                                                  T* acc, const float* __restrict__ alpha, int64_t bbeg, int64_t bend) {
   using WB = WBT<R>;
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
   FSmem<T, R, KB>& s = reinterpret_cast<FSmem<T, R, KB>*>(smem)[warp];
-  const int64_t b0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * KB;
-  if (b0 >= g.nblocks) return;
+  const int64_t b0 = bbeg + ((int64_t)blockIdx.x * (blockDim.x >> 5) + warp) * KB;
+  if (b0 >= bend) return;
   const int lane = lane_id();
   const unsigned lt = (1u << lane) - 1u;
   int64_t y0s[KB], x0s[KB];
@@ -1580,7 +1580,7 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
     const int64_t b = b0 + k;
     hs[k] = ws[k] = 0;
     y0s[k] = x0s[k] = 0;
-    if (b < g.nblocks) g.block_box(b, y0s[k], x0s[k], hs[k], ws[k]);
+    if (b < bend) g.block_box(b, y0s[k], x0s[k], hs[k], ws[k]);
 #if FA_FIN_PREFETCH
     // pull the block's output rows into L2 before the walks' reductions
     // reach them: a reduction on a line that is not in L2 waits for its DRAM
@@ -1675,7 +1675,8 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
 }
 
 template <class T, int R, int KB>
-cudaError_t launch_finalize_k(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st) {
+cudaError_t launch_finalize_k(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st,
+                              int64_t bbeg, int64_t bend) {
   constexpr int NWC = 4;  // warps per CTA
   // At least 24 KB of shared memory per CTA: at most 9 CTAs (36 warps) per
   // SM, which keeps the acc rows the walks touch in L2 (measured on cfg3:
@@ -1684,15 +1685,16 @@ cudaError_t launch_finalize_k(const Geom& g, const T* x_slot, const uint8_t* dir
   sm = sm < 24576 ? 24576 : sm;
   auto k = k_finalize<T, R, KB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  const int64_t groups = (g.nblocks + KB - 1) / KB;
-  k<<<(unsigned)((groups + NWC - 1) / NWC), 32 * NWC, sm, st>>>(g, x_slot, dirs, acc, nullptr);
+  const int64_t groups = (bend - bbeg + KB - 1) / KB;
+  k<<<(unsigned)((groups + NWC - 1) / NWC), 32 * NWC, sm, st>>>(g, x_slot, dirs, acc, nullptr, bbeg, bend);
   return cudaGetLastError();
 }
 
 // one block per warp (2 or 4 measured slower on cfg3)
 template <class T, int R>
-cudaError_t launch_finalize_r(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st) {
-  return launch_finalize_k<T, R, 1>(g, x_slot, dirs, acc, st);
+cudaError_t launch_finalize_r(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st,
+                              int64_t bbeg, int64_t bend) {
+  return launch_finalize_k<T, R, 1>(g, x_slot, dirs, acc, st, bbeg, bend);
 }
 
 // absorption (f64, 32x32 blocks): pass 1 and the finalize with alpha
@@ -1700,7 +1702,7 @@ cudaError_t launch_pass1_absorb(const PassArgs<double, 0>* a0, const PassArgs<do
                                 cudaStream_t st) {
   auto go = [&](auto k, const auto& a) {
     const size_t sm = (from_dem ? sizeof(WSmem<double, 32, true>) : sizeof(WSmem<double, 32, false>)) * (size_t)a.g.nw;
-    const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
+    const unsigned grid = (unsigned)((a.b_end - a.b_begin + a.g.nw - 1) / a.g.nw);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<grid, 32 * a.g.nw, sm, st>>>(a);
   };
@@ -1724,22 +1726,28 @@ cudaError_t launch_retain_absorb(const Geom& g, const double* x_slot, const uint
   sm = sm < 24576 ? 24576 : sm;
   auto k = k_finalize<double, 32, 1, true>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k<<<(unsigned)((g.nblocks + NWC - 1) / NWC), 32 * NWC, sm, st>>>(g, x_slot, dirs, acc, alpha);
+  k<<<(unsigned)((g.nblocks + NWC - 1) / NWC), 32 * NWC, sm, st>>>(g, x_slot, dirs, acc, alpha, 0, g.nblocks);
   return cudaGetLastError();
 }
 
+// bend < 0: every block
 template <class T>
-cudaError_t launch_retain(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st) {
+cudaError_t launch_retain(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st,
+                          int64_t bbeg, int64_t bend) {
   if (g.bc != 32) return cudaErrorInvalidValue;
-  if (g.br == 32) return launch_finalize_r<T, 32>(g, x_slot, dirs, acc, st);
-  if (g.br == 16) return launch_finalize_r<T, 16>(g, x_slot, dirs, acc, st);
-  if (g.br == 64) return launch_finalize_r<T, 64>(g, x_slot, dirs, acc, st);
+  if (bend < 0) bend = g.nblocks;
+  if (bend <= bbeg) return cudaSuccess;
+  if (g.br == 32) return launch_finalize_r<T, 32>(g, x_slot, dirs, acc, st, bbeg, bend);
+  if (g.br == 16) return launch_finalize_r<T, 16>(g, x_slot, dirs, acc, st, bbeg, bend);
+  if (g.br == 64) return launch_finalize_r<T, 64>(g, x_slot, dirs, acc, st, bbeg, bend);
   return cudaErrorInvalidValue;
 }
-template cudaError_t launch_retain<uint32_t>(const Geom&, const uint32_t*, const uint8_t*, uint32_t*, cudaStream_t);
+template cudaError_t launch_retain<uint32_t>(const Geom&, const uint32_t*, const uint8_t*, uint32_t*, cudaStream_t,
+                                             int64_t, int64_t);
 template cudaError_t launch_retain<unsigned long long>(const Geom&, const unsigned long long*, const uint8_t*,
-                                                       unsigned long long*, cudaStream_t);
-template cudaError_t launch_retain<double>(const Geom&, const double*, const uint8_t*, double*, cudaStream_t);
+                                                       unsigned long long*, cudaStream_t, int64_t, int64_t);
+template cudaError_t launch_retain<double>(const Geom&, const double*, const uint8_t*, double*, cudaStream_t, int64_t,
+                                           int64_t);
 
 // ---------------------------------------------------------------- launchers
 // pass 1: the block's values on chip (k_pass1v) or in the output raster
@@ -1749,19 +1757,19 @@ template <class T, int R, int WK>
 cudaError_t launch_pass1_r(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t st) {
   if (a.vsmem) {
     const size_t sm = sizeof(VSmem<T, R>) * (size_t)kNWV;
-    const unsigned grid = (unsigned)((a.g.nblocks + kNWV - 1) / kNWV);
+    const unsigned grid = (unsigned)((a.b_end - a.b_begin + kNWV - 1) / kNWV);
     auto k = from_dem ? k_pass1v<T, R, WK, true> : k_pass1v<T, R, WK, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<grid, 32 * kNWV, sm, st>>>(a);
   } else if (from_dem) {
     const size_t sm = sizeof(WSmem<T, R, true>) * (size_t)a.g.nw;
-    const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
+    const unsigned grid = (unsigned)((a.b_end - a.b_begin + a.g.nw - 1) / a.g.nw);
     auto k = k_pass1<T, R, WK, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<grid, 32 * a.g.nw, sm, st>>>(a);
   } else {
     const size_t sm = sizeof(WSmem<T, R, false>) * (size_t)a.g.nw;
-    const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
+    const unsigned grid = (unsigned)((a.b_end - a.b_begin + a.g.nw - 1) / a.g.nw);
     auto k = k_pass1<T, R, WK, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<grid, 32 * a.g.nw, sm, st>>>(a);
@@ -1773,14 +1781,14 @@ template <class T, int R, int WK>
 cudaError_t launch_pass2_r(const PassArgs<T, WK>& a, cudaStream_t st) {
   if (!a.vsmem) {
     const size_t sm = sizeof(WSmem<T, R, false>) * (size_t)a.g.nw;
-    const unsigned grid = (unsigned)((a.g.nblocks + a.g.nw - 1) / a.g.nw);
+    const unsigned grid = (unsigned)((a.b_end - a.b_begin + a.g.nw - 1) / a.g.nw);
     auto k = k_pass2<T, R, WK>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<grid, 32 * a.g.nw, sm, st>>>(a);
     return cudaGetLastError();
   }
   const size_t sm = sizeof(VSmem<T, R>) * (size_t)kNWV;
-  const unsigned grid = (unsigned)((a.g.nblocks + kNWV - 1) / kNWV);
+  const unsigned grid = (unsigned)((a.b_end - a.b_begin + kNWV - 1) / kNWV);
   auto k = k_pass2v<T, R, WK>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k<<<grid, 32 * kNWV, sm, st>>>(a);

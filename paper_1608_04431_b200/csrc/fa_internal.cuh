@@ -240,6 +240,7 @@ struct PassArgs {
   uint32_t* status;
   bool retain;  // pass 1 writes the block-local accumulation into acc (RETAIN)
   bool vsmem;   // block values on chip (k_pass1v / k_pass2v) instead of in acc (FA_OPT_VALUES)
+  int64_t b_begin, b_end;  // the launch covers blocks [b_begin, b_end) (chunked: host-buffer pipelining)
   bool cut;     // tile records wanted: slot roots also for every slot on a tile edge
   // absorption: per-cell fraction of A passed on
   // (row-major like acc), the product of alpha along each entry slot's

@@ -31,7 +31,8 @@ cudaError_t launch_pass1(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t s
 template <class T, int WK>
 cudaError_t launch_pass2(const PassArgs<T, WK>& a, cudaStream_t st);
 template <class T>
-cudaError_t launch_retain(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st);
+cudaError_t launch_retain(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st,
+                          int64_t bbeg = 0, int64_t bend = -1);
 cudaError_t launch_d8(const float* dem, const float* dem_up, const float* dem_dn, int64_t H, int64_t W,
                       float nodata, uint8_t* dirs,
                       cudaStream_t st);
@@ -313,6 +314,8 @@ fa::PassArgs<T, WK> pass_args(fa_ctx* ctx, Strip<T>& s) {
   a.acc = s.acc ? s.acc : s.acc_tmp;  // pass 1 accumulates in place (RETAIN)
   a.retain = s.acc != nullptr && ctx->retain();
   a.vsmem = ctx->opt_values == FA_VALUES_SMEM;
+  a.b_begin = 0;
+  a.b_end = s.g.nblocks;
   return a;
 }
 

@@ -28,7 +28,7 @@ EXPORTS = ["fa_create", "fa_destroy", "fa_last_error", "fa_flowdirs", "fa_accumu
            "fa_accumulate_strips", "fa_perimeter_slots", "fa_perimeter_records", "fa_nccl_unique_id",
            "fa_accumulate_dist", "fa_get_stats", "fa_accumulate_streamed",
            "fa_accumulate_absorb", "fa_accumulate_absorb_dist", "fa_accumulate_absorb_streamed", "fa_fill",
-           "fa_set_option", "fa_get_option", "fa_accumulate_dist_loopback"]
+           "fa_set_option", "fa_get_option", "fa_accumulate_dist_loopback", "fa_accumulate_batch"]
 # context options (fa.h fa_option); values: RETAIN / EVICT, D8_SPLIT / D8_FUSED, block rows 32 / 16,
 # graph walk cap, fill tile 32 / 64
 OPT_RETENTION, OPT_D8, OPT_BLOCK_ROWS, OPT_WALK_CAP, OPT_FILL_TILE, OPT_VALUES, OPT_GRAPH, OPT_DIST_RECORDS = range(1, 9)
@@ -67,7 +67,7 @@ class Stats(ctypes.Structure):
                 ("tile_nodes", ctypes.c_int64), ("peel_rounds", ctypes.c_int64),
                 ("contract_levels", ctypes.c_int64), ("jump_rounds", ctypes.c_int64),
                 ("bytes_exchanged", ctypes.c_int64), ("launches", ctypes.c_int64),
-                ("ms_d8", ctypes.c_double), ("ms_block", ctypes.c_double)]
+                ("ms_d8", ctypes.c_double), ("ms_block", ctypes.c_double), ("ms_compute", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -110,6 +110,7 @@ def load() -> ctypes.CDLL:
     PP = ctypes.POINTER(P)
     lib.fa_accumulate_dist_loopback.argtypes = [PP, ctypes.c_int, I, I, ctypes.POINTER(I), ctypes.POINTER(I), PP, F,
                                                 PP, PP, ctypes.c_int, PP, PP, ctypes.c_int]
+    lib.fa_accumulate_batch.argtypes = [P, ctypes.c_int, I, I, PP, F, PP, PP, ctypes.c_int, PP, ctypes.c_int]
     for fn in EXPORTS:
         if fn not in ("fa_last_error", "fa_perimeter_slots"):
             getattr(lib, fn).restype = ctypes.c_int
@@ -276,6 +277,50 @@ class Context:
         self._check(self.lib.fa_accumulate_strips(self.h, int(nstrips), rows, cols, _ptr(dem), float(nodata),
                                                   _ptr(dirs), _ptr(w), _wtype(w), _ptr(out), a))
         return out
+
+    def accumulate_batch(self, dems=None, dirs=None, ws=None, atype: str = "u32", nodata: float = -9999.0,
+                         outs=None):
+        """fa_accumulate_batch: a list of independent host rasters (numpy, or CPU / pinned
+        torch tensors) of one shape; uploads, device work and downloads of neighbouring
+        rasters overlap.  Returns the list of outputs (host, pinned when the inputs are)."""
+        srcs = dems if dems is not None else dirs
+        if srcs is None or (dems is not None and dirs is not None):
+            raise ValueError("give exactly one of dems, dirs")
+        n = len(srcs)
+        if ws is not None and len(ws) != n:
+            raise ValueError("ws must have one entry per raster")
+        if n == 0:
+            return []
+        rows, cols = srcs[0].shape
+        for i in range(n):
+            _check_inputs(dems[i] if dems is not None else None, dirs[i] if dirs is not None else None,
+                          ws[i] if ws is not None else None, (rows, cols))
+        wt = _wtype(ws[0]) if ws is not None else W_NONE
+        if ws is not None and any(_wtype(x) != wt for x in ws):
+            raise TypeError("all weights must have one dtype")
+        a = ATYPES[atype]
+        if outs is None:
+            outs = []
+            for s in srcs:
+                if isinstance(s, torch.Tensor):
+                    outs.append(torch.empty((rows, cols), dtype=TORCH_ACC[a], pin_memory=s.is_pinned()))
+                else:
+                    import numpy as np
+
+                    outs.append(np.empty((rows, cols), {A_U32: np.uint32, A_U64: np.uint64, A_F64: np.float64}[a]))
+        if len(outs) != n:
+            raise ValueError("outs must have one entry per raster")
+        for o in outs:
+            _check(o, "out", (ACC_DTYPE[a],), (rows, cols))
+
+        def arr(lst):
+            if lst is None:
+                return None
+            return (ctypes.c_void_p * n)(*[_ptr(x) for x in lst])
+
+        self._check(self.lib.fa_accumulate_batch(self.h, n, rows, cols, arr(dems), float(nodata), arr(dirs),
+                                                 arr(ws), wt, arr(outs), a))
+        return outs
 
     def accumulate_streamed(self, dem=None, dirs=None, w=None, atype: str = "u32", nodata: float = -9999.0,
                             strip_rows: int = 0, out=None):

@@ -71,3 +71,24 @@ def test_cfg4_recipe_eight_strips_u64(fa_lib):
         one = ctx.accumulate(dem=_cuda(cfg.dem), atype="u64").cpu().numpy()
     assert (got == exp).all()
     assert (one == exp).all()
+
+
+@pytest.mark.slow
+def test_serpentine_beyond_2_31_cells(fa_lib):
+    """49152^2 = 2.42e9 cells on one GPU (more than 2^31, as a cfg4 strip of
+    8 ranks holds 2^31): every cell index, block id and slot crosses 32-bit
+    signed ranges, and the river is ONE chain of 2.4e9 cells through ~75 M
+    block exits (the graph's chain contraction at its deepest).  Closed
+    form P6: A = W*y + (y even ? x : W-1-x) + 1, up to 2.42e9 (fits u32)."""
+    n = 49152
+    d = inputs.serpentine(n, n)
+    with fa_lib.Context(0) as ctx:
+        got = ctx.accumulate(dirs=torch.from_numpy(d).cuda(), atype="u32")
+        torch.cuda.synchronize()
+    del d
+    x = np.arange(n, dtype=np.uint64)
+    for y0 in range(0, n, 4096):
+        rows = got[y0:y0 + 4096].cpu().numpy().astype(np.uint64)
+        y = np.arange(y0, y0 + rows.shape[0], dtype=np.uint64)[:, None]
+        exp = n * y + np.where(y % 2 == 0, x[None, :], n - 1 - x[None, :]) + 1
+        assert (rows == exp).all(), y0

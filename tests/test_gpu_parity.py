@@ -297,6 +297,13 @@ def test_errors(fa_lib):
         with pytest.raises(fa_lib.FaError) as e:
             ctx.accumulate(dirs=_cuda(np.zeros((64, 64), np.uint8)), w=_cuda(wbig), atype="u32")
         assert e.value.status == fa_lib.FA_E_OVERFLOW
+        for shape in ((0, 16), (16, 0)):  # empty rasters are rejected, not run
+            with pytest.raises(fa_lib.FaError) as e:
+                ctx.accumulate(dirs=torch.zeros(shape, dtype=torch.uint8, device="cuda"), atype="u32")
+            assert e.value.status == fa_lib.FA_E_ARG
+        with pytest.raises(fa_lib.FaError) as e:  # dem and dirs together
+            ctx.accumulate(dem=_cuda(z), dirs=_cuda(np.zeros((10, 10), np.uint8)), atype="u32")
+        assert e.value.status == fa_lib.FA_E_ARG
 
 
 def test_cycle_across_blocks(fa_lib):
