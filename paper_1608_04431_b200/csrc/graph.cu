@@ -71,6 +71,37 @@ __global__ void k_fold_leaves(int64_t nslots, const T* __restrict__ x_slot, cons
   }
 }
 
+// A_T at every root of a tile-cut block-exit forest without solving it: the
+// root's subtree sum is the sum of the own values (node value + folded
+// leaves) of every node whose root it is (linearity), weighted by
+// the product of edge weights up to the root with absorption (ptroot)
+// Big trees put thousands of nodes on one root (node ids are allocated block
+// by block, so neighbouring ids share roots): lanes of a warp with the same
+// root are summed with shuffles first, one reduction per root per warp.
+template <class T>
+__global__ void k_root_sum(uint32_t nn, const uint32_t* __restrict__ troot, const T* __restrict__ own,
+                           const double* __restrict__ ptroot, T* R) {
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t base = blockIdx.x * blockDim.x; base < nn; base += stride) {
+    const uint32_t v = base + threadIdx.x;  // base is warp-uniform: whole warps reach the match
+    const bool ok = v < nn;
+    T x = (T)0;
+    uint32_t r = 0xFFFFFFFFu;
+    if (ok) {
+      x = own[v];
+      if constexpr (std::is_same<T, double>::value) {
+        if (ptroot) x *= ptroot[v];
+      }
+      r = troot[v];
+    }
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, r);
+    T sum = (T)0;
+    for (unsigned m = peers; m; m &= m - 1u) sum += __shfl_sync(peers, x, __ffs(m) - 1);
+    if (ok && lane == __ffs(peers) - 1 && sum != (T)0) atomic_add(&R[r], sum);
+  }
+}
+
 // H4 tile perimeter records of one strip: F (direction), L (Alg. 2 link) and
 // A_T (tile-local accumulation, at FlowExternal slots) per tile perimeter slot
 // absorption (ABS): also tile_f per slot -- a linked slot's factor to its
@@ -245,6 +276,21 @@ template cudaError_t launch_fold_leaves<uint32_t>(cudaStream_t, int64_t, const u
 template cudaError_t launch_fold_leaves<unsigned long long>(cudaStream_t, int64_t, const unsigned long long*,
                                                             const uint32_t*, unsigned long long*);
 template cudaError_t launch_fold_leaves<double>(cudaStream_t, int64_t, const double*, const uint32_t*, double*);
+
+template <class T>
+cudaError_t launch_root_sum(cudaStream_t st, uint32_t nn, const uint32_t* troot, const T* own, const double* ptroot,
+                            T* R) {
+  if (nn == 0) return cudaSuccess;
+  k_root_sum<T><<<grid_for(nn), 256, 0, st>>>(nn, troot, own, ptroot, R);
+  return cudaGetLastError();
+}
+template cudaError_t launch_root_sum<uint32_t>(cudaStream_t, uint32_t, const uint32_t*, const uint32_t*,
+                                               const double*, uint32_t*);
+template cudaError_t launch_root_sum<unsigned long long>(cudaStream_t, uint32_t, const uint32_t*,
+                                                         const unsigned long long*, const double*,
+                                                         unsigned long long*);
+template cudaError_t launch_root_sum<double>(cudaStream_t, uint32_t, const uint32_t*, const double*, const double*,
+                                             double*);
 
 template <class T>
 cudaError_t launch_scatter_x(cudaStream_t st, uint32_t nn, const uint32_t* tgt, const uint8_t* flags,

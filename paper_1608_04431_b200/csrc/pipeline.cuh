@@ -60,6 +60,9 @@ cudaError_t launch_scatter_x(cudaStream_t st, uint32_t nn, const uint32_t* tgt, 
 template <class T>
 cudaError_t launch_fold_leaves(cudaStream_t st, int64_t nslots, const T* x_slot, const uint32_t* slot_root, T* S);
 template <class T>
+cudaError_t launch_root_sum(cudaStream_t st, uint32_t nn, const uint32_t* troot, const T* own, const double* ptroot,
+                            T* R);
+template <class T>
 cudaError_t launch_tile_records(cudaStream_t st, const Geom& g, int64_t nslots, const int64_t* tbase,
                                 const uint8_t* dirs, const uint32_t* slot_root, const uint32_t* troot,
                                 const uint8_t* flags, const uint32_t* node_slot, const T* S1,
@@ -269,6 +272,7 @@ struct Strip {
   uint32_t* troot = nullptr;
   int64_t slot0 = 0, nslots = 0;  // this strip's range of global tile perimeter slots
   int64_t* dtbase = nullptr;      // local tile slot bases (device)
+  bool own_in_S = false;          // S holds node values + folded leaves (strip_records): phase B starts there
   void release(fa::Runtime& rt) {
     for (void* p : {(void*)dirs_buf, (void*)slot_root, (void*)node_val, (void*)node_slot, (void*)node_tgt,
                     (void*)node_flags, (void*)x_slot, (void*)parent, (void*)S, (void*)troot, (void*)dtbase,
@@ -459,22 +463,35 @@ fa_status strip_records(fa_ctx* ctx, Strip<T>& s, uint32_t* links, uint8_t* fdir
                              s.slot_root, s.wv, s.S));
       CK(launch_g1_weights_cut(st, s.nn, s.node_flags, s.wv));
       rt.launches += 3;
-      CK(forest_solve_weighted(rt, s.nn, s.parent, s.wv, s.S));
       CK(forest_roots_weighted(rt, s.nn, s.parent, s.wv, s.troot, s.ptroot));
+      T* R = rt.alloc<T>(s.nn);
+      if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+      CK(cudaMemsetAsync(R, 0, (s.nn ? s.nn : 1) * sizeof(T), st));
+      CK(launch_root_sum<T>(st, s.nn, s.troot, s.S, s.ptroot, R));
       CK(launch_tile_records<T>(st, s.g, s.nslots, s.dtbase, s.dirs_in(), s.slot_root, s.troot, s.node_flags,
-                                s.node_slot, s.S, links, fdir, tile_acc, s.slot_f,
+                                s.node_slot, R, links, fdir, tile_acc, s.slot_f,
                                 s.ptroot, s.alpha, tile_f));
-      ++rt.launches;
+      rt.launches += 2;
+      rt.free(R);
       return FA_OK;
     }
   }
   CK(launch_fold_leaves<T>(st, s.g.nblocks * s.g.pb, s.x_slot, s.slot_root, s.S));  // leaves raked in pass 1
   ++rt.launches;
-  CK(forest_solve<T>(rt, s.nn, s.parent, s.S));  // A_T at every block exit (Alg. 1 on each tile)
+  // A_T is needed at the tile exits only (the roots of the tile-cut forest):
+  // root ids by pointer jumping, then one reduction of the own values by
+  // root -- no forest solve here; phase B (strip_finish) solves the strip
+  // graph once, with the injected offsets
   CK(forest_roots(rt, s.nn, s.parent, s.troot));
+  T* R = rt.alloc<T>(s.nn);
+  if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+  CK(cudaMemsetAsync(R, 0, (s.nn ? s.nn : 1) * sizeof(T), st));
+  CK(launch_root_sum<T>(st, s.nn, s.troot, s.S, nullptr, R));
   CK(launch_tile_records<T>(st, s.g, s.nslots, s.dtbase, s.dirs_in(), s.slot_root, s.troot, s.node_flags,
-                            s.node_slot, s.S, links, fdir, tile_acc));
-  ++rt.launches;
+                            s.node_slot, R, links, fdir, tile_acc));
+  rt.launches += 2;
+  rt.free(R);
+  s.own_in_S = true;
   return FA_OK;
 }
 
@@ -519,7 +536,7 @@ fa_status strip_finish(fa_ctx* ctx, Strip<T>& s, const T* xT_global) {
   using namespace fa;
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
-  CK(cudaMemcpyAsync(s.S, s.node_val, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
+  if (!s.own_in_S) CK(cudaMemcpyAsync(s.S, s.node_val, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
   if constexpr (std::is_same<T, double>::value) {
     if (s.alpha) {
       // absorption: weighted fold, injection scaled by the entry path factor,
@@ -545,9 +562,12 @@ fa_status strip_finish(fa_ctx* ctx, Strip<T>& s, const T* xT_global) {
       return FA_OK;
     }
   }
-  // leaves first (x_slot holds only their pass-1 values here), then x_T
-  CK(launch_fold_leaves<T>(st, s.g.nblocks * s.g.pb, s.x_slot, s.slot_root, s.S));
-  ++rt.launches;
+  // leaves first (x_slot holds only their pass-1 values here; strip_records
+  // of the same strip object has folded them already), then x_T
+  if (!s.own_in_S) {
+    CK(launch_fold_leaves<T>(st, s.g.nblocks * s.g.pb, s.x_slot, s.slot_root, s.S));
+    ++rt.launches;
+  }
   CK(launch_inject_slots<T>(st, s.g, s.nslots, s.dtbase, xT_global + s.slot0, s.slot_root, s.S, s.x_slot));
   ++rt.launches;
   CK(forest_solve<T>(rt, s.nn, s.parent, s.S));  // true A at every block exit
