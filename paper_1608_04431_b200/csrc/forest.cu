@@ -502,6 +502,10 @@ template cudaError_t forest_solve<double>(Runtime&, uint32_t, const uint32_t*, d
 
 cudaError_t forest_roots(Runtime& rt, uint32_t n, const uint32_t* parent, uint32_t* root) {
   if (n == 0) return cudaSuccess;
+  {  // one cooperative launch when possible (no host read between rounds)
+    const cudaError_t e = forest_roots_device(rt, n, parent, root);
+    if (e != cudaErrorNotSupported) return e;
+  }
   cudaStream_t st = rt.st;
   uint32_t* tmp = rt.alloc<uint32_t>(n);
   uint32_t* ctr = rt.alloc<uint32_t>(1);

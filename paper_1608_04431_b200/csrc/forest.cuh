@@ -61,6 +61,8 @@ cudaError_t forest_roots_weighted(Runtime& rt, uint32_t n, const uint32_t* paren
 
 // root of every node in a forest (pointer jumping); cycles -> ST_CYCLE
 cudaError_t forest_roots(Runtime& rt, uint32_t n, const uint32_t* parent, uint32_t* root);
+// the same as one cooperative launch (forest_dev.cu); cudaErrorNotSupported when that is not possible
+cudaError_t forest_roots_device(Runtime& rt, uint32_t n, const uint32_t* parent, uint32_t* root);
 
 inline unsigned grid_for(int64_t n, int threads = 256) {
   int64_t g = (n + threads - 1) / threads;

@@ -400,6 +400,45 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
   }
 }
 
+// the root of every node (pointer jumping, forest.cu's k_root_jump rounds)
+// as one cooperative launch: the convergence test after each round is read
+// by every thread after the barrier (rotating flag slots as above), so no
+// host read between rounds.  The result ends in ra.
+__global__ void __launch_bounds__(256) k_roots_dev(uint32_t n, const uint32_t* __restrict__ parent, uint32_t* ra,
+                                                   uint32_t* rb, uint32_t* flags, uint32_t* status) {
+  cg::grid_group grid = cg::this_grid();
+  const uint32_t tid = (uint32_t)grid.thread_rank();
+  const uint32_t nth = (uint32_t)grid.size();
+  for (uint32_t v = tid; v < n; v += nth) {
+    const uint32_t p = parent[v];
+    ra[v] = p == kNone ? v : p;
+  }
+  grid.sync();
+  uint32_t* a = ra;
+  uint32_t* b = rb;
+  for (int j = 0;; ++j) {
+    bool ch = false;
+    for (uint32_t v = tid; v < n; v += nth) {
+      const uint32_t x = ld(&a[v]), y = ld(&a[x]);
+      b[v] = y;
+      ch |= x != y;
+    }
+    if (__syncthreads_or(ch) && threadIdx.x == 0) atomicOr(&flags[j % 3], 1u);
+    if (tid == 0) flags[(j + 1) % 3] = 0u;  // last read two barriers ago
+    grid.sync();
+    uint32_t* t = a;
+    a = b;
+    b = t;
+    if (!ld(&flags[j % 3])) break;
+    if (j + 1 > kDevMaxJump) {
+      if (tid == 0) atomicOr(status, ST_CYCLE);
+      break;
+    }
+  }
+  if (a != ra)
+    for (uint32_t v = tid; v < n; v += nth) ra[v] = a[v];
+}
+
 template <class T, bool WG>
 cudaError_t solve_dev(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, const T* wv, bool& done) {
   done = false;
@@ -529,6 +568,32 @@ template cudaError_t forest_solve_device_async<unsigned long long>(Runtime&, uin
                                                                    const uint32_t*, unsigned long long*, uint32_t*);
 template cudaError_t forest_solve_device_async<double>(Runtime&, uint32_t, const uint32_t*, const uint32_t*, double*,
                                                        uint32_t*);
+
+cudaError_t forest_roots_device(Runtime& rt, uint32_t n, const uint32_t* parent, uint32_t* root) {
+  if (n == 0) return cudaSuccess;
+  int dev = 0, sms = 0, coop = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_roots_dev, 256, 0) != cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    return cudaErrorNotSupported;
+  }
+  cudaStream_t st = rt.st;
+  uint32_t* tmp = rt.alloc<uint32_t>(n);
+  uint32_t* flags = rt.alloc<uint32_t>(4);
+  if (rt.err) return rt.err;
+  cudaMemsetAsync(flags, 0, 4 * sizeof(uint32_t), st);
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * per_sm, ((int64_t)n + 255) / 256));
+  uint32_t* status = rt.d_status;
+  void* args[] = {&n, &parent, &root, &tmp, &flags, &status};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_roots_dev, grid, 256, args, 0, st);
+  ++rt.launches;
+  rt.free(tmp);
+  rt.free(flags);
+  return e;
+}
 
 template <class T>
 cudaError_t forest_solve_device(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, bool& done) {
