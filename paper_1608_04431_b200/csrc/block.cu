@@ -80,24 +80,28 @@ namespace fa {
 #endif
 constexpr uint8_t kOut = 254;  // ring cell: outside the block, data
 
-// Successor byte of an in-block cell: its D8 code (bits 0-3) plus
-// SB_DROP (it drains into in-block NoData: the flow is dropped, D8) and
-// SB_EXIT (its code leaves the block); NoData cells keep 255.  The cell
-// continues to an in-block data target iff the byte is a bare code 1..8,
-// and the target is the cell index plus the code's offset (sb_target).
-constexpr uint32_t SB_DROP = 0x10u, SB_EXIT = 0x20u;
-__device__ __forceinline__ bool sb_go(uint32_t sb) { return sb - 1u < 8u; }
+// Successor byte of an in-block cell.  A cell that continues to an
+// in-block data target holds its code's block offset biased by SB_BIAS
+// (31..97, bit 7 clear), so a step is one compare (sb_go) and one add
+// (WBT::target).  Stops have bit 7 set: SB_STOP (NoFlow), SB_STOP | SB_DROP
+// (drains into in-block NoData: the flow is dropped, D8), SB_STOP | SB_EXIT
+// (the code leaves the block: a block exit); NoData cells keep 255.
+constexpr uint32_t SB_BIAS = 64u, SB_STOP = 0x80u, SB_DROP = 0x10u, SB_EXIT = 0x20u;
+__device__ __forceinline__ bool sb_go(uint32_t sb) { return sb < SB_STOP; }
+// a data cell's successor byte says it leaves the block (255 also matches: callers know the cell is data)
+__device__ __forceinline__ bool sb_exit(uint32_t sb) { return (sb & (SB_STOP | SB_EXIT)) == (SB_STOP | SB_EXIT); }
 // direction codes (bit k) leaving a cell through its N / S / W / E side
 constexpr uint32_t DM_N = (1u << 1) | (1u << 2) | (1u << 8);
 constexpr uint32_t DM_S = (1u << 4) | (1u << 5) | (1u << 6);
 constexpr uint32_t DM_W = (1u << 6) | (1u << 7) | (1u << 8);
 constexpr uint32_t DM_E = (1u << 2) | (1u << 3) | (1u << 4);
 
-// packed signed 8-bit offsets of direction codes 1..8 for a row stride S
-__host__ __device__ constexpr uint64_t pack_offsets(int S) {
+// packed 8-bit offsets of direction codes 1..8 for a row stride S, plus a
+// per-byte bias (0: signed offsets; SB_BIAS: the successor-byte encoding)
+__host__ __device__ constexpr uint64_t pack_offsets(int S, int bias = 0) {
   uint64_t t = 0;
   for (int k = 1; k <= 8; ++k)
-    t |= (uint64_t)(uint8_t)(int8_t)(dir_dy(k) * S + dir_dx(k)) << (8 * (k - 1));
+    t |= (uint64_t)(uint8_t)(int8_t)(dir_dy(k) * S + dir_dx(k) + bias) << (8 * (k - 1));
   return t;
 }
 
@@ -113,13 +117,13 @@ struct WBT {
   static constexpr int ZN = ZR * ZS;
   static constexpr uint64_t OFFH = pack_offsets(HS);
   static constexpr uint64_t OFFA = pack_offsets(BC);
+  static constexpr uint64_t OFFB = pack_offsets(BC, (int)SB_BIAS);  // successor bytes of codes 1..8
+  static_assert(BC + 1 + SB_BIAS < SB_STOP && SB_BIAS > BC + 1, "biased offsets fit below SB_STOP");
   __device__ static __forceinline__ int offH(int d) { return (int)(int8_t)(OFFH >> (8 * (d - 1))); }
   __device__ static __forceinline__ int offA(int d) { return (int)(int8_t)(OFFA >> (8 * (d - 1))); }
-  // in-block target of cell c with bare code d (1..8): a PRMT picks the
-  // code's signed offset byte, then a sign extension
-  __device__ static __forceinline__ uint32_t target(uint32_t c, uint32_t d) {
-    return c + (uint32_t)(int32_t)(int8_t)__byte_perm((uint32_t)OFFA, (uint32_t)(OFFA >> 32), d - 1u);
-  }
+  __device__ static __forceinline__ uint32_t offB(int d) { return (uint32_t)(uint8_t)(OFFB >> (8 * (d - 1))); }
+  // in-block target of cell c from its (continuing) successor byte sb
+  __device__ static __forceinline__ uint32_t target(uint32_t c, uint32_t sb) { return c + sb - SB_BIAS; }
   __device__ static __forceinline__ int hidx(int ly, int lx) { return (ly + 1) * HS + HOFF + lx; }
   __device__ static __forceinline__ int zidx(int ly, int lx) { return (ly + 2) * ZS + ZOFF + lx; }
   static constexpr int NJ = (PB + 31) / 32;  // perimeter slots per lane
@@ -192,10 +196,11 @@ __device__ __forceinline__ int bperim_index(int x, int y, int h, int w) {
 // is NoData) and the codes that leave the block from this cell (forb)
 __device__ __forceinline__ uint32_t succ_byte(int d, uint32_t forb) {
   const int k = d & 15;
-  if (d == kNoData || k == 0) return (uint32_t)(d == kNoData ? kNoData : 0);
-  if ((forb >> k) & 1u) return (uint32_t)k | SB_EXIT;
-  if (d & 16) return (uint32_t)k | SB_DROP;  // drains into in-block NoData: dropped (D8)
-  return (uint32_t)k;
+  if (d == kNoData) return kNoData;
+  if (k == 0) return SB_STOP;
+  if ((forb >> k) & 1u) return SB_STOP | SB_EXIT;
+  if (d & 16) return SB_STOP | SB_DROP;  // drains into in-block NoData: dropped (D8)
+  return WBT<32>::offB(k);
 }
 
 __device__ __forceinline__ uint32_t forb_col(int lx, int w) {
@@ -203,6 +208,18 @@ __device__ __forceinline__ uint32_t forb_col(int lx, int w) {
 }
 __device__ __forceinline__ uint32_t forb_row(int ly, int h) {
   return (ly == 0 ? DM_N : 0u) | (ly == h - 1 ? DM_S : 0u);
+}
+
+// four successor bytes of a full block's word: codes c1 (0..8, NoData 255),
+// the byte-permute selectors nib (code - 1 per nibble) and ex4 (0x01 in the
+// bytes whose code leaves the block)
+__device__ __forceinline__ uint32_t sb_word(uint32_t c1, uint32_t nib, uint32_t ex4) {
+  const uint32_t offs = __byte_perm((uint32_t)WBT<32>::OFFB, (uint32_t)(WBT<32>::OFFB >> 32), nib);
+  const uint32_t nz = ((((c1 & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | c1) >> 7) & 0x01010101u;  // bytes != 0
+  const uint32_t nd = ((c1 >> 7) & 0x01010101u) * 0xFFu;  // NoData bytes (codes are <= 8 otherwise)
+  const uint32_t go = ((nz & ~ex4) * 0xFFu) & ~nd;         // continuing cells
+  const uint32_t stop = 0x80808080u | ((ex4 & nz) << 5) | nd;  // SB_STOP [| SB_EXIT]; NoData 255
+  return (offs & go) | (stop & ~go);
 }
 
 // ---------------------------------------------------------------- staging
@@ -524,8 +541,7 @@ __device__ __forceinline__ int build_masks(S& s, uint32_t& nsrc, int h, int w) {
         if (ly == WB::BR - 1) ex4 |= __byte_perm(0x01000000u, 0x00000101u, nib);  // SE, S, SW
         if (lx0 == 0) ex4 |= __byte_perm(0u, 0x01010100u, nib) & 0xFFu;           // SW, W, NW (cell 0)
         if (lx0 == WB::BC - 4) ex4 |= __byte_perm(0x01010100u, 0u, nib) & 0xFF000000u;  // NE, E, SE (cell 3)
-        const uint32_t nz = ((((c1 & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | c1) >> 7) & 0x01010101u;  // bytes != 0 (NoFlow stays 0)
-        sbw = c1 | ((ex4 & nz) << 5);  // NoData bytes stay 255
+        sbw = sb_word(c1, nib, ex4);
       } else {
         sbw = 0u;
         const uint32_t fr = forb_row(ly, h);
@@ -557,7 +573,7 @@ __device__ __forceinline__ int build_masks(S& s, uint32_t& nsrc, int h, int w) {
         while (mm) {
           const int kk = __ffs(mm);
           mm &= mm - 1;
-          s.sb[4 * q + j + WB::offA(kk)] |= (uint8_t)SB_DROP;
+          s.sb[4 * q + j + WB::offA(kk)] = (uint8_t)(SB_STOP | SB_DROP);
         }
       }
     }
@@ -587,8 +603,33 @@ __device__ __forceinline__ int build_masks(S& s, uint32_t& nsrc, int h, int w) {
 // queue (sources) are set and A (= w [+ x]) is in the block's rows of acc,
 // all visible to the warp.  Returns the number of cells popped (retired;
 // warp-uniform).
+// fire-and-forget reduction into global memory (explicit .global: the
+// addresses come from elt(), whose state space the compiler cannot see)
 template <class T>
-__device__ __forceinline__ void g_add(T* p, T v) { atomicAdd(p, v); }
+__device__ __forceinline__ void g_add(T* p, T v);
+template <>
+__device__ __forceinline__ void g_add<double>(double* p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v));
+}
+template <>
+__device__ __forceinline__ void g_add<uint32_t>(uint32_t* p, uint32_t v) {
+  asm volatile("red.global.add.u32 [%0], %1;" ::"l"(p), "r"(v));
+}
+template <>
+__device__ __forceinline__ void g_add<unsigned long long>(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.global.add.u64 [%0], %1;" ::"l"(p), "l"(v));
+}
+// &base[i] for a 32-bit element offset as ONE wide multiply-add (the
+// compiler otherwise splits the block's base into a uniform pointer and a
+// 64-bit offset and rebuilds the sum with 4 instructions per access)
+template <class T>
+__device__ __forceinline__ T* elt(T* base, uint32_t i) {
+  T* r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(i), "n"((int)sizeof(T)), "l"(base));
+  return r;
+}
+// element offset of block cell c = 32*ly + lx in rows of stride 32 + wm
+__device__ __forceinline__ uint32_t cell_off(uint32_t c, uint32_t wm) { return c + (c >> 5) * wm; }
 
 // Tail of Alg. 1's queue loop with chain bursts.  When few cells are ready
 // the block is working through its long in-block chains, one L2 round trip
@@ -658,10 +699,10 @@ __device__ __forceinline__ uint32_t kahn_chain_tail(WSmem<T, R, Z>& s, uint32_t 
     if (c >= 0) {
       T x[K];
       T* pk[K];
-      if (fresh) a = __ldcg(Ab + ((uint32_t)c + ((uint32_t)c >> 5) * wm));
+      if (fresh) a = __ldcg(elt(Ab, cell_off((uint32_t)c, wm)));
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        pk[k] = Ab + (cc[k] + (cc[k] >> 5) * wm);
+        pk[k] = elt(Ab, cell_off(cc[k], wm));
         if (k < n) x[k] = __ldcg(pk[k]);
       }
 #pragma unroll
@@ -679,7 +720,7 @@ __device__ __forceinline__ uint32_t kahn_chain_tail(WSmem<T, R, Z>& s, uint32_t 
         if (end_ok) {
           // "A(n) <- A(n) + A(c)", "decrement D(n)" (Alg. 1)
           t = end_t;
-          g_add(Ab + (t + (t >> 5) * wm), a);
+          g_add(elt(Ab, cell_off(t, wm)), a);
           const uint32_t sh = (t & 7u) * 4u;
           const uint32_t old = atomicAdd(&s.pend[t >> 3], 0u - (1u << sh));
           ready = ((old >> sh) & 0xFu) == 1u;
@@ -729,9 +770,9 @@ __device__ __forceinline__ uint32_t kahn_block(WSmem<T, R, Z>& s, uint32_t nsrc,
         // A(c) is final: every donor of c was popped in an earlier iteration
         t = WBT<R>::target(c, sbv);
         FA_CHECK(c < (uint32_t)WBT<R>::BN && t < (uint32_t)WBT<R>::BN);
-        T a = __ldcg(Ab + (c + (c >> 5) * wm));
+        T a = __ldcg(elt(Ab, cell_off(c, wm)));
         if constexpr (ABS) a *= (T)__ldg(Alb + (c + (c >> 5) * wm));  // "alpha(n) A(n)"
-        g_add(Ab + (t + (t >> 5) * wm), a);
+        g_add(elt(Ab, cell_off(t, wm)), a);
         const uint32_t sh = (t & 7u) * 4u;
         const uint32_t old = atomicAdd(&s.pend[t >> 3], 0u - (1u << sh));
         ready = ((old >> sh) & 0xFu) == 1u;  // the last pending donor: n joins the queue
@@ -788,9 +829,9 @@ __device__ __forceinline__ unsigned long long init_values(WSmem<T, R, Z>& s, con
         v[j] = (T)u[j];
         if (data) wsum += u[j];
       } else {
-        const float f = __uint_as_float(u[j]);
-        if (data && !weight_ok<WK>(f)) bad = true;
-        v[j] = (T)f;
+        // weight_ok on the bits (D21): finite and >= 0 is u <= 0x7F7FFFFF or -0
+        bad |= data & (u[j] > 0x7F7FFFFFu) & (u[j] != 0x80000000u);
+        v[j] = (T)__uint_as_float(u[j]);
       }
       if (code == kNoData) v[j] = AccT<T>::marker();
     }
@@ -877,7 +918,7 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
       bperim_xy(p, h, w, px, py);
       cell[j] = py * WB::BC + px;
       const bool data = s.dirh[WB::hidx(py, px)] != kNoData;
-      ex[j] = data && (s.sb[cell[j]] & SB_EXIT) != 0u;
+      ex[j] = data && sb_exit(s.sb[cell[j]]);
       if (P.cut) {  // tile records: every slot on a tile edge needs its link
         const int64_t gy = y0 + py, gx = x0 + px;
         tedge[j] = gy == t0y || gx == t0x || gy == t0y + th - 1 || gx == t0x + tw - 1;
@@ -905,7 +946,7 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
   }
   int head = 0;
   int p = -1, c = 0;
-  uint32_t sbv = 0u;  // successor byte of the walk's cell
+  uint32_t sbv = SB_STOP;  // successor byte of the walk's cell
   T f = (T)1;  // absorption: product of alpha along the walked path so far
   for (;;) {
     const unsigned idle = __ballot_sync(kFull, p < 0);
@@ -939,7 +980,7 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
     if (!sb_go(sbv)) {
       if (ABS) P.slot_f[b * WB::PB + p] = f;  // the entry's offset reaches its exit scaled by f
       uint32_t rp = kNoP;
-      if (sbv & SB_EXIT) {
+      if (sb_exit(sbv)) {
         rp = (uint32_t)bperim_index(c & 31, c >> 5, h, w);
         // tile-records mode: an exit reached from a tile-edge slot is a node too
         const uint32_t k = s.need[p] ? s.need[p] : (P.cut ? 1u : 0u);
@@ -1326,8 +1367,7 @@ __device__ __forceinline__ int build_counts_v(S& s, uint32_t& nsrc, int h, int w
       if (ly == WB::BR - 1) ex4 |= __byte_perm(0x01000000u, 0x00000101u, nib);
       if (lx0 == 0) ex4 |= __byte_perm(0u, 0x01010100u, nib) & 0xFFu;
       if (lx0 == WB::BC - 4) ex4 |= __byte_perm(0x01010100u, 0u, nib) & 0xFF000000u;
-      const uint32_t nz = ((((c1 & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | c1) >> 7) & 0x01010101u;
-      sbw = c1 | ((ex4 & nz) << 5);
+      sbw = sb_word(c1, nib, ex4);
     } else {
       sbw = 0u;
       const uint32_t fr = forb_row(ly, h);
@@ -1355,7 +1395,7 @@ __device__ __forceinline__ int build_counts_v(S& s, uint32_t& nsrc, int h, int w
         while (mm) {
           const int kk = __ffs(mm);
           mm &= mm - 1;
-          s.sb[4 * q + j + WB::offA(kk)] |= (uint8_t)SB_DROP;
+          s.sb[4 * q + j + WB::offA(kk)] = (uint8_t)(SB_STOP | SB_DROP);
         }
       }
     }
@@ -1403,7 +1443,7 @@ __device__ __forceinline__ uint32_t kahn_push(S& s, uint32_t nsrc) {
       }
     }
     head = min(head + (uint32_t)__popc(idle), nsrc);
-    const uint32_t sbv = cur >= 0 ? (uint32_t)s.sb[cur] : 0u;
+    const uint32_t sbv = cur >= 0 ? (uint32_t)s.sb[cur] : SB_STOP;
     const bool go = sb_go(sbv);
     if (!go) cur = -1;  // NoFlow, NoData target or a block exit: A(cur) is final and stored
     // one pusher per target cell and iteration: every pusher writes its lane
