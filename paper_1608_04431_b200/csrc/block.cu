@@ -56,12 +56,13 @@
 namespace fa {
 
 #ifndef FA_FIN_STEPS
-#define FA_FIN_STEPS 1
+#define FA_FIN_STEPS 4  // successor-byte walks: 1 / 4 steps per refill round -> 3.20 / 2.95 ms (cfg3)
 #endif
 #ifndef FA_FIN_PREFETCH
 // L2 prefetches per block row at the start of the finalize (0: none).  cfg3:
-// 0 / 1 / 2 / 4 / 8 -> 3.85 / 3.81 / 3.11 / 3.07 / 3.10 ms
-#define FA_FIN_PREFETCH 4
+// 0 / 1 / 2 / 4 / 8 -> 3.85 / 3.81 / 3.11 / 3.07 / 3.10 ms with the code
+// walks; with the successor-byte walks 2 / 4 -> 2.92 / 3.14 ms
+#define FA_FIN_PREFETCH 2
 #endif
 #ifndef FA_REC_STEPS
 #define FA_REC_STEPS 4
@@ -73,7 +74,7 @@ namespace fa {
 #define FA_CHAIN_K 4
 #endif
 #ifndef FA_P1_MINB
-#define FA_P1_MINB 8
+#define FA_P1_MINB 9  // CTAs of 4 warps per SM: 9 (56 registers, 36 warps) vs 8 (64, 32): cfg3 block kernel 12.06 vs 12.21 ms
 #endif
 #ifndef FA_P1_PREFETCH
 #define FA_P1_PREFETCH 1  // pass 1 L2 prefetches: 1 the block's weight rows, 2 the neighbours' entry offsets
@@ -208,6 +209,23 @@ __device__ __forceinline__ uint32_t forb_col(int lx, int w) {
 }
 __device__ __forceinline__ uint32_t forb_row(int ly, int h) {
   return (ly == 0 ? DM_N : 0u) | (ly == h - 1 ? DM_S : 0u);
+}
+
+// byte-permute selectors (code - 1 per nibble) of a word of 4 codes, and
+// 0x01 in the bytes whose code leaves a full BR x 32 block (word at row ly,
+// columns lx0..lx0+3): a per-byte lookup of the codes leaving through each side
+__device__ __forceinline__ uint32_t code_nibbles(uint32_t c1) {
+  const uint32_t sel = __vsub4(c1, 0x01010101u) & 0x07070707u;  // code - 1 per byte (no borrow)
+  return (sel & 7u) | ((sel >> 4) & 0x70u) | ((sel >> 8) & 0x700u) | ((sel >> 12) & 0x7000u);
+}
+template <int BR>
+__device__ __forceinline__ uint32_t border_exits(uint32_t nib, int ly, int lx0) {
+  uint32_t ex4 = 0;
+  if (ly == 0) ex4 |= __byte_perm(0x00000101u, 0x01000000u, nib);           // N, NE, NW
+  if (ly == BR - 1) ex4 |= __byte_perm(0x01000000u, 0x00000101u, nib);      // SE, S, SW
+  if (lx0 == 0) ex4 |= __byte_perm(0u, 0x01010100u, nib) & 0xFFu;           // SW, W, NW (cell 0)
+  if (lx0 == 32 - 4) ex4 |= __byte_perm(0x01010100u, 0u, nib) & 0xFF000000u;  // NE, E, SE (cell 3)
+  return ex4;
 }
 
 // four successor bytes of a full block's word: codes c1 (0..8, NoData 255),
@@ -534,14 +552,8 @@ __device__ __forceinline__ int build_masks(S& s, uint32_t& nsrc, int h, int w) {
         // full block: the successor bytes are the codes themselves, plus
         // SB_EXIT on the block border -- a per-byte lookup (selector = code
         // - 1) of the codes that leave the block through that side
-        const uint32_t sel = __vsub4(c1, 0x01010101u) & 0x07070707u;  // code - 1 per byte (no borrow)
-        const uint32_t nib = (sel & 7u) | ((sel >> 4) & 0x70u) | ((sel >> 8) & 0x700u) | ((sel >> 12) & 0x7000u);
-        uint32_t ex4 = 0;  // 0x01 in the bytes whose code leaves the block
-        if (ly == 0) ex4 |= __byte_perm(0x00000101u, 0x01000000u, nib);           // N, NE, NW
-        if (ly == WB::BR - 1) ex4 |= __byte_perm(0x01000000u, 0x00000101u, nib);  // SE, S, SW
-        if (lx0 == 0) ex4 |= __byte_perm(0u, 0x01010100u, nib) & 0xFFu;           // SW, W, NW (cell 0)
-        if (lx0 == WB::BC - 4) ex4 |= __byte_perm(0x01010100u, 0u, nib) & 0xFF000000u;  // NE, E, SE (cell 3)
-        sbw = sb_word(c1, nib, ex4);
+        const uint32_t nib = code_nibbles(c1);
+        sbw = sb_word(c1, nib, border_exits<WB::BR>(nib, ly, lx0));
       } else {
         sbw = 0u;
         const uint32_t fr = forb_row(ly, h);
@@ -1360,14 +1372,8 @@ __device__ __forceinline__ int build_counts_v(S& s, uint32_t& nsrc, int h, int w
     uint32_t sbw;
     if (h == WB::BR && w == WB::BC) {
       // full block: the codes plus SB_EXIT on the border (see build_masks)
-      const uint32_t sel = __vsub4(c1, 0x01010101u) & 0x07070707u;
-      const uint32_t nib = (sel & 7u) | ((sel >> 4) & 0x70u) | ((sel >> 8) & 0x700u) | ((sel >> 12) & 0x7000u);
-      uint32_t ex4 = 0;
-      if (ly == 0) ex4 |= __byte_perm(0x00000101u, 0x01000000u, nib);
-      if (ly == WB::BR - 1) ex4 |= __byte_perm(0x01000000u, 0x00000101u, nib);
-      if (lx0 == 0) ex4 |= __byte_perm(0u, 0x01010100u, nib) & 0xFFu;
-      if (lx0 == WB::BC - 4) ex4 |= __byte_perm(0x01010100u, 0u, nib) & 0xFF000000u;
-      sbw = sb_word(c1, nib, ex4);
+      const uint32_t nib = code_nibbles(c1);
+      sbw = sb_word(c1, nib, border_exits<WB::BR>(nib, ly, lx0));
     } else {
       sbw = 0u;
       const uint32_t fr = forb_row(ly, h);
@@ -1594,6 +1600,33 @@ __global__ void __launch_bounds__(32 * kNWV) k_pass2v(PassArgs<T, WK> P) {
 // NoData is dropped, D8) with fire-and-forget global atomics; a lane whose
 // walk ends takes the next entry.  A = A_B + the offsets whose path passes
 // the cell (linearity, D12).
+// codes of a staged block (row stride 32) -> successor bytes in place
+// (sb_word; the finalize's walks).  Bytes > 8 other than NoData (bad codes,
+// already rejected by pass 1) read as NoData, so a walk can never leave the
+// block's cells.
+template <int R>
+__device__ __forceinline__ void succ_bytes_inplace(uint8_t* d, int h, int w) {
+  uint32_t* D = reinterpret_cast<uint32_t*>(d);
+  for (int q = lane_id(); q < h * 8; q += 32) {
+    const int ly = q >> 3, lx0 = (q & 7) * 4;
+    const uint32_t c1 = D[q] | __vcmpgtu4(D[q], 0x08080808u);
+    uint32_t sbw;
+    if (h == R && w == 32) {
+      const uint32_t nib = code_nibbles(c1);
+      sbw = sb_word(c1, nib, border_exits<R>(nib, ly, lx0));
+    } else {
+      sbw = 0u;
+      const uint32_t fr = forb_row(ly, h);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        sbw |= (lx0 + j < w ? succ_byte((c1 >> (8 * j)) & 0xFF, fr | forb_col(lx0 + j, w)) : (uint32_t)kNoData)
+               << (8 * j);
+    }
+    D[q] = sbw;
+  }
+  __syncwarp();
+}
+
 template <class T, int R, int KB>
 struct __align__(16) FSmem {
   using WB = WBT<R>;
@@ -1658,10 +1691,15 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
         if (lx < w) s.d[k][i] = dirs[(y0s[k] + ly) * g.W + x0s[k] + lx];
       }
     }
+    __syncwarp();
+    succ_bytes_inplace<R>(s.d[k], h, w);
   }
   __syncwarp();
-  // walks
-  int head = 0, k = -1, cy = 0, cx = 0, h = 0, w = 0;
+  // walks over block cell indices c = 32*ly + lx: a step is one byte load,
+  // one reduction, one compare and one add (successor bytes, see sb_word)
+  const uint32_t wm = (uint32_t)g.W - 32u;
+  int head = 0, k = -1;
+  uint32_t c = 0;
   T x = (T)0;
   T* rowp = nullptr;  // acc + y0 * W + x0 of the walk's block
   const float* arow = nullptr;  // absorption: alpha + y0 * W + x0
@@ -1677,7 +1715,7 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
         int kk = 0;
 #pragma unroll
         for (int j = 1; j < KB; ++j) kk = k == j ? j : kk;
-        h = hs[0]; w = ws[0];
+        int h = hs[0], w = ws[0];
         int64_t yy = y0s[0], xx = x0s[0];
 #pragma unroll
         for (int j = 1; j < KB; ++j)
@@ -1685,7 +1723,9 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
         x = x_slot[(b0 + k) * WB::PB + p];
         rowp = acc + yy * g.W + xx;
         if (ABS) arow = alpha + yy * g.W + xx;
+        int cx, cy;
         bperim_xy(p, h, w, cx, cy);
+        c = (uint32_t)(cy * WB::BC + cx);
       }
     }
     head += __popc(idle);
@@ -1694,22 +1734,15 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
     // paid once per round)
 #pragma unroll
     for (int u = 0; u < FA_FIN_STEPS; ++u) {
-      FA_CHECK((unsigned)cy < (unsigned)h && (unsigned)cx < (unsigned)w);
-      atomic_add(rowp + (int64_t)cy * g.W + cx, x);
-      const int d = s.d[k][cy * WB::BC + cx];
-      const int ty = cy + dir_dy(d), tx = cx + dir_dx(d);
-      bool stop = d == kNoFlow || d > 8 || (unsigned)ty >= (unsigned)h || (unsigned)tx >= (unsigned)w;
-      // Flow into NoData is dropped (D8).  For f64 the walk may step onto the
-      // NoData cell instead of checking it: NaN + x = NaN, and its code (255)
-      // ends the walk there; integer markers would change, so they check.
-      if (!std::is_same<T, double>::value) stop = stop || s.d[k][ty * WB::BC + tx] == kNoData;
-      if (stop) {
-        k = -1;  // terminal, block exit, or dropped into NoData
-        break;
-      }
-      if (ABS) x *= (T)__ldg(arow + (int64_t)cy * g.W + cx);  // the cell passes on alpha of it
-      cy = ty;
-      cx = tx;
+      FA_CHECK(c < (uint32_t)WB::BN);
+      const uint32_t sb = s.d[k][c];
+      // a walk that reaches in-block NoData stops there: the flow is dropped (D8)
+      if (sb == kNoData) { k = -1; break; }
+      const uint32_t off = cell_off(c, wm);
+      g_add(elt(rowp, off), x);
+      if (!sb_go(sb)) { k = -1; break; }  // terminal or block exit
+      if (ABS) x *= (T)__ldg(arow + off);  // the cell passes on alpha of it
+      c = WB::target(c, sb);
     }
   }
 }

@@ -61,15 +61,19 @@ __device__ __forceinline__ void cta_append(bool pred, uint32_t v, uint32_t* list
 }
 
 // frontier = {v : cnt[v] == 0}; done[v] = 0.  All threads iterate uniformly.
+// one[v]: v has exactly one child (k_walk's fast path).
 __global__ void __launch_bounds__(256) k_init_frontier(uint32_t n, const uint32_t* __restrict__ cnt, uint8_t* done,
-                                                       uint32_t* front, uint32_t* fcount) {
+                                                       uint8_t* one, uint32_t* front, uint32_t* fcount) {
   __shared__ uint32_t s_tmp[256 / 32 + 1];
   const uint32_t stride = gridDim.x * blockDim.x;
   for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += stride) {
     const uint32_t v = base + threadIdx.x;
-    const bool ok = v < n && cnt[v] == 0;
-    if (v < n) done[v] = 0;
-    cta_append<256>(ok, v, front, fcount, s_tmp);
+    const uint32_t c = v < n ? cnt[v] : 1u;
+    if (v < n) {
+      done[v] = 0;
+      one[v] = c == 1u;
+    }
+    cta_append<256>(c == 0u, v, front, fcount, s_tmp);
   }
 }
 
@@ -113,8 +117,9 @@ __global__ void k_peel_dev(const uint32_t* __restrict__ front, const uint32_t* _
 // steps and re-queues the ready node, leaving deep chains to contraction.
 template <class T, bool WG = false>
 __global__ void k_walk(const uint32_t* __restrict__ front, const uint32_t* __restrict__ nf_dev,
-                       const uint32_t* __restrict__ parent, T* val, uint32_t* cnt, uint8_t* done, uint32_t* next,
-                       uint32_t* ncount, uint32_t* nretired, int cap, const T* __restrict__ wv) {
+                       const uint32_t* __restrict__ parent, T* val, uint32_t* cnt, uint8_t* done,
+                       const uint8_t* __restrict__ one, uint32_t* next, uint32_t* ncount, uint32_t* nretired, int cap,
+                       const T* __restrict__ wv) {
   const uint32_t nf = *nf_dev;  // frontier size read on the device: no host round trip before the launch
   const uint32_t stride = gridDim.x * blockDim.x;
   uint32_t retired = 0;
@@ -125,23 +130,42 @@ __global__ void k_walk(const uint32_t* __restrict__ front, const uint32_t* __res
     if (i < nf) {
       uint32_t v = front[i];
       T s = __ldcg(&val[v]);
+      uint32_t p = parent[v];
       for (int steps = 0;; ++steps) {
         done[v] = 1;
         ++retired;
-        const uint32_t p = parent[v];
         if (p == kNone) break;
-        atomic_add(&val[p], WG ? wv[v] * s : s);
-        // acq_rel decrement: our contribution is released before it, and the
-        // last arrival acquires every other child's contribution
-        cuda::atomic_ref<uint32_t, cuda::thread_scope_device> cp(cnt[p]);
-        if (cp.fetch_sub(1u, cuda::memory_order_acq_rel) != 1u) break;
-        if (steps + 1 >= cap) {
-          push = true;
-          pnode = p;
-          break;
+        // p's flag, value and parent in one round of loads: with a single
+        // child (v) p is final once v's sum is added -- no atomics, one L2
+        // round trip per step along chains
+        const bool single = one[p] != 0;
+        const T vp = __ldcg(&val[p]);
+        const uint32_t pp = parent[p];
+        const T add = WG ? wv[v] * s : s;
+        if (single) {
+          s = vp + add;
+          val[p] = s;
+          if (steps + 1 >= cap) {
+            cnt[p] = 0u;  // ready: no pending child
+            push = true;
+            pnode = p;
+            break;
+          }
+        } else {
+          atomic_add(&val[p], add);
+          // acq_rel decrement: our contribution is released before it, and the
+          // last arrival acquires every other child's contribution
+          cuda::atomic_ref<uint32_t, cuda::thread_scope_device> cp(cnt[p]);
+          if (cp.fetch_sub(1u, cuda::memory_order_acq_rel) != 1u) break;
+          if (steps + 1 >= cap) {
+            push = true;
+            pnode = p;
+            break;
+          }
+          s = __ldcg(&val[p]);
         }
-        s = __ldcg(&val[p]);
         v = p;
+        p = pp;
       }
     }
     warp_append(push, pnode, next, ncount);
@@ -322,6 +346,7 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
   cudaStream_t st = rt.st;
   uint32_t* cnt = rt.alloc<uint32_t>(n);
   uint8_t* done = rt.alloc<uint8_t>(n);
+  uint8_t* one = rt.alloc<uint8_t>(n);
   uint32_t* fa_ = rt.alloc<uint32_t>(n);
   uint32_t* fb = rt.alloc<uint32_t>(n);
   uint32_t* ctr = rt.alloc<uint32_t>(4);
@@ -330,7 +355,7 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
   cudaMemsetAsync(ctr, 0, 4 * sizeof(uint32_t), st);
   k_count_children<<<grid_for(n), 256, 0, st>>>(n, parent, cnt);
   ++rt.launches;
-  k_init_frontier<<<grid_for(n), 256, 0, st>>>(n, cnt, done, fa_, ctr);
+  k_init_frontier<<<grid_for(n), 256, 0, st>>>(n, cnt, done, one, fa_, ctr);
   ++rt.launches;
   uint32_t nf = 1;  // the frontier size stays on the device until after the walks
   uint64_t remaining = n;
@@ -344,7 +369,7 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
     // bulk of the forest: one launch of capped walks from every leaf (a
     // grid for all n nodes; the walks read the frontier size themselves)
     cudaMemsetAsync(ctr + 1, 0, 2 * sizeof(uint32_t), st);
-    k_walk<T, WG><<<grid_for(n), 256, 0, st>>>(fa_, ctr, parent, val, cnt, done, fb, ctr + 1, ctr + 2, cap, wv);
+    k_walk<T, WG><<<grid_for(n), 256, 0, st>>>(fa_, ctr, parent, val, cnt, done, one, fb, ctr + 1, ctr + 2, cap, wv);
     ++rt.launches;
     ++rt.peel_rounds;
     std::swap(fa_, fb);
@@ -463,6 +488,7 @@ cudaError_t solve_level(Runtime& rt, uint32_t n, const uint32_t* parent, T* val,
   if (!contracted && remaining != 0) k_set_flag<<<1, 1, 0, st>>>(rt.d_status, ST_CYCLE);
   rt.free(cnt);
   rt.free(done);
+  rt.free(one);
   rt.free(fa_);
   rt.free(fb);
   rt.free(ctr);

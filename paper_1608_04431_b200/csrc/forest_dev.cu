@@ -34,12 +34,18 @@ namespace cg = cooperative_groups;
 namespace fa {
 namespace {
 
+#ifndef FA_FOREST_PER_SM
+#define FA_FOREST_PER_SM 0  // cooperative CTAs per SM (0: as many as fit)
+#endif
 #ifndef FA_FOREST_MINB
 #define FA_FOREST_MINB 8  // CTAs of 256 per SM: 2048 resident threads (the walks are latency-bound)
 #endif
 constexpr int kDevMaxLevels = 32;
 constexpr int kDevMaxJump = 40;
 constexpr uint64_t kDevContractRatio = 8;
+// leaves this few relative to the nodes: a chain-dominated forest (cfg2's
+// serpentine), contracted at once instead of walked leaf by leaf
+constexpr uint64_t kDevLeafRatio = 64;
 
 template <class T>
 struct DevLevel {
@@ -61,6 +67,7 @@ struct DevArgs {
   const T* wv0;
   uint32_t* cnt;      // n0: pending children
   uint8_t* done;      // n0
+  uint8_t* one;       // n0: the node has exactly one child (walk fast path)
   uint32_t* fa;       // n0: frontier lists
   uint32_t* fb;
   uint32_t* rid;      // n0: node -> residual index
@@ -149,8 +156,9 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
     }
     sync_all();
     for (uint32_t t = 0, v = tid; t < trips(n); ++t, v += nth) {
-      const bool leaf = v < n && ld(&A.cnt[v]) == 0u;
-      append(leaf, v, A.fa, &C[C_F + 0]);
+      const uint32_t c = v < n ? ld(&A.cnt[v]) : 1u;
+      if (v < n) A.one[v] = c == 1u;
+      append(c == 0u, v, A.fa, &C[C_F + 0]);
     }
     sync_all();
     // rounds of capped walks ("the last arrival continues"); round r reads
@@ -163,7 +171,7 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
     unsigned long long remaining = n;
     bool contract = false;
     while (nf > 0) {
-      if (r > 0 && (unsigned long long)nf * kDevContractRatio < remaining) {
+      if ((unsigned long long)nf * (r > 0 ? kDevContractRatio : kDevLeafRatio) < remaining) {
         contract = true;
         break;
       }
@@ -174,21 +182,40 @@ __global__ void __launch_bounds__(256, FA_FOREST_MINB) k_forest_dev(DevArgs<T, W
         if (i < nf) {
           uint32_t v = cur[i];
           T s = __ldcg(&val[v]);
+          uint32_t p = parent[v];
           for (int steps = 0;; ++steps) {
             A.done[v] = 1u;
             ++ret;
-            const uint32_t p = parent[v];
             if (p == kNone) break;
-            atomic_add(&val[p], WG ? wv[v] * s : s);
-            cuda::atomic_ref<uint32_t, cuda::thread_scope_device> cp(A.cnt[p]);
-            if (cp.fetch_sub(1u, cuda::memory_order_acq_rel) != 1u) break;
-            if (steps + 1 >= A.cap) {
-              push = true;
-              pnode = p;
-              break;
+            // p's data is loaded in one round: with a single child (v) its
+            // value is final once v's is added -- no atomics, one L2 round
+            // trip per step along chains
+            const bool one = __ldcg(&A.one[p]) != 0;
+            const T vp = __ldcg(&val[p]);
+            const uint32_t pp = parent[p];
+            const T add = WG ? wv[v] * s : s;
+            if (one) {
+              s = vp + add;
+              val[p] = s;
+              if (steps + 1 >= A.cap) {
+                A.cnt[p] = 0u;  // ready: no pending child
+                push = true;
+                pnode = p;
+                break;
+              }
+            } else {
+              atomic_add(&val[p], add);
+              cuda::atomic_ref<uint32_t, cuda::thread_scope_device> cp(A.cnt[p]);
+              if (cp.fetch_sub(1u, cuda::memory_order_acq_rel) != 1u) break;
+              if (steps + 1 >= A.cap) {
+                push = true;
+                pnode = p;
+                break;
+              }
+              s = __ldcg(&val[p]);
             }
-            s = __ldcg(&val[p]);
             v = p;
+            p = pp;
           }
         }
         append(push, pnode, nxt, &C[C_F + (r + 1) % 3]);
@@ -464,6 +491,7 @@ cudaError_t solve_dev(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, c
   a.wv0 = wv;
   a.cnt = rt.alloc<uint32_t>(n);
   a.done = rt.alloc<uint8_t>(n);
+  a.one = rt.alloc<uint8_t>(n);
   a.fa = rt.alloc<uint32_t>(n);
   a.fb = rt.alloc<uint32_t>(n);
   a.rid = rt.alloc<uint32_t>(n);
@@ -484,7 +512,7 @@ cudaError_t solve_dev(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, c
   ++rt.launches;
   if (e != cudaSuccess) {
     cudaGetLastError();
-    for (void* p : {(void*)a.cnt, (void*)a.done, (void*)a.fa, (void*)a.fb, (void*)a.rid, (void*)a.ctr,
+    for (void* p : {(void*)a.cnt, (void*)a.done, (void*)a.one, (void*)a.fa, (void*)a.fb, (void*)a.rid, (void*)a.ctr,
                     (void*)a.pool, (void*)a.lv})
       rt.free(p);
     return cudaSuccess;  // not done: forest.cu solves it
@@ -493,7 +521,7 @@ cudaError_t solve_dev(Runtime& rt, uint32_t n, const uint32_t* parent, T* val, c
   // copy, after the solve; never set in practice)
   e = cudaMemcpyAsync(rt.h_cnt + 12, a.ctr + C_OVF, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  for (void* p : {(void*)a.cnt, (void*)a.done, (void*)a.fa, (void*)a.fb, (void*)a.rid, (void*)a.ctr,
+  for (void* p : {(void*)a.cnt, (void*)a.done, (void*)a.one, (void*)a.fa, (void*)a.fb, (void*)a.rid, (void*)a.ctr,
                   (void*)a.pool, (void*)a.lv})
     rt.free(p);
   if (e != cudaSuccess) return e;
@@ -531,6 +559,7 @@ cudaError_t solve_dev_async(Runtime& rt, uint32_t n_max, const uint32_t* n_dev, 
   a.val0 = val;
   a.cnt = rt.alloc<uint32_t>(n_max);
   a.done = rt.alloc<uint8_t>(n_max);
+  a.one = rt.alloc<uint8_t>(n_max);
   a.fa = rt.alloc<uint32_t>(n_max);
   a.fb = rt.alloc<uint32_t>(n_max);
   a.rid = rt.alloc<uint32_t>(n_max);
@@ -545,11 +574,12 @@ cudaError_t solve_dev_async(Runtime& rt, uint32_t n_max, const uint32_t* n_dev, 
   cudaMemsetAsync(a.ctr, 0, 64 * sizeof(uint32_t), st);
   // a small graph gets a small grid: its barriers are cheaper (one CTA per
   // 256 nodes; a single CTA synchronises with its own barrier)
+  if (FA_FOREST_PER_SM > 0 && per_sm > FA_FOREST_PER_SM) per_sm = FA_FOREST_PER_SM;
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * per_sm, ((int64_t)n_max + 255) / 256));
   void* args[] = {&a};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, grid, 256, args, 0, st);
   ++rt.launches;
-  for (void* p : {(void*)a.cnt, (void*)a.done, (void*)a.fa, (void*)a.fb, (void*)a.rid, (void*)a.ctr, (void*)a.pool,
+  for (void* p : {(void*)a.cnt, (void*)a.done, (void*)a.one, (void*)a.fa, (void*)a.fb, (void*)a.rid, (void*)a.ctr, (void*)a.pool,
                   (void*)a.lv})
     rt.free(p);
   return e;
