@@ -814,50 +814,64 @@ __device__ __forceinline__ unsigned long long init_values(WSmem<T, R, Z>& s, con
   const bool vec = w == WB::BC && ((x0 & 3) == 0) && ((g.W & 3) == 0) &&
                    (WK == 0 || (reinterpret_cast<uintptr_t>(wp) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-  const uint32_t* W32 = static_cast<const uint32_t*>(wp);
+  // the block's first cell in w and out; cell offsets ly * W + lx in 32 bits
+  // (as in the queue loop), one wide multiply-add per access
+  const uint32_t* Wb = static_cast<const uint32_t*>(wp) + (WK != 0 ? y0 * g.W + x0 : 0);
+  T* ob = out + y0 * g.W + x0;
+  const uint32_t WW = (uint32_t)g.W;
   for (int q = lane; q < h * (WB::BC / 4); q += 32) {
     const int ly = q >> 3, lx = (q & 7) * 4;
     const uint32_t dw = *reinterpret_cast<const uint32_t*>(&s.dirh[WB::hidx(ly, lx)]);
-    const int64_t gi = (y0 + ly) * g.W + x0 + lx;
+    const uint32_t off = (uint32_t)ly * WW + (uint32_t)lx;
+    // NoData (255) or cells right of a ragged block (255): the rare path
+    const bool anynd = (dw & 0x80808080u) != 0u;
     uint32_t u[4] = {1u, 1u, 1u, 1u};
     if (WK != 0) {
       if (vec) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(W32 + gi));
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(elt(Wb, off)));
         u[0] = v.x; u[1] = v.y; u[2] = v.z; u[3] = v.w;
       } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (lx + j < w) u[j] = __ldg(W32 + gi + j);
+          if (lx + j < w) u[j] = __ldg(elt(Wb, off + j));
       }
     }
     alignas(16) T v[4];
+    uint32_t badw = 0;  // f32 weights failing weight_ok, data or not (checked below)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int code = (dw >> (8 * j)) & 0xFF;
-      const bool data = code < kOut;  // excludes NoData and cells outside
       if constexpr (WK == 0) {
         v[j] = (T)1;
       } else if constexpr (WK == 1) {
         v[j] = (T)u[j];
-        if (data) wsum += u[j];
+        if (((dw >> (8 * j)) & 0xFF) < kOut) wsum += u[j];
       } else {
         // weight_ok on the bits (D21): finite and >= 0 is u <= 0x7F7FFFFF or -0
-        bad |= data & (u[j] > 0x7F7FFFFFu) & (u[j] != 0x80000000u);
+        badw |= (uint32_t)((u[j] > 0x7F7FFFFFu) & (u[j] != 0x80000000u)) << j;
         v[j] = (T)__uint_as_float(u[j]);
       }
-      if (code == kNoData) v[j] = AccT<T>::marker();
     }
+    if (anynd) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (((dw >> (8 * j)) & 0xFF) == kNoData) {
+          v[j] = AccT<T>::marker();
+          badw &= ~(1u << j);  // NoData weights are ignored
+        }
+    }
+    if (badw) bad = true;
     if (vec) {
       if constexpr (sizeof(T) == 4) {
-        *reinterpret_cast<uint4*>(out + gi) = *reinterpret_cast<const uint4*>(v);
+        *reinterpret_cast<uint4*>(elt(ob, off)) = *reinterpret_cast<const uint4*>(v);
       } else {
-        reinterpret_cast<uint4*>(out + gi)[0] = *reinterpret_cast<const uint4*>(&v[0]);
-        reinterpret_cast<uint4*>(out + gi)[1] = *reinterpret_cast<const uint4*>(&v[2]);
+        uint4* o = reinterpret_cast<uint4*>(elt(ob, off));
+        o[0] = *reinterpret_cast<const uint4*>(&v[0]);
+        o[1] = *reinterpret_cast<const uint4*>(&v[2]);
       }
     } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (lx + j < w) out[gi + j] = v[j];
+        if (lx + j < w) *elt(ob, off + j) = v[j];
     }
   }
   if (bad) atomicOr(status, ST_BADWEIGHT);
