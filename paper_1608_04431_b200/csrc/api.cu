@@ -218,9 +218,28 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
   fa_status r = solve_g2<T>(ctx, gg, nslots, hbase, links, fdir, tile_acc, xT, tile_f);
   if (r != FA_OK) { cleanup(); return r; }
   CK(cudaEventRecord(ctx->ev[2], st));
-  for (auto& s : strips) {
-    r = strip_finish<T, WK>(ctx, s, xT);
+  bool joint = false;
+  if (!alpha && G > 1) {
+    // the strips' graphs as one forest: inject every strip, one solve, finish
+    for (auto& s : strips) {
+      r = strip_finish<T, WK>(ctx, s, xT, FIN_PRE);
+      if (r != FA_OK) { cleanup(); return r; }
+    }
+    r = solve_strips<T>(ctx, strips, joint);
     if (r != FA_OK) { cleanup(); return r; }
+    if (!joint)
+      for (auto& s : strips) {
+        CK(forest_solve<T>(rt, s.nn, s.parent, s.S));
+      }
+    for (auto& s : strips) {
+      r = strip_finish<T, WK>(ctx, s, xT, FIN_POST);
+      if (r != FA_OK) { cleanup(); return r; }
+    }
+  } else {
+    for (auto& s : strips) {
+      r = strip_finish<T, WK>(ctx, s, xT);
+      if (r != FA_OK) { cleanup(); return r; }
+    }
   }
   CK(cudaEventRecord(ctx->ev[3], st));
   if (rec.want) {

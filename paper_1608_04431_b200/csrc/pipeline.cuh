@@ -531,11 +531,25 @@ fa_status solve_g2(fa_ctx* ctx, const Geom& gg, int64_t nslots, const std::vecto
 }
 
 // phase B tail: inject x_T, solve the tile-cut graph, scatter, pass 2
+// parts of strip_finish: everything, or the steps before / after the
+// tile-cut graph solve (strips solved together as one forest: solve_strips)
+enum : int { FIN_ALL = 0, FIN_PRE = 1, FIN_POST = 2 };
+
 template <class T, int WK>
-fa_status strip_finish(fa_ctx* ctx, Strip<T>& s, const T* xT_global) {
+fa_status strip_finish(fa_ctx* ctx, Strip<T>& s, const T* xT_global, int part = FIN_ALL) {
   using namespace fa;
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
+  if (part == FIN_POST) {
+    CK(launch_scatter_x<T>(st, s.nn, s.node_tgt, s.node_flags, s.S, s.x_slot, true));
+    ++rt.launches;
+    if (s.acc) {
+      if (ctx->retain()) CK(launch_retain<T>(s.g, s.x_slot, s.dirs_in(), s.acc, st));
+      else CK(launch_pass2<T, WK>(pass_args<T, WK>(ctx, s), st));
+      ++rt.launches;
+    }
+    return FA_OK;
+  }
   if (!s.own_in_S) CK(cudaMemcpyAsync(s.S, s.node_val, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
   if constexpr (std::is_same<T, double>::value) {
     if (s.alpha) {
@@ -570,6 +584,7 @@ fa_status strip_finish(fa_ctx* ctx, Strip<T>& s, const T* xT_global) {
   }
   CK(launch_inject_slots<T>(st, s.g, s.nslots, s.dtbase, xT_global + s.slot0, s.slot_root, s.S, s.x_slot));
   ++rt.launches;
+  if (part == FIN_PRE) return FA_OK;
   CK(forest_solve<T>(rt, s.nn, s.parent, s.S));  // true A at every block exit
   CK(launch_scatter_x<T>(st, s.nn, s.node_tgt, s.node_flags, s.S, s.x_slot, true));
   ++rt.launches;
@@ -578,6 +593,51 @@ fa_status strip_finish(fa_ctx* ctx, Strip<T>& s, const T* xT_global) {
     else CK(launch_pass2<T, WK>(pass_args<T, WK>(ctx, s), st));
     ++rt.launches;
   }
+  return FA_OK;
+}
+
+static __global__ void k_offset_parents(uint32_t n, const uint32_t* __restrict__ par, uint32_t off,
+                                        uint32_t* __restrict__ out) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const uint32_t p = par[v];
+    out[v] = p == fa::kNone ? fa::kNone : p + off;
+  }
+}
+
+// phase B on one device: the strips' tile-cut graphs are disjoint forests, so
+// they are solved as ONE forest (node ids offset by strip) -- one solve and
+// its handful of host reads instead of one per strip.  Returns false (nothing
+// done) when the joint node count would not fit 32-bit ids.
+template <class T>
+fa_status solve_strips(fa_ctx* ctx, std::vector<Strip<T>>& strips, bool& done) {
+  using namespace fa;
+  cudaStream_t st = ctx->st;
+  Runtime& rt = ctx->rt;
+  done = false;
+  uint64_t n = 0;
+  for (auto& s : strips) n += s.nn;
+  if (n == 0 || n >= (uint64_t)kNone) return FA_OK;
+  uint32_t* par = rt.alloc<uint32_t>(n);
+  T* val = rt.alloc<T>(n);
+  if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+  uint32_t off = 0;
+  for (auto& s : strips) {
+    if (s.nn) {
+      k_offset_parents<<<grid_for(s.nn), 256, 0, st>>>(s.nn, s.parent, off, par + off);
+      ++rt.launches;
+      CK(cudaMemcpyAsync(val + off, s.S, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    }
+    off += s.nn;
+  }
+  CK(forest_solve<T>(rt, (uint32_t)n, par, val));  // true A at every block exit of every strip
+  off = 0;
+  for (auto& s : strips) {
+    if (s.nn) CK(cudaMemcpyAsync(s.S, val + off, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    off += s.nn;
+  }
+  rt.free(val);
+  rt.free(par);
+  done = true;
   return FA_OK;
 }
 
