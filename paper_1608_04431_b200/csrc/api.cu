@@ -172,9 +172,11 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
   const int G = nstrips < 1 ? 1 : (int)(nstrips > gg.TR ? gg.TR : nstrips);
   std::vector<Strip<T>> strips(G);
   int64_t blocks = 0, nodes = 0;
+  const bool joint_ok = !alpha && G > 1;
+  uint32_t* par_all = nullptr;  // the strips' parents as one forest (joint_parents)
   auto cleanup = [&]() {
     for (auto& s : strips) s.release(rt);
-    for (void* p : {(void*)links, (void*)fdir, (void*)tile_acc, (void*)xT, (void*)tile_f}) rt.free(p);
+    for (void* p : {(void*)links, (void*)fdir, (void*)tile_acc, (void*)xT, (void*)tile_f, (void*)par_all}) rt.free(p);
   };
   for (int i = 0; i < G; ++i) {
     // strip i: tile rows [i*TR/G, (i+1)*TR/G)
@@ -202,10 +204,28 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
     fa_status r = strip_pass1<T, WK>(ctx, s, true);
     if (r != FA_OK) { cleanup(); return r; }
     r = strip_records<T>(ctx, s, links + s.slot0, fdir + s.slot0, tile_acc + s.slot0,
-                         tile_f ? tile_f + s.slot0 : nullptr);
+                         tile_f ? tile_f + s.slot0 : nullptr, joint_ok ? REC_PRE : REC_ALL);
     if (r != FA_OK) { cleanup(); return r; }
     blocks += s.g.nblocks;
     nodes += s.nn;
+  }
+  // several strips on one device: their graphs as ONE forest (tile roots in
+  // phase A, the solve in phase B), so the per-solve launches and host reads
+  // are paid once, not once per strip
+  uint32_t n_all = 0;
+  if (joint_ok) {
+    par_all = joint_parents<T>(ctx, strips, &n_all);
+    if (rt.err) { cleanup(); return set_err(ctx, FA_E_NOMEM, "device allocation failed"); }
+    if (par_all) {
+      fa_status r = roots_strips<T>(ctx, strips, par_all, n_all);
+      if (r != FA_OK) { cleanup(); return r; }
+    } else {
+      for (auto& s : strips) CK(forest_roots(rt, s.nn, s.parent, s.troot));
+    }
+    for (auto& s : strips) {
+      fa_status r = strip_records<T>(ctx, s, links + s.slot0, fdir + s.slot0, tile_acc + s.slot0, nullptr, REC_POST);
+      if (r != FA_OK) { cleanup(); return r; }
+    }
   }
   CK(cudaEventRecord(ctx->ev[1], st));
   CK(rt.read(ctx->d_small + 1, 3));
@@ -218,19 +238,18 @@ fa_status run_acc(fa_ctx* ctx, int64_t H, int64_t W, const float* dem, float nod
   fa_status r = solve_g2<T>(ctx, gg, nslots, hbase, links, fdir, tile_acc, xT, tile_f);
   if (r != FA_OK) { cleanup(); return r; }
   CK(cudaEventRecord(ctx->ev[2], st));
-  bool joint = false;
-  if (!alpha && G > 1) {
+  if (joint_ok) {
     // the strips' graphs as one forest: inject every strip, one solve, finish
     for (auto& s : strips) {
       r = strip_finish<T, WK>(ctx, s, xT, FIN_PRE);
       if (r != FA_OK) { cleanup(); return r; }
     }
-    r = solve_strips<T>(ctx, strips, joint);
-    if (r != FA_OK) { cleanup(); return r; }
-    if (!joint)
-      for (auto& s : strips) {
-        CK(forest_solve<T>(rt, s.nn, s.parent, s.S));
-      }
+    if (par_all) {
+      r = solve_strips<T>(ctx, strips, par_all, n_all);
+      if (r != FA_OK) { cleanup(); return r; }
+    } else {
+      for (auto& s : strips) CK(forest_solve<T>(rt, s.nn, s.parent, s.S));
+    }
     for (auto& s : strips) {
       r = strip_finish<T, WK>(ctx, s, xT, FIN_POST);
       if (r != FA_OK) { cleanup(); return r; }

@@ -440,12 +440,17 @@ static __global__ void k_tile_bases(fa::Geom g, int64_t* base) {
 
 // phase A tail: A_T at block exits, tile roots, tile perimeter records; the
 // output pointers are the strip's own first slot (its nslots records follow)
+// parts of strip_records: everything, or the steps before / after the tile
+// roots (strips rooted together as one forest: roots_strips)
+enum : int { REC_ALL = 0, REC_PRE = 1, REC_POST = 2 };
+
 template <class T>
 fa_status strip_records(fa_ctx* ctx, Strip<T>& s, uint32_t* links, uint8_t* fdir, T* tile_acc,
-                        T* tile_f = nullptr) {
+                        T* tile_f = nullptr, int part = REC_ALL) {
   using namespace fa;
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
+  if (part == REC_POST) goto post;
   s.troot = rt.alloc<uint32_t>(s.nn);
   s.nslots = tile_perim_total(s.g, nullptr);
   s.dtbase = rt.alloc<int64_t>((size_t)(s.g.TR * s.g.TC + 1));
@@ -478,19 +483,23 @@ fa_status strip_records(fa_ctx* ctx, Strip<T>& s, uint32_t* links, uint8_t* fdir
   }
   CK(launch_fold_leaves<T>(st, s.g.nblocks * s.g.pb, s.x_slot, s.slot_root, s.S));  // leaves raked in pass 1
   ++rt.launches;
+  if (part == REC_PRE) return FA_OK;
   // A_T is needed at the tile exits only (the roots of the tile-cut forest):
   // root ids by pointer jumping, then one reduction of the own values by
   // root -- no forest solve here; phase B (strip_finish) solves the strip
   // graph once, with the injected offsets
   CK(forest_roots(rt, s.nn, s.parent, s.troot));
-  T* R = rt.alloc<T>(s.nn);
-  if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
-  CK(cudaMemsetAsync(R, 0, (s.nn ? s.nn : 1) * sizeof(T), st));
-  CK(launch_root_sum<T>(st, s.nn, s.troot, s.S, nullptr, R));
-  CK(launch_tile_records<T>(st, s.g, s.nslots, s.dtbase, s.dirs_in(), s.slot_root, s.troot, s.node_flags,
-                            s.node_slot, R, links, fdir, tile_acc));
-  rt.launches += 2;
-  rt.free(R);
+post:
+  {
+    T* R = rt.alloc<T>(s.nn);
+    if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+    CK(cudaMemsetAsync(R, 0, (s.nn ? s.nn : 1) * sizeof(T), st));
+    CK(launch_root_sum<T>(st, s.nn, s.troot, s.S, nullptr, R));
+    CK(launch_tile_records<T>(st, s.g, s.nslots, s.dtbase, s.dirs_in(), s.slot_root, s.troot, s.node_flags,
+                              s.node_slot, R, links, fdir, tile_acc));
+    rt.launches += 2;
+    rt.free(R);
+  }
   s.own_in_S = true;
   return FA_OK;
 }
@@ -608,36 +617,78 @@ static __global__ void k_offset_parents(uint32_t n, const uint32_t* __restrict__
 // they are solved as ONE forest (node ids offset by strip) -- one solve and
 // its handful of host reads instead of one per strip.  Returns false (nothing
 // done) when the joint node count would not fit 32-bit ids.
+static __global__ void k_unoffset(uint32_t n, const uint32_t* __restrict__ in, uint32_t off, uint32_t* __restrict__ out) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) out[v] = in[v] - off;
+}
+
+// the strips' tile-cut graphs are disjoint forests: their parents with node
+// ids offset by strip form ONE forest (nullptr when the joint node count does
+// not fit 32-bit ids); *n_out = its node count
 template <class T>
-fa_status solve_strips(fa_ctx* ctx, std::vector<Strip<T>>& strips, bool& done) {
+uint32_t* joint_parents(fa_ctx* ctx, std::vector<Strip<T>>& strips, uint32_t* n_out) {
+  using namespace fa;
+  Runtime& rt = ctx->rt;
+  uint64_t n = 0;
+  for (auto& s : strips) n += s.nn;
+  *n_out = 0;
+  if (n == 0 || n >= (uint64_t)kNone) return nullptr;
+  uint32_t* par = rt.alloc<uint32_t>(n);
+  if (rt.err) return nullptr;
+  uint32_t off = 0;
+  for (auto& s : strips) {
+    if (s.nn) {
+      k_offset_parents<<<grid_for(s.nn), 256, 0, ctx->st>>>(s.nn, s.parent, off, par + off);
+      ++rt.launches;
+    }
+    off += s.nn;
+  }
+  *n_out = (uint32_t)n;
+  return par;
+}
+
+// phase A on one device: the tile roots of every strip by ONE pointer-jumping
+// solve over the joint forest (roots of strip i lie in strip i: ids minus its offset)
+template <class T>
+fa_status roots_strips(fa_ctx* ctx, std::vector<Strip<T>>& strips, const uint32_t* par, uint32_t n) {
   using namespace fa;
   cudaStream_t st = ctx->st;
   Runtime& rt = ctx->rt;
-  done = false;
-  uint64_t n = 0;
-  for (auto& s : strips) n += s.nn;
-  if (n == 0 || n >= (uint64_t)kNone) return FA_OK;
-  uint32_t* par = rt.alloc<uint32_t>(n);
+  uint32_t* root = rt.alloc<uint32_t>(n);
+  if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
+  CK(forest_roots(rt, n, par, root));
+  uint32_t off = 0;
+  for (auto& s : strips) {
+    if (s.nn) {
+      k_unoffset<<<grid_for(s.nn), 256, 0, st>>>(s.nn, root + off, off, s.troot);
+      ++rt.launches;
+    }
+    off += s.nn;
+  }
+  rt.free(root);
+  return FA_OK;
+}
+
+// phase B on one device: the strips' tile-cut graphs solved as ONE forest --
+// one solve and its handful of host reads instead of one per strip
+template <class T>
+fa_status solve_strips(fa_ctx* ctx, std::vector<Strip<T>>& strips, const uint32_t* par, uint32_t n) {
+  using namespace fa;
+  cudaStream_t st = ctx->st;
+  Runtime& rt = ctx->rt;
   T* val = rt.alloc<T>(n);
   if (rt.err) return set_err(ctx, FA_E_NOMEM, "device allocation failed");
   uint32_t off = 0;
   for (auto& s : strips) {
-    if (s.nn) {
-      k_offset_parents<<<grid_for(s.nn), 256, 0, st>>>(s.nn, s.parent, off, par + off);
-      ++rt.launches;
-      CK(cudaMemcpyAsync(val + off, s.S, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
-    }
+    if (s.nn) CK(cudaMemcpyAsync(val + off, s.S, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
     off += s.nn;
   }
-  CK(forest_solve<T>(rt, (uint32_t)n, par, val));  // true A at every block exit of every strip
+  CK(forest_solve<T>(rt, n, par, val));  // true A at every block exit of every strip
   off = 0;
   for (auto& s : strips) {
     if (s.nn) CK(cudaMemcpyAsync(s.S, val + off, s.nn * sizeof(T), cudaMemcpyDeviceToDevice, st));
     off += s.nn;
   }
   rt.free(val);
-  rt.free(par);
-  done = true;
   return FA_OK;
 }
 
