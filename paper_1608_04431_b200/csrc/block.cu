@@ -76,6 +76,9 @@ namespace fa {
 #ifndef FA_P1_MINB
 #define FA_P1_MINB 9  // CTAs of 4 warps per SM: 9 (56 registers, 36 warps) vs 8 (64, 32): cfg3 block kernel 12.06 vs 12.21 ms
 #endif
+#ifndef FA_PEND_BYTES
+#define FA_PEND_BYTES 0  // pending counts: 4 bits per cell (0) or a byte (1: cfg3 block kernel 13.38 vs 11.97 ms)
+#endif
 #ifndef FA_P1_PREFETCH
 #define FA_P1_PREFETCH 1  // pass 1 L2 prefetches: 1 the block's weight rows, 2 the neighbours' entry offsets
 #endif
@@ -145,18 +148,42 @@ struct __align__(16) WSmem {
   } u;
   __device__ __forceinline__ float* zwin() { return u.z; }
   uint8_t dirh[WB::HN];
-  uint32_t pend[WB::BN / 8];  // pending in-block donor counts, 4 bits per cell (<= 8)
+  uint32_t pend[WB::BN / (FA_PEND_BYTES ? 4 : 8)];  // pending in-block donor counts (<= 8): a byte / 4 bits per cell
   alignas(8) uint8_t sb[WB::BN];  // successor bytes
   // ready queue of Alg. 1 (sources first; each cell enters at most once);
   // after the queue loop: [0,NP) slot -> node id, [NP,2NP) per exit slot:
   // outside donors of the entries draining to it
   alignas(16) uint16_t src[WB::BN];
   alignas(4) uint8_t need[WB::NP];  // per perimeter slot: donors outside the block (ring cells draining in)
+#ifdef FA_SMEM_PAD
+  uint8_t pad_[FA_SMEM_PAD];  // tuning builds only: extra shared memory per warp
+#endif
   __device__ __forceinline__ uint32_t* slot_nid() { return reinterpret_cast<uint32_t*>(src); }
   static_assert(WB::BN * 2 >= 2 * WB::NP * 4, "records scratch lives in the queue");
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+// pending in-block donor count of cell t (Alg. 1's D(t)), and its decrement
+// (true for the last pending donor: t is ready).  Counts never borrow across
+// cells: a count is decremented only while it is >= 1.
+__device__ __forceinline__ uint32_t pend_get(const uint32_t* pend, uint32_t t) {
+#if FA_PEND_BYTES
+  return reinterpret_cast<const uint8_t*>(pend)[t];
+#else
+  return (pend[t >> 3] >> ((t & 7u) * 4u)) & 0xFu;
+#endif
+}
+__device__ __forceinline__ bool pend_dec(uint32_t* pend, uint32_t t) {
+#if FA_PEND_BYTES
+  const uint32_t sh = (t & 3u) * 8u;
+  const uint32_t old = atomicAdd(&pend[t >> 2], 0u - (1u << sh));
+  return ((old >> sh) & 0xFFu) == 1u;
+#else
+  const uint32_t sh = (t & 7u) * 4u;
+  const uint32_t old = atomicAdd(&pend[t >> 3], 0u - (1u << sh));
+  return ((old >> sh) & 0xFu) == 1u;
+#endif
+}
 // +1 on byte p of a 4-aligned byte array (counts stay < 256)
 __device__ __forceinline__ void need_inc(uint8_t* need, int p) {
   atomicAdd(reinterpret_cast<uint32_t*>(need) + (p >> 2), 1u << (8 * (p & 3)));
@@ -542,8 +569,12 @@ __device__ __forceinline__ int build_masks(S& s, uint32_t& nsrc, int h, int w) {
     uint32_t cnt = m - ((m >> 1) & 0x55555555u);
     cnt = (cnt & 0x33333333u) + ((cnt >> 2) & 0x33333333u);
     cnt = (cnt + (cnt >> 4)) & 0x0F0F0F0Fu;
+#if FA_PEND_BYTES
+    s.pend[q] = cnt;
+#else
     reinterpret_cast<uint16_t*>(s.pend)[q] =
         (uint16_t)((cnt & 0xFu) | ((cnt >> 4) & 0xF0u) | ((cnt >> 8) & 0xF00u) | ((cnt >> 12) & 0xF000u));
+#endif
     ndbits |= (sink ? 1u : 0u) << k;
     ndata += 4 - (__popc(nd) >> 3);
     if constexpr (SUCC) {
@@ -694,7 +725,7 @@ __device__ __forceinline__ uint32_t kahn_chain_tail(WSmem<T, R, Z>& s, uint32_t 
         const bool ok = sb_go(sbv);
         const uint32_t t = ok ? WBT<R>::target(cur, sbv) : 0u;
         FA_CHECK(t < (uint32_t)WBT<R>::BN);
-        go = ok && ((s.pend[t >> 3] >> ((t & 7u) * 4u)) & 0xFu) == 1u;
+        go = ok && pend_get(s.pend, t) == 1u;
         if (go) {
           cc[k] = t;
           cur = t;
@@ -733,9 +764,7 @@ __device__ __forceinline__ uint32_t kahn_chain_tail(WSmem<T, R, Z>& s, uint32_t 
           // "A(n) <- A(n) + A(c)", "decrement D(n)" (Alg. 1)
           t = end_t;
           g_add(elt(Ab, cell_off(t, wm)), a);
-          const uint32_t sh = (t & 7u) * 4u;
-          const uint32_t old = atomicAdd(&s.pend[t >> 3], 0u - (1u << sh));
-          ready = ((old >> sh) & 0xFu) == 1u;
+          ready = pend_dec(s.pend, t);
         }
       }
     }
@@ -785,9 +814,7 @@ __device__ __forceinline__ uint32_t kahn_block(WSmem<T, R, Z>& s, uint32_t nsrc,
         T a = __ldcg(elt(Ab, cell_off(c, wm)));
         if constexpr (ABS) a *= (T)__ldg(Alb + (c + (c >> 5) * wm));  // "alpha(n) A(n)"
         g_add(elt(Ab, cell_off(t, wm)), a);
-        const uint32_t sh = (t & 7u) * 4u;
-        const uint32_t old = atomicAdd(&s.pend[t >> 3], 0u - (1u << sh));
-        ready = ((old >> sh) & 0xFu) == 1u;  // the last pending donor: n joins the queue
+        ready = pend_dec(s.pend, t);  // the last pending donor: n joins the queue
       }
     }
     const unsigned bm = __ballot_sync(kFull, ready != 0u);
