@@ -1695,6 +1695,18 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
     hs[k] = ws[k] = 0;
     y0s[k] = x0s[k] = 0;
     if (b < bend) g.block_box(b, y0s[k], x0s[k], hs[k], ws[k]);
+    // the block's work list first: a block no offset reaches (NoData, ridges)
+    // skips the prefetch and the code staging
+    const int n0 = n;
+    const int np = bperim_count(hs[k], ws[k]);
+    for (int p0 = 0; p0 < WB::PB; p0 += 32) {
+      const int p = p0 + lane;
+      const bool act = p < np && x_slot[b * WB::PB + p] != (T)0;
+      const unsigned m = __ballot_sync(kFull, act);
+      if (act) s.item[n + __popc(m & lt)] = (uint16_t)((k << 8) | p);
+      n += __popc(m);
+    }
+    if (n == n0 || hs[k] <= 0 || ws[k] <= 0) continue;
 #if FA_FIN_PREFETCH
     // pull the block's output rows into L2 before the walks' reductions
     // reach them: a reduction on a line that is not in L2 waits for its DRAM
@@ -1707,15 +1719,6 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
       if (part * (WB::BC / FA_FIN_PREFETCH) < ws[k]) asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
     }
 #endif
-    const int np = bperim_count(hs[k], ws[k]);
-    for (int p0 = 0; p0 < WB::PB; p0 += 32) {
-      const int p = p0 + lane;
-      const bool act = p < np && x_slot[b * WB::PB + p] != (T)0;
-      const unsigned m = __ballot_sync(kFull, act);
-      if (act) s.item[n + __popc(m & lt)] = (uint16_t)((k << 8) | p);
-      n += __popc(m);
-    }
-    if (hs[k] <= 0 || ws[k] <= 0) continue;
     // codes: 16-byte rows when aligned
     const int h = hs[k], w = ws[k];
     const bool vec = w == WB::BC && ((x0s[k] & 15) == 0) && ((g.W & 15) == 0) &&
