@@ -25,6 +25,10 @@
 
 #include "forest.cuh"
 
+#ifndef FA_WALK_FAST
+#define FA_WALK_FAST 1  // walks take single-child parents without atomics
+#endif
+
 namespace fa {
 
 namespace {
@@ -138,7 +142,7 @@ __global__ void k_walk(const uint32_t* __restrict__ front, const uint32_t* __res
         // p's flag, value and parent in one round of loads: with a single
         // child (v) p is final once v's sum is added -- no atomics, one L2
         // round trip per step along chains
-        const bool single = one[p] != 0;
+        const bool single = FA_WALK_FAST && one[p] != 0;
         const T vp = __ldcg(&val[p]);
         const uint32_t pp = parent[p];
         const T add = WG ? wv[v] * s : s;
