@@ -1151,7 +1151,10 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
 }
 
 // ---------------------------------------------------------------- pass 1
-template <class T, int R, int WK, bool FROM_DEM, bool ABS = false>
+// FULL: every non-empty block of the launch is a whole R x 32 block (the
+// raster, strip and tile sizes are multiples of the block shape): h and w
+// are compile-time constants, the ragged-block paths compile out
+template <class T, int R, int WK, bool FROM_DEM, bool ABS = false, bool FULL = false>
 __global__ void __launch_bounds__(128, FA_P1_MINB) k_pass1(PassArgs<T, WK> P) {
   using WB = WBT<R>;
   constexpr bool Z = FROM_DEM;
@@ -1168,6 +1171,10 @@ __global__ void __launch_bounds__(128, FA_P1_MINB) k_pass1(PassArgs<T, WK> P) {
   if (h <= 0 || w <= 0) {
     for (int p = lane; p < WB::PB; p += 32) P.slot_root[b * WB::PB + p] = kNone;
     return;
+  }
+  if constexpr (FULL) {
+    h = WB::BR;
+    w = WB::BC;
   }
 #if FA_P1_PREFETCH & 1
   // the block's weight rows are read only after the codes are staged and the
@@ -1887,7 +1894,11 @@ cudaError_t launch_pass1_r(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t
   } else {
     const size_t sm = sizeof(WSmem<T, R, false>) * (size_t)a.g.nw;
     const unsigned grid = (unsigned)((a.b_end - a.b_begin + a.g.nw - 1) / a.g.nw);
-    auto k = k_pass1<T, R, WK, false>;
+    const Geom& g = a.g;
+    // whole blocks everywhere (cfg0-4: sizes are multiples of 32)
+    const bool full = R == 32 && g.H % R == 0 && g.W % 32 == 0 && (g.TH % R == 0 || g.TH >= g.H) &&
+                      (g.TW % 32 == 0 || g.TW >= g.W);
+    auto k = full ? k_pass1<T, R, WK, false, false, R == 32> : k_pass1<T, R, WK, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<grid, 32 * a.g.nw, sm, st>>>(a);
   }
