@@ -1682,7 +1682,7 @@ struct __align__(16) FSmem {
   uint16_t item[KB * WB::PB];            // work list: (block-in-group << 8) | slot
 };
 
-template <class T, int R, int KB, bool ABS = false>
+template <class T, int R, int KB, bool ABS = false, bool FULL = false>
 __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ x_slot, const uint8_t* __restrict__ dirs,
                                                   T* acc, const float* __restrict__ alpha, int64_t bbeg, int64_t bend) {
   using WB = WBT<R>;
@@ -1702,6 +1702,10 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
     hs[k] = ws[k] = 0;
     y0s[k] = x0s[k] = 0;
     if (b < bend) g.block_box(b, y0s[k], x0s[k], hs[k], ws[k]);
+    if (FULL && hs[k] > 0 && ws[k] > 0) {  // whole blocks: the shape as constants
+      hs[k] = R;
+      ws[k] = 32;
+    }
     // the block's work list first: a block no offset reaches (NoData, ridges)
     // skips the prefetch and the code staging
     const int n0 = n;
@@ -1798,6 +1802,14 @@ __global__ void __launch_bounds__(128) k_finalize(Geom g, const T* __restrict__ 
   }
 }
 
+// every non-empty block of the geometry is a whole R x 32 block (the raster,
+// strip and tile sizes are multiples of the block shape; cfg0-4): kernels
+// specialised for it have the block shape as constants
+static bool whole_blocks(const Geom& g, int R) {
+  return R == 32 && g.H % R == 0 && g.W % 32 == 0 && (g.TH % R == 0 || g.TH >= g.H) &&
+         (g.TW % 32 == 0 || g.TW >= g.W);
+}
+
 template <class T, int R, int KB>
 cudaError_t launch_finalize_k(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st,
                               int64_t bbeg, int64_t bend) {
@@ -1807,7 +1819,7 @@ cudaError_t launch_finalize_k(const Geom& g, const T* x_slot, const uint8_t* dir
   // 3.82 ms vs 3.92 ms at full occupancy).
   size_t sm = sizeof(FSmem<T, R, KB>) * NWC;
   sm = sm < 24576 ? 24576 : sm;
-  auto k = k_finalize<T, R, KB>;
+  auto k = whole_blocks(g, R) ? k_finalize<T, R, KB, false, R == 32> : k_finalize<T, R, KB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int64_t groups = (bend - bbeg + KB - 1) / KB;
   k<<<(unsigned)((groups + NWC - 1) / NWC), 32 * NWC, sm, st>>>(g, x_slot, dirs, acc, nullptr, bbeg, bend);
@@ -1833,10 +1845,12 @@ cudaError_t launch_pass1_absorb(const PassArgs<double, 0>* a0, const PassArgs<do
   if (a0) {
     if (a0->g.br != 32 || a0->g.bc != 32) return cudaErrorInvalidValue;
     if (from_dem) go(k_pass1<double, 32, 0, true, true>, *a0);
+    else if (whole_blocks(a0->g, 32)) go(k_pass1<double, 32, 0, false, true, true>, *a0);
     else go(k_pass1<double, 32, 0, false, true>, *a0);
   } else {
     if (a2->g.br != 32 || a2->g.bc != 32) return cudaErrorInvalidValue;
     if (from_dem) go(k_pass1<double, 32, 2, true, true>, *a2);
+    else if (whole_blocks(a2->g, 32)) go(k_pass1<double, 32, 2, false, true, true>, *a2);
     else go(k_pass1<double, 32, 2, false, true>, *a2);
   }
   return cudaGetLastError();
@@ -1848,7 +1862,7 @@ cudaError_t launch_retain_absorb(const Geom& g, const double* x_slot, const uint
   constexpr int NWC = 4;
   size_t sm = sizeof(FSmem<double, 32, 1>) * NWC;
   sm = sm < 24576 ? 24576 : sm;
-  auto k = k_finalize<double, 32, 1, true>;
+  auto k = whole_blocks(g, 32) ? k_finalize<double, 32, 1, true, true> : k_finalize<double, 32, 1, true>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k<<<(unsigned)((g.nblocks + NWC - 1) / NWC), 32 * NWC, sm, st>>>(g, x_slot, dirs, acc, alpha, 0, g.nblocks);
   return cudaGetLastError();
@@ -1894,11 +1908,7 @@ cudaError_t launch_pass1_r(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t
   } else {
     const size_t sm = sizeof(WSmem<T, R, false>) * (size_t)a.g.nw;
     const unsigned grid = (unsigned)((a.b_end - a.b_begin + a.g.nw - 1) / a.g.nw);
-    const Geom& g = a.g;
-    // whole blocks everywhere (cfg0-4: sizes are multiples of 32)
-    const bool full = R == 32 && g.H % R == 0 && g.W % 32 == 0 && (g.TH % R == 0 || g.TH >= g.H) &&
-                      (g.TW % 32 == 0 || g.TW >= g.W);
-    auto k = full ? k_pass1<T, R, WK, false, false, R == 32> : k_pass1<T, R, WK, false>;
+    auto k = whole_blocks(a.g, R) ? k_pass1<T, R, WK, false, false, R == 32> : k_pass1<T, R, WK, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<grid, 32 * a.g.nw, sm, st>>>(a);
   }
