@@ -7,7 +7,8 @@ oracle's exact fixed-point sum (P11), both through the single-device path
 bench.py calls and through the row-strip path of the multi-GPU launch
 (8 strips of 4096 rows, the N=8 configuration, on one device).  cfg4's recipe
 (30 % NoData, w = 1, u64) is checked bit-exactly at a one-GPU size with the
-N=8 strip layout.  The oracle needs ~4 minutes of one host core for cfg3.
+N=8 strip layout, and certified (P8) on one tile row at cfg4's full width
+of 131072 columns.  The oracle needs ~4 minutes of one host core for cfg3.
 """
 import numpy as np
 import pytest
@@ -71,6 +72,23 @@ def test_cfg4_recipe_eight_strips_u64(fa_lib):
         one = ctx.accumulate(dem=_cuda(cfg.dem), atype="u64").cpu().numpy()
     assert (got == exp).all()
     assert (one == exp).all()
+
+
+def test_cfg4_recipe_full_width_certified(fa_lib):
+    """One tile row of cfg4 at its full width (4096 x 131072 cells, 30 %
+    NoData, w = 1, u64, 4096^2 tiles): the column indices, the 4096 block
+    columns and the 32 tile columns a rank of the 8-GPU run works with.  The
+    oracle's own D8 codes must match byte for byte and its donor-identity
+    certificate (P8: identity + mass balance on an acyclic D8 field is a
+    complete certificate) must hold on every cell."""
+    H, W = 4096, 131072
+    cfg = inputs.make_config("cfg4", H, W)
+    d = oracle.d8(cfg.dem)
+    with fa_lib.Context(0, tile=(4096, 4096)) as ctx:
+        dz = _cuda(cfg.dem)
+        assert (ctx.flowdirs(dz).cpu().numpy() == d).all()
+        got = ctx.accumulate(dem=dz, atype="u64").cpu().numpy()
+    assert oracle.certify(d, got) == 0
 
 
 @pytest.mark.slow

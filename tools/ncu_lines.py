@@ -8,7 +8,8 @@ import collections
 import csv
 import sys
 
-rows = list(csv.reader(open(sys.argv[1])))
+import gzip
+rows = list(csv.reader(gzip.open(sys.argv[1], "rt") if sys.argv[1].endswith(".gz") else open(sys.argv[1])))
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 cells = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0
 agg = collections.defaultdict(lambda: [0, 0, 0, 0, ""])

@@ -1,7 +1,8 @@
 """Sum an ncu source-page dump (cuda,sass) over line ranges of one file.
 usage: python tools/ncu_regions.py dump.csv cells name:a-b name:a-b ..."""
 import collections, csv, sys
-rows = list(csv.reader(open(sys.argv[1])))
+import gzip
+rows = list(csv.reader(gzip.open(sys.argv[1], "rt") if sys.argv[1].endswith(".gz") else open(sys.argv[1])))
 cells = float(sys.argv[2])
 regs = [(x.split(":")[0], *map(int, x.split(":")[1].split("-"))) for x in sys.argv[3:]]
 hdr = None; fname = ""; cur = None
