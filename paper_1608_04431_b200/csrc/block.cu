@@ -64,11 +64,14 @@ namespace fa {
 // walks; with the successor-byte walks 2 / 4 -> 2.92 / 3.14 ms
 #define FA_FIN_PREFETCH 2
 #endif
+#ifndef FA_FIN_NW
+#define FA_FIN_NW 2  // warps (blocks) per CTA of the finalize (4 / 2: cfg3 2.85 / 2.81 ms)
+#endif
 #ifndef FA_REC_STEPS
-#define FA_REC_STEPS 4
+#define FA_REC_STEPS 8  // entry walks: path steps per refill round (4 / 6 / 8 / 16: cfg3 block kernel 10.76 / 10.70 / 10.67 / 10.67 ms)
 #endif
 #ifndef FA_CHAIN_TAIL
-#define FA_CHAIN_TAIL 32  // queue width below which the loop switches to chain bursts (0: never)
+#define FA_CHAIN_TAIL 48  // queue width below which the loop switches to chain bursts (0: never; 32 / 48 with the whole-block kernel: 10.67 / 10.63 ms)
 #endif
 #ifndef FA_CHAIN_K
 #define FA_CHAIN_K 4
@@ -1155,7 +1158,7 @@ __device__ __forceinline__ void block_records(S& s, const PassArgs<T, WK>& P, in
 // raster, strip and tile sizes are multiples of the block shape): h and w
 // are compile-time constants, the ragged-block paths compile out
 template <class T, int R, int WK, bool FROM_DEM, bool ABS = false, bool FULL = false>
-__global__ void __launch_bounds__(128, FA_P1_MINB) k_pass1(PassArgs<T, WK> P) {
+__global__ void __launch_bounds__(32 * kNW, FA_P1_MINB * 4 / kNW) k_pass1(PassArgs<T, WK> P) {
   using WB = WBT<R>;
   constexpr bool Z = FROM_DEM;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1237,7 +1240,7 @@ __global__ void __launch_bounds__(128, FA_P1_MINB) k_pass1(PassArgs<T, WK> P) {
 
 // ---------------------------------------------------------------- pass 2
 template <class T, int R, int WK>
-__global__ void __launch_bounds__(128) k_pass2(PassArgs<T, WK> P) {
+__global__ void __launch_bounds__(32 * kNW) k_pass2(PassArgs<T, WK> P) {
   using WB = WBT<R>;
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5;
@@ -1813,12 +1816,12 @@ static bool whole_blocks(const Geom& g, int R) {
 template <class T, int R, int KB>
 cudaError_t launch_finalize_k(const Geom& g, const T* x_slot, const uint8_t* dirs, T* acc, cudaStream_t st,
                               int64_t bbeg, int64_t bend) {
-  constexpr int NWC = 4;  // warps per CTA
-  // At least 24 KB of shared memory per CTA: at most 9 CTAs (36 warps) per
-  // SM, which keeps the acc rows the walks touch in L2 (measured on cfg3:
-  // 3.82 ms vs 3.92 ms at full occupancy).
+  constexpr int NWC = FA_FIN_NW;  // warps per CTA
+  // At least 6 KB of shared memory per warp: at most 36 warps per SM, which
+  // keeps the acc rows the walks touch in L2 (measured on cfg3: 3.82 ms vs
+  // 3.92 ms at full occupancy).
   size_t sm = sizeof(FSmem<T, R, KB>) * NWC;
-  sm = sm < 24576 ? 24576 : sm;
+  sm = sm < 6144 * NWC ? 6144 * NWC : sm;
   auto k = whole_blocks(g, R) ? k_finalize<T, R, KB, false, R == 32> : k_finalize<T, R, KB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int64_t groups = (bend - bbeg + KB - 1) / KB;

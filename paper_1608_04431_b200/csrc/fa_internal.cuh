@@ -33,7 +33,10 @@ constexpr uint32_t kFlowTerminates = 0xFFFFFFFFu;  // Alg. 2 sentinel
 // parameter of the block kernels (block.cu) and a run-time field of Geom.
 constexpr int kBR = 32;  // default block rows
 constexpr int kBC = 32;  // default block cols
-constexpr int kNW = 4;   // default warps (one block each) per CTA of the block kernels (measured best)
+#ifndef FA_NW
+#define FA_NW 2
+#endif
+constexpr int kNW = FA_NW;   // warps (one block each) per CTA of the block kernels (cfg3 block kernel, 1 / 2 / 4: 10.94 / 10.57 / 10.63 ms; smaller CTAs free their slots sooner, 1-warp CTAs hit the 32-CTA limit)
 
 // status bits (device flag word)
 constexpr uint32_t ST_BADCODE = 1u;
