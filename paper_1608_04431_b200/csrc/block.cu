@@ -67,6 +67,9 @@ namespace fa {
 #ifndef FA_FIN_NW
 #define FA_FIN_NW 2  // warps (blocks) per CTA of the finalize (4 / 2: cfg3 2.85 / 2.81 ms)
 #endif
+#ifndef FA_P1_KPW
+#define FA_P1_KPW 1  // blocks per warp of pass 1 (interleaved over the launch)
+#endif
 #ifndef FA_REC_STEPS
 #define FA_REC_STEPS 8  // entry walks: path steps per refill round (4 / 6 / 8 / 16: cfg3 block kernel 10.76 / 10.70 / 10.67 / 10.67 ms)
 #endif
@@ -1165,15 +1168,30 @@ __global__ void __launch_bounds__(32 * kNW, FA_P1_MINB * 4 / kNW) k_pass1(PassAr
   const int warp = threadIdx.x >> 5;
   WSmem<T, R, Z>& s = reinterpret_cast<WSmem<T, R, Z>*>(smem)[warp];
   const Geom& g = P.g;
+  const int lane = lane_id();
+  // FA_P1_KPW blocks per warp, one after another (a CTA owns KPW * nw
+  // consecutive blocks): a CTA slot is refilled KPW times less often
+#if FA_P1_KPW > 1
+#pragma unroll 1
+  for (int it = 0; it < FA_P1_KPW; ++it) {
+  if (it) __syncwarp();
+  const int64_t b = P.b_begin + ((int64_t)blockIdx.x * FA_P1_KPW + it) * g.nw + warp;
+  if (b >= P.b_end) return;
+#else
+  {
   const int64_t b = P.b_begin + (int64_t)blockIdx.x * g.nw + warp;
   if (b >= P.b_end) return;
-  const int lane = lane_id();
+#endif
   int64_t y0, x0;
   int h, w;
   g.block_box(b, y0, x0, h, w);
   if (h <= 0 || w <= 0) {
     for (int p = lane; p < WB::PB; p += 32) P.slot_root[b * WB::PB + p] = kNone;
+#if FA_P1_KPW > 1
+    continue;
+#else
     return;
+#endif
   }
   if constexpr (FULL) {
     h = WB::BR;
@@ -1236,6 +1254,7 @@ __global__ void __launch_bounds__(32 * kNW, FA_P1_MINB * 4 / kNW) k_pass1(PassAr
     if (lane == 0 && wsum) atomicAdd(P.wsum, wsum);
   }
   block_records<T, R, WSmem<T, R, Z>, WK, ABS>(s, P, b, y0, x0, h, w);
+  }
 }
 
 // ---------------------------------------------------------------- pass 2
@@ -1836,12 +1855,18 @@ cudaError_t launch_finalize_r(const Geom& g, const T* x_slot, const uint8_t* dir
   return launch_finalize_k<T, R, 1>(g, x_slot, dirs, acc, st, bbeg, bend);
 }
 
+// CTAs of a pass-1 launch over n blocks: nw warps per CTA, FA_P1_KPW blocks per warp
+static unsigned p1_grid(int64_t n, int nw) {
+  const int64_t per = (int64_t)nw * FA_P1_KPW;
+  return (unsigned)((n + per - 1) / per);
+}
+
 // absorption (f64, 32x32 blocks): pass 1 and the finalize with alpha
 cudaError_t launch_pass1_absorb(const PassArgs<double, 0>* a0, const PassArgs<double, 2>* a2, bool from_dem,
                                 cudaStream_t st) {
   auto go = [&](auto k, const auto& a) {
     const size_t sm = (from_dem ? sizeof(WSmem<double, 32, true>) : sizeof(WSmem<double, 32, false>)) * (size_t)a.g.nw;
-    const unsigned grid = (unsigned)((a.b_end - a.b_begin + a.g.nw - 1) / a.g.nw);
+    const unsigned grid = p1_grid(a.b_end - a.b_begin, a.g.nw);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<grid, 32 * a.g.nw, sm, st>>>(a);
   };
@@ -1904,13 +1929,13 @@ cudaError_t launch_pass1_r(const PassArgs<T, WK>& a, bool from_dem, cudaStream_t
     k<<<grid, 32 * kNWV, sm, st>>>(a);
   } else if (from_dem) {
     const size_t sm = sizeof(WSmem<T, R, true>) * (size_t)a.g.nw;
-    const unsigned grid = (unsigned)((a.b_end - a.b_begin + a.g.nw - 1) / a.g.nw);
+    const unsigned grid = p1_grid(a.b_end - a.b_begin, a.g.nw);
     auto k = k_pass1<T, R, WK, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<grid, 32 * a.g.nw, sm, st>>>(a);
   } else {
     const size_t sm = sizeof(WSmem<T, R, false>) * (size_t)a.g.nw;
-    const unsigned grid = (unsigned)((a.b_end - a.b_begin + a.g.nw - 1) / a.g.nw);
+    const unsigned grid = p1_grid(a.b_end - a.b_begin, a.g.nw);
     auto k = whole_blocks(a.g, R) ? k_pass1<T, R, WK, false, false, R == 32> : k_pass1<T, R, WK, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<grid, 32 * a.g.nw, sm, st>>>(a);
