@@ -70,6 +70,9 @@ namespace fa {
 #ifndef FA_P1_KPW
 #define FA_P1_KPW 1  // blocks per warp of pass 1 (interleaved over the launch)
 #endif
+#ifndef FA_FIN_SMEM_FLOOR
+#define FA_FIN_SMEM_FLOOR 6144  // finalize: shared-memory bytes per warp at least (caps the warps per SM)
+#endif
 #ifndef FA_REC_STEPS
 #define FA_REC_STEPS 8  // entry walks: path steps per refill round (4 / 6 / 8 / 16: cfg3 block kernel 10.76 / 10.70 / 10.67 / 10.67 ms)
 #endif
@@ -1840,7 +1843,7 @@ cudaError_t launch_finalize_k(const Geom& g, const T* x_slot, const uint8_t* dir
   // keeps the acc rows the walks touch in L2 (measured on cfg3: 3.82 ms vs
   // 3.92 ms at full occupancy).
   size_t sm = sizeof(FSmem<T, R, KB>) * NWC;
-  sm = sm < 6144 * NWC ? 6144 * NWC : sm;
+  sm = sm < FA_FIN_SMEM_FLOOR * NWC ? FA_FIN_SMEM_FLOOR * NWC : sm;
   auto k = whole_blocks(g, R) ? k_finalize<T, R, KB, false, R == 32> : k_finalize<T, R, KB>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int64_t groups = (bend - bbeg + KB - 1) / KB;
