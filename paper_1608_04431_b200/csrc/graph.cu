@@ -267,8 +267,44 @@ template cudaError_t launch_copy_n<unsigned long long>(cudaStream_t, uint32_t, c
                                                        const unsigned long long*, unsigned long long*);
 template cudaError_t launch_copy_n<double>(cudaStream_t, uint32_t, const uint32_t*, const double*, double*);
 
+#ifndef FA_FOLD_VEC
+#define FA_FOLD_VEC 0  // fold: 8-byte offsets read two at a time (16-byte loads)
+#endif
+// the same fold with two 8-byte offsets per load (the scan over all slots is
+// a plain stream: most offsets are zero)
+template <class T>
+__global__ void k_fold_leaves2(int64_t npairs, const T* __restrict__ x_slot, const uint32_t* __restrict__ slot_root,
+                               T* S) {
+  static_assert(sizeof(T) == 8, "pairs of 8-byte offsets");
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npairs;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(x_slot) + i);
+    T x0, x1;
+    memcpy(&x0, &v.x, 8);
+    memcpy(&x1, &v.y, 8);
+    if (x0 != (T)0) {
+      const uint32_t e = slot_root[2 * i];
+      if (e != kNone) atomic_add(&S[e], x0);
+    }
+    if (x1 != (T)0) {
+      const uint32_t e = slot_root[2 * i + 1];
+      if (e != kNone) atomic_add(&S[e], x1);
+    }
+  }
+}
+
 template <class T>
 cudaError_t launch_fold_leaves(cudaStream_t st, int64_t nslots, const T* x_slot, const uint32_t* slot_root, T* S) {
+#if FA_FOLD_VEC
+  if constexpr (sizeof(T) == 8) {
+    if ((reinterpret_cast<uintptr_t>(x_slot) & 15) == 0 && nslots >= 2) {
+      const int64_t np = nslots / 2;
+      k_fold_leaves2<T><<<grid_for(np), 256, 0, st>>>(np, x_slot, slot_root, S);
+      if (nslots & 1) k_fold_leaves<T><<<1, 32, 0, st>>>(1, x_slot + (nslots - 1), slot_root + (nslots - 1), S);
+      return cudaGetLastError();
+    }
+  }
+#endif
   k_fold_leaves<T><<<grid_for(nslots), 256, 0, st>>>(nslots, x_slot, slot_root, S);
   return cudaGetLastError();
 }
