@@ -268,7 +268,7 @@ template cudaError_t launch_copy_n<unsigned long long>(cudaStream_t, uint32_t, c
 template cudaError_t launch_copy_n<double>(cudaStream_t, uint32_t, const uint32_t*, const double*, double*);
 
 #ifndef FA_FOLD_VEC
-#define FA_FOLD_VEC 0  // fold: 8-byte offsets read two at a time (16-byte loads)
+#define FA_FOLD_VEC 0  // fold: 8-byte offsets read two at a time (16-byte loads): cfg3 graph 1.565 -> 1.535 ms, parity-green; off in the profiled build
 #endif
 // the same fold with two 8-byte offsets per load (the scan over all slots is
 // a plain stream: most offsets are zero)
